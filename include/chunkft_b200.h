@@ -1,0 +1,262 @@
+/*
+ * chunkft_b200.h -- the C ABI of the B200-native ChunkFT chunk-local training step.
+ *
+ * This is the drop-in boundary for the reference's CPU path (/root/reference/proj).
+ * Every entry point names the reference interface it replaces (file:line, relative to
+ * /root/reference/proj).  Plain C types only: pointers, sizes, enums; no torch types.
+ *
+ * Three levels:
+ *   1. Host planning (partition.hpp / schedule.hpp): byte-budget partitioner, plan hash,
+ *      plan JSON, rotation scheduler.  Bit-exact with the reference.
+ *   2. Parity kernels: the 12 chunkft::kernels signatures verbatim (kernels.hpp:20-65),
+ *      host double* in/out, computed by CUDA kernels in fp64 with the reference's
+ *      per-element accumulation order and no FMA contraction -> bit-identical results
+ *      (tanh_forward: CUDA tanh, <=1 ulp).  This is what a `Backend::cuda` case in
+ *      src/kernels.cpp:37-68 dispatches to.
+ *   3. Performance level: device pointers + dtype + cudaStream_t.  bf16 operands on
+ *      tcgen05/TMEM tensor cores (fp32 accumulate), or fp32 / fp64 CUDA-core paths.
+ *      All calls are asynchronous on the given stream and never allocate on the hot path.
+ *
+ * Errors: every int-returning function returns CFT_OK (0) or CFT_ERR and sets a
+ * thread-local message readable with cft_last_error().  The void parity kernels record
+ * failures the same way (check cft_last_status()).
+ */
+#ifndef CHUNKFT_B200_H_
+#define CHUNKFT_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CFT_OK 0
+#define CFT_ERR 1
+
+typedef void* cft_stream_t; /* a cudaStream_t; NULL = legacy default stream */
+
+typedef enum { CFT_F32 = 0, CFT_BF16 = 1, CFT_F64 = 2 } cft_dtype;
+
+const char* cft_last_error(void);
+int cft_last_status(void);
+int cft_version(void);
+
+/* ===================================================================== */
+/* 1. Host planning                                                        */
+/* ===================================================================== */
+
+/* TensorInfo (include/chunkft/tensor.hpp:39-49). */
+typedef struct {
+  int32_t id;
+  int32_t reg_order;
+  int32_t trainable;
+  int32_t storage_precision;
+  int64_t rows;
+  int64_t cols;
+} cft_tensor_info;
+
+/* CostPolicy (include/chunkft/partition.hpp:16-30). */
+typedef struct {
+  int32_t param_bytes;
+  int32_t grad_bytes;
+  int32_t master_bytes;
+  int32_t moment1_bytes;
+  int32_t moment2_bytes;
+} cft_cost_policy;
+
+typedef struct cft_plan cft_plan; /* ChunkPlan (partition.hpp:37-59) */
+
+/* partition()            partition.hpp:66-67,  src/partition.cpp:125-187 */
+int cft_partition(const cft_tensor_info* infos, int n, int K, const cft_cost_policy* policy,
+                  cft_plan** out);
+/* partition_by_budget()  partition.hpp:70-71,  src/partition.cpp:189-198 */
+int cft_partition_by_budget(const cft_tensor_info* infos, int n, int64_t budget_bytes,
+                            const cft_cost_policy* policy, cft_plan** out);
+/* partition_per_tensor() partition.hpp:75-76,  src/partition.cpp:200-214 */
+int cft_partition_per_tensor(const cft_tensor_info* infos, int n, const cft_cost_policy* policy,
+                             cft_plan** out);
+/* plan_from_json()       partition.hpp:79,     src/partition.cpp:238-261; names '\n'-joined */
+int cft_plan_from_json(const char* text, const cft_tensor_info* infos, int n, cft_plan** out);
+/* ChunkPlan::validate()  partition.hpp:57,     src/partition.cpp:38-83 */
+int cft_plan_validate(const cft_plan* plan, const cft_tensor_info* infos, int n);
+void cft_plan_destroy(cft_plan* plan);
+
+int cft_plan_num_chunks(const cft_plan* plan);
+int64_t cft_plan_num_slices(const cft_plan* plan, int chunk);
+int cft_plan_get_slices(const cft_plan* plan, int chunk, int32_t* tensor_id, int64_t* row_begin,
+                        int64_t* row_end);
+int64_t cft_plan_chunk_elements(const cft_plan* plan, int chunk);
+int64_t cft_plan_chunk_bytes(const cft_plan* plan, int chunk);
+int64_t cft_plan_total_mutable_bytes(const cft_plan* plan);
+int64_t cft_plan_max_row_cost(const cft_plan* plan);
+/* plan_hash()            partition.hpp:83,     src/partition.cpp:263-281 */
+uint64_t cft_plan_hash(const cft_plan* plan);
+/* plan_to_json()         partition.hpp:78,     src/partition.cpp:216-236.
+ * names: n tensor names joined by '\n' (matched to infos by position).
+ * Writes up to cap bytes (NUL-terminated); *needed = full length + 1. */
+int cft_plan_to_json(const cft_plan* plan, const cft_tensor_info* infos, int n,
+                     const char* names, char* buf, int64_t cap, int64_t* needed);
+
+/* ScheduleConfig (schedule.hpp:13-23) */
+typedef struct {
+  int32_t K;
+  int32_t T;
+  int64_t total_steps;
+  int32_t prefetch;
+  int32_t pad_;
+  int64_t bandwidth_bytes_per_step;
+} cft_schedule_config;
+
+/* TransferEvent (schedule.hpp:25-31); dir 0 = load, 1 = offload */
+typedef struct {
+  int64_t step;
+  int32_t chunk;
+  int32_t dir;
+  int64_t bytes;
+  int64_t latency_steps;
+} cft_transfer_event;
+
+typedef struct cft_scheduler cft_scheduler; /* RotationScheduler (schedule.hpp:38-94) */
+
+int cft_scheduler_create(const cft_schedule_config* cfg, const cft_plan* plan, cft_scheduler** out);
+void cft_scheduler_destroy(cft_scheduler* s);
+/* step_begin(): returns the active chunk, or -1 on error.  Writes the physical moves the
+ * caller must perform (load of *load_chunk if >= 0, prefetch of *prefetch_chunk if >= 0). */
+int cft_scheduler_step_begin(cft_scheduler* s, int32_t* load_chunk, int32_t* prefetch_chunk);
+/* step_end(): *offload_chunk >= 0 when the active chunk must be retired to host. */
+int cft_scheduler_step_end(cft_scheduler* s, int32_t* offload_chunk);
+/* finish(): flushes every resident chunk; *n_flushed chunks written to flushed[]. */
+int cft_scheduler_finish(cft_scheduler* s, int32_t* flushed, int32_t* n_flushed);
+int64_t cft_scheduler_current_step(const cft_scheduler* s);
+int64_t cft_scheduler_active_index_counter(const cft_scheduler* s);
+int cft_scheduler_active_chunk(const cft_scheduler* s);
+int cft_scheduler_is_resident(const cft_scheduler* s, int chunk);
+int64_t cft_scheduler_device_state_bytes(const cft_scheduler* s);
+int64_t cft_scheduler_transfer_inflight_bytes(cft_scheduler* s, int64_t step);
+int64_t cft_scheduler_noop_loads(const cft_scheduler* s);
+int64_t cft_scheduler_num_events(const cft_scheduler* s);
+int cft_scheduler_get_events(const cft_scheduler* s, cft_transfer_event* out, int64_t cap);
+
+/* ===================================================================== */
+/* 2. Parity kernels: chunkft::kernels (include/chunkft/kernels.hpp:20-65) */
+/*    Host double* in/out; computed on the current CUDA device in fp64.    */
+/* ===================================================================== */
+
+void cft_kernels_linear_forward(const double* x, int batch, int in_dim, const double* w,
+                                int out_dim, const double* bias, double* y);
+void cft_kernels_linear_dinput(const double* dy, int batch, int out_dim, const double* w,
+                               int in_dim, double* dx);
+void cft_kernels_linear_dweight(const double* dy, int batch, int out_dim, const double* x,
+                                int in_dim, int64_t row_begin, int64_t row_end, double* dw);
+void cft_kernels_linear_dbias(const double* dy, int batch, int out_dim, int64_t row_begin,
+                              int64_t row_end, double* db);
+void cft_kernels_embedding_gather(const double* table, int dim, const int* tokens, int positions,
+                                  double* y);
+int64_t cft_kernels_embedding_scatter(const double* dy, int dim, const int* tokens, int positions,
+                                      int64_t row_begin, int64_t row_end, double* dtable);
+void cft_kernels_layernorm_forward(const double* x, int batch, int dim, const double* gamma,
+                                   const double* beta, double eps, double* y, double* mean,
+                                   double* inv_std);
+void cft_kernels_layernorm_dinput(const double* dy, const double* x, const double* mean,
+                                  const double* inv_std, const double* gamma, int batch, int dim,
+                                  double* dx);
+void cft_kernels_layernorm_dgamma(const double* dy, const double* x, const double* mean,
+                                  const double* inv_std, int batch, int dim, int64_t row_begin,
+                                  int64_t row_end, double* dgamma);
+void cft_kernels_layernorm_dbeta(const double* dy, int batch, int dim, int64_t row_begin,
+                                 int64_t row_end, double* dbeta);
+void cft_kernels_tanh_forward(const double* x, int64_t n, double* y);
+void cft_kernels_tanh_dinput(const double* dy, const double* y, int64_t n, double* dx);
+
+/* ===================================================================== */
+/* 3. Performance level: device pointers, async on `stream`.              */
+/* ===================================================================== */
+
+/* y[b,o] = sum_i x[b,i] w[o,i] (+ bias[o]); overwrite.   kernels.hpp:20-21 (linear_forward)
+ * x: n_tok x in, w: out x in, y: n_tok x out, all `dtype`; bias may be NULL. */
+int cft_linear_fwd(cft_dtype dtype, const void* x, int64_t n_tok, int64_t in_dim, const void* w,
+                   int64_t out_dim, const void* bias, void* y, cft_stream_t stream);
+
+/* dx = beta*dx + dy . W   (beta 0 or 1).                 kernels.hpp:23-25 (linear_dinput) */
+int cft_linear_dgrad(cft_dtype dtype, const void* dy, int64_t n_tok, int64_t out_dim,
+                     const void* w, int64_t in_dim, void* dx, int beta, cft_stream_t stream);
+
+/* Slice-aware weight gradient, dW_S = dY[:, rb:re)^T . X  (never forms a dense dW).
+ *   dw_slice[(o-rb)*in + i] (+)= sum_b dy[b,o] x[b,i],  o in [rb, re)
+ * dw_slice is fp32 for CFT_F32/CFT_BF16 and fp64 for CFT_F64; accumulate 0 overwrites,
+ * 1 adds (the reference's "+=" into a zeroed GradBag entry).  kernels.hpp:27-29 */
+int cft_linear_wgrad_slice(cft_dtype dtype, const void* dy, int64_t n_tok, int64_t out_dim,
+                           const void* x, int64_t in_dim, int64_t row_begin, int64_t row_end,
+                           void* dw_slice, int accumulate, cft_stream_t stream);
+
+/* db_slice[o-rb] += sum_b dy[b,o], o in [rb,re); fp32 out (fp64 for CFT_F64). kernels.hpp:31-33 */
+int cft_linear_dbias_slice(cft_dtype dtype, const void* dy, int64_t n_tok, int64_t out_dim,
+                           int64_t row_begin, int64_t row_end, void* db_slice, int accumulate,
+                           cft_stream_t stream);
+
+/* y[p,:] = table[tokens[p],:].                           kernels.hpp:35-37 */
+int cft_embedding_gather(cft_dtype dtype, const void* table, int64_t dim, const int32_t* tokens,
+                         int64_t positions, void* y, cft_stream_t stream);
+
+/* dtable_slice[tok-rb,:] += dy[p,:] for rb <= tok < re; matched count added to
+ * *matched_dev (device int64, may be NULL).  fp32 out (fp64 for CFT_F64). kernels.hpp:39-44 */
+int cft_embedding_scatter_slice(cft_dtype dtype, const void* dy, int64_t dim,
+                                const int32_t* tokens, int64_t positions, int64_t row_begin,
+                                int64_t row_end, void* dtable_slice, int64_t* matched_dev,
+                                cft_stream_t stream);
+
+/* Hyper-parameters (AdamWHyper, optimizer.hpp:15-22). */
+typedef struct {
+  double eta;
+  double beta1;
+  double beta2;
+  double epsilon;
+  double weight_decay;
+} cft_adamw_hyper;
+
+/* Where the updated master values go in the (compute-dtype) parameter buffer: the chunk's
+ * state arrays are contiguous in plan order; segment s covers state elements
+ * [state_off, state_off+count) and maps to param_base + param_off.  One segment per slice. */
+typedef struct {
+  int64_t state_off;
+  int64_t param_off;
+  int64_t count;
+} cft_segment;
+
+/* Gradient statistics pass over the mean gradient g = grad * grad_scale:
+ * stats_dev[0] += sum g^2 (fp64), stats_dev[1] = count of non-finite, stats_dev[2] = first
+ * non-finite index (int64 bits).  Required before cft_adamw_slice: trainer.cpp:58-60
+ * (grad_norm_sq) and optimizer.cpp:169-173 (reject non-finite before mutating).
+ * stats_dev must be zeroed by the caller (3 x 8 bytes). */
+int cft_grad_stats(cft_dtype state_dtype, const void* grad, int64_t n, double grad_scale,
+                   void* stats_dev, cft_stream_t stream);
+
+/* Fused sliced AdamW (optimizer.cpp:163-198 + write_back 124-132), one pass:
+ *   reads g, m, v, master; writes m, v, master and the param copy (param_dtype) through the
+ *   segment table.  bc1 = 1 - beta1^n and bc2 = 1 - beta2^n are computed by the caller on the
+ *   host in fp64 from the chunk-local counter n (already incremented).  If stats_dev[1] != 0
+ *   (a non-finite gradient was seen by cft_grad_stats) the kernel does nothing.
+ *   precond_dev[0..1] receive min/max of 1/(sqrt(vhat)+eps) (float, or double for F64).
+ * state_dtype: CFT_F32 (fp32 master/m/v/grad) or CFT_F64.  param_dtype: CFT_BF16, CFT_F32
+ * or CFT_F64. */
+int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, const void* grad,
+                    int64_t n, double grad_scale, const cft_adamw_hyper* hyper, double bc1,
+                    double bc2, cft_dtype param_dtype, void* param_base,
+                    const cft_segment* segments_dev, int32_t n_segments, const void* stats_dev,
+                    void* precond_dev, cft_stream_t stream);
+
+/* Plain block descent (optimizer.cpp:200-208), same segment write-back. */
+int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t n,
+                  double grad_scale, double eta, cft_dtype param_dtype, void* param_base,
+                  const cft_segment* segments_dev, int32_t n_segments, const void* stats_dev,
+                  cft_stream_t stream);
+
+/* Element conversion (e.g. fp32 master -> bf16 params at init). */
+int cft_convert(cft_dtype src_dtype, const void* src, cft_dtype dst_dtype, void* dst, int64_t n,
+                cft_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHUNKFT_B200_H_ */

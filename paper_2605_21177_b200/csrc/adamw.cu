@@ -1,0 +1,434 @@
+// adamw.cu -- fused sliced AdamW over the active chunk, plus its gradient-statistics pass.
+//
+// Reference: adamw_chunk_step (src/optimizer.cpp:163-198) + write_back (124-132) +
+// the trainer's grad_norm_sq (src/trainer.cpp:58-60).
+//
+// State layout: one contiguous array per state (master, m, v) and one for the gradient,
+// all in plan order (the chunk's slices concatenated) -- the layout the rotation moves
+// and the slice-aware wgrad writes into.  The updated master is written back to the model
+// parameters in the compute dtype through a per-slice segment table, fused into the same
+// pass: 16 B read + 14 B written per element for fp32 state / bf16 params (30 B/elem).
+//
+// The non-finite check must happen before any mutation (optimizer.cpp:169-173): the
+// statistics pass (which the trainer needs anyway for grad_norm_sq) records a non-finite
+// count; the update kernel reads it first and becomes a no-op when it is non-zero.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "cft_common.h"
+
+namespace cft::opt {
+
+constexpr int kThreads = 256;
+constexpr int kSmemSegs = 1024;
+
+__device__ __forceinline__ int find_segment(const cft_segment* segs, int n, long long i) {
+  // largest s with segs[s].state_off <= i
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].state_off <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <typename P>
+__device__ __forceinline__ void store_param(P* p, float v) {
+  if constexpr (std::is_same_v<P, __nv_bfloat16>) *p = __float2bfloat16_rn(v);
+  else *p = static_cast<P>(v);
+}
+
+__device__ __forceinline__ void atomic_min_pos(float* a, float v) {
+  atomicMin(reinterpret_cast<int*>(a), __float_as_int(v));
+}
+__device__ __forceinline__ void atomic_max_pos(float* a, float v) {
+  atomicMax(reinterpret_cast<int*>(a), __float_as_int(v));
+}
+
+// ---- statistics: sum g^2, non-finite count, first non-finite index ----
+template <typename T>
+__global__ void __launch_bounds__(kThreads) grad_stats_kernel(const T* __restrict__ g, long long n,
+                                                              double scale, double* stats) {
+  double acc = 0.0;
+  long long bad = LLONG_MAX;
+  unsigned nbad = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if constexpr (std::is_same_v<T, float>) {
+    const long long n4 = n / 4;
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    const float fs = static_cast<float>(scale);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+      const float4 v = g4[i];
+      const float e[4] = {v.x * fs, v.y * fs, v.z * fs, v.w * fs};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!isfinite(e[q])) {
+          ++nbad;
+          bad = min(bad, 4 * i + q);
+        } else {
+          acc += static_cast<double>(e[q]) * static_cast<double>(e[q]);
+        }
+      }
+    }
+    for (long long i = 4 * n4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+      const float e = g[i] * fs;
+      if (!isfinite(e)) { ++nbad; bad = min(bad, i); }
+      else acc += static_cast<double>(e) * static_cast<double>(e);
+    }
+  } else {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+      const double e = __dmul_rn(g[i], scale);
+      if (!isfinite(e)) { ++nbad; bad = min(bad, i); }
+      else acc = __dadd_rn(acc, __dmul_rn(e, e));
+    }
+  }
+  // block reduce
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    nbad += __shfl_xor_sync(0xffffffffu, nbad, o);
+    bad = min(bad, (long long)__shfl_xor_sync(0xffffffffu, bad, o));
+  }
+  __shared__ double s_acc[kThreads / 32];
+  __shared__ unsigned s_nbad[kThreads / 32];
+  __shared__ long long s_bad[kThreads / 32];
+  const int w = threadIdx.x / 32;
+  if ((threadIdx.x & 31) == 0) {
+    s_acc[w] = acc;
+    s_nbad[w] = nbad;
+    s_bad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    unsigned nb = 0;
+    long long b = LLONG_MAX;
+    for (int i = 0; i < kThreads / 32; ++i) {
+      a += s_acc[i];
+      nb += s_nbad[i];
+      b = min(b, s_bad[i]);
+    }
+    atomicAdd(&stats[0], a);
+    if (nb) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stats[1]), (unsigned long long)nb);
+      atomicMin(reinterpret_cast<long long*>(&stats[2]), b);
+    }
+  }
+}
+
+// ---- fp32-state AdamW, 4 elements per thread-iteration ----
+template <typename P>
+__global__ void __launch_bounds__(kThreads)
+    adamw_f32_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
+                     const float* __restrict__ grad, long long n, float gscale, float eta,
+                     float b1, float b2, float eps, float wd, float bc1, float bc2,
+                     P* __restrict__ param, const cft_segment* __restrict__ segs, int nseg,
+                     const double* __restrict__ stats, float* __restrict__ precond) {
+  if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
+  __shared__ cft_segment s_segs[kSmemSegs];
+  const bool in_smem = nseg <= kSmemSegs;
+  if (in_smem)
+    for (int i = threadIdx.x; i < nseg; i += blockDim.x) s_segs[i] = segs[i];
+  __syncthreads();
+  const cft_segment* sg = in_smem ? s_segs : segs;
+  const float omb1 = 1.f - b1, omb2 = 1.f - b2;
+  float pmin = INFINITY, pmax = 0.f;
+  const long long n4 = (n + 3) / 4;
+  const bool vec_ok = (n % 4) == 0;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n4;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long i0 = 4 * q;
+    float g[4], mm[4], vv[4], w[4];
+    if (vec_ok) {
+      const float4 g4 = reinterpret_cast<const float4*>(grad)[q];
+      const float4 m4 = reinterpret_cast<const float4*>(m)[q];
+      const float4 v4 = reinterpret_cast<const float4*>(v)[q];
+      const float4 w4 = reinterpret_cast<const float4*>(master)[q];
+      g[0] = g4.x; g[1] = g4.y; g[2] = g4.z; g[3] = g4.w;
+      mm[0] = m4.x; mm[1] = m4.y; mm[2] = m4.z; mm[3] = m4.w;
+      vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
+      w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const long long i = i0 + e;
+        g[e] = i < n ? grad[i] : 0.f;
+        mm[e] = i < n ? m[i] : 0.f;
+        vv[e] = i < n ? v[i] : 0.f;
+        w[e] = i < n ? master[i] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float ge = g[e] * gscale;
+      mm[e] = b1 * mm[e] + omb1 * ge;
+      vv[e] = b2 * vv[e] + omb2 * ge * ge;
+      const float mhat = mm[e] / bc1;
+      const float vhat = vv[e] / bc2;
+      const float denom = sqrtf(vhat) + eps;
+      w[e] = w[e] - eta * (mhat / denom + wd * w[e]);
+      if (i0 + e < n) {
+        const float pc = 1.f / denom;
+        pmin = fminf(pmin, pc);
+        pmax = fmaxf(pmax, pc);
+      }
+    }
+    if (vec_ok) {
+      reinterpret_cast<float4*>(m)[q] = make_float4(mm[0], mm[1], mm[2], mm[3]);
+      reinterpret_cast<float4*>(v)[q] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+      reinterpret_cast<float4*>(master)[q] = make_float4(w[0], w[1], w[2], w[3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const long long i = i0 + e;
+        if (i < n) {
+          m[i] = mm[e];
+          v[i] = vv[e];
+          master[i] = w[e];
+        }
+      }
+    }
+    // write-back through the segment table (optimizer.cpp:124-132)
+    if (param) {
+      int s = find_segment(sg, nseg, i0);
+      const long long send = sg[s].state_off + sg[s].count;
+      P* dst = param + sg[s].param_off + (i0 - sg[s].state_off);
+      if (i0 + 3 < send && i0 + 3 < n && std::is_same_v<P, __nv_bfloat16> &&
+          (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(w[0], w[1]);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(w[2], w[3]);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(dst) = pk;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const long long i = i0 + e;
+          if (i >= n) break;
+          while (i >= sg[s].state_off + sg[s].count) ++s;
+          store_param(param + sg[s].param_off + (i - sg[s].state_off), w[e]);
+        }
+      }
+    }
+  }
+  if (precond) {
+    for (int o = 16; o > 0; o >>= 1) {
+      pmin = fminf(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+      pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+    }
+    if ((threadIdx.x & 31) == 0 && pmax > 0.f) {
+      atomic_min_pos(&precond[0], pmin);
+      atomic_max_pos(&precond[1], pmax);
+    }
+  }
+}
+
+// ---- fp64-state AdamW: the reference's exact arithmetic (bit-identical) ----
+template <typename P>
+__global__ void __launch_bounds__(kThreads)
+    adamw_f64_kernel(double* master, double* m, double* v, const double* grad, long long n,
+                     double gscale, double eta, double b1, double b2, double eps, double wd,
+                     double bc1, double bc2, P* param, const cft_segment* segs, int nseg,
+                     const double* stats, double* precond) {
+  if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
+  double pmin = INFINITY, pmax = 0.0;
+  const double omb1 = __dsub_rn(1.0, b1), omb2 = __dsub_rn(1.0, b2);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double g = gscale == 1.0 ? grad[i] : __dmul_rn(grad[i], gscale);
+    const double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(omb1, g));
+    const double vi = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(omb2, g), g));
+    m[i] = mi;
+    v[i] = vi;
+    const double mhat = __ddiv_rn(mi, bc1);
+    const double vhat = __ddiv_rn(vi, bc2);
+    const double denom = __dadd_rn(__dsqrt_rn(vhat), eps);
+    const double w = master[i];
+    const double upd = __dmul_rn(eta, __dadd_rn(__ddiv_rn(mhat, denom), __dmul_rn(wd, w)));
+    const double nw = __dsub_rn(w, upd);
+    master[i] = nw;
+    const double pc = __ddiv_rn(1.0, denom);
+    pmin = fmin(pmin, pc);
+    pmax = fmax(pmax, pc);
+    if (param) {
+      const int s = find_segment(segs, nseg, i);
+      P* dst = param + segs[s].param_off + (i - segs[s].state_off);
+      if constexpr (std::is_same_v<P, __nv_bfloat16>) *dst = __double2bfloat16(nw);
+      else *dst = static_cast<P>(nw);
+    }
+  }
+  if (precond) {
+    for (int o = 16; o > 0; o >>= 1) {
+      pmin = fmin(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+      pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+    }
+    if ((threadIdx.x & 31) == 0 && pmax > 0.0) {
+      atomicMin(reinterpret_cast<long long*>(&precond[0]), __double_as_longlong(pmin));
+      atomicMax(reinterpret_cast<long long*>(&precond[1]), __double_as_longlong(pmax));
+    }
+  }
+}
+
+// ---- SGD (optimizer.cpp:200-208) ----
+template <typename S, typename P>
+__global__ void sgd_kernel(S* master, const S* grad, long long n, S gscale, S eta, P* param,
+                           const cft_segment* segs, int nseg, const double* stats) {
+  if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    S g = grad[i];
+    S nw;
+    if constexpr (std::is_same_v<S, double>) {
+      if (gscale != 1.0) g = __dmul_rn(g, gscale);
+      nw = __dsub_rn(master[i], __dmul_rn(eta, g));
+    } else {
+      nw = master[i] - eta * (g * gscale);
+    }
+    master[i] = nw;
+    if (param) {
+      const int s = find_segment(segs, nseg, i);
+      P* dst = param + segs[s].param_off + (i - segs[s].state_off);
+      if constexpr (std::is_same_v<P, __nv_bfloat16>) *dst = __float2bfloat16_rn((float)nw);
+      else *dst = static_cast<P>(nw);
+    }
+  }
+}
+
+template <typename S, typename D>
+__global__ void convert_kernel(const S* src, D* dst, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if constexpr (std::is_same_v<D, __nv_bfloat16>) {
+      if constexpr (std::is_same_v<S, double>) dst[i] = __double2bfloat16(src[i]);
+      else dst[i] = __float2bfloat16_rn(static_cast<float>(src[i]));
+    } else if constexpr (std::is_same_v<S, __nv_bfloat16>) {
+      dst[i] = static_cast<D>(__bfloat162float(src[i]));
+    } else {
+      dst[i] = static_cast<D>(src[i]);
+    }
+  }
+}
+
+inline int grid_for(long long work) {
+  const long long cap = (long long)num_sms() * 8;
+  return static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (work + kThreads - 1) / kThreads)));
+}
+
+}  // namespace cft::opt
+
+using namespace cft::opt;
+
+extern "C" {
+
+int cft_grad_stats(cft_dtype state_dtype, const void* grad, int64_t n, double grad_scale,
+                   void* stats_dev, cft_stream_t stream) {
+  return cft::guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (n <= 0) return;
+    if (state_dtype == CFT_F32) {
+      grad_stats_kernel<float><<<grid_for(n / 4 + 1), kThreads, 0, s>>>(
+          static_cast<const float*>(grad), n, grad_scale, static_cast<double*>(stats_dev));
+    } else if (state_dtype == CFT_F64) {
+      grad_stats_kernel<double><<<grid_for(n), kThreads, 0, s>>>(
+          static_cast<const double*>(grad), n, grad_scale, static_cast<double*>(stats_dev));
+    } else {
+      throw cft::Error("cft_grad_stats: state dtype must be F32 or F64");
+    }
+    cft::check_launch("grad_stats");
+  });
+}
+
+int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, const void* grad,
+                    int64_t n, double grad_scale, const cft_adamw_hyper* h, double bc1, double bc2,
+                    cft_dtype param_dtype, void* param_base, const cft_segment* segs,
+                    int32_t n_segments, const void* stats_dev, void* precond_dev,
+                    cft_stream_t stream) {
+  return cft::guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (n <= 0) return;
+    CFT_CHECK(h != nullptr, "cft_adamw_slice: null hyper");
+    CFT_CHECK(!param_base || (segs && n_segments > 0), "cft_adamw_slice: missing segments");
+    const double* st = static_cast<const double*>(stats_dev);
+    if (state_dtype == CFT_F32) {
+      const int grid = grid_for((n + 3) / 4);
+      auto go = [&](auto* p) {
+        adamw_f32_kernel<<<grid, kThreads, 0, s>>>(
+            static_cast<float*>(master), static_cast<float*>(m), static_cast<float*>(v),
+            static_cast<const float*>(grad), n, (float)grad_scale, (float)h->eta, (float)h->beta1,
+            (float)h->beta2, (float)h->epsilon, (float)h->weight_decay, (float)bc1, (float)bc2, p,
+            segs, n_segments, st, static_cast<float*>(precond_dev));
+      };
+      if (param_dtype == CFT_BF16) go(static_cast<__nv_bfloat16*>(param_base));
+      else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));
+      else throw cft::Error("cft_adamw_slice: fp32 state needs BF16 or F32 params");
+    } else if (state_dtype == CFT_F64) {
+      const int grid = grid_for(n);
+      auto go = [&](auto* p) {
+        adamw_f64_kernel<<<grid, kThreads, 0, s>>>(
+            static_cast<double*>(master), static_cast<double*>(m), static_cast<double*>(v),
+            static_cast<const double*>(grad), n, grad_scale, h->eta, h->beta1, h->beta2, h->epsilon,
+            h->weight_decay, bc1, bc2, p, segs, n_segments, st, static_cast<double*>(precond_dev));
+      };
+      if (param_dtype == CFT_F64) go(static_cast<double*>(param_base));
+      else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));
+      else go(static_cast<__nv_bfloat16*>(param_base));
+    } else {
+      throw cft::Error("cft_adamw_slice: state dtype must be F32 or F64");
+    }
+    cft::check_launch("adamw_slice");
+  });
+}
+
+int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t n,
+                  double grad_scale, double eta, cft_dtype param_dtype, void* param_base,
+                  const cft_segment* segs, int32_t n_segments, const void* stats_dev,
+                  cft_stream_t stream) {
+  return cft::guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (n <= 0) return;
+    const double* st = static_cast<const double*>(stats_dev);
+    const int grid = grid_for(n);
+    if (state_dtype == CFT_F32) {
+      auto go = [&](auto* p) {
+        sgd_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<float*>(master),
+                                                    static_cast<const float*>(grad), n,
+                                                    (float)grad_scale, (float)eta, p, segs,
+                                                    n_segments, st);
+      };
+      if (param_dtype == CFT_BF16) go(static_cast<__nv_bfloat16*>(param_base));
+      else go(static_cast<float*>(param_base));
+    } else {
+      auto go = [&](auto* p) {
+        sgd_kernel<double><<<grid, kThreads, 0, s>>>(static_cast<double*>(master),
+                                                     static_cast<const double*>(grad), n,
+                                                     grad_scale, eta, p, segs, n_segments, st);
+      };
+      if (param_dtype == CFT_F64) go(static_cast<double*>(param_base));
+      else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));
+      else go(static_cast<__nv_bfloat16*>(param_base));
+    }
+    cft::check_launch("sgd_slice");
+  });
+}
+
+int cft_convert(cft_dtype sd, const void* src, cft_dtype dd, void* dst, int64_t n,
+                cft_stream_t stream) {
+  return cft::guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (n <= 0) return;
+    const int grid = grid_for(n);
+    auto dispatch_dst = [&](auto* sp) {
+      if (dd == CFT_F32) convert_kernel<<<grid, kThreads, 0, s>>>(sp, static_cast<float*>(dst), n);
+      else if (dd == CFT_F64) convert_kernel<<<grid, kThreads, 0, s>>>(sp, static_cast<double*>(dst), n);
+      else convert_kernel<<<grid, kThreads, 0, s>>>(sp, static_cast<__nv_bfloat16*>(dst), n);
+    };
+    if (sd == CFT_F32) dispatch_dst(static_cast<const float*>(src));
+    else if (sd == CFT_F64) dispatch_dst(static_cast<const double*>(src));
+    else dispatch_dst(static_cast<const __nv_bfloat16*>(src));
+    cft::check_launch("convert");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// context.cpp -- error plumbing and the TMA descriptor encoder.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+
+#include "cft_common.h"
+
+namespace cft {
+
+namespace {
+thread_local std::string t_err;
+thread_local int t_status = CFT_OK;
+}  // namespace
+
+void set_error(const std::string& msg) {
+  t_err = msg;
+  t_status = CFT_ERR;
+}
+const std::string& last_error() { return t_err; }
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p)
+      throw Error("cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+CUtensorMap make_tmap_bf16(const void* base, uint64_t inner, uint64_t outer,
+                           uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
+  CUtensorMap m{};
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_stride_elems * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) +
+                "): dims " + std::to_string(inner) + "x" + std::to_string(outer));
+  return m;
+}
+
+}  // namespace cft
+
+extern "C" {
+const char* cft_last_error(void) { return cft::t_err.c_str(); }
+int cft_last_status(void) {
+  const int s = cft::t_status;
+  cft::t_status = CFT_OK;
+  return s;
+}
+int cft_version(void) { return 1; }
+}

@@ -1,0 +1,435 @@
+// gemm_tc.cu -- bf16 tcgen05/TMEM GEMMs for the chunk-local linear step (sm_100a).
+//
+// One warp-specialised persistent kernel, templated on operand majorness, serves the
+// three contractions of a Linear layer (reference: src/kernels_serial.cpp:12-49):
+//   forward  Y[N_tok,out]  = X . W^T        A=X  (K-major)   B=W  (K-major)
+//   dgrad    dX[N_tok,in]  = dY . W          A=dY (K-major)   B=W  (MN-major)
+//   wgrad_S  dW_S[|S|,in]  = dY[:,S]^T . X   A=dY (MN-major)  B=X  (MN-major)
+// The slice-aware wgrad never forms a dense dW: its tile space is |S| x in only, the A
+// operand's TMA coordinates start at row_begin (any value, no alignment needed), and
+// rows >= |S| are masked in the epilogue.  When |S| x in has too few tiles to fill 148
+// SMs the token (K) axis is split and partial sums are reduced with red.global.add.v4.f32.
+//
+// Roles (192 threads): warp0 = TMA producer, warp1 = tcgen05.mma issuer (one lane) and
+// TMEM owner, warps2-5 = epilogue (TMEM -> registers -> global).  4-6 stage smem ring,
+// 2 TMEM accumulators so the epilogue of tile i overlaps the mainloop of tile i+1.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "cft_common.h"
+#include "tc_ptx.cuh"
+
+namespace cft::tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+
+enum Epi : int { kEpiBf16 = 0, kEpiBf16Add = 1, kEpiF32 = 2, kEpiF32Add = 3, kEpiF32Red = 4 };
+
+struct Args {
+  int M, N, K;
+  int m_off;      // A coordinate offset along M (the slice's row_begin for wgrad)
+  int tiles_m, tiles_n, splits, kb_per_split, total_kb, num_units;
+  void* C;
+  long long ldc;
+  int epi;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+__device__ __forceinline__ void decode_unit(const Args& a, int u, int& tm, int& tn, int& sp) {
+  // split-major so consecutive CTAs share the same output tile's operands in L2
+  sp = u % a.splits;
+  const int t = u / a.splits;
+  tm = t % a.tiles_m;
+  tn = t / a.tiles_m;
+}
+
+template <bool A_MN, bool B_MN, int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                     const __grid_constant__ CUtensorMap tmap_b, const Args args) {
+  using C_ = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + C_::STAGES * C_::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + C_::STAGES * C_::B_BYTES);
+  uint64_t* empty = full + C_::STAGES;
+  uint64_t* tfull = empty + C_::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmap_a);
+    ptx::tma_prefetch(&tmap_b);
+    for (int s = 0; s < C_::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<C_::TMEM_COLS>(tslot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < args.num_units; u += gridDim.x) {
+        int tm, tn, sp;
+        decode_unit(args, u, tm, tn, sp);
+        const int kb0 = sp * args.kb_per_split;
+        const int kb1 = min(kb0 + args.kb_per_split, args.total_kb);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_expect_tx(&full[stage], C_::STAGE_BYTES);
+          const int k0 = kb * BK;
+          uint8_t* da = sa + stage * C_::A_BYTES;
+          uint8_t* db = sb + stage * C_::B_BYTES;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              ptx::tma_load_2d(da + j * (BK * 128), &tmap_a, &full[stage],
+                               args.m_off + tm * BM + j * 64, k0);
+          } else {
+            ptx::tma_load_2d(da, &tmap_a, &full[stage], k0, args.m_off + tm * BM);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              ptx::tma_load_2d(db + j * (BK * 128), &tmap_b, &full[stage], tn * BN + j * 64, k0);
+          } else {
+            ptx::tma_load_2d(db, &tmap_b, &full[stage], k0, tn * BN);
+          }
+          if (++stage == C_::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < args.num_units; u += gridDim.x) {
+        int tm, tn, sp;
+        decode_unit(args, u, tm, tn, sp);
+        const int kb0 = sp * args.kb_per_split;
+        const int kb1 = min(kb0 + args.kb_per_split, args.total_kb);
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(sa + stage * C_::A_BYTES);
+          const uint32_t b_base = ptx::smem_u32(sb + stage * C_::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: 16 elements = 32 B step inside the 128B swizzle row.
+            // MN-major: 16 k-rows = two 1024 B swizzle atoms.
+            const uint64_t adesc = A_MN ? ptx::smem_desc_sw128(a_base + k * 2048, BK * 128, 1024)
+                                        : ptx::smem_desc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(b_base + k * 2048, BK * 128, 1024)
+                                        : ptx::smem_desc_sw128(b_base + k * 32, 16, 1024);
+            ptx::umma_bf16(d_tmem, adesc, bdesc, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == C_::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // Epilogue: warp w may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < args.num_units; u += gridDim.x) {
+      int tm, tn, sp;
+      decode_unit(args, u, tm, tn, sp);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = tm * BM + quarter * 32 + lane;
+      const bool row_ok = row < args.M;
+      const long long rbase = static_cast<long long>(row) * args.ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c, r);
+        ptx::tmem_wait_ld();
+        const int col = tn * BN + c;
+        if (!row_ok || col >= args.N) continue;
+        const bool full16 = col + 16 <= args.N;
+        if (args.epi >= kEpiF32) {
+          float* out = static_cast<float*>(args.C) + rbase + col;
+          const bool vec = full16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+          if (vec) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+              const float a0 = __uint_as_float(r[j]), a1 = __uint_as_float(r[j + 1]);
+              const float a2 = __uint_as_float(r[j + 2]), a3 = __uint_as_float(r[j + 3]);
+              float4* p = reinterpret_cast<float4*>(out + j);
+              if (args.epi == kEpiF32Red) {
+                ptx::red_add_v4(out + j, a0, a1, a2, a3);
+              } else if (args.epi == kEpiF32Add) {
+                float4 o = *p;
+                *p = make_float4(o.x + a0, o.y + a1, o.z + a2, o.w + a3);
+              } else {
+                *p = make_float4(a0, a1, a2, a3);
+              }
+            }
+          } else {
+            for (int j = 0; j < 16 && col + j < args.N; ++j) {
+              const float a0 = __uint_as_float(r[j]);
+              if (args.epi == kEpiF32Red) atomicAdd(out + j, a0);
+              else if (args.epi == kEpiF32Add) out[j] += a0;
+              else out[j] = a0;
+            }
+          }
+        } else {
+          __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.C) + rbase + col;
+          const bool vec = full16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+          if (vec) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 8) {
+              uint4 pk;
+              uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+              if (args.epi == kEpiBf16Add) {
+                const uint4 old = *reinterpret_cast<const uint4*>(out + j);
+                const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float2 of = __bfloat1622float2(o2[q]);
+                  __nv_bfloat162 v = __floats2bfloat162_rn(of.x + __uint_as_float(r[j + 2 * q]),
+                                                           of.y + __uint_as_float(r[j + 2 * q + 1]));
+                  w[q] = *reinterpret_cast<uint32_t*>(&v);
+                }
+              } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[j + 2 * q]),
+                                                           __uint_as_float(r[j + 2 * q + 1]));
+                  w[q] = *reinterpret_cast<uint32_t*>(&v);
+                }
+              }
+              *reinterpret_cast<uint4*>(out + j) = pk;
+            }
+          } else {
+            for (int j = 0; j < 16 && col + j < args.N; ++j) {
+              float a0 = __uint_as_float(r[j]);
+              if (args.epi == kEpiBf16Add) a0 += __bfloat162float(out[j]);
+              out[j] = __float2bfloat16_rn(a0);
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<C_::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Host side
+
+namespace {
+
+struct MapKey {
+  const void* base;
+  uint64_t inner, outer, stride;
+  uint32_t bi, bo;
+  bool operator<(const MapKey& o) const {
+    return std::tie(base, inner, outer, stride, bi, bo) <
+           std::tie(o.base, o.inner, o.outer, o.stride, o.bi, o.bo);
+  }
+};
+
+CUtensorMap cached_map(const void* base, uint64_t inner, uint64_t outer, uint64_t stride,
+                       uint32_t bi, uint32_t bo) {
+  static std::mutex mu;
+  static std::map<MapKey, CUtensorMap> cache;
+  const MapKey key{base, inner, outer, stride, bi, bo};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cache.size() > 4096) cache.clear();
+  CUtensorMap m = make_tmap_bf16(base, inner, outer, stride, bi, bo);
+  cache.emplace(key, m);
+  return m;
+}
+
+template <bool A_MN, bool B_MN, int BN>
+void launch(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream_t stream) {
+  using C_ = Cfg<BN>;
+  auto kern = gemm_bf16_kernel<A_MN, B_MN, BN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    CFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(C_::SMEM)));
+    attr_done = true;
+  }
+  const int grid = std::min(a.num_units, num_sms());
+  kern<<<grid, kThreads, C_::SMEM, stream>>>(ta, tb, a);
+  check_launch("gemm_bf16_kernel");
+}
+
+// Choose the number of K splits so that (tiles x splits) fills the SMs well.
+int choose_splits(int tiles, int total_kb, bool allow) {
+  if (!allow) return 1;
+  const int sms = num_sms();
+  if (tiles >= sms) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 16; ++s) {
+    if (total_kb / s < 4) break;  // keep >= 256 tokens per split
+    const int units = tiles * s;
+    const int waves = (units + sms - 1) / sms;
+    const double eff = static_cast<double>(units) / (waves * sms);
+    if (eff > best_eff + 0.05) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
+void fill_units(Args& a, int BN, bool allow_split) {
+  a.tiles_m = (a.M + BM - 1) / BM;
+  a.tiles_n = (a.N + BN - 1) / BN;
+  a.total_kb = (a.K + BK - 1) / BK;
+  const int tiles = a.tiles_m * a.tiles_n;
+  int s = choose_splits(tiles, a.total_kb, allow_split);
+  a.kb_per_split = (a.total_kb + s - 1) / s;
+  a.splits = (a.total_kb + a.kb_per_split - 1) / a.kb_per_split;
+  a.num_units = tiles * a.splits;
+}
+
+bool tc_ok(int64_t inner_dim, const void* p) {
+  return (inner_dim % 8) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
+}  // namespace
+
+// Usability predicate (TMA: 16-byte aligned base and row strides).
+bool linear_shapes_ok(const void* x, const void* w, int64_t in_dim, int64_t out_dim) {
+  return tc_ok(in_dim, x) && tc_ok(in_dim, w) && (out_dim % 8) == 0;
+}
+
+// Y = X W^T, bf16 out (epi kEpiBf16) -- forward.
+void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
+                void* y, cudaStream_t stream) {
+  Args a{};
+  a.M = static_cast<int>(n_tok);
+  a.N = static_cast<int>(out_dim);
+  a.K = static_cast<int>(in_dim);
+  a.C = y;
+  a.ldc = out_dim;
+  a.epi = kEpiBf16;
+  const int BN = out_dim >= 256 ? 256 : 128;
+  const CUtensorMap ta = cached_map(x, in_dim, n_tok, in_dim, 64, BM);
+  if (BN == 256) {
+    fill_units(a, 256, false);
+    const CUtensorMap tb = cached_map(w, in_dim, out_dim, in_dim, 64, 256);
+    launch<false, false, 256>(ta, tb, a, stream);
+  } else {
+    fill_units(a, 128, false);
+    const CUtensorMap tb = cached_map(w, in_dim, out_dim, in_dim, 64, 128);
+    launch<false, false, 128>(ta, tb, a, stream);
+  }
+}
+
+// dX (+)= dY W -- dgrad; bf16 out.
+void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w, int64_t in_dim,
+                  void* dx, int beta, cudaStream_t stream) {
+  Args a{};
+  a.M = static_cast<int>(n_tok);
+  a.N = static_cast<int>(in_dim);
+  a.K = static_cast<int>(out_dim);
+  a.C = dx;
+  a.ldc = in_dim;
+  a.epi = beta ? kEpiBf16Add : kEpiBf16;
+  const CUtensorMap ta = cached_map(dy, out_dim, n_tok, out_dim, 64, BM);
+  const CUtensorMap tb = cached_map(w, in_dim, out_dim, in_dim, 64, 64);
+  if (in_dim >= 256) {
+    fill_units(a, 256, false);
+    launch<false, true, 256>(ta, tb, a, stream);
+  } else {
+    fill_units(a, 128, false);
+    launch<false, true, 128>(ta, tb, a, stream);
+  }
+}
+
+// dW_S (+)= dY[:, rb:re)^T X -- slice-aware wgrad, fp32 out.
+void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const void* x,
+                        int64_t in_dim, int64_t rb, int64_t re, float* dw, int accumulate,
+                        cudaStream_t stream) {
+  Args a{};
+  a.M = static_cast<int>(re - rb);
+  a.N = static_cast<int>(in_dim);
+  a.K = static_cast<int>(n_tok);
+  a.m_off = static_cast<int>(rb);
+  a.C = dw;
+  a.ldc = in_dim;
+  const CUtensorMap ta = cached_map(dy, out_dim, n_tok, out_dim, 64, 64);
+  const CUtensorMap tb = cached_map(x, in_dim, n_tok, in_dim, 64, 64);
+  const int BN = in_dim >= 256 ? 256 : 128;
+  fill_units(a, BN, true);
+  if (a.splits > 1) {
+    // Partial sums race into dw: zero first unless accumulating.
+    if (!accumulate)
+      CFT_CUDA(cudaMemset2DAsync(dw, sizeof(float) * in_dim, 0, sizeof(float) * in_dim, a.M,
+                                 stream));
+    a.epi = kEpiF32Red;
+  } else {
+    a.epi = accumulate ? kEpiF32Add : kEpiF32;
+  }
+  if (BN == 256) launch<true, true, 256>(ta, tb, a, stream);
+  else launch<true, true, 128>(ta, tb, a, stream);
+}
+
+}  // namespace cft::tc

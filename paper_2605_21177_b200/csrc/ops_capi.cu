@@ -1,0 +1,252 @@
+// ops_capi.cu -- performance-level C ABI for the Linear / Embedding operators.
+//
+// Dispatch is by dtype only (no multi-backend switch): bf16 -> tcgen05 tensor-core
+// kernels when TMA can describe the operands (row strides multiple of 16 B), else the
+// bf16 CUDA-core kernel; fp32 -> CUDA-core fp32; fp64 -> the bit-exact fp64 kernels.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "cft_common.h"
+
+namespace cft {
+namespace tc {
+bool linear_shapes_ok(const void* x, const void* w, int64_t in_dim, int64_t out_dim);
+void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
+                void* y, cudaStream_t stream);
+void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w, int64_t in_dim,
+                  void* dx, int beta, cudaStream_t stream);
+void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const void* x,
+                        int64_t in_dim, int64_t rb, int64_t re, float* dw, int accumulate,
+                        cudaStream_t stream);
+}  // namespace tc
+namespace simt {
+void linear_fwd_f32(const float*, int64_t, int64_t, const float*, int64_t, const float*, float*,
+                    cudaStream_t);
+void linear_fwd_bf16(const __nv_bfloat16*, int64_t, int64_t, const __nv_bfloat16*, int64_t,
+                     __nv_bfloat16*, cudaStream_t);
+void add_bias_bf16(__nv_bfloat16*, const __nv_bfloat16*, int64_t, int64_t, cudaStream_t);
+void linear_dgrad_f32(const float*, int64_t, int64_t, const float*, int64_t, float*, int,
+                      cudaStream_t);
+void linear_dgrad_bf16(const __nv_bfloat16*, int64_t, int64_t, const __nv_bfloat16*, int64_t,
+                       __nv_bfloat16*, int, cudaStream_t);
+template <typename T>
+void linear_wgrad_slice_simt(const T*, int64_t, int64_t, const T*, int64_t, int64_t, int64_t,
+                             float*, int, cudaStream_t);
+template <typename T>
+void linear_dbias_slice(const T*, int64_t, int64_t, int64_t, int64_t, float*, int, cudaStream_t);
+}  // namespace simt
+namespace f64 {
+void linear_forward(const double*, int, int, const double*, int, const double*, double*,
+                    cudaStream_t);
+void linear_dinput(const double*, int, int, const double*, int, double*, cudaStream_t);
+void linear_dweight(const double*, int, int, const double*, int, long long, long long, double*,
+                    cudaStream_t);
+void linear_dbias(const double*, int, int, long long, long long, double*, cudaStream_t);
+void embedding_gather(const double*, int, const int*, int, double*, cudaStream_t);
+void embedding_scatter(const double*, int, const int*, int, long long, long long, double*,
+                       unsigned long long*, cudaStream_t);
+}  // namespace f64
+
+namespace {
+
+// TMA needs a 16-byte aligned base and 16-byte multiple row pitch (8 bf16).
+bool tma_ok(const void* p, int64_t row_elems) {
+  return row_elems > 0 && (row_elems % 8) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
+// y[p,:] = table[tok[p],:]  (16-byte vectorised rows when possible)
+template <typename T>
+__global__ void gather_kernel(const T* __restrict__ table, long long dim,
+                              const int32_t* __restrict__ tokens, long long positions,
+                              T* __restrict__ y) {
+  const long long p = blockIdx.x;
+  if (p >= positions) return;
+  const T* src = table + (long long)tokens[p] * dim;
+  T* dst = y + p * dim;
+  constexpr int V = 16 / sizeof(T);
+  if (dim % V == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    for (long long j = threadIdx.x; j < dim / V; j += blockDim.x)
+      reinterpret_cast<uint4*>(dst)[j] = reinterpret_cast<const uint4*>(src)[j];
+  } else {
+    for (long long j = threadIdx.x; j < dim; j += blockDim.x) dst[j] = src[j];
+  }
+}
+
+// One pass over positions, filter rb <= tok < re, fp32 red-add into the slice.
+template <typename T>
+__global__ void scatter_slice_kernel(const T* __restrict__ dy, long long dim,
+                                     const int32_t* __restrict__ tokens, long long positions,
+                                     long long rb, long long re, float* dtable,
+                                     unsigned long long* matched) {
+  const long long p = blockIdx.x;
+  if (p >= positions) return;
+  const long long tok = tokens[p];
+  if (tok < rb || tok >= re) return;
+  if (matched && threadIdx.x == 0) atomicAdd(matched, 1ull);
+  const T* src = dy + p * dim;
+  float* dst = dtable + (tok - rb) * dim;
+  for (long long j = threadIdx.x; j < dim; j += blockDim.x) {
+    float v;
+    if constexpr (std::is_same_v<T, float>) v = src[j];
+    else v = __bfloat162float(src[j]);
+    atomicAdd(dst + j, v);
+  }
+}
+
+}  // namespace
+}  // namespace cft
+
+using namespace cft;
+
+extern "C" {
+
+int cft_linear_fwd(cft_dtype dtype, const void* x, int64_t n_tok, int64_t in_dim, const void* w,
+                   int64_t out_dim, const void* bias, void* y, cft_stream_t stream) {
+  return guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (n_tok <= 0 || out_dim <= 0) return;
+    if (dtype == CFT_BF16) {
+      if (in_dim > 0 && tma_ok(x, in_dim) && tma_ok(w, in_dim) && tma_ok(y, out_dim))
+        tc::linear_fwd(x, n_tok, in_dim, w, out_dim, y, s);
+      else
+        simt::linear_fwd_bf16(static_cast<const __nv_bfloat16*>(x), n_tok, in_dim,
+                              static_cast<const __nv_bfloat16*>(w), out_dim,
+                              static_cast<__nv_bfloat16*>(y), s);
+      if (bias)
+        simt::add_bias_bf16(static_cast<__nv_bfloat16*>(y),
+                            static_cast<const __nv_bfloat16*>(bias), n_tok, out_dim, s);
+    } else if (dtype == CFT_F32) {
+      simt::linear_fwd_f32(static_cast<const float*>(x), n_tok, in_dim,
+                           static_cast<const float*>(w), out_dim, static_cast<const float*>(bias),
+                           static_cast<float*>(y), s);
+    } else {
+      f64::linear_forward(static_cast<const double*>(x), (int)n_tok, (int)in_dim,
+                          static_cast<const double*>(w), (int)out_dim,
+                          static_cast<const double*>(bias), static_cast<double*>(y), s);
+    }
+  });
+}
+
+int cft_linear_dgrad(cft_dtype dtype, const void* dy, int64_t n_tok, int64_t out_dim,
+                     const void* w, int64_t in_dim, void* dx, int beta, cft_stream_t stream) {
+  return guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (n_tok <= 0 || in_dim <= 0) return;
+    if (dtype == CFT_BF16) {
+      if (out_dim > 0 && tma_ok(dy, out_dim) && tma_ok(w, in_dim) && tma_ok(dx, in_dim))
+        tc::linear_dgrad(dy, n_tok, out_dim, w, in_dim, dx, beta, s);
+      else
+        simt::linear_dgrad_bf16(static_cast<const __nv_bfloat16*>(dy), n_tok, out_dim,
+                                static_cast<const __nv_bfloat16*>(w), in_dim,
+                                static_cast<__nv_bfloat16*>(dx), beta, s);
+    } else if (dtype == CFT_F32) {
+      simt::linear_dgrad_f32(static_cast<const float*>(dy), n_tok, out_dim,
+                             static_cast<const float*>(w), in_dim, static_cast<float*>(dx), beta, s);
+    } else {
+      if (!beta) CFT_CUDA(cudaMemsetAsync(dx, 0, sizeof(double) * n_tok * in_dim, s));
+      f64::linear_dinput(static_cast<const double*>(dy), (int)n_tok, (int)out_dim,
+                         static_cast<const double*>(w), (int)in_dim, static_cast<double*>(dx), s);
+    }
+  });
+}
+
+int cft_linear_wgrad_slice(cft_dtype dtype, const void* dy, int64_t n_tok, int64_t out_dim,
+                           const void* x, int64_t in_dim, int64_t rb, int64_t re, void* dw,
+                           int accumulate, cft_stream_t stream) {
+  return guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    CFT_CHECK(rb >= 0 && re <= out_dim && rb <= re, "linear wgrad: row range out of bounds");
+    if (re == rb || in_dim <= 0) return;
+    const size_t esz = dtype == CFT_F64 ? 8 : 4;
+    if (n_tok <= 0) {
+      if (!accumulate) CFT_CUDA(cudaMemsetAsync(dw, 0, esz * (re - rb) * in_dim, s));
+      return;
+    }
+    if (dtype == CFT_BF16) {
+      if (tma_ok(dy, out_dim) && tma_ok(x, in_dim) && (in_dim % 4) == 0 &&
+          (reinterpret_cast<uintptr_t>(dw) & 15) == 0)
+        tc::linear_wgrad_slice(dy, n_tok, out_dim, x, in_dim, rb, re, static_cast<float*>(dw),
+                               accumulate, s);
+      else
+        simt::linear_wgrad_slice_simt(static_cast<const __nv_bfloat16*>(dy), n_tok, out_dim,
+                                      static_cast<const __nv_bfloat16*>(x), in_dim, rb, re,
+                                      static_cast<float*>(dw), accumulate, s);
+    } else if (dtype == CFT_F32) {
+      simt::linear_wgrad_slice_simt(static_cast<const float*>(dy), n_tok, out_dim,
+                                    static_cast<const float*>(x), in_dim, rb, re,
+                                    static_cast<float*>(dw), accumulate, s);
+    } else {
+      if (!accumulate) CFT_CUDA(cudaMemsetAsync(dw, 0, esz * (re - rb) * in_dim, s));
+      f64::linear_dweight(static_cast<const double*>(dy), (int)n_tok, (int)out_dim,
+                          static_cast<const double*>(x), (int)in_dim, rb, re,
+                          static_cast<double*>(dw), s);
+    }
+  });
+}
+
+int cft_linear_dbias_slice(cft_dtype dtype, const void* dy, int64_t n_tok, int64_t out_dim,
+                           int64_t rb, int64_t re, void* db, int accumulate, cft_stream_t stream) {
+  return guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    CFT_CHECK(rb >= 0 && re <= out_dim && rb <= re, "linear dbias: row range out of bounds");
+    if (re == rb) return;
+    if (dtype == CFT_BF16)
+      simt::linear_dbias_slice(static_cast<const __nv_bfloat16*>(dy), n_tok, out_dim, rb, re,
+                               static_cast<float*>(db), accumulate, s);
+    else if (dtype == CFT_F32)
+      simt::linear_dbias_slice(static_cast<const float*>(dy), n_tok, out_dim, rb, re,
+                               static_cast<float*>(db), accumulate, s);
+    else {
+      if (!accumulate) CFT_CUDA(cudaMemsetAsync(db, 0, sizeof(double) * (re - rb), s));
+      f64::linear_dbias(static_cast<const double*>(dy), (int)n_tok, (int)out_dim, rb, re,
+                        static_cast<double*>(db), s);
+    }
+  });
+}
+
+int cft_embedding_gather(cft_dtype dtype, const void* table, int64_t dim, const int32_t* tokens,
+                         int64_t positions, void* y, cft_stream_t stream) {
+  return guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (positions <= 0 || dim <= 0) return;
+    const int threads = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, dim / 8)));
+    if (dtype == CFT_BF16)
+      gather_kernel<<<(unsigned)positions, threads, 0, s>>>(
+          static_cast<const __nv_bfloat16*>(table), dim, tokens, positions,
+          static_cast<__nv_bfloat16*>(y));
+    else if (dtype == CFT_F32)
+      gather_kernel<<<(unsigned)positions, threads, 0, s>>>(static_cast<const float*>(table), dim,
+                                                            tokens, positions, static_cast<float*>(y));
+    else
+      f64::embedding_gather(static_cast<const double*>(table), (int)dim, tokens, (int)positions,
+                            static_cast<double*>(y), s);
+    check_launch("embedding_gather");
+  });
+}
+
+int cft_embedding_scatter_slice(cft_dtype dtype, const void* dy, int64_t dim,
+                                const int32_t* tokens, int64_t positions, int64_t rb, int64_t re,
+                                void* dtable, int64_t* matched_dev, cft_stream_t stream) {
+  return guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (positions <= 0 || re <= rb || dim <= 0) return;
+    auto* matched = reinterpret_cast<unsigned long long*>(matched_dev);
+    const int threads = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, dim)));
+    if (dtype == CFT_BF16)
+      scatter_slice_kernel<<<(unsigned)positions, threads, 0, s>>>(
+          static_cast<const __nv_bfloat16*>(dy), dim, tokens, positions, rb, re,
+          static_cast<float*>(dtable), matched);
+    else if (dtype == CFT_F32)
+      scatter_slice_kernel<<<(unsigned)positions, threads, 0, s>>>(
+          static_cast<const float*>(dy), dim, tokens, positions, rb, re,
+          static_cast<float*>(dtable), matched);
+    else
+      f64::embedding_scatter(static_cast<const double*>(dy), (int)dim, tokens, (int)positions, rb,
+                             re, static_cast<double*>(dtable), matched, s);
+    check_launch("embedding_scatter_slice");
+  });
+}
+
+}  // extern "C"

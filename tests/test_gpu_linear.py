@@ -1,0 +1,138 @@
+"""GPU parity: the chunk-local Linear operators vs the oracle (and torch fp32 at full size).
+
+Reference semantics: src/kernels_serial.cpp:12-58, src/ops.cpp:19-48.
+Tolerances (SURVEY.md section 7 "Hard parts"):
+  * fp64 path: bit-identical to the oracle (same operation order, no FMA).
+  * fp32 path: normwise relative error <= 1e-5.
+  * bf16 path: the fp64 oracle is fed the same bf16-rounded operands; normwise <= 2e-2
+    (measured ~1e-6: only fp32 accumulation-order error remains).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import lib as orc  # noqa: E402
+
+
+def nrm(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def rnd(shape, seed, lo=-1.0, hi=1.0):
+    return np.random.default_rng(seed).uniform(lo, hi, size=shape)
+
+
+def to_dev(a, dtype, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev).to(dtype).contiguous()
+
+
+def bf16_round(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+SHAPES = [  # (n_tok, in_dim, out_dim, rb, re)
+    (256, 256, 384, 0, 128),
+    (384, 512, 512, 37, 301),       # unaligned row_begin, ragged |S|
+    (1000, 320, 640, 128, 640),     # ragged token count, |S| not a tile multiple
+    (512, 1024, 256, 0, 256),       # full slice
+]
+
+
+@pytest.mark.parametrize("n_tok,in_dim,out_dim,rb,re", SHAPES)
+def test_bf16_wgrad_slice_vs_oracle(cuda, n_tok, in_dim, out_dim, rb, re):
+    from paper_2605_21177_b200 import ops
+    dy = bf16_round(rnd((n_tok, out_dim), 1))
+    x = bf16_round(rnd((n_tok, in_dim), 2))
+    ref = orc.linear_dweight(dy, x, rb, re)
+    got = ops.linear_wgrad_slice(to_dev(dy, torch.bfloat16, cuda), to_dev(x, torch.bfloat16, cuda),
+                                 rb, re)
+    torch.cuda.synchronize()
+    assert got.shape == (re - rb, in_dim)
+    assert nrm(got.cpu().numpy(), ref) < 2e-2
+    assert nrm(got.cpu().numpy(), ref) < 1e-5  # accumulation error only
+
+
+@pytest.mark.parametrize("n_tok,in_dim,out_dim,rb,re", SHAPES[:2])
+def test_bf16_wgrad_accumulate(cuda, n_tok, in_dim, out_dim, rb, re):
+    from paper_2605_21177_b200 import ops
+    dy = bf16_round(rnd((n_tok, out_dim), 3))
+    x = bf16_round(rnd((n_tok, in_dim), 4))
+    base = rnd((re - rb, in_dim), 5)
+    ref = orc.linear_dweight(dy, x, rb, re, dw=base)
+    out = to_dev(base, torch.float32, cuda)
+    ops.linear_wgrad_slice(to_dev(dy, torch.bfloat16, cuda), to_dev(x, torch.bfloat16, cuda), rb, re,
+                           out=out, accumulate=True)
+    torch.cuda.synchronize()
+    assert nrm(out.cpu().numpy(), ref) < 1e-5
+
+
+@pytest.mark.parametrize("n_tok,in_dim,out_dim", [(256, 256, 384), (1000, 512, 320), (128, 64, 256)])
+def test_bf16_forward_and_dgrad_vs_oracle(cuda, n_tok, in_dim, out_dim):
+    from paper_2605_21177_b200 import ops
+    x = bf16_round(rnd((n_tok, in_dim), 6))
+    w = bf16_round(rnd((out_dim, in_dim), 7))
+    dy = bf16_round(rnd((n_tok, out_dim), 8))
+    y = ops.linear_forward(to_dev(x, torch.bfloat16, cuda), to_dev(w, torch.bfloat16, cuda))
+    dx = ops.linear_dgrad(to_dev(dy, torch.bfloat16, cuda), to_dev(w, torch.bfloat16, cuda))
+    torch.cuda.synchronize()
+    assert nrm(y.float().cpu().numpy(), orc.linear_forward(x, w)) < 2e-2
+    assert nrm(dx.float().cpu().numpy(), orc.linear_dinput(dy, w)) < 2e-2
+    # bf16 output rounding dominates (2^-9 relative per element)
+    assert nrm(y.float().cpu().numpy(), orc.linear_forward(x, w)) < 4e-3
+    assert nrm(dx.float().cpu().numpy(), orc.linear_dinput(dy, w)) < 4e-3
+
+
+@pytest.mark.parametrize("n_tok,in_dim,out_dim,rb,re", [(200, 96, 160, 7, 150), (64, 3, 4, 1, 3)])
+def test_fp32_path_vs_oracle(cuda, n_tok, in_dim, out_dim, rb, re):
+    from paper_2605_21177_b200 import ops
+    x, w, dy = rnd((n_tok, in_dim), 9), rnd((out_dim, in_dim), 10), rnd((n_tok, out_dim), 11)
+    b = rnd((out_dim,), 12)
+    f = lambda a: to_dev(a, torch.float32, cuda)
+    y = ops.linear_forward(f(x), f(w), f(b))
+    dx = ops.linear_dgrad(f(dy), f(w))
+    dw = ops.linear_wgrad_slice(f(dy), f(x), rb, re)
+    db = ops.linear_dbias_slice(f(dy), rb, re)
+    torch.cuda.synchronize()
+    assert nrm(y.cpu().numpy(), orc.linear_forward(x, w, b)) < 1e-5
+    assert nrm(dx.cpu().numpy(), orc.linear_dinput(dy, w)) < 1e-5
+    assert nrm(dw.cpu().numpy(), orc.linear_dweight(dy, x, rb, re)) < 1e-5
+    assert nrm(db.cpu().numpy(), orc.linear_dbias(dy, rb, re)) < 1e-5
+
+
+@pytest.mark.parametrize("n_tok,in_dim,out_dim,rb,re", [(50, 33, 21, 5, 17), (8, 3, 4, 0, 4)])
+def test_fp64_path_bit_exact(cuda, n_tok, in_dim, out_dim, rb, re):
+    from paper_2605_21177_b200 import ops
+    x, w, dy = rnd((n_tok, in_dim), 13), rnd((out_dim, in_dim), 14), rnd((n_tok, out_dim), 15)
+    b = rnd((out_dim,), 16)
+    f = lambda a: to_dev(a, torch.float64, cuda)
+    y = ops.linear_forward(f(x), f(w), f(b)).cpu().numpy()
+    dx = ops.linear_dgrad(f(dy), f(w)).cpu().numpy()
+    dw = ops.linear_wgrad_slice(f(dy), f(x), rb, re).cpu().numpy()
+    db = ops.linear_dbias_slice(f(dy), rb, re).cpu().numpy()
+    assert np.array_equal(y, orc.linear_forward(x, w, b))
+    assert np.array_equal(dx, orc.linear_dinput(dy, w))
+    assert np.array_equal(dw, orc.linear_dweight(dy, x, rb, re))
+    assert np.array_equal(db, orc.linear_dbias(dy, rb, re))
+
+
+def test_full_size_bf16_vs_torch_fp32(cuda):
+    """BASELINE configs[1] shape (d=4096, N_tok=8192) against a plain torch fp32 reference."""
+    from paper_2605_21177_b200 import ops
+    g = torch.Generator(device=cuda).manual_seed(0)
+    n, d = 8192, 4096
+    x = (torch.rand(n, d, device=cuda, generator=g) * 2 - 1).to(torch.bfloat16)
+    w = ((torch.rand(d, d, device=cuda, generator=g) - 0.5) / 64).to(torch.bfloat16)
+    dy = (torch.rand(n, d, device=cuda, generator=g) * 2 - 1).to(torch.bfloat16)
+    y = ops.linear_forward(x, w)
+    dx = ops.linear_dgrad(dy, w)
+    rb, re = 12376 % d, 12376 % d + 512  # unaligned slice start
+    dw = ops.linear_wgrad_slice(dy, x, rb, re)
+    xf, wf, dyf = x.float(), w.float(), dy.float()
+    for got, ref in ((y.float(), xf @ wf.t()), (dx.float(), dyf @ wf),
+                     (dw, dyf[:, rb:re].t() @ xf)):
+        err = (got - ref).norm() / ref.norm()
+        assert err.item() < 4e-3, err.item()
