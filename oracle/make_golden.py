@@ -1,0 +1,125 @@
+"""TEST INFRASTRUCTURE ONLY -- regenerate tests/golden/*.json from the reference library.
+
+Run here (where /root/reference exists):  make -C oracle ref && python -m oracle.make_golden
+Every value in the fixtures is produced by the UNMODIFIED reference code (oracle/_ref).
+"""
+import json
+import os
+
+import numpy as np
+
+from . import ref
+from .shapes import llama8b, llama70b
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def plans():
+    cases = []
+    # reference unit-test shapes (tests/test_partition.cpp)
+    cases.append(dict(name="a100x10_b20x10_K1", tensors=[(0, 100, 10), (1, 20, 10)], K=1))
+    cases.append(dict(name="a100x10_b20x10_K2", tensors=[(0, 100, 10), (1, 20, 10)], K=2))
+    cases.append(dict(name="a100x10_b20x10_K3", tensors=[(0, 100, 10), (1, 20, 10)], K=3))
+    cases.append(dict(name="virtual7e9_K8", tensors=[(0, 7_000_000, 1000)], K=8))
+    cases.append(dict(name="budget_half", tensors=[(0, 100, 10)], budget=8000))
+    cases.append(dict(name="budget_row", tensors=[(0, 100, 10)], budget=160))
+    cases.append(dict(name="four_by_100x3_K100", tensors=[(i, 100, 3) for i in range(4)], K=100))
+    cases.append(dict(name="frozen", tensors=[(0, 10, 2), (1, 50, 2, 1, False)], K=2))
+    cases.append(dict(name="per_tensor", tensors=[(0, 30, 4), (1, 5, 4), (2, 9, 9, 2, False)],
+                      per_tensor=True))
+    cases.append(dict(name="reg_order_shuffled", tensors=[(0, 7, 3, 2), (1, 5, 2, 0), (2, 9, 1, 1)], K=4))
+    cases.append(dict(name="policy_fp32_params", tensors=[(0, 33, 5), (1, 17, 8)], K=5,
+                      policy=(4, 4, 4, 4, 4)))
+    # quadratic-k2 preset: one 8x8 linear, K=2 (tests/test_runner.cpp:205 pins f48d7162a88bf8a9)
+    cases.append(dict(name="quadratic_k2", tensors=[(0, 8, 8)], K=2))
+    # random trials in the style of tests/test_partition.cpp:152-211
+    rng = np.random.default_rng(99)
+    for trial in range(40):
+        n = int(rng.integers(1, 7))
+        ts = [(i, int(rng.integers(1, 41)), int(rng.integers(1, 9))) for i in range(n)]
+        total = sum(t[1] for t in ts)
+        K = int(rng.integers(1, min(total, 12) + 1))
+        cases.append(dict(name=f"random{trial}", tensors=ts, K=K))
+    # Llama shapes (SURVEY.md section 8(c) lists K=8/64/128 hashes for 8B)
+    l8 = [(i, r, c) for i, (_, r, c) in enumerate(llama8b())]
+    for K in (1, 8, 64, 128):
+        cases.append(dict(name=f"llama8b_K{K}", tensors=l8, K=K, compact=True))
+    cases.append(dict(name="llama8b_budget2GiB", tensors=l8, budget=2 << 30, compact=True))
+    l70 = [(i, r, c) for i, (_, r, c) in enumerate(llama70b())]
+    cases.append(dict(name="llama70b_K64", tensors=l70, K=64, compact=True))
+    out = []
+    for c in cases:
+        names = [f"t{t[0]}" for t in c["tensors"]]
+        r = ref.partition(c["tensors"], K=c.get("K"), budget=c.get("budget"),
+                          per_tensor=c.get("per_tensor", False), policy=c.get("policy", (2, 4, 4, 4, 4)),
+                          names=names, want_json=not c.get("compact"))
+        rec = dict(name=c["name"], K_arg=c.get("K"), budget=c.get("budget"),
+                   per_tensor=c.get("per_tensor", False), policy=list(c.get("policy", (2, 4, 4, 4, 4))),
+                   hash=f"{r['hash']:016x}", K=r["K"], chunks=r["chunks"], byte_cost=r["byte_cost"],
+                   elements=r["elements"], total_mutable_bytes=r["total_mutable_bytes"],
+                   max_row_cost=r["max_row_cost"], json=r["json"])
+        if c.get("compact"):
+            rec["tensors"] = "llama8b" if "8b" in c["name"] else "llama70b"
+        else:
+            rec["tensors"] = [list(t) for t in c["tensors"]]
+        out.append(rec)
+    # error cases
+    errors = []
+    for name, kw in [("K_exceeds_rows", dict(tensors=[(0, 4, 2)], K=5)),
+                     ("K_zero", dict(tensors=[(0, 4, 2)], K=0)),
+                     ("budget_below_row", dict(tensors=[(0, 100, 10)], budget=159)),
+                     ("no_trainable", dict(tensors=[(0, 4, 2, 0, False)], K=1))]:
+        try:
+            ref.partition(kw["tensors"], K=kw.get("K"), budget=kw.get("budget"))
+            errors.append(dict(name=name, tensors=kw["tensors"], K=kw.get("K"), budget=kw.get("budget"),
+                               error=None))
+        except ValueError as e:
+            errors.append(dict(name=name, tensors=[list(t) for t in kw["tensors"]], K=kw.get("K"),
+                               budget=kw.get("budget"), error=str(e)))
+    return dict(plans=out, errors=errors)
+
+
+def schedules():
+    out = []
+    cases = [
+        (2, 3, 8, [16, 16], False, 0), (1, 2, 6, [48], False, 0), (3, 1, 6, [16, 16, 16], False, 0),
+        (3, 2, 8, [16, 16, 16], False, 100), (3, 2, 8, [16, 16, 16], True, 100),
+        (4, 4, 37, [100, 90, 80, 70], True, 250), (5, 1, 23, [10, 20, 30, 40, 50], True, 1000),
+        (2, 2, 9, [7, 9], True, 0), (64, 64, 200, [125_517_824] * 64, True, 1 << 30),
+        (8, 1, 30, list(range(1, 9)), False, 5), (6, 3, 41, [3, 1, 4, 1, 5, 9], True, 7),
+    ]
+    for (K, T, steps, elems, pf, bw) in cases:
+        r = ref.schedule(K, T, steps, elems, prefetch=pf, bw=bw)
+        out.append(dict(K=K, T=T, steps=steps, elems=elems, prefetch=pf, bw=bw, **r))
+    return out
+
+
+def adamw():
+    rng = np.random.default_rng(5)
+    out = []
+    for (E, n0, hyper) in [(64, 0, (1e-3, 0.9, 0.999, 1e-8, 0.0)), (33, 4, (5e-3, 0.8, 0.99, 1e-6, 0.1)),
+                           (1, 0, (0.1, 0.9, 0.999, 1e-8, 0.0))]:
+        master = rng.uniform(-0.5, 0.5, E)
+        m = rng.uniform(-1e-3, 1e-3, E) if n0 else np.zeros(E)
+        v = rng.uniform(0, 1e-6, E) if n0 else np.zeros(E)
+        g = rng.uniform(-1, 1, E)
+        r = ref.adamw(master, m, v, g, n0, hyper)
+        out.append(dict(hyper=list(hyper), n_in=n0, master=master.tolist(), m=m.tolist(), v=v.tolist(),
+                        g=g.tolist(), master_out=r[0].tolist(), m_out=r[1].tolist(), v_out=r[2].tolist(),
+                        n_out=r[3], pmin=r[4], pmax=r[5]))
+    return out
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "plans.json"), "w") as f:
+        json.dump(plans(), f, indent=0)
+    with open(os.path.join(OUT, "schedules.json"), "w") as f:
+        json.dump(schedules(), f)
+    with open(os.path.join(OUT, "adamw.json"), "w") as f:
+        json.dump(adamw(), f)
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()

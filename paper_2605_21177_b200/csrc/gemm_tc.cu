@@ -6,8 +6,9 @@
 //   dgrad    dX[N_tok,in]  = dY . W          A=dY (K-major)   B=W  (MN-major)
 //   wgrad_S  dW_S[|S|,in]  = dY[:,S]^T . X   A=dY (MN-major)  B=X  (MN-major)
 // The slice-aware wgrad never forms a dense dW: its tile space is |S| x in only, the A
-// operand's TMA coordinates start at row_begin (any value, no alignment needed), and
-// rows >= |S| are masked in the epilogue.  When |S| x in has too few tiles to fill 148
+// operand's TMA coordinates start at row_begin (rounded down to the 16-byte TMA coordinate
+// granule; the < 8 extra leading rows are dropped), and rows outside |S| are masked in
+// the epilogue.  When |S| x in has too few tiles to fill 148
 // SMs the token (K) axis is split and partial sums are reduced with red.global.add.v4.f32.
 //
 // Roles (192 threads): warp0 = TMA producer, warp1 = tcgen05.mma issuer (one lane) and
@@ -33,7 +34,8 @@ enum Epi : int { kEpiBf16 = 0, kEpiBf16Add = 1, kEpiF32 = 2, kEpiF32Add = 3, kEp
 
 struct Args {
   int M, N, K;
-  int m_off;      // A coordinate offset along M (the slice's row_begin for wgrad)
+  int m_off;      // A coordinate offset along M (row_begin rounded down to 8 elements)
+  int row_skip;   // row_begin - m_off: leading tile rows that belong to the previous slice
   int tiles_m, tiles_n, splits, kb_per_split, total_kb, num_units;
   void* C;
   long long ldc;
@@ -184,8 +186,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode_unit(args, u, tm, tn, sp);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row = tm * BM + quarter * 32 + lane;
-      const bool row_ok = row < args.M;
+      const int row = tm * BM + quarter * 32 + lane - args.row_skip;
+      const bool row_ok = row >= 0 && row < args.M;
       const long long rbase = static_cast<long long>(row) * args.ldc;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
@@ -318,20 +320,26 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream_t s
   check_launch("gemm_bf16_kernel");
 }
 
-// Choose the number of K splits so that (tiles x splits) fills the SMs well.
-int choose_splits(int tiles, int total_kb, bool allow) {
+// Choose the number of K splits for a small tile space.  Cost model (per CTA wave):
+// one 128xBN x 64 k-block costs ~0.45 us per CTA at BN=256 (measured: 1.27 PFLOP/s over
+// 148 SMs in the dense forward), and split partials cost a zero-fill plus s fp32
+// red-adds of the output through L2 (~2 TB/s measured for red.global.add.v4.f32).
+int choose_splits(int tiles, int total_kb, long long out_elems, int BN, bool allow) {
   if (!allow) return 1;
   const int sms = num_sms();
   if (tiles >= sms) return 1;
+  const double us_per_kb = 0.45 * BN / 256.0;
+  double best_t = 1e30;
   int best = 1;
-  double best_eff = 0.0;
   for (int s = 1; s <= 16; ++s) {
-    if (total_kb / s < 4) break;  // keep >= 256 tokens per split
+    const int kbps = (total_kb + s - 1) / s;
+    if (s > 1 && kbps < 4) break;
     const int units = tiles * s;
     const int waves = (units + sms - 1) / sms;
-    const double eff = static_cast<double>(units) / (waves * sms);
-    if (eff > best_eff + 0.05) {
-      best_eff = eff;
+    double t = waves * kbps * us_per_kb;
+    if (s > 1) t += (s + 1) * out_elems * 4.0 / 2.0e6;
+    if (t < best_t * 0.97) {
+      best_t = t;
       best = s;
     }
   }
@@ -339,11 +347,11 @@ int choose_splits(int tiles, int total_kb, bool allow) {
 }
 
 void fill_units(Args& a, int BN, bool allow_split) {
-  a.tiles_m = (a.M + BM - 1) / BM;
+  a.tiles_m = (a.M + a.row_skip + BM - 1) / BM;
   a.tiles_n = (a.N + BN - 1) / BN;
   a.total_kb = (a.K + BK - 1) / BK;
   const int tiles = a.tiles_m * a.tiles_n;
-  int s = choose_splits(tiles, a.total_kb, allow_split);
+  int s = choose_splits(tiles, a.total_kb, static_cast<long long>(a.M) * a.N, BN, allow_split);
   a.kb_per_split = (a.total_kb + s - 1) / s;
   a.splits = (a.total_kb + a.kb_per_split - 1) / a.kb_per_split;
   a.num_units = tiles * a.splits;
@@ -412,7 +420,10 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   a.M = static_cast<int>(re - rb);
   a.N = static_cast<int>(in_dim);
   a.K = static_cast<int>(n_tok);
-  a.m_off = static_cast<int>(rb);
+  // TMA requires the innermost box coordinate to be a 16-byte multiple: start the tile
+  // space at rb rounded down to 8 rows and drop the (< 8) leading rows in the epilogue.
+  a.m_off = static_cast<int>(rb & ~int64_t{7});
+  a.row_skip = static_cast<int>(rb - a.m_off);
   a.C = dw;
   a.ldc = in_dim;
   const CUtensorMap ta = cached_map(dy, out_dim, n_tok, out_dim, 64, 64);
