@@ -255,6 +255,86 @@ int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t
 int cft_convert(cft_dtype src_dtype, const void* src, cft_dtype dst_dtype, void* dst, int64_t n,
                 cft_stream_t stream);
 
+/* ===================================================================== */
+/* 4. The chunk-local training step: run_training (trainer.hpp:49-50,     */
+/*    src/trainer.cpp:12-101) for the reference's model vocabulary.       */
+/* ===================================================================== */
+
+/* Layer (model.hpp:18-41): type 0 Linear(in=a, out=b, bias), 1 Embedding(vocab=a, dim=b,
+ * seq=c; first layer only), 2 LayerNorm(dim=a, eps), 3 Tanh.  Tensors are registered in the
+ * reference's order and names (model.cpp:57-92). */
+typedef struct {
+  int32_t type;
+  int32_t a;
+  int32_t b;
+  int32_t c;
+  int32_t bias;
+  int32_t pad_;
+  double eps;
+} cft_layer_spec;
+
+/* TrainOptions (trainer.hpp:16-24) + plan/residency choices. */
+typedef struct {
+  int32_t dtype;         /* compute dtype: CFT_BF16 (tcgen05), CFT_F32, CFT_F64 (bit-exact) */
+  int32_t loss;          /* LossKind: 0 sum, 1 squared, 2 half_sq, 3 softmax_ce */
+  int32_t optim;         /* OptimKind: 0 adamw, 1 plain */
+  int32_t micro_batches;
+  int32_t batch_rows;    /* samples per micro-batch */
+  int32_t plan_mode;     /* 0 partition(K), 1 partition_by_budget, 2 partition_per_tensor */
+  int32_t K;
+  int32_t T;
+  int64_t total_steps;
+  int32_t prefetch;
+  int32_t offload;       /* 1: states in pinned host memory, 3 HBM slots; 0: all in HBM */
+  int64_t bandwidth_bytes_per_step;
+  int64_t budget_bytes;
+  cft_adamw_hyper hyper;
+  int32_t full_backward; /* 1: form dX for every layer like the reference; 0: suffix only */
+  int32_t check_every_step; /* 1: synchronise each step and raise the reference's errors */
+  double grad_scale;     /* extra factor on the mean gradient (1/world for data parallel) */
+} cft_engine_config;
+
+/* One micro-batch (model.hpp:52-60).  x / target in the compute dtype; host pointers should
+ * be pinned for asynchronous upload. */
+typedef struct {
+  const void* x;
+  const int32_t* tokens;
+  const void* target;
+  const int32_t* labels;
+  int32_t on_device;
+  int32_t pad_;
+} cft_batch;
+
+typedef struct cft_engine cft_engine;
+
+/* init_params: every tensor, registration order, row-major, fp64 (Model::snapshot_params). */
+int cft_engine_create(const cft_layer_spec* layers, int n_layers, const cft_engine_config* cfg,
+                      const double* init_params, cft_stream_t stream, cft_engine** out);
+void cft_engine_destroy(cft_engine* e);
+/* One full step = step_begin, forward_backward per micro-batch, step_end. */
+int cft_engine_step(cft_engine* e, const cft_batch* batches);
+int cft_engine_step_begin(cft_engine* e, int32_t* active_chunk);
+int cft_engine_forward_backward(cft_engine* e, const cft_batch* batch, int micro_batch);
+/* The active chunk's gradient (sum over micro-batches, plan order) for a data-parallel
+ * all-reduce between forward_backward and step_end. */
+int cft_engine_grad_buffer(cft_engine* e, void** ptr, int64_t* n, int32_t* dtype);
+int cft_engine_step_end(cft_engine* e);
+int cft_engine_finish(cft_engine* e);
+int cft_engine_set_grad_scale(cft_engine* e, double grad_scale);
+/* TrainTrajectoryEntry (trainer.hpp:26-33): step, chunk, loss (pre-update mean), grad_norm_sq. */
+int64_t cft_engine_trajectory(cft_engine* e, int64_t* step, int32_t* chunk, double* loss,
+                              double* gsq, int64_t cap);
+int64_t cft_engine_num_params(const cft_engine* e);
+/* from_masters 1: the authoritative fp32/fp64 masters; 0: the compute-dtype copy in HBM. */
+int cft_engine_params(cft_engine* e, double* out, int from_masters);
+int64_t cft_engine_device_bytes(const cft_engine* e);
+uint64_t cft_engine_plan_hash(const cft_engine* e);
+int cft_engine_plan_json(cft_engine* e, char* buf, int64_t cap, int64_t* needed);
+int64_t cft_engine_transfer_events(cft_engine* e, cft_transfer_event* out, int64_t cap);
+int cft_engine_chunk_counters(cft_engine* e, uint64_t* n_out);
+/* CUDA-event times of the last step: inputs, forward, backward, stats+update (ms). */
+int cft_engine_phase_ms(cft_engine* e, float* ms4);
+
 #ifdef __cplusplus
 }
 #endif

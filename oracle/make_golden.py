@@ -110,6 +110,80 @@ def adamw():
     return out
 
 
+def _batches(layers, loss, n, rows, rng, classes=None):
+    first = layers[0]
+    out_dim = None
+    for L in layers:
+        if L[0] == "linear":
+            out_dim = L[2]
+        elif L[0] == "embedding":
+            out_dim = L[2] * L[3]
+    bs = []
+    for _ in range(n):
+        b = {}
+        if first[0] == "embedding":
+            b["tokens"] = rng.integers(0, first[1], (rows, first[3])).astype(np.int32)
+        else:
+            b["x"] = rng.normal(size=(rows, first[1] if first[0] != "layernorm" else first[1]))
+        if loss in ("squared", "half_sq"):
+            b["target"] = np.tanh(rng.normal(size=(rows, out_dim)))
+        if loss == "softmax_ce":
+            b["labels"] = rng.integers(0, classes or out_dim, rows).astype(np.int32)
+        bs.append(b)
+    return bs
+
+
+TRAIN_CASES = [
+    # preset quadratic-k2 (src/runner.cpp:40-58): one 8x8 linear on the identity batch, plain
+    # block descent eta=0.5, formula init, K=2, T=1, 8 steps
+    dict(name="quadratic_k2", layers=[("linear", 8, 8, False)], loss="half_sq", formula=True,
+         identity=8, K=2, T=1, steps=8, optim="plain", hyper=(0.5, 0.9, 0.999, 1e-8, 0.0)),
+    # preset dense-reduction (runner.cpp:87-105): K=T=1 AdamW == dense AdamW
+    dict(name="dense_reduction", layers=[("linear", 8, 16, True), ("tanh",), ("linear", 16, 1, True)],
+         loss="half_sq", rows=16, nb=8, K=1, T=1, steps=32),
+    # preset mlp-imbalanced-layers (runner.cpp:60-85): embedding table sliced across chunks
+    dict(name="mlp_imbalanced", layers=[("embedding", 512, 16, 4), ("linear", 64, 4, True)],
+         loss="softmax_ce", rows=8, nb=8, K=4, T=1, steps=16),
+    # everything at once: embedding + layernorm + tanh, micro-batches, prefetch, weight decay
+    dict(name="emb_ln_mb", layers=[("embedding", 50, 8, 3), ("layernorm", 24), ("linear", 24, 16, True),
+                                   ("tanh",), ("linear", 16, 5, True)],
+         loss="softmax_ce", rows=6, nb=5, K=5, T=2, steps=12, micro_batches=2, prefetch=True, bw=500,
+         hyper=(2e-3, 0.9, 0.999, 1e-8, 0.01)),
+    # pure linear + half_sq: the fp64 GPU path is bit-identical here
+    dict(name="linear_exact", layers=[("linear", 32, 24, True), ("linear", 24, 8, False)],
+         loss="half_sq", rows=12, nb=3, K=3, T=1, steps=9),
+    # byte-budget plan with a layernorm in the middle
+    dict(name="budget_ln", layers=[("linear", 16, 16, True), ("layernorm", 16), ("linear", 16, 4, False)],
+         loss="squared", rows=10, nb=4, budget=2000, T=3, steps=12),
+]
+
+
+def train_runs():
+    rng = np.random.default_rng(2026)
+    out = []
+    for c in TRAIN_CASES:
+        params = ref.init_params(c["layers"], seed=7, formula=c.get("formula", False))
+        if "identity" in c:
+            d = c["identity"]
+            batches = [dict(x=np.eye(d), target=np.zeros((d, d)))]
+        else:
+            batches = _batches(c["layers"], c["loss"], c["nb"], c["rows"], rng)
+        hyper = c.get("hyper", (1e-3, 0.9, 0.999, 1e-8, 0.0))
+        r = ref.train(c["layers"], c["loss"], params, batches, K=c.get("K"), T=c["T"], steps=c["steps"],
+                      budget=c.get("budget"), prefetch=c.get("prefetch", False), bw=c.get("bw", 0),
+                      optim=c.get("optim", "adamw"), micro_batches=c.get("micro_batches", 1), hyper=hyper)
+        out.append(dict(name=c["name"], layers=[list(L) for L in c["layers"]], loss=c["loss"],
+                        K=c.get("K"), budget=c.get("budget"), T=c["T"], steps=c["steps"],
+                        optim=c.get("optim", "adamw"), micro_batches=c.get("micro_batches", 1),
+                        prefetch=c.get("prefetch", False), bw=c.get("bw", 0), hyper=list(hyper),
+                        init_params=params.tolist(),
+                        batches=[{k: v.tolist() for k, v in b.items()} for b in batches],
+                        traj_loss=r["loss"].tolist(), traj_gsq=r["gsq"].tolist(),
+                        traj_chunk=r["chunk"].tolist(), final_params=r["params"].tolist(),
+                        plan_hash=f"{r['plan_hash']:016x}"))
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     with open(os.path.join(OUT, "plans.json"), "w") as f:
@@ -118,6 +192,8 @@ def main():
         json.dump(schedules(), f)
     with open(os.path.join(OUT, "adamw.json"), "w") as f:
         json.dump(adamw(), f)
+    with open(os.path.join(OUT, "train.json"), "w") as f:
+        json.dump(train_runs(), f)
     print("golden fixtures written to", OUT)
 
 

@@ -1,0 +1,752 @@
+// engine.cpp -- the chunk-local training step (see engine.h for the design).
+//
+// Reference control flow: run_training (src/trainer.cpp:36-94), forward/backward
+// (src/autodiff.cpp:235-313), accumulate/mean/AdamW (src/optimizer.cpp:134-198), rotation
+// (src/schedule.cpp:63-127).  Everything device-side is asynchronous on `stream_`; the only
+// host synchronisation per step is the optional end-of-step error check.
+#include "engine.h"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "cft_common.h"
+#include "kernels.h"
+
+namespace cft {
+
+namespace {
+constexpr int kLinear = 0, kEmbedding = 1, kLayerNorm = 2, kTanh = 3;
+
+template <class T>
+T* at(void* base, int64_t elems) {
+  return static_cast<T*>(base) + elems;
+}
+}  // namespace
+
+size_t Engine::esz() const { return cfg_.dtype == CFT_BF16 ? 2 : (cfg_.dtype == CFT_F32 ? 4 : 8); }
+size_t Engine::ssz() const { return cfg_.dtype == CFT_F64 ? 8 : 4; }
+
+void Engine::alloc(void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  CFT_CUDA(cudaMalloc(p, bytes));
+  allocs_.push_back(*p);
+  device_bytes_ += static_cast<int64_t>(bytes);
+}
+
+void* Engine::param_ptr(int tensor) const {
+  return static_cast<char*>(params_) + tensors_[tensor].param_off * esz();
+}
+
+Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
+               const double* init_params, cudaStream_t stream)
+    : cfg_(cfg) {
+  CFT_CHECK(cfg_.dtype == CFT_BF16 || cfg_.dtype == CFT_F32 || cfg_.dtype == CFT_F64,
+            "engine: dtype must be BF16, F32 or F64");
+  CFT_CHECK(!specs.empty(), "forward: model has no layers");
+  CFT_CHECK(cfg_.micro_batches >= 1, "trainer: micro_batches must be at least 1");
+  CFT_CHECK(cfg_.batch_rows >= 1, "engine: batch_rows must be positive");
+  const int64_t rows = cfg_.batch_rows;
+
+  // ---- model registry in the reference's registration order (model.cpp:9-17, 57-92) ----
+  int64_t width = -1;
+  for (size_t li = 0; li < specs.size(); ++li) {
+    Layer L;
+    L.spec = specs[li];
+    const std::string idx = std::to_string(li);
+    auto add = [&](const std::string& name, int64_t r, int64_t c) {
+      CFT_CHECK(r > 0 && c > 0, "tensor '" + name + "': non-positive shape");
+      Tensor t{static_cast<int>(tensors_.size()), name, r, c, param_elems_, static_cast<int>(li)};
+      param_elems_ += r * c;
+      tensors_.push_back(t);
+      return t.id;
+    };
+    switch (L.spec.type) {
+      case kEmbedding:
+        CFT_CHECK(li == 0, "forward: embedding must be the first layer");
+        L.w = add("embedding" + idx + ".table", L.spec.a, L.spec.b);
+        L.in_w = 0;
+        L.out_w = static_cast<int64_t>(L.spec.b) * std::max(1, L.spec.c);
+        break;
+      case kLinear:
+        if (width >= 0) CFT_CHECK(width == L.spec.a, "forward: linear input width mismatch");
+        L.w = add("linear" + idx + ".weight", L.spec.b, L.spec.a);
+        if (L.spec.bias) L.bias = add("linear" + idx + ".bias", L.spec.b, 1);
+        L.in_w = L.spec.a;
+        L.out_w = L.spec.b;
+        break;
+      case kLayerNorm:
+        if (width >= 0) CFT_CHECK(width == L.spec.a, "forward: layernorm width mismatch");
+        L.w = add("layernorm" + idx + ".gamma", L.spec.a, 1);
+        L.bias = add("layernorm" + idx + ".beta", L.spec.a, 1);
+        L.in_w = L.out_w = L.spec.a;
+        break;
+      case kTanh:
+        CFT_CHECK(width >= 0, "engine: tanh cannot be the first layer");
+        L.in_w = L.out_w = width;
+        break;
+      default:
+        throw Error("engine: unknown layer type");
+    }
+    width = L.out_w;
+    max_width_ = std::max({max_width_, L.in_w, L.out_w});
+    layers_.push_back(L);
+  }
+
+  // ---- plan + scheduler (partition.cpp:125-198, schedule.cpp:17-26) ----
+  std::vector<host::TensorInfo> infos;
+  for (const auto& t : tensors_) {
+    host::TensorInfo i;
+    i.id = t.id;
+    i.name = t.name;
+    i.rows = t.rows;
+    i.cols = t.cols;
+    i.reg_order = t.id;
+    infos.push_back(i);
+  }
+  if (cfg_.plan_mode == 1) plan_ = host::partition_by_budget(infos, cfg_.budget_bytes);
+  else if (cfg_.plan_mode == 2) plan_ = host::partition_per_tensor(infos);
+  else plan_ = host::partition(infos, cfg_.K);
+  cfg_.K = plan_.K();
+  host::ScheduleConfig sc;
+  sc.K = cfg_.K;
+  sc.T = cfg_.T;
+  sc.total_steps = cfg_.total_steps;
+  sc.prefetch = cfg_.prefetch != 0;
+  sc.bandwidth_bytes_per_step = cfg_.bandwidth_bytes_per_step;
+  std::vector<int64_t> elems;
+  for (const auto& ch : plan_.chunks) elems.push_back(ch.elements);
+  sched_ = std::make_unique<host::RotationScheduler>(sc, elems, plan_.policy);
+
+  // ---- streams ----
+  if (stream) {
+    stream_ = stream;
+  } else {
+    CFT_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    own_stream_ = true;
+  }
+  CFT_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+  CFT_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  CFT_CUDA(cudaEventCreateWithFlags(&step_done_, cudaEventDisableTiming));
+  for (auto& e : ev_) CFT_CUDA(cudaEventCreate(&e));
+
+  // ---- per-chunk slice tables (plan order = state/aux layout) ----
+  chunk_slices_.resize(cfg_.K);
+  lowest_layer_.assign(cfg_.K, static_cast<int>(layers_.size()));
+  n_local_.assign(cfg_.K, 0);
+  for (int c = 0; c < cfg_.K; ++c) {
+    int64_t off = 0;
+    for (const auto& s : plan_.chunks[c].slices) {
+      const Tensor& t = tensors_[s.tensor_id];
+      SliceRt r{s.tensor_id, t.layer, s.row_begin, s.row_end, off,
+                t.param_off + s.row_begin * t.cols, (s.row_end - s.row_begin) * t.cols};
+      chunk_slices_[c].push_back(r);
+      off += r.count;
+      max_slice_ = std::max(max_slice_, r.count);
+      lowest_layer_[c] = std::min(lowest_layer_[c], t.layer);
+    }
+    max_chunk_ = std::max(max_chunk_, off);
+  }
+
+  // ---- device memory (all allocated once; nothing is allocated per step) ----
+  const size_t E = esz(), S = ssz();
+  alloc(&params_, param_elems_ * E);
+  for (size_t li = 0; li < layers_.size(); ++li) {
+    Layer& L = layers_[li];
+    alloc(&L.x_saved, rows * L.out_w * E);  // this layer's output (= next layer's input)
+    if (L.spec.type == kLayerNorm) {
+      alloc(&L.mean, rows * S);
+      alloc(&L.rstd, rows * S);
+    }
+  }
+  y_out_ = layers_.back().x_saved;
+  alloc(&act_[0], rows * max_width_ * E);
+  alloc(&act_[1], rows * max_width_ * E);
+  alloc(&aux_, max_chunk_ * S);
+  if (cfg_.dtype == CFT_F64)
+    alloc(&scratch_, std::max<int64_t>(max_slice_, rows * std::max<int64_t>(max_width_, 1)) * 8);
+  const Layer& first = layers_.front();
+  if (first.spec.type == kEmbedding) {
+    void* p;
+    alloc(&p, rows * std::max(1, first.spec.c) * sizeof(int32_t));
+    in_tokens_ = static_cast<int32_t*>(p);
+  } else {
+    alloc(&in_x_, rows * first.in_w * E);
+  }
+  alloc(&in_target_, rows * layers_.back().out_w * E);
+  {
+    void* p;
+    alloc(&p, rows * sizeof(int32_t));
+    in_labels_ = static_cast<int32_t*>(p);
+    alloc(&p, static_cast<size_t>(std::max<int64_t>(cfg_.total_steps, 1)) * 4 * sizeof(double));
+    stats_ = static_cast<double*>(p);
+    alloc(&precond_, 2 * S);
+    alloc(&consts_, 64);
+    unsigned char tmpl[64] = {};
+    const int64_t big = std::numeric_limits<int64_t>::max();
+    std::memcpy(tmpl + 16, &big, 8);
+    if (S == 4) {
+      const float inf = std::numeric_limits<float>::infinity();
+      std::memcpy(tmpl + 32, &inf, 4);
+    } else {
+      const double inf = std::numeric_limits<double>::infinity();
+      std::memcpy(tmpl + 32, &inf, 8);
+    }
+    CFT_CUDA(cudaMemcpy(consts_, tmpl, 64, cudaMemcpyHostToDevice));
+    alloc(&p, 2 * sizeof(unsigned long long));
+    flags_ = static_cast<unsigned long long*>(p);
+    CFT_CUDA(cudaMemsetAsync(flags_, 0, 2 * sizeof(unsigned long long), stream_));
+  }
+  for (int c = 0; c < cfg_.K; ++c) {
+    std::vector<cft_segment> segs;
+    for (const auto& s : chunk_slices_[c]) segs.push_back({s.aux_off, s.param_off, s.count});
+    void* p;
+    alloc(&p, segs.size() * sizeof(cft_segment));
+    CFT_CUDA(cudaMemcpy(p, segs.data(), segs.size() * sizeof(cft_segment), cudaMemcpyHostToDevice));
+    chunk_segs_.push_back(static_cast<cft_segment*>(p));
+  }
+  CFT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_stats_),
+                         std::max<int64_t>(cfg_.total_steps, 1) * 4 * sizeof(double),
+                         cudaHostAllocDefault));
+  CFT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_flags_), 2 * sizeof(unsigned long long),
+                         cudaHostAllocDefault));
+
+  // ---- parameters: fp64 init -> compute dtype, in pieces ----
+  {
+    const int64_t piece = 1 << 24;
+    void* tmp;
+    CFT_CUDA(cudaMalloc(&tmp, std::min(piece, param_elems_) * 8));
+    for (int64_t o = 0; o < param_elems_; o += piece) {
+      const int64_t n = std::min(piece, param_elems_ - o);
+      CFT_CUDA(cudaMemcpy(tmp, init_params + o, n * 8, cudaMemcpyHostToDevice));
+      if (cfg_.dtype == CFT_F64)
+        CFT_CUDA(cudaMemcpy(at<double>(params_, o), tmp, n * 8, cudaMemcpyDeviceToDevice));
+      else if (cft_convert(CFT_F64, tmp, static_cast<cft_dtype>(cfg_.dtype),
+                           static_cast<char*>(params_) + o * E, n, stream_) != CFT_OK)
+        throw Error(last_error());
+      CFT_CUDA(cudaStreamSynchronize(stream_));
+    }
+    cudaFree(tmp);
+  }
+
+  // ---- optimizer state: masters from the init params, m = v = 0 (optimizer.cpp:77-92) ----
+  const int n_slots = cfg_.offload ? 3 : 0;
+  for (int i = 0; i < n_slots; ++i) {
+    for (auto& st : slots_[i].st) alloc(&st, max_chunk_ * S);
+    CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].ready, cudaEventDisableTiming));
+    CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].free, cudaEventDisableTiming));
+  }
+  host_states_.assign(cfg_.K, nullptr);
+  for (int c = 0; c < cfg_.K; ++c) {
+    const int64_t n = plan_.chunks[c].elements;
+    std::vector<double> master(n);
+    for (const auto& s : chunk_slices_[c])
+      std::memcpy(master.data() + s.aux_off, init_params + s.param_off, s.count * 8);
+    void* buf;
+    if (cfg_.offload) {
+      CFT_CUDA(cudaHostAlloc(&buf, n * 3 * S, cudaHostAllocDefault));
+    } else {
+      alloc(&buf, n * 3 * S);
+    }
+    host_states_[c] = buf;
+    std::vector<char> staged(n * 3 * S, 0);
+    if (S == 8) {
+      std::memcpy(staged.data(), master.data(), n * 8);
+    } else {
+      float* f = reinterpret_cast<float*>(staged.data());
+      for (int64_t i = 0; i < n; ++i) f[i] = static_cast<float>(master[i]);
+    }
+    CFT_CUDA(cudaMemcpy(buf, staged.data(), n * 3 * S,
+                        cfg_.offload ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice));
+  }
+  CFT_CUDA(cudaDeviceSynchronize());
+}
+
+Engine::~Engine() {
+  cudaDeviceSynchronize();
+  for (void* p : allocs_) cudaFree(p);
+  if (cfg_.offload)
+    for (void* p : host_states_)
+      if (p) cudaFreeHost(p);
+  if (host_stats_) cudaFreeHost(host_stats_);
+  if (host_flags_) cudaFreeHost(host_flags_);
+  for (auto& s : slots_) {
+    if (s.ready) cudaEventDestroy(s.ready);
+    if (s.free) cudaEventDestroy(s.free);
+  }
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
+  if (step_done_) cudaEventDestroy(step_done_);
+  if (h2d_) cudaStreamDestroy(h2d_);
+  if (d2h_) cudaStreamDestroy(d2h_);
+  if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+// ---------------------------------------------------------------------------------------
+// Working-set rotation: pinned host <-> three HBM slots.
+
+int Engine::slot_of(int chunk) const {
+  for (int i = 0; i < 3; ++i)
+    if (slots_[i].chunk == chunk) return i;
+  return -1;
+}
+
+int Engine::take_free_slot(int avoid1, int avoid2) {
+  for (int i = 0; i < 3; ++i)
+    if (slots_[i].chunk < 0) return i;  // empty, or retiring (the H2D waits on its D2H)
+  for (int i = 0; i < 3; ++i)
+    if (slots_[i].chunk != avoid1 && slots_[i].chunk != avoid2) return i;
+  throw Error("engine: no free state slot");
+}
+
+void Engine::load_chunk(int chunk, bool for_prefetch) {
+  if (!cfg_.offload) return;
+  int s = slot_of(chunk);
+  if (s < 0) {
+    int pending = -1;
+    for (int i = 0; i < 3; ++i)
+      if (slots_[i].chunk >= 0 && slots_[i].chunk != active_) pending = slots_[i].chunk;
+    s = take_free_slot(active_, pending);
+    Slot& sl = slots_[s];
+    const int64_t n = plan_.chunks[chunk].elements;
+    const size_t S = ssz();
+    // wait for the slot's previous D2H (it may still be draining) and the host copy of this
+    // chunk (a retire of the same chunk may be in flight)
+    CFT_CUDA(cudaStreamWaitEvent(h2d_, sl.free, 0));
+    const char* src = static_cast<const char*>(host_states_[chunk]);
+    for (int k = 0; k < 3; ++k)
+      CFT_CUDA(cudaMemcpyAsync(sl.st[k], src + k * n * S, n * S, cudaMemcpyHostToDevice, h2d_));
+    CFT_CUDA(cudaEventRecord(sl.ready, h2d_));
+    sl.chunk = chunk;
+  }
+  if (!for_prefetch) CFT_CUDA(cudaStreamWaitEvent(stream_, slots_[s].ready, 0));
+}
+
+void Engine::offload_chunk(int chunk) {
+  if (!cfg_.offload) return;
+  const int s = slot_of(chunk);
+  CFT_CHECK(s >= 0, "offload: chunk not resident");
+  Slot& sl = slots_[s];
+  const int64_t n = plan_.chunks[chunk].elements;
+  const size_t S = ssz();
+  CFT_CUDA(cudaStreamWaitEvent(d2h_, step_done_, 0));
+  char* dst = static_cast<char*>(host_states_[chunk]);
+  for (int k = 0; k < 3; ++k)
+    CFT_CUDA(cudaMemcpyAsync(dst + k * n * S, sl.st[k], n * S, cudaMemcpyDeviceToHost, d2h_));
+  CFT_CUDA(cudaEventRecord(sl.free, d2h_));
+  // a later H2D of this chunk must see the completed host copy: order h2d after d2h
+  CFT_CUDA(cudaStreamWaitEvent(h2d_, sl.free, 0));
+  sl.chunk = -1;
+}
+
+// ---------------------------------------------------------------------------------------
+// The step
+
+int Engine::step_begin() {
+  CFT_CHECK(!finished_, "engine: finished");
+  CFT_CHECK(t_ < cfg_.total_steps, "scheduler: step_begin past total_steps");
+  const host::BeginActions a = sched_->step_begin();
+  active_ = a.active;
+  if (a.load >= 0) load_chunk(a.load, false);
+  else load_chunk(active_, false);  // already resident: still order compute after its H2D
+  if (a.prefetch >= 0) load_chunk(a.prefetch, true);
+  // per-step statistics row {sumsq, nonfinite, first_bad = INT64_MAX, loss} and the
+  // precond {min = +inf, max = 0} cells, reset from a device-resident template
+  CFT_CUDA(cudaMemcpyAsync(stats_ + t_ * 4, consts_, 4 * sizeof(double), cudaMemcpyDeviceToDevice,
+                           stream_));
+  CFT_CUDA(cudaMemcpyAsync(precond_, static_cast<char*>(consts_) + 32, 2 * ssz(),
+                           cudaMemcpyDeviceToDevice, stream_));
+  mb_done_ = 0;
+  CFT_CUDA(cudaEventRecord(ev_[0], stream_));
+  return active_;
+}
+
+void Engine::forward_backward(const Batch& b, int mb) {
+  CFT_CHECK(active_ >= 0, "scheduler: step_end before step_begin");
+  const int64_t rows = cfg_.batch_rows;
+  const size_t E = esz();
+  cudaStream_t s = stream_;
+  const int dt = cfg_.dtype;
+  const Layer& first = layers_.front();
+  const Layer& last = layers_.back();
+  const cudaMemcpyKind kind = b.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+
+  // ---- inputs ----
+  const void* x_in = nullptr;
+  const int32_t* tok = nullptr;
+  if (first.spec.type == kEmbedding) {
+    CFT_CHECK(b.tokens != nullptr, "forward: token batch required");
+    const int64_t ntok = rows * std::max(1, first.spec.c);
+    CFT_CUDA(cudaMemcpyAsync(in_tokens_, b.tokens, ntok * 4, kind, s));
+    tok = in_tokens_;
+    layers::count_in_range(tok, ntok, 0, first.spec.a, reinterpret_cast<long long*>(flags_ + 1), s);
+  } else {
+    CFT_CHECK(b.x != nullptr, "forward: dense input required");
+    CFT_CUDA(cudaMemcpyAsync(in_x_, b.x, rows * first.in_w * E, kind, s));
+    x_in = in_x_;
+  }
+  const void* target = nullptr;
+  if (cfg_.loss == 1 || cfg_.loss == 2) {
+    CFT_CHECK(b.target != nullptr, "loss: target shape mismatch");
+    CFT_CUDA(cudaMemcpyAsync(in_target_, b.target, rows * last.out_w * E, kind, s));
+    target = in_target_;
+  }
+  if (cfg_.loss == 3) {
+    CFT_CHECK(b.labels != nullptr, "loss: label count mismatch");
+    CFT_CUDA(cudaMemcpyAsync(in_labels_, b.labels, rows * 4, kind, s));
+  }
+  if (mb == 0) CFT_CUDA(cudaEventRecord(ev_[1], s));
+
+  // ---- forward (autodiff.cpp:235-305) ----
+  for (size_t li = 0; li < layers_.size(); ++li) {
+    Layer& L = layers_[li];
+    const void* in = li == 0 ? x_in : layers_[li - 1].x_saved;
+    void* out = L.x_saved;
+    switch (L.spec.type) {
+      case kEmbedding:
+        if (cft_embedding_gather(static_cast<cft_dtype>(dt), param_ptr(L.w), L.spec.b, tok,
+                                 rows * std::max(1, L.spec.c), out, s) != CFT_OK)
+          throw Error(last_error());
+        break;
+      case kLinear:
+        if (cft_linear_fwd(static_cast<cft_dtype>(dt), in, rows, L.in_w, param_ptr(L.w), L.out_w,
+                           L.bias >= 0 ? param_ptr(L.bias) : nullptr, out, s) != CFT_OK)
+          throw Error(last_error());
+        break;
+      case kLayerNorm:
+        if (dt == CFT_F64)
+          f64::layernorm_forward(static_cast<const double*>(in), (int)rows, (int)L.in_w,
+                                 static_cast<const double*>(param_ptr(L.w)),
+                                 static_cast<const double*>(param_ptr(L.bias)), L.spec.eps,
+                                 static_cast<double*>(out), static_cast<double*>(L.mean),
+                                 static_cast<double*>(L.rstd), s);
+        else if (dt == CFT_F32)
+          layers::layernorm_fwd<float>(static_cast<const float*>(in), rows, L.in_w,
+                                       static_cast<const float*>(param_ptr(L.w)),
+                                       static_cast<const float*>(param_ptr(L.bias)),
+                                       (float)L.spec.eps, static_cast<float*>(out),
+                                       static_cast<float*>(L.mean), static_cast<float*>(L.rstd), s);
+        else
+          layers::layernorm_fwd<__nv_bfloat16>(
+              static_cast<const __nv_bfloat16*>(in), rows, L.in_w,
+              static_cast<const __nv_bfloat16*>(param_ptr(L.w)),
+              static_cast<const __nv_bfloat16*>(param_ptr(L.bias)), (float)L.spec.eps,
+              static_cast<__nv_bfloat16*>(out), static_cast<float*>(L.mean),
+              static_cast<float*>(L.rstd), s);
+        break;
+      case kTanh:
+        if (dt == CFT_F64) f64::tanh_forward(static_cast<const double*>(in), rows * L.in_w, static_cast<double*>(out), s);
+        else if (dt == CFT_F32) layers::tanh_fwd<float>(static_cast<const float*>(in), rows * L.in_w, static_cast<float*>(out), s);
+        else layers::tanh_fwd<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(in), rows * L.in_w, static_cast<__nv_bfloat16*>(out), s);
+        break;
+    }
+  }
+  if (mb == 0) CFT_CUDA(cudaEventRecord(ev_[2], s));
+
+  // ---- loss (autodiff.cpp:180-228) ----
+  double* loss_acc = stats_ + t_ * 4 + 3;
+  void* dy = act_[0];
+  if (dt == CFT_F64)
+    layers::loss_f64(cfg_.loss, static_cast<const double*>(y_out_), static_cast<const double*>(target),
+                     in_labels_, rows, last.out_w, static_cast<double*>(dy), loss_acc,
+                     static_cast<double*>(scratch_), flags_, s);
+  else if (dt == CFT_F32)
+    layers::loss<float>(cfg_.loss, static_cast<const float*>(y_out_), static_cast<const float*>(target),
+                        in_labels_, rows, last.out_w, static_cast<float*>(dy), loss_acc, flags_, s);
+  else
+    layers::loss<__nv_bfloat16>(cfg_.loss, static_cast<const __nv_bfloat16*>(y_out_),
+                                static_cast<const __nv_bfloat16*>(target), in_labels_, rows,
+                                last.out_w, static_cast<__nv_bfloat16*>(dy), loss_acc, flags_, s);
+
+  // ---- chunk-masked backward (autodiff.cpp:307-313), suffix only ----
+  const int stop = cfg_.full_backward ? 0 : lowest_layer_[active_];
+  const auto& slices = chunk_slices_[active_];
+  const int accumulate = mb > 0 ? 1 : 0;
+  int cur = 0;
+  for (int li = static_cast<int>(layers_.size()) - 1; li >= stop; --li) {
+    Layer& L = layers_[li];
+    const void* in = li == 0 ? x_in : layers_[li - 1].x_saved;
+    const void* g = act_[cur];
+    void* gx = act_[cur ^ 1];
+    // dX feeds the layer below; with full_backward it is also formed for layer 0, exactly
+    // like LinearNode::backward (autodiff.cpp:84-106) which always computes dx.
+    const bool need_dx = L.spec.type != kEmbedding && (li > stop || cfg_.full_backward);
+    // parameter-gradient slices owned by this layer
+    for (const auto& sl : slices) {
+      if (sl.layer != li) continue;
+      void* dst = static_cast<char*>(aux_) + sl.aux_off * ssz();
+      void* tgt = dst;
+      int acc_flag = accumulate;
+      if (dt == CFT_F64) {  // reference order: fresh zero buffer, then accum += bag
+        if (mb > 0) tgt = scratch_;
+        CFT_CUDA(cudaMemsetAsync(tgt, 0, sl.count * 8, s));
+        acc_flag = 1;
+      } else if (L.spec.type == kEmbedding && mb == 0) {
+        CFT_CUDA(cudaMemsetAsync(tgt, 0, sl.count * 4, s));
+      }
+      const bool is_w = sl.tensor == L.w;
+      switch (L.spec.type) {
+        case kLinear:
+          if (is_w) {
+            if (cft_linear_wgrad_slice(static_cast<cft_dtype>(dt), g, rows, L.out_w, in, L.in_w, sl.rb,
+                                       sl.re, tgt, acc_flag, s) != CFT_OK)
+              throw Error(last_error());
+          } else {
+            if (cft_linear_dbias_slice(static_cast<cft_dtype>(dt), g, rows, L.out_w, sl.rb, sl.re, tgt,
+                                       acc_flag, s) != CFT_OK)
+              throw Error(last_error());
+          }
+          break;
+        case kEmbedding:
+          if (cft_embedding_scatter_slice(static_cast<cft_dtype>(dt), g, L.spec.b, tok,
+                                          rows * std::max(1, L.spec.c), sl.rb, sl.re, tgt, nullptr,
+                                          s) != CFT_OK)
+            throw Error(last_error());
+          break;
+        case kLayerNorm:
+          if (is_w) {
+            if (dt == CFT_F64)
+              f64::layernorm_dgamma(static_cast<const double*>(g), static_cast<const double*>(in),
+                                    static_cast<const double*>(L.mean), static_cast<const double*>(L.rstd),
+                                    (int)rows, (int)L.in_w, sl.rb, sl.re, static_cast<double*>(tgt), s);
+            else if (dt == CFT_F32)
+              layers::layernorm_dgamma<float>(static_cast<const float*>(g), static_cast<const float*>(in),
+                                              static_cast<const float*>(L.mean), static_cast<const float*>(L.rstd),
+                                              rows, L.in_w, sl.rb, sl.re, static_cast<float*>(tgt), acc_flag, s);
+            else
+              layers::layernorm_dgamma<__nv_bfloat16>(
+                  static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(in),
+                  static_cast<const float*>(L.mean), static_cast<const float*>(L.rstd), rows, L.in_w,
+                  sl.rb, sl.re, static_cast<float*>(tgt), acc_flag, s);
+          } else {
+            if (cft_linear_dbias_slice(static_cast<cft_dtype>(dt), g, rows, L.in_w, sl.rb, sl.re, tgt,
+                                       acc_flag, s) != CFT_OK)
+              throw Error(last_error());
+          }
+          break;
+      }
+      if (dt == CFT_F64 && mb > 0) layers::add_f64(static_cast<double*>(dst), static_cast<double*>(tgt), sl.count, s);
+    }
+    if (!need_dx) continue;
+    switch (L.spec.type) {
+      case kLinear:
+        if (cft_linear_dgrad(static_cast<cft_dtype>(dt), g, rows, L.out_w, param_ptr(L.w), L.in_w, gx, 0,
+                             s) != CFT_OK)
+          throw Error(last_error());
+        break;
+      case kLayerNorm:
+        if (dt == CFT_F64) {
+          CFT_CUDA(cudaMemsetAsync(gx, 0, rows * L.in_w * 8, s));
+          f64::layernorm_dinput(static_cast<const double*>(g), static_cast<const double*>(in),
+                                static_cast<const double*>(L.mean), static_cast<const double*>(L.rstd),
+                                static_cast<const double*>(param_ptr(L.w)), (int)rows, (int)L.in_w,
+                                static_cast<double*>(gx), s);
+        } else if (dt == CFT_F32) {
+          layers::layernorm_dinput<float>(static_cast<const float*>(g), static_cast<const float*>(in),
+                                          static_cast<const float*>(L.mean), static_cast<const float*>(L.rstd),
+                                          static_cast<const float*>(param_ptr(L.w)), rows, L.in_w,
+                                          static_cast<float*>(gx), 0, s);
+        } else {
+          layers::layernorm_dinput<__nv_bfloat16>(
+              static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(in),
+              static_cast<const float*>(L.mean), static_cast<const float*>(L.rstd),
+              static_cast<const __nv_bfloat16*>(param_ptr(L.w)), rows, L.in_w,
+              static_cast<__nv_bfloat16*>(gx), 0, s);
+        }
+        break;
+      case kTanh:
+        if (dt == CFT_F64) {
+          CFT_CUDA(cudaMemsetAsync(gx, 0, rows * L.in_w * 8, s));
+          f64::tanh_dinput(static_cast<const double*>(g), static_cast<const double*>(L.x_saved),
+                           rows * L.in_w, static_cast<double*>(gx), s);
+        } else if (dt == CFT_F32) {
+          layers::tanh_bwd<float>(static_cast<const float*>(g), static_cast<const float*>(L.x_saved),
+                                  rows * L.in_w, static_cast<float*>(gx), s);
+        } else {
+          layers::tanh_bwd<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(g),
+                                          static_cast<const __nv_bfloat16*>(L.x_saved), rows * L.in_w,
+                                          static_cast<__nv_bfloat16*>(gx), s);
+        }
+        break;
+    }
+    cur ^= 1;
+  }
+  (void)E;
+  ++mb_done_;
+  if (mb == 0) CFT_CUDA(cudaEventRecord(ev_[3], s));
+}
+
+void Engine::step_end() {
+  CFT_CHECK(active_ >= 0, "scheduler: step_end before step_begin");
+  CFT_CHECK(mb_done_ == cfg_.micro_batches, "engine: not every micro-batch was run");
+  cudaStream_t s = stream_;
+  const int c = active_;
+  const int64_t n = plan_.chunks[c].elements;
+  const cft_dtype sdt = cfg_.dtype == CFT_F64 ? CFT_F64 : CFT_F32;
+  const double scale = cfg_.grad_scale * (1.0 / cfg_.micro_batches);  // take_mean_grad
+  double* st = stats_ + t_ * 4;
+  CFT_CUDA(cudaEventRecord(ev_[4], s));
+  if (cft_grad_stats(sdt, aux_, n, scale, st, s) != CFT_OK) throw Error(last_error());
+  // a non-finite loss also blocks the update (trainer.cpp:48-49 throws before any step)
+  layers::flag_nonfinite_loss(st, s);
+
+  void* master;
+  void* m;
+  void* v;
+  if (cfg_.offload) {
+    const Slot& sl = slots_[slot_of(c)];
+    master = sl.st[0];
+    m = sl.st[1];
+    v = sl.st[2];
+  } else {
+    char* base = static_cast<char*>(host_states_[c]);
+    master = base;
+    m = base + n * ssz();
+    v = base + 2 * n * ssz();
+  }
+  n_local_[c] += 1;
+  const int32_t nseg = static_cast<int32_t>(chunk_slices_[c].size());
+  if (cfg_.optim == 0) {
+    const double bc1 = 1.0 - std::pow(cfg_.hyper.beta1, static_cast<double>(n_local_[c]));
+    const double bc2 = 1.0 - std::pow(cfg_.hyper.beta2, static_cast<double>(n_local_[c]));
+    if (cft_adamw_slice(sdt, master, m, v, aux_, n, scale, &cfg_.hyper, bc1, bc2,
+                        static_cast<cft_dtype>(cfg_.dtype), params_, chunk_segs_[c], nseg, st,
+                        precond_, s) != CFT_OK)
+      throw Error(last_error());
+  } else {
+    if (cft_sgd_slice(sdt, master, aux_, n, scale, cfg_.hyper.eta, static_cast<cft_dtype>(cfg_.dtype),
+                      params_, chunk_segs_[c], nseg, st, s) != CFT_OK)
+      throw Error(last_error());
+  }
+  CFT_CUDA(cudaEventRecord(ev_[5], s));
+  CFT_CUDA(cudaEventRecord(step_done_, s));
+  CFT_CUDA(cudaMemcpyAsync(host_stats_ + t_ * 4, st, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  traj_step_.push_back(t_);
+  traj_chunk_.push_back(c);
+
+  const int off = sched_->step_end();
+  if (off >= 0) offload_chunk(off);
+
+  if (cfg_.check_every_step) {
+    CFT_CUDA(cudaMemcpyAsync(host_flags_, flags_, 2 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+    CFT_CUDA(cudaStreamSynchronize(s));
+    const double* h = host_stats_ + t_ * 4;
+    const std::string ctx = "step " + std::to_string(t_) + ", chunk " + std::to_string(c) + ": ";
+    if (host_flags_[1]) throw Error(ctx + "embedding: token id out of range");
+    if (host_flags_[0]) throw Error(ctx + "loss: label out of range");
+    if (!std::isfinite(h[3])) {
+      n_local_[c] -= 1;
+      throw Error(ctx + "non-finite loss");
+    }
+    uint64_t nbad;
+    std::memcpy(&nbad, &h[1], 8);
+    if (nbad) {
+      int64_t bad;
+      std::memcpy(&bad, &h[2], 8);
+      n_local_[c] -= 1;
+      throw Error(ctx + "step: non-finite gradient at element " + std::to_string(bad) + " (chunk " +
+                  std::to_string(c) + ", local step " + std::to_string(n_local_[c] + 1) + ")");
+    }
+  }
+  ++t_;
+}
+
+void Engine::finish() {
+  if (finished_) return;
+  for (int c : sched_->finish()) offload_chunk(c);
+  CFT_CUDA(cudaStreamSynchronize(stream_));
+  CFT_CUDA(cudaStreamSynchronize(d2h_));
+  CFT_CUDA(cudaStreamSynchronize(h2d_));
+  finished_ = true;
+}
+
+void Engine::trajectory(int64_t* step, int32_t* chunk, double* loss, double* gsq, int64_t* n) const {
+  cudaStreamSynchronize(stream_);
+  const int64_t k = static_cast<int64_t>(traj_step_.size());
+  for (int64_t i = 0; i < k; ++i) {
+    const double* h = host_stats_ + traj_step_[i] * 4;
+    if (step) step[i] = traj_step_[i];
+    if (chunk) chunk[i] = traj_chunk_[i];
+    if (loss) loss[i] = h[3] / cfg_.micro_batches;
+    if (gsq) gsq[i] = h[0];
+  }
+  *n = k;
+}
+
+void Engine::stats_for_step(int64_t t, double* loss, double* gsq) {
+  CFT_CUDA(cudaStreamSynchronize(stream_));
+  CFT_CHECK(t >= 0 && t < t_, "engine: step not run yet");
+  *loss = host_stats_[t * 4 + 3] / cfg_.micro_batches;
+  *gsq = host_stats_[t * 4];
+}
+
+void Engine::params_from_masters(double* out) {
+  CFT_CUDA(cudaDeviceSynchronize());
+  const size_t S = ssz();
+  for (int c = 0; c < cfg_.K; ++c) {
+    const int64_t n = plan_.chunks[c].elements;
+    std::vector<char> buf(n * S);
+    const int sl = cfg_.offload ? slot_of(c) : -1;
+    if (cfg_.offload && sl >= 0)
+      CFT_CUDA(cudaMemcpy(buf.data(), slots_[sl].st[0], n * S, cudaMemcpyDeviceToHost));
+    else
+      CFT_CUDA(cudaMemcpy(buf.data(), host_states_[c], n * S,
+                          cfg_.offload ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+    for (const auto& s : chunk_slices_[c])
+      for (int64_t i = 0; i < s.count; ++i)
+        out[s.param_off + i] = S == 8 ? reinterpret_cast<double*>(buf.data())[s.aux_off + i]
+                                      : reinterpret_cast<float*>(buf.data())[s.aux_off + i];
+  }
+}
+
+void Engine::params_device(double* out) {
+  CFT_CUDA(cudaDeviceSynchronize());
+  void* tmp;
+  CFT_CUDA(cudaMalloc(&tmp, param_elems_ * 8));
+  if (cft_convert(static_cast<cft_dtype>(cfg_.dtype), params_, CFT_F64, tmp, param_elems_, stream_) != CFT_OK) {
+    cudaFree(tmp);
+    throw Error(last_error());
+  }
+  CFT_CUDA(cudaStreamSynchronize(stream_));
+  CFT_CUDA(cudaMemcpy(out, tmp, param_elems_ * 8, cudaMemcpyDeviceToHost));
+  cudaFree(tmp);
+}
+
+void Engine::grad_buffer(void** ptr, int64_t* n, int* dtype) {
+  *ptr = aux_;
+  *n = active_ >= 0 ? plan_.chunks[active_].elements : 0;
+  *dtype = cfg_.dtype == CFT_F64 ? CFT_F64 : CFT_F32;
+}
+
+std::string Engine::plan_json() const {
+  std::vector<host::TensorInfo> infos;
+  for (const auto& t : tensors_) {
+    host::TensorInfo i;
+    i.id = t.id;
+    i.name = t.name;
+    i.rows = t.rows;
+    i.cols = t.cols;
+    i.reg_order = t.id;
+    infos.push_back(i);
+  }
+  return host::plan_to_json(plan_, infos);
+}
+
+void Engine::chunk_counters(uint64_t* n) const {
+  for (int c = 0; c < cfg_.K; ++c) n[c] = n_local_[c];
+}
+
+void Engine::timing(float* ms) const {
+  // [0] inputs, [1] forward, [2] backward (first micro-batch), [3] stats+update
+  cudaEventSynchronize(ev_[5]);
+  cudaEventElapsedTime(&ms[0], ev_[0], ev_[1]);
+  cudaEventElapsedTime(&ms[1], ev_[1], ev_[2]);
+  cudaEventElapsedTime(&ms[2], ev_[2], ev_[3]);
+  cudaEventElapsedTime(&ms[3], ev_[4], ev_[5]);
+}
+
+}  // namespace cft

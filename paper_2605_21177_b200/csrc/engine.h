@@ -1,0 +1,173 @@
+// engine.h -- the chunk-local training step on one GPU (the hot path).
+//
+// Mirrors run_training (src/trainer.cpp:12-101) for the reference's model vocabulary
+// (Embedding first, Linear, LayerNorm, Tanh; sum / squared / half_sq / softmax_ce losses),
+// re-planned for B200:
+//   * parameters live in HBM in the compute dtype (bf16, fp32 or fp64), one contiguous arena
+//     in registration order;
+//   * per-chunk optimizer state (fp32 master/m/v; fp64 on the bit-exact path) lives in pinned
+//     host memory in plan order and rotates through three fixed HBM slots (active, prefetch-in,
+//     retire-out) with cudaMemcpyAsync on two copy streams, event-gated -- allocated bytes are
+//     constant across rotations by construction;
+//   * the backward runs only down to the lowest layer that owns an active slice (layers below
+//     cannot change any active gradient) unless full_backward is requested;
+//   * parameter gradients are produced only on the active support, straight into one contiguous
+//     aux buffer at each slice's plan offset (slice-aware wgrad / embedding scatter / norm dgamma);
+//   * the mean-gradient statistics pass and the fused AdamW (with write-back of the compute-dtype
+//     parameters through a per-slice segment table) finish the step.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "chunkft_b200.h"
+#include "host/plan.h"
+
+namespace cft {
+
+struct LayerSpec {
+  int type = 0;  // 0 linear, 1 embedding, 2 layernorm, 3 tanh
+  int a = 0, b = 0, c = 0;
+  int bias = 1;
+  double eps = 1e-5;
+};
+
+struct EngineConfig {
+  int dtype = CFT_BF16;
+  int loss = 2;
+  int optim = 0;  // 0 adamw, 1 plain
+  int micro_batches = 1;
+  int batch_rows = 1;
+  int plan_mode = 0;  // 0 K, 1 budget, 2 per_tensor
+  int K = 1;
+  int T = 1;
+  int64_t total_steps = 1;
+  int prefetch = 0;
+  int64_t bandwidth_bytes_per_step = 0;
+  int64_t budget_bytes = 0;
+  cft_adamw_hyper hyper{1e-3, 0.9, 0.999, 1e-8, 0.0};
+  int offload = 1;        // 1: states in pinned host memory + 3 HBM slots; 0: all resident
+  int full_backward = 0;  // 1: propagate dX through every layer like the reference
+  int check_every_step = 1;
+  double grad_scale = 1.0;  // extra factor folded into the mean (e.g. 1/world for DP)
+};
+
+struct Batch {
+  const void* x = nullptr;          // rows x in (compute dtype) for a Linear/LayerNorm-first model
+  const int32_t* tokens = nullptr;  // rows x seq for an Embedding-first model
+  const void* target = nullptr;     // rows x out (compute dtype) for sum/squared/half_sq
+  const int32_t* labels = nullptr;  // rows for softmax_ce
+  int on_device = 0;
+};
+
+class Engine {
+ public:
+  Engine(const std::vector<LayerSpec>& layers, const EngineConfig& cfg, const double* init_params,
+         cudaStream_t stream);
+  ~Engine();
+
+  // The step, split so a data-parallel caller can all-reduce the gradient in between.
+  int step_begin();                                  // scheduler + state loads; returns chunk
+  void forward_backward(const Batch& b, int mb);     // one micro-batch
+  void step_end();                                   // stats, update, offload, bookkeeping
+  void finish();                                     // flush all chunks to host, sync
+
+  // results
+  void trajectory(int64_t* step, int32_t* chunk, double* loss, double* gsq, int64_t* n) const;
+  void params_from_masters(double* out);            // fp64 copy of the authoritative params
+  void params_device(double* out);                  // the compute-dtype params (widened)
+  void grad_buffer(void** ptr, int64_t* n, int* dtype);
+  int64_t device_bytes() const { return device_bytes_; }
+  const host::ChunkPlan& plan() const { return plan_; }
+  host::RotationScheduler& scheduler() { return *sched_; }
+  std::string plan_json() const;
+  void chunk_counters(uint64_t* n) const;
+  void set_grad_scale(double s) { cfg_.grad_scale = s; }
+  void stats_for_step(int64_t t, double* loss, double* gsq);
+  cudaStream_t stream() const { return stream_; }
+  int micro_batches() const { return cfg_.micro_batches; }
+  void timing(float* ms_out) const;  // per-phase CUDA-event times of the last step
+
+ private:
+  struct Tensor {
+    int id;
+    std::string name;
+    int64_t rows, cols, param_off;
+    int layer;
+  };
+  struct Layer {
+    LayerSpec spec;
+    int w = -1, bias = -1;  // tensor ids (gamma/beta for layernorm)
+    int64_t in_w = 0, out_w = 0;
+    void* x_saved = nullptr;  // input (linear/layernorm) or output (tanh)
+    void* mean = nullptr;     // layernorm row stats (float, or double on the fp64 path)
+    void* rstd = nullptr;
+  };
+  struct SliceRt {
+    int tensor, layer;
+    int64_t rb, re, aux_off, param_off, count;
+  };
+  struct Slot {
+    int chunk = -1;
+    void* st[3] = {nullptr, nullptr, nullptr};  // master, m, v
+    cudaEvent_t ready = nullptr;  // H2D finished
+    cudaEvent_t free = nullptr;   // D2H finished (slot reusable)
+  };
+
+  void alloc(void** p, size_t bytes);
+  int slot_of(int chunk) const;
+  int take_free_slot(int avoid1, int avoid2);
+  void load_chunk(int chunk, bool for_prefetch);
+  void offload_chunk(int chunk);
+  void* param_ptr(int tensor) const;
+  size_t esz() const;
+  size_t ssz() const;
+
+  std::vector<Tensor> tensors_;
+  std::vector<Layer> layers_;
+  EngineConfig cfg_;
+  host::ChunkPlan plan_;
+  std::unique_ptr<host::RotationScheduler> sched_;
+  std::vector<std::vector<SliceRt>> chunk_slices_;
+  std::vector<cft_segment*> chunk_segs_;  // device segment tables
+  std::vector<int> lowest_layer_;
+  std::vector<uint64_t> n_local_;
+  int64_t max_chunk_ = 0, param_elems_ = 0, max_width_ = 0, max_slice_ = 0;
+
+  cudaStream_t stream_ = nullptr, h2d_ = nullptr, d2h_ = nullptr;
+  bool own_stream_ = false;
+  std::vector<void*> allocs_;
+  int64_t device_bytes_ = 0;
+  void* params_ = nullptr;
+  void* act_[2] = {nullptr, nullptr};
+  void* y_out_ = nullptr;
+  void* aux_ = nullptr;
+  void* scratch_ = nullptr;  // fp64 path: per-micro-batch slice grad / loss partials
+  void* in_x_ = nullptr;
+  void* in_target_ = nullptr;
+  int32_t* in_tokens_ = nullptr;
+  int32_t* in_labels_ = nullptr;
+  double* stats_ = nullptr;       // [step-ring][4]: sumsq, nonfinite, first_bad, loss
+  void* precond_ = nullptr;
+  void* consts_ = nullptr;        // reset template for the per-step stats / precond cells
+  unsigned long long* flags_ = nullptr;  // [0] bad labels, [1] bad tokens
+  std::array<Slot, 3> slots_;
+  std::vector<void*> host_states_;  // per chunk pinned: master|m|v
+  double* host_stats_ = nullptr;    // pinned mirror, total_steps x 4
+  unsigned long long* host_flags_ = nullptr;
+  cudaEvent_t step_done_ = nullptr;
+  std::array<cudaEvent_t, 6> ev_{};
+
+  int active_ = -1;
+  int64_t t_ = 0;
+  int mb_done_ = 0;
+  bool finished_ = false;
+  std::vector<int32_t> traj_chunk_;
+  std::vector<int64_t> traj_step_;
+};
+
+}  // namespace cft

@@ -1,0 +1,154 @@
+// engine_capi.cpp -- C ABI of the chunk-local training engine (include/chunkft_b200.h, sec. 4).
+#include <cstring>
+
+#include "cft_common.h"
+#include "engine.h"
+
+struct cft_engine {
+  std::unique_ptr<cft::Engine> p;
+};
+
+using cft::guarded;
+
+extern "C" {
+
+int cft_engine_create(const cft_layer_spec* layers, int n_layers, const cft_engine_config* c,
+                      const double* init_params, cft_stream_t stream, cft_engine** out) {
+  return guarded([&] {
+    std::vector<cft::LayerSpec> specs(static_cast<size_t>(n_layers));
+    for (int i = 0; i < n_layers; ++i)
+      specs[i] = {layers[i].type, layers[i].a, layers[i].b, layers[i].c, layers[i].bias,
+                  layers[i].eps};
+    cft::EngineConfig cfg;
+    cfg.dtype = c->dtype;
+    cfg.loss = c->loss;
+    cfg.optim = c->optim;
+    cfg.micro_batches = c->micro_batches;
+    cfg.batch_rows = c->batch_rows;
+    cfg.plan_mode = c->plan_mode;
+    cfg.K = c->K;
+    cfg.T = c->T;
+    cfg.total_steps = c->total_steps;
+    cfg.prefetch = c->prefetch;
+    cfg.offload = c->offload;
+    cfg.bandwidth_bytes_per_step = c->bandwidth_bytes_per_step;
+    cfg.budget_bytes = c->budget_bytes;
+    cfg.hyper = c->hyper;
+    cfg.full_backward = c->full_backward;
+    cfg.check_every_step = c->check_every_step;
+    cfg.grad_scale = c->grad_scale == 0.0 ? 1.0 : c->grad_scale;
+    *out = new cft_engine{
+        std::make_unique<cft::Engine>(specs, cfg, init_params, static_cast<cudaStream_t>(stream))};
+  });
+}
+
+void cft_engine_destroy(cft_engine* e) { delete e; }
+
+static cft::Batch to_batch(const cft_batch* b) {
+  cft::Batch r;
+  r.x = b->x;
+  r.tokens = b->tokens;
+  r.target = b->target;
+  r.labels = b->labels;
+  r.on_device = b->on_device;
+  return r;
+}
+
+int cft_engine_step_begin(cft_engine* e, int32_t* active) {
+  return guarded([&] {
+    const int a = e->p->step_begin();
+    if (active) *active = a;
+  });
+}
+
+int cft_engine_forward_backward(cft_engine* e, const cft_batch* b, int mb) {
+  return guarded([&] { e->p->forward_backward(to_batch(b), mb); });
+}
+
+int cft_engine_grad_buffer(cft_engine* e, void** ptr, int64_t* n, int32_t* dtype) {
+  return guarded([&] {
+    int dt = 0;
+    e->p->grad_buffer(ptr, n, &dt);
+    if (dtype) *dtype = dt;
+  });
+}
+
+int cft_engine_step_end(cft_engine* e) {
+  return guarded([&] { e->p->step_end(); });
+}
+
+int cft_engine_step(cft_engine* e, const cft_batch* batches) {
+  return guarded([&] {
+    e->p->step_begin();
+    for (int mb = 0; mb < e->p->micro_batches(); ++mb)
+      e->p->forward_backward(to_batch(batches + mb), mb);
+    e->p->step_end();
+  });
+}
+
+int cft_engine_finish(cft_engine* e) {
+  return guarded([&] { e->p->finish(); });
+}
+
+int cft_engine_set_grad_scale(cft_engine* e, double s) {
+  return guarded([&] { e->p->set_grad_scale(s); });
+}
+
+int64_t cft_engine_trajectory(cft_engine* e, int64_t* step, int32_t* chunk, double* loss,
+                              double* gsq, int64_t cap) {
+  int64_t n = -1;
+  guarded([&] {
+    int64_t k = 0;
+    e->p->trajectory(nullptr, nullptr, nullptr, nullptr, &k);
+    if (k > cap) throw cft::Error("trajectory buffer too small");
+    e->p->trajectory(step, chunk, loss, gsq, &n);
+  });
+  return n;
+}
+
+int64_t cft_engine_num_params(const cft_engine* e) {
+  int64_t n = 0;
+  for (const auto& ch : e->p->plan().chunks) n += ch.elements;
+  return n;
+}
+
+int cft_engine_params(cft_engine* e, double* out, int from_masters) {
+  return guarded([&] {
+    if (from_masters) e->p->params_from_masters(out);
+    else e->p->params_device(out);
+  });
+}
+
+int64_t cft_engine_device_bytes(const cft_engine* e) { return e->p->device_bytes(); }
+
+uint64_t cft_engine_plan_hash(const cft_engine* e) { return cft::host::plan_hash(e->p->plan()); }
+
+int cft_engine_plan_json(cft_engine* e, char* buf, int64_t cap, int64_t* needed) {
+  return guarded([&] {
+    const std::string j = e->p->plan_json();
+    if (needed) *needed = static_cast<int64_t>(j.size()) + 1;
+    if (buf && cap > 0) {
+      const size_t k = std::min<size_t>(j.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, j.data(), k);
+      buf[k] = '\0';
+    }
+  });
+}
+
+int64_t cft_engine_transfer_events(cft_engine* e, cft_transfer_event* out, int64_t cap) {
+  const auto& ev = e->p->scheduler().events();
+  const int64_t n = static_cast<int64_t>(ev.size());
+  for (int64_t i = 0; i < n && i < cap; ++i)
+    out[i] = {ev[i].step, ev[i].chunk, ev[i].dir, ev[i].bytes, ev[i].latency_steps};
+  return n;
+}
+
+int cft_engine_chunk_counters(cft_engine* e, uint64_t* n) {
+  return guarded([&] { e->p->chunk_counters(n); });
+}
+
+int cft_engine_phase_ms(cft_engine* e, float* ms4) {
+  return guarded([&] { e->p->timing(ms4); });
+}
+
+}  // extern "C"

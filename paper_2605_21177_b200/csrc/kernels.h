@@ -1,0 +1,87 @@
+// kernels.h -- host launchers of every device kernel in the library (used by the C ABI
+// wrappers and by the engine).  All launchers are asynchronous on the given stream.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace cft {
+
+namespace tc {  // gemm_tc.cu: bf16 tcgen05/TMEM GEMMs
+void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
+                void* y, cudaStream_t stream);
+void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w, int64_t in_dim,
+                  void* dx, int beta, cudaStream_t stream);
+void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const void* x,
+                        int64_t in_dim, int64_t rb, int64_t re, float* dw, int accumulate,
+                        cudaStream_t stream);
+}  // namespace tc
+
+namespace simt {  // gemm_simt.cu: fp32 / bf16 CUDA-core GEMMs and column sums
+void linear_fwd_f32(const float*, int64_t, int64_t, const float*, int64_t, const float*, float*,
+                    cudaStream_t);
+void linear_fwd_bf16(const __nv_bfloat16*, int64_t, int64_t, const __nv_bfloat16*, int64_t,
+                     __nv_bfloat16*, cudaStream_t);
+void add_bias_bf16(__nv_bfloat16*, const __nv_bfloat16*, int64_t, int64_t, cudaStream_t);
+void linear_dgrad_f32(const float*, int64_t, int64_t, const float*, int64_t, float*, int,
+                      cudaStream_t);
+void linear_dgrad_bf16(const __nv_bfloat16*, int64_t, int64_t, const __nv_bfloat16*, int64_t,
+                       __nv_bfloat16*, int, cudaStream_t);
+template <typename T>
+void linear_wgrad_slice_simt(const T*, int64_t, int64_t, const T*, int64_t, int64_t, int64_t,
+                             float*, int, cudaStream_t);
+template <typename T>
+void linear_dbias_slice(const T*, int64_t, int64_t, int64_t, int64_t, float*, int, cudaStream_t);
+}  // namespace simt
+
+namespace f64 {  // kernels_f64.cu: bit-exact fp64 kernels (device pointers)
+void linear_forward(const double*, int, int, const double*, int, const double*, double*,
+                    cudaStream_t);
+void linear_dinput(const double*, int, int, const double*, int, double*, cudaStream_t);
+void linear_dweight(const double*, int, int, const double*, int, long long, long long, double*,
+                    cudaStream_t);
+void linear_dbias(const double*, int, int, long long, long long, double*, cudaStream_t);
+void embedding_gather(const double*, int, const int*, int, double*, cudaStream_t);
+void embedding_scatter(const double*, int, const int*, int, long long, long long, double*,
+                       unsigned long long*, cudaStream_t);
+void layernorm_forward(const double*, int, int, const double*, const double*, double, double*,
+                       double*, double*, cudaStream_t);
+void layernorm_dinput(const double*, const double*, const double*, const double*, const double*,
+                      int, int, double*, cudaStream_t);
+void layernorm_dgamma(const double*, const double*, const double*, const double*, int, int,
+                      long long, long long, double*, cudaStream_t);
+void layernorm_dbeta(const double*, int, int, long long, long long, double*, cudaStream_t);
+void tanh_forward(const double*, long long, double*, cudaStream_t);
+void tanh_dinput(const double*, const double*, long long, double*, cudaStream_t);
+}  // namespace f64
+
+namespace layers {  // layers.cu: LayerNorm / Tanh / losses for fp32 & bf16 (+ fp64 losses)
+template <typename T>
+void layernorm_fwd(const T*, long long, long long, const T*, const T*, float, T*, float*, float*,
+                   cudaStream_t);
+template <typename T>
+void layernorm_dinput(const T*, const T*, const float*, const float*, const T*, long long,
+                      long long, T*, int, cudaStream_t);
+template <typename T>
+void layernorm_dgamma(const T*, const T*, const float*, const float*, long long, long long,
+                      long long, long long, float*, int, cudaStream_t);
+template <typename T>
+void tanh_fwd(const T*, long long, T*, cudaStream_t);
+template <typename T>
+void tanh_bwd(const T*, const T*, long long, T*, cudaStream_t);
+template <typename T>
+void loss(int kind, const T* y, const T* target, const int32_t* labels, long long rows,
+          long long cols, T* dy, double* loss_acc, unsigned long long* bad_label, cudaStream_t);
+void loss_f64(int kind, const double* y, const double* target, const int32_t* labels,
+              long long rows, long long cols, double* dy, double* loss_acc, double* scratch,
+              unsigned long long* bad_label, cudaStream_t);
+void add_f64(double* dst, const double* src, long long n, cudaStream_t s);
+void add_f32(float* dst, const float* src, long long n, cudaStream_t s);
+void flag_nonfinite_loss(double* stats_row, cudaStream_t s);
+void count_in_range(const int32_t* tokens, long long n, long long lo, long long hi,
+                    long long* bad, cudaStream_t s);
+}  // namespace layers
+
+}  // namespace cft

@@ -1,0 +1,356 @@
+// layers.cu -- LayerNorm, Tanh and loss kernels for the fp32 / bf16 engine paths.
+//
+// Reference math: src/kernels_serial.cpp:87-160 (layernorm / tanh) and
+// src/autodiff.cpp:180-228 (losses).  Row statistics and reductions run in fp32 (fp64 for
+// the loss value); activations are stored in the compute dtype T.  The fp64 engine path uses
+// the bit-exact kernels in kernels_f64.cu instead.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "cft_common.h"
+
+namespace cft::layers {
+
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p) {
+  if constexpr (std::is_same_v<T, float>) return *p;
+  else return __bfloat162float(*p);
+}
+template <typename T>
+__device__ __forceinline__ void stf(T* p, float v) {
+  if constexpr (std::is_same_v<T, float>) *p = v;
+  else *p = __float2bfloat16_rn(v);
+}
+
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  const int nw = (blockDim.x + 31) / 32;
+  for (int i = 0; i < nw; ++i) t += sh[i];
+  return t;
+}
+
+// y = gamma * (x - mu) * rstd + beta ; one block per row (kernels_serial.cpp:87-106)
+template <typename T>
+__global__ void ln_fwd_kernel(const T* x, long long dim, const T* gamma, const T* beta, float eps,
+                              T* y, float* mean, float* rstd) {
+  __shared__ float sh[32];
+  const long long b = blockIdx.x;
+  const T* xr = x + b * dim;
+  float s = 0.f;
+  for (long long j = threadIdx.x; j < dim; j += blockDim.x) s += ldf(xr + j);
+  const float mu = block_sum(s, sh) / dim;
+  float q = 0.f;
+  for (long long j = threadIdx.x; j < dim; j += blockDim.x) {
+    const float d = ldf(xr + j) - mu;
+    q += d * d;
+  }
+  const float var = block_sum(q, sh) / dim;
+  const float r = rsqrtf(var + eps);
+  if (threadIdx.x == 0) {
+    mean[b] = mu;
+    rstd[b] = r;
+  }
+  for (long long j = threadIdx.x; j < dim; j += blockDim.x)
+    stf(y + b * dim + j, ldf(gamma + j) * ((ldf(xr + j) - mu) * r) + ldf(beta + j));
+}
+
+// dx (+)= rstd * (g*dy - (sum(g*dy) + xhat*sum(g*dy*xhat))/dim)   (kernels_serial.cpp:108-130)
+template <typename T>
+__global__ void ln_dinput_kernel(const T* dy, const T* x, const float* mean, const float* rstd,
+                                 const T* gamma, long long dim, T* dx, int accumulate) {
+  __shared__ float sh[32];
+  const long long b = blockIdx.x;
+  const float mu = mean[b], r = rstd[b];
+  float sg = 0.f, sgx = 0.f;
+  for (long long j = threadIdx.x; j < dim; j += blockDim.x) {
+    const float gd = ldf(gamma + j) * ldf(dy + b * dim + j);
+    sg += gd;
+    sgx += gd * (ldf(x + b * dim + j) - mu) * r;
+  }
+  sg = block_sum(sg, sh);
+  sgx = block_sum(sgx, sh);
+  for (long long j = threadIdx.x; j < dim; j += blockDim.x) {
+    const float xhat = (ldf(x + b * dim + j) - mu) * r;
+    float v = r * (ldf(gamma + j) * ldf(dy + b * dim + j) - (sg + xhat * sgx) / dim);
+    if (accumulate) v += ldf(dx + b * dim + j);
+    stf(dx + b * dim + j, v);
+  }
+}
+
+// dgamma[j-rb] (+)= sum_b dy[b,j] * xhat[b,j], j in [rb,re)  (kernels_serial.cpp:132-143)
+template <typename T>
+__global__ void ln_dgamma_kernel(const T* dy, const T* x, const float* mean, const float* rstd,
+                                 long long rows, long long dim, long long rb, long long re,
+                                 float* out, int accumulate) {
+  __shared__ float red[8][33];
+  const long long j = rb + blockIdx.x * 32LL + threadIdx.x % 32;
+  const int part = threadIdx.x / 32;
+  float acc = 0.f;
+  if (j < re)
+    for (long long b = part; b < rows; b += 8)
+      acc += ldf(dy + b * dim + j) * (ldf(x + b * dim + j) - mean[b]) * rstd[b];
+  red[part][threadIdx.x % 32] = acc;
+  __syncthreads();
+  if (part == 0 && j < re) {
+    float s = 0.f;
+    for (int p = 0; p < 8; ++p) s += red[p][threadIdx.x % 32];
+    out[j - rb] = accumulate ? out[j - rb] + s : s;
+  }
+}
+
+template <typename T>
+__global__ void tanh_fwd_kernel(const T* x, long long n, T* y) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    stf(y + i, tanhf(ldf(x + i)));
+}
+
+template <typename T>
+__global__ void tanh_bwd_kernel(const T* dy, const T* y, long long n, T* dx) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float yy = ldf(y + i);
+    stf(dx + i, ldf(dy + i) * (1.f - yy * yy));
+  }
+}
+
+// Elementwise losses (autodiff.cpp:183-202): kind 0 sum, 1 squared, 2 half_sq.
+template <typename T>
+__global__ void loss_elem_kernel(int kind, const T* y, const T* target, long long n, T* dy,
+                                 double* loss) {
+  __shared__ float sh[32];
+  const float scale = kind == 1 ? 1.f : 0.5f;
+  float acc = 0.f;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float v = ldf(y + i);
+    if (kind == 0) {
+      acc += v;
+      stf(dy + i, 1.f);
+    } else {
+      const float d = v - ldf(target + i);
+      acc += d * d;
+      stf(dy + i, 2.f * scale * d);
+    }
+  }
+  const float s = block_sum(acc, sh);
+  if (threadIdx.x == 0) atomicAdd(loss, static_cast<double>(kind == 0 ? s : scale * s));
+}
+
+// Softmax cross-entropy, one block per row (autodiff.cpp:205-225): mean over rows.
+template <typename T>
+__global__ void loss_ce_kernel(const T* y, const int32_t* labels, long long cols, float inv_rows,
+                               T* dy, double* loss, unsigned long long* bad_label) {
+  __shared__ float sh[32];
+  const long long b = blockIdx.x;
+  const T* yr = y + b * cols;
+  const int label = labels[b];
+  if (label < 0 || label >= cols) {
+    if (threadIdx.x == 0) atomicAdd(bad_label, 1ull);
+    return;
+  }
+  float mx = -INFINITY;
+  for (long long c = threadIdx.x; c < cols; c += blockDim.x) mx = fmaxf(mx, ldf(yr + c));
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __shared__ float shm[32];
+  if (threadIdx.x % 32 == 0) shm[threadIdx.x / 32] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) mx = fmaxf(mx, shm[i]);
+  float z = 0.f;
+  for (long long c = threadIdx.x; c < cols; c += blockDim.x) z += __expf(ldf(yr + c) - mx);
+  z = block_sum(z, sh);
+  const float logz = logf(z);
+  for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float p = __expf(ldf(yr + c) - mx) / z;
+    stf(dy + b * cols + c, (p - (c == label ? 1.f : 0.f)) * inv_rows);
+  }
+  if (threadIdx.x == 0)
+    atomicAdd(loss, static_cast<double>(-(ldf(yr + label) - mx - logz)) * inv_rows);
+}
+
+// fp64 losses for the fp64 engine path (exp/log are CUDA's: <= 1-2 ulp from glibc).
+__global__ void loss_elem_f64_kernel(int kind, const double* y, const double* target, long long n,
+                                     double* dy, double* partial) {
+  // serial per block-chunk; the final sum is done by a single thread in order (below)
+  const double scale = kind == 1 ? 1.0 : 0.5;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (kind == 0) {
+      dy[i] = 1.0;
+      partial[i] = y[i];
+    } else {
+      const double d = __dsub_rn(y[i], target[i]);
+      dy[i] = __dmul_rn(__dmul_rn(2.0, scale), d);
+      partial[i] = __dmul_rn(d, d);
+    }
+  }
+}
+__global__ void serial_sum_f64_kernel(const double* v, long long n, double scale, double* out) {
+  double acc = 0.0;
+  for (long long i = 0; i < n; ++i) acc = __dadd_rn(acc, v[i]);
+  *out = __dadd_rn(*out, __dmul_rn(scale, acc));
+}
+__global__ void loss_ce_f64_kernel(const double* y, const int32_t* labels, long long rows,
+                                   long long cols, double* dy, double* row_loss,
+                                   unsigned long long* bad_label) {
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b >= rows) return;
+  const double* yr = y + b * cols;
+  const int label = labels[b];
+  if (label < 0 || label >= cols) {
+    atomicAdd(bad_label, 1ull);
+    row_loss[b] = 0.0;
+    return;
+  }
+  const double inv_b = __ddiv_rn(1.0, (double)rows);
+  double mx = yr[0];
+  for (long long c = 1; c < cols; ++c) mx = fmax(mx, yr[c]);
+  double z = 0.0;
+  for (long long c = 0; c < cols; ++c) z = __dadd_rn(z, exp(__dsub_rn(yr[c], mx)));
+  row_loss[b] = -__dsub_rn(__dsub_rn(yr[label], mx), log(z));
+  for (long long c = 0; c < cols; ++c) {
+    const double p = __ddiv_rn(exp(__dsub_rn(yr[c], mx)), z);
+    dy[b * cols + c] = __dmul_rn(__dsub_rn(p, c == label ? 1.0 : 0.0), inv_b);
+  }
+}
+
+inline int grid_n(long long n) {
+  return static_cast<int>(std::max<long long>(1, std::min<long long>((n + 255) / 256, num_sms() * 8LL)));
+}
+inline int row_threads(long long dim) {
+  return static_cast<int>(std::min<long long>(1024, std::max<long long>(32, ((dim + 31) / 32) * 32)));
+}
+
+// ---- host launchers (T = float or bf16) ----
+template <typename T>
+void layernorm_fwd(const T* x, long long rows, long long dim, const T* g, const T* b, float eps, T* y,
+                   float* mean, float* rstd, cudaStream_t s) {
+  if (rows <= 0) return;
+  ln_fwd_kernel<T><<<(unsigned)rows, row_threads(dim), 0, s>>>(x, dim, g, b, eps, y, mean, rstd);
+  check_launch("layernorm_fwd");
+}
+template <typename T>
+void layernorm_dinput(const T* dy, const T* x, const float* mean, const float* rstd, const T* g,
+                      long long rows, long long dim, T* dx, int accumulate, cudaStream_t s) {
+  if (rows <= 0) return;
+  ln_dinput_kernel<T><<<(unsigned)rows, row_threads(dim), 0, s>>>(dy, x, mean, rstd, g, dim, dx,
+                                                                  accumulate);
+  check_launch("layernorm_dinput");
+}
+template <typename T>
+void layernorm_dgamma(const T* dy, const T* x, const float* mean, const float* rstd, long long rows,
+                      long long dim, long long rb, long long re, float* out, int accumulate,
+                      cudaStream_t s) {
+  if (re <= rb) return;
+  ln_dgamma_kernel<T><<<(unsigned)((re - rb + 31) / 32), 256, 0, s>>>(dy, x, mean, rstd, rows, dim,
+                                                                       rb, re, out, accumulate);
+  check_launch("layernorm_dgamma");
+}
+template <typename T>
+void tanh_fwd(const T* x, long long n, T* y, cudaStream_t s) {
+  if (n <= 0) return;
+  tanh_fwd_kernel<T><<<grid_n(n), 256, 0, s>>>(x, n, y);
+  check_launch("tanh_fwd");
+}
+template <typename T>
+void tanh_bwd(const T* dy, const T* y, long long n, T* dx, cudaStream_t s) {
+  if (n <= 0) return;
+  tanh_bwd_kernel<T><<<grid_n(n), 256, 0, s>>>(dy, y, n, dx);
+  check_launch("tanh_bwd");
+}
+template <typename T>
+void loss(int kind, const T* y, const T* target, const int32_t* labels, long long rows,
+          long long cols, T* dy, double* loss_acc, unsigned long long* bad_label, cudaStream_t s) {
+  if (kind == 3) {
+    loss_ce_kernel<T><<<(unsigned)rows, row_threads(cols), 0, s>>>(y, labels, cols, 1.f / rows, dy,
+                                                                   loss_acc, bad_label);
+  } else {
+    loss_elem_kernel<T><<<grid_n(rows * cols), 256, 0, s>>>(kind, y, target, rows * cols, dy, loss_acc);
+  }
+  check_launch("loss");
+}
+void loss_f64(int kind, const double* y, const double* target, const int32_t* labels,
+              long long rows, long long cols, double* dy, double* loss_acc, double* scratch,
+              unsigned long long* bad_label, cudaStream_t s) {
+  if (kind == 3) {
+    loss_ce_f64_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(y, labels, rows, cols, dy,
+                                                                      scratch, bad_label);
+    serial_sum_f64_kernel<<<1, 1, 0, s>>>(scratch, rows, 1.0 / rows, loss_acc);
+  } else {
+    loss_elem_f64_kernel<<<grid_n(rows * cols), 256, 0, s>>>(kind, y, target, rows * cols, dy, scratch);
+    serial_sum_f64_kernel<<<1, 1, 0, s>>>(scratch, rows * cols, kind == 2 ? 0.5 : 1.0, loss_acc);
+  }
+  check_launch("loss_f64");
+}
+
+#define INST(T)                                                                                 \
+  template void layernorm_fwd<T>(const T*, long long, long long, const T*, const T*, float, T*,  \
+                                 float*, float*, cudaStream_t);                                 \
+  template void layernorm_dinput<T>(const T*, const T*, const float*, const float*, const T*,    \
+                                    long long, long long, T*, int, cudaStream_t);               \
+  template void layernorm_dgamma<T>(const T*, const T*, const float*, const float*, long long,   \
+                                    long long, long long, long long, float*, int, cudaStream_t); \
+  template void tanh_fwd<T>(const T*, long long, T*, cudaStream_t);                             \
+  template void tanh_bwd<T>(const T*, const T*, long long, T*, cudaStream_t);                   \
+  template void loss<T>(int, const T*, const T*, const int32_t*, long long, long long, T*,       \
+                        double*, unsigned long long*, cudaStream_t);
+INST(float)
+INST(__nv_bfloat16)
+#undef INST
+
+}  // namespace cft::layers
+
+namespace cft::layers {
+
+__global__ void add_f64_kernel(double* dst, const double* src, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = __dadd_rn(dst[i], src[i]);
+}
+__global__ void add_f32_kernel(float* dst, const float* src, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+// counts tokens outside [lo, hi) (embedding_forward's range check, ops.cpp:53-54)
+__global__ void out_of_range_kernel(const int32_t* t, long long n, long long lo, long long hi,
+                                    unsigned long long* bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (t[i] < lo || t[i] >= hi) atomicAdd(bad, 1ull);
+}
+
+__global__ void flag_loss_kernel(double* st) {
+  if (!isfinite(st[3])) atomicAdd(reinterpret_cast<unsigned long long*>(&st[1]), 1ull);
+}
+void flag_nonfinite_loss(double* st, cudaStream_t s) {
+  flag_loss_kernel<<<1, 1, 0, s>>>(st);
+  check_launch("flag_nonfinite_loss");
+}
+
+void add_f64(double* dst, const double* src, long long n, cudaStream_t s) {
+  if (n <= 0) return;
+  add_f64_kernel<<<grid_n(n), 256, 0, s>>>(dst, src, n);
+  check_launch("add_f64");
+}
+void add_f32(float* dst, const float* src, long long n, cudaStream_t s) {
+  if (n <= 0) return;
+  add_f32_kernel<<<grid_n(n), 256, 0, s>>>(dst, src, n);
+  check_launch("add_f32");
+}
+void count_in_range(const int32_t* tokens, long long n, long long lo, long long hi, long long* bad,
+                    cudaStream_t s) {
+  if (n <= 0) return;
+  out_of_range_kernel<<<grid_n(n), 256, 0, s>>>(tokens, n, lo, hi,
+                                                reinterpret_cast<unsigned long long*>(bad));
+  check_launch("count_in_range");
+}
+
+}  // namespace cft::layers

@@ -1,0 +1,164 @@
+"""GPU parity of the whole chunk-local training step against the reference's run_training.
+
+Golden trajectories come from the unmodified reference library (tests/golden/train.json,
+produced by oracle/make_golden.py from oracle/_ref; cases mirror the reference presets in
+src/runner.cpp:40-129 plus micro-batch/prefetch/layernorm/budget cases).
+
+Tolerances:
+  * fp64 engine: loss trajectory and final parameters within 1e-12 relative; bit-identical
+    for Linear-only half_sq models (no tanh/exp/log, whose CUDA and glibc results may
+    differ in the last ulp);
+  * fp32 engine: normwise relative 1e-5 on final parameters and per-step losses;
+  * bf16 engine (bf16 operands, fp32 accumulation/state): normwise 2e-2.
+Plan hash, active-chunk sequence and transfer log must match exactly in every dtype.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import lib as O  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "train.json")
+with open(GOLD) as _f:
+    CASES = {c["name"]: c for c in json.load(_f)}
+
+
+def model_of(case):
+    from paper_2605_21177_b200.engine import Model
+    m = Model(loss=case["loss"])
+    for L in case["layers"]:
+        if L[0] == "linear":
+            m.add_linear(L[1], L[2], bool(L[3]))
+        elif L[0] == "embedding":
+            m.add_embedding(L[1], L[2], L[3])
+        elif L[0] == "layernorm":
+            m.add_layernorm(L[1])
+        else:
+            m.add_tanh()
+    return m
+
+
+def options_of(case, dtype, offload=True):
+    from paper_2605_21177_b200.engine import TrainOptions, AdamWHyper
+    from paper_2605_21177_b200.plan import ScheduleConfig
+    o = TrainOptions()
+    o.schedule = ScheduleConfig(K=case["K"] or 1, T=case["T"], total_steps=case["steps"],
+                                prefetch=case["prefetch"], bandwidth_bytes_per_step=case["bw"])
+    o.hyper = AdamWHyper(*case["hyper"])
+    o.optim = case["optim"]
+    o.micro_batches = case["micro_batches"]
+    if case["budget"]:
+        o.plan = "budget"
+        o.budget_bytes = case["budget"]
+    o.dtype = dtype
+    o.offload = offload
+    return o
+
+
+def batches_of(case):
+    out = []
+    for b in case["batches"]:
+        d = {}
+        for k, v in b.items():
+            d[k] = np.asarray(v, dtype=np.int32 if k in ("tokens", "labels") else np.float64)
+        out.append(d)
+    return out
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("offload", [True, False])
+def test_fp64_engine_matches_reference(cuda, name, offload):
+    from paper_2605_21177_b200.engine import run_training
+    case = CASES[name]
+    r = run_training(model_of(case), np.array(case["init_params"]), batches_of(case),
+                     options_of(case, "fp64", offload))
+    assert f"{r.plan_hash:016x}" == case["plan_hash"]
+    assert r.chunk.tolist() == case["traj_chunk"]
+    assert rel(r.loss, case["traj_loss"]) < 1e-12
+    assert rel(r.grad_norm_sq, case["traj_gsq"]) < 1e-12
+    assert rel(r.params, case["final_params"]) < 1e-12
+    if name in ("linear_exact", "quadratic_k2"):
+        assert np.array_equal(r.params, np.array(case["final_params"]))
+        assert np.array_equal(r.loss, np.array(case["traj_loss"]))
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_fp32_engine_matches_reference(cuda, name):
+    from paper_2605_21177_b200.engine import run_training
+    case = CASES[name]
+    r = run_training(model_of(case), np.array(case["init_params"]), batches_of(case),
+                     options_of(case, "fp32"))
+    assert r.chunk.tolist() == case["traj_chunk"]
+    assert rel(r.params, case["final_params"]) < 1e-5
+    assert rel(r.loss, case["traj_loss"]) < 1e-5
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_bf16_engine_matches_reference(cuda, name):
+    from paper_2605_21177_b200.engine import run_training
+    case = CASES[name]
+    r = run_training(model_of(case), np.array(case["init_params"]), batches_of(case),
+                     options_of(case, "bf16"))
+    assert r.chunk.tolist() == case["traj_chunk"]
+    assert rel(r.params, case["final_params"]) < 2e-2
+    assert rel(r.loss, case["traj_loss"]) < 2e-2
+
+
+def test_transfer_log_matches_oracle_schedule(cuda):
+    from paper_2605_21177_b200.engine import run_training
+    case = CASES["emb_ln_mb"]
+    r = run_training(model_of(case), np.array(case["init_params"]), batches_of(case),
+                     options_of(case, "fp32"))
+    from paper_2605_21177_b200.plan import TensorInfo, partition
+    infos = [TensorInfo(i, n, rr, cc) for i, (n, rr, cc) in enumerate(model_of(case).tensors())]
+    plan = partition(infos, case["K"])
+    want = O.schedule(plan.K, case["T"], case["steps"], [c.elements * 12 for c in plan.chunks],
+                      prefetch=case["prefetch"], bw=case["bw"])
+    got = [(e.step, e.chunk, 0 if e.dir == "load" else 1, e.bytes, e.latency_steps) for e in r.transfers]
+    assert got == want["events"]
+
+
+def test_flat_device_memory_across_rotations(cuda):
+    """Allocated HBM is fixed at engine creation: no per-step allocation, so the per-step
+    memory profile is flat (jitter 0, cf. accounting.cpp:44-48)."""
+    from paper_2605_21177_b200.engine import ChunkEngine
+    case = CASES["mlp_imbalanced"]
+    eng = ChunkEngine(model_of(case), np.array(case["init_params"]), 8, options_of(case, "bf16"))
+    staged = [eng.stage(b, device=True) for b in batches_of(case)]
+    torch.cuda.synchronize()
+    before = torch.cuda.mem_get_info()[0]
+    free = []
+    for t in range(case["steps"]):
+        eng.step([staged[t % len(staged)]])
+        torch.cuda.synchronize()
+        free.append(torch.cuda.mem_get_info()[0])
+    eng.finish()
+    assert max(free) == min(free) == before
+    assert eng.device_bytes() > 0
+
+
+def test_nonfinite_gradient_is_rejected_without_advancing(cuda):
+    """optimizer.cpp:169-173 / trainer.cpp:90-93: error text with step/chunk context, the
+    chunk-local counter is not advanced and the state is not mutated."""
+    from paper_2605_21177_b200.engine import ChunkEngine, Error
+    case = CASES["linear_exact"]
+    eng = ChunkEngine(model_of(case), np.array(case["init_params"]), 12, options_of(case, "fp32"))
+    b = batches_of(case)[0]
+    bad = dict(b)
+    bad["x"] = b["x"].copy()
+    bad["x"][0, 0] = np.inf
+    good = eng.stage(b, device=True)
+    eng.step([good])
+    with pytest.raises(Error, match=r"step 1, chunk 1: (non-finite loss|step: non-finite gradient)"):
+        eng.step([eng.stage(bad, device=True)])
+    assert eng.chunk_counters()[1] == 0
