@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""bench.py -- the chunk-local fine-tuning step on B200 (BASELINE.json configs[1]).
+
+Workload ("linear4096_chunk_local_step"): one Linear(4096 -> 4096, no bias) layer, half_sq loss,
+N_tok = 8192 synthetic tokens per GPU per step, byte-balanced plan K = 8 (active slice = 1/8 of
+the rows = 512 x 4096), T = K (the reference's default dwell, config.cpp:204), prefetch on,
+AdamW, optimizer state in pinned host memory rotating through three HBM slots.  One step =
+forward GEMM + half_sq loss + dX = dY.W (formed like LinearNode::backward always does) +
+slice-aware dW_S = dY_S^T.X + grad statistics + fused AdamW with bf16 write-back: exactly the
+reference's run_training step (src/trainer.cpp:36-94) for this model.
+
+value   = tokens/s over all ranks, inputs resident in HBM (4 rotating batches = 512 MiB > L2).
+e2e     = the same step through the C ABI with pinned HOST batches uploaded inside the timed
+          region and every step's loss read back on the host.
+roofline: the tcgen05 GEMM kernel family (fwd + dgrad + sliced wgrad), CUDA events on the
+          engine stream; peak = MEASURED_PEAKS.json sustained bf16.
+--impl reference: the unmodified reference CPU library (oracle/_ref, built from
+          /root/reference) on the host cores, bounded token sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D = 4096
+N_TOK = 8192
+K_CHUNKS = 8
+METRIC = "chunk-local FT step tokens/s; sliced-dW TFLOP/s and AdamW GB/s vs B200 peak"
+WORKLOAD = "linear4096_chunk_local_step (BASELINE configs[1]: single Linear d=4096, N_tok=8192, " \
+           "active slice 1/8 of rows, bf16 operands / fp32 accumulate+state)"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return dict(hbm=float(p["hbm_gbs"]), bf16=float(p["bf16_tflops"]),
+                    bf16_sustained=float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                    source="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, source="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+# Reference CPU path (oracle/_ref = the unmodified reference library), bounded sample
+
+def reference_cpu(rows: int = 64, steps=(1, 3)):
+    """Per-step time of the reference's run_training on the configs[1] model with a reduced
+    token count (rows); tokens/s = rows / step_time.  Two runs of different length cancel the
+    setup cost (state init/serialisation)."""
+    from oracle import ref as R
+    if not R.available:
+        return reference_port(rows)
+    R.set_backend(True)
+    rng = np.random.default_rng(42)
+    layers = [("linear", D, D, False)]
+    params = R.init_params(layers, seed=7)
+    batches = [dict(x=rng.uniform(-1, 1, (rows, D)), target=rng.uniform(-1, 1, (rows, D)))]
+    times = []
+    for s in steps:
+        t0 = time.perf_counter()
+        R.train(layers, "half_sq", params, batches, K=K_CHUNKS, T=K_CHUNKS, steps=s)
+        times.append(time.perf_counter() - t0)
+    per_step = (times[1] - times[0]) / (steps[1] - steps[0])
+    return dict(value=rows / per_step, unit="tokens/s", cores=R.openmp_threads(), kind="reference",
+                sample=f"reference run_training (oracle/_ref, OpenMP backend), Linear 4096x4096 "
+                       f"half_sq K=8 T=8 AdamW, {rows} tokens/step, per-step time = "
+                       f"(t[{steps[1]} steps] - t[{steps[0]} step]) / {steps[1] - steps[0]}",
+                step_s=per_step)
+
+
+def reference_port(rows: int = 64):
+    """Fallback: the oracle's C restatement, single thread, one step's operator sequence."""
+    from oracle import lib as O
+    rng = np.random.default_rng(42)
+    x = rng.uniform(-1, 1, (rows, D))
+    w = rng.uniform(-0.5, 0.5, (D, D)) / np.sqrt(D)
+    t = rng.uniform(-1, 1, (rows, D))
+    E = D * D // K_CHUNKS
+    st = [w[: D // K_CHUNKS].ravel().copy(), np.zeros(E), np.zeros(E)]
+    t0 = time.perf_counter()
+    y = O.linear_forward(x, w)
+    _, dy = O.eval_loss("half_sq", y, target=t)
+    O.linear_dinput(dy, w)
+    g = O.linear_dweight(dy, x, 0, D // K_CHUNKS)
+    O.adamw(st[0], st[1], st[2], g.ravel(), 0)
+    dt = time.perf_counter() - t0
+    return dict(value=rows / dt, unit="tokens/s", cores=1, kind="port",
+                sample=f"oracle C restatement (single thread), one step at {rows} tokens", step_s=dt)
+
+
+# ---------------------------------------------------------------------------------------
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_21177_b200.engine import ChunkEngine, Model, TrainOptions
+    from paper_2605_21177_b200.plan import ScheduleConfig
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    peaks = load_peaks()
+    W, S = args.warmup, args.steps
+    total = 2 * (W + S) + 2
+
+    model = Model(loss="half_sq").add_linear(D, D, bias=False)
+    rng = np.random.default_rng(7)
+    init = (rng.uniform(-0.5, 0.5, D * D) / np.sqrt(D))  # model.cpp:114-115 init rule
+    opt = TrainOptions(schedule=ScheduleConfig(K=K_CHUNKS, T=K_CHUNKS, total_steps=total, prefetch=True),
+                       dtype="bf16", offload=True, full_backward=True, check_every_step=False)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        eng = ChunkEngine(model, init, N_TOK, opt, stream=stream)
+    if world > 1:
+        eng.set_grad_scale(1.0 / world)
+
+    # synthetic inputs: 4 distinct batches per rank (512 MiB bf16 > 126 MB L2)
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    dev_batches, host_batches = [], []
+    for i in range(4):
+        x = (torch.rand(N_TOK, D, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+        tg = (torch.rand(N_TOK, D, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+        dev_batches.append(eng.stage({"x": x, "target": tg}, device=True))
+        if i < 2:
+            host_batches.append(eng.stage({"x": x.cpu(), "target": tg.cpu()}, device=False))
+    torch.cuda.synchronize()
+
+    def one_step(b):
+        if world == 1:
+            eng.step([b])
+            return
+        eng.step_begin()
+        eng.forward_backward(b, 0)
+        with torch.cuda.stream(stream):
+            dist.all_reduce(eng.grad_tensor())
+        eng.step_end()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timing ----
+    for i in range(W):
+        one_step(dev_batches[i % 4])
+    barrier()
+    eng.profile(True, 64 * (S + 2))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for i in range(S):
+            one_step(dev_batches[(W + i) % 4])
+        e1.record(stream)
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    phases = eng.phase_totals()
+    eng.profile(False, 0)
+
+    # ---- end-to-end through the C ABI: pinned host batches, per-step loss read ----
+    step_base = W + S
+    for i in range(W):
+        one_step(host_batches[i % 2])
+        eng.wait_step(step_base + i)
+    barrier()
+    t0 = time.perf_counter()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    losses = []
+    for i in range(S):
+        one_step(host_batches[i % 2])
+        if i > 0:
+            losses.append(eng.wait_step(step_base + W + i - 1)[0])
+    losses.append(eng.wait_step(step_base + W + S - 1)[0])
+    f1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+    eng.finish()
+    finite = all(np.isfinite(losses))
+
+    tokens = N_TOK * world * S
+    value = tokens / (ms / 1e3)
+    e2e_value = tokens / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel family (tcgen05 GEMMs) ----
+    S_rows = D // K_CHUNKS
+    fl_fwd = 2.0 * N_TOK * D * D
+    fl_dgrad = 2.0 * N_TOK * D * D
+    fl_wgrad = 2.0 * N_TOK * S_rows * D
+    gemm_ms = phases["fwd_gemm"][0] + phases["dgrad"][0] + phases["wgrad"][0]
+    gemm_tflops = (fl_fwd + fl_dgrad + fl_wgrad) * S / (gemm_ms / 1e3) / 1e12
+    wgrad_tflops = fl_wgrad * S / (phases["wgrad"][0] / 1e3) / 1e12
+    E = D * D // K_CHUNKS
+    adamw_gbs = 30.0 * E * S / (phases["update"][0] / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get("gemm_bytes_per_launch")
+        except Exception:
+            traffic = None
+    kernels_per_step = sum(c for k, (_, c) in phases.items() if k != "inputs") / max(S, 1) + 1
+    step_ms = ms / S
+
+    res = None
+    if rank == 0:
+        clocks = clk.summary()
+        res = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": S,
+            "warmup": W,
+            "ms_per_step": step_ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (seeded uniform tokens x activations and targets, random-init weights)",
+            "config": {"workload": WORKLOAD, "d": D, "tokens_per_gpu_per_step": N_TOK,
+                       "global_batch_tokens": N_TOK * world, "K": K_CHUNKS, "T": K_CHUNKS,
+                       "active_slice_rows": S_rows, "prefetch": True, "state_residency":
+                       "pinned host + 3 HBM slots", "parallelism": f"dp{world}",
+                       "l2": "inputs larger than L2: 4 rotating 128 MiB batches"},
+            "e2e": {"value": e2e_value, "unit": "tokens/s",
+                    "h2d_bytes_per_step": 2 * N_TOK * D * 2, "d2h_bytes_per_step": 32,
+                    "ms_per_step": e2e_ms / S, "losses_finite": finite},
+            "roofline": {"bound": "tensor", "kernel": "gemm_bf16_kernel (tcgen05: fwd+dgrad+sliced wgrad)",
+                         "achieved": gemm_tflops, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
+                         "frac": gemm_tflops / peaks["bf16_sustained"], "traffic": traffic,
+                         "peak_source": peaks["source"] + " sustained bf16 (MEASURED_PEAKS.json)",
+                         "algorithmic_flops_per_step": fl_fwd + fl_dgrad + fl_wgrad},
+            "sliced_dw": {"tflops": wgrad_tflops, "frac_of_measured_peak": wgrad_tflops / peaks["bf16"],
+                          "frac_of_spec_2250": wgrad_tflops / 2250.0, "shape": f"{S_rows}x{D} over {N_TOK} tokens"},
+            "adamw": {"GBps": adamw_gbs, "frac_of_measured_hbm": adamw_gbs / peaks["hbm"],
+                      "frac_of_spec_8000": adamw_gbs / 8000.0, "elements": E, "bytes_per_elem": 30},
+            "phases_ms_per_step": {k: v[0] / S for k, v in phases.items()},
+            "gpu_launches": int(round(kernels_per_step * S)),
+            "clocks": clocks,
+        }
+    return res
+
+
+def slice_sweep(local_rank):
+    """sliced-dW TFLOP/s for active-slice widths 1/8 .. 1/1 (configs[1] sweep)."""
+    import torch
+    from paper_2605_21177_b200 import ops
+    dev = torch.device("cuda", local_rank)
+    x = (torch.rand(N_TOK, D, device=dev) * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand(N_TOK, D, device=dev) * 2 - 1).to(torch.bfloat16)
+    out = {}
+    for f in (8, 4, 2, 1):
+        s = D // f
+        rb = (12376 % D) if f > 1 else 0
+        rb = min(rb, D - s)
+        buf = torch.empty(s, D, device=dev)
+        for _ in range(3):
+            ops.linear_wgrad_slice(dy, x, rb, rb + s, out=buf)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(10):
+            ops.linear_wgrad_slice(dy, x, rb, rb + s, out=buf)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 10
+        out[f"1/{f}"] = {"rows": s, "row_begin": rb, "ms": t, "tflops": 2 * N_TOK * s * D / t / 1e9}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=24)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="add the 1/8..1/1 sliced-dW sweep")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cpu = reference_cpu()
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cpu["step_s"] * 1e3 * N_TOK / 64, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "reference_sample_tokens": 64},
+            "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}))
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if args.sweep:
+            res["sliced_dw"]["sweep"] = slice_sweep(local_rank)
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = reference_cpu()
+            res["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(res))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -334,6 +334,16 @@ int64_t cft_engine_transfer_events(cft_engine* e, cft_transfer_event* out, int64
 int cft_engine_chunk_counters(cft_engine* e, uint64_t* n_out);
 /* CUDA-event times of the last step: inputs, forward, backward, stats+update (ms). */
 int cft_engine_phase_ms(cft_engine* e, float* ms4);
+/* Kernel-category profiler: CUDA events on the engine stream around every launch of a
+ * category (0 inputs, 1 forward GEMM, 2 other forward, 3 loss, 4 slice wgrad, 5 dgrad,
+ * 6 other backward, 7 gradient statistics, 8 AdamW/SGD update).  max_marks bounds the
+ * preallocated event pool.  phase_totals synchronises, returns summed ms and launch counts
+ * per category (9 entries each) and clears the marks. */
+int cft_engine_profile(cft_engine* e, int enable, int64_t max_marks);
+int cft_engine_phase_totals(cft_engine* e, float* ms9, int64_t* counts9);
+/* Block the host until step t's loss / grad_norm_sq reached host memory (t within the last
+ * 4 steps) -- a per-step result read that does not drain the device queue. */
+int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq);
 
 #ifdef __cplusplus
 }

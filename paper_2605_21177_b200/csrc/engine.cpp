@@ -132,6 +132,7 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
   CFT_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   CFT_CUDA(cudaEventCreateWithFlags(&step_done_, cudaEventDisableTiming));
   for (auto& e : ev_) CFT_CUDA(cudaEventCreate(&e));
+  for (auto& e : stats_ev_) CFT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
   // ---- per-chunk slice tables (plan order = state/aux layout) ----
   chunk_slices_.resize(cfg_.K);
@@ -265,8 +266,60 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
   CFT_CUDA(cudaDeviceSynchronize());
 }
 
+void Engine::profile(bool on, int64_t max_marks) {
+  profiling_ = on;
+  marks_.clear();
+  pool_next_ = 0;
+  while (static_cast<int64_t>(pool_.size()) < 2 * max_marks) {
+    cudaEvent_t e;
+    CFT_CUDA(cudaEventCreate(&e));
+    pool_.push_back(e);
+  }
+}
+
+void Engine::pb(int phase) {
+  if (!profiling_ || pool_next_ + 2 > pool_.size()) return;
+  open_phase_ = phase;
+  open_ev_ = pool_[pool_next_++];
+  CFT_CUDA(cudaEventRecord(open_ev_, stream_));
+}
+
+void Engine::pe() {
+  if (!profiling_ || open_phase_ < 0) return;
+  cudaEvent_t b = pool_[pool_next_++];
+  CFT_CUDA(cudaEventRecord(b, stream_));
+  marks_.push_back({open_phase_, open_ev_, b});
+  open_phase_ = -1;
+}
+
+void Engine::phase_totals(float* ms, int64_t* counts) {
+  CFT_CUDA(cudaStreamSynchronize(stream_));
+  for (int i = 0; i < kNumPhases; ++i) {
+    ms[i] = 0.f;
+    if (counts) counts[i] = 0;
+  }
+  for (const auto& m : marks_) {
+    float t = 0.f;
+    CFT_CUDA(cudaEventElapsedTime(&t, m.a, m.b));
+    ms[m.phase] += t;
+    if (counts) counts[m.phase] += 1;
+  }
+  marks_.clear();
+  pool_next_ = 0;
+}
+
+void Engine::wait_step(int64_t t, double* loss, double* gsq) {
+  CFT_CHECK(t >= 0 && t < t_ && t >= t_ - 4, "engine: step result no longer tracked");
+  CFT_CUDA(cudaEventSynchronize(stats_ev_[t % 4]));
+  if (loss) *loss = host_stats_[t * 4 + 3] / cfg_.micro_batches;
+  if (gsq) *gsq = host_stats_[t * 4];
+}
+
 Engine::~Engine() {
   cudaDeviceSynchronize();
+  for (auto e : pool_) cudaEventDestroy(e);
+  for (auto e : stats_ev_)
+    if (e) cudaEventDestroy(e);
   for (void* p : allocs_) cudaFree(p);
   if (cfg_.offload)
     for (void* p : host_states_)
@@ -375,6 +428,7 @@ void Engine::forward_backward(const Batch& b, int mb) {
   const cudaMemcpyKind kind = b.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
 
   // ---- inputs ----
+  pb(kInputs);
   const void* x_in = nullptr;
   const int32_t* tok = nullptr;
   if (first.spec.type == kEmbedding) {
@@ -398,6 +452,7 @@ void Engine::forward_backward(const Batch& b, int mb) {
     CFT_CHECK(b.labels != nullptr, "loss: label count mismatch");
     CFT_CUDA(cudaMemcpyAsync(in_labels_, b.labels, rows * 4, kind, s));
   }
+  pe();
   if (mb == 0) CFT_CUDA(cudaEventRecord(ev_[1], s));
 
   // ---- forward (autodiff.cpp:235-305) ----
@@ -405,6 +460,7 @@ void Engine::forward_backward(const Batch& b, int mb) {
     Layer& L = layers_[li];
     const void* in = li == 0 ? x_in : layers_[li - 1].x_saved;
     void* out = L.x_saved;
+    pb(L.spec.type == kLinear ? kFwdGemm : kFwdOther);
     switch (L.spec.type) {
       case kEmbedding:
         if (cft_embedding_gather(static_cast<cft_dtype>(dt), param_ptr(L.w), L.spec.b, tok,
@@ -443,8 +499,10 @@ void Engine::forward_backward(const Batch& b, int mb) {
         else layers::tanh_fwd<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(in), rows * L.in_w, static_cast<__nv_bfloat16*>(out), s);
         break;
     }
+    pe();
   }
   if (mb == 0) CFT_CUDA(cudaEventRecord(ev_[2], s));
+  pb(kLoss);
 
   // ---- loss (autodiff.cpp:180-228) ----
   double* loss_acc = stats_ + t_ * 4 + 3;
@@ -460,6 +518,8 @@ void Engine::forward_backward(const Batch& b, int mb) {
     layers::loss<__nv_bfloat16>(cfg_.loss, static_cast<const __nv_bfloat16*>(y_out_),
                                 static_cast<const __nv_bfloat16*>(target), in_labels_, rows,
                                 last.out_w, static_cast<__nv_bfloat16*>(dy), loss_acc, flags_, s);
+
+  pe();
 
   // ---- chunk-masked backward (autodiff.cpp:307-313), suffix only ----
   const int stop = cfg_.full_backward ? 0 : lowest_layer_[active_];
@@ -488,6 +548,7 @@ void Engine::forward_backward(const Batch& b, int mb) {
         CFT_CUDA(cudaMemsetAsync(tgt, 0, sl.count * 4, s));
       }
       const bool is_w = sl.tensor == L.w;
+      pb(L.spec.type == kLinear && is_w ? kWgrad : kBwdOther);
       switch (L.spec.type) {
         case kLinear:
           if (is_w) {
@@ -528,9 +589,11 @@ void Engine::forward_backward(const Batch& b, int mb) {
           }
           break;
       }
+      pe();
       if (dt == CFT_F64 && mb > 0) layers::add_f64(static_cast<double*>(dst), static_cast<double*>(tgt), sl.count, s);
     }
     if (!need_dx) continue;
+    pb(L.spec.type == kLinear ? kDgrad : kBwdOther);
     switch (L.spec.type) {
       case kLinear:
         if (cft_linear_dgrad(static_cast<cft_dtype>(dt), g, rows, L.out_w, param_ptr(L.w), L.in_w, gx, 0,
@@ -572,6 +635,7 @@ void Engine::forward_backward(const Batch& b, int mb) {
         }
         break;
     }
+    pe();
     cur ^= 1;
   }
   (void)E;
@@ -589,9 +653,11 @@ void Engine::step_end() {
   const double scale = cfg_.grad_scale * (1.0 / cfg_.micro_batches);  // take_mean_grad
   double* st = stats_ + t_ * 4;
   CFT_CUDA(cudaEventRecord(ev_[4], s));
+  pb(kStats);
   if (cft_grad_stats(sdt, aux_, n, scale, st, s) != CFT_OK) throw Error(last_error());
   // a non-finite loss also blocks the update (trainer.cpp:48-49 throws before any step)
   layers::flag_nonfinite_loss(st, s);
+  pe();
 
   void* master;
   void* m;
@@ -609,6 +675,7 @@ void Engine::step_end() {
   }
   n_local_[c] += 1;
   const int32_t nseg = static_cast<int32_t>(chunk_slices_[c].size());
+  pb(kUpdate);
   if (cfg_.optim == 0) {
     const double bc1 = 1.0 - std::pow(cfg_.hyper.beta1, static_cast<double>(n_local_[c]));
     const double bc2 = 1.0 - std::pow(cfg_.hyper.beta2, static_cast<double>(n_local_[c]));
@@ -621,9 +688,11 @@ void Engine::step_end() {
                       params_, chunk_segs_[c], nseg, st, s) != CFT_OK)
       throw Error(last_error());
   }
+  pe();
   CFT_CUDA(cudaEventRecord(ev_[5], s));
   CFT_CUDA(cudaEventRecord(step_done_, s));
   CFT_CUDA(cudaMemcpyAsync(host_stats_ + t_ * 4, st, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CFT_CUDA(cudaEventRecord(stats_ev_[t_ % 4], s));
   traj_step_.push_back(t_);
   traj_chunk_.push_back(c);
 

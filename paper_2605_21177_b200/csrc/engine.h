@@ -92,6 +92,13 @@ class Engine {
   int micro_batches() const { return cfg_.micro_batches; }
   void timing(float* ms_out) const;  // per-phase CUDA-event times of the last step
 
+  // Kernel-category profiler (CUDA events on the engine stream, preallocated pool).
+  enum Phase { kInputs = 0, kFwdGemm, kFwdOther, kLoss, kWgrad, kDgrad, kBwdOther, kStats,
+               kUpdate, kNumPhases };
+  void profile(bool on, int64_t max_marks);
+  void phase_totals(float* ms, int64_t* counts);  // syncs; resets the marks
+  void wait_step(int64_t t, double* loss, double* gsq);  // host waits for step t's result only
+
  private:
   struct Tensor {
     int id;
@@ -161,6 +168,19 @@ class Engine {
   unsigned long long* host_flags_ = nullptr;
   cudaEvent_t step_done_ = nullptr;
   std::array<cudaEvent_t, 6> ev_{};
+  std::array<cudaEvent_t, 4> stats_ev_{};
+  struct Mark {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  bool profiling_ = false;
+  std::vector<cudaEvent_t> pool_;
+  size_t pool_next_ = 0;
+  std::vector<Mark> marks_;
+  int open_phase_ = -1;
+  cudaEvent_t open_ev_ = nullptr;
+  void pb(int phase);
+  void pe();
 
   int active_ = -1;
   int64_t t_ = 0;

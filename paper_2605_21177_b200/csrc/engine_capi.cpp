@@ -151,4 +151,16 @@ int cft_engine_phase_ms(cft_engine* e, float* ms4) {
   return guarded([&] { e->p->timing(ms4); });
 }
 
+int cft_engine_profile(cft_engine* e, int enable, int64_t max_marks) {
+  return guarded([&] { e->p->profile(enable != 0, max_marks); });
+}
+
+int cft_engine_phase_totals(cft_engine* e, float* ms9, int64_t* counts9) {
+  return guarded([&] { e->p->phase_totals(ms9, counts9); });
+}
+
+int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq) {
+  return guarded([&] { e->p->wait_step(t, loss, gsq); });
+}
+
 }  // extern "C"

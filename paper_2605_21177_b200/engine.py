@@ -63,6 +63,9 @@ for _n, _r, _a in [
     ("cft_engine_transfer_events", C.c_int64, [C.c_void_p, _P(N.TransferEventC), C.c_int64]),
     ("cft_engine_chunk_counters", C.c_int, [C.c_void_p, C.c_void_p]),
     ("cft_engine_phase_ms", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("cft_engine_profile", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
+    ("cft_engine_phase_totals", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("cft_engine_wait_step", C.c_int, [C.c_void_p, C.c_int64, _P(C.c_double), _P(C.c_double)]),
 ]:
     _f = getattr(_L, _n)
     _f.restype = _r
@@ -321,6 +324,23 @@ class ChunkEngine:
         out = np.zeros(max(K, 1), np.uint64)
         N.check(_L.cft_engine_chunk_counters(self._h, out.ctypes.data))
         return out
+
+    PHASES = ("inputs", "fwd_gemm", "fwd_other", "loss", "wgrad", "dgrad", "bwd_other", "stats",
+              "update")
+
+    def profile(self, enable: bool = True, max_marks: int = 1 << 14):
+        N.check(_L.cft_engine_profile(self._h, int(enable), max_marks))
+
+    def phase_totals(self):
+        ms = np.zeros(9, np.float32)
+        cnt = np.zeros(9, np.int64)
+        N.check(_L.cft_engine_phase_totals(self._h, ms.ctypes.data, cnt.ctypes.data))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PHASES)}
+
+    def wait_step(self, t: int):
+        lo, gs = C.c_double(), C.c_double()
+        N.check(_L.cft_engine_wait_step(self._h, t, C.byref(lo), C.byref(gs)))
+        return lo.value, gs.value
 
     def phase_ms(self):
         out = np.zeros(4, np.float32)
