@@ -170,18 +170,23 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
   if (cfg_.dtype == CFT_F64)
     alloc(&scratch_, std::max<int64_t>(max_slice_, rows * std::max<int64_t>(max_width_, 1)) * 8);
   const Layer& first = layers_.front();
-  if (first.spec.type == kEmbedding) {
+  for (int k = 0; k < 2; ++k) {
     void* p;
-    alloc(&p, rows * std::max(1, first.spec.c) * sizeof(int32_t));
-    in_tokens_ = static_cast<int32_t*>(p);
-  } else {
-    alloc(&in_x_, rows * first.in_w * E);
+    if (first.spec.type == kEmbedding) {
+      alloc(&p, rows * std::max(1, first.spec.c) * sizeof(int32_t));
+      in_tokens_[k] = static_cast<int32_t*>(p);
+    } else {
+      alloc(&in_x_[k], rows * first.in_w * E);
+    }
+    alloc(&in_target_[k], rows * layers_.back().out_w * E);
+    alloc(&p, rows * sizeof(int32_t));
+    in_labels_[k] = static_cast<int32_t*>(p);
+    CFT_CUDA(cudaEventCreateWithFlags(&in_ready_[k], cudaEventDisableTiming));
+    CFT_CUDA(cudaEventCreateWithFlags(&in_free_[k], cudaEventDisableTiming));
   }
-  alloc(&in_target_, rows * layers_.back().out_w * E);
+  CFT_CUDA(cudaStreamCreateWithFlags(&in_stream_, cudaStreamNonBlocking));
   {
     void* p;
-    alloc(&p, rows * sizeof(int32_t));
-    in_labels_ = static_cast<int32_t*>(p);
     alloc(&p, static_cast<size_t>(std::max<int64_t>(cfg_.total_steps, 1)) * 4 * sizeof(double));
     stats_ = static_cast<double*>(p);
     alloc(&precond_, 2 * S);
@@ -334,6 +339,11 @@ Engine::~Engine() {
     if (e) cudaEventDestroy(e);
   if (step_done_) cudaEventDestroy(step_done_);
   if (h2d_) cudaStreamDestroy(h2d_);
+  if (in_stream_) cudaStreamDestroy(in_stream_);
+  for (int k = 0; k < 2; ++k) {
+    if (in_ready_[k]) cudaEventDestroy(in_ready_[k]);
+    if (in_free_[k]) cudaEventDestroy(in_free_[k]);
+  }
   if (d2h_) cudaStreamDestroy(d2h_);
   if (own_stream_) cudaStreamDestroy(stream_);
 }
@@ -427,31 +437,48 @@ void Engine::forward_backward(const Batch& b, int mb) {
   const Layer& last = layers_.back();
   const cudaMemcpyKind kind = b.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
 
-  // ---- inputs ----
+  // ---- inputs: device batches are consumed in place; host batches upload on in_stream_
+  // into staging buffer k (reusable once the step that last read it has finished) ----
   pb(kInputs);
   const void* x_in = nullptr;
   const int32_t* tok = nullptr;
-  if (first.spec.type == kEmbedding) {
-    CFT_CHECK(b.tokens != nullptr, "forward: token batch required");
-    const int64_t ntok = rows * std::max(1, first.spec.c);
-    CFT_CUDA(cudaMemcpyAsync(in_tokens_, b.tokens, ntok * 4, kind, s));
-    tok = in_tokens_;
-    layers::count_in_range(tok, ntok, 0, first.spec.a, reinterpret_cast<long long*>(flags_ + 1), s);
-  } else {
-    CFT_CHECK(b.x != nullptr, "forward: dense input required");
-    CFT_CUDA(cudaMemcpyAsync(in_x_, b.x, rows * first.in_w * E, kind, s));
-    x_in = in_x_;
-  }
   const void* target = nullptr;
-  if (cfg_.loss == 1 || cfg_.loss == 2) {
-    CFT_CHECK(b.target != nullptr, "loss: target shape mismatch");
-    CFT_CUDA(cudaMemcpyAsync(in_target_, b.target, rows * last.out_w * E, kind, s));
-    target = in_target_;
+  const int32_t* labels = nullptr;
+  const bool need_target = cfg_.loss == 1 || cfg_.loss == 2;
+  if (first.spec.type == kEmbedding) CFT_CHECK(b.tokens != nullptr, "forward: token batch required");
+  else CFT_CHECK(b.x != nullptr, "forward: dense input required");
+  if (need_target) CFT_CHECK(b.target != nullptr, "loss: target shape mismatch");
+  if (cfg_.loss == 3) CFT_CHECK(b.labels != nullptr, "loss: label count mismatch");
+  const int64_t ntok = rows * std::max(1, first.spec.c);
+  if (b.on_device) {
+    x_in = b.x;
+    tok = b.tokens;
+    target = b.target;
+    labels = b.labels;
+  } else {
+    const int k = static_cast<int>(uploads_++ & 1);
+    CFT_CUDA(cudaStreamWaitEvent(in_stream_, in_free_[k], 0));
+    if (first.spec.type == kEmbedding) {
+      CFT_CUDA(cudaMemcpyAsync(in_tokens_[k], b.tokens, ntok * 4, kind, in_stream_));
+      tok = in_tokens_[k];
+    } else {
+      CFT_CUDA(cudaMemcpyAsync(in_x_[k], b.x, rows * first.in_w * E, kind, in_stream_));
+      x_in = in_x_[k];
+    }
+    if (need_target) {
+      CFT_CUDA(cudaMemcpyAsync(in_target_[k], b.target, rows * last.out_w * E, kind, in_stream_));
+      target = in_target_[k];
+    }
+    if (cfg_.loss == 3) {
+      CFT_CUDA(cudaMemcpyAsync(in_labels_[k], b.labels, rows * 4, kind, in_stream_));
+      labels = in_labels_[k];
+    }
+    CFT_CUDA(cudaEventRecord(in_ready_[k], in_stream_));
+    CFT_CUDA(cudaStreamWaitEvent(s, in_ready_[k], 0));
+    staged_slot_ = k;
   }
-  if (cfg_.loss == 3) {
-    CFT_CHECK(b.labels != nullptr, "loss: label count mismatch");
-    CFT_CUDA(cudaMemcpyAsync(in_labels_, b.labels, rows * 4, kind, s));
-  }
+  if (first.spec.type == kEmbedding)
+    layers::count_in_range(tok, ntok, 0, first.spec.a, reinterpret_cast<long long*>(flags_ + 1), s);
   pe();
   if (mb == 0) CFT_CUDA(cudaEventRecord(ev_[1], s));
 
@@ -509,14 +536,14 @@ void Engine::forward_backward(const Batch& b, int mb) {
   void* dy = act_[0];
   if (dt == CFT_F64)
     layers::loss_f64(cfg_.loss, static_cast<const double*>(y_out_), static_cast<const double*>(target),
-                     in_labels_, rows, last.out_w, static_cast<double*>(dy), loss_acc,
+                     labels, rows, last.out_w, static_cast<double*>(dy), loss_acc,
                      static_cast<double*>(scratch_), flags_, s);
   else if (dt == CFT_F32)
     layers::loss<float>(cfg_.loss, static_cast<const float*>(y_out_), static_cast<const float*>(target),
-                        in_labels_, rows, last.out_w, static_cast<float*>(dy), loss_acc, flags_, s);
+                        labels, rows, last.out_w, static_cast<float*>(dy), loss_acc, flags_, s);
   else
     layers::loss<__nv_bfloat16>(cfg_.loss, static_cast<const __nv_bfloat16*>(y_out_),
-                                static_cast<const __nv_bfloat16*>(target), in_labels_, rows,
+                                static_cast<const __nv_bfloat16*>(target), labels, rows,
                                 last.out_w, static_cast<__nv_bfloat16*>(dy), loss_acc, flags_, s);
 
   pe();
@@ -639,6 +666,10 @@ void Engine::forward_backward(const Batch& b, int mb) {
     cur ^= 1;
   }
   (void)E;
+  if (staged_slot_ >= 0) {
+    CFT_CUDA(cudaEventRecord(in_free_[staged_slot_], s));
+    staged_slot_ = -1;
+  }
   ++mb_done_;
   if (mb == 0) CFT_CUDA(cudaEventRecord(ev_[3], s));
 }

@@ -154,10 +154,17 @@ class Engine {
   void* y_out_ = nullptr;
   void* aux_ = nullptr;
   void* scratch_ = nullptr;  // fp64 path: per-micro-batch slice grad / loss partials
-  void* in_x_ = nullptr;
-  void* in_target_ = nullptr;
-  int32_t* in_tokens_ = nullptr;
-  int32_t* in_labels_ = nullptr;
+  // double-buffered input staging: host batches upload on in_stream_ while the previous
+  // step computes; buffer b is reused only after the step that read it has finished
+  void* in_x_[2] = {nullptr, nullptr};
+  void* in_target_[2] = {nullptr, nullptr};
+  int32_t* in_tokens_[2] = {nullptr, nullptr};
+  int32_t* in_labels_[2] = {nullptr, nullptr};
+  cudaStream_t in_stream_ = nullptr;
+  cudaEvent_t in_ready_[2] = {nullptr, nullptr};
+  cudaEvent_t in_free_[2] = {nullptr, nullptr};
+  int64_t uploads_ = 0;
+  int staged_slot_ = -1;
   double* stats_ = nullptr;       // [step-ring][4]: sumsq, nonfinite, first_bad, loss
   void* precond_ = nullptr;
   void* consts_ = nullptr;        // reset template for the per-step stats / precond cells

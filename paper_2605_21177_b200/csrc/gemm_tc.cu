@@ -53,11 +53,12 @@ struct Cfg {
 };
 
 __device__ __forceinline__ void decode_unit(const Args& a, int u, int& tm, int& tn, int& sp) {
-  // split-major so consecutive CTAs share the same output tile's operands in L2
+  // splits fastest, then N, then M: the CTAs of one wave cover ~148/tiles_n row-blocks of A
+  // across all column blocks, so A streams from HBM once and B (the weight) stays L2-resident.
   sp = u % a.splits;
   const int t = u / a.splits;
-  tm = t % a.tiles_m;
-  tn = t / a.tiles_m;
+  tn = t % a.tiles_n;
+  tm = t / a.tiles_n;
 }
 
 template <bool A_MN, bool B_MN, int BN>

@@ -162,3 +162,17 @@ def test_nonfinite_gradient_is_rejected_without_advancing(cuda):
     with pytest.raises(Error, match=r"step 1, chunk 1: (non-finite loss|step: non-finite gradient)"):
         eng.step([eng.stage(bad, device=True)])
     assert eng.chunk_counters()[1] == 0
+
+
+@pytest.mark.parametrize("name", ["linear_exact", "emb_ln_mb"])
+def test_host_batches_match_device_batches(cuda, name):
+    """Pinned-host batches go through the double-buffered upload stream; results must be
+    bit-identical to device-resident batches (fp64 path)."""
+    from paper_2605_21177_b200.engine import run_training
+    case = CASES[name]
+    a = run_training(model_of(case), np.array(case["init_params"]), batches_of(case),
+                     options_of(case, "fp64"), device_inputs=True)
+    b = run_training(model_of(case), np.array(case["init_params"]), batches_of(case),
+                     options_of(case, "fp64"), device_inputs=False)
+    assert np.array_equal(a.params, b.params)
+    assert np.array_equal(a.loss, b.loss)
