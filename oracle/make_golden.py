@@ -152,6 +152,9 @@ TRAIN_CASES = [
     # pure linear + half_sq: the fp64 GPU path is bit-identical here
     dict(name="linear_exact", layers=[("linear", 32, 24, True), ("linear", 24, 8, False)],
          loss="half_sq", rows=12, nb=3, K=3, T=1, steps=9),
+    # data-parallel oracle: micro_batches = 2 stands for world = 2 (trainer.cpp:45-58)
+    dict(name="linear_dp2", layers=[("linear", 16, 12, True), ("linear", 12, 8, False)],
+         loss="half_sq", rows=5, nb=12, K=3, T=1, steps=6, micro_batches=2),
     # byte-budget plan with a layernorm in the middle
     dict(name="budget_ln", layers=[("linear", 16, 16, True), ("layernorm", 16), ("linear", 16, 4, False)],
          loss="squared", rows=10, nb=4, budget=2000, T=3, steps=12),

@@ -1,0 +1,157 @@
+"""Data-parallel path on CPU: world size 2 over gloo (127.0.0.1).
+
+The DP driver (paper_2605_21177_b200/dp.py) runs the chunk-local step with the product's host
+planner/scheduler and a CPU stand-in engine whose arithmetic is the oracle's (fp64, reference
+order).  Rank r consumes the batch the reference's micro-batch r would (trainer.cpp:45-58); the
+all-reduced, 1/world-scaled gradient must reproduce the reference run with micro_batches = 2
+(golden `linear_dp2`, generated from the reference library) bit for bit.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import lib as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "train.json")
+
+
+class OracleEngine:
+    """CPU stand-in with the engine's step API (Linear layers + half_sq only)."""
+
+    def __init__(self, layers, params, plan, sched, hyper, micro_batches):
+        from paper_2605_21177_b200 import plan as P  # noqa: F401  (product host code)
+        self.layers = layers
+        self.tensors = []  # (layer, kind, rows, cols, offset)
+        off = 0
+        for li, L in enumerate(layers):
+            self.tensors.append((li, "w", L[2], L[1], off))
+            off += L[2] * L[1]
+            if L[3]:
+                self.tensors.append((li, "b", L[2], 1, off))
+                off += L[2]
+        self.params = np.array(params, dtype=np.float64)
+        self.plan, self.sched, self.hyper, self.mb = plan, sched, hyper, micro_batches
+        self.scale = 1.0
+        K = plan.K
+        self.n = [0] * K
+        self.state = []
+        for c in range(K):
+            master = np.concatenate([self._slice_vals(s) for s in plan.chunks[c].slices])
+            self.state.append([master, np.zeros_like(master), np.zeros_like(master)])
+
+    def _slice_vals(self, s):
+        _, _, r, c, off = self.tensors[s.tensor_id]
+        return self.params[off + s.row_begin * c: off + s.row_end * c].copy()
+
+    def set_grad_scale(self, s):
+        self.scale = s
+
+    def step_begin(self):
+        self.active = self.sched.step_begin()
+        n = self.plan.chunks[self.active].elements
+        self.grad = torch.zeros(n, dtype=torch.float64)
+        return self.active
+
+    def forward_backward(self, batch, mb):
+        xs = [batch["x"]]
+        for li, L in enumerate(self.layers):
+            w = self._w(li)
+            b = self._b(li)
+            xs.append(O.linear_forward(xs[-1], w, b))
+        loss, dy = O.eval_loss("half_sq", xs[-1], target=batch["target"])
+        offs = {}
+        o = 0
+        for s in self.plan.chunks[self.active].slices:
+            offs[s.tensor_id] = (s, o)
+            o += s.row_count() * self.tensors[s.tensor_id][3]
+        g = self.grad.numpy()
+        for li in reversed(range(len(self.layers))):
+            for tid, (li2, kind, r, c, off) in enumerate(self.tensors):
+                if li2 != li or tid not in offs:
+                    continue
+                s, ao = offs[tid]
+                if kind == "w":
+                    part = O.linear_dweight(dy, xs[li], s.row_begin, s.row_end).ravel()
+                else:
+                    part = O.linear_dbias(dy, s.row_begin, s.row_end)
+                g[ao: ao + part.size] += part
+            dy = O.linear_dinput(dy, self._w(li))
+        return loss
+
+    def _w(self, li):
+        for (l2, kind, r, c, off) in self.tensors:
+            if l2 == li and kind == "w":
+                return self.params[off: off + r * c].reshape(r, c)
+
+    def _b(self, li):
+        for (l2, kind, r, c, off) in self.tensors:
+            if l2 == li and kind == "b":
+                return self.params[off: off + r]
+        return None
+
+    def grad_tensor(self):
+        return self.grad
+
+    def step_end(self):
+        c = self.active
+        mean = self.grad.numpy() * (self.scale * (1.0 / self.mb))
+        h = self.hyper
+        master, m, v, self.n[c], _, _ = O.adamw(*self.state[c], mean, self.n[c], *h)
+        self.state[c] = [master, m, v]
+        o = 0
+        for s in self.plan.chunks[c].slices:
+            _, _, r, cols, off = self.tensors[s.tensor_id]
+            k = s.row_count() * cols
+            self.params[off + s.row_begin * cols: off + s.row_begin * cols + k] = master[o: o + k]
+            o += k
+        self.sched.step_end()
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_21177_b200 import plan as P
+        from paper_2605_21177_b200.dp import DataParallelStep
+        case = {c["name"]: c for c in json.load(open(GOLD))}["linear_dp2"]
+        layers = case["layers"]
+        tensors = []
+        for li, L in enumerate(layers):
+            tensors.append((f"linear{li}.weight", L[2], L[1]))
+            if L[3]:
+                tensors.append((f"linear{li}.bias", L[2], 1))
+        infos = [P.TensorInfo(i, n, r, c) for i, (n, r, c) in enumerate(tensors)]
+        plan = P.partition(infos, case["K"])
+        sched = P.RotationScheduler(P.ScheduleConfig(case["K"], case["T"], case["steps"]), plan)
+        eng = OracleEngine(layers, case["init_params"], plan, sched, tuple(case["hyper"]), 1)
+        step = DataParallelStep(eng)
+        batches = [{k: np.asarray(v) for k, v in b.items()} for b in case["batches"]]
+        cursor = 0
+        chunks = []
+        for t in range(case["steps"]):
+            # rank r takes micro-batch r of the reference's step t
+            b = batches[(cursor + rank) % len(batches)]
+            cursor = (cursor + world) % len(batches)
+            chunks.append(step.step([b]))
+        out[rank] = (eng.params.tolist(), chunks)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dp_world2_matches_reference_micro_batches():
+    case = {c["name"]: c for c in json.load(open(GOLD))}["linear_dp2"]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = 29500 + (os.getpid() % 2000)
+    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    p0, c0 = out[0]
+    p1, c1 = out[1]
+    assert c0 == c1 == case["traj_chunk"]
+    assert p0 == p1  # replicas stay identical
+    assert np.array_equal(np.array(p0), np.array(case["final_params"]))

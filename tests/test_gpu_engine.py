@@ -176,3 +176,37 @@ def test_host_batches_match_device_batches(cuda, name):
                      options_of(case, "fp64"), device_inputs=False)
     assert np.array_equal(a.params, b.params)
     assert np.array_equal(a.loss, b.loss)
+
+
+def test_engine_dp_exchange_matches_reference_micro_batches(cuda):
+    """The engine's data-parallel API (step_begin / forward_backward / grad buffer / step_end,
+    grad_scale = 1/world) with the all-reduce done by summing the two replicas' buffers:
+    bit-identical to the reference with micro_batches = 2 (fp64 path)."""
+    from paper_2605_21177_b200.engine import ChunkEngine
+    case = CASES["linear_dp2"]
+    opts = options_of(case, "fp64")
+    opts.micro_batches = 1
+    engs = [ChunkEngine(model_of(case), np.array(case["init_params"]), 5, opts) for _ in range(2)]
+    for e in engs:
+        e.set_grad_scale(0.5)
+    bs = batches_of(case)
+    staged = [[e.stage(b, device=True) for b in bs] for e in engs]
+    cursor = 0
+    for t in range(case["steps"]):
+        for r, e in enumerate(engs):
+            e.step_begin()
+            e.forward_backward(staged[r][(cursor + r) % len(bs)], 0)
+        cursor = (cursor + 2) % len(bs)
+        torch.cuda.synchronize()
+        g0, g1 = engs[0].grad_tensor(), engs[1].grad_tensor()
+        s = g0 + g1
+        g0.copy_(s)
+        g1.copy_(s)
+        torch.cuda.synchronize()
+        for e in engs:
+            e.step_end()
+    for e in engs:
+        e.finish()
+    p0, p1 = engs[0].params(), engs[1].params()
+    assert np.array_equal(p0, p1)
+    assert np.array_equal(p0, np.array(case["final_params"]))
