@@ -251,6 +251,10 @@ int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t
                   const cft_segment* segments_dev, int32_t n_segments, const void* stats_dev,
                   cft_stream_t stream);
 
+/* bf16 GEMM tiling policy: 0 auto (CTA-pair 256x256 tcgen05 tiles when the tile space fills
+ * the chip, single-CTA 128x256 otherwise), 1 force single-CTA, 2 force CTA pairs. */
+int cft_set_gemm_policy(int policy);
+
 /* Element conversion (e.g. fp32 master -> bf16 params at init). */
 int cft_convert(cft_dtype src_dtype, const void* src, cft_dtype dst_dtype, void* dst, int64_t n,
                 cft_stream_t stream);

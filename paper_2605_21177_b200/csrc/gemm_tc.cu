@@ -61,6 +61,74 @@ __device__ __forceinline__ void decode_unit(const Args& a, int u, int& tm, int& 
   tm = t / a.tiles_n;
 }
 
+// Epilogue store of 16 consecutive accumulator columns of one output row (one thread).
+__device__ __forceinline__ void store16(const Args& args, long long rbase, int col,
+                                        const uint32_t (&r)[16]) {
+  const bool full16 = col + 16 <= args.N;
+  if (args.epi >= kEpiF32) {
+    float* out = static_cast<float*>(args.C) + rbase + col;
+    const bool vec = full16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    if (vec) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        const float a0 = __uint_as_float(r[j]), a1 = __uint_as_float(r[j + 1]);
+        const float a2 = __uint_as_float(r[j + 2]), a3 = __uint_as_float(r[j + 3]);
+        float4* p = reinterpret_cast<float4*>(out + j);
+        if (args.epi == kEpiF32Red) {
+          ptx::red_add_v4(out + j, a0, a1, a2, a3);
+        } else if (args.epi == kEpiF32Add) {
+          float4 o = *p;
+          *p = make_float4(o.x + a0, o.y + a1, o.z + a2, o.w + a3);
+        } else {
+          *p = make_float4(a0, a1, a2, a3);
+        }
+      }
+    } else {
+      for (int j = 0; j < 16 && col + j < args.N; ++j) {
+        const float a0 = __uint_as_float(r[j]);
+        if (args.epi == kEpiF32Red) atomicAdd(out + j, a0);
+        else if (args.epi == kEpiF32Add) out[j] += a0;
+        else out[j] = a0;
+      }
+    }
+  } else {
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.C) + rbase + col;
+    const bool vec = full16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    if (vec) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 8) {
+        uint4 pk;
+        uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+        if (args.epi == kEpiBf16Add) {
+          const uint4 old = *reinterpret_cast<const uint4*>(out + j);
+          const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 of = __bfloat1622float2(o2[q]);
+            __nv_bfloat162 v = __floats2bfloat162_rn(of.x + __uint_as_float(r[j + 2 * q]),
+                                                     of.y + __uint_as_float(r[j + 2 * q + 1]));
+            w[q] = *reinterpret_cast<uint32_t*>(&v);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[j + 2 * q]),
+                                                     __uint_as_float(r[j + 2 * q + 1]));
+            w[q] = *reinterpret_cast<uint32_t*>(&v);
+          }
+        }
+        *reinterpret_cast<uint4*>(out + j) = pk;
+      }
+    } else {
+      for (int j = 0; j < 16 && col + j < args.N; ++j) {
+        float a0 = __uint_as_float(r[j]);
+        if (args.epi == kEpiBf16Add) a0 += __bfloat162float(out[j]);
+        out[j] = __float2bfloat16_rn(a0);
+      }
+    }
+  }
+}
+
 template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -196,70 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_ld16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c, r);
         ptx::tmem_wait_ld();
         const int col = tn * BN + c;
-        if (!row_ok || col >= args.N) continue;
-        const bool full16 = col + 16 <= args.N;
-        if (args.epi >= kEpiF32) {
-          float* out = static_cast<float*>(args.C) + rbase + col;
-          const bool vec = full16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-          if (vec) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              const float a0 = __uint_as_float(r[j]), a1 = __uint_as_float(r[j + 1]);
-              const float a2 = __uint_as_float(r[j + 2]), a3 = __uint_as_float(r[j + 3]);
-              float4* p = reinterpret_cast<float4*>(out + j);
-              if (args.epi == kEpiF32Red) {
-                ptx::red_add_v4(out + j, a0, a1, a2, a3);
-              } else if (args.epi == kEpiF32Add) {
-                float4 o = *p;
-                *p = make_float4(o.x + a0, o.y + a1, o.z + a2, o.w + a3);
-              } else {
-                *p = make_float4(a0, a1, a2, a3);
-              }
-            }
-          } else {
-            for (int j = 0; j < 16 && col + j < args.N; ++j) {
-              const float a0 = __uint_as_float(r[j]);
-              if (args.epi == kEpiF32Red) atomicAdd(out + j, a0);
-              else if (args.epi == kEpiF32Add) out[j] += a0;
-              else out[j] = a0;
-            }
-          }
-        } else {
-          __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.C) + rbase + col;
-          const bool vec = full16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-          if (vec) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 8) {
-              uint4 pk;
-              uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
-              if (args.epi == kEpiBf16Add) {
-                const uint4 old = *reinterpret_cast<const uint4*>(out + j);
-                const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&old);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float2 of = __bfloat1622float2(o2[q]);
-                  __nv_bfloat162 v = __floats2bfloat162_rn(of.x + __uint_as_float(r[j + 2 * q]),
-                                                           of.y + __uint_as_float(r[j + 2 * q + 1]));
-                  w[q] = *reinterpret_cast<uint32_t*>(&v);
-                }
-              } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[j + 2 * q]),
-                                                           __uint_as_float(r[j + 2 * q + 1]));
-                  w[q] = *reinterpret_cast<uint32_t*>(&v);
-                }
-              }
-              *reinterpret_cast<uint4*>(out + j) = pk;
-            }
-          } else {
-            for (int j = 0; j < 16 && col + j < args.N; ++j) {
-              float a0 = __uint_as_float(r[j]);
-              if (args.epi == kEpiBf16Add) a0 += __bfloat162float(out[j]);
-              out[j] = __float2bfloat16_rn(a0);
-            }
-          }
-        }
+        if (row_ok && col < args.N) store16(args, rbase, col, r);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -274,6 +279,184 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C_::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a 256 x 256 tile
+// with M = 256 UMMAs issued by the leader.  Each CTA stages only its 128 rows of A and its
+// 128 columns of B per k-block (32 KB instead of 48 KB), so 6 stages fit in 192 KB and the
+// L2 -> SM operand traffic per FLOP drops by a third.  Each CTA's TMEM holds its 128 rows of
+// the accumulator (x2 buffers = 512 columns); both epilogues release the leader's TMEM slot.
+
+template <int BNP>  // pair tile N: 256 (dense GEMMs) or 128 (narrow wgrad slices)
+struct PairCfg {
+  static constexpr int STAGES = BNP == 256 ? 6 : 8;
+  static constexpr uint32_t A_BYTES = 128 * BK * 2;        // this CTA's 128 rows of A
+  static constexpr uint32_t B_BYTES = (BNP / 2) * BK * 2;  // this CTA's BNP/2 columns of B
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t TMEM_COLS = 2 * BNP;
+  static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+template <bool A_MN, bool B_MN, int BNP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                         const __grid_constant__ CUtensorMap tmap_b, const Args args) {
+  using P_ = PairCfg<BNP>;
+  constexpr int kPairStages = P_::STAGES;
+  constexpr uint32_t kPairABytes = P_::A_BYTES;
+  constexpr uint32_t kPairBBytes = P_::B_BYTES;
+  constexpr uint32_t kPairStageBytes = P_::STAGE_BYTES;
+  constexpr int BMP = 256;  // pair tile M (each CTA owns 128 rows)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kPairStages * kPairABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kPairStages * kPairBBytes);
+  uint64_t* empty = full + kPairStages;
+  uint64_t* tfull = empty + kPairStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x / 2;
+  const int npairs = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmap_a);
+    ptx::tma_prefetch(&tmap_b);
+    for (int s = 0; s < kPairStages; ++s) {
+      ptx::mbar_init(&full[s], 1);   // leader's expect_tx; both CTAs' TMA bytes complete it
+      ptx::mbar_init(&empty[s], 1);  // the leader's multicast commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (used on the leader)
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc_2sm<P_::TMEM_COLS>(tslot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < args.num_units; u += npairs) {
+        int tm, tn, sp;
+        decode_unit(args, u, tm, tn, sp);
+        const int kb0 = sp * args.kb_per_split;
+        const int kb1 = min(kb0 + args.kb_per_split, args.total_kb);
+        const int m0 = args.m_off + tm * BMP + static_cast<int>(rank) * 128;
+        const int n0 = tn * BNP + static_cast<int>(rank) * (BNP / 2);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) ptx::mbar_expect_tx(&full[stage], 2 * kPairStageBytes);
+          const int k0 = kb * BK;
+          uint8_t* da = sa + stage * kPairABytes;
+          uint8_t* db = sb + stage * kPairBBytes;
+          if constexpr (A_MN) {
+            ptx::tma_load_2d_2sm(da, &tmap_a, &full[stage], m0, k0);
+            ptx::tma_load_2d_2sm(da + BK * 128, &tmap_a, &full[stage], m0 + 64, k0);
+          } else {
+            ptx::tma_load_2d_2sm(da, &tmap_a, &full[stage], k0, m0);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BNP / 128; ++j)
+              ptx::tma_load_2d_2sm(db + j * (BK * 128), &tmap_b, &full[stage], n0 + 64 * j, k0);
+          } else {
+            ptx::tma_load_2d_2sm(db, &tmap_b, &full[stage], k0, n0);
+          }
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BMP, BNP, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = pair; u < args.num_units; u += npairs) {
+        int tm, tn, sp;
+        decode_unit(args, u, tm, tn, sp);
+        const int kb0 = sp * args.kb_per_split;
+        const int kb1 = min(kb0 + args.kb_per_split, args.total_kb);
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BNP;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(sa + stage * kPairABytes);
+          const uint32_t b_base = ptx::smem_u32(sb + stage * kPairBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t adesc = A_MN ? ptx::smem_desc_sw128(a_base + k * 2048, BK * 128, 1024)
+                                        : ptx::smem_desc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(b_base + k * 2048, BK * 128, 1024)
+                                        : ptx::smem_desc_sw128(b_base + k * 32, 16, 1024);
+            ptx::umma_bf16_2sm(d_tmem, adesc, bdesc, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          ptx::umma_commit_2sm(&empty[stage], 0x3);
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit_2sm(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const uint32_t tempty_leader[2] = {ptx::mapa(ptx::smem_u32(&tempty[0]), 0),
+                                       ptx::mapa(ptx::smem_u32(&tempty[1]), 0)};
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = pair; u < args.num_units; u += npairs) {
+      int tm, tn, sp;
+      decode_unit(args, u, tm, tn, sp);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = tm * BMP + static_cast<int>(rank) * 128 + quarter * 32 + lane - args.row_skip;
+      const bool row_ok = row >= 0 && row < args.M;
+      const long long rbase = static_cast<long long>(row) * args.ldc;
+#pragma unroll 1
+      for (int c = 0; c < BNP; c += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BNP + c, r);
+        ptx::tmem_wait_ld();
+        const int col = tn * BNP + c;
+        if (row_ok && col < args.N) store16(args, rbase, col, r);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm<P_::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -321,22 +504,20 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream_t s
   check_launch("gemm_bf16_kernel");
 }
 
-// Choose the number of K splits for a small tile space.  Cost model (per CTA wave):
-// one 128xBN x 64 k-block costs ~0.45 us per CTA at BN=256 (measured: 1.27 PFLOP/s over
-// 148 SMs in the dense forward), and split partials cost a zero-fill plus s fp32
-// red-adds of the output through L2 (~2 TB/s measured for red.global.add.v4.f32).
-int choose_splits(int tiles, int total_kb, long long out_elems, int BN, bool allow) {
-  if (!allow) return 1;
-  const int sms = num_sms();
-  if (tiles >= sms) return 1;
-  const double us_per_kb = 0.45 * BN / 256.0;
+// Choose the number of K splits for a small tile space.  Cost model (per wave of `slots`
+// concurrent tile workers): one k-block of a 128x256 tile costs ~0.45 us per SM (measured:
+// 1.27 PFLOP/s over 148 SMs in the dense forward), and split partials cost a zero-fill plus
+// s fp32 red-adds of the output through L2 (~2 TB/s measured for red.global.add.v4.f32).
+int choose_splits(int tiles, int slots, int total_kb, long long out_elems, double us_per_kb,
+                  bool allow) {
+  if (!allow || tiles >= slots) return 1;
   double best_t = 1e30;
   int best = 1;
   for (int s = 1; s <= 16; ++s) {
     const int kbps = (total_kb + s - 1) / s;
     if (s > 1 && kbps < 4) break;
     const int units = tiles * s;
-    const int waves = (units + sms - 1) / sms;
+    const int waves = (units + slots - 1) / slots;
     double t = waves * kbps * us_per_kb;
     if (s > 1) t += (s + 1) * out_elems * 4.0 / 2.0e6;
     if (t < best_t * 0.97) {
@@ -347,27 +528,46 @@ int choose_splits(int tiles, int total_kb, long long out_elems, int BN, bool all
   return best;
 }
 
-void fill_units(Args& a, int BN, bool allow_split) {
-  a.tiles_m = (a.M + a.row_skip + BM - 1) / BM;
-  a.tiles_n = (a.N + BN - 1) / BN;
+void fill_units(Args& a, int bm, int bn, int slots, double us_per_kb, bool allow_split) {
+  a.tiles_m = (a.M + a.row_skip + bm - 1) / bm;
+  a.tiles_n = (a.N + bn - 1) / bn;
   a.total_kb = (a.K + BK - 1) / BK;
   const int tiles = a.tiles_m * a.tiles_n;
-  int s = choose_splits(tiles, a.total_kb, static_cast<long long>(a.M) * a.N, BN, allow_split);
+  const int s = choose_splits(tiles, slots, a.total_kb, static_cast<long long>(a.M) * a.N,
+                              us_per_kb, allow_split);
   a.kb_per_split = (a.total_kb + s - 1) / s;
   a.splits = (a.total_kb + a.kb_per_split - 1) / a.kb_per_split;
   a.num_units = tiles * a.splits;
 }
 
-bool tc_ok(int64_t inner_dim, const void* p) {
-  return (inner_dim % 8) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+template <bool A_MN, bool B_MN, int BNP>
+void launch_2sm(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream_t stream) {
+  auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN, BNP>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    CFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(PairCfg<BNP>::SMEM)));
+    attr_done = true;
+  }
+  const int pairs = std::min(a.num_units, num_sms() / 2);
+  kern<<<2 * pairs, kThreads, PairCfg<BNP>::SMEM, stream>>>(ta, tb, a);
+  check_launch("gemm_bf16_2sm_kernel");
+}
+
+int g_policy = 0;  // 0 auto, 1 force 1-SM tiles, 2 force CTA-pair tiles
+
+// CTA pairs when the 256x256 tile space fills the chip; 128xBN single-CTA tiles otherwise.
+bool use_pairs(int M, int N, int K, bool allow_split) {
+  if (g_policy == 1) return false;
+  if (g_policy == 2) return N >= 128;
+  if (N < 256 || K < 256) return false;
+  const int pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  return pair_tiles >= num_sms() / 2 || (allow_split && pair_tiles * 4 >= num_sms() / 2);
 }
 
 }  // namespace
 
-// Usability predicate (TMA: 16-byte aligned base and row strides).
-bool linear_shapes_ok(const void* x, const void* w, int64_t in_dim, int64_t out_dim) {
-  return tc_ok(in_dim, x) && tc_ok(in_dim, w) && (out_dim % 8) == 0;
-}
+void set_policy(int p) { g_policy = p; }
 
 // Y = X W^T, bf16 out (epi kEpiBf16) -- forward.
 void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
@@ -379,14 +579,17 @@ void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int
   a.C = y;
   a.ldc = out_dim;
   a.epi = kEpiBf16;
-  const int BN = out_dim >= 256 ? 256 : 128;
   const CUtensorMap ta = cached_map(x, in_dim, n_tok, in_dim, 64, BM);
-  if (BN == 256) {
-    fill_units(a, 256, false);
+  if (use_pairs(a.M, a.N, a.K, false)) {
+    fill_units(a, 256, 256, num_sms() / 2, 0.45, false);
+    const CUtensorMap tb = cached_map(w, in_dim, out_dim, in_dim, 64, 128);
+    launch_2sm<false, false, 256>(ta, tb, a, stream);
+  } else if (out_dim >= 256) {
+    fill_units(a, BM, 256, num_sms(), 0.45, false);
     const CUtensorMap tb = cached_map(w, in_dim, out_dim, in_dim, 64, 256);
     launch<false, false, 256>(ta, tb, a, stream);
   } else {
-    fill_units(a, 128, false);
+    fill_units(a, BM, 128, num_sms(), 0.225, false);
     const CUtensorMap tb = cached_map(w, in_dim, out_dim, in_dim, 64, 128);
     launch<false, false, 128>(ta, tb, a, stream);
   }
@@ -404,11 +607,14 @@ void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w,
   a.epi = beta ? kEpiBf16Add : kEpiBf16;
   const CUtensorMap ta = cached_map(dy, out_dim, n_tok, out_dim, 64, BM);
   const CUtensorMap tb = cached_map(w, in_dim, out_dim, in_dim, 64, 64);
-  if (in_dim >= 256) {
-    fill_units(a, 256, false);
+  if (use_pairs(a.M, a.N, a.K, false)) {
+    fill_units(a, 256, 256, num_sms() / 2, 0.45, false);
+    launch_2sm<false, true, 256>(ta, tb, a, stream);
+  } else if (in_dim >= 256) {
+    fill_units(a, BM, 256, num_sms(), 0.45, false);
     launch<false, true, 256>(ta, tb, a, stream);
   } else {
-    fill_units(a, 128, false);
+    fill_units(a, BM, 128, num_sms(), 0.225, false);
     launch<false, true, 128>(ta, tb, a, stream);
   }
 }
@@ -429,8 +635,30 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   a.ldc = in_dim;
   const CUtensorMap ta = cached_map(dy, out_dim, n_tok, out_dim, 64, 64);
   const CUtensorMap tb = cached_map(x, in_dim, n_tok, in_dim, 64, 64);
+  // Candidate tilings for the (usually narrow) slice: CTA-pair 256x256 or 256x128 tiles, or
+  // single-CTA 128xBN tiles; each with its best split count under the cost model.
+  const bool pairs = use_pairs(a.M, a.N, a.K, true);
   const int BN = in_dim >= 256 ? 256 : 128;
-  fill_units(a, BN, true);
+  int pair_bn = 256;
+  if (pairs) {
+    Args a256 = a, a128 = a;
+    fill_units(a256, 256, 256, num_sms() / 2, 0.40, true);
+    fill_units(a128, 256, 128, num_sms() / 2, 0.21, true);
+    auto cost = [](const Args& x, double us_per_kb) {
+      const int waves = (x.num_units + num_sms() / 2 - 1) / (num_sms() / 2);
+      double t = waves * x.kb_per_split * us_per_kb;
+      if (x.splits > 1) t += (x.splits + 1) * static_cast<double>(x.M) * x.N * 4.0 / 2.0e6;
+      return t;
+    };
+    if (g_policy == 0 && cost(a128, 0.21) < cost(a256, 0.40)) {
+      a = a128;
+      pair_bn = 128;
+    } else {
+      a = a256;
+    }
+  } else {
+    fill_units(a, BM, BN, num_sms(), 0.45 * BN / 256.0, true);
+  }
   if (a.splits > 1) {
     // Partial sums race into dw: zero first unless accumulating.
     if (!accumulate)
@@ -440,8 +668,15 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   } else {
     a.epi = accumulate ? kEpiF32Add : kEpiF32;
   }
-  if (BN == 256) launch<true, true, 256>(ta, tb, a, stream);
+  if (pairs && pair_bn == 128) launch_2sm<true, true, 128>(ta, tb, a, stream);
+  else if (pairs) launch_2sm<true, true, 256>(ta, tb, a, stream);
+  else if (BN == 256) launch<true, true, 256>(ta, tb, a, stream);
   else launch<true, true, 128>(ta, tb, a, stream);
 }
 
 }  // namespace cft::tc
+
+extern "C" int cft_set_gemm_policy(int policy) {
+  cft::tc::set_policy(policy);
+  return CFT_OK;
+}

@@ -34,6 +34,17 @@ def bf16_round(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(torch.float64).numpy()
 
 
+@pytest.fixture(params=[0, 1, 2], ids=["auto", "single_cta", "cta_pair"])
+def gemm_policy(request):
+    """Run the bf16 tests under each tcgen05 tiling: auto, 128xBN single-CTA, 256x256 pairs."""
+    import ctypes
+    from paper_2605_21177_b200 import _native as N
+    N.lib.cft_set_gemm_policy.argtypes = [ctypes.c_int]
+    N.lib.cft_set_gemm_policy(request.param)
+    yield request.param
+    N.lib.cft_set_gemm_policy(0)
+
+
 SHAPES = [  # (n_tok, in_dim, out_dim, rb, re)
     (256, 256, 384, 0, 128),
     (384, 512, 512, 37, 301),       # unaligned row_begin, ragged |S|
@@ -43,7 +54,7 @@ SHAPES = [  # (n_tok, in_dim, out_dim, rb, re)
 
 
 @pytest.mark.parametrize("n_tok,in_dim,out_dim,rb,re", SHAPES)
-def test_bf16_wgrad_slice_vs_oracle(cuda, n_tok, in_dim, out_dim, rb, re):
+def test_bf16_wgrad_slice_vs_oracle(cuda, gemm_policy, n_tok, in_dim, out_dim, rb, re):
     from paper_2605_21177_b200 import ops
     dy = bf16_round(rnd((n_tok, out_dim), 1))
     x = bf16_round(rnd((n_tok, in_dim), 2))
@@ -57,7 +68,7 @@ def test_bf16_wgrad_slice_vs_oracle(cuda, n_tok, in_dim, out_dim, rb, re):
 
 
 @pytest.mark.parametrize("n_tok,in_dim,out_dim,rb,re", SHAPES[:2])
-def test_bf16_wgrad_accumulate(cuda, n_tok, in_dim, out_dim, rb, re):
+def test_bf16_wgrad_accumulate(cuda, gemm_policy, n_tok, in_dim, out_dim, rb, re):
     from paper_2605_21177_b200 import ops
     dy = bf16_round(rnd((n_tok, out_dim), 3))
     x = bf16_round(rnd((n_tok, in_dim), 4))
@@ -71,7 +82,7 @@ def test_bf16_wgrad_accumulate(cuda, n_tok, in_dim, out_dim, rb, re):
 
 
 @pytest.mark.parametrize("n_tok,in_dim,out_dim", [(256, 256, 384), (1000, 512, 320), (128, 64, 256)])
-def test_bf16_forward_and_dgrad_vs_oracle(cuda, n_tok, in_dim, out_dim):
+def test_bf16_forward_and_dgrad_vs_oracle(cuda, gemm_policy, n_tok, in_dim, out_dim):
     from paper_2605_21177_b200 import ops
     x = bf16_round(rnd((n_tok, in_dim), 6))
     w = bf16_round(rnd((out_dim, in_dim), 7))
@@ -119,7 +130,7 @@ def test_fp64_path_bit_exact(cuda, n_tok, in_dim, out_dim, rb, re):
     assert np.array_equal(db, orc.linear_dbias(dy, rb, re))
 
 
-def test_full_size_bf16_vs_torch_fp32(cuda):
+def test_full_size_bf16_vs_torch_fp32(cuda, gemm_policy):
     """BASELINE configs[1] shape (d=4096, N_tok=8192) against a plain torch fp32 reference."""
     from paper_2605_21177_b200 import ops
     g = torch.Generator(device=cuda).manual_seed(0)
