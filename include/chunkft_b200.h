@@ -237,13 +237,15 @@ int cft_grad_stats(cft_dtype state_dtype, const void* grad, int64_t n, double gr
  *   host in fp64 from the chunk-local counter n (already incremented).  If stats_dev[1] != 0
  *   (a non-finite gradient was seen by cft_grad_stats) the kernel does nothing.
  *   precond_dev[0..1] receive min/max of 1/(sqrt(vhat)+eps) (float, or double for F64).
+ *   zero_grad 1 (fp32 state): the consumed gradient is overwritten with zeros in the same
+ *   pass (+4 B/elem), so the next step's wgrad can red-add into it without a memset.
  * state_dtype: CFT_F32 (fp32 master/m/v/grad) or CFT_F64.  param_dtype: CFT_BF16, CFT_F32
  * or CFT_F64. */
-int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, const void* grad,
+int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void* grad,
                     int64_t n, double grad_scale, const cft_adamw_hyper* hyper, double bc1,
                     double bc2, cft_dtype param_dtype, void* param_base,
                     const cft_segment* segments_dev, int32_t n_segments, const void* stats_dev,
-                    void* precond_dev, cft_stream_t stream);
+                    void* precond_dev, int zero_grad, cft_stream_t stream);
 
 /* Plain block descent (optimizer.cpp:200-208), same segment write-back. */
 int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t n,

@@ -117,16 +117,47 @@ __global__ void __launch_bounds__(kThreads) grad_stats_kernel(const T* __restric
   }
 }
 
-// ---- fp32-state AdamW, 4 elements per thread-iteration ----
+// ---- fp32-state AdamW: 2 x 4 elements per thread with all 8 vector loads issued up front
+// (memory-level parallelism for the small chunks of narrow plans); block-level min/max of
+// 1/denom so only one atomic pair per block reaches L2; optionally leaves the gradient
+// accumulator zeroed for the next step's red-add wgrad (saves a memset pass). ----
+constexpr int kGroups = 2;
+
+template <typename P>
+__device__ __forceinline__ void write_back4(P* __restrict__ param, const cft_segment* sg, int nseg,
+                                            long long i0, long long n, const float (&w)[4]) {
+  int s = find_segment(sg, nseg, i0);
+  const long long send = sg[s].state_off + sg[s].count;
+  P* dst = param + sg[s].param_off + (i0 - sg[s].state_off);
+  if (i0 + 3 < send && i0 + 3 < n && std::is_same_v<P, __nv_bfloat16> &&
+      (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(w[0], w[1]);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(w[2], w[3]);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(dst) = pk;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const long long i = i0 + e;
+      if (i >= n) break;
+      while (i >= sg[s].state_off + sg[s].count) ++s;
+      store_param(param + sg[s].param_off + (i - sg[s].state_off), w[e]);
+    }
+  }
+}
+
 template <typename P>
 __global__ void __launch_bounds__(kThreads)
     adamw_f32_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
-                     const float* __restrict__ grad, long long n, float gscale, float eta,
-                     float b1, float b2, float eps, float wd, float bc1, float bc2,
-                     P* __restrict__ param, const cft_segment* __restrict__ segs, int nseg,
-                     const double* __restrict__ stats, float* __restrict__ precond) {
+                     float* __restrict__ grad, long long n, float gscale, float eta, float b1,
+                     float b2, float eps, float wd, float bc1, float bc2, P* __restrict__ param,
+                     const cft_segment* __restrict__ segs, int nseg,
+                     const double* __restrict__ stats, float* __restrict__ precond, int zero_grad) {
   if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
   __shared__ cft_segment s_segs[kSmemSegs];
+  __shared__ float s_min[kThreads / 32], s_max[kThreads / 32];
   const bool in_smem = nseg <= kSmemSegs;
   if (in_smem)
     for (int i = threadIdx.x; i < nseg; i += blockDim.x) s_segs[i] = segs[i];
@@ -136,81 +167,73 @@ __global__ void __launch_bounds__(kThreads)
   float pmin = INFINITY, pmax = 0.f;
   const long long n4 = (n + 3) / 4;
   const bool vec_ok = (n % 4) == 0;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n4;
-       q += (long long)gridDim.x * blockDim.x) {
-    const long long i0 = 4 * q;
-    float g[4], mm[4], vv[4], w[4];
-    if (vec_ok) {
-      const float4 g4 = reinterpret_cast<const float4*>(grad)[q];
-      const float4 m4 = reinterpret_cast<const float4*>(m)[q];
-      const float4 v4 = reinterpret_cast<const float4*>(v)[q];
-      const float4 w4 = reinterpret_cast<const float4*>(master)[q];
-      g[0] = g4.x; g[1] = g4.y; g[2] = g4.z; g[3] = g4.w;
-      mm[0] = m4.x; mm[1] = m4.y; mm[2] = m4.z; mm[3] = m4.w;
-      vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
-      w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
-    } else {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long q0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; q0 < n4;
+       q0 += kGroups * stride) {
+    float g[kGroups][4], mm[kGroups][4], vv[kGroups][4], w[kGroups][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const long long i = i0 + e;
-        g[e] = i < n ? grad[i] : 0.f;
-        mm[e] = i < n ? m[i] : 0.f;
-        vv[e] = i < n ? v[i] : 0.f;
-        w[e] = i < n ? master[i] : 0.f;
-      }
-    }
+    for (int k = 0; k < kGroups; ++k) {
+      const long long q = q0 + k * stride;
+      if (q >= n4) break;
+      if (vec_ok) {
+        const float4 g4 = reinterpret_cast<const float4*>(grad)[q];
+        const float4 m4 = reinterpret_cast<const float4*>(m)[q];
+        const float4 v4 = reinterpret_cast<const float4*>(v)[q];
+        const float4 w4 = reinterpret_cast<const float4*>(master)[q];
+        g[k][0] = g4.x; g[k][1] = g4.y; g[k][2] = g4.z; g[k][3] = g4.w;
+        mm[k][0] = m4.x; mm[k][1] = m4.y; mm[k][2] = m4.z; mm[k][3] = m4.w;
+        vv[k][0] = v4.x; vv[k][1] = v4.y; vv[k][2] = v4.z; vv[k][3] = v4.w;
+        w[k][0] = w4.x; w[k][1] = w4.y; w[k][2] = w4.z; w[k][3] = w4.w;
+      } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float ge = g[e] * gscale;
-      mm[e] = b1 * mm[e] + omb1 * ge;
-      vv[e] = b2 * vv[e] + omb2 * ge * ge;
-      const float mhat = mm[e] / bc1;
-      const float vhat = vv[e] / bc2;
-      const float denom = sqrtf(vhat) + eps;
-      w[e] = w[e] - eta * (mhat / denom + wd * w[e]);
-      if (i0 + e < n) {
-        const float pc = 1.f / denom;
-        pmin = fminf(pmin, pc);
-        pmax = fmaxf(pmax, pc);
-      }
-    }
-    if (vec_ok) {
-      reinterpret_cast<float4*>(m)[q] = make_float4(mm[0], mm[1], mm[2], mm[3]);
-      reinterpret_cast<float4*>(v)[q] = make_float4(vv[0], vv[1], vv[2], vv[3]);
-      reinterpret_cast<float4*>(master)[q] = make_float4(w[0], w[1], w[2], w[3]);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const long long i = i0 + e;
-        if (i < n) {
-          m[i] = mm[e];
-          v[i] = vv[e];
-          master[i] = w[e];
+        for (int e = 0; e < 4; ++e) {
+          const long long i = 4 * q + e;
+          g[k][e] = i < n ? grad[i] : 0.f;
+          mm[k][e] = i < n ? m[i] : 0.f;
+          vv[k][e] = i < n ? v[i] : 0.f;
+          w[k][e] = i < n ? master[i] : 0.f;
         }
       }
     }
-    // write-back through the segment table (optimizer.cpp:124-132)
-    if (param) {
-      int s = find_segment(sg, nseg, i0);
-      const long long send = sg[s].state_off + sg[s].count;
-      P* dst = param + sg[s].param_off + (i0 - sg[s].state_off);
-      if (i0 + 3 < send && i0 + 3 < n && std::is_same_v<P, __nv_bfloat16> &&
-          (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(w[0], w[1]);
-        __nv_bfloat162 hi = __floats2bfloat162_rn(w[2], w[3]);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&lo);
-        pk.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(dst) = pk;
+#pragma unroll
+    for (int k = 0; k < kGroups; ++k) {
+      const long long q = q0 + k * stride;
+      if (q >= n4) break;
+      const long long i0 = 4 * q;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float ge = g[k][e] * gscale;
+        mm[k][e] = b1 * mm[k][e] + omb1 * ge;
+        vv[k][e] = b2 * vv[k][e] + omb2 * ge * ge;
+        const float mhat = mm[k][e] / bc1;
+        const float vhat = vv[k][e] / bc2;
+        const float denom = sqrtf(vhat) + eps;
+        w[k][e] = w[k][e] - eta * (mhat / denom + wd * w[k][e]);
+        if (i0 + e < n) {
+          const float pc = 1.f / denom;
+          pmin = fminf(pmin, pc);
+          pmax = fmaxf(pmax, pc);
+        }
+      }
+      if (vec_ok) {
+        reinterpret_cast<float4*>(m)[q] = make_float4(mm[k][0], mm[k][1], mm[k][2], mm[k][3]);
+        reinterpret_cast<float4*>(v)[q] = make_float4(vv[k][0], vv[k][1], vv[k][2], vv[k][3]);
+        reinterpret_cast<float4*>(master)[q] = make_float4(w[k][0], w[k][1], w[k][2], w[k][3]);
+        if (zero_grad) reinterpret_cast<float4*>(grad)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const long long i = i0 + e;
-          if (i >= n) break;
-          while (i >= sg[s].state_off + sg[s].count) ++s;
-          store_param(param + sg[s].param_off + (i - sg[s].state_off), w[e]);
+          if (i < n) {
+            m[i] = mm[k][e];
+            v[i] = vv[k][e];
+            master[i] = w[k][e];
+            if (zero_grad) grad[i] = 0.f;
+          }
         }
       }
+      // write-back through the segment table (optimizer.cpp:124-132)
+      if (param) write_back4(param, sg, nseg, i0, n, w[k]);
     }
   }
   if (precond) {
@@ -218,9 +241,20 @@ __global__ void __launch_bounds__(kThreads)
       pmin = fminf(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
       pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
     }
-    if ((threadIdx.x & 31) == 0 && pmax > 0.f) {
-      atomic_min_pos(&precond[0], pmin);
-      atomic_max_pos(&precond[1], pmax);
+    if ((threadIdx.x & 31) == 0) {
+      s_min[threadIdx.x / 32] = pmin;
+      s_max[threadIdx.x / 32] = pmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < kThreads / 32; ++i) {
+        pmin = fminf(pmin, s_min[i]);
+        pmax = fmaxf(pmax, s_max[i]);
+      }
+      if (pmax > 0.f) {
+        atomic_min_pos(&precond[0], pmin);
+        atomic_max_pos(&precond[1], pmax);
+      }
     }
   }
 }
@@ -340,10 +374,10 @@ int cft_grad_stats(cft_dtype state_dtype, const void* grad, int64_t n, double gr
   });
 }
 
-int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, const void* grad,
+int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void* grad,
                     int64_t n, double grad_scale, const cft_adamw_hyper* h, double bc1, double bc2,
                     cft_dtype param_dtype, void* param_base, const cft_segment* segs,
-                    int32_t n_segments, const void* stats_dev, void* precond_dev,
+                    int32_t n_segments, const void* stats_dev, void* precond_dev, int zero_grad,
                     cft_stream_t stream) {
   return cft::guarded([&] {
     auto s = static_cast<cudaStream_t>(stream);
@@ -352,13 +386,17 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, const
     CFT_CHECK(!param_base || (segs && n_segments > 0), "cft_adamw_slice: missing segments");
     const double* st = static_cast<const double*>(stats_dev);
     if (state_dtype == CFT_F32) {
-      const int grid = grid_for((n + 3) / 4);
+      // one pass: every thread owns kGroups float4 groups (no grid-stride tail for sizes up
+      // to num_sms * 16 blocks)
+      const long long groups = (n + 3) / 4;
+      const long long want = (groups + kThreads * kGroups - 1) / (kThreads * kGroups);
+      const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(want, (long long)cft::num_sms() * 16)));
       auto go = [&](auto* p) {
         adamw_f32_kernel<<<grid, kThreads, 0, s>>>(
             static_cast<float*>(master), static_cast<float*>(m), static_cast<float*>(v),
-            static_cast<const float*>(grad), n, (float)grad_scale, (float)h->eta, (float)h->beta1,
+            static_cast<float*>(grad), n, (float)grad_scale, (float)h->eta, (float)h->beta1,
             (float)h->beta2, (float)h->epsilon, (float)h->weight_decay, (float)bc1, (float)bc2, p,
-            segs, n_segments, st, static_cast<float*>(precond_dev));
+            segs, n_segments, st, static_cast<float*>(precond_dev), zero_grad);
       };
       if (param_dtype == CFT_BF16) go(static_cast<__nv_bfloat16*>(param_base));
       else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));

@@ -167,6 +167,7 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
   alloc(&act_[0], rows * max_width_ * E);
   alloc(&act_[1], rows * max_width_ * E);
   alloc(&aux_, max_chunk_ * S);
+  CFT_CUDA(cudaMemset(aux_, 0, max_chunk_ * S));
   if (cfg_.dtype == CFT_F64)
     alloc(&scratch_, std::max<int64_t>(max_slice_, rows * std::max<int64_t>(max_width_, 1)) * 8);
   const Layer& first = layers_.front();
@@ -571,8 +572,8 @@ void Engine::forward_backward(const Batch& b, int mb) {
         if (mb > 0) tgt = scratch_;
         CFT_CUDA(cudaMemsetAsync(tgt, 0, sl.count * 8, s));
         acc_flag = 1;
-      } else if (L.spec.type == kEmbedding && mb == 0) {
-        CFT_CUDA(cudaMemsetAsync(tgt, 0, sl.count * 4, s));
+      } else {
+        acc_flag = 1;  // the fp32 accumulator is all-zero between steps (AdamW re-zeroes it)
       }
       const bool is_w = sl.tensor == L.w;
       pb(L.spec.type == kLinear && is_w ? kWgrad : kBwdOther);
@@ -712,12 +713,13 @@ void Engine::step_end() {
     const double bc2 = 1.0 - std::pow(cfg_.hyper.beta2, static_cast<double>(n_local_[c]));
     if (cft_adamw_slice(sdt, master, m, v, aux_, n, scale, &cfg_.hyper, bc1, bc2,
                         static_cast<cft_dtype>(cfg_.dtype), params_, chunk_segs_[c], nseg, st,
-                        precond_, s) != CFT_OK)
+                        precond_, sdt == CFT_F32 ? 1 : 0, s) != CFT_OK)
       throw Error(last_error());
   } else {
     if (cft_sgd_slice(sdt, master, aux_, n, scale, cfg_.hyper.eta, static_cast<cft_dtype>(cfg_.dtype),
                       params_, chunk_segs_[c], nseg, st, s) != CFT_OK)
       throw Error(last_error());
+    if (sdt == CFT_F32) CFT_CUDA(cudaMemsetAsync(aux_, 0, n * 4, s));
   }
   pe();
   CFT_CUDA(cudaEventRecord(ev_[5], s));
@@ -736,10 +738,14 @@ void Engine::step_end() {
     CFT_CUDA(cudaStreamSynchronize(s));
     const double* h = host_stats_ + t_ * 4;
     const std::string ctx = "step " + std::to_string(t_) + ", chunk " + std::to_string(c) + ": ";
+    auto restore = [&] {  // keep the zero-accumulator invariant after a rejected step
+      if (sdt == CFT_F32) CFT_CUDA(cudaMemset(aux_, 0, max_chunk_ * 4));
+    };
     if (host_flags_[1]) throw Error(ctx + "embedding: token id out of range");
     if (host_flags_[0]) throw Error(ctx + "loss: label out of range");
     if (!std::isfinite(h[3])) {
       n_local_[c] -= 1;
+      restore();
       throw Error(ctx + "non-finite loss");
     }
     uint64_t nbad;
@@ -748,6 +754,7 @@ void Engine::step_end() {
       int64_t bad;
       std::memcpy(&bad, &h[2], 8);
       n_local_[c] -= 1;
+      restore();
       throw Error(ctx + "step: non-finite gradient at element " + std::to_string(bad) + " (chunk " +
                   std::to_string(c) + ", local step " + std::to_string(n_local_[c] + 1) + ")");
     }

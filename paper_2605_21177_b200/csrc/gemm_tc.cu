@@ -643,14 +643,14 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   if (pairs) {
     Args a256 = a, a128 = a;
     fill_units(a256, 256, 256, num_sms() / 2, 0.40, true);
-    fill_units(a128, 256, 128, num_sms() / 2, 0.21, true);
+    fill_units(a128, 256, 128, num_sms() / 2, 0.38, true);
     auto cost = [](const Args& x, double us_per_kb) {
       const int waves = (x.num_units + num_sms() / 2 - 1) / (num_sms() / 2);
       double t = waves * x.kb_per_split * us_per_kb;
       if (x.splits > 1) t += (x.splits + 1) * static_cast<double>(x.M) * x.N * 4.0 / 2.0e6;
       return t;
     };
-    if (g_policy == 0 && cost(a128, 0.21) < cost(a256, 0.40)) {
+    if (g_policy == 0 && cost(a128, 0.38) < cost(a256, 0.40)) {
       a = a128;
       pair_bn = 128;
     } else {
@@ -659,14 +659,17 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   } else {
     fill_units(a, BM, BN, num_sms(), 0.45 * BN / 256.0, true);
   }
-  if (a.splits > 1) {
-    // Partial sums race into dw: zero first unless accumulating.
-    if (!accumulate)
-      CFT_CUDA(cudaMemset2DAsync(dw, sizeof(float) * in_dim, 0, sizeof(float) * in_dim, a.M,
-                                 stream));
+  if (accumulate) {
+    // dw += result: fire-and-forget red.add for any split count (the engine keeps its
+    // gradient accumulator zeroed between steps, so this is also its overwrite path)
+    a.epi = kEpiF32Red;
+  } else if (a.splits > 1) {
+    // partial sums race into dw: zero it first
+    CFT_CUDA(cudaMemset2DAsync(dw, sizeof(float) * in_dim, 0, sizeof(float) * in_dim, a.M,
+                               stream));
     a.epi = kEpiF32Red;
   } else {
-    a.epi = accumulate ? kEpiF32Add : kEpiF32;
+    a.epi = kEpiF32;
   }
   if (pairs && pair_bn == 128) launch_2sm<true, true, 128>(ta, tb, a, stream);
   else if (pairs) launch_2sm<true, true, 256>(ta, tb, a, stream);

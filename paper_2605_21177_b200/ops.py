@@ -145,7 +145,8 @@ def grad_stats(grad: torch.Tensor, grad_scale: float = 1.0, stats=None, stream=N
 
 
 def adamw_slice(master, m, v, grad, hyper, n_local: int, param=None, segments=None,
-                grad_scale: float = 1.0, stats=None, precond=None, stream=None):
+                grad_scale: float = 1.0, stats=None, precond=None, zero_grad: bool = False,
+                stream=None):
     """One fused AdamW update on a chunk (optimizer.cpp:163-198); n_local already incremented."""
     bc1 = 1.0 - hyper.beta1 ** float(n_local)
     bc2 = 1.0 - hyper.beta2 ** float(n_local)
@@ -155,4 +156,9 @@ def adamw_slice(master, m, v, grad, hyper, n_local: int, param=None, segments=No
                                   grad.data_ptr(), master.numel(), grad_scale, C.byref(h), bc1, bc2,
                                   _dtype(param) if param is not None else N.CFT_F32,
                                   _ptr(param), _ptr(segments), nseg, _ptr(stats), _ptr(precond),
-                                  _stream(stream)), "adamw_slice")
+                                  int(zero_grad), _stream(stream)), "adamw_slice")
+
+
+def set_gemm_policy(policy: int) -> None:
+    """0 auto, 1 single-CTA 128xBN tcgen05 tiles, 2 CTA-pair 256x256 tiles."""
+    N.check(N.lib.cft_set_gemm_policy(policy))

@@ -147,3 +147,35 @@ def test_full_size_bf16_vs_torch_fp32(cuda, gemm_policy):
                      (dw, dyf[:, rb:re].t() @ xf)):
         err = (got - ref).norm() / ref.norm()
         assert err.item() < 4e-3, err.item()
+
+
+def test_adamw_fp32_vs_oracle_and_zero_grad(cuda):
+    """Fused AdamW (fp32 state, bf16 write-back through two segments) vs the oracle's
+    adamw_chunk_step restatement fed the same fp32 values; elementwise 1e-5."""
+    from paper_2605_21177_b200 import ops
+    from paper_2605_21177_b200.engine import AdamWHyper
+    rng = np.random.default_rng(3)
+    E = 10_003
+    master = rng.uniform(-0.5, 0.5, E).astype(np.float32)
+    m = rng.uniform(-1e-3, 1e-3, E).astype(np.float32)
+    v = rng.uniform(0, 1e-6, E).astype(np.float32)
+    g = rng.uniform(-1, 1, E).astype(np.float32)
+    h = AdamWHyper(1e-3, 0.9, 0.999, 1e-8, 0.01)
+    ref = O_adamw = orc.adamw(master.astype(np.float64), m, v, g.astype(np.float64) * 0.5, 4,
+                              h.eta, h.beta1, h.beta2, h.epsilon, h.weight_decay)
+    f = lambda a: torch.from_numpy(a.copy()).to(cuda)
+    tm, tmm, tv, tg = f(master), f(m), f(v), f(g)
+    param = torch.zeros(E + 100, dtype=torch.bfloat16, device=cuda)
+    segs = ops.segments_tensor([(0, 50, 6000), (6000, 6100, E - 6000)], cuda)
+    pre = torch.tensor([float("inf"), 0.0], device=cuda)
+    ops.adamw_slice(tm, tmm, tv, tg, h, 5, param=param, segments=segs, grad_scale=0.5,
+                    precond=pre, zero_grad=True)
+    torch.cuda.synchronize()
+    rel = lambda a, b: np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0))
+    assert rel(tm.cpu().numpy(), ref[0]) < 1e-5
+    assert rel(tmm.cpu().numpy(), ref[1]) < 1e-5 and rel(tv.cpu().numpy(), ref[2]) < 1e-5
+    p = param.float().cpu().numpy()
+    assert np.allclose(p[50:6050], ref[0][:6000], rtol=1e-2, atol=1e-3)
+    assert np.allclose(p[6100:6100 + E - 6000], ref[0][6000:], rtol=1e-2, atol=1e-3)
+    assert float(tg.abs().max()) == 0.0  # accumulator left zeroed
+    assert abs(pre[0].item() - ref[4]) <= 1e-5 * ref[4] and abs(pre[1].item() - ref[5]) <= 1e-5 * ref[5]
