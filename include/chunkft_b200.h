@@ -350,6 +350,13 @@ int cft_engine_phase_totals(cft_engine* e, float* ms9, int64_t* counts9);
 /* Block the host until step t's loss / grad_norm_sq reached host memory (t within the last
  * 4 steps) -- a per-step result read that does not drain the device queue. */
 int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq);
+/* CKFT v1 checkpoints (write_chunk_checkpoint / read_chunk_checkpoint, optimizer.hpp:117-125,
+ * FORMATS.md:176-194): dir/chunk_NNNN.bin per chunk, plan-hash guarded, master/m/v widened to
+ * fp64 -- byte-compatible with the reference.  write after cft_engine_finish; read (resume)
+ * before the first step: restores masters, moments, the chunk-local counters and the
+ * compute-dtype parameters. */
+int cft_engine_write_checkpoints(cft_engine* e, const char* dir);
+int cft_engine_read_checkpoints(cft_engine* e, const char* dir);
 
 #ifdef __cplusplus
 }

@@ -187,8 +187,36 @@ def train_runs():
     return out
 
 
+def checkpoints():
+    """CKFT v1 files written by the reference after training (write_chunk_checkpoint)."""
+    import base64
+    import tempfile
+    cases = {c["name"]: c for c in TRAIN_CASES}
+    out = {}
+    for name in ("linear_exact", "emb_ln_mb"):
+        c = cases[name]
+        rng = np.random.default_rng(77)
+        params = ref.init_params(c["layers"], seed=7)
+        batches = _batches(c["layers"], c["loss"], c["nb"], c["rows"], rng)
+        d = tempfile.mkdtemp()
+        hyper = c.get("hyper", (1e-3, 0.9, 0.999, 1e-8, 0.0))
+        ref.train(c["layers"], c["loss"], params, batches, K=c.get("K"), T=c["T"], steps=c["steps"],
+                  prefetch=c.get("prefetch", False), bw=c.get("bw", 0), optim=c.get("optim", "adamw"),
+                  micro_batches=c.get("micro_batches", 1), hyper=hyper, ckpt_dir=d)
+        files = {}
+        for fn in sorted(os.listdir(d)):
+            with open(os.path.join(d, fn), "rb") as f:
+                files[fn] = base64.b64encode(f.read()).decode()
+        out[name] = dict(init_params=params.tolist(),
+                         batches=[{k: v.tolist() for k, v in b.items()} for b in batches],
+                         files=files)
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "checkpoints.json"), "w") as f:
+        json.dump(checkpoints(), f)
     with open(os.path.join(OUT, "plans.json"), "w") as f:
         json.dump(plans(), f, indent=0)
     with open(os.path.join(OUT, "schedules.json"), "w") as f:

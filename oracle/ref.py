@@ -52,7 +52,7 @@ if REF is not None:
     _s("ref_adamw", CT.c_int, vp, vp, vp, vp, i64, vp, vp, vp, vp)
     _s("ref_init_params", i64, vp, CT.c_int, CT.c_int, u64, vp, i64)
     _s("ref_train", CT.c_int, vp, CT.c_int, CT.c_int, vp, CT.c_int, CT.c_int, CT.c_int, vp, CT.c_int,
-       vp, CT.c_int, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp)
+       vp, CT.c_int, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, CT.c_char_p)
 
 
 def partition(tensors, K=None, budget=None, per_tensor=False, policy=(2, 4, 4, 4, 4), names=None,
@@ -220,7 +220,7 @@ def init_params(layers, seed=7, formula=False):
 
 def train(layers, loss, params, batches, K=None, T=1, steps=1, budget=None, per_tensor=False,
           prefetch=False, bw=0, optim="adamw", micro_batches=1,
-          hyper=(1e-3, 0.9, 0.999, 1e-8, 0.0)):
+          hyper=(1e-3, 0.9, 0.999, 1e-8, 0.0), ckpt_dir=None):
     """Run the reference's run_training.  batches: list of dicts with x / tokens / target /
     labels numpy arrays (same shapes for every batch)."""
     _need()
@@ -245,7 +245,7 @@ def train(layers, loss, params, batches, K=None, T=1, steps=1, budget=None, per_
     cn = np.zeros(p0.size + 8, np.uint64)
     rc = REF.ref_train(_p(la), len(layers), LOSS_CODES[loss], _p(p0), nb, rows, xc, _p(X), seq, _p(TOK),
                        tc, _p(TG), _p(LB), _p(opts), budget or 0, _p(_f(hyper)), _p(tl), _p(tg),
-                       _p(tch), _p(fp), _p(h), _p(cn))
+                       _p(tch), _p(fp), _p(h), _p(cn), ckpt_dir.encode() if ckpt_dir else None)
     if rc != 0:
         raise ValueError(_err())
     return dict(loss=tl, gsq=tg, chunk=tch, params=fp, plan_hash=int(h[0]))

@@ -10,7 +10,9 @@
 //   * adamw_chunk_step                 (include/chunkft/optimizer.hpp:50-100)
 //   * run_training end to end          (include/chunkft/trainer.hpp:49-50)
 // Nothing here is product code and nothing in the product links it.
+#include <cstdio>
 #include <cstring>
+#include <filesystem>
 #include <exception>
 #include <memory>
 #include <string>
@@ -315,7 +317,7 @@ int ref_train(const int32_t* layers, int n_layers, int loss_kind, const double* 
               int target_cols, const double* target, const int* labels, const int64_t* opts,
               int64_t budget, const double* hyper5, double* traj_loss, double* traj_gsq,
               int32_t* traj_chunk, double* final_params, uint64_t* plan_hash_out,
-              uint64_t* chunk_n_out) {
+              uint64_t* chunk_n_out, const char* ckpt_dir) {
   try {
     Model m = build_model(layers, n_layers, loss_kind);
     m.restore_params(std::vector<double>(init_params, init_params + m.total_parameters()));
@@ -369,6 +371,13 @@ int ref_train(const int32_t* layers, int n_layers, int loss_kind, const double* 
     *plan_hash_out = plan_hash(plan);
     if (chunk_n_out)
       for (int c = 0; c < plan.K(); ++c) chunk_n_out[c] = r.states[c].n;
+    if (ckpt_dir) {  // runner.cpp:182-187 naming
+      for (int c = 0; c < plan.K(); ++c) {
+        char name[32];
+        std::snprintf(name, sizeof(name), "chunk_%04d.bin", c);
+        write_chunk_checkpoint(r.states[c], plan_hash(plan), std::filesystem::path(ckpt_dir) / name);
+      }
+    }
     return 0;
   } catch (const std::exception& e) {
     set_err(e.what());

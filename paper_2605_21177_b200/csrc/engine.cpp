@@ -843,6 +843,106 @@ std::string Engine::plan_json() const {
   return host::plan_to_json(plan_, infos);
 }
 
+namespace {
+constexpr char kMagic[4] = {'C', 'K', 'F', 'T'};
+constexpr uint32_t kVersion = 1;
+
+std::string chunk_file(const std::string& dir, int c) {
+  char name[32];
+  std::snprintf(name, sizeof(name), "chunk_%04d.bin", c);
+  return dir + "/" + name;
+}
+}  // namespace
+
+void Engine::write_checkpoints(const std::string& dir) {
+  CFT_CHECK(finished_, "checkpoint: flush chunk to host tier first");
+  const uint64_t hash = host::plan_hash(plan_);
+  const size_t S = ssz();
+  for (int c = 0; c < cfg_.K; ++c) {
+    const int64_t n = plan_.chunks[c].elements;
+    std::vector<char> raw(n * 3 * S);
+    CFT_CUDA(cudaMemcpy(raw.data(), host_states_[c], raw.size(),
+                        cfg_.offload ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+    std::vector<double> wide(n * 3);
+    for (int64_t i = 0; i < 3 * n; ++i)
+      wide[i] = S == 8 ? reinterpret_cast<double*>(raw.data())[i]
+                       : static_cast<double>(reinterpret_cast<float*>(raw.data())[i]);
+    const std::string path = chunk_file(dir, c);
+    FILE* f = std::fopen(path.c_str(), "wb");
+    CFT_CHECK(f != nullptr, "checkpoint: cannot open '" + path + "' for writing");
+    const int32_t chunk = c;
+    const uint64_t nl = n_local_[c];
+    const int64_t E = n;
+    bool ok = std::fwrite(kMagic, 1, 4, f) == 4 && std::fwrite(&kVersion, 4, 1, f) == 1 &&
+              std::fwrite(&hash, 8, 1, f) == 1 && std::fwrite(&chunk, 4, 1, f) == 1 &&
+              std::fwrite(&nl, 8, 1, f) == 1 && std::fwrite(&E, 8, 1, f) == 1 &&
+              std::fwrite(wide.data(), 8, wide.size(), f) == wide.size();
+    ok = (std::fclose(f) == 0) && ok;
+    CFT_CHECK(ok, "checkpoint: write failed for '" + path + "'");
+  }
+}
+
+void Engine::read_checkpoints(const std::string& dir) {
+  CFT_CHECK(t_ == 0 && !finished_, "checkpoint: restore before the first step");
+  const uint64_t want = host::plan_hash(plan_);
+  const size_t S = ssz();
+  std::vector<double> params(param_elems_);
+  params_device(params.data());  // start from the current values (frozen tensors keep theirs)
+  for (int c = 0; c < cfg_.K; ++c) {
+    const std::string path = chunk_file(dir, c);
+    FILE* f = std::fopen(path.c_str(), "rb");
+    CFT_CHECK(f != nullptr, "checkpoint: cannot open '" + path + "'");
+    char magic[4];
+    uint32_t version = 0;
+    uint64_t hash = 0, nl = 0;
+    int32_t chunk = -1;
+    int64_t E = -1;
+    const bool hdr = std::fread(magic, 1, 4, f) == 4;
+    if (!hdr || std::memcmp(magic, kMagic, 4) != 0) {
+      std::fclose(f);
+      throw Error("checkpoint: bad magic in '" + path + "'");
+    }
+    if (std::fread(&version, 4, 1, f) != 1 || version != kVersion) {
+      std::fclose(f);
+      throw Error("checkpoint: unsupported version");
+    }
+    if (std::fread(&hash, 8, 1, f) != 1 || hash != want) {
+      std::fclose(f);
+      throw Error("checkpoint: plan hash mismatch (checkpoint belongs to a different plan)");
+    }
+    const int64_t n = plan_.chunks[c].elements;
+    std::vector<double> wide(3 * n);
+    const bool body = std::fread(&chunk, 4, 1, f) == 1 && std::fread(&nl, 8, 1, f) == 1 &&
+                      std::fread(&E, 8, 1, f) == 1 && E == n &&
+                      std::fread(wide.data(), 8, wide.size(), f) == wide.size();
+    std::fclose(f);
+    CFT_CHECK(body && chunk == c, "checkpoint: truncated payload");
+    n_local_[c] = nl;
+    std::vector<char> raw(n * 3 * S);
+    for (int64_t i = 0; i < 3 * n; ++i) {
+      if (S == 8) reinterpret_cast<double*>(raw.data())[i] = wide[i];
+      else reinterpret_cast<float*>(raw.data())[i] = static_cast<float>(wide[i]);
+    }
+    CFT_CUDA(cudaMemcpy(host_states_[c], raw.data(), raw.size(),
+                        cfg_.offload ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice));
+    for (const auto& s : chunk_slices_[c])  // masters are the authoritative parameters
+      std::memcpy(params.data() + s.param_off, wide.data() + s.aux_off, s.count * 8);
+  }
+  // refresh the compute-dtype parameter arena from the restored masters
+  void* tmp;
+  CFT_CUDA(cudaMalloc(&tmp, param_elems_ * 8));
+  CFT_CUDA(cudaMemcpy(tmp, params.data(), param_elems_ * 8, cudaMemcpyHostToDevice));
+  if (cfg_.dtype == CFT_F64) {
+    CFT_CUDA(cudaMemcpy(params_, tmp, param_elems_ * 8, cudaMemcpyDeviceToDevice));
+  } else if (cft_convert(CFT_F64, tmp, static_cast<cft_dtype>(cfg_.dtype), params_, param_elems_,
+                         stream_) != CFT_OK) {
+    cudaFree(tmp);
+    throw Error(last_error());
+  }
+  CFT_CUDA(cudaStreamSynchronize(stream_));
+  cudaFree(tmp);
+}
+
 void Engine::chunk_counters(uint64_t* n) const {
   for (int c = 0; c < cfg_.K; ++c) n[c] = n_local_[c];
 }

@@ -99,6 +99,11 @@ class Engine {
   void phase_totals(float* ms, int64_t* counts);  // syncs; resets the marks
   void wait_step(int64_t t, double* loss, double* gsq);  // host waits for step t's result only
 
+  // CKFT v1 checkpoints (optimizer.cpp:210-251, FORMATS.md:176-194): one chunk_NNNN.bin per
+  // chunk with the plan hash, the local counter n and master/m/v as raw doubles.
+  void write_checkpoints(const std::string& dir);  // after finish()
+  void read_checkpoints(const std::string& dir);   // before the first step (resume)
+
  private:
   struct Tensor {
     int id;

@@ -164,3 +164,15 @@ int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int cft_engine_write_checkpoints(cft_engine* e, const char* dir) {
+  return guarded([&] { e->p->write_checkpoints(dir); });
+}
+
+int cft_engine_read_checkpoints(cft_engine* e, const char* dir) {
+  return guarded([&] { e->p->read_checkpoints(dir); });
+}
+
+}  // extern "C"

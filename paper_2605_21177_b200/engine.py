@@ -66,6 +66,8 @@ for _n, _r, _a in [
     ("cft_engine_profile", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
     ("cft_engine_phase_totals", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("cft_engine_wait_step", C.c_int, [C.c_void_p, C.c_int64, _P(C.c_double), _P(C.c_double)]),
+    ("cft_engine_write_checkpoints", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("cft_engine_read_checkpoints", C.c_int, [C.c_void_p, C.c_char_p]),
 ]:
     _f = getattr(_L, _n)
     _f.restype = _r
@@ -336,6 +338,14 @@ class ChunkEngine:
         cnt = np.zeros(9, np.int64)
         N.check(_L.cft_engine_phase_totals(self._h, ms.ctypes.data, cnt.ctypes.data))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PHASES)}
+
+    def write_checkpoints(self, directory: str):
+        """CKFT v1 files dir/chunk_NNNN.bin (optimizer.cpp:210-230); call after finish()."""
+        N.check(_L.cft_engine_write_checkpoints(self._h, directory.encode()), "checkpoint")
+
+    def read_checkpoints(self, directory: str):
+        """Resume from CKFT v1 files (optimizer.cpp:232-251) before the first step."""
+        N.check(_L.cft_engine_read_checkpoints(self._h, directory.encode()), "checkpoint")
 
     def wait_step(self, t: int):
         lo, gs = C.c_double(), C.c_double()

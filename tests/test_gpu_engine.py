@@ -210,3 +210,76 @@ def test_engine_dp_exchange_matches_reference_micro_batches(cuda):
     p0, p1 = engs[0].params(), engs[1].params()
     assert np.array_equal(p0, p1)
     assert np.array_equal(p0, np.array(case["final_params"]))
+
+
+CKPT = os.path.join(os.path.dirname(__file__), "golden", "checkpoints.json")
+
+
+@pytest.mark.parametrize("name", ["linear_exact", "emb_ln_mb"])
+def test_checkpoints_match_reference_files(cuda, name, tmp_path):
+    """CKFT v1 files (FORMATS.md:176-194) written by the fp64 engine vs the files the reference
+    library wrote after the same run: identical bytes for Linear/half_sq, and identical
+    headers + values within 1e-12 where tanh/exp/log enter."""
+    import base64
+    from paper_2605_21177_b200.engine import ChunkEngine
+    case = CASES[name]
+    g = json.load(open(CKPT))[name]
+    gold = {k: base64.b64decode(v) for k, v in g["files"].items()}
+    eng = ChunkEngine(model_of(case), np.array(g["init_params"]), len(g["batches"][0][next(iter(g["batches"][0]))]),
+                      options_of(case, "fp64"))
+    bs = [eng.stage({k: np.asarray(v, dtype=np.int32 if k in ("tokens", "labels") else np.float64)
+                     for k, v in b.items()}, device=True) for b in g["batches"]]
+    cursor = 0
+    for t in range(case["steps"]):
+        mbs = []
+        for _ in range(case["micro_batches"]):
+            mbs.append(bs[cursor])
+            cursor = (cursor + 1) % len(bs)
+        eng.step(mbs)
+    eng.finish()
+    eng.write_checkpoints(str(tmp_path))
+    for fn, want in gold.items():
+        got = (tmp_path / fn).read_bytes()
+        assert len(got) == len(want) and got[:36] == want[:36]  # magic, version, hash, chunk, n, E
+        if name == "linear_exact":
+            assert got == want
+        else:
+            a = np.frombuffer(got[36:], np.float64)
+            b = np.frombuffer(want[36:], np.float64)
+            assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+
+
+def test_checkpoint_resume_continues_bit_identically(cuda, tmp_path):
+    """Run 9 steps straight vs 3 steps -> checkpoint -> new engine resumes -> 6 steps (fp64):
+    the resumed run reproduces the straight run's parameters exactly.  Restoring under a
+    different plan is refused by the hash guard (optimizer.cpp:241-243)."""
+    from paper_2605_21177_b200.engine import ChunkEngine, Error
+    case = CASES["linear_exact"]
+    bsz = 12
+    opts = options_of(case, "fp64")
+    bs_np = batches_of(case)
+
+    def run(eng, steps, start):
+        staged = [eng.stage(b, device=True) for b in bs_np]
+        for t in range(start, start + steps):
+            eng.step([staged[t % len(staged)]])
+        eng.finish()
+
+    full = ChunkEngine(model_of(case), np.array(case["init_params"]), bsz, opts)
+    run(full, 9, 0)
+    opts3 = options_of(case, "fp64")
+    opts3.schedule.total_steps = 3
+    a = ChunkEngine(model_of(case), np.array(case["init_params"]), bsz, opts3)
+    run(a, 3, 0)
+    a.write_checkpoints(str(tmp_path))
+    opts6 = options_of(case, "fp64")
+    opts6.schedule.total_steps = 6
+    b = ChunkEngine(model_of(case), np.array(case["init_params"]), bsz, opts6)
+    b.read_checkpoints(str(tmp_path))
+    run(b, 6, 3)  # T=1, K=3: after 3 steps the rotation is back at chunk 0
+    assert np.array_equal(b.params(), full.params())
+    other = options_of(case, "fp64")
+    other.schedule.K = 2
+    c = ChunkEngine(model_of(case), np.array(case["init_params"]), bsz, other)
+    with pytest.raises(Error, match="plan hash mismatch"):
+        c.read_checkpoints(str(tmp_path))
