@@ -313,9 +313,23 @@ typedef struct {
 
 typedef struct cft_engine cft_engine;
 
+/* Llama-3-shaped decoder (the build's extension; the reference has no such
+ * model): embed, layers x {attn_norm, wq, wk, wv, wo, mlp_norm, w1, w3, w2}, norm, lm_head;
+ * GQA causal attention with RoPE, SwiGLU, RMSNorm, next-token softmax_ce.  bf16 only.
+ * Batches: tokens [batch_rows x seq] and labels [batch_rows x seq] (int32). */
+typedef struct {
+  int32_t layers, d, heads, kv_heads, head_dim, ffn, vocab, seq;
+  double eps, rope_theta;
+} cft_llama_spec;
+
 /* init_params: every tensor, registration order, row-major, fp64 (Model::snapshot_params). */
 int cft_engine_create(const cft_layer_spec* layers, int n_layers, const cft_engine_config* cfg,
                       const double* init_params, cft_stream_t stream, cft_engine** out);
+/* init_params may be NULL: parameters are then initialised on the device from `seed` with
+ * the reference's rule U(-0.5,0.5)/sqrt(cols), gains 1 (model.cpp:99-117). */
+int cft_engine_create_llama(const cft_llama_spec* spec, const cft_engine_config* cfg,
+                            const double* init_params, uint64_t seed, cft_stream_t stream,
+                            cft_engine** out);
 void cft_engine_destroy(cft_engine* e);
 /* One full step = step_begin, forward_backward per micro-batch, step_end. */
 int cft_engine_step(cft_engine* e, const cft_batch* batches);

@@ -14,6 +14,7 @@
 #include <limits>
 
 #include "cft_common.h"
+#include "attn.h"
 #include "kernels.h"
 
 namespace cft {
@@ -95,6 +96,14 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
     max_width_ = std::max({max_width_, L.in_w, L.out_w});
     layers_.push_back(L);
   }
+  (void)rows;
+  setup(init_params, 0, stream);
+}
+
+void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream) {
+  const int64_t rows = cfg_.batch_rows;
+  CFT_CHECK(init_params != nullptr || kind_ == kLlamaModel,
+            "engine: initial parameters required for this model");
 
   // ---- plan + scheduler (partition.cpp:125-198, schedule.cpp:17-26) ----
   std::vector<host::TensorInfo> infos;
@@ -137,6 +146,7 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
   // ---- per-chunk slice tables (plan order = state/aux layout) ----
   chunk_slices_.resize(cfg_.K);
   lowest_layer_.assign(cfg_.K, static_cast<int>(layers_.size()));
+  stop_id_.assign(cfg_.K, static_cast<int>(tensors_.size()));
   n_local_.assign(cfg_.K, 0);
   for (int c = 0; c < cfg_.K; ++c) {
     int64_t off = 0;
@@ -148,6 +158,7 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
       off += r.count;
       max_slice_ = std::max(max_slice_, r.count);
       lowest_layer_[c] = std::min(lowest_layer_[c], t.layer);
+      stop_id_[c] = std::min(stop_id_[c], s.tensor_id);
     }
     max_chunk_ = std::max(max_chunk_, off);
   }
@@ -155,33 +166,39 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
   // ---- device memory (all allocated once; nothing is allocated per step) ----
   const size_t E = esz(), S = ssz();
   alloc(&params_, param_elems_ * E);
-  for (size_t li = 0; li < layers_.size(); ++li) {
-    Layer& L = layers_[li];
-    alloc(&L.x_saved, rows * L.out_w * E);  // this layer's output (= next layer's input)
-    if (L.spec.type == kLayerNorm) {
-      alloc(&L.mean, rows * S);
-      alloc(&L.rstd, rows * S);
-    }
-  }
-  y_out_ = layers_.back().x_saved;
-  alloc(&act_[0], rows * max_width_ * E);
-  alloc(&act_[1], rows * max_width_ * E);
   alloc(&aux_, max_chunk_ * S);
   CFT_CUDA(cudaMemset(aux_, 0, max_chunk_ * S));
-  if (cfg_.dtype == CFT_F64)
-    alloc(&scratch_, std::max<int64_t>(max_slice_, rows * std::max<int64_t>(max_width_, 1)) * 8);
-  const Layer& first = layers_.front();
-  for (int k = 0; k < 2; ++k) {
-    void* p;
-    if (first.spec.type == kEmbedding) {
-      alloc(&p, rows * std::max(1, first.spec.c) * sizeof(int32_t));
-      in_tokens_[k] = static_cast<int32_t*>(p);
-    } else {
-      alloc(&in_x_[k], rows * first.in_w * E);
+  if (kind_ == kLlamaModel) {
+    llama_alloc();
+  } else {
+    for (size_t li = 0; li < layers_.size(); ++li) {
+      Layer& L = layers_[li];
+      alloc(&L.x_saved, rows * L.out_w * E);  // this layer's output (= next layer's input)
+      if (L.spec.type == kLayerNorm) {
+        alloc(&L.mean, rows * S);
+        alloc(&L.rstd, rows * S);
+      }
     }
-    alloc(&in_target_[k], rows * layers_.back().out_w * E);
-    alloc(&p, rows * sizeof(int32_t));
-    in_labels_[k] = static_cast<int32_t*>(p);
+    y_out_ = layers_.back().x_saved;
+    alloc(&act_[0], rows * max_width_ * E);
+    alloc(&act_[1], rows * max_width_ * E);
+    if (cfg_.dtype == CFT_F64)
+      alloc(&scratch_, std::max<int64_t>(max_slice_, rows * std::max<int64_t>(max_width_, 1)) * 8);
+    const Layer& first = layers_.front();
+    for (int k = 0; k < 2; ++k) {
+      void* p;
+      if (first.spec.type == kEmbedding) {
+        alloc(&p, rows * std::max(1, first.spec.c) * sizeof(int32_t));
+        in_tokens_[k] = static_cast<int32_t*>(p);
+      } else {
+        alloc(&in_x_[k], rows * first.in_w * E);
+      }
+      alloc(&in_target_[k], rows * layers_.back().out_w * E);
+      alloc(&p, rows * sizeof(int32_t));
+      in_labels_[k] = static_cast<int32_t*>(p);
+    }
+  }
+  for (int k = 0; k < 2; ++k) {
     CFT_CUDA(cudaEventCreateWithFlags(&in_ready_[k], cudaEventDisableTiming));
     CFT_CUDA(cudaEventCreateWithFlags(&in_free_[k], cudaEventDisableTiming));
   }
@@ -221,6 +238,42 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
   CFT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_flags_), 2 * sizeof(unsigned long long),
                          cudaHostAllocDefault));
 
+  const int n_slots = cfg_.offload ? 3 : 0;
+  for (int i = 0; i < n_slots; ++i) {
+    for (auto& st : slots_[i].st) alloc(&st, max_chunk_ * S);
+    CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].ready, cudaEventDisableTiming));
+    CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].free, cudaEventDisableTiming));
+  }
+  host_states_.assign(cfg_.K, nullptr);
+
+  if (!init_params) {
+    // ---- device-side init (models too large for a host fp64 copy): per plan slice, the
+    // fp32 master and the bf16 parameter from the same counter-hash value; m = v = 0 ----
+    CFT_CHECK(cfg_.dtype == CFT_BF16, "engine: device init needs the bf16 path");
+    float* tmp;
+    CFT_CUDA(cudaMalloc(reinterpret_cast<void**>(&tmp), max_chunk_ * 3 * sizeof(float)));
+    for (int c = 0; c < cfg_.K; ++c) {
+      const int64_t n = plan_.chunks[c].elements;
+      CFT_CUDA(cudaMemsetAsync(tmp, 0, n * 3 * sizeof(float), stream_));
+      for (const auto& s : chunk_slices_[c]) {
+        const Tensor& t = tensors_[s.tensor];
+        llama::init_slice(tmp + s.aux_off, static_cast<__nv_bfloat16*>(params_) + s.param_off,
+                          s.count, seed, s.tensor, s.rb * t.cols, t.cols, t.cols == 1, stream_);
+      }
+      void* buf;
+      if (cfg_.offload) CFT_CUDA(cudaHostAlloc(&buf, n * 3 * S, cudaHostAllocDefault));
+      else alloc(&buf, n * 3 * S);
+      host_states_[c] = buf;
+      CFT_CUDA(cudaMemcpyAsync(buf, tmp, n * 3 * S,
+                               cfg_.offload ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                               stream_));
+      CFT_CUDA(cudaStreamSynchronize(stream_));
+    }
+    cudaFree(tmp);
+    CFT_CUDA(cudaDeviceSynchronize());
+    return;
+  }
+
   // ---- parameters: fp64 init -> compute dtype, in pieces ----
   {
     const int64_t piece = 1 << 24;
@@ -240,13 +293,6 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
   }
 
   // ---- optimizer state: masters from the init params, m = v = 0 (optimizer.cpp:77-92) ----
-  const int n_slots = cfg_.offload ? 3 : 0;
-  for (int i = 0; i < n_slots; ++i) {
-    for (auto& st : slots_[i].st) alloc(&st, max_chunk_ * S);
-    CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].ready, cudaEventDisableTiming));
-    CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].free, cudaEventDisableTiming));
-  }
-  host_states_.assign(cfg_.K, nullptr);
   for (int c = 0; c < cfg_.K; ++c) {
     const int64_t n = plan_.chunks[c].elements;
     std::vector<double> master(n);
@@ -430,6 +476,11 @@ int Engine::step_begin() {
 
 void Engine::forward_backward(const Batch& b, int mb) {
   CFT_CHECK(active_ >= 0, "scheduler: step_end before step_begin");
+  if (kind_ == kLlamaModel) {
+    llama_forward_backward(b, mb);
+    ++mb_done_;
+    return;
+  }
   const int64_t rows = cfg_.batch_rows;
   const size_t E = esz();
   cudaStream_t s = stream_;

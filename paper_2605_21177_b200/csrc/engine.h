@@ -28,6 +28,9 @@
 #include "host/plan.h"
 
 namespace cft {
+namespace attn {
+class Context;
+}
 
 struct LayerSpec {
   int type = 0;  // 0 linear, 1 embedding, 2 layernorm, 3 tanh
@@ -56,6 +59,16 @@ struct EngineConfig {
   double grad_scale = 1.0;  // extra factor folded into the mean (e.g. 1/world for DP)
 };
 
+// Llama-3-shaped decoder: embedding, L x [RMSNorm, GQA attention with
+// RoPE, RMSNorm, SwiGLU MLP] with residuals, final RMSNorm, untied lm_head, next-token CE.
+// Registration order per layer: attn_norm, wq, wk, wv, wo, mlp_norm, w1, w3, w2 (so wq|wk|wv
+// and w1|w3 are contiguous in the parameter arena and run as single stacked GEMMs).
+struct LlamaSpec {
+  int layers = 2, d = 256, heads = 4, kv_heads = 2, head_dim = 64, ffn = 768, vocab = 1024,
+      seq = 128;
+  double eps = 1e-5, rope_theta = 500000.0;
+};
+
 struct Batch {
   const void* x = nullptr;          // rows x in (compute dtype) for a Linear/LayerNorm-first model
   const int32_t* tokens = nullptr;  // rows x seq for an Embedding-first model
@@ -67,6 +80,10 @@ struct Batch {
 class Engine {
  public:
   Engine(const std::vector<LayerSpec>& layers, const EngineConfig& cfg, const double* init_params,
+         cudaStream_t stream);
+  // Llama decoder; init_params may be null: parameters are then initialised on the device
+  // from `seed` (U(-0.5,0.5)/sqrt(cols), gains 1 -- model.cpp:99-117's rule).
+  Engine(const LlamaSpec& spec, const EngineConfig& cfg, const double* init_params, uint64_t seed,
          cudaStream_t stream);
   ~Engine();
 
@@ -131,7 +148,25 @@ class Engine {
   };
 
   void alloc(void** p, size_t bytes);
+  void setup(const double* init_params, uint64_t seed, cudaStream_t stream);
+  void llama_alloc();
+  void llama_forward_backward(const Batch& b, int mb);
   int slot_of(int chunk) const;
+
+  enum Kind { kSequential = 0, kLlamaModel = 1 };
+  Kind kind_ = kSequential;
+  LlamaSpec ls_;
+  struct LlamaLayerBufs {
+    void *x, *a, *qkv, *o, *h, *m, *ug, *s;  // bf16 activations saved for the backward
+    float *lse, *rstd1, *rstd2;
+  };
+  std::vector<LlamaLayerBufs> lb_;
+  void *l_xf_ = nullptr, *l_logits_ = nullptr;
+  float* l_rstdf_ = nullptr;
+  void *l_gx_ = nullptr, *l_gh_ = nullptr, *l_da_ = nullptr, *l_do_ = nullptr, *l_dxf_ = nullptr,
+       *l_ds_ = nullptr, *l_dug_ = nullptr, *l_dqkv_ = nullptr;
+  std::vector<int> stop_id_;  // per chunk: lowest registered tensor id among its slices
+  std::unique_ptr<attn::Context> attn_;
   int take_free_slot(int avoid1, int avoid2);
   void load_chunk(int chunk, bool for_prefetch);
   void offload_chunk(int chunk);

@@ -10,6 +10,28 @@ struct cft_engine {
 
 using cft::guarded;
 
+static cft::EngineConfig to_config(const cft_engine_config* c) {
+  cft::EngineConfig cfg;
+  cfg.dtype = c->dtype;
+  cfg.loss = c->loss;
+  cfg.optim = c->optim;
+  cfg.micro_batches = c->micro_batches;
+  cfg.batch_rows = c->batch_rows;
+  cfg.plan_mode = c->plan_mode;
+  cfg.K = c->K;
+  cfg.T = c->T;
+  cfg.total_steps = c->total_steps;
+  cfg.prefetch = c->prefetch;
+  cfg.offload = c->offload;
+  cfg.bandwidth_bytes_per_step = c->bandwidth_bytes_per_step;
+  cfg.budget_bytes = c->budget_bytes;
+  cfg.hyper = c->hyper;
+  cfg.full_backward = c->full_backward;
+  cfg.check_every_step = c->check_every_step;
+  cfg.grad_scale = c->grad_scale == 0.0 ? 1.0 : c->grad_scale;
+  return cfg;
+}
+
 extern "C" {
 
 int cft_engine_create(const cft_layer_spec* layers, int n_layers, const cft_engine_config* c,
@@ -19,24 +41,7 @@ int cft_engine_create(const cft_layer_spec* layers, int n_layers, const cft_engi
     for (int i = 0; i < n_layers; ++i)
       specs[i] = {layers[i].type, layers[i].a, layers[i].b, layers[i].c, layers[i].bias,
                   layers[i].eps};
-    cft::EngineConfig cfg;
-    cfg.dtype = c->dtype;
-    cfg.loss = c->loss;
-    cfg.optim = c->optim;
-    cfg.micro_batches = c->micro_batches;
-    cfg.batch_rows = c->batch_rows;
-    cfg.plan_mode = c->plan_mode;
-    cfg.K = c->K;
-    cfg.T = c->T;
-    cfg.total_steps = c->total_steps;
-    cfg.prefetch = c->prefetch;
-    cfg.offload = c->offload;
-    cfg.bandwidth_bytes_per_step = c->bandwidth_bytes_per_step;
-    cfg.budget_bytes = c->budget_bytes;
-    cfg.hyper = c->hyper;
-    cfg.full_backward = c->full_backward;
-    cfg.check_every_step = c->check_every_step;
-    cfg.grad_scale = c->grad_scale == 0.0 ? 1.0 : c->grad_scale;
+    cft::EngineConfig cfg = to_config(c);
     *out = new cft_engine{
         std::make_unique<cft::Engine>(specs, cfg, init_params, static_cast<cudaStream_t>(stream))};
   });
@@ -176,3 +181,24 @@ int cft_engine_read_checkpoints(cft_engine* e, const char* dir) {
 }
 
 }  // extern "C"
+
+extern "C" int cft_engine_create_llama(const cft_llama_spec* s, const cft_engine_config* c,
+                                       const double* init_params, uint64_t seed,
+                                       cft_stream_t stream, cft_engine** out) {
+  return guarded([&] {
+    cft::LlamaSpec spec;
+    spec.layers = s->layers;
+    spec.d = s->d;
+    spec.heads = s->heads;
+    spec.kv_heads = s->kv_heads;
+    spec.head_dim = s->head_dim;
+    spec.ffn = s->ffn;
+    spec.vocab = s->vocab;
+    spec.seq = s->seq;
+    spec.eps = s->eps;
+    spec.rope_theta = s->rope_theta;
+    cft::EngineConfig cfg = to_config(c);
+    *out = new cft_engine{std::make_unique<cft::Engine>(spec, cfg, init_params, seed,
+                                                       static_cast<cudaStream_t>(stream))};
+  });
+}

@@ -40,6 +40,7 @@ struct Args {
   void* C;
   long long ldc;
   int epi;
+  const void* R;  // bf16 residual added in the epilogue (same layout as C; may alias C)
 };
 
 template <int BN>
@@ -93,14 +94,18 @@ __device__ __forceinline__ void store16(const Args& args, long long rbase, int c
     }
   } else {
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.C) + rbase + col;
-    const bool vec = full16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    const __nv_bfloat16* res =
+        args.R ? static_cast<const __nv_bfloat16*>(args.R) + rbase + col
+               : (args.epi == kEpiBf16Add ? out : nullptr);
+    const bool vec = full16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(res) & 15) == 0);
     if (vec) {
 #pragma unroll
       for (int j = 0; j < 16; j += 8) {
         uint4 pk;
         uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
-        if (args.epi == kEpiBf16Add) {
-          const uint4 old = *reinterpret_cast<const uint4*>(out + j);
+        if (res) {
+          const uint4 old = *reinterpret_cast<const uint4*>(res + j);
           const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&old);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -122,7 +127,7 @@ __device__ __forceinline__ void store16(const Args& args, long long rbase, int c
     } else {
       for (int j = 0; j < 16 && col + j < args.N; ++j) {
         float a0 = __uint_as_float(r[j]);
-        if (args.epi == kEpiBf16Add) a0 += __bfloat162float(out[j]);
+        if (res) a0 += __bfloat162float(res[j]);
         out[j] = __float2bfloat16_rn(a0);
       }
     }
@@ -571,7 +576,7 @@ void set_policy(int p) { g_policy = p; }
 
 // Y = X W^T, bf16 out (epi kEpiBf16) -- forward.
 void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
-                void* y, cudaStream_t stream) {
+                void* y, cudaStream_t stream, const void* residual) {
   Args a{};
   a.M = static_cast<int>(n_tok);
   a.N = static_cast<int>(out_dim);
@@ -579,6 +584,7 @@ void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int
   a.C = y;
   a.ldc = out_dim;
   a.epi = kEpiBf16;
+  a.R = residual;
   const CUtensorMap ta = cached_map(x, in_dim, n_tok, in_dim, 64, BM);
   if (use_pairs(a.M, a.N, a.K, false)) {
     fill_units(a, 256, 256, num_sms() / 2, 0.45, false);

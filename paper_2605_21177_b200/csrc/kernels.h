@@ -11,7 +11,7 @@ namespace cft {
 
 namespace tc {  // gemm_tc.cu: bf16 tcgen05/TMEM GEMMs
 void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
-                void* y, cudaStream_t stream);
+                void* y, cudaStream_t stream, const void* residual = nullptr);
 void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w, int64_t in_dim,
                   void* dx, int beta, cudaStream_t stream);
 void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const void* x,
@@ -83,5 +83,22 @@ void flag_nonfinite_loss(double* stats_row, cudaStream_t s);
 void count_in_range(const int32_t* tokens, long long n, long long lo, long long hi,
                     long long* bad, cudaStream_t s);
 }  // namespace layers
+
+namespace llama {  // llama_kernels.cu
+void rms_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, long long rows, int d, float eps,
+             __nv_bfloat16* y, float* rstd, cudaStream_t s);
+void rms_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd,
+             const __nv_bfloat16* g, const __nv_bfloat16* res, long long rows, int d,
+             __nv_bfloat16* out, cudaStream_t s);
+void rms_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd,
+                long long rows, int d, long long rb, long long re, float* out, cudaStream_t s);
+void rope(__nv_bfloat16* qkv, long long tokens, int seq, int heads, int hd, int ld, float theta,
+          bool backward, cudaStream_t s);
+void swiglu_fwd(const __nv_bfloat16* ug, long long rows, int F, __nv_bfloat16* out, cudaStream_t s);
+void swiglu_bwd(const __nv_bfloat16* ds, const __nv_bfloat16* ug, long long rows, int F,
+                __nv_bfloat16* dug, cudaStream_t s);
+void init_slice(float* master, __nv_bfloat16* param, long long count, uint64_t seed, int tensor,
+                long long elem0, long long cols, bool is_gain, cudaStream_t s);
+}  // namespace llama
 
 }  // namespace cft

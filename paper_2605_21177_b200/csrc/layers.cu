@@ -184,6 +184,7 @@ __global__ void loss_ce_kernel(const T* y, const int32_t* labels, long long cols
     if (threadIdx.x == 0) atomicAdd(bad_label, 1ull);
     return;
   }
+  const float ylab = ldf(yr + label);  // read before dy may overwrite y (in-place use)
   float mx = -INFINITY;
   for (long long c = threadIdx.x; c < cols; c += blockDim.x) mx = fmaxf(mx, ldf(yr + c));
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -201,7 +202,7 @@ __global__ void loss_ce_kernel(const T* y, const int32_t* labels, long long cols
     stf(dy + b * cols + c, (p - (c == label ? 1.f : 0.f)) * inv_rows);
   }
   if (threadIdx.x == 0)
-    atomicAdd(loss, static_cast<double>(-(ldf(yr + label) - mx - logz)) * inv_rows);
+    atomicAdd(loss, static_cast<double>(-(ylab - mx - logz)) * inv_rows);
 }
 
 // fp64 losses for the fp64 engine path (exp/log are CUDA's: <= 1-2 ulp from glibc).

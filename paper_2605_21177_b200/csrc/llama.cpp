@@ -1,0 +1,313 @@
+// llama.cpp -- the chunk-local step for a Llama-3-shaped decoder.
+//
+// Same rotation / plan / gradient-accumulator / fused-AdamW machinery as engine.cpp; this file
+// adds the decoder's forward and the chunk-masked backward over the suffix the active chunk
+// needs.  Tensor registration (and therefore the byte-balanced plan and its hash) follows
+// oracle/shapes.py: embed, per layer {attn_norm, wq, wk, wv, wo, mlp_norm, w1, w3, w2}, norm,
+// lm_head -- for the 8B shape the K = 8/64/128 plan hashes equal the reference's.
+//
+// Backward suffix rule: with `stop` = the lowest registered tensor id in the active chunk
+// (registration order is forward order), a gradient is formed only when some active tensor
+// at or below that point needs it -- the layers below the chunk run forward only, and within
+// the lowest layer only the sub-blocks at or above its lowest active tensor run backward.
+// Dropping that work changes no active gradient (the reference computes it and discards it,
+// autodiff.cpp:307-313).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "attn.h"
+#include "cft_common.h"
+#include "engine.h"
+#include "kernels.h"
+
+namespace cft {
+
+namespace {
+using bf16 = __nv_bfloat16;
+}
+
+Engine::Engine(const LlamaSpec& spec, const EngineConfig& cfg, const double* init_params,
+               uint64_t seed, cudaStream_t stream)
+    : cfg_(cfg) {
+  kind_ = kLlamaModel;
+  ls_ = spec;
+  CFT_CHECK(cfg_.dtype == CFT_BF16, "llama engine: bf16 compute only");
+  CFT_CHECK(cfg_.micro_batches >= 1, "trainer: micro_batches must be at least 1");
+  CFT_CHECK(spec.heads % spec.kv_heads == 0, "llama engine: heads must be a multiple of kv_heads");
+  CFT_CHECK(spec.d % 8 == 0 && spec.ffn % 8 == 0 && spec.head_dim % 8 == 0,
+            "llama engine: dims must be multiples of 8");
+  CFT_CHECK(cfg_.loss == 3, "llama engine: next-token softmax_ce loss");
+  const int64_t d = spec.d, q = int64_t(spec.heads) * spec.head_dim,
+                kv = int64_t(spec.kv_heads) * spec.head_dim;
+  auto add = [&](const std::string& name, int64_t r, int64_t c, int depth) {
+    tensors_.push_back({static_cast<int>(tensors_.size()), name, r, c, param_elems_, depth});
+    param_elems_ += r * c;
+  };
+  add("embed", spec.vocab, d, 0);
+  for (int l = 0; l < spec.layers; ++l) {
+    const std::string p = "L" + std::to_string(l) + ".";
+    add(p + "attn_norm", d, 1, l + 1);
+    add(p + "wq", q, d, l + 1);
+    add(p + "wk", kv, d, l + 1);
+    add(p + "wv", kv, d, l + 1);
+    add(p + "wo", d, q, l + 1);
+    add(p + "mlp_norm", d, 1, l + 1);
+    add(p + "w1", spec.ffn, d, l + 1);
+    add(p + "w3", spec.ffn, d, l + 1);
+    add(p + "w2", d, spec.ffn, l + 1);
+  }
+  add("norm", d, 1, spec.layers + 1);
+  add("lm_head", spec.vocab, d, spec.layers + 1);
+  setup(init_params, seed, stream);
+}
+
+void Engine::llama_alloc() {
+  const LlamaSpec& s = ls_;
+  const int64_t N = int64_t(cfg_.batch_rows) * s.seq;  // tokens per micro-batch
+  const int64_t d = s.d, q = int64_t(s.heads) * s.head_dim,
+                qkv = q + 2 * int64_t(s.kv_heads) * s.head_dim, F = s.ffn;
+  auto A = [&](int64_t elems, size_t es = 2) {
+    void* p;
+    alloc(&p, elems * es);
+    return p;
+  };
+  lb_.resize(s.layers + 1);
+  for (int l = 0; l <= s.layers; ++l) {
+    LlamaLayerBufs& b = lb_[l];
+    b.x = A(N * d);
+    if (l == s.layers) break;  // x[L] only
+    b.a = A(N * d);
+    b.qkv = A(N * qkv);
+    b.o = A(N * q);
+    b.h = A(N * d);
+    b.m = A(N * d);
+    b.ug = A(N * 2 * F);
+    b.s = A(N * F);
+    b.lse = static_cast<float*>(A(int64_t(cfg_.batch_rows) * s.heads * s.seq, 4));
+    b.rstd1 = static_cast<float*>(A(N, 4));
+    b.rstd2 = static_cast<float*>(A(N, 4));
+  }
+  l_xf_ = A(N * d);
+  l_rstdf_ = static_cast<float*>(A(N, 4));
+  l_logits_ = A(N * int64_t(s.vocab));
+  l_gx_ = A(N * d);
+  l_gh_ = A(N * d);
+  l_da_ = A(N * d);
+  l_do_ = A(N * q);
+  l_dxf_ = A(N * d);
+  l_ds_ = A(N * F);
+  l_dug_ = A(N * 2 * F);
+  l_dqkv_ = A(N * qkv);
+  for (int k = 0; k < 2; ++k) {
+    in_tokens_[k] = static_cast<int32_t*>(A(N, 4));
+    in_labels_[k] = static_cast<int32_t*>(A(N, 4));
+  }
+  attn_ = std::make_unique<attn::Context>();
+  attn_->prepare(cfg_.batch_rows, s.heads, s.kv_heads, s.seq, s.head_dim);
+}
+
+void Engine::llama_forward_backward(const Batch& b, int mb) {
+  const LlamaSpec& S = ls_;
+  cudaStream_t st = stream_;
+  const int B = cfg_.batch_rows, L = S.layers;
+  const int64_t N = int64_t(B) * S.seq;
+  const int64_t d = S.d, Q = int64_t(S.heads) * S.head_dim, KV = int64_t(S.kv_heads) * S.head_dim,
+                QKV = Q + 2 * KV, F = S.ffn, V = S.vocab;
+  const int ld = static_cast<int>(QKV);
+  auto P = [&](int tensor) { return static_cast<const bf16*>(param_ptr(tensor)); };
+  auto id = [&](int l, int k) { return 1 + 9 * l + k; };  // k: 0 an,1 q,2 k,3 v,4 o,5 mn,6 w1,7 w3,8 w2
+  const int norm_id = 1 + 9 * L, head_id = 2 + 9 * L;
+  const auto& slices = chunk_slices_[active_];
+  const int stop = stop_id_[active_];
+  auto slice_of = [&](int tensor) -> const SliceRt* {
+    for (const auto& s : slices)
+      if (s.tensor == tensor) return &s;
+    return nullptr;
+  };
+  auto aux_at = [&](const SliceRt* s) { return static_cast<float*>(aux_) + s->aux_off; };
+  // sliced weight gradient of a (possibly stacked) weight; `row0` = the tensor's first row
+  // within the stacked operand
+  auto wgrad = [&](int tensor, const void* dy, int64_t out_dim, const void* x, int64_t in_dim,
+                   int64_t row0) {
+    const SliceRt* s = slice_of(tensor);
+    if (!s) return;
+    pb(kWgrad);
+    tc::linear_wgrad_slice(dy, N, out_dim, x, in_dim, row0 + s->rb, row0 + s->re, aux_at(s), 1, st);
+    pe();
+  };
+
+  // ---- inputs ----
+  pb(kInputs);
+  const int32_t* tok;
+  const int32_t* lab;
+  if (b.on_device) {
+    tok = b.tokens;
+    lab = b.labels;
+  } else {
+    const int k = static_cast<int>(uploads_++ & 1);
+    CFT_CUDA(cudaStreamWaitEvent(in_stream_, in_free_[k], 0));
+    CFT_CUDA(cudaMemcpyAsync(in_tokens_[k], b.tokens, N * 4, cudaMemcpyHostToDevice, in_stream_));
+    CFT_CUDA(cudaMemcpyAsync(in_labels_[k], b.labels, N * 4, cudaMemcpyHostToDevice, in_stream_));
+    CFT_CUDA(cudaEventRecord(in_ready_[k], in_stream_));
+    CFT_CUDA(cudaStreamWaitEvent(st, in_ready_[k], 0));
+    tok = in_tokens_[k];
+    lab = in_labels_[k];
+    staged_slot_ = k;
+  }
+  CFT_CHECK(tok != nullptr && lab != nullptr, "forward: token batch required");
+  layers::count_in_range(tok, N, 0, V, reinterpret_cast<long long*>(flags_ + 1), st);
+  pe();
+
+  // ---- forward ----
+  pb(kFwdOther);
+  if (cft_embedding_gather(CFT_BF16, P(0), d, tok, N, lb_[0].x, st) != CFT_OK)
+    throw Error(last_error());
+  pe();
+  for (int l = 0; l < L; ++l) {
+    LlamaLayerBufs& z = lb_[l];
+    pb(kFwdOther);
+    llama::rms_fwd(static_cast<bf16*>(z.x), P(id(l, 0)), N, S.d, (float)S.eps,
+                   static_cast<bf16*>(z.a), z.rstd1, st);
+    pe();
+    pb(kFwdGemm);
+    tc::linear_fwd(z.a, N, d, P(id(l, 1)), QKV, z.qkv, st);  // wq|wk|wv stacked
+    pe();
+    pb(kFwdOther);
+    llama::rope(static_cast<bf16*>(z.qkv), N, S.seq, S.heads, S.head_dim, ld, (float)S.rope_theta,
+                false, st);
+    llama::rope(static_cast<bf16*>(z.qkv) + Q, N, S.seq, S.kv_heads, S.head_dim, ld,
+                (float)S.rope_theta, false, st);
+    attn_->forward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, z.lse, st);
+    pe();
+    pb(kFwdGemm);
+    tc::linear_fwd(z.o, N, Q, P(id(l, 4)), d, z.h, st, z.x);  // h = x + o Wo^T
+    pe();
+    pb(kFwdOther);
+    llama::rms_fwd(static_cast<bf16*>(z.h), P(id(l, 5)), N, S.d, (float)S.eps,
+                   static_cast<bf16*>(z.m), z.rstd2, st);
+    pe();
+    pb(kFwdGemm);
+    tc::linear_fwd(z.m, N, d, P(id(l, 6)), 2 * F, z.ug, st);  // w1|w3 stacked
+    pe();
+    pb(kFwdOther);
+    llama::swiglu_fwd(static_cast<bf16*>(z.ug), N, S.ffn, static_cast<bf16*>(z.s), st);
+    pe();
+    pb(kFwdGemm);
+    tc::linear_fwd(z.s, N, F, P(id(l, 8)), d, lb_[l + 1].x, st, z.h);  // x' = h + s W2^T
+    pe();
+  }
+  pb(kFwdOther);
+  llama::rms_fwd(static_cast<bf16*>(lb_[L].x), P(norm_id), N, S.d, (float)S.eps,
+                 static_cast<bf16*>(l_xf_), l_rstdf_, st);
+  pe();
+  pb(kFwdGemm);
+  tc::linear_fwd(l_xf_, N, d, P(head_id), V, l_logits_, st);
+  pe();
+
+  // ---- next-token CE (autodiff.cpp:205-225); dlogits written in place ----
+  pb(kLoss);
+  layers::loss<bf16>(3, static_cast<bf16*>(l_logits_), nullptr, lab, N, V,
+                     static_cast<bf16*>(l_logits_), stats_ + t_ * 4 + 3, flags_, st);
+  pe();
+
+  // ---- chunk-masked backward over the suffix ----
+  auto need = [&](int tensor) { return stop <= tensor; };    // gradient at/above `tensor`
+  auto below = [&](int tensor) { return stop < tensor; };    // something below `tensor`
+  const bf16* dlog = static_cast<const bf16*>(l_logits_);
+  wgrad(head_id, dlog, V, l_xf_, d, 0);
+  if (need(norm_id)) {
+    pb(kDgrad);
+    tc::linear_dgrad(dlog, N, V, P(head_id), d, l_dxf_, 0, st);
+    pe();
+    if (const SliceRt* s = slice_of(norm_id)) {
+      pb(kBwdOther);
+      llama::rms_dgamma(static_cast<bf16*>(l_dxf_), static_cast<bf16*>(lb_[L].x), l_rstdf_, N,
+                        S.d, s->rb, s->re, aux_at(s), st);
+      pe();
+    }
+  }
+  if (below(norm_id)) {
+    pb(kBwdOther);
+    llama::rms_bwd(static_cast<bf16*>(l_dxf_), static_cast<bf16*>(lb_[L].x), l_rstdf_, P(norm_id),
+                   nullptr, N, S.d, static_cast<bf16*>(l_gx_), st);
+    pe();
+  }
+  for (int l = L - 1; l >= 0 && below(id(l, 8) + 1); --l) {
+    LlamaLayerBufs& z = lb_[l];
+    // x_{l+1} = h + s W2^T      (GX = dL/dx_{l+1})
+    wgrad(id(l, 8), l_gx_, d, z.s, F, 0);
+    if (!need(id(l, 7))) break;
+    pb(kDgrad);
+    tc::linear_dgrad(l_gx_, N, d, P(id(l, 8)), F, l_ds_, 0, st);
+    pe();
+    pb(kBwdOther);
+    llama::swiglu_bwd(static_cast<bf16*>(l_ds_), static_cast<bf16*>(z.ug), N, S.ffn,
+                      static_cast<bf16*>(l_dug_), st);
+    pe();
+    wgrad(id(l, 6), l_dug_, 2 * F, z.m, d, 0);  // w1 rows [0,F) of the stack
+    wgrad(id(l, 7), l_dug_, 2 * F, z.m, d, F);  // w3 rows [F,2F)
+    if (!need(id(l, 5))) break;
+    pb(kDgrad);
+    tc::linear_dgrad(l_dug_, N, 2 * F, P(id(l, 6)), d, l_da_, 0, st);  // dM (reuses da buffer)
+    pe();
+    if (const SliceRt* s = slice_of(id(l, 5))) {
+      pb(kBwdOther);
+      llama::rms_dgamma(static_cast<bf16*>(l_da_), static_cast<bf16*>(z.h), z.rstd2, N, S.d, s->rb,
+                        s->re, aux_at(s), st);
+      pe();
+    }
+    if (!below(id(l, 5))) break;
+    pb(kBwdOther);  // GH = GX + rms_bwd(dM)
+    llama::rms_bwd(static_cast<bf16*>(l_da_), static_cast<bf16*>(z.h), z.rstd2, P(id(l, 5)),
+                   static_cast<bf16*>(l_gx_), N, S.d, static_cast<bf16*>(l_gh_), st);
+    pe();
+    // h = x + o Wo^T
+    wgrad(id(l, 4), l_gh_, d, z.o, Q, 0);
+    if (!need(id(l, 3))) break;
+    pb(kDgrad);
+    tc::linear_dgrad(l_gh_, N, d, P(id(l, 4)), Q, l_do_, 0, st);
+    pe();
+    pb(kBwdOther);
+    attn_->backward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, l_do_, z.lse, l_dqkv_, st);
+    llama::rope(static_cast<bf16*>(l_dqkv_), N, S.seq, S.heads, S.head_dim, ld, (float)S.rope_theta,
+                true, st);
+    llama::rope(static_cast<bf16*>(l_dqkv_) + Q, N, S.seq, S.kv_heads, S.head_dim, ld,
+                (float)S.rope_theta, true, st);
+    pe();
+    wgrad(id(l, 1), l_dqkv_, QKV, z.a, d, 0);
+    wgrad(id(l, 2), l_dqkv_, QKV, z.a, d, Q);
+    wgrad(id(l, 3), l_dqkv_, QKV, z.a, d, Q + KV);
+    if (!need(id(l, 0))) break;
+    pb(kDgrad);
+    tc::linear_dgrad(l_dqkv_, N, QKV, P(id(l, 1)), d, l_da_, 0, st);  // dA
+    pe();
+    if (const SliceRt* s = slice_of(id(l, 0))) {
+      pb(kBwdOther);
+      llama::rms_dgamma(static_cast<bf16*>(l_da_), static_cast<bf16*>(z.x), z.rstd1, N, S.d, s->rb,
+                        s->re, aux_at(s), st);
+      pe();
+    }
+    if (!below(id(l, 0))) break;
+    pb(kBwdOther);  // GX = GH + rms_bwd(dA)
+    llama::rms_bwd(static_cast<bf16*>(l_da_), static_cast<bf16*>(z.x), z.rstd1, P(id(l, 0)),
+                   static_cast<bf16*>(l_gh_), N, S.d, static_cast<bf16*>(l_gx_), st);
+    pe();
+  }
+  if (const SliceRt* s = slice_of(0)) {  // embedding rows: one pass over positions
+    pb(kBwdOther);
+    if (cft_embedding_scatter_slice(CFT_BF16, l_gx_, d, tok, N, s->rb, s->re, aux_at(s), nullptr,
+                                    st) != CFT_OK)
+      throw Error(last_error());
+    pe();
+  }
+  if (staged_slot_ >= 0) {
+    CFT_CUDA(cudaEventRecord(in_free_[staged_slot_], st));
+    staged_slot_ = -1;
+  }
+  (void)mb;
+}
+
+}  // namespace cft

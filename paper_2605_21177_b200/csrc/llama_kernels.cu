@@ -1,0 +1,269 @@
+// llama_kernels.cu -- the decoder glue around the chunk-local GEMMs:
+// RMSNorm forward / backward / sliced dgamma, rotary embedding, SwiGLU, and device-side
+// parameter initialisation for models too large to initialise on the host.
+//
+// The reference has no Llama layers; these follow the standard definitions and are
+// checked against a plain PyTorch fp32 reference (tests/test_gpu_llama.py).  RMSNorm dgamma is
+// the reference's layernorm_dgamma (kernels_serial.cpp:132-143) with mean = 0 and
+// inv_std = rstd.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "cft_common.h"
+
+namespace cft::llama {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float block_sum(float v) {
+  __shared__ float sh[32];
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) t += sh[i];
+  return t;
+}
+
+// 8 bf16 <-> 8 floats
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 p = __bfloat1622float2(h[i]);
+    f[2 * i] = p.x;
+    f[2 * i + 1] = p.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+// y = x * rstd * gamma, rstd = 1/sqrt(mean(x^2) + eps); one block per row, d % 8 == 0.
+__global__ void rms_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g, int d,
+                               float eps, bf16* __restrict__ y, float* __restrict__ rstd) {
+  const long long r = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + r * d);
+  float ss = 0.f;
+  for (int j = threadIdx.x; j < d / 8; j += blockDim.x) {
+    float f[8];
+    unpack8(xr[j], f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ss += f[e] * f[e];
+  }
+  const float rs = rsqrtf(block_sum(ss) / d + eps);
+  if (threadIdx.x == 0) rstd[r] = rs;
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  uint4* yr = reinterpret_cast<uint4*>(y + r * d);
+  for (int j = threadIdx.x; j < d / 8; j += blockDim.x) {
+    float f[8], gg[8];
+    unpack8(xr[j], f);
+    unpack8(gr[j], gg);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = f[e] * rs * gg[e];
+    yr[j] = pack8(f);
+  }
+}
+
+// dx = res + rstd * (g*dy - xhat * sum(g*dy*xhat)/d), xhat = x*rstd   (out may alias res)
+__global__ void rms_bwd_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                               const float* __restrict__ rstd, const bf16* __restrict__ g,
+                               const bf16* res, int d, bf16* out) {
+  const long long r = blockIdx.x;
+  const float rs = rstd[r];
+  const uint4* dyr = reinterpret_cast<const uint4*>(dy + r * d);
+  const uint4* xr = reinterpret_cast<const uint4*>(x + r * d);
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  float c = 0.f;
+  for (int j = threadIdx.x; j < d / 8; j += blockDim.x) {
+    float a[8], b[8], gg[8];
+    unpack8(dyr[j], a);
+    unpack8(xr[j], b);
+    unpack8(gr[j], gg);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) c += gg[e] * a[e] * b[e] * rs;
+  }
+  c = block_sum(c) / d;
+  const uint4* rr = res ? reinterpret_cast<const uint4*>(res + r * d) : nullptr;
+  uint4* orow = reinterpret_cast<uint4*>(out + r * d);
+  for (int j = threadIdx.x; j < d / 8; j += blockDim.x) {
+    float a[8], b[8], gg[8], o[8];
+    unpack8(dyr[j], a);
+    unpack8(xr[j], b);
+    unpack8(gr[j], gg);
+    if (rr) unpack8(rr[j], o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float v = rs * (gg[e] * a[e] - b[e] * rs * c);
+      o[e] = rr ? o[e] + v : v;
+    }
+    orow[j] = pack8(o);
+  }
+}
+
+// dgamma[j-rb] += sum_b dy[b,j] * x[b,j] * rstd[b]  (layernorm_dgamma with mean = 0)
+__global__ void rms_dgamma_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                  const float* __restrict__ rstd, long long rows, int d,
+                                  long long rb, long long re, float* out) {
+  __shared__ float red[8][33];
+  const long long j = rb + blockIdx.x * 32LL + threadIdx.x % 32;
+  const int part = threadIdx.x / 32;
+  float acc = 0.f;
+  if (j < re)
+    for (long long b = part; b < rows; b += 8)
+      acc += __bfloat162float(dy[b * d + j]) * __bfloat162float(x[b * d + j]) * rstd[b];
+  red[part][threadIdx.x % 32] = acc;
+  __syncthreads();
+  if (part == 0 && j < re) {
+    float s = 0.f;
+    for (int p = 0; p < 8; ++p) s += red[p][threadIdx.x % 32];
+    out[j - rb] += s;
+  }
+}
+
+// Rotary embedding in place on the q and k heads of the fused qkv buffer (rotate-half pairs
+// (i, i + hd/2)); sign = +1 forward, -1 backward (the transpose rotation).
+__global__ void rope_kernel(bf16* qkv, long long tokens, int seq, int heads, int hd, int ld,
+                            float theta, float sign) {
+  const int half = hd / 2;
+  const long long total = tokens * heads * half;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(t % half);
+    const long long th = t / half;
+    const int h = static_cast<int>(th % heads);
+    const long long tok = th / heads;
+    const int pos = static_cast<int>(tok % seq);
+    const float inv = powf(theta, -2.0f * i / hd);
+    float s, c;
+    sincosf(pos * inv, &s, &c);
+    s *= sign;
+    bf16* p = qkv + tok * ld + static_cast<long long>(h) * hd;
+    const float x1 = __bfloat162float(p[i]), x2 = __bfloat162float(p[i + half]);
+    p[i] = __float2bfloat16_rn(x1 * c - x2 * s);
+    p[i + half] = __float2bfloat16_rn(x2 * c + x1 * s);
+  }
+}
+
+__device__ __forceinline__ float sigm(float u) { return 1.f / (1.f + __expf(-u)); }
+
+// s = silu(u) * g over rows laid out [u (F) | g (F)]
+__global__ void swiglu_fwd_kernel(const bf16* __restrict__ ug, long long rows, int F,
+                                  bf16* __restrict__ s) {
+  const long long total = rows * (F / 8);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t / (F / 8);
+    const int j = static_cast<int>(t % (F / 8));
+    float u[8], g[8], o[8];
+    unpack8(reinterpret_cast<const uint4*>(ug + r * 2 * F)[j], u);
+    unpack8(reinterpret_cast<const uint4*>(ug + r * 2 * F + F)[j], g);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = u[e] * sigm(u[e]) * g[e];
+    reinterpret_cast<uint4*>(s + r * F)[j] = pack8(o);
+  }
+}
+
+// [du | dg] from ds: du = ds * g * sig(u) * (1 + u (1 - sig(u))), dg = ds * silu(u)
+__global__ void swiglu_bwd_kernel(const bf16* __restrict__ ds, const bf16* __restrict__ ug,
+                                  long long rows, int F, bf16* __restrict__ dug) {
+  const long long total = rows * (F / 8);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t / (F / 8);
+    const int j = static_cast<int>(t % (F / 8));
+    float d[8], u[8], g[8], du[8], dg[8];
+    unpack8(reinterpret_cast<const uint4*>(ds + r * F)[j], d);
+    unpack8(reinterpret_cast<const uint4*>(ug + r * 2 * F)[j], u);
+    unpack8(reinterpret_cast<const uint4*>(ug + r * 2 * F + F)[j], g);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float sg = sigm(u[e]);
+      du[e] = d[e] * g[e] * sg * (1.f + u[e] * (1.f - sg));
+      dg[e] = d[e] * u[e] * sg;
+    }
+    reinterpret_cast<uint4*>(dug + r * 2 * F)[j] = pack8(du);
+    reinterpret_cast<uint4*>(dug + r * 2 * F + F)[j] = pack8(dg);
+  }
+}
+
+// Device-side init for one plan slice: master (fp32) and the bf16 parameter copy.
+// Weights: U(-0.5, 0.5) / sqrt(cols) from a counter hash (model.cpp:99-117's rule, not its
+// RNG stream); norm gains: 1.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__global__ void init_slice_kernel(float* master, bf16* param, long long count, uint64_t seed,
+                                  int tensor, long long elem0, long long cols, int is_gain) {
+  const float scale = rsqrtf(static_cast<float>(cols));
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    float v;
+    if (is_gain) {
+      v = 1.f;
+    } else {
+      const uint64_t h = mix64(seed ^ mix64((static_cast<uint64_t>(tensor) << 40) + elem0 + i));
+      v = (static_cast<float>(h >> 40) * (1.0f / 16777216.0f) - 0.5f) * scale;
+    }
+    master[i] = v;
+    param[i] = __float2bfloat16_rn(v);
+  }
+}
+
+inline int grid_for(long long n) {
+  return static_cast<int>(std::max<long long>(1, std::min<long long>((n + 255) / 256, num_sms() * 16LL)));
+}
+inline int row_threads(int d) { return std::max(32, std::min(1024, ((d / 8 + 31) / 32) * 32)); }
+
+void rms_fwd(const bf16* x, const bf16* g, long long rows, int d, float eps, bf16* y, float* rstd,
+             cudaStream_t s) {
+  rms_fwd_kernel<<<(unsigned)rows, row_threads(d), 0, s>>>(x, g, d, eps, y, rstd);
+  check_launch("rms_fwd");
+}
+void rms_bwd(const bf16* dy, const bf16* x, const float* rstd, const bf16* g, const bf16* res,
+             long long rows, int d, bf16* out, cudaStream_t s) {
+  rms_bwd_kernel<<<(unsigned)rows, row_threads(d), 0, s>>>(dy, x, rstd, g, res, d, out);
+  check_launch("rms_bwd");
+}
+void rms_dgamma(const bf16* dy, const bf16* x, const float* rstd, long long rows, int d,
+                long long rb, long long re, float* out, cudaStream_t s) {
+  if (re <= rb) return;
+  rms_dgamma_kernel<<<(unsigned)((re - rb + 31) / 32), 256, 0, s>>>(dy, x, rstd, rows, d, rb, re, out);
+  check_launch("rms_dgamma");
+}
+void rope(bf16* qkv, long long tokens, int seq, int heads, int hd, int ld, float theta,
+          bool backward, cudaStream_t s) {
+  rope_kernel<<<grid_for(tokens * heads * hd / 2), 256, 0, s>>>(qkv, tokens, seq, heads, hd, ld,
+                                                                theta, backward ? -1.f : 1.f);
+  check_launch("rope");
+}
+void swiglu_fwd(const bf16* ug, long long rows, int F, bf16* out, cudaStream_t s) {
+  swiglu_fwd_kernel<<<grid_for(rows * F / 8), 256, 0, s>>>(ug, rows, F, out);
+  check_launch("swiglu_fwd");
+}
+void swiglu_bwd(const bf16* ds, const bf16* ug, long long rows, int F, bf16* dug, cudaStream_t s) {
+  swiglu_bwd_kernel<<<grid_for(rows * F / 8), 256, 0, s>>>(ds, ug, rows, F, dug);
+  check_launch("swiglu_bwd");
+}
+void init_slice(float* master, bf16* param, long long count, uint64_t seed, int tensor,
+                long long elem0, long long cols, bool is_gain, cudaStream_t s) {
+  init_slice_kernel<<<grid_for(count), 256, 0, s>>>(master, param, count, seed, tensor, elem0, cols,
+                                                    is_gain ? 1 : 0);
+  check_launch("init_slice");
+}
+
+}  // namespace cft::llama

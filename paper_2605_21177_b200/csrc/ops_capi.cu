@@ -13,7 +13,7 @@ namespace cft {
 namespace tc {
 bool linear_shapes_ok(const void* x, const void* w, int64_t in_dim, int64_t out_dim);
 void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
-                void* y, cudaStream_t stream);
+                void* y, cudaStream_t stream, const void* residual);
 void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w, int64_t in_dim,
                   void* dx, int beta, cudaStream_t stream);
 void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const void* x,
@@ -109,7 +109,7 @@ int cft_linear_fwd(cft_dtype dtype, const void* x, int64_t n_tok, int64_t in_dim
     if (n_tok <= 0 || out_dim <= 0) return;
     if (dtype == CFT_BF16) {
       if (in_dim > 0 && tma_ok(x, in_dim) && tma_ok(w, in_dim) && tma_ok(y, out_dim))
-        tc::linear_fwd(x, n_tok, in_dim, w, out_dim, y, s);
+        tc::linear_fwd(x, n_tok, in_dim, w, out_dim, y, s, nullptr);
       else
         simt::linear_fwd_bf16(static_cast<const __nv_bfloat16*>(x), n_tok, in_dim,
                               static_cast<const __nv_bfloat16*>(w), out_dim,

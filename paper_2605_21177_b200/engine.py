@@ -43,8 +43,16 @@ class BatchC(C.Structure):
                 ("labels", C.c_void_p), ("on_device", C.c_int32), ("pad_", C.c_int32)]
 
 
+class LlamaSpecC(C.Structure):
+    _fields_ = [("layers", C.c_int32), ("d", C.c_int32), ("heads", C.c_int32),
+                ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32),
+                ("vocab", C.c_int32), ("seq", C.c_int32), ("eps", C.c_double),
+                ("rope_theta", C.c_double)]
+
+
 _P = C.POINTER
 for _n, _r, _a in [
+    ("cft_engine_create_llama", C.c_int, [_P(LlamaSpecC), _P(EngineConfigC), C.c_void_p, C.c_uint64, C.c_void_p, _P(C.c_void_p)]),
     ("cft_engine_create", C.c_int, [_P(LayerSpecC), C.c_int, _P(EngineConfigC), C.c_void_p, C.c_void_p, _P(C.c_void_p)]),
     ("cft_engine_destroy", None, [C.c_void_p]),
     ("cft_engine_step", C.c_int, [C.c_void_p, _P(BatchC)]),
@@ -158,6 +166,46 @@ class Model:
 
 
 @dataclass
+class LlamaModel:
+    """Llama-3-shaped decoder (the build's extension).  Defaults: configs[0]."""
+    layers: int = 2
+    d: int = 256
+    heads: int = 4
+    kv_heads: int = 2
+    head_dim: int = 64
+    ffn: int = 768
+    vocab: int = 1024
+    seq: int = 128
+    eps: float = 1e-5
+    rope_theta: float = 500000.0
+    loss: str = "softmax_ce"
+
+    @staticmethod
+    def llama3_8b(layers=32):
+        return LlamaModel(layers=layers, d=4096, heads=32, kv_heads=8, head_dim=128, ffn=14336,
+                          vocab=128256, seq=1024)
+
+    def tensors(self):
+        """[(name, rows, cols)] in registration order (= oracle/shapes.py)."""
+        q, kv = self.heads * self.head_dim, self.kv_heads * self.head_dim
+        out = [("embed", self.vocab, self.d)]
+        for i in range(self.layers):
+            p = f"L{i}."
+            out += [(p + "attn_norm", self.d, 1), (p + "wq", q, self.d), (p + "wk", kv, self.d),
+                    (p + "wv", kv, self.d), (p + "wo", self.d, q), (p + "mlp_norm", self.d, 1),
+                    (p + "w1", self.ffn, self.d), (p + "w3", self.ffn, self.d),
+                    (p + "w2", self.d, self.ffn)]
+        return out + [("norm", self.d, 1), ("lm_head", self.vocab, self.d)]
+
+    def num_params(self):
+        return sum(r * c for _, r, c in self.tensors())
+
+    def _spec(self):
+        return LlamaSpecC(self.layers, self.d, self.heads, self.kv_heads, self.head_dim, self.ffn,
+                          self.vocab, self.seq, self.eps, self.rope_theta)
+
+
+@dataclass
 class TrainOptions:
     """include/chunkft/trainer.hpp:16-24 plus the plan and residency choices."""
     schedule: ScheduleConfig = field(default_factory=ScheduleConfig)
@@ -175,8 +223,8 @@ class TrainOptions:
 class ChunkEngine:
     """Owns one native engine on the current CUDA device."""
 
-    def __init__(self, model: Model, init_params, batch_rows: int, options: TrainOptions,
-                 stream: Optional[torch.cuda.Stream] = None):
+    def __init__(self, model, init_params, batch_rows: int, options: TrainOptions,
+                 stream: Optional[torch.cuda.Stream] = None, seed: int = 7):
         self.model = model
         self.opt = options
         self.dtype = options.dtype
@@ -201,15 +249,24 @@ class ChunkEngine:
         cfg.full_backward = int(o.full_backward)
         cfg.check_every_step = int(o.check_every_step)
         cfg.grad_scale = 1.0
-        p = np.ascontiguousarray(init_params, dtype=np.float64)
-        if p.size != model.num_params():
-            raise Error("restore_params: size mismatch")
         self.rows = batch_rows
         self.stream = stream or torch.cuda.current_stream()
         out = C.c_void_p()
-        specs = model._specs()
-        N.check(_L.cft_engine_create(specs, len(model.layers), C.byref(cfg), p.ctypes.data,
-                                     self.stream.cuda_stream, C.byref(out)), "engine")
+        if isinstance(model, LlamaModel):
+            p = None if init_params is None else np.ascontiguousarray(init_params, dtype=np.float64)
+            if p is not None and p.size != model.num_params():
+                raise Error("restore_params: size mismatch")
+            spec = model._spec()
+            N.check(_L.cft_engine_create_llama(C.byref(spec), C.byref(cfg),
+                                               None if p is None else p.ctypes.data, seed,
+                                               self.stream.cuda_stream, C.byref(out)), "engine")
+        else:
+            p = np.ascontiguousarray(init_params, dtype=np.float64)
+            if p.size != model.num_params():
+                raise Error("restore_params: size mismatch")
+            specs = model._specs()
+            N.check(_L.cft_engine_create(specs, len(model.layers), C.byref(cfg), p.ctypes.data,
+                                         self.stream.cuda_stream, C.byref(out)), "engine")
         self._h = out
         self._keep = []
 
