@@ -172,7 +172,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     peaks = load_peaks()
-    W, S = args.warmup, args.steps
+    W, S = max(args.warmup, 16), args.steps
     total = 2 * (W + S) + 2
 
     model = Model(loss="half_sq").add_linear(D, D, bias=False)
@@ -236,6 +236,7 @@ def run_ours(args, rank, world, local_rank):
     ms = max_over_ranks(e0.elapsed_time(e1))
     phases = eng.phase_totals()
     eng.profile(False, 0)
+    clocks = clk.summary()
 
     # ---- end-to-end through the C ABI: pinned host batches, per-step loss read ----
     step_base = W + S
@@ -285,7 +286,6 @@ def run_ours(args, rank, world, local_rank):
 
     res = None
     if rank == 0:
-        clocks = clk.summary()
         res = {
             "metric": METRIC,
             "value": value,
@@ -323,6 +323,223 @@ def run_ours(args, rank, world, local_rank):
     return res
 
 
+LLAMA_WORKLOAD = ("llama3_8b_chunk_local_step (BASELINE configs[2]: Llama-3-8B-shaped decoder, 32 "
+                  "layers, d=4096, 32/8 heads, ffn 14336, vocab 128256, seq 1024, 8 sequences = "
+                  "8192 tokens per GPU per step, byte-budget chunks of 2 GiB -> K=60 rotating every "
+                  "step (T=1) over all layers, bf16 operands / fp32 accumulate + state)")
+
+
+def reference_llama_cpu(rows: int = 16, K: int = 60):
+    """The reference CPU path (oracle/_ref, OpenMP on all host cores) for the configs[2] step,
+    EXTRAPOLATED per SURVEY.md 8(d): one decoder layer's seven Linear shapes (forward + dX,
+    which the reference always forms) timed at `rows` tokens, x 32 layers, + the lm_head
+    (forward + dX), + dW on one chunk's worth of rows (the active slice), + adamw_chunk_step on
+    one chunk.  Attention / RMSNorm / SwiGLU (absent from the reference) are not charged, so
+    the figure is optimistic for the reference."""
+    from oracle import ref as R
+    if not R.available:
+        return None
+    R.set_backend(True)
+    rng = np.random.default_rng(3)
+    d, ffn, kv, vocab, L = 4096, 14336, 1024, 128256, 32
+    P = 8_030_261_248
+    shapes = [(d, d), (kv, d), (kv, d), (d, d), (ffn, d), (ffn, d), (d, ffn)]
+
+    def timed(fn):
+        t0 = time.perf_counter()
+        fn()
+        return time.perf_counter() - t0
+
+    t_layer = 0.0
+    for out_dim, in_dim in shapes:
+        x = rng.uniform(-1, 1, (rows, in_dim))
+        w = rng.uniform(-0.5, 0.5, (out_dim, in_dim)) / np.sqrt(in_dim)
+        dy = rng.uniform(-1, 1, (rows, out_dim))
+        t_layer += timed(lambda: R.linear_forward(x, w)) + timed(lambda: R.linear_dinput(dy, w))
+    # lm_head: time a 1/8 row block and scale (forward + dX are linear in the row count)
+    hb = vocab // 8
+    xh = rng.uniform(-1, 1, (rows, d))
+    wh = rng.uniform(-0.5, 0.5, (hb, d)) / np.sqrt(d)
+    dyh = rng.uniform(-1, 1, (rows, hb))
+    t_head = 8 * (timed(lambda: R.linear_forward(xh, wh)) + timed(lambda: R.linear_dinput(dyh, wh)))
+    # dW on one chunk (P/K elements): time dW for 2048 rows of w1 and scale by element count
+    x1 = rng.uniform(-1, 1, (rows, d))
+    dy1 = rng.uniform(-1, 1, (rows, ffn))
+    t_dw = timed(lambda: R.linear_dweight(dy1, x1, 0, 2048)) * (P / K) / (2048 * d)
+    # adamw_chunk_step on 8.4 M elements, scaled to a chunk
+    E = 1 << 23
+    st = [rng.uniform(-1, 1, E) * 0.01, np.zeros(E), np.zeros(E)]
+    g = rng.uniform(-1, 1, E)
+    t_adam = timed(lambda: R.adamw(*st, g, 0)) * (P / K) / E
+    step_s = L * t_layer + t_head + t_dw + t_adam
+    return dict(value=rows / step_s, unit="tokens/s", cores=R.openmp_threads(), kind="reference",
+                sample=f"EXTRAPOLATED: reference kernels (oracle/_ref, OpenMP) at {rows} tokens: one "
+                       f"decoder layer's 7 Linear fwd+dX ({t_layer:.2f} s) x 32 + lm_head fwd+dX "
+                       f"({t_head:.2f} s) + dW on one chunk ({t_dw:.2f} s) + AdamW on one chunk "
+                       f"({t_adam:.2f} s); attention/norm/SwiGLU not charged",
+                step_s=step_s)
+
+
+def host_ram_bytes():
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except Exception:
+        pass
+    return 0
+
+
+def run_llama(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_21177_b200.engine import ChunkEngine, LlamaModel, TrainOptions
+    from paper_2605_21177_b200.plan import ScheduleConfig, TensorInfo, partition_by_budget
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    peaks = load_peaks()
+    model = LlamaModel.llama3_8b(layers=args.layers)
+    B = 8
+    tokens_per_gpu = B * model.seq
+    budget = 2 << 30
+    infos = [TensorInfo(i, n, r, c) for i, (n, r, c) in enumerate(model.tensors())]
+    plan = partition_by_budget(infos, budget)
+    K = plan.K
+    W = args.warmup
+    S = args.steps if args.steps > 0 else K  # default: one full rotation = rotation average
+    E2E = 0 if args.no_e2e else S
+    total = W + S + (W + E2E if E2E else 0) + 2
+    # optimizer state (12 B/param fp32 master+m+v) in pinned host memory when the host has
+    # room for every local rank's copy, else resident in HBM (still flat, no rotation copies)
+    state_bytes = 12 * model.num_params()
+    offload = host_ram_bytes() > int(1.15 * state_bytes * max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=total, prefetch=True),
+                        dtype="bf16", plan="budget", budget_bytes=budget, offload=offload,
+                        check_every_step=False)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        eng = ChunkEngine(model, None, B, opts, stream=stream, seed=1234)
+    if world > 1:
+        eng.set_grad_scale(1.0 / world)
+    rng = np.random.default_rng(100 + rank)
+    dev_b, host_b = [], []
+    for i in range(4):
+        seqs = rng.integers(0, model.vocab, (B, model.seq + 1)).astype(np.int32)
+        b = {"tokens": seqs[:, :-1].copy(), "labels": seqs[:, 1:].copy()}
+        dev_b.append(eng.stage(b, device=True))
+        host_b.append(eng.stage(b, device=False))
+    torch.cuda.synchronize()
+
+    def one_step(b):
+        if world == 1:
+            eng.step([b])
+            return
+        eng.step_begin()
+        eng.forward_backward(b, 0)
+        with torch.cuda.stream(stream):
+            dist.all_reduce(eng.grad_tensor())
+        eng.step_end()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(W):
+        one_step(dev_b[i % 4])
+    barrier()
+    eng.profile(True, 2048 * (S + 2))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for i in range(S):
+            one_step(dev_b[i % 4])
+        e1.record(stream)
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        phases = eng.phase_totals(with_work=True)
+        eng.profile(False, 0)
+        losses = [eng.wait_step(W + S - 1)[0]]
+        e2e_ms = None
+        if E2E:
+            base = W + S
+            for i in range(W):
+                one_step(host_b[i % 4])
+                eng.wait_step(base + i)
+            barrier()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for i in range(E2E):
+                one_step(host_b[i % 4])
+                if i > 0:
+                    losses.append(eng.wait_step(base + W + i - 1)[0])
+            losses.append(eng.wait_step(base + W + E2E - 1)[0])
+            f1.record(stream)
+            barrier()
+            e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+    eng.finish()
+    tr = eng.trajectory()
+    finite = bool(np.all(np.isfinite(tr["loss"])))
+
+    value = tokens_per_gpu * world * S / (ms / 1e3)
+    gemm_flops = phases["fwd_gemm"][2] + phases["dgrad"][2] + phases["wgrad"][2]
+    gemm_ms = phases["fwd_gemm"][0] + phases["dgrad"][0] + phases["wgrad"][0]
+    gemm_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12
+    wg_tflops = phases["wgrad"][2] / max(phases["wgrad"][0], 1e-9) / 1e9
+    adam_gbs = phases["update"][2] / max(phases["update"][0], 1e-9) / 1e6
+    launches = int(sum(v[1] for k, v in phases.items() if k != "inputs") + 2 * S)
+    res = None
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": S,
+            "warmup": W, "ms_per_step": ms / S, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded uniform token ids; random-init weights, U(-0.5,0.5)/sqrt(fan-in))",
+            "config": {"workload": LLAMA_WORKLOAD, "layers": args.layers, "params": model.num_params(),
+                       "tokens_per_gpu_per_step": tokens_per_gpu,
+                       "global_batch_tokens": tokens_per_gpu * world, "seq_len": model.seq,
+                       "K": K, "T": 1, "budget_bytes": budget, "plan_hash": f"{plan.hash():016x}",
+                       "prefetch": True,
+                       "state_residency": "pinned host + 3 HBM slots" if offload else "HBM (host RAM too small for all ranks)",
+                       "parallelism": f"dp{world}",
+                       "l2": "step working set >> L2 (16 GB of bf16 weights streamed per step)",
+                       "timed_steps_cover": "one full rotation (every chunk once)" if S % K == 0 else f"{S} steps"},
+            "e2e": {"value": (tokens_per_gpu * world * E2E / (e2e_ms / 1e3)) if E2E else None,
+                    "unit": "tokens/s", "h2d_bytes_per_step": 2 * 4 * tokens_per_gpu,
+                    "d2h_bytes_per_step": 32,
+                    "ms_per_step": (e2e_ms / E2E) if E2E else None, "losses_finite": finite},
+            "roofline": {"bound": "tensor",
+                         "kernel": "gemm_bf16_2sm_kernel / gemm_bf16_kernel (tcgen05 fwd + dgrad + sliced wgrad)",
+                         "achieved": gemm_tflops, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
+                         "frac": gemm_tflops / peaks["bf16_sustained"], "traffic": None,
+                         "peak_source": peaks["source"] + " sustained bf16 (MEASURED_PEAKS.json)",
+                         "algorithmic_flops_per_step": gemm_flops / S,
+                         "share_of_step": gemm_ms / ms},
+            "sliced_dw": {"tflops_in_step": wg_tflops, "frac_of_measured_peak": wg_tflops / peaks["bf16"],
+                          "flops_per_step": phases["wgrad"][2] / S},
+            "adamw": {"GBps_in_step": adam_gbs, "frac_of_measured_hbm": adam_gbs / peaks["hbm"],
+                      "frac_of_spec_8000": adam_gbs / 8000.0, "bytes_per_elem": 30,
+                      "elements_per_chunk": model.num_params() / K},
+            "phases_ms_per_step": {k: v[0] / S for k, v in phases.items()},
+            "gpu_launches": launches,
+            "device_bytes": eng.device_bytes(),
+            "final_loss": float(tr["loss"][-1]),
+            "clocks": clk.summary(),
+        }
+    return res
+
+
 def slice_sweep(local_rank):
     """sliced-dW TFLOP/s for active-slice widths 1/8 .. 1/1 (configs[1] sweep)."""
     import torch
@@ -353,14 +570,21 @@ def slice_sweep(local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=0,
+                    help="timed steps (default: one full rotation for llama8b, 200 for linear4096)")
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["llama8b", "linear4096"], default="llama8b",
+                    help="llama8b = BASELINE configs[2] (headline); linear4096 = configs[1]")
+    ap.add_argument("--layers", type=int, default=32, help="llama8b depth (32 = Llama-3-8B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="add the 1/8..1/1 sliced-dW sweep")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[1] sliced-dW sweep")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.workload == "linear4096" and args.steps <= 0:
+        args.steps = 200
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -369,13 +593,21 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cpu = reference_cpu()
+        if args.workload == "llama8b":
+            cpu = reference_llama_cpu()
+            workload, sample_tokens, per_step_tokens = LLAMA_WORKLOAD, 16, 8192
+        else:
+            cpu = None
+        if cpu is None:
+            cpu = reference_cpu()
+            workload, sample_tokens, per_step_tokens = WORKLOAD, 64, N_TOK
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": cpu["step_s"] * 1e3 * N_TOK / 64, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "reference_sample_tokens": 64},
+            "ms_per_step": cpu["step_s"] * 1e3 * per_step_tokens / sample_tokens,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": workload, "reference_sample_tokens": sample_tokens},
             "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}))
@@ -386,12 +618,17 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    res = run_ours(args, rank, world, local_rank)
+    if args.workload == "llama8b":
+        res = run_llama(args, rank, world, local_rank)
+    else:
+        res = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        if args.sweep:
-            res["sliced_dw"]["sweep"] = slice_sweep(local_rank)
+        if not args.no_sweep:
+            res.setdefault("sliced_dw", {})["configs1_sweep"] = slice_sweep(local_rank)
         if world == 1 and not args.no_cpu_baseline:
-            cpu = reference_cpu()
+            cpu = reference_llama_cpu() if args.workload == "llama8b" else None
+            if cpu is None:
+                cpu = reference_cpu()
             res["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(res))
     if world > 1:

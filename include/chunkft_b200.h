@@ -357,10 +357,11 @@ int cft_engine_phase_ms(cft_engine* e, float* ms4);
 /* Kernel-category profiler: CUDA events on the engine stream around every launch of a
  * category (0 inputs, 1 forward GEMM, 2 other forward, 3 loss, 4 slice wgrad, 5 dgrad,
  * 6 other backward, 7 gradient statistics, 8 AdamW/SGD update).  max_marks bounds the
- * preallocated event pool.  phase_totals synchronises, returns summed ms and launch counts
- * per category (9 entries each) and clears the marks. */
+ * preallocated event pool.  phase_totals synchronises, returns summed ms, launch counts and
+ * algorithmic work (GEMM FLOPs for 1/4/5; bytes for 7/8) per category (9 entries each; any
+ * pointer may be NULL) and clears the marks. */
 int cft_engine_profile(cft_engine* e, int enable, int64_t max_marks);
-int cft_engine_phase_totals(cft_engine* e, float* ms9, int64_t* counts9);
+int cft_engine_phase_totals(cft_engine* e, float* ms9, int64_t* counts9, double* work9);
 /* Block the host until step t's loss / grad_norm_sq reached host memory (t within the last
  * 4 steps) -- a per-step result read that does not drain the device queue. */
 int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq);

@@ -131,12 +131,7 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
   sched_ = std::make_unique<host::RotationScheduler>(sc, elems, plan_.policy);
 
   // ---- streams ----
-  if (stream) {
-    stream_ = stream;
-  } else {
-    CFT_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    own_stream_ = true;
-  }
+  stream_ = stream;  // NULL = the legacy default stream (include/chunkft_b200.h)
   CFT_CUDA(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   CFT_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   CFT_CUDA(cudaEventCreateWithFlags(&step_done_, cudaEventDisableTiming));
@@ -344,11 +339,13 @@ void Engine::pe() {
   open_phase_ = -1;
 }
 
-void Engine::phase_totals(float* ms, int64_t* counts) {
+void Engine::phase_totals(float* ms, int64_t* counts, double* work) {
   CFT_CUDA(cudaStreamSynchronize(stream_));
   for (int i = 0; i < kNumPhases; ++i) {
     ms[i] = 0.f;
     if (counts) counts[i] = 0;
+    if (work) work[i] = work_[i];
+    work_[i] = 0.0;
   }
   for (const auto& m : marks_) {
     float t = 0.f;
@@ -540,6 +537,7 @@ void Engine::forward_backward(const Batch& b, int mb) {
     const void* in = li == 0 ? x_in : layers_[li - 1].x_saved;
     void* out = L.x_saved;
     pb(L.spec.type == kLinear ? kFwdGemm : kFwdOther);
+    if (L.spec.type == kLinear) add_work(kFwdGemm, 2.0 * rows * L.in_w * L.out_w);
     switch (L.spec.type) {
       case kEmbedding:
         if (cft_embedding_gather(static_cast<cft_dtype>(dt), param_ptr(L.w), L.spec.b, tok,
@@ -628,6 +626,7 @@ void Engine::forward_backward(const Batch& b, int mb) {
       }
       const bool is_w = sl.tensor == L.w;
       pb(L.spec.type == kLinear && is_w ? kWgrad : kBwdOther);
+      if (L.spec.type == kLinear && is_w) add_work(kWgrad, 2.0 * rows * (sl.re - sl.rb) * L.in_w);
       switch (L.spec.type) {
         case kLinear:
           if (is_w) {
@@ -673,6 +672,7 @@ void Engine::forward_backward(const Batch& b, int mb) {
     }
     if (!need_dx) continue;
     pb(L.spec.type == kLinear ? kDgrad : kBwdOther);
+    if (L.spec.type == kLinear) add_work(kDgrad, 2.0 * rows * L.in_w * L.out_w);
     switch (L.spec.type) {
       case kLinear:
         if (cft_linear_dgrad(static_cast<cft_dtype>(dt), g, rows, L.out_w, param_ptr(L.w), L.in_w, gx, 0,
@@ -737,6 +737,7 @@ void Engine::step_end() {
   double* st = stats_ + t_ * 4;
   CFT_CUDA(cudaEventRecord(ev_[4], s));
   pb(kStats);
+  add_work(kStats, 4.0 * n);
   if (cft_grad_stats(sdt, aux_, n, scale, st, s) != CFT_OK) throw Error(last_error());
   // a non-finite loss also blocks the update (trainer.cpp:48-49 throws before any step)
   layers::flag_nonfinite_loss(st, s);
@@ -759,6 +760,7 @@ void Engine::step_end() {
   n_local_[c] += 1;
   const int32_t nseg = static_cast<int32_t>(chunk_slices_[c].size());
   pb(kUpdate);
+  add_work(kUpdate, (cfg_.optim == 0 ? 30.0 : 14.0) * n);
   if (cfg_.optim == 0) {
     const double bc1 = 1.0 - std::pow(cfg_.hyper.beta1, static_cast<double>(n_local_[c]));
     const double bc2 = 1.0 - std::pow(cfg_.hyper.beta2, static_cast<double>(n_local_[c]));

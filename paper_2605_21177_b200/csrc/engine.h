@@ -113,7 +113,9 @@ class Engine {
   enum Phase { kInputs = 0, kFwdGemm, kFwdOther, kLoss, kWgrad, kDgrad, kBwdOther, kStats,
                kUpdate, kNumPhases };
   void profile(bool on, int64_t max_marks);
-  void phase_totals(float* ms, int64_t* counts);  // syncs; resets the marks
+  // syncs; per phase: summed ms, launch count, algorithmic work (GEMM FLOPs; bytes for the
+  // statistics / update passes); resets the marks
+  void phase_totals(float* ms, int64_t* counts, double* work);
   void wait_step(int64_t t, double* loss, double* gsq);  // host waits for step t's result only
 
   // CKFT v1 checkpoints (optimizer.cpp:210-251, FORMATS.md:176-194): one chunk_NNNN.bin per
@@ -227,6 +229,10 @@ class Engine {
   int open_phase_ = -1;
   cudaEvent_t open_ev_ = nullptr;
   void pb(int phase);
+  double work_[16] = {};
+  void add_work(int phase, double w) {
+    if (profiling_) work_[phase] += w;
+  }
   void pe();
 
   int active_ = -1;

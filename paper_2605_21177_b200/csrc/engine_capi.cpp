@@ -160,8 +160,8 @@ int cft_engine_profile(cft_engine* e, int enable, int64_t max_marks) {
   return guarded([&] { e->p->profile(enable != 0, max_marks); });
 }
 
-int cft_engine_phase_totals(cft_engine* e, float* ms9, int64_t* counts9) {
-  return guarded([&] { e->p->phase_totals(ms9, counts9); });
+int cft_engine_phase_totals(cft_engine* e, float* ms9, int64_t* counts9, double* work9) {
+  return guarded([&] { e->p->phase_totals(ms9, counts9, work9); });
 }
 
 int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq) {

@@ -135,6 +135,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
     const SliceRt* s = slice_of(tensor);
     if (!s) return;
     pb(kWgrad);
+    add_work(kWgrad, 2.0 * N * double(s->re - s->rb) * in_dim);
     tc::linear_wgrad_slice(dy, N, out_dim, x, in_dim, row0 + s->rb, row0 + s->re, aux_at(s), 1, st);
     pe();
   };
@@ -173,6 +174,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
                    static_cast<bf16*>(z.a), z.rstd1, st);
     pe();
     pb(kFwdGemm);
+    add_work(kFwdGemm, 2.0 * N * d * QKV);
     tc::linear_fwd(z.a, N, d, P(id(l, 1)), QKV, z.qkv, st);  // wq|wk|wv stacked
     pe();
     pb(kFwdOther);
@@ -183,6 +185,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
     attn_->forward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, z.lse, st);
     pe();
     pb(kFwdGemm);
+    add_work(kFwdGemm, 2.0 * N * Q * d);
     tc::linear_fwd(z.o, N, Q, P(id(l, 4)), d, z.h, st, z.x);  // h = x + o Wo^T
     pe();
     pb(kFwdOther);
@@ -190,12 +193,14 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
                    static_cast<bf16*>(z.m), z.rstd2, st);
     pe();
     pb(kFwdGemm);
+    add_work(kFwdGemm, 2.0 * N * d * 2 * F);
     tc::linear_fwd(z.m, N, d, P(id(l, 6)), 2 * F, z.ug, st);  // w1|w3 stacked
     pe();
     pb(kFwdOther);
     llama::swiglu_fwd(static_cast<bf16*>(z.ug), N, S.ffn, static_cast<bf16*>(z.s), st);
     pe();
     pb(kFwdGemm);
+    add_work(kFwdGemm, 2.0 * N * F * d);
     tc::linear_fwd(z.s, N, F, P(id(l, 8)), d, lb_[l + 1].x, st, z.h);  // x' = h + s W2^T
     pe();
   }
@@ -204,6 +209,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
                  static_cast<bf16*>(l_xf_), l_rstdf_, st);
   pe();
   pb(kFwdGemm);
+  add_work(kFwdGemm, 2.0 * N * d * V);
   tc::linear_fwd(l_xf_, N, d, P(head_id), V, l_logits_, st);
   pe();
 
@@ -220,6 +226,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
   wgrad(head_id, dlog, V, l_xf_, d, 0);
   if (need(norm_id)) {
     pb(kDgrad);
+    add_work(kDgrad, 2.0 * N * V * d);
     tc::linear_dgrad(dlog, N, V, P(head_id), d, l_dxf_, 0, st);
     pe();
     if (const SliceRt* s = slice_of(norm_id)) {
@@ -241,6 +248,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
     wgrad(id(l, 8), l_gx_, d, z.s, F, 0);
     if (!need(id(l, 7))) break;
     pb(kDgrad);
+    add_work(kDgrad, 2.0 * N * d * F);
     tc::linear_dgrad(l_gx_, N, d, P(id(l, 8)), F, l_ds_, 0, st);
     pe();
     pb(kBwdOther);
@@ -251,6 +259,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
     wgrad(id(l, 7), l_dug_, 2 * F, z.m, d, F);  // w3 rows [F,2F)
     if (!need(id(l, 5))) break;
     pb(kDgrad);
+    add_work(kDgrad, 2.0 * N * 2 * F * d);
     tc::linear_dgrad(l_dug_, N, 2 * F, P(id(l, 6)), d, l_da_, 0, st);  // dM (reuses da buffer)
     pe();
     if (const SliceRt* s = slice_of(id(l, 5))) {
@@ -268,6 +277,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
     wgrad(id(l, 4), l_gh_, d, z.o, Q, 0);
     if (!need(id(l, 3))) break;
     pb(kDgrad);
+    add_work(kDgrad, 2.0 * N * d * Q);
     tc::linear_dgrad(l_gh_, N, d, P(id(l, 4)), Q, l_do_, 0, st);
     pe();
     pb(kBwdOther);
@@ -282,6 +292,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
     wgrad(id(l, 3), l_dqkv_, QKV, z.a, d, Q + KV);
     if (!need(id(l, 0))) break;
     pb(kDgrad);
+    add_work(kDgrad, 2.0 * N * QKV * d);
     tc::linear_dgrad(l_dqkv_, N, QKV, P(id(l, 1)), d, l_da_, 0, st);  // dA
     pe();
     if (const SliceRt* s = slice_of(id(l, 0))) {

@@ -72,7 +72,7 @@ for _n, _r, _a in [
     ("cft_engine_chunk_counters", C.c_int, [C.c_void_p, C.c_void_p]),
     ("cft_engine_phase_ms", C.c_int, [C.c_void_p, C.c_void_p]),
     ("cft_engine_profile", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
-    ("cft_engine_phase_totals", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("cft_engine_phase_totals", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("cft_engine_wait_step", C.c_int, [C.c_void_p, C.c_int64, _P(C.c_double), _P(C.c_double)]),
     ("cft_engine_write_checkpoints", C.c_int, [C.c_void_p, C.c_char_p]),
     ("cft_engine_read_checkpoints", C.c_int, [C.c_void_p, C.c_char_p]),
@@ -390,10 +390,16 @@ class ChunkEngine:
     def profile(self, enable: bool = True, max_marks: int = 1 << 14):
         N.check(_L.cft_engine_profile(self._h, int(enable), max_marks))
 
-    def phase_totals(self):
+    def phase_totals(self, with_work: bool = False):
+        """{phase: (ms, launches)} or, with_work, {phase: (ms, launches, work)} where work is
+        algorithmic GEMM FLOPs (fwd_gemm / wgrad / dgrad) or bytes (stats / update)."""
         ms = np.zeros(9, np.float32)
         cnt = np.zeros(9, np.int64)
-        N.check(_L.cft_engine_phase_totals(self._h, ms.ctypes.data, cnt.ctypes.data))
+        work = np.zeros(9, np.float64)
+        N.check(_L.cft_engine_phase_totals(self._h, ms.ctypes.data, cnt.ctypes.data,
+                                           work.ctypes.data))
+        if with_work:
+            return {k: (float(ms[i]), int(cnt[i]), float(work[i])) for i, k in enumerate(self.PHASES)}
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PHASES)}
 
     def write_checkpoints(self, directory: str):
