@@ -205,6 +205,79 @@ __global__ void loss_ce_kernel(const T* y, const int32_t* labels, long long cols
     atomicAdd(loss, static_cast<double>(-(ylab - mx - logz)) * inv_rows);
 }
 
+// Softmax cross-entropy over wide bf16 rows (cols % 8 == 0, e.g. a 128k vocabulary): one
+// online pass for (max, sum of exp) with 16-byte loads, one pass writing dy (may alias y).
+__device__ __forceinline__ void online_merge(float& m, float& s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  if (mn == -INFINITY) return;
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+  m = mn;
+}
+
+__global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels, long long cols,
+                                   float inv_rows, __nv_bfloat16* dy, double* loss,
+                                   unsigned long long* bad_label) {
+  __shared__ float sm[32], ss[32];
+  const long long b = blockIdx.x;
+  const __nv_bfloat16* yr = y + b * cols;
+  const int label = labels[b];
+  if (label < 0 || label >= cols) {
+    if (threadIdx.x == 0) atomicAdd(bad_label, 1ull);
+    return;
+  }
+  const float ylab = __bfloat162float(yr[label]);
+  const long long nv = cols / 8;
+  float m = -INFINITY, s = 0.f;
+  for (long long j = threadIdx.x; j < nv; j += blockDim.x) {
+    const uint4 u = reinterpret_cast<const uint4*>(yr)[j];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(h[q]);
+      v[2 * q] = f.x;
+      v[2 * q + 1] = f.y;
+    }
+    float lm = v[0];
+#pragma unroll
+    for (int e = 1; e < 8; ++e) lm = fmaxf(lm, v[e]);
+    float ls = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ls += __expf(v[e] - lm);
+    online_merge(m, s, lm, ls);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    online_merge(m, s, m2, s2);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sm[threadIdx.x / 32] = m;
+    ss[threadIdx.x / 32] = s;
+  }
+  __syncthreads();
+  m = -INFINITY;
+  s = 0.f;
+  for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) online_merge(m, s, sm[i], ss[i]);
+  const float logz = m + logf(s);
+  for (long long j = threadIdx.x; j < nv; j += blockDim.x) {
+    const uint4 u = reinterpret_cast<const uint4*>(yr)[j];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    uint4 o;
+    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(h[q]);
+      const long long c0 = 8 * j + 2 * q;
+      const float p0 = __expf(f.x - logz) - (c0 == label ? 1.f : 0.f);
+      const float p1 = __expf(f.y - logz) - (c0 + 1 == label ? 1.f : 0.f);
+      oh[q] = __floats2bfloat162_rn(p0 * inv_rows, p1 * inv_rows);
+    }
+    reinterpret_cast<uint4*>(dy + b * cols)[j] = o;
+  }
+  if (threadIdx.x == 0) atomicAdd(loss, static_cast<double>(-(ylab - logz)) * inv_rows);
+}
+
 // fp64 losses for the fp64 engine path (exp/log are CUDA's: <= 1-2 ulp from glibc).
 __global__ void loss_elem_f64_kernel(int kind, const double* y, const double* target, long long n,
                                      double* dy, double* partial) {
@@ -299,6 +372,15 @@ template <typename T>
 void loss(int kind, const T* y, const T* target, const int32_t* labels, long long rows,
           long long cols, T* dy, double* loss_acc, unsigned long long* bad_label, cudaStream_t s) {
   if (kind == 3) {
+    if constexpr (std::is_same_v<T, __nv_bfloat16>) {
+      if (cols % 8 == 0 &&
+          ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0) {
+        loss_ce_vec_kernel<<<(unsigned)rows, 512, 0, s>>>(y, labels, cols, 1.f / rows, dy, loss_acc,
+                                                          bad_label);
+        check_launch("loss_ce_vec");
+        return;
+      }
+    }
     loss_ce_kernel<T><<<(unsigned)rows, row_threads(cols), 0, s>>>(y, labels, cols, 1.f / rows, dy,
                                                                    loss_acc, bad_label);
   } else {

@@ -9,6 +9,9 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "cft_common.h"
 
@@ -112,23 +115,27 @@ __global__ void rms_bwd_kernel(const bf16* __restrict__ dy, const bf16* __restri
   }
 }
 
-// dgamma[j-rb] += sum_b dy[b,j] * x[b,j] * rstd[b]  (layernorm_dgamma with mean = 0)
+// dgamma[j-rb] += sum_b dy[b,j] * x[b,j] * rstd[b]  (layernorm_dgamma with mean = 0).
+// Grid: (column blocks of 32) x (row chunks); 8 row partitions per block; fp32 atomics into
+// the zero-initialised gradient accumulator.
 __global__ void rms_dgamma_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                                   const float* __restrict__ rstd, long long rows, int d,
                                   long long rb, long long re, float* out) {
   __shared__ float red[8][33];
   const long long j = rb + blockIdx.x * 32LL + threadIdx.x % 32;
   const int part = threadIdx.x / 32;
+  const long long per = (rows + gridDim.y - 1) / gridDim.y;
+  const long long r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
   float acc = 0.f;
   if (j < re)
-    for (long long b = part; b < rows; b += 8)
+    for (long long b = r0 + part; b < r1; b += 8)
       acc += __bfloat162float(dy[b * d + j]) * __bfloat162float(x[b * d + j]) * rstd[b];
   red[part][threadIdx.x % 32] = acc;
   __syncthreads();
   if (part == 0 && j < re) {
     float s = 0.f;
     for (int p = 0; p < 8; ++p) s += red[p][threadIdx.x % 32];
-    out[j - rb] += s;
+    atomicAdd(out + (j - rb), s);
   }
 }
 
@@ -242,11 +249,76 @@ void rms_bwd(const bf16* dy, const bf16* x, const float* rstd, const bf16* g, co
 void rms_dgamma(const bf16* dy, const bf16* x, const float* rstd, long long rows, int d,
                 long long rb, long long re, float* out, cudaStream_t s) {
   if (re <= rb) return;
-  rms_dgamma_kernel<<<(unsigned)((re - rb + 31) / 32), 256, 0, s>>>(dy, x, rstd, rows, d, rb, re, out);
+  const unsigned cb = static_cast<unsigned>((re - rb + 31) / 32);
+  const unsigned rc = static_cast<unsigned>(std::max<long long>(1, std::min<long long>(
+      rows / 64, (num_sms() * 8LL + cb - 1) / cb)));
+  rms_dgamma_kernel<<<dim3(cb, rc), 256, 0, s>>>(dy, x, rstd, rows, d, rb, re, out);
   check_launch("rms_dgamma");
 }
+// (cos, sin) table for every (position, pair): angle = pos * theta^(-2i/hd), in fp64
+__global__ void rope_table_kernel(float2* cs, int seq, int half, double theta) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= seq * half) return;
+  const int pos = t / half, i = t % half;
+  const double a = pos * pow(theta, -2.0 * i / (2.0 * half));
+  cs[t] = make_float2(static_cast<float>(cos(a)), static_cast<float>(sin(a)));
+}
+
+// Table-driven, 8 pairs per thread with 16-byte loads/stores.
+__global__ void rope_vec_kernel(bf16* qkv, long long tokens, int seq, int heads, int hd, int ld,
+                                const float2* __restrict__ cs, float sign) {
+  const int half = hd / 2, vpr = half / 8;
+  const long long total = tokens * heads * vpr;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int v = static_cast<int>(t % vpr);
+    const long long th = t / vpr;
+    const int h = static_cast<int>(th % heads);
+    const long long tok = th / heads;
+    const int pos = static_cast<int>(tok % seq);
+    bf16* p = qkv + tok * ld + static_cast<long long>(h) * hd + v * 8;
+    float x1[8], x2[8];
+    unpack8(*reinterpret_cast<const uint4*>(p), x1);
+    unpack8(*reinterpret_cast<const uint4*>(p + half), x2);
+    const float2* c = cs + static_cast<long long>(pos) * half + v * 8;
+    float y1[8], y2[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float2 q = c[e];
+      const float sn = sign * q.y;
+      y1[e] = x1[e] * q.x - x2[e] * sn;
+      y2[e] = x2[e] * q.x + x1[e] * sn;
+    }
+    *reinterpret_cast<uint4*>(p) = pack8(y1);
+    *reinterpret_cast<uint4*>(p + half) = pack8(y2);
+  }
+}
+
 void rope(bf16* qkv, long long tokens, int seq, int heads, int hd, int ld, float theta,
           bool backward, cudaStream_t s) {
+  const int half = hd / 2;
+  if (half % 8 == 0 && ld % 8 == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, float>, float2*> tables;
+    float2* cs;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      auto key = std::make_tuple(seq, hd, theta);
+      auto it = tables.find(key);
+      if (it == tables.end()) {
+        CFT_CUDA(cudaMalloc(&cs, sizeof(float2) * seq * half));
+        rope_table_kernel<<<(seq * half + 255) / 256, 256, 0, s>>>(cs, seq, half, theta);
+        check_launch("rope_table");
+        tables.emplace(key, cs);
+      } else {
+        cs = it->second;
+      }
+    }
+    rope_vec_kernel<<<grid_for(tokens * heads * half / 8), 256, 0, s>>>(
+        qkv, tokens, seq, heads, hd, ld, cs, backward ? -1.f : 1.f);
+    check_launch("rope_vec");
+    return;
+  }
   rope_kernel<<<grid_for(tokens * heads * hd / 2), 256, 0, s>>>(qkv, tokens, seq, heads, hd, ld,
                                                                 theta, backward ? -1.f : 1.f);
   check_launch("rope");
