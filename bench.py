@@ -281,7 +281,8 @@ def run_ours(args, rank, world, local_rank):
                 traffic = json.load(f).get("gemm_bytes_per_launch")
         except Exception:
             traffic = None
-    kernels_per_step = sum(c for k, (_, c) in phases.items() if k != "inputs") / max(S, 1) + 1
+    kernels_per_step = sum(c for k, (_, c) in phases.items()
+                           if k not in ("inputs", "rot_wait", "h2d", "d2h", "graph")) / max(S, 1) + 1
     step_ms = ms / S
 
     res = None
@@ -415,12 +416,15 @@ def run_llama(args, rank, world, local_rank):
     # room for every local rank's copy, else resident in HBM (still flat, no rotation copies)
     state_bytes = 12 * model.num_params()
     offload = host_ram_bytes() > int(1.15 * state_bytes * max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    if args.state != "auto":
+        offload = args.state == "host"
     opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=total, prefetch=True),
                         dtype="bf16", plan="budget", budget_bytes=budget, offload=offload,
                         check_every_step=False)
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
         eng = ChunkEngine(model, None, B, opts, stream=stream, seed=1234)
+    eng.prepare_graphs()  # one forward+backward CUDA graph per chunk, captured before timing
     if world > 1:
         eng.set_grad_scale(1.0 / world)
     rng = np.random.default_rng(100 + rank)
@@ -471,9 +475,13 @@ def run_llama(args, rank, world, local_rank):
         # launch; kept out of the headline timing because the ~800 extra event records per
         # step cost ~8%): per-kernel times for the roofline and the phase split
         eng.profile(True, 2048 * (S + 2))
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
         for i in range(S):
             one_step(dev_b[i % 4])
+        p1.record(stream)
         phases = eng.phase_totals(with_work=True)
+        prof_wall_ms = p0.elapsed_time(p1)
         eng.profile(False, 0)
         losses = [eng.wait_step(W + 2 * S - 1)[0]]
         e2e_ms = None
@@ -503,8 +511,9 @@ def run_llama(args, rank, world, local_rank):
     gemm_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12
     wg_tflops = phases["wgrad"][2] / max(phases["wgrad"][0], 1e-9) / 1e9
     adam_gbs = phases["update"][2] / max(phases["update"][0], 1e-9) / 1e6
-    launches = int(sum(v[1] for k, v in phases.items() if k != "inputs") + 2 * S)
-    prof_ms = sum(v[0] for v in phases.values())
+    launches = int(sum(v[1] for k, v in phases.items()
+                       if k not in ("inputs", "rot_wait", "h2d", "d2h", "graph")) + 2 * S)
+    prof_ms = sum(v[0] for k, v in phases.items() if k not in ("h2d", "d2h"))
     res = None
     if rank == 0:
         res = {
@@ -539,6 +548,8 @@ def run_llama(args, rank, world, local_rank):
                       "frac_of_spec_8000": adam_gbs / 8000.0, "bytes_per_elem": 30,
                       "elements_per_chunk": model.num_params() / K},
             "phases_ms_per_step": {k: v[0] / S for k, v in phases.items()},
+            "profiled_step_ms": prof_wall_ms / S,
+            "unattributed_ms_per_step": (prof_wall_ms - prof_ms) / S,
             "gpu_launches": launches,
             "device_bytes": eng.device_bytes(),
             "final_loss": float(tr["loss"][-1]),
@@ -585,6 +596,8 @@ def main():
                     help="llama8b = BASELINE configs[2] (headline); linear4096 = configs[1]")
     ap.add_argument("--layers", type=int, default=32, help="llama8b depth (32 = Llama-3-8B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--state", choices=["auto", "host", "hbm"], default="auto",
+                    help="optimizer-state residency for llama8b (auto: pinned host when RAM allows)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[1] sliced-dW sweep")
     args = ap.parse_args()

@@ -298,6 +298,9 @@ typedef struct {
   int32_t full_backward; /* 1: form dX for every layer like the reference; 0: suffix only */
   int32_t check_every_step; /* 1: synchronise each step and raise the reference's errors */
   double grad_scale;     /* extra factor on the mean gradient (1/world for data parallel) */
+  int32_t cuda_graphs;   /* 1: replay each chunk's forward+backward as one captured CUDA graph
+                            (Llama engine; captured on the chunk's first step) */
+  int32_t pad_;
 } cft_engine_config;
 
 /* One micro-batch (model.hpp:52-60).  x / target in the compute dtype; host pointers should
@@ -340,6 +343,9 @@ int cft_engine_forward_backward(cft_engine* e, const cft_batch* batch, int micro
 int cft_engine_grad_buffer(cft_engine* e, void** ptr, int64_t* n, int32_t* dtype);
 int cft_engine_step_end(cft_engine* e);
 int cft_engine_finish(cft_engine* e);
+/* Capture every chunk's forward+backward CUDA graph now instead of on each chunk's first step
+ * (cuda_graphs = 1, Llama engine; a no-op otherwise).  Call between steps. */
+int cft_engine_prepare_graphs(cft_engine* e);
 int cft_engine_set_grad_scale(cft_engine* e, double grad_scale);
 /* TrainTrajectoryEntry (trainer.hpp:26-33): step, chunk, loss (pre-update mean), grad_norm_sq. */
 int64_t cft_engine_trajectory(cft_engine* e, int64_t* step, int32_t* chunk, double* loss,
@@ -356,12 +362,19 @@ int cft_engine_chunk_counters(cft_engine* e, uint64_t* n_out);
 int cft_engine_phase_ms(cft_engine* e, float* ms4);
 /* Kernel-category profiler: CUDA events on the engine stream around every launch of a
  * category (0 inputs, 1 forward GEMM, 2 other forward, 3 loss, 4 slice wgrad, 5 dgrad,
- * 6 other backward, 7 gradient statistics, 8 AdamW/SGD update).  max_marks bounds the
- * preallocated event pool.  phase_totals synchronises, returns summed ms, launch counts and
- * algorithmic work (GEMM FLOPs for 1/4/5; bytes for 7/8) per category (9 entries each; any
- * pointer may be NULL) and clears the marks. */
+ * 6 other backward, 7 gradient statistics, 8 AdamW/SGD update, 9 engine stream waiting for
+ * the active chunk's state upload, 10 / 11 state H2D / D2H time on the copy streams, 12 a
+ * replayed forward+backward graph).  enable: 0 off, 1 per-category marks (the Llama engine
+ * then launches eagerly), 2 coarse marks only (CUDA graphs stay on).
+ * max_marks bounds the preallocated event pool.  phase_totals synchronises, returns summed ms,
+ * launch counts and algorithmic work (GEMM FLOPs for 1/4/5; bytes for 7/8) per category
+ * (CFT_NUM_PHASES entries each; any pointer may be NULL) and clears the marks. */
+#define CFT_NUM_PHASES 13
 int cft_engine_profile(cft_engine* e, int enable, int64_t max_marks);
-int cft_engine_phase_totals(cft_engine* e, float* ms9, int64_t* counts9, double* work9);
+int cft_engine_phase_totals(cft_engine* e, float* ms, int64_t* counts, double* work);
+/* Host-side submission time per profiler category (CFT_NUM_PHASES entries, ms) accumulated
+ * since the previous call -- shows whether the step is launch-bound. */
+int cft_engine_host_phase_ms(cft_engine* e, double* ms);
 /* Block the host until step t's loss / grad_norm_sq reached host memory (t within the last
  * 4 steps) -- a per-step result read that does not drain the device queue. */
 int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq);

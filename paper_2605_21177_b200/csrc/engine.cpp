@@ -229,15 +229,23 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
   }
   CFT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_stats_),
                          std::max<int64_t>(cfg_.total_steps, 1) * 4 * sizeof(double),
-                         cudaHostAllocDefault));
+                         cudaHostAllocMapped));
   CFT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_flags_), 2 * sizeof(unsigned long long),
-                         cudaHostAllocDefault));
+                         cudaHostAllocMapped));
+  // written by kernels through UVA (layers::sm_copy): the mapped address must be the host one
+  CFT_CHECK(layers::host_pinned(host_stats_) && layers::host_pinned(host_flags_),
+            "engine: pinned result buffers are not mapped at their host address");
 
   const int n_slots = cfg_.offload ? 3 : 0;
   for (int i = 0; i < n_slots; ++i) {
     for (auto& st : slots_[i].st) alloc(&st, max_chunk_ * S);
     CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].ready, cudaEventDisableTiming));
     CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].free, cudaEventDisableTiming));
+  }
+  if (cfg_.offload) {
+    chunk_d2h_.assign(cfg_.K, nullptr);
+    for (auto& e : chunk_d2h_) CFT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    chunk_offloaded_.assign(cfg_.K, 0);
   }
   host_states_.assign(cfg_.K, nullptr);
 
@@ -313,8 +321,9 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
   CFT_CUDA(cudaDeviceSynchronize());
 }
 
-void Engine::profile(bool on, int64_t max_marks) {
-  profiling_ = on;
+void Engine::profile(int mode, int64_t max_marks) {
+  profiling_ = mode != 0;
+  coarse_ = mode == 2;
   marks_.clear();
   pool_next_ = 0;
   while (static_cast<int64_t>(pool_.size()) < 2 * max_marks) {
@@ -329,20 +338,45 @@ void Engine::pb(int phase) {
   open_phase_ = phase;
   open_ev_ = pool_[pool_next_++];
   CFT_CUDA(cudaEventRecord(open_ev_, stream_));
+  host_t0_ = std::chrono::steady_clock::now();
 }
 
 void Engine::pe() {
   if (!profiling_ || open_phase_ < 0) return;
+  host_ms_[open_phase_] +=
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0_).count();
   cudaEvent_t b = pool_[pool_next_++];
   CFT_CUDA(cudaEventRecord(b, stream_));
   marks_.push_back({open_phase_, open_ev_, b});
   open_phase_ = -1;
 }
 
+void Engine::mark(int phase, cudaStream_t s, bool begin) {
+  if (!profiling_ || pool_next_ + 2 > pool_.size()) return;
+  cudaEvent_t e = pool_[pool_next_++];
+  CFT_CUDA(cudaEventRecord(e, s));
+  cudaEvent_t& open = copy_open_[phase == kD2H ? 1 : 0];
+  if (begin) {
+    open = e;
+  } else if (open) {
+    marks_.push_back({phase, open, e});
+    open = nullptr;
+  }
+}
+
+void Engine::host_phase_ms(double* ms) {
+  for (int i = 0; i < kNumPhases; ++i) {
+    ms[i] = host_ms_[i];
+    host_ms_[i] = 0.0;
+  }
+}
+
 void Engine::phase_totals(float* ms, int64_t* counts, double* work) {
   CFT_CUDA(cudaStreamSynchronize(stream_));
+  CFT_CUDA(cudaStreamSynchronize(h2d_));
+  CFT_CUDA(cudaStreamSynchronize(d2h_));
   for (int i = 0; i < kNumPhases; ++i) {
-    ms[i] = 0.f;
+    if (ms) ms[i] = 0.f;
     if (counts) counts[i] = 0;
     if (work) work[i] = work_[i];
     work_[i] = 0.0;
@@ -350,7 +384,7 @@ void Engine::phase_totals(float* ms, int64_t* counts, double* work) {
   for (const auto& m : marks_) {
     float t = 0.f;
     CFT_CUDA(cudaEventElapsedTime(&t, m.a, m.b));
-    ms[m.phase] += t;
+    if (ms) ms[m.phase] += t;
     if (counts) counts[m.phase] += 1;
   }
   marks_.clear();
@@ -366,6 +400,9 @@ void Engine::wait_step(int64_t t, double* loss, double* gsq) {
 
 Engine::~Engine() {
   cudaDeviceSynchronize();
+  for (auto g : graphs_)
+    if (g) cudaGraphExecDestroy(g);
+  if (cap_) cudaStreamDestroy(cap_);
   for (auto e : pool_) cudaEventDestroy(e);
   for (auto e : stats_ev_)
     if (e) cudaEventDestroy(e);
@@ -375,6 +412,8 @@ Engine::~Engine() {
       if (p) cudaFreeHost(p);
   if (host_stats_) cudaFreeHost(host_stats_);
   if (host_flags_) cudaFreeHost(host_flags_);
+  for (auto e : chunk_d2h_)
+    if (e) cudaEventDestroy(e);
   for (auto& s : slots_) {
     if (s.ready) cudaEventDestroy(s.ready);
     if (s.free) cudaEventDestroy(s.free);
@@ -402,8 +441,12 @@ int Engine::slot_of(int chunk) const {
 }
 
 int Engine::take_free_slot(int avoid1, int avoid2) {
+  // empty or retiring slots: take the one retired longest ago, so a prefetch does not queue
+  // behind the D2H that is still draining the most recently retired chunk
+  int best = -1;
   for (int i = 0; i < 3; ++i)
-    if (slots_[i].chunk < 0) return i;  // empty, or retiring (the H2D waits on its D2H)
+    if (slots_[i].chunk < 0 && (best < 0 || slots_[i].retired < slots_[best].retired)) best = i;
+  if (best >= 0) return best;
   for (int i = 0; i < 3; ++i)
     if (slots_[i].chunk != avoid1 && slots_[i].chunk != avoid2) return i;
   throw Error("engine: no free state slot");
@@ -420,16 +463,23 @@ void Engine::load_chunk(int chunk, bool for_prefetch) {
     Slot& sl = slots_[s];
     const int64_t n = plan_.chunks[chunk].elements;
     const size_t S = ssz();
-    // wait for the slot's previous D2H (it may still be draining) and the host copy of this
-    // chunk (a retire of the same chunk may be in flight)
+    // wait for the slot's previous D2H (it may still be draining) and for this chunk's own
+    // last D2H (its host copy must be complete before it is read back)
     CFT_CUDA(cudaStreamWaitEvent(h2d_, sl.free, 0));
+    if (chunk_offloaded_[chunk]) CFT_CUDA(cudaStreamWaitEvent(h2d_, chunk_d2h_[chunk], 0));
     const char* src = static_cast<const char*>(host_states_[chunk]);
+    mark(kH2D, h2d_, true);
     for (int k = 0; k < 3; ++k)
       CFT_CUDA(cudaMemcpyAsync(sl.st[k], src + k * n * S, n * S, cudaMemcpyHostToDevice, h2d_));
+    mark(kH2D, h2d_, false);
     CFT_CUDA(cudaEventRecord(sl.ready, h2d_));
     sl.chunk = chunk;
   }
-  if (!for_prefetch) CFT_CUDA(cudaStreamWaitEvent(stream_, slots_[s].ready, 0));
+  if (!for_prefetch) {
+    pb(kRotWait);
+    CFT_CUDA(cudaStreamWaitEvent(stream_, slots_[s].ready, 0));
+    pe();
+  }
 }
 
 void Engine::offload_chunk(int chunk) {
@@ -441,12 +491,15 @@ void Engine::offload_chunk(int chunk) {
   const size_t S = ssz();
   CFT_CUDA(cudaStreamWaitEvent(d2h_, step_done_, 0));
   char* dst = static_cast<char*>(host_states_[chunk]);
+  mark(kD2H, d2h_, true);
   for (int k = 0; k < 3; ++k)
     CFT_CUDA(cudaMemcpyAsync(dst + k * n * S, sl.st[k], n * S, cudaMemcpyDeviceToHost, d2h_));
+  mark(kD2H, d2h_, false);
   CFT_CUDA(cudaEventRecord(sl.free, d2h_));
-  // a later H2D of this chunk must see the completed host copy: order h2d after d2h
-  CFT_CUDA(cudaStreamWaitEvent(h2d_, sl.free, 0));
+  CFT_CUDA(cudaEventRecord(chunk_d2h_[chunk], d2h_));
+  chunk_offloaded_[chunk] = 1;
   sl.chunk = -1;
+  sl.retired = ++retire_seq_;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -462,10 +515,9 @@ int Engine::step_begin() {
   if (a.prefetch >= 0) load_chunk(a.prefetch, true);
   // per-step statistics row {sumsq, nonfinite, first_bad = INT64_MAX, loss} and the
   // precond {min = +inf, max = 0} cells, reset from a device-resident template
-  CFT_CUDA(cudaMemcpyAsync(stats_ + t_ * 4, consts_, 4 * sizeof(double), cudaMemcpyDeviceToDevice,
-                           stream_));
-  CFT_CUDA(cudaMemcpyAsync(precond_, static_cast<char*>(consts_) + 32, 2 * ssz(),
-                           cudaMemcpyDeviceToDevice, stream_));
+  // (SM copies: the copy engines may be busy with a state rotation)
+  layers::sm_copy(stats_ + t_ * 4, consts_, 4 * sizeof(double), stream_);
+  layers::sm_copy(precond_, static_cast<char*>(consts_) + 32, 2 * ssz(), stream_);
   mb_done_ = 0;
   CFT_CUDA(cudaEventRecord(ev_[0], stream_));
   return active_;
@@ -777,7 +829,7 @@ void Engine::step_end() {
   pe();
   CFT_CUDA(cudaEventRecord(ev_[5], s));
   CFT_CUDA(cudaEventRecord(step_done_, s));
-  CFT_CUDA(cudaMemcpyAsync(host_stats_ + t_ * 4, st, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  layers::sm_copy(host_stats_ + t_ * 4, st, 4 * sizeof(double), s);  // into pinned host memory
   CFT_CUDA(cudaEventRecord(stats_ev_[t_ % 4], s));
   traj_step_.push_back(t_);
   traj_chunk_.push_back(c);
@@ -786,8 +838,7 @@ void Engine::step_end() {
   if (off >= 0) offload_chunk(off);
 
   if (cfg_.check_every_step) {
-    CFT_CUDA(cudaMemcpyAsync(host_flags_, flags_, 2 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, s));
+    layers::sm_copy(host_flags_, flags_, 2 * sizeof(unsigned long long), s);
     CFT_CUDA(cudaStreamSynchronize(s));
     const double* h = host_stats_ + t_ * 4;
     const std::string ctx = "step " + std::to_string(t_) + ", chunk " + std::to_string(c) + ": ";

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <chrono>
 #include <memory>
 #include <string>
 #include <vector>
@@ -57,6 +58,7 @@ struct EngineConfig {
   int full_backward = 0;  // 1: propagate dX through every layer like the reference
   int check_every_step = 1;
   double grad_scale = 1.0;  // extra factor folded into the mean (e.g. 1/world for DP)
+  int cuda_graphs = 0;      // Llama engine: replay forward+backward per chunk as a CUDA graph
 };
 
 // Llama-3-shaped decoder: embedding, L x [RMSNorm, GQA attention with
@@ -92,6 +94,7 @@ class Engine {
   void forward_backward(const Batch& b, int mb);     // one micro-batch
   void step_end();                                   // stats, update, offload, bookkeeping
   void finish();                                     // flush all chunks to host, sync
+  void prepare_graphs();  // capture every chunk's forward+backward graph now (Llama engine)
 
   // results
   void trajectory(int64_t* step, int32_t* chunk, double* loss, double* gsq, int64_t* n) const;
@@ -110,12 +113,18 @@ class Engine {
   void timing(float* ms_out) const;  // per-phase CUDA-event times of the last step
 
   // Kernel-category profiler (CUDA events on the engine stream, preallocated pool).
+  // kRotWait: the engine stream waiting for the active chunk's state H2D; kH2D / kD2H: time on
+  // the copy streams (overlapped with compute, not part of the step's critical path unless
+  // kRotWait is non-zero)
+  // kGraph: a replayed forward+backward graph (coarse profiling keeps graphs on)
   enum Phase { kInputs = 0, kFwdGemm, kFwdOther, kLoss, kWgrad, kDgrad, kBwdOther, kStats,
-               kUpdate, kNumPhases };
-  void profile(bool on, int64_t max_marks);
+               kUpdate, kRotWait, kH2D, kD2H, kGraph, kNumPhases };
+  // mode 0 off, 1 per-kernel-category marks (eager launches), 2 coarse marks (graphs stay on)
+  void profile(int mode, int64_t max_marks);
   // syncs; per phase: summed ms, launch count, algorithmic work (GEMM FLOPs; bytes for the
   // statistics / update passes); resets the marks
   void phase_totals(float* ms, int64_t* counts, double* work);
+  void host_phase_ms(double* ms);  // host (submission) time per phase since the last call
   void wait_step(int64_t t, double* loss, double* gsq);  // host waits for step t's result only
 
   // CKFT v1 checkpoints (optimizer.cpp:210-251, FORMATS.md:176-194): one chunk_NNNN.bin per
@@ -147,12 +156,24 @@ class Engine {
     void* st[3] = {nullptr, nullptr, nullptr};  // master, m, v
     cudaEvent_t ready = nullptr;  // H2D finished
     cudaEvent_t free = nullptr;   // D2H finished (slot reusable)
+    uint64_t retired = 0;         // retire order (0: never held a chunk)
   };
+  std::vector<cudaEvent_t> chunk_d2h_;  // per chunk: its last D2H finished
+  std::vector<char> chunk_offloaded_;
+  uint64_t retire_seq_ = 0;
 
   void alloc(void** p, size_t bytes);
   void setup(const double* init_params, uint64_t seed, cudaStream_t stream);
   void llama_alloc();
   void llama_forward_backward(const Batch& b, int mb);
+  // the device work of one micro-batch for the active chunk; reads tokens/labels and
+  // accumulates the loss only through the pointers given (capturable)
+  void llama_body(const int32_t* tok, const int32_t* lab, double* loss_cell, cudaStream_t st);
+  std::vector<cudaGraphExec_t> graphs_;  // per chunk, captured on first use
+  cudaGraphExec_t capture_chunk_graph();
+  cudaStream_t cap_ = nullptr;           // capture stream (the engine stream may be legacy)
+  int32_t *g_tok_ = nullptr, *g_lab_ = nullptr;
+  double* g_loss_ = nullptr;
   int slot_of(int chunk) const;
 
   enum Kind { kSequential = 0, kLlamaModel = 1 };
@@ -223,13 +244,18 @@ class Engine {
     cudaEvent_t a, b;
   };
   bool profiling_ = false;
+  bool coarse_ = false;
   std::vector<cudaEvent_t> pool_;
   size_t pool_next_ = 0;
   std::vector<Mark> marks_;
   int open_phase_ = -1;
   cudaEvent_t open_ev_ = nullptr;
+  cudaEvent_t copy_open_[2] = {nullptr, nullptr};
   void pb(int phase);
+  void mark(int phase, cudaStream_t s, bool begin);  // copy-stream marks
   double work_[16] = {};
+  double host_ms_[16] = {};
+  std::chrono::steady_clock::time_point host_t0_;
   void add_work(int phase, double w) {
     if (profiling_) work_[phase] += w;
   }

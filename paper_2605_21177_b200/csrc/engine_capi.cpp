@@ -29,6 +29,7 @@ static cft::EngineConfig to_config(const cft_engine_config* c) {
   cfg.full_backward = c->full_backward;
   cfg.check_every_step = c->check_every_step;
   cfg.grad_scale = c->grad_scale == 0.0 ? 1.0 : c->grad_scale;
+  cfg.cuda_graphs = c->cuda_graphs;
   return cfg;
 }
 
@@ -157,11 +158,19 @@ int cft_engine_phase_ms(cft_engine* e, float* ms4) {
 }
 
 int cft_engine_profile(cft_engine* e, int enable, int64_t max_marks) {
-  return guarded([&] { e->p->profile(enable != 0, max_marks); });
+  return guarded([&] { e->p->profile(enable, max_marks); });
 }
 
-int cft_engine_phase_totals(cft_engine* e, float* ms9, int64_t* counts9, double* work9) {
-  return guarded([&] { e->p->phase_totals(ms9, counts9, work9); });
+int cft_engine_prepare_graphs(cft_engine* e) {
+  return guarded([&] { e->p->prepare_graphs(); });
+}
+
+int cft_engine_host_phase_ms(cft_engine* e, double* ms) {
+  return guarded([&] { e->p->host_phase_ms(ms); });
+}
+
+int cft_engine_phase_totals(cft_engine* e, float* ms, int64_t* counts, double* work) {
+  return guarded([&] { e->p->phase_totals(ms, counts, work); });
 }
 
 int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq) {

@@ -78,6 +78,9 @@ void loss_f64(int kind, const double* y, const double* target, const int32_t* la
               long long rows, long long cols, double* dy, double* loss_acc, double* scratch,
               unsigned long long* bad_label, cudaStream_t);
 void add_f64(double* dst, const double* src, long long n, cudaStream_t s);
+// SM-driven copy for small transfers (either side may be pinned host memory)
+void sm_copy(void* dst, const void* src, long long bytes, cudaStream_t s);
+bool host_pinned(const void* p);  // pinned + mapped at the same address (UVA)
 void add_f32(float* dst, const float* src, long long n, cudaStream_t s);
 void flag_nonfinite_loss(double* stats_row, cudaStream_t s);
 void count_in_range(const int32_t* tokens, long long n, long long lo, long long hi,
@@ -92,6 +95,7 @@ void rms_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd,
              __nv_bfloat16* out, cudaStream_t s);
 void rms_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd,
                 long long rows, int d, long long rb, long long re, float* out, cudaStream_t s);
+void rope_prepare(int seq, int hd, float theta);  // build the cos/sin table (not capturable)
 void rope(__nv_bfloat16* qkv, long long tokens, int seq, int heads, int hd, int ld, float theta,
           bool backward, cudaStream_t s);
 void swiglu_fwd(const __nv_bfloat16* ug, long long rows, int F, __nv_bfloat16* out, cudaStream_t s);

@@ -447,6 +447,45 @@ void flag_nonfinite_loss(double* st, cudaStream_t s) {
   check_launch("flag_nonfinite_loss");
 }
 
+// Small copies done by the SMs instead of a copy engine: the engine's copy engines are busy
+// with multi-GB state rotations, and a 32-byte cudaMemcpyAsync on the compute stream would
+// queue behind them.  Either side may be pinned host memory (mapped through UVA).
+__global__ void sm_copy_kernel(uint4* dst, const uint4* src, long long n16, uint8_t* dtail,
+                               const uint8_t* stail, int tail) {
+  const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long i = i0; i < n16; i += (long long)gridDim.x * blockDim.x) dst[i] = src[i];
+  if (i0 < tail) dtail[i0] = stail[i0];
+}
+__global__ void sm_copy_bytes_kernel(uint8_t* dst, const uint8_t* src, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+void sm_copy(void* dst, const void* src, long long bytes, cudaStream_t s) {
+  if (bytes <= 0) return;
+  const auto d = reinterpret_cast<uintptr_t>(dst), r = reinterpret_cast<uintptr_t>(src);
+  if (((d | r) & 15) == 0) {
+    const long long n16 = bytes / 16;
+    const int tail = static_cast<int>(bytes - n16 * 16);
+    const long long blocks = std::max<long long>(1, std::min<long long>((n16 + 255) / 256, 64));
+    sm_copy_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+        static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16,
+        static_cast<uint8_t*>(dst) + n16 * 16, static_cast<const uint8_t*>(src) + n16 * 16, tail);
+  } else {
+    sm_copy_bytes_kernel<<<(unsigned)std::min<long long>((bytes + 255) / 256, 64), 256, 0, s>>>(
+        static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes);
+  }
+  check_launch("sm_copy");
+}
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+}
+
 void add_f64(double* dst, const double* src, long long n, cudaStream_t s) {
   if (n <= 0) return;
   add_f64_kernel<<<grid_n(n), 256, 0, s>>>(dst, src, n);

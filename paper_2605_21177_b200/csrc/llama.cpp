@@ -105,13 +105,114 @@ void Engine::llama_alloc() {
     in_tokens_[k] = static_cast<int32_t*>(A(N, 4));
     in_labels_[k] = static_cast<int32_t*>(A(N, 4));
   }
+  g_tok_ = static_cast<int32_t*>(A(N, 4));
+  g_lab_ = static_cast<int32_t*>(A(N, 4));
+  g_loss_ = static_cast<double*>(A(1, 8));
+  CFT_CUDA(cudaStreamCreateWithFlags(&cap_, cudaStreamNonBlocking));
+  // everything a capture may not do (allocation, first-use tables, cuDNN plan builds and
+  // workspace) happens here, before any step
   attn_ = std::make_unique<attn::Context>();
   attn_->prepare(cfg_.batch_rows, s.heads, s.kv_heads, s.seq, s.head_dim);
+  llama::rope_prepare(s.seq, s.head_dim, static_cast<float>(s.rope_theta));
 }
 
 void Engine::llama_forward_backward(const Batch& b, int mb) {
-  const LlamaSpec& S = ls_;
+  const int64_t N = int64_t(cfg_.batch_rows) * ls_.seq;
   cudaStream_t st = stream_;
+  // ---- inputs: device batches are read in place; host batches upload on in_stream_ into
+  // staging buffer k (reusable once the step that read it has finished) ----
+  pb(kInputs);
+  const int32_t* tok;
+  const int32_t* lab;
+  int staged = -1;
+  if (b.on_device) {
+    tok = b.tokens;
+    lab = b.labels;
+  } else {
+    const int k = static_cast<int>(uploads_++ & 1);
+    CFT_CUDA(cudaStreamWaitEvent(in_stream_, in_free_[k], 0));
+    // pinned batches are pulled by the SMs over PCIe (the copy engines may be busy with a
+    // state rotation); pageable ones go through the copy engine
+    if (layers::host_pinned(b.tokens) && layers::host_pinned(b.labels)) {
+      layers::sm_copy(in_tokens_[k], b.tokens, N * 4, in_stream_);
+      layers::sm_copy(in_labels_[k], b.labels, N * 4, in_stream_);
+    } else {
+      CFT_CUDA(cudaMemcpyAsync(in_tokens_[k], b.tokens, N * 4, cudaMemcpyHostToDevice, in_stream_));
+      CFT_CUDA(cudaMemcpyAsync(in_labels_[k], b.labels, N * 4, cudaMemcpyHostToDevice, in_stream_));
+    }
+    CFT_CUDA(cudaEventRecord(in_ready_[k], in_stream_));
+    CFT_CUDA(cudaStreamWaitEvent(st, in_ready_[k], 0));
+    tok = in_tokens_[k];
+    lab = in_labels_[k];
+    staged = k;
+  }
+  CFT_CHECK(tok != nullptr && lab != nullptr, "forward: token batch required");
+  double* loss_cell = stats_ + t_ * 4 + 3;
+  const bool graphed = cfg_.cuda_graphs && (!profiling_ || coarse_);
+  if (graphed) {
+    // the captured graph reads fixed buffers: copy this micro-batch in (2 x N x 4 bytes)
+    layers::sm_copy(g_tok_, tok, N * 4, st);
+    layers::sm_copy(g_lab_, lab, N * 4, st);
+  }
+  pe();
+  if (staged >= 0 && graphed) CFT_CUDA(cudaEventRecord(in_free_[staged], st));
+
+  if (graphed) {
+    if (graphs_.empty()) graphs_.assign(plan_.chunks.size(), nullptr);
+    cudaGraphExec_t& ge = graphs_[active_];
+    if (!ge) ge = capture_chunk_graph();
+    pb(kGraph);
+    CFT_CUDA(cudaGraphLaunch(ge, st));
+    pe();
+    layers::add_f64(loss_cell, g_loss_, 1, st);
+  } else {
+    llama_body(tok, lab, loss_cell, st);
+    if (staged >= 0) CFT_CUDA(cudaEventRecord(in_free_[staged], st));
+  }
+  (void)mb;
+}
+
+// Capture the active chunk's forward+backward (fixed input buffers, fixed loss cell) on the
+// private capture stream; capture records, it does not execute.
+cudaGraphExec_t Engine::capture_chunk_graph() {
+  const bool prof = profiling_;
+  profiling_ = false;  // no profiler events inside a capture
+  CFT_CUDA(cudaStreamBeginCapture(cap_, cudaStreamCaptureModeThreadLocal));
+  try {
+    CFT_CUDA(cudaMemsetAsync(g_loss_, 0, sizeof(double), cap_));
+    llama_body(g_tok_, g_lab_, g_loss_, cap_);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(cap_, &g);
+    if (g) cudaGraphDestroy(g);
+    profiling_ = prof;
+    throw;
+  }
+  profiling_ = prof;
+  cudaGraph_t g = nullptr;
+  CFT_CUDA(cudaStreamEndCapture(cap_, &g));
+  cudaGraphExec_t ge = nullptr;
+  CFT_CUDA(cudaGraphInstantiate(&ge, g, 0));
+  CFT_CUDA(cudaGraphDestroy(g));
+  return ge;
+}
+
+void Engine::prepare_graphs() {
+  if (kind_ != kLlamaModel || !cfg_.cuda_graphs) return;
+  CFT_CHECK(active_ < 0 || mb_done_ == 0, "engine: prepare_graphs inside a step");
+  if (graphs_.empty()) graphs_.assign(plan_.chunks.size(), nullptr);
+  const int keep = active_;
+  for (int c = 0; c < static_cast<int>(plan_.chunks.size()); ++c) {
+    if (graphs_[c]) continue;
+    active_ = c;
+    graphs_[c] = capture_chunk_graph();
+  }
+  active_ = keep;
+}
+
+void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cell,
+                        cudaStream_t st) {
+  const LlamaSpec& S = ls_;
   const int B = cfg_.batch_rows, L = S.layers;
   const int64_t N = int64_t(B) * S.seq;
   const int64_t d = S.d, Q = int64_t(S.heads) * S.head_dim, KV = int64_t(S.kv_heads) * S.head_dim,
@@ -140,25 +241,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
     pe();
   };
 
-  // ---- inputs ----
   pb(kInputs);
-  const int32_t* tok;
-  const int32_t* lab;
-  if (b.on_device) {
-    tok = b.tokens;
-    lab = b.labels;
-  } else {
-    const int k = static_cast<int>(uploads_++ & 1);
-    CFT_CUDA(cudaStreamWaitEvent(in_stream_, in_free_[k], 0));
-    CFT_CUDA(cudaMemcpyAsync(in_tokens_[k], b.tokens, N * 4, cudaMemcpyHostToDevice, in_stream_));
-    CFT_CUDA(cudaMemcpyAsync(in_labels_[k], b.labels, N * 4, cudaMemcpyHostToDevice, in_stream_));
-    CFT_CUDA(cudaEventRecord(in_ready_[k], in_stream_));
-    CFT_CUDA(cudaStreamWaitEvent(st, in_ready_[k], 0));
-    tok = in_tokens_[k];
-    lab = in_labels_[k];
-    staged_slot_ = k;
-  }
-  CFT_CHECK(tok != nullptr && lab != nullptr, "forward: token batch required");
   layers::count_in_range(tok, N, 0, V, reinterpret_cast<long long*>(flags_ + 1), st);
   pe();
 
@@ -216,7 +299,7 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
   // ---- next-token CE (autodiff.cpp:205-225); dlogits written in place ----
   pb(kLoss);
   layers::loss<bf16>(3, static_cast<bf16*>(l_logits_), nullptr, lab, N, V,
-                     static_cast<bf16*>(l_logits_), stats_ + t_ * 4 + 3, flags_, st);
+                     static_cast<bf16*>(l_logits_), loss_cell, flags_, st);
   pe();
 
   // ---- chunk-masked backward over the suffix ----
@@ -314,11 +397,6 @@ void Engine::llama_forward_backward(const Batch& b, int mb) {
       throw Error(last_error());
     pe();
   }
-  if (staged_slot_ >= 0) {
-    CFT_CUDA(cudaEventRecord(in_free_[staged_slot_], st));
-    staged_slot_ = -1;
-  }
-  (void)mb;
 }
 
 }  // namespace cft

@@ -294,26 +294,34 @@ __global__ void rope_vec_kernel(bf16* qkv, long long tokens, int seq, int heads,
   }
 }
 
+namespace {
+// cos/sin tables per (seq, head_dim, theta), built once on the device; looked up at launch
+std::mutex g_rope_mu;
+std::map<std::tuple<int, int, float>, float2*> g_rope_tables;
+
+float2* rope_table(int seq, int hd, float theta) {
+  std::lock_guard<std::mutex> lock(g_rope_mu);
+  const auto key = std::make_tuple(seq, hd, theta);
+  auto it = g_rope_tables.find(key);
+  if (it != g_rope_tables.end()) return it->second;
+  const int half = hd / 2;
+  float2* cs = nullptr;
+  CFT_CUDA(cudaMalloc(&cs, sizeof(float2) * seq * half));
+  rope_table_kernel<<<(seq * half + 255) / 256, 256>>>(cs, seq, half, theta);
+  check_launch("rope_table");
+  CFT_CUDA(cudaDeviceSynchronize());
+  g_rope_tables.emplace(key, cs);
+  return cs;
+}
+}  // namespace
+
+void rope_prepare(int seq, int hd, float theta) { rope_table(seq, hd, theta); }
+
 void rope(bf16* qkv, long long tokens, int seq, int heads, int hd, int ld, float theta,
           bool backward, cudaStream_t s) {
   const int half = hd / 2;
   if (half % 8 == 0 && ld % 8 == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0) {
-    static std::mutex mu;
-    static std::map<std::tuple<int, int, float>, float2*> tables;
-    float2* cs;
-    {
-      std::lock_guard<std::mutex> lock(mu);
-      auto key = std::make_tuple(seq, hd, theta);
-      auto it = tables.find(key);
-      if (it == tables.end()) {
-        CFT_CUDA(cudaMalloc(&cs, sizeof(float2) * seq * half));
-        rope_table_kernel<<<(seq * half + 255) / 256, 256, 0, s>>>(cs, seq, half, theta);
-        check_launch("rope_table");
-        tables.emplace(key, cs);
-      } else {
-        cs = it->second;
-      }
-    }
+    const float2* cs = rope_table(seq, hd, theta);
     rope_vec_kernel<<<grid_for(tokens * heads * half / 8), 256, 0, s>>>(
         qkv, tokens, seq, heads, hd, ld, cs, backward ? -1.f : 1.f);
     check_launch("rope_vec");

@@ -35,7 +35,8 @@ class EngineConfigC(C.Structure):
                 ("prefetch", C.c_int32), ("offload", C.c_int32),
                 ("bandwidth_bytes_per_step", C.c_int64), ("budget_bytes", C.c_int64),
                 ("hyper", N.AdamWHyperC), ("full_backward", C.c_int32),
-                ("check_every_step", C.c_int32), ("grad_scale", C.c_double)]
+                ("check_every_step", C.c_int32), ("grad_scale", C.c_double),
+                ("cuda_graphs", C.c_int32), ("pad_", C.c_int32)]
 
 
 class BatchC(C.Structure):
@@ -73,6 +74,8 @@ for _n, _r, _a in [
     ("cft_engine_phase_ms", C.c_int, [C.c_void_p, C.c_void_p]),
     ("cft_engine_profile", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
     ("cft_engine_phase_totals", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("cft_engine_host_phase_ms", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("cft_engine_prepare_graphs", C.c_int, [C.c_void_p]),
     ("cft_engine_wait_step", C.c_int, [C.c_void_p, C.c_int64, _P(C.c_double), _P(C.c_double)]),
     ("cft_engine_write_checkpoints", C.c_int, [C.c_void_p, C.c_char_p]),
     ("cft_engine_read_checkpoints", C.c_int, [C.c_void_p, C.c_char_p]),
@@ -218,6 +221,7 @@ class TrainOptions:
     offload: bool = True
     full_backward: bool = False
     check_every_step: bool = True
+    cuda_graphs: bool = True      # Llama engine: one captured graph per chunk's forward+backward
 
 
 class ChunkEngine:
@@ -242,6 +246,7 @@ class ChunkEngine:
         cfg.total_steps = o.schedule.total_steps
         cfg.prefetch = int(o.schedule.prefetch)
         cfg.offload = int(o.offload)
+        cfg.cuda_graphs = int(o.cuda_graphs)
         cfg.bandwidth_bytes_per_step = o.schedule.bandwidth_bytes_per_step
         cfg.budget_bytes = o.budget_bytes
         h = o.hyper
@@ -385,22 +390,35 @@ class ChunkEngine:
         return out
 
     PHASES = ("inputs", "fwd_gemm", "fwd_other", "loss", "wgrad", "dgrad", "bwd_other", "stats",
-              "update")
+              "update", "rot_wait", "h2d", "d2h", "graph")
 
-    def profile(self, enable: bool = True, max_marks: int = 1 << 14):
+    def profile(self, enable=True, max_marks: int = 1 << 14):
+        """enable: False/0 off, True/1 per-kernel-category marks (eager launches), 2 coarse
+        marks with CUDA graphs kept on."""
         N.check(_L.cft_engine_profile(self._h, int(enable), max_marks))
 
     def phase_totals(self, with_work: bool = False):
         """{phase: (ms, launches)} or, with_work, {phase: (ms, launches, work)} where work is
         algorithmic GEMM FLOPs (fwd_gemm / wgrad / dgrad) or bytes (stats / update)."""
-        ms = np.zeros(9, np.float32)
-        cnt = np.zeros(9, np.int64)
-        work = np.zeros(9, np.float64)
+        n = len(self.PHASES)
+        ms = np.zeros(n, np.float32)
+        cnt = np.zeros(n, np.int64)
+        work = np.zeros(n, np.float64)
         N.check(_L.cft_engine_phase_totals(self._h, ms.ctypes.data, cnt.ctypes.data,
                                            work.ctypes.data))
         if with_work:
             return {k: (float(ms[i]), int(cnt[i]), float(work[i])) for i, k in enumerate(self.PHASES)}
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PHASES)}
+
+    def prepare_graphs(self):
+        """Capture every chunk's forward+backward CUDA graph now (Llama engine)."""
+        N.check(_L.cft_engine_prepare_graphs(self._h), "prepare_graphs")
+
+    def host_phase_ms(self):
+        """{phase: host submission ms} accumulated since the previous call (profiling on)."""
+        ms = np.zeros(len(self.PHASES), np.float64)
+        N.check(_L.cft_engine_host_phase_ms(self._h, ms.ctypes.data))
+        return {k: float(ms[i]) for i, k in enumerate(self.PHASES)}
 
     def write_checkpoints(self, directory: str):
         """CKFT v1 files dir/chunk_NNNN.bin (optimizer.cpp:210-230); call after finish()."""

@@ -77,7 +77,8 @@ def torch_reference(model, flat, tokens, labels):
     return loss.item(), p.grad.double().cpu().numpy()
 
 
-def test_llama_chunk_gradients_vs_torch_fp32(cuda):
+@pytest.mark.parametrize("graphs", [True, False], ids=["graph", "eager"])
+def test_llama_chunk_gradients_vs_torch_fp32(cuda, graphs):
     from paper_2605_21177_b200.engine import ChunkEngine, LlamaModel, TrainOptions
     from paper_2605_21177_b200.plan import ScheduleConfig, TensorInfo, partition
     model = LlamaModel()
@@ -89,7 +90,8 @@ def test_llama_chunk_gradients_vs_torch_fp32(cuda):
     ref_loss, ref_grad = torch_reference(model, flat, tokens, labels)
 
     K = 6
-    opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=K), dtype="bf16")
+    opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=K), dtype="bf16",
+                        cuda_graphs=graphs)
     eng = ChunkEngine(model, flat, B, opts)
     infos = [TensorInfo(i, n, r, c) for i, (n, r, c) in enumerate(model.tensors())]
     plan = partition(infos, K)
@@ -141,3 +143,33 @@ def test_llama_device_init_and_rotation_smoke(cuda):
     tr = eng.trajectory()
     assert np.all(np.isfinite(tr["loss"])) and np.all(tr["loss"] > 0)
     assert tr["chunk"].tolist() == [t % plan.K for t in range(2 * plan.K)]
+
+
+def test_llama_graph_replay_matches_eager(cuda):
+    """Per-chunk CUDA-graph replay (tokens copied into the graph's fixed input buffers, loss
+    accumulated through a fixed cell) gives the eager path's trajectory; host batches take
+    the double-buffered upload path."""
+    from paper_2605_21177_b200.engine import ChunkEngine, LlamaModel, TrainOptions
+    from paper_2605_21177_b200.plan import ScheduleConfig
+    model = LlamaModel(layers=2)
+    B, K = 2, 5
+    flat = init_params(model, seed=5)
+    rng = np.random.default_rng(4)
+    batches = []
+    for _ in range(3):
+        seqs = rng.integers(0, model.vocab, (B, model.seq + 1)).astype(np.int32)
+        batches.append({"tokens": seqs[:, :-1].copy(), "labels": seqs[:, 1:].copy()})
+    out = {}
+    for graphs in (False, True):
+        opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=3 * K, prefetch=True),
+                            dtype="bf16", cuda_graphs=graphs, check_every_step=False)
+        eng = ChunkEngine(model, flat, B, opts)
+        staged = [eng.stage(b, device=(i % 2 == 0)) for i, b in enumerate(batches)]
+        for t in range(3 * K):
+            eng.step([staged[t % 3]])
+        eng.finish()
+        out[graphs] = (eng.trajectory()["loss"], eng.params(from_masters=True))
+    (l0, p0), (l1, p1) = out[False], out[True]
+    assert np.all(np.isfinite(l1))
+    np.testing.assert_allclose(l1, l0, rtol=2e-3)
+    assert np.linalg.norm(p1 - p0) / np.linalg.norm(p0) < 1e-3
