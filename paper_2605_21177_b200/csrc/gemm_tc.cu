@@ -17,6 +17,8 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -37,6 +39,7 @@ struct Args {
   int m_off;      // A coordinate offset along M (row_begin rounded down to 8 elements)
   int row_skip;   // row_begin - m_off: leading tile rows that belong to the previous slice
   int tiles_m, tiles_n, splits, kb_per_split, total_kb, num_units;
+  int group_m;    // row-blocks per rasterisation group (see decode_unit)
   void* C;
   long long ldc;
   int epi;
@@ -54,12 +57,18 @@ struct Cfg {
 };
 
 __device__ __forceinline__ void decode_unit(const Args& a, int u, int& tm, int& tn, int& sp) {
-  // splits fastest, then N, then M: the CTAs of one wave cover ~148/tiles_n row-blocks of A
-  // across all column blocks, so A streams from HBM once and B (the weight) stays L2-resident.
+  // splits fastest; tiles in groups of group_m row-blocks, M fastest inside a group, so the
+  // ~148 tiles in flight at once form a compact ~group_m x (slots/group_m) block: each k-slab of
+  // A is shared by ~slots/group_m concurrent tiles and each k-slab of B by ~group_m, and the
+  // wave's operand traffic is ~(group_m + slots/group_m) slabs instead of (1 + slots) for a
+  // row-major order over a wide N (measured: 2.4 GB DRAM reads for a 0.5 GB dgrad).
   sp = u % a.splits;
   const int t = u / a.splits;
-  tn = t % a.tiles_n;
-  tm = t / a.tiles_n;
+  const int per_group = a.group_m * a.tiles_n;
+  const int g = t / per_group, r = t - g * per_group;
+  const int rows = min(a.group_m, a.tiles_m - g * a.group_m);
+  tm = g * a.group_m + r % rows;
+  tn = r / rows;
 }
 
 // Epilogue store of 16 consecutive accumulator columns of one output row (one thread).
@@ -543,6 +552,20 @@ void fill_units(Args& a, int bm, int bn, int slots, double us_per_kb, bool allow
   a.kb_per_split = (a.total_kb + s - 1) / s;
   a.splits = (a.total_kb + a.kb_per_split - 1) / a.kb_per_split;
   a.num_units = tiles * a.splits;
+  // concurrent tiles ~ slots: the square-ish block (in bytes of operand slab per tile side)
+  // minimises the wave's distinct k-slabs: group_m ~ sqrt(slots * bn / bm).  CTA-pair tiles:
+  // measured under the power cap (tools/probe_group.py, 8B shapes), tall groups (16) win for
+  // wide N or long K -- fewer DRAM re-reads of the weight -- and short ones (2) for the small
+  // 4096-wide GEMMs.
+  const int concurrent = std::max(1, slots / a.splits);
+  int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(concurrent) * bn / bm)));
+  if (bm == 256) g = (a.tiles_n > 20 || a.K > 8192) ? 16 : 2;
+  static const int forced = [] {
+    const char* e = std::getenv("CFT_GEMM_GROUP_M");  // experiments: fixed group size
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0) g = forced;
+  a.group_m = std::max(1, std::min(g, a.tiles_m));
 }
 
 template <bool A_MN, bool B_MN, int BNP>
