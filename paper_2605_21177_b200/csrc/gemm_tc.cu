@@ -94,7 +94,9 @@ __device__ __forceinline__ void store16(const Args& args, long long rbase, int c
         }
       }
     } else {
-      for (int j = 0; j < 16 && col + j < args.N; ++j) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {  // static indices keep r[] in registers
+        if (col + j >= args.N) break;
         const float a0 = __uint_as_float(r[j]);
         if (args.epi == kEpiF32Red) atomicAdd(out + j, a0);
         else if (args.epi == kEpiF32Add) out[j] += a0;
@@ -134,7 +136,9 @@ __device__ __forceinline__ void store16(const Args& args, long long rbase, int c
         *reinterpret_cast<uint4*>(out + j) = pk;
       }
     } else {
-      for (int j = 0; j < 16 && col + j < args.N; ++j) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (col + j >= args.N) break;
         float a0 = __uint_as_float(r[j]);
         if (res) a0 += __bfloat162float(res[j]);
         out[j] = __float2bfloat16_rn(a0);
@@ -438,8 +442,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quarter = warp & 3;
-    const uint32_t tempty_leader[2] = {ptx::mapa(ptx::smem_u32(&tempty[0]), 0),
-                                       ptx::mapa(ptx::smem_u32(&tempty[1]), 0)};
+    const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0),
+                   tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = pair; u < args.num_units; u += npairs) {
@@ -460,7 +464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader[acc]);
+      if (lane == 0) ptx::mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
