@@ -181,6 +181,17 @@ int cft_linear_fwd(cft_dtype dtype, const void* x, int64_t n_tok, int64_t in_dim
 int cft_linear_dgrad(cft_dtype dtype, const void* dy, int64_t n_tok, int64_t out_dim,
                      const void* w, int64_t in_dim, void* dx, int beta, cft_stream_t stream);
 
+/* Llama MLP with SwiGLU fused into the GEMM epilogues (bf16 only; SURVEY 8(f1) extension):
+ *   fwd: s = silu(x w1^T) * (x w3^T), w13 = [w1; w3] (2F x in); ug (n_tok x 2F, may be NULL)
+ *        receives [x w1^T | x w3^T] for the backward.  F % 128 == 0.
+ *   bwd: [du | dg] = swiglu_backward(dy . w2, u, g), w2: out x F, ug / dug: n_tok x 2F.
+ *        F % 32 == 0.
+ * Rounding equals the unfused GEMM + elementwise pair exactly. */
+int cft_linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void* w13,
+                          int64_t F, void* s, void* ug, cft_stream_t stream);
+int cft_linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2,
+                            int64_t F, const void* ug, void* dug, cft_stream_t stream);
+
 /* Slice-aware weight gradient, dW_S = dY[:, rb:re)^T . X  (never forms a dense dW).
  *   dw_slice[(o-rb)*in + i] (+)= sum_b dy[b,o] x[b,i],  o in [rb, re)
  * dw_slice is fp32 for CFT_F32/CFT_BF16 and fp64 for CFT_F64; accumulate 0 overwrites,
@@ -256,6 +267,9 @@ int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t
 /* bf16 GEMM tiling policy: 0 auto (CTA-pair 256x256 tcgen05 tiles when the tile space fills
  * the chip, single-CTA 128x256 otherwise), 1 force single-CTA, 2 force CTA pairs. */
 int cft_set_gemm_policy(int policy);
+/* Epilogue fusions of the Llama engine (SwiGLU in the w1|w3 forward and w2 dgrad GEMMs):
+ * 1 on (default), 0 off -- results are bit-identical either way. */
+int cft_set_fusion(int enable);
 
 /* Element conversion (e.g. fp32 master -> bf16 params at init). */
 int cft_convert(cft_dtype src_dtype, const void* src, cft_dtype dst_dtype, void* dst, int64_t n,

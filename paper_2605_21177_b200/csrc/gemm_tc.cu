@@ -30,7 +30,11 @@ namespace cft::tc {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;
+// warp 0: TMA producer, warp 1: MMA issuer + TMEM owner, warps 2..9: epilogue -- two warps
+// per TMEM lane quarter, each taking half of the tile's columns (twice the memory-level
+// parallelism for epilogues that read as well as write: residual adds, the SwiGLU backward)
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 enum Epi : int { kEpiBf16 = 0, kEpiBf16Add = 1, kEpiF32 = 2, kEpiF32Add = 3, kEpiF32Red = 4 };
 
@@ -40,6 +44,14 @@ struct Args {
   int row_skip;   // row_begin - m_off: leading tile rows that belong to the previous slice
   int tiles_m, tiles_n, splits, kb_per_split, total_kb, num_units;
   int group_m;    // row-blocks per rasterisation group (see decode_unit)
+  // SwiGLU fusion (Llama MLP).  glu 1 (forward, pair kernel): B is the stacked [w1; w3] with
+  //   w3 at row glu_F; CTA rank 0 stages w1 rows, rank 1 the matching w3 rows, so accumulator
+  //   columns [0,128) hold u and [128,256) g for output features tn*128..; the epilogue writes
+  //   s = silu(u) g to C (ld = glu_F) and, if glu_ug, [u | g] to glu_ug (ld = 2 glu_F).
+  // glu 2 (dgrad of w2): the accumulator is ds; the epilogue reads [u | g] from glu_ug and
+  //   writes [du | dg] to C (ld = 2 glu_F).  Both round exactly like the unfused kernels.
+  int glu, glu_F;
+  void* glu_ug;
   void* C;
   long long ldc;
   int epi;
@@ -147,6 +159,112 @@ __device__ __forceinline__ void store16(const Args& args, long long rbase, int c
   }
 }
 
+// fast reciprocal (MUFU.RCP): the same expression as llama::sigm, so fused == unfused bitwise
+__device__ __forceinline__ float glu_sigm(float u) { return __fdividef(1.f, 1.f + __expf(-u)); }
+__device__ __forceinline__ float bf16_round(float v) {
+  return __bfloat162float(__float2bfloat16_rn(v));
+}
+__device__ __forceinline__ uint4 pack8_bf16(const float* f) {
+  uint4 pk;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
+    w[q] = *reinterpret_cast<uint32_t*>(&v);
+  }
+  return pk;
+}
+__device__ __forceinline__ void unpack8_bf16(const uint4& pk, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&pk);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 v = __bfloat1622float2(h[q]);
+    f[2 * q] = v.x;
+    f[2 * q + 1] = v.y;
+  }
+}
+
+// glu 1: 16 output features of one row from the u / g accumulator columns (F % 128 == 0, so a
+// chunk is never partial).  Same math as swiglu_fwd_kernel on the bf16-rounded u, g.
+__device__ __forceinline__ void glu_fwd_store16(const Args& args, long long row, int col,
+                                                const uint32_t (&ru)[16],
+                                                const uint32_t (&rg)[16]) {
+  const long long F = args.glu_F;
+  float u[16], g[16], o[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    u[j] = bf16_round(__uint_as_float(ru[j]));
+    g[j] = bf16_round(__uint_as_float(rg[j]));
+    o[j] = u[j] * glu_sigm(u[j]) * g[j];
+  }
+  uint4* out = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + row * F + col);
+  out[0] = pack8_bf16(o);
+  out[1] = pack8_bf16(o + 8);
+  if (args.glu_ug) {
+    __nv_bfloat16* ug = static_cast<__nv_bfloat16*>(args.glu_ug) + row * 2 * F + col;
+    reinterpret_cast<uint4*>(ug)[0] = pack8_bf16(u);
+    reinterpret_cast<uint4*>(ug)[1] = pack8_bf16(u + 8);
+    reinterpret_cast<uint4*>(ug + F)[0] = pack8_bf16(g);
+    reinterpret_cast<uint4*>(ug + F)[1] = pack8_bf16(g + 8);
+  }
+}
+
+// glu 2: the epilogue of one tile row (this thread's row, BN accumulator columns = ds):
+// [du | dg] from ds and the saved [u | g], 32 features per step with the next step's u / g
+// loads in flight while this step's TMEM columns are read (the ug reads would otherwise
+// serialise the epilogue on memory latency).  Same math as swiglu_bwd_kernel on bf16 ds.
+template <int BN>
+__device__ __forceinline__ void glu_bwd_epilogue(const Args& args, uint32_t tacc, int row,
+                                                 bool row_ok, int tn, int c0, int c1) {
+  const long long F = args.glu_F;
+  const __nv_bfloat16* ugr =
+      static_cast<const __nv_bfloat16*>(args.glu_ug) + static_cast<long long>(row) * 2 * F;
+  __nv_bfloat16* outr = static_cast<__nv_bfloat16*>(args.C) + static_cast<long long>(row) * 2 * F;
+  uint4 cu[4], cg[4], nu[4], ng[4];
+  auto load = [&](int c, uint4 (&U)[4], uint4 (&G)[4]) {
+    const int col = tn * BN + c;
+    if (row_ok && col < args.N) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // streaming: keep the GEMM operands in L2
+        U[i] = __ldcs(reinterpret_cast<const uint4*>(ugr + col) + i);
+        G[i] = __ldcs(reinterpret_cast<const uint4*>(ugr + F + col) + i);
+      }
+    }
+  };
+  load(c0, cu, cg);
+#pragma unroll 1
+  for (int c = c0; c < c1; c += 32) {
+    if (c + 32 < c1) load(c + 32, nu, ng);
+    uint32_t r[32];
+    ptx::tmem_ld16(tacc + c, *reinterpret_cast<uint32_t(*)[16]>(r));
+    ptx::tmem_ld16(tacc + c + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
+    ptx::tmem_wait_ld();
+    const int col = tn * BN + c;
+    if (row_ok && col < args.N) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        float u[8], g[8], du[8], dg[8];
+        unpack8_bf16(cu[h], u);
+        unpack8_bf16(cg[h], g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = bf16_round(__uint_as_float(r[8 * h + j]));
+          const float sg = glu_sigm(u[j]);
+          du[j] = d * g[j] * sg * (1.f + u[j] * (1.f - sg));
+          dg[j] = d * u[j] * sg;
+        }
+        __stcs(reinterpret_cast<uint4*>(outr + col) + h, pack8_bf16(du));
+        __stcs(reinterpret_cast<uint4*>(outr + F + col) + h, pack8_bf16(dg));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      cu[i] = nu[i];
+      cg[i] = ng[i];
+    }
+  }
+}
+
 template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -175,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4);
+      ptx::mbar_init(&tempty[a], kEpiWarps);
     }
     ptx::fence_barrier_init();
   }
@@ -266,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // Epilogue: warp w may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
     const int quarter = warp & 3;
+    const int half = (warp - 2) / 4;  // which half of the tile's columns
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < args.num_units; u += gridDim.x) {
@@ -276,13 +395,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = tm * BM + quarter * 32 + lane - args.row_skip;
       const bool row_ok = row >= 0 && row < args.M;
       const long long rbase = static_cast<long long>(row) * args.ldc;
+      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      if (args.glu == 2) {
+        glu_bwd_epilogue<BN>(args, tacc, row, row_ok, tn, half * (BN / 2), (half + 1) * (BN / 2));
+      } else {
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        ptx::tmem_ld16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c, r);
-        ptx::tmem_wait_ld();
-        const int col = tn * BN + c;
-        if (row_ok && col < args.N) store16(args, rbase, col, r);
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
+          uint32_t r[16];
+          ptx::tmem_ld16(tacc + c, r);
+          ptx::tmem_wait_ld();
+          const int col = tn * BN + c;
+          if (row_ok && col < args.N) store16(args, rbase, col, r);
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -354,7 +478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (used on the leader)
+      ptx::mbar_init(&tempty[a], 2 * kEpiWarps);  // epilogue warps x 2 CTAs (on the leader)
     }
     ptx::fence_barrier_init();
   }
@@ -374,7 +498,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int kb0 = sp * args.kb_per_split;
         const int kb1 = min(kb0 + args.kb_per_split, args.total_kb);
         const int m0 = args.m_off + tm * BMP + static_cast<int>(rank) * 128;
-        const int n0 = tn * BNP + static_cast<int>(rank) * (BNP / 2);
+        const int n0 = args.glu == 1 ? tn * (BNP / 2) + static_cast<int>(rank) * args.glu_F
+                                     : tn * BNP + static_cast<int>(rank) * (BNP / 2);
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_expect_tx(&full[stage], 2 * kPairStageBytes);
@@ -442,6 +567,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quarter = warp & 3;
+    const int half = (warp - 2) / 4;  // which half of the tile's columns
     const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0),
                    tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
     int acc = 0;
@@ -454,13 +580,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int row = tm * BMP + static_cast<int>(rank) * 128 + quarter * 32 + lane - args.row_skip;
       const bool row_ok = row >= 0 && row < args.M;
       const long long rbase = static_cast<long long>(row) * args.ldc;
+      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BNP;
+      if (args.glu == 1) {
 #pragma unroll 1
-      for (int c = 0; c < BNP; c += 16) {
-        uint32_t r[16];
-        ptx::tmem_ld16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BNP + c, r);
-        ptx::tmem_wait_ld();
-        const int col = tn * BNP + c;
-        if (row_ok && col < args.N) store16(args, rbase, col, r);
+        for (int c = half * (BNP / 4); c < (half + 1) * (BNP / 4); c += 16) {
+          uint32_t ru[16], rg[16];
+          ptx::tmem_ld16(tacc + c, ru);
+          ptx::tmem_ld16(tacc + BNP / 2 + c, rg);
+          ptx::tmem_wait_ld();
+          const int col = tn * (BNP / 2) + c;
+          if (row_ok && col < args.N) glu_fwd_store16(args, row, col, ru, rg);
+        }
+      } else if (args.glu == 2) {
+        glu_bwd_epilogue<BNP>(args, tacc, row, row_ok, tn, half * (BNP / 2),
+                              (half + 1) * (BNP / 2));
+      } else {
+#pragma unroll 1
+        for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 16) {
+          uint32_t r[16];
+          ptx::tmem_ld16(tacc + c, r);
+          ptx::tmem_wait_ld();
+          const int col = tn * BNP + c;
+          if (row_ok && col < args.N) store16(args, rbase, col, r);
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -601,6 +743,67 @@ bool use_pairs(int M, int N, int K, bool allow_split) {
 
 void set_policy(int p) { g_policy = p; }
 
+namespace {
+int g_fuse = 1;
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+}  // namespace
+void set_fusion(int on) { g_fuse = on; }
+
+// s = silu(X W1^T) * (X W3^T) with W13 = [w1; w3] (2F x in) in one CTA-pair GEMM; [u | g] is
+// also written to ug when non-null (the backward needs it).  Returns false when the shape or
+// policy does not allow the fusion (the caller runs linear_fwd + swiglu_fwd).
+bool linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void* w13, int64_t F,
+                       void* s, void* ug, cudaStream_t stream) {
+  if (!g_fuse || g_policy == 1 || F % 128 != 0 || in_dim % 8 != 0 || n_tok < 1 ||
+      !aligned16(s) || (ug && !aligned16(ug)))
+    return false;
+  Args a{};
+  a.M = static_cast<int>(n_tok);
+  a.N = static_cast<int>(F);
+  a.K = static_cast<int>(in_dim);
+  a.C = s;
+  a.ldc = F;
+  a.epi = kEpiBf16;
+  a.glu = 1;
+  a.glu_F = static_cast<int>(F);
+  a.glu_ug = ug;
+  const CUtensorMap ta = cached_map(x, in_dim, n_tok, in_dim, 64, BM);
+  const CUtensorMap tb = cached_map(w13, in_dim, 2 * F, in_dim, 64, 128);
+  fill_units(a, 256, 128, num_sms() / 2, 0.45, false);  // a tile = 128 features (256 B rows)
+  launch_2sm<false, false, 256>(ta, tb, a, stream);
+  return true;
+}
+
+// [du | dg] = swiglu_bwd(dY W2, u, g): the w2 dgrad with the SwiGLU backward in its epilogue
+// (dY: n_tok x out_dim, W2: out_dim x F, ug / dug: n_tok x 2F).  False when not applicable.
+bool linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2, int64_t F,
+                         const void* ug, void* dug, cudaStream_t stream) {
+  if (!g_fuse || F % 32 != 0 || !aligned16(ug) || !aligned16(dug)) return false;
+  Args a{};
+  a.M = static_cast<int>(n_tok);
+  a.N = static_cast<int>(F);
+  a.K = static_cast<int>(out_dim);
+  a.C = dug;
+  a.ldc = 2 * F;
+  a.epi = kEpiBf16;
+  a.glu = 2;
+  a.glu_F = static_cast<int>(F);
+  a.glu_ug = const_cast<void*>(ug);
+  const CUtensorMap ta = cached_map(dy, out_dim, n_tok, out_dim, 64, BM);
+  const CUtensorMap tb = cached_map(w2, F, out_dim, F, 64, 64);
+  if (use_pairs(a.M, a.N, a.K, false)) {
+    fill_units(a, 256, 256, num_sms() / 2, 0.45, false);
+    launch_2sm<false, true, 256>(ta, tb, a, stream);
+  } else if (F >= 256) {
+    fill_units(a, BM, 256, num_sms(), 0.45, false);
+    launch<false, true, 256>(ta, tb, a, stream);
+  } else {
+    fill_units(a, BM, 128, num_sms(), 0.225, false);
+    launch<false, true, 128>(ta, tb, a, stream);
+  }
+  return true;
+}
+
 // Y = X W^T, bf16 out (epi kEpiBf16) -- forward.
 void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
                 void* y, cudaStream_t stream, const void* residual) {
@@ -714,5 +917,10 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
 
 extern "C" int cft_set_gemm_policy(int policy) {
   cft::tc::set_policy(policy);
+  return CFT_OK;
+}
+
+extern "C" int cft_set_fusion(int enable) {
+  cft::tc::set_fusion(enable);
   return CFT_OK;
 }

@@ -17,6 +17,12 @@ void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w,
 void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const void* x,
                         int64_t in_dim, int64_t rb, int64_t re, float* dw, int accumulate,
                         cudaStream_t stream);
+// SwiGLU-fused Llama MLP GEMMs (false: shape/policy not eligible, run the unfused pair)
+bool linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void* w13, int64_t F,
+                       void* s, void* ug, cudaStream_t stream);
+bool linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2, int64_t F,
+                         const void* ug, void* dug, cudaStream_t stream);
+void set_fusion(int on);
 }  // namespace tc
 
 namespace simt {  // gemm_simt.cu: fp32 / bf16 CUDA-core GEMMs and column sums

@@ -275,13 +275,19 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     llama::rms_fwd(static_cast<bf16*>(z.h), P(id(l, 5)), N, S.d, (float)S.eps,
                    static_cast<bf16*>(z.m), z.rstd2, st);
     pe();
+    // w1|w3 stacked with SwiGLU in the epilogue; [u | g] is kept only where the backward
+    // suffix will read it
     pb(kFwdGemm);
     add_work(kFwdGemm, 2.0 * N * d * 2 * F);
-    tc::linear_fwd(z.m, N, d, P(id(l, 6)), 2 * F, z.ug, st);  // w1|w3 stacked
+    const bool fused = tc::linear_fwd_swiglu(z.m, N, d, P(id(l, 6)), F, z.s,
+                                             stop <= id(l, 7) ? z.ug : nullptr, st);
+    if (!fused) tc::linear_fwd(z.m, N, d, P(id(l, 6)), 2 * F, z.ug, st);
     pe();
-    pb(kFwdOther);
-    llama::swiglu_fwd(static_cast<bf16*>(z.ug), N, S.ffn, static_cast<bf16*>(z.s), st);
-    pe();
+    if (!fused) {
+      pb(kFwdOther);
+      llama::swiglu_fwd(static_cast<bf16*>(z.ug), N, S.ffn, static_cast<bf16*>(z.s), st);
+      pe();
+    }
     pb(kFwdGemm);
     add_work(kFwdGemm, 2.0 * N * F * d);
     tc::linear_fwd(z.s, N, F, P(id(l, 8)), d, lb_[l + 1].x, st, z.h);  // x' = h + s W2^T
@@ -330,14 +336,17 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     // x_{l+1} = h + s W2^T      (GX = dL/dx_{l+1})
     wgrad(id(l, 8), l_gx_, d, z.s, F, 0);
     if (!need(id(l, 7))) break;
-    pb(kDgrad);
+    pb(kDgrad);  // dS = GX W2 with the SwiGLU backward in the epilogue -> [du | dg]
     add_work(kDgrad, 2.0 * N * d * F);
-    tc::linear_dgrad(l_gx_, N, d, P(id(l, 8)), F, l_ds_, 0, st);
+    const bool fused = tc::linear_dgrad_swiglu(l_gx_, N, d, P(id(l, 8)), F, z.ug, l_dug_, st);
+    if (!fused) tc::linear_dgrad(l_gx_, N, d, P(id(l, 8)), F, l_ds_, 0, st);
     pe();
-    pb(kBwdOther);
-    llama::swiglu_bwd(static_cast<bf16*>(l_ds_), static_cast<bf16*>(z.ug), N, S.ffn,
-                      static_cast<bf16*>(l_dug_), st);
-    pe();
+    if (!fused) {
+      pb(kBwdOther);
+      llama::swiglu_bwd(static_cast<bf16*>(l_ds_), static_cast<bf16*>(z.ug), N, S.ffn,
+                        static_cast<bf16*>(l_dug_), st);
+      pe();
+    }
     wgrad(id(l, 6), l_dug_, 2 * F, z.m, d, 0);  // w1 rows [0,F) of the stack
     wgrad(id(l, 7), l_dug_, 2 * F, z.m, d, F);  // w3 rows [F,2F)
     if (!need(id(l, 5))) break;

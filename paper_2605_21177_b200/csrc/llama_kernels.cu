@@ -163,7 +163,7 @@ __global__ void rope_kernel(bf16* qkv, long long tokens, int seq, int heads, int
   }
 }
 
-__device__ __forceinline__ float sigm(float u) { return 1.f / (1.f + __expf(-u)); }
+__device__ __forceinline__ float sigm(float u) { return __fdividef(1.f, 1.f + __expf(-u)); }
 
 // s = silu(u) * g over rows laid out [u (F) | g (F)]
 __global__ void swiglu_fwd_kernel(const bf16* __restrict__ ug, long long rows, int F,

@@ -19,6 +19,10 @@ void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w,
 void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const void* x,
                         int64_t in_dim, int64_t rb, int64_t re, float* dw, int accumulate,
                         cudaStream_t stream);
+bool linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void* w13, int64_t F,
+                       void* s, void* ug, cudaStream_t stream);
+bool linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2, int64_t F,
+                         const void* ug, void* dug, cudaStream_t stream);
 }  // namespace tc
 namespace simt {
 void linear_fwd_f32(const float*, int64_t, int64_t, const float*, int64_t, const float*, float*,
@@ -149,6 +153,27 @@ int cft_linear_dgrad(cft_dtype dtype, const void* dy, int64_t n_tok, int64_t out
       f64::linear_dinput(static_cast<const double*>(dy), (int)n_tok, (int)out_dim,
                          static_cast<const double*>(w), (int)in_dim, static_cast<double*>(dx), s);
     }
+  });
+}
+
+int cft_linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void* w13,
+                          int64_t F, void* s, void* ug, cft_stream_t stream) {
+  return guarded([&] {
+    CFT_CHECK(n_tok > 0 && in_dim > 0 && F > 0, "linear_fwd_swiglu: empty shape");
+    CFT_CHECK(tma_ok(x, in_dim) && tma_ok(w13, in_dim), "linear_fwd_swiglu: operand alignment");
+    if (!tc::linear_fwd_swiglu(x, n_tok, in_dim, w13, F, s, ug, static_cast<cudaStream_t>(stream)))
+      throw Error("linear_fwd_swiglu: shape not eligible (F % 128, 16-byte alignment, fusion on)");
+  });
+}
+
+int cft_linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2,
+                            int64_t F, const void* ug, void* dug, cft_stream_t stream) {
+  return guarded([&] {
+    CFT_CHECK(n_tok > 0 && out_dim > 0 && F > 0, "linear_dgrad_swiglu: empty shape");
+    CFT_CHECK(tma_ok(dy, out_dim) && tma_ok(w2, F), "linear_dgrad_swiglu: operand alignment");
+    if (!tc::linear_dgrad_swiglu(dy, n_tok, out_dim, w2, F, ug, dug,
+                                 static_cast<cudaStream_t>(stream)))
+      throw Error("linear_dgrad_swiglu: shape not eligible (F % 32, 16-byte alignment, fusion on)");
   });
 }
 

@@ -159,6 +159,35 @@ def adamw_slice(master, m, v, grad, hyper, n_local: int, param=None, segments=No
                                   int(zero_grad), _stream(stream)), "adamw_slice")
 
 
+def linear_fwd_swiglu(x: torch.Tensor, w13: torch.Tensor, keep_ug: bool = True, stream=None):
+    """s = silu(x w1^T) * (x w3^T) with w13 = [w1; w3]; returns (s, ug or None)."""
+    _contig(x, w13)
+    n_tok, in_dim = x.shape
+    F = w13.shape[0] // 2
+    s = torch.empty(n_tok, F, dtype=x.dtype, device=x.device)
+    ug = torch.empty(n_tok, 2 * F, dtype=x.dtype, device=x.device) if keep_ug else None
+    N.check(N.lib.cft_linear_fwd_swiglu(x.data_ptr(), n_tok, in_dim, w13.data_ptr(), F,
+                                        s.data_ptr(), _ptr(ug), _stream(stream)), "linear_fwd_swiglu")
+    return s, ug
+
+
+def linear_dgrad_swiglu(dy: torch.Tensor, w2: torch.Tensor, ug: torch.Tensor, stream=None):
+    """[du | dg] = SwiGLU backward of (dy . w2) at the saved ug = [u | g]."""
+    _contig(dy, w2, ug)
+    n_tok, out_dim = dy.shape
+    F = w2.shape[1]
+    dug = torch.empty(n_tok, 2 * F, dtype=dy.dtype, device=dy.device)
+    N.check(N.lib.cft_linear_dgrad_swiglu(dy.data_ptr(), n_tok, out_dim, w2.data_ptr(), F,
+                                          ug.data_ptr(), dug.data_ptr(), _stream(stream)),
+            "linear_dgrad_swiglu")
+    return dug
+
+
+def set_fusion(enable: bool) -> None:
+    """SwiGLU epilogue fusions in the Llama engine's MLP GEMMs (bit-identical on/off)."""
+    N.check(N.lib.cft_set_fusion(int(enable)))
+
+
 def set_gemm_policy(policy: int) -> None:
     """0 auto, 1 single-CTA 128xBN tcgen05 tiles, 2 CTA-pair 256x256 tiles."""
     N.check(N.lib.cft_set_gemm_policy(policy))

@@ -173,3 +173,42 @@ def test_llama_graph_replay_matches_eager(cuda):
     assert np.all(np.isfinite(l1))
     np.testing.assert_allclose(l1, l0, rtol=2e-3)
     assert np.linalg.norm(p1 - p0) / np.linalg.norm(p0) < 1e-3
+
+
+@pytest.mark.parametrize("policy", [0, 2], ids=["auto", "pairs"])
+def test_llama_swiglu_fusion_bit_identical(cuda, policy):
+    """SwiGLU fused into the w1|w3 forward epilogue and the w2 dgrad epilogue rounds exactly
+    like the separate kernels: every chunk's gradient and loss agree to the run-to-run
+    reproducibility of the atomics elsewhere in the step (split-K red.add, CE loss sum)."""
+    from paper_2605_21177_b200 import ops
+    from paper_2605_21177_b200.engine import ChunkEngine, LlamaModel, TrainOptions
+    from paper_2605_21177_b200.plan import ScheduleConfig
+    model = LlamaModel(layers=2)
+    B, K = 4, 6
+    flat = init_params(model, seed=9)
+    rng = np.random.default_rng(2)
+    seqs = rng.integers(0, model.vocab, (B, model.seq + 1)).astype(np.int32)
+    grads = {}
+    ops.set_gemm_policy(policy)
+    try:
+        for fuse in (False, True):
+            ops.set_fusion(fuse)
+            opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=K), dtype="bf16",
+                                cuda_graphs=False)
+            eng = ChunkEngine(model, flat, B, opts)
+            batch = eng.stage({"tokens": seqs[:, :-1].copy(), "labels": seqs[:, 1:].copy()},
+                              device=True)
+            out = []
+            for _ in range(K):
+                eng.step_begin()
+                eng.forward_backward(batch, 0)
+                out.append(eng.grad_tensor().cpu().numpy().copy())
+                eng.step_end()
+            eng.finish()
+            grads[fuse] = (out, eng.trajectory()["loss"])
+    finally:
+        ops.set_fusion(True)
+        ops.set_gemm_policy(0)
+    for a, b in zip(grads[False][0], grads[True][0]):
+        assert np.linalg.norm(b - a) <= 1e-5 * np.linalg.norm(a)
+    np.testing.assert_allclose(grads[True][1], grads[False][1], rtol=1e-6)
