@@ -16,6 +16,8 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+from llama_ref import torch_reference  # noqa: E402
+
 
 def init_params(model, seed=7):
     rng = np.random.default_rng(seed)
@@ -26,55 +28,6 @@ def init_params(model, seed=7):
         else:
             out.append(rng.uniform(-0.5, 0.5, r * c) / math.sqrt(c))
     return np.concatenate(out)
-
-
-def torch_reference(model, flat, tokens, labels):
-    """fp32 forward + autograd over bf16-rounded parameters; returns loss, grads (flat)."""
-    dev = "cuda"
-    p = torch.tensor(flat, dtype=torch.float64).to(torch.bfloat16).to(torch.float32).to(dev)
-    p.requires_grad_(True)
-    views, off = {}, 0
-    for name, r, c in model.tensors():
-        views[name] = p[off: off + r * c].view(r, c) if c > 1 else p[off: off + r]
-        off += r * c
-    B, S = tokens.shape
-    hd, H, KVH = model.head_dim, model.heads, model.kv_heads
-    tok = torch.tensor(tokens, device=dev, dtype=torch.long)
-    lab = torch.tensor(labels, device=dev, dtype=torch.long).reshape(-1)
-
-    def rms(x, g):
-        return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + model.eps) * g
-
-    pos = torch.arange(S, device=dev, dtype=torch.float32)
-    inv = model.rope_theta ** (-2.0 * torch.arange(hd // 2, device=dev, dtype=torch.float32) / hd)
-    ang = pos[:, None] * inv[None, :]
-    cos, sin = torch.cos(ang), torch.sin(ang)
-
-    def rope(x):  # [B, S, h, hd], rotate-half pairs (i, i + hd/2)
-        x1, x2 = x[..., : hd // 2], x[..., hd // 2:]
-        c, s = cos[None, :, None, :], sin[None, :, None, :]
-        return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
-
-    x = views["embed"][tok]  # [B, S, d]
-    mask = torch.full((S, S), float("-inf"), device=dev).triu(1)
-    for l in range(model.layers):
-        P = lambda n: views[f"L{l}.{n}"]
-        a = rms(x, P("attn_norm"))
-        q = rope((a @ P("wq").t()).view(B, S, H, hd))
-        k = rope((a @ P("wk").t()).view(B, S, KVH, hd))
-        v = (a @ P("wv").t()).view(B, S, KVH, hd)
-        k = k.repeat_interleave(H // KVH, dim=2)
-        v = v.repeat_interleave(H // KVH, dim=2)
-        att = torch.einsum("bqhd,bkhd->bhqk", q, k) / math.sqrt(hd) + mask
-        o = torch.einsum("bhqk,bkhd->bqhd", att.softmax(-1), v).reshape(B, S, H * hd)
-        h = x + o @ P("wo").t()
-        m = rms(h, P("mlp_norm"))
-        s = torch.nn.functional.silu(m @ P("w1").t()) * (m @ P("w3").t())
-        x = h + s @ P("w2").t()
-    logits = rms(x, views["norm"]) @ views["lm_head"].t()
-    loss = torch.nn.functional.cross_entropy(logits.reshape(-1, model.vocab), lab)
-    loss.backward()
-    return loss.item(), p.grad.double().cpu().numpy()
 
 
 @pytest.mark.parametrize("graphs", [True, False], ids=["graph", "eager"])
