@@ -314,6 +314,8 @@ typedef struct {
   double grad_scale;     /* extra factor on the mean gradient (1/world for data parallel) */
   int32_t cuda_graphs;   /* 1: replay each chunk's forward+backward as one captured CUDA graph
                             (Llama engine; captured on the chunk's first step) */
+  int32_t shard_rank;    /* sharded optimizer state: this rank's index and the */
+  int32_t shard_world;   /* number of ranks; 0 or 1 = every rank keeps the whole chunk state */
   int32_t pad_;
 } cft_engine_config;
 
@@ -361,6 +363,24 @@ int cft_engine_finish(cft_engine* e);
  * (cuda_graphs = 1, Llama engine; a no-op otherwise).  Call between steps. */
 int cft_engine_prepare_graphs(cft_engine* e);
 int cft_engine_set_grad_scale(cft_engine* e, double grad_scale);
+/* Sharded optimizer state (shard_world > 1).  Each chunk's state is split into shard_world
+ * equal padded shards; rank r keeps master/m/v of shard r only (host RAM and PCIe traffic per
+ * rank / shard_world).  Step protocol between forward_backward and the next step_begin:
+ *   1. reduce-scatter (SUM) cft_engine_grad_buffer (n = world x padded, zero padding)
+ *      into cft_engine_shard_buffer (padded elements; the first n_valid are real);
+ *   2. cft_engine_shard_stats -> device pointer to {sumsq, nonfinite, loss} (3 doubles):
+ *      all-reduce (SUM) them;
+ *   3. cft_engine_step_end: AdamW on the shard, updated parameters written (compute dtype)
+ *      into this rank's part of the gather buffer;
+ *   4. all-gather cft_engine_gather_buffer (n_total elements; this rank's part starts at
+ *      my_offset) in place, then cft_engine_gather_end to unpack it into the parameters.
+ * The per-element math is the unsharded step's; only the summation order of the gradient
+ * reduction may differ. */
+int cft_engine_shard_buffer(cft_engine* e, void** ptr, int64_t* n_padded, int64_t* n_valid);
+int cft_engine_shard_stats(cft_engine* e, double** red3_dev);
+int cft_engine_gather_buffer(cft_engine* e, void** ptr, int64_t* n_total, int64_t* my_offset,
+                             int32_t* dtype);
+int cft_engine_gather_end(cft_engine* e);
 /* TrainTrajectoryEntry (trainer.hpp:26-33): step, chunk, loss (pre-update mean), grad_norm_sq. */
 int64_t cft_engine_trajectory(cft_engine* e, int64_t* step, int32_t* chunk, double* loss,
                               double* gsq, int64_t cap);

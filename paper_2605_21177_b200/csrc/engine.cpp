@@ -157,12 +157,43 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
     }
     max_chunk_ = std::max(max_chunk_, off);
   }
+  CFT_CHECK(cfg_.shard_world >= 1 && cfg_.shard_rank >= 0 && cfg_.shard_rank < cfg_.shard_world,
+            "engine: shard rank out of range");
+  sh_size_.assign(cfg_.K, 0);
+  st_lo_.assign(cfg_.K, 0);
+  st_n_.assign(cfg_.K, 0);
+  for (int c = 0; c < cfg_.K; ++c) {
+    const int64_t n = plan_.chunks[c].elements, W = cfg_.shard_world;
+    if (W == 1) {
+      sh_size_[c] = n;
+      st_n_[c] = n;
+    } else {
+      sh_size_[c] = ((n + W - 1) / W + 63) / 64 * 64;  // equal padded shards, 256-byte aligned
+      st_lo_[c] = std::min(n, cfg_.shard_rank * sh_size_[c]);
+      st_n_[c] = std::min(n - st_lo_[c], sh_size_[c]);
+    }
+    max_state_ = std::max(max_state_, st_n_[c]);
+    max_padded_ = std::max(max_padded_, W * sh_size_[c]);
+  }
 
   // ---- device memory (all allocated once; nothing is allocated per step) ----
   const size_t E = esz(), S = ssz();
   alloc(&params_, param_elems_ * E);
-  alloc(&aux_, max_chunk_ * S);
-  CFT_CUDA(cudaMemset(aux_, 0, max_chunk_ * S));
+  alloc(&aux_, max_padded_ * S);
+  CFT_CUDA(cudaMemset(aux_, 0, max_padded_ * S));
+  if (sharded()) {
+    alloc(&gshard_, std::max<int64_t>(max_padded_ / cfg_.shard_world, 1) * S);
+    alloc(&gather_, max_padded_ * E);
+    void* p;
+    alloc(&p, 4 * sizeof(double));
+    red_ = static_cast<double*>(p);
+    for (int c = 0; c < cfg_.K; ++c) {
+      const cft_segment seg{0, cfg_.shard_rank * sh_size_[c], st_n_[c]};
+      alloc(&p, sizeof(cft_segment));
+      CFT_CUDA(cudaMemcpy(p, &seg, sizeof(seg), cudaMemcpyHostToDevice));
+      shard_segs_.push_back(static_cast<cft_segment*>(p));
+    }
+  }
   if (kind_ == kLlamaModel) {
     llama_alloc();
   } else {
@@ -238,7 +269,7 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
 
   const int n_slots = cfg_.offload ? 3 : 0;
   for (int i = 0; i < n_slots; ++i) {
-    for (auto& st : slots_[i].st) alloc(&st, max_chunk_ * S);
+    for (auto& st : slots_[i].st) alloc(&st, max_state_ * S);
     CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].ready, cudaEventDisableTiming));
     CFT_CUDA(cudaEventCreateWithFlags(&slots_[i].free, cudaEventDisableTiming));
   }
@@ -256,20 +287,21 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
     float* tmp;
     CFT_CUDA(cudaMalloc(reinterpret_cast<void**>(&tmp), max_chunk_ * 3 * sizeof(float)));
     for (int c = 0; c < cfg_.K; ++c) {
-      const int64_t n = plan_.chunks[c].elements;
+      const int64_t n = plan_.chunks[c].elements, lo = st_lo_[c], sn = st_n_[c];
       CFT_CUDA(cudaMemsetAsync(tmp, 0, n * 3 * sizeof(float), stream_));
       for (const auto& s : chunk_slices_[c]) {
         const Tensor& t = tensors_[s.tensor];
         llama::init_slice(tmp + s.aux_off, static_cast<__nv_bfloat16*>(params_) + s.param_off,
                           s.count, seed, s.tensor, s.rb * t.cols, t.cols, t.cols == 1, stream_);
       }
+      // this rank's states: master[lo, lo + sn) and zero m, v (tmp[n, 3n) is zero)
       void* buf;
-      if (cfg_.offload) CFT_CUDA(cudaHostAlloc(&buf, n * 3 * S, cudaHostAllocDefault));
-      else alloc(&buf, n * 3 * S);
+      if (cfg_.offload) CFT_CUDA(cudaHostAlloc(&buf, std::max<int64_t>(sn, 1) * 3 * S, cudaHostAllocDefault));
+      else alloc(&buf, std::max<int64_t>(sn, 1) * 3 * S);
       host_states_[c] = buf;
-      CFT_CUDA(cudaMemcpyAsync(buf, tmp, n * 3 * S,
-                               cfg_.offload ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
-                               stream_));
+      const cudaMemcpyKind kind = cfg_.offload ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+      CFT_CUDA(cudaMemcpyAsync(buf, tmp + lo, sn * S, kind, stream_));
+      CFT_CUDA(cudaMemcpyAsync(static_cast<char*>(buf) + sn * S, tmp + n, 2 * sn * S, kind, stream_));
       CFT_CUDA(cudaStreamSynchronize(stream_));
     }
     cudaFree(tmp);
@@ -297,25 +329,26 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
 
   // ---- optimizer state: masters from the init params, m = v = 0 (optimizer.cpp:77-92) ----
   for (int c = 0; c < cfg_.K; ++c) {
-    const int64_t n = plan_.chunks[c].elements;
+    const int64_t n = plan_.chunks[c].elements, lo = st_lo_[c], sn = st_n_[c];
     std::vector<double> master(n);
     for (const auto& s : chunk_slices_[c])
       std::memcpy(master.data() + s.aux_off, init_params + s.param_off, s.count * 8);
     void* buf;
+    const size_t bytes = std::max<int64_t>(sn, 1) * 3 * S;
     if (cfg_.offload) {
-      CFT_CUDA(cudaHostAlloc(&buf, n * 3 * S, cudaHostAllocDefault));
+      CFT_CUDA(cudaHostAlloc(&buf, bytes, cudaHostAllocDefault));
     } else {
-      alloc(&buf, n * 3 * S);
+      alloc(&buf, bytes);
     }
     host_states_[c] = buf;
-    std::vector<char> staged(n * 3 * S, 0);
+    std::vector<char> staged(bytes, 0);  // [master | m = 0 | v = 0] of this rank's elements
     if (S == 8) {
-      std::memcpy(staged.data(), master.data(), n * 8);
+      std::memcpy(staged.data(), master.data() + lo, sn * 8);
     } else {
       float* f = reinterpret_cast<float*>(staged.data());
-      for (int64_t i = 0; i < n; ++i) f[i] = static_cast<float>(master[i]);
+      for (int64_t i = 0; i < sn; ++i) f[i] = static_cast<float>(master[lo + i]);
     }
-    CFT_CUDA(cudaMemcpy(buf, staged.data(), n * 3 * S,
+    CFT_CUDA(cudaMemcpy(buf, staged.data(), bytes,
                         cfg_.offload ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice));
   }
   CFT_CUDA(cudaDeviceSynchronize());
@@ -461,7 +494,7 @@ void Engine::load_chunk(int chunk, bool for_prefetch) {
       if (slots_[i].chunk >= 0 && slots_[i].chunk != active_) pending = slots_[i].chunk;
     s = take_free_slot(active_, pending);
     Slot& sl = slots_[s];
-    const int64_t n = plan_.chunks[chunk].elements;
+    const int64_t n = st_n_[chunk];
     const size_t S = ssz();
     // wait for the slot's previous D2H (it may still be draining) and for this chunk's own
     // last D2H (its host copy must be complete before it is read back)
@@ -487,7 +520,7 @@ void Engine::offload_chunk(int chunk) {
   const int s = slot_of(chunk);
   CFT_CHECK(s >= 0, "offload: chunk not resident");
   Slot& sl = slots_[s];
-  const int64_t n = plan_.chunks[chunk].elements;
+  const int64_t n = st_n_[chunk];
   const size_t S = ssz();
   CFT_CUDA(cudaStreamWaitEvent(d2h_, step_done_, 0));
   char* dst = static_cast<char*>(host_states_[chunk]);
@@ -788,12 +821,25 @@ void Engine::step_end() {
   const double scale = cfg_.grad_scale * (1.0 / cfg_.micro_batches);  // take_mean_grad
   double* st = stats_ + t_ * 4;
   CFT_CUDA(cudaEventRecord(ev_[4], s));
-  pb(kStats);
-  add_work(kStats, 4.0 * n);
-  if (cft_grad_stats(sdt, aux_, n, scale, st, s) != CFT_OK) throw Error(last_error());
-  // a non-finite loss also blocks the update (trainer.cpp:48-49 throws before any step)
-  layers::flag_nonfinite_loss(st, s);
-  pe();
+  // the gradient the update reads: the whole chunk, or (sharded) this rank's reduce-scattered
+  // part, whose statistics shard_stats() formed and the caller all-reduced
+  void* grad = aux_;
+  int64_t gn = n;
+  if (sharded()) {
+    CFT_CHECK(stats_done_, "engine: sharded step_end needs shard_stats() and its all-reduce first");
+    stats_done_ = false;
+    layers::unpack_shard_stats(red_, st, 1.0 / cfg_.shard_world, s);
+    grad = gshard_;
+    gn = st_n_[c];
+    if (sdt == CFT_F32) CFT_CUDA(cudaMemsetAsync(aux_, 0, n * 4, s));  // zero-accumulator invariant
+  } else {
+    pb(kStats);
+    add_work(kStats, 4.0 * n);
+    if (cft_grad_stats(sdt, aux_, n, scale, st, s) != CFT_OK) throw Error(last_error());
+    // a non-finite loss also blocks the update (trainer.cpp:48-49 throws before any step)
+    layers::flag_nonfinite_loss(st, s);
+    pe();
+  }
 
   void* master;
   void* m;
@@ -806,25 +852,31 @@ void Engine::step_end() {
   } else {
     char* base = static_cast<char*>(host_states_[c]);
     master = base;
-    m = base + n * ssz();
-    v = base + 2 * n * ssz();
+    m = base + gn * ssz();
+    v = base + 2 * gn * ssz();
   }
   n_local_[c] += 1;
-  const int32_t nseg = static_cast<int32_t>(chunk_slices_[c].size());
+  // write-back target: the parameter arena through the chunk's segment table, or (sharded)
+  // this rank's slot of the packed gather buffer
+  void* pbase = sharded() ? gather_ : params_;
+  const cft_segment* segs = sharded() ? shard_segs_[c] : chunk_segs_[c];
+  const int32_t nseg = sharded() ? 1 : static_cast<int32_t>(chunk_slices_[c].size());
   pb(kUpdate);
-  add_work(kUpdate, (cfg_.optim == 0 ? 30.0 : 14.0) * n);
-  if (cfg_.optim == 0) {
-    const double bc1 = 1.0 - std::pow(cfg_.hyper.beta1, static_cast<double>(n_local_[c]));
-    const double bc2 = 1.0 - std::pow(cfg_.hyper.beta2, static_cast<double>(n_local_[c]));
-    if (cft_adamw_slice(sdt, master, m, v, aux_, n, scale, &cfg_.hyper, bc1, bc2,
-                        static_cast<cft_dtype>(cfg_.dtype), params_, chunk_segs_[c], nseg, st,
-                        precond_, sdt == CFT_F32 ? 1 : 0, s) != CFT_OK)
-      throw Error(last_error());
-  } else {
-    if (cft_sgd_slice(sdt, master, aux_, n, scale, cfg_.hyper.eta, static_cast<cft_dtype>(cfg_.dtype),
-                      params_, chunk_segs_[c], nseg, st, s) != CFT_OK)
-      throw Error(last_error());
-    if (sdt == CFT_F32) CFT_CUDA(cudaMemsetAsync(aux_, 0, n * 4, s));
+  add_work(kUpdate, (cfg_.optim == 0 ? 30.0 : 14.0) * gn);
+  if (gn > 0) {
+    if (cfg_.optim == 0) {
+      const double bc1 = 1.0 - std::pow(cfg_.hyper.beta1, static_cast<double>(n_local_[c]));
+      const double bc2 = 1.0 - std::pow(cfg_.hyper.beta2, static_cast<double>(n_local_[c]));
+      if (cft_adamw_slice(sdt, master, m, v, grad, gn, scale, &cfg_.hyper, bc1, bc2,
+                          static_cast<cft_dtype>(cfg_.dtype), pbase, segs, nseg, st, precond_,
+                          sdt == CFT_F32 ? 1 : 0, s) != CFT_OK)
+        throw Error(last_error());
+    } else {
+      if (cft_sgd_slice(sdt, master, grad, gn, scale, cfg_.hyper.eta,
+                        static_cast<cft_dtype>(cfg_.dtype), pbase, segs, nseg, st, s) != CFT_OK)
+        throw Error(last_error());
+      if (sdt == CFT_F32) CFT_CUDA(cudaMemsetAsync(grad, 0, gn * 4, s));
+    }
   }
   pe();
   CFT_CUDA(cudaEventRecord(ev_[5], s));
@@ -843,7 +895,8 @@ void Engine::step_end() {
     const double* h = host_stats_ + t_ * 4;
     const std::string ctx = "step " + std::to_string(t_) + ", chunk " + std::to_string(c) + ": ";
     auto restore = [&] {  // keep the zero-accumulator invariant after a rejected step
-      if (sdt == CFT_F32) CFT_CUDA(cudaMemset(aux_, 0, max_chunk_ * 4));
+      if (sdt == CFT_F32) CFT_CUDA(cudaMemset(aux_, 0, max_padded_ * 4));
+      if (sdt == CFT_F32 && gshard_) CFT_CUDA(cudaMemset(gshard_, 0, max_padded_ / cfg_.shard_world * 4));
     };
     if (host_flags_[1]) throw Error(ctx + "embedding: token id out of range");
     if (host_flags_[0]) throw Error(ctx + "loss: label out of range");
@@ -896,6 +949,7 @@ void Engine::stats_for_step(int64_t t, double* loss, double* gsq) {
 }
 
 void Engine::params_from_masters(double* out) {
+  CFT_CHECK(!sharded(), "engine: states are sharded across ranks (read params_device)");
   CFT_CUDA(cudaDeviceSynchronize());
   const size_t S = ssz();
   for (int c = 0; c < cfg_.K; ++c) {
@@ -929,8 +983,59 @@ void Engine::params_device(double* out) {
 
 void Engine::grad_buffer(void** ptr, int64_t* n, int* dtype) {
   *ptr = aux_;
-  *n = active_ >= 0 ? plan_.chunks[active_].elements : 0;
+  // sharded: world equal padded shards (the padding stays zero), the reduce-scatter input
+  *n = active_ < 0 ? 0 : sharded() ? cfg_.shard_world * sh_size_[active_]
+                                   : plan_.chunks[active_].elements;
   *dtype = cfg_.dtype == CFT_F64 ? CFT_F64 : CFT_F32;
+}
+
+void Engine::shard_buffer(void** ptr, int64_t* n_padded, int64_t* n_valid) {
+  CFT_CHECK(sharded(), "engine: states are not sharded");
+  CFT_CHECK(active_ >= 0, "scheduler: step_end before step_begin");
+  *ptr = gshard_;
+  *n_padded = sh_size_[active_];
+  *n_valid = st_n_[active_];
+}
+
+double* Engine::shard_stats() {
+  CFT_CHECK(sharded(), "engine: states are not sharded");
+  CFT_CHECK(active_ >= 0, "scheduler: step_end before step_begin");
+  CFT_CHECK(mb_done_ == cfg_.micro_batches, "engine: not every micro-batch was run");
+  cudaStream_t s = stream_;
+  const int64_t sn = st_n_[active_];
+  const cft_dtype sdt = cfg_.dtype == CFT_F64 ? CFT_F64 : CFT_F32;
+  const double scale = cfg_.grad_scale * (1.0 / cfg_.micro_batches);
+  double* st = stats_ + t_ * 4;
+  pb(kStats);
+  add_work(kStats, 4.0 * sn);
+  if (sn > 0 && cft_grad_stats(sdt, gshard_, sn, scale, st, s) != CFT_OK) throw Error(last_error());
+  layers::flag_nonfinite_loss(st, s);
+  layers::pack_shard_stats(st, red_, s);
+  pe();
+  stats_done_ = true;
+  return red_;
+}
+
+void Engine::gather_buffer(void** ptr, int64_t* n_total, int64_t* my_offset, int* dtype) {
+  CFT_CHECK(sharded(), "engine: states are not sharded");
+  const int c = traj_chunk_.empty() ? -1 : traj_chunk_.back();
+  CFT_CHECK(c >= 0, "engine: no step finished yet");
+  *ptr = gather_;
+  *n_total = cfg_.shard_world * sh_size_[c];
+  *my_offset = cfg_.shard_rank * sh_size_[c];
+  *dtype = cfg_.dtype;
+}
+
+void Engine::gather_end() {
+  CFT_CHECK(sharded(), "engine: states are not sharded");
+  const int c = traj_chunk_.empty() ? -1 : traj_chunk_.back();
+  CFT_CHECK(c >= 0, "engine: no step finished yet");
+  // unpack the gathered chunk into the arena (skipped on device when the step was rejected)
+  const double* st = stats_ + traj_step_.back() * 4;
+  for (const auto& sl : chunk_slices_[c])
+    layers::copy_unless_flagged(static_cast<char*>(params_) + sl.param_off * esz(),
+                                static_cast<const char*>(gather_) + sl.aux_off * esz(), sl.count,
+                                static_cast<int>(esz()), st, stream_);
 }
 
 std::string Engine::plan_json() const {
@@ -960,6 +1065,7 @@ std::string chunk_file(const std::string& dir, int c) {
 
 void Engine::write_checkpoints(const std::string& dir) {
   CFT_CHECK(finished_, "checkpoint: flush chunk to host tier first");
+  CFT_CHECK(!sharded(), "checkpoint: states are sharded across ranks");
   const uint64_t hash = host::plan_hash(plan_);
   const size_t S = ssz();
   for (int c = 0; c < cfg_.K; ++c) {
@@ -988,6 +1094,7 @@ void Engine::write_checkpoints(const std::string& dir) {
 
 void Engine::read_checkpoints(const std::string& dir) {
   CFT_CHECK(t_ == 0 && !finished_, "checkpoint: restore before the first step");
+  CFT_CHECK(!sharded(), "checkpoint: states are sharded across ranks");
   const uint64_t want = host::plan_hash(plan_);
   const size_t S = ssz();
   std::vector<double> params(param_elems_);

@@ -59,6 +59,10 @@ struct EngineConfig {
   int check_every_step = 1;
   double grad_scale = 1.0;  // extra factor folded into the mean (e.g. 1/world for DP)
   int cuda_graphs = 0;      // Llama engine: replay forward+backward per chunk as a CUDA graph
+  // Sharded optimizer state: this rank keeps master/m/v only for its 1/world
+  // slice of every chunk; the caller reduce-scatters the gradient, all-reduces the statistics
+  // and all-gathers the updated parameters (see include/chunkft_b200.h).
+  int shard_rank = 0, shard_world = 1;
 };
 
 // Llama-3-shaped decoder: embedding, L x [RMSNorm, GQA attention with
@@ -94,6 +98,14 @@ class Engine {
   void forward_backward(const Batch& b, int mb);     // one micro-batch
   void step_end();                                   // stats, update, offload, bookkeeping
   void finish();                                     // flush all chunks to host, sync
+  // sharded-state protocol (shard_world > 1), between forward_backward and step_end:
+  //   reduce-scatter grad_buffer -> shard_buffer; shard_stats; all-reduce its 3 doubles;
+  //   step_end (AdamW on the shard into the gather buffer); all-gather; gather_end
+  bool sharded() const { return cfg_.shard_world > 1; }
+  void shard_buffer(void** ptr, int64_t* n_padded, int64_t* n_valid);
+  double* shard_stats();
+  void gather_buffer(void** ptr, int64_t* n_total, int64_t* my_offset, int* dtype);
+  void gather_end();
   void prepare_graphs();  // capture every chunk's forward+backward graph now (Llama engine)
 
   // results
@@ -207,6 +219,15 @@ class Engine {
   std::vector<int> lowest_layer_;
   std::vector<uint64_t> n_local_;
   int64_t max_chunk_ = 0, param_elems_ = 0, max_width_ = 0, max_slice_ = 0;
+  // per chunk: padded shard size, this rank's first state element and count (unsharded:
+  // n, 0, n); the state slots / host buffers hold st_n_[c] elements
+  std::vector<int64_t> sh_size_, st_lo_, st_n_;
+  int64_t max_state_ = 0, max_padded_ = 0;
+  void* gshard_ = nullptr;                  // reduce-scatter output (this rank's mean-grad part)
+  void* gather_ = nullptr;                  // packed chunk params in the compute dtype
+  double* red_ = nullptr;                   // {sumsq, nonfinite, loss} for the all-reduce
+  std::vector<cft_segment*> shard_segs_;    // per chunk: {0, rank * padded, st_n}
+  bool stats_done_ = false;
 
   cudaStream_t stream_ = nullptr, h2d_ = nullptr, d2h_ = nullptr;
   bool own_stream_ = false;

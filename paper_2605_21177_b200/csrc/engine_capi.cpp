@@ -30,6 +30,8 @@ static cft::EngineConfig to_config(const cft_engine_config* c) {
   cfg.check_every_step = c->check_every_step;
   cfg.grad_scale = c->grad_scale == 0.0 ? 1.0 : c->grad_scale;
   cfg.cuda_graphs = c->cuda_graphs;
+  cfg.shard_rank = c->shard_rank;
+  cfg.shard_world = c->shard_world > 1 ? c->shard_world : 1;
   return cfg;
 }
 
@@ -159,6 +161,27 @@ int cft_engine_phase_ms(cft_engine* e, float* ms4) {
 
 int cft_engine_profile(cft_engine* e, int enable, int64_t max_marks) {
   return guarded([&] { e->p->profile(enable, max_marks); });
+}
+
+int cft_engine_shard_buffer(cft_engine* e, void** ptr, int64_t* n_padded, int64_t* n_valid) {
+  return guarded([&] { e->p->shard_buffer(ptr, n_padded, n_valid); });
+}
+
+int cft_engine_shard_stats(cft_engine* e, double** red3_dev) {
+  return guarded([&] { *red3_dev = e->p->shard_stats(); });
+}
+
+int cft_engine_gather_buffer(cft_engine* e, void** ptr, int64_t* n_total, int64_t* my_offset,
+                             int32_t* dtype) {
+  return guarded([&] {
+    int dt = 0;
+    e->p->gather_buffer(ptr, n_total, my_offset, &dt);
+    *dtype = dt;
+  });
+}
+
+int cft_engine_gather_end(cft_engine* e) {
+  return guarded([&] { e->p->gather_end(); });
 }
 
 int cft_engine_prepare_graphs(cft_engine* e) {

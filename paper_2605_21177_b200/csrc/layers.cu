@@ -477,6 +477,64 @@ void sm_copy(void* dst, const void* src, long long bytes, cudaStream_t s) {
   }
   check_launch("sm_copy");
 }
+// Sharded-state statistics exchange: {sumsq, nonfinite count, loss} as doubles for a SUM
+// all-reduce, and back into the step's statistics row (loss as the mean over ranks).
+__global__ void pack_shard_stats_kernel(const double* st, double* red) {
+  unsigned long long nbad;
+  memcpy(&nbad, &st[1], 8);
+  red[0] = st[0];
+  red[1] = static_cast<double>(nbad);
+  red[2] = st[3];
+}
+__global__ void unpack_shard_stats_kernel(const double* red, double* st, double inv_world) {
+  const unsigned long long nbad = static_cast<unsigned long long>(red[1]);
+  st[0] = red[0];
+  memcpy(&st[1], &nbad, 8);
+  st[3] = red[2] * inv_world;
+}
+void pack_shard_stats(const double* st, double* red, cudaStream_t s) {
+  pack_shard_stats_kernel<<<1, 1, 0, s>>>(st, red);
+  check_launch("pack_shard_stats");
+}
+void unpack_shard_stats(const double* red, double* st, double inv_world, cudaStream_t s) {
+  unpack_shard_stats_kernel<<<1, 1, 0, s>>>(red, st, inv_world);
+  check_launch("unpack_shard_stats");
+}
+
+// dst[0, n) = src[0, n) (element size esz) unless the step's statistics row flags a rejected
+// update (the gathered values would be stale)
+template <typename V>
+__global__ void copy_unless_flagged_kernel(V* dst, const V* src, long long n, const double* st) {
+  unsigned long long nbad;
+  memcpy(&nbad, &st[1], 8);
+  if (nbad) return;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+void copy_unless_flagged(void* dst, const void* src, long long elems, int esz, const double* st,
+                         cudaStream_t s) {
+  if (elems <= 0) return;
+  const long long bytes = elems * esz;
+  const bool v16 = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0 &&
+                   bytes % 16 == 0;
+  auto blocks = [](long long n) { return static_cast<unsigned>(std::min<long long>((n + 255) / 256, 2048)); };
+  if (v16) {
+    copy_unless_flagged_kernel<uint4><<<blocks(bytes / 16), 256, 0, s>>>(
+        static_cast<uint4*>(dst), static_cast<const uint4*>(src), bytes / 16, st);
+  } else if (esz == 8) {
+    copy_unless_flagged_kernel<unsigned long long><<<blocks(elems), 256, 0, s>>>(
+        static_cast<unsigned long long*>(dst), static_cast<const unsigned long long*>(src), elems, st);
+  } else if (esz == 4) {
+    copy_unless_flagged_kernel<unsigned><<<blocks(elems), 256, 0, s>>>(
+        static_cast<unsigned*>(dst), static_cast<const unsigned*>(src), elems, st);
+  } else {
+    copy_unless_flagged_kernel<unsigned short><<<blocks(elems), 256, 0, s>>>(
+        static_cast<unsigned short*>(dst), static_cast<const unsigned short*>(src), elems, st);
+  }
+  check_launch("copy_unless_flagged");
+}
+
 bool host_pinned(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {

@@ -36,7 +36,8 @@ class EngineConfigC(C.Structure):
                 ("bandwidth_bytes_per_step", C.c_int64), ("budget_bytes", C.c_int64),
                 ("hyper", N.AdamWHyperC), ("full_backward", C.c_int32),
                 ("check_every_step", C.c_int32), ("grad_scale", C.c_double),
-                ("cuda_graphs", C.c_int32), ("pad_", C.c_int32)]
+                ("cuda_graphs", C.c_int32), ("shard_rank", C.c_int32),
+                ("shard_world", C.c_int32), ("pad_", C.c_int32)]
 
 
 class BatchC(C.Structure):
@@ -76,6 +77,10 @@ for _n, _r, _a in [
     ("cft_engine_phase_totals", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("cft_engine_host_phase_ms", C.c_int, [C.c_void_p, C.c_void_p]),
     ("cft_engine_prepare_graphs", C.c_int, [C.c_void_p]),
+    ("cft_engine_shard_buffer", C.c_int, [C.c_void_p, _P(C.c_void_p), _P(C.c_int64), _P(C.c_int64)]),
+    ("cft_engine_shard_stats", C.c_int, [C.c_void_p, _P(C.c_void_p)]),
+    ("cft_engine_gather_buffer", C.c_int, [C.c_void_p, _P(C.c_void_p), _P(C.c_int64), _P(C.c_int64), _P(C.c_int32)]),
+    ("cft_engine_gather_end", C.c_int, [C.c_void_p]),
     ("cft_engine_wait_step", C.c_int, [C.c_void_p, C.c_int64, _P(C.c_double), _P(C.c_double)]),
     ("cft_engine_write_checkpoints", C.c_int, [C.c_void_p, C.c_char_p]),
     ("cft_engine_read_checkpoints", C.c_int, [C.c_void_p, C.c_char_p]),
@@ -222,6 +227,8 @@ class TrainOptions:
     full_backward: bool = False
     check_every_step: bool = True
     cuda_graphs: bool = True      # Llama engine: one captured graph per chunk's forward+backward
+    shard_rank: int = 0           # sharded optimizer state; world 1 = unsharded
+    shard_world: int = 1
 
 
 class ChunkEngine:
@@ -247,6 +254,8 @@ class ChunkEngine:
         cfg.prefetch = int(o.schedule.prefetch)
         cfg.offload = int(o.offload)
         cfg.cuda_graphs = int(o.cuda_graphs)
+        cfg.shard_rank = o.shard_rank
+        cfg.shard_world = o.shard_world
         cfg.bandwidth_bytes_per_step = o.schedule.bandwidth_bytes_per_step
         cfg.budget_bytes = o.budget_bytes
         h = o.hyper
@@ -335,6 +344,32 @@ class ChunkEngine:
         ptr, n, dt = self.grad_buffer()
         tdt = torch.float64 if dt == N.CFT_F64 else torch.float32
         return _wrap_device(ptr, n, tdt)
+
+    # ---- sharded optimizer state (include/chunkft_b200.h: cft_engine_shard_*) ----
+    def shard_grad_tensor(self) -> torch.Tensor:
+        """This rank's reduce-scatter output (padded shard of the active chunk's gradient)."""
+        p, n, _ = C.c_void_p(), C.c_int64(), C.c_int64()
+        N.check(_L.cft_engine_shard_buffer(self._h, C.byref(p), C.byref(n), C.byref(_)))
+        tdt = torch.float64 if self.grad_buffer()[2] == N.CFT_F64 else torch.float32
+        return _wrap_device(p.value, n.value, tdt)
+
+    def shard_stats(self) -> torch.Tensor:
+        """{sumsq, nonfinite, loss} of this rank's shard (device, float64) -- SUM all-reduce it."""
+        p = C.c_void_p()
+        N.check(_L.cft_engine_shard_stats(self._h, C.byref(p)), "shard_stats")
+        return _wrap_device(p.value, 3, torch.float64)
+
+    def gather_tensor(self):
+        """(packed parameter buffer of the last updated chunk, this rank's offset, shard size)."""
+        p, n, off, dt = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int32()
+        N.check(_L.cft_engine_gather_buffer(self._h, C.byref(p), C.byref(n), C.byref(off),
+                                            C.byref(dt)))
+        tdt = {N.CFT_BF16: torch.bfloat16, N.CFT_F32: torch.float32, N.CFT_F64: torch.float64}[dt.value]
+        world = self.opt.shard_world
+        return _wrap_device(p.value, n.value, tdt), off.value, n.value // world
+
+    def gather_end(self):
+        N.check(_L.cft_engine_gather_end(self._h), "gather_end")
 
     def set_grad_scale(self, s: float):
         N.check(_L.cft_engine_set_grad_scale(self._h, s))
@@ -445,10 +480,11 @@ def _wrap_device(ptr: int, n: int, dtype) -> torch.Tensor:
     class _CAI:
         pass
     cai = _CAI()
-    typestr = {torch.float32: "<f4", torch.float64: "<f8"}[dtype]
+    typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.bfloat16: "<i2"}[dtype]
     cai.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
                                     "version": 3, "strides": None}
-    return torch.as_tensor(cai, device="cuda")
+    t = torch.as_tensor(cai, device="cuda")
+    return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
 
 
 @dataclass

@@ -97,6 +97,7 @@ class OracleEngine:
     def grad_tensor(self):
         return self.grad
 
+
     def step_end(self):
         c = self.active
         mean = self.grad.numpy() * (self.scale * (1.0 / self.mb))
@@ -112,7 +113,79 @@ class OracleEngine:
         self.sched.step_end()
 
 
-def _worker(rank, world, port, out):
+def shard_layout(n, rank, world):
+    """The engine's shard rule (engine.cpp setup): equal shards of ceil(n/world) rounded up to
+    64 elements; rank r owns [min(n, r*S), min(n, (r+1)*S))."""
+    size = ((n + world - 1) // world + 63) // 64 * 64
+    lo = min(n, rank * size)
+    return size, lo, min(n - lo, size)
+
+
+class ShardedOracleEngine(OracleEngine):
+    """CPU stand-in with the sharded-state protocol: this rank keeps master/m/v only for its
+    shard of each chunk, updates it from the reduce-scattered gradient and publishes the new
+    parameters through a packed gather buffer."""
+
+    def __init__(self, layers, params, plan, sched, hyper, micro_batches, rank, world):
+        super().__init__(layers, params, plan, sched, hyper, micro_batches)
+        self.rank, self.world = rank, world
+        for c in range(plan.K):
+            _, lo, cnt = shard_layout(plan.chunks[c].elements, rank, world)
+            self.state[c] = [a[lo: lo + cnt].copy() for a in self.state[c]]
+
+    def step_begin(self):
+        active = super().step_begin()
+        n = self.plan.chunks[active].elements
+        size, _, _ = shard_layout(n, self.rank, self.world)
+        self.grad = torch.zeros(self.world * size, dtype=torch.float64)  # padded RS input
+        self.gshard = torch.zeros(size, dtype=torch.float64)
+        return active
+
+    def forward_backward(self, batch, mb):
+        n = self.plan.chunks[self.active].elements
+        full = self.grad
+        self.grad = full[:n]  # the base class accumulates into the real elements
+        try:
+            return super().forward_backward(batch, mb)
+        finally:
+            self.grad = full
+
+    def shard_grad_tensor(self):
+        return self.gshard
+
+    def shard_stats(self):
+        _, _, cnt = shard_layout(self.plan.chunks[self.active].elements, self.rank, self.world)
+        g = self.gshard.numpy()[:cnt] * (self.scale * (1.0 / self.mb))
+        return torch.tensor([float(np.sum(g * g)), float(np.sum(~np.isfinite(g))), 0.0],
+                            dtype=torch.float64)
+
+    def step_end(self):
+        c = self.active
+        n = self.plan.chunks[c].elements
+        size, lo, cnt = shard_layout(n, self.rank, self.world)
+        mean = self.gshard.numpy()[:cnt] * (self.scale * (1.0 / self.mb))
+        h = self.hyper
+        master, m, v, self.n[c], _, _ = O.adamw(*self.state[c], mean, self.n[c], *h)
+        self.state[c] = [master, m, v]
+        self.gather = torch.zeros(self.world * size, dtype=torch.float64)
+        self.gather[self.rank * size: self.rank * size + cnt] = torch.from_numpy(master)
+        self.sched.step_end()
+
+    def gather_tensor(self):
+        size, _, _ = shard_layout(self.plan.chunks[self.active].elements, self.rank, self.world)
+        return self.gather, self.rank * size, size
+
+    def gather_end(self):
+        packed = self.gather.numpy()
+        o = 0
+        for s in self.plan.chunks[self.active].slices:
+            _, _, r, cols, off = self.tensors[s.tensor_id]
+            k = s.row_count() * cols
+            self.params[off + s.row_begin * cols: off + s.row_begin * cols + k] = packed[o: o + k]
+            o += k
+
+
+def _worker(rank, world, port, out, sharded=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -129,8 +202,12 @@ def _worker(rank, world, port, out):
         infos = [P.TensorInfo(i, n, r, c) for i, (n, r, c) in enumerate(tensors)]
         plan = P.partition(infos, case["K"])
         sched = P.RotationScheduler(P.ScheduleConfig(case["K"], case["T"], case["steps"]), plan)
-        eng = OracleEngine(layers, case["init_params"], plan, sched, tuple(case["hyper"]), 1)
-        step = DataParallelStep(eng)
+        if sharded:
+            eng = ShardedOracleEngine(layers, case["init_params"], plan, sched,
+                                      tuple(case["hyper"]), 1, rank, world)
+        else:
+            eng = OracleEngine(layers, case["init_params"], plan, sched, tuple(case["hyper"]), 1)
+        step = DataParallelStep(eng, sharded=sharded)
         batches = [{k: np.asarray(v) for k, v in b.items()} for b in case["batches"]]
         cursor = 0
         chunks = []
@@ -154,4 +231,19 @@ def test_dp_world2_matches_reference_micro_batches():
     p1, c1 = out[1]
     assert c0 == c1 == case["traj_chunk"]
     assert p0 == p1  # replicas stay identical
+    assert np.array_equal(np.array(p0), np.array(case["final_params"]))
+
+
+def test_dp_sharded_states_world2_matches_reference_micro_batches():
+    """Sharded optimizer state (reduce-scatter / shard AdamW / all-gather) gives
+    the reference micro_batches=2 run bit for bit, with each rank holding half the state."""
+    case = {c["name"]: c for c in json.load(open(GOLD))}["linear_dp2"]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = 31500 + (os.getpid() % 2000)
+    mp.spawn(_worker, args=(2, port, out, True), nprocs=2, join=True)
+    p0, c0 = out[0]
+    p1, c1 = out[1]
+    assert c0 == c1 == case["traj_chunk"]
+    assert p0 == p1
     assert np.array_equal(np.array(p0), np.array(case["final_params"]))

@@ -212,6 +212,112 @@ def test_engine_dp_exchange_matches_reference_micro_batches(cuda):
     assert np.array_equal(p0, np.array(case["final_params"]))
 
 
+def _sharded_exchange(engs):
+    """The collectives of the sharded-state step (reduce-scatter, stats all-reduce) done by
+    hand across engines that stand in for ranks; returns after step_end + all-gather."""
+    W = len(engs)
+    torch.cuda.synchronize()
+    total = sum(e.grad_tensor() for e in engs)
+    for r, e in enumerate(engs):
+        sh = e.shard_grad_tensor()
+        sh.copy_(total[r * sh.numel(): (r + 1) * sh.numel()])
+    reds = [e.shard_stats() for e in engs]
+    torch.cuda.synchronize()
+    red = sum(reds)
+    for x in reds:
+        x.copy_(red)
+    torch.cuda.synchronize()
+    for e in engs:
+        e.step_end()
+    torch.cuda.synchronize()
+    bufs = [e.gather_tensor() for e in engs]
+    for r, (buf, off, n) in enumerate(bufs):
+        for q, (buf2, _, _) in enumerate(bufs):
+            if q != r:
+                buf2[off: off + n].copy_(buf[off: off + n])
+    torch.cuda.synchronize()
+    for e in engs:
+        e.gather_end()
+
+
+@pytest.mark.parametrize("offload", [True, False])
+def test_engine_sharded_states_match_reference_micro_batches(cuda, offload):
+    """Sharded optimizer state: two engines standing in for two ranks, each
+    holding master/m/v for its half of every chunk; reduce-scatter -> shard AdamW ->
+    all-gather reproduces the reference with micro_batches = 2 bit for bit (fp64 path)."""
+    from paper_2605_21177_b200.engine import ChunkEngine
+    case = CASES["linear_dp2"]
+    engs = []
+    for r in range(2):
+        opts = options_of(case, "fp64", offload=offload)
+        opts.micro_batches = 1
+        opts.shard_rank, opts.shard_world = r, 2
+        e = ChunkEngine(model_of(case), np.array(case["init_params"]), 5, opts)
+        e.set_grad_scale(0.5)
+        engs.append(e)
+    bs = batches_of(case)
+    staged = [[e.stage(b, device=True) for b in bs] for e in engs]
+    cursor = 0
+    for t in range(case["steps"]):
+        for r, e in enumerate(engs):
+            e.step_begin()
+            e.forward_backward(staged[r][(cursor + r) % len(bs)], 0)
+        cursor = (cursor + 2) % len(bs)
+        _sharded_exchange(engs)
+    for e in engs:
+        e.finish()
+    p0, p1 = engs[0].params(from_masters=False), engs[1].params(from_masters=False)
+    assert np.array_equal(p0, p1)
+    assert np.array_equal(p0, np.array(case["final_params"]))
+    assert engs[0].trajectory()["chunk"].tolist() == case["traj_chunk"]
+
+
+def test_llama_sharded_states_match_replicated(cuda):
+    """bf16 Llama decoder, 2 stand-in ranks: sharded states + reduce-scatter/all-gather give
+    the replicated-state all-reduce run (same per-element AdamW; the all-gather moves the
+    exact bf16 values), with half the optimizer state per rank.  Replicas stay bit-identical;
+    the two runs agree to the run-to-run reproducibility of the fp32 atomics in the step."""
+    from paper_2605_21177_b200.engine import ChunkEngine, LlamaModel, TrainOptions
+    from paper_2605_21177_b200.plan import ScheduleConfig
+    model = LlamaModel(layers=2)
+    K, B = 5, 2
+    rng = np.random.default_rng(8)
+    seqs = [rng.integers(0, model.vocab, (B, model.seq + 1)).astype(np.int32) for _ in range(2)]
+    out = {}
+    for sharded in (False, True):
+        engs = []
+        for r in range(2):
+            o = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=2 * K, prefetch=True),
+                             dtype="bf16", check_every_step=False)
+            if sharded:
+                o.shard_rank, o.shard_world = r, 2
+            e = ChunkEngine(model, None, B, o, seed=11)
+            e.set_grad_scale(0.5)
+            engs.append(e)
+        staged = [e.stage({"tokens": seqs[r][:, :-1].copy(), "labels": seqs[r][:, 1:].copy()},
+                          device=True) for r, e in enumerate(engs)]
+        for t in range(2 * K):
+            for r, e in enumerate(engs):
+                e.step_begin()
+                e.forward_backward(staged[r], 0)
+            if sharded:
+                _sharded_exchange(engs)
+            else:
+                torch.cuda.synchronize()
+                g = engs[0].grad_tensor() + engs[1].grad_tensor()
+                for e in engs:
+                    e.grad_tensor().copy_(g)
+                torch.cuda.synchronize()
+                for e in engs:
+                    e.step_end()
+        for e in engs:
+            e.finish()
+        ps = [e.params(from_masters=False) for e in engs]
+        assert np.array_equal(ps[0], ps[1])
+        out[sharded] = ps[0]
+    assert rel(out[True], out[False]) < 1e-3
+
+
 CKPT = os.path.join(os.path.dirname(__file__), "golden", "checkpoints.json")
 
 
