@@ -204,8 +204,16 @@ def run_ours(args, rank, world, local_rank):
         eng.step_begin()
         eng.forward_backward(b, 0)
         with torch.cuda.stream(stream):
-            dist.all_reduce(eng.grad_tensor())
-        eng.step_end()
+            if not sharded:
+                dist.all_reduce(eng.grad_tensor())
+                eng.step_end()
+                return
+            dist.reduce_scatter_tensor(eng.shard_grad_tensor(), eng.grad_tensor())
+            dist.all_reduce(eng.shard_stats())
+            eng.step_end()
+            buf, off, n = eng.gather_tensor()
+            dist.all_gather_into_tensor(buf, buf[off: off + n])
+            eng.gather_end()
 
     def barrier():
         torch.cuda.synchronize()
@@ -414,13 +422,18 @@ def run_llama(args, rank, world, local_rank):
     total = W + 2 * S + (W + E2E if E2E else 0) + 2
     # optimizer state (12 B/param fp32 master+m+v) in pinned host memory when the host has
     # room for every local rank's copy, else resident in HBM (still flat, no rotation copies)
-    state_bytes = 12 * model.num_params()
-    offload = host_ram_bytes() > int(1.15 * state_bytes * max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    # N > 1: optimizer state sharded 1/world per rank (reduce-scatter -> shard AdamW ->
+    # all-gather), so every rank's pinned host share is 12 B/param / world
+    sharded = world > 1 and not args.replicated_state
+    state_bytes = 12 * model.num_params() // (world if sharded else 1)
+    local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+    offload = host_ram_bytes() > int(1.15 * state_bytes * local)
     if args.state != "auto":
         offload = args.state == "host"
     opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=total, prefetch=True),
                         dtype="bf16", plan="budget", budget_bytes=budget, offload=offload,
-                        check_every_step=False)
+                        check_every_step=False,
+                        shard_rank=rank if sharded else 0, shard_world=world if sharded else 1)
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
         eng = ChunkEngine(model, None, B, opts, stream=stream, seed=1234)
@@ -443,8 +456,16 @@ def run_llama(args, rank, world, local_rank):
         eng.step_begin()
         eng.forward_backward(b, 0)
         with torch.cuda.stream(stream):
-            dist.all_reduce(eng.grad_tensor())
-        eng.step_end()
+            if not sharded:
+                dist.all_reduce(eng.grad_tensor())
+                eng.step_end()
+                return
+            dist.reduce_scatter_tensor(eng.shard_grad_tensor(), eng.grad_tensor())
+            dist.all_reduce(eng.shard_stats())
+            eng.step_end()
+            buf, off, n = eng.gather_tensor()
+            dist.all_gather_into_tensor(buf, buf[off: off + n])
+            eng.gather_end()
 
     def barrier():
         torch.cuda.synchronize()
@@ -526,7 +547,8 @@ def run_llama(args, rank, world, local_rank):
                        "global_batch_tokens": tokens_per_gpu * world, "seq_len": model.seq,
                        "K": K, "T": 1, "budget_bytes": budget, "plan_hash": f"{plan.hash():016x}",
                        "prefetch": True,
-                       "state_residency": "pinned host + 3 HBM slots" if offload else "HBM (host RAM too small for all ranks)",
+                       "state_residency": ("pinned host + 3 HBM slots" if offload else "HBM (host RAM too small for all ranks)")
+                       + (f", sharded 1/{world} per rank (reduce-scatter / shard AdamW / all-gather)" if sharded else ""),
                        "parallelism": f"dp{world}",
                        "l2": "step working set >> L2 (16 GB of bf16 weights streamed per step)",
                        "timed_steps_cover": "one full rotation (every chunk once)" if S % K == 0 else f"{S} steps"},
@@ -596,6 +618,8 @@ def main():
                     help="llama8b = BASELINE configs[2] (headline); linear4096 = configs[1]")
     ap.add_argument("--layers", type=int, default=32, help="llama8b depth (32 = Llama-3-8B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicated-state", action="store_true",
+                    help="N>1: keep the whole optimizer state on every rank (all-reduce exchange)")
     ap.add_argument("--state", choices=["auto", "host", "hbm"], default="auto",
                     help="optimizer-state residency for llama8b (auto: pinned host when RAM allows)")
     ap.add_argument("--no-e2e", action="store_true")
