@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   const cft_segment* sg = in_smem ? s_segs : segs;
   const float omb1 = 1.f - b1, omb2 = 1.f - b2;
+  const float inv_bc1 = 1.f / bc1, inv_bc2 = 1.f / bc2;
   float pmin = INFINITY, pmax = 0.f;
   const long long n4 = (n + 3) / 4;
   const bool vec_ok = (n % 4) == 0;
@@ -202,15 +203,16 @@ __global__ void __launch_bounds__(kThreads)
       const long long i0 = 4 * q;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
+        // one correctly rounded reciprocal instead of four IEEE divisions: inside the step the
+        // SM clock sits at the power cap and the division sequences, not HBM, were the limit
         const float ge = g[k][e] * gscale;
         mm[k][e] = b1 * mm[k][e] + omb1 * ge;
         vv[k][e] = b2 * vv[k][e] + omb2 * ge * ge;
-        const float mhat = mm[k][e] / bc1;
-        const float vhat = vv[k][e] / bc2;
-        const float denom = sqrtf(vhat) + eps;
-        w[k][e] = w[k][e] - eta * (mhat / denom + wd * w[k][e]);
+        const float mhat = mm[k][e] * inv_bc1;
+        const float vhat = vv[k][e] * inv_bc2;
+        const float pc = __frcp_rn(sqrtf(vhat) + eps);
+        w[k][e] = w[k][e] - eta * (mhat * pc + wd * w[k][e]);
         if (i0 + e < n) {
-          const float pc = 1.f / denom;
           pmin = fminf(pmin, pc);
           pmax = fmaxf(pmax, pc);
         }

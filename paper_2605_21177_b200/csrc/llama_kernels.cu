@@ -79,6 +79,97 @@ __global__ void rms_fwd_kernel(const bf16* __restrict__ x, const bf16* __restric
   }
 }
 
+// Register-resident variants: a row is VPT*blockDim 16-byte vectors, every thread loads its
+// VPT vectors once (all loads in flight together) and keeps them across the row reduction --
+// one HBM read of x per row instead of a latency-bound load / reduce / re-load.
+template <int VPT>
+__device__ __forceinline__ float block_sum_small(float v) {
+  __shared__ float sh[32];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < (int)blockDim.x / 32; ++i) t += sh[i];
+  return t;
+}
+
+template <int VPT>
+__global__ void rms_fwd_reg_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g, int d,
+                                   float eps, bf16* __restrict__ y, float* __restrict__ rstd) {
+  const long long r = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + r * d);
+  uint4 xv[VPT];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) xv[k] = __ldcs(xr + threadIdx.x + k * blockDim.x);
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    float f[8];
+    unpack8(xv[k], f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ss += f[e] * f[e];
+  }
+  const float rs = rsqrtf(block_sum_small<VPT>(ss) / d + eps);
+  if (threadIdx.x == 0) rstd[r] = rs;
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  uint4* yr = reinterpret_cast<uint4*>(y + r * d);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int j = threadIdx.x + k * blockDim.x;
+    float f[8], gg[8];
+    unpack8(xv[k], f);
+    unpack8(gr[j], gg);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = f[e] * rs * gg[e];
+    yr[j] = pack8(f);
+  }
+}
+
+template <int VPT>
+__global__ void rms_bwd_reg_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                   const float* __restrict__ rstd, const bf16* __restrict__ g,
+                                   const bf16* res, int d, bf16* out) {
+  const long long r = blockIdx.x;
+  const float rs = rstd[r];
+  const uint4* dyr = reinterpret_cast<const uint4*>(dy + r * d);
+  const uint4* xr = reinterpret_cast<const uint4*>(x + r * d);
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  uint4 dv[VPT], xv[VPT];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    dv[k] = __ldcs(dyr + threadIdx.x + k * blockDim.x);
+    xv[k] = xr[threadIdx.x + k * blockDim.x];
+  }
+  float c = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    float a[8], b[8], gg[8];
+    unpack8(dv[k], a);
+    unpack8(xv[k], b);
+    unpack8(gr[threadIdx.x + k * blockDim.x], gg);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) c += gg[e] * a[e] * b[e] * rs;
+  }
+  c = block_sum_small<VPT>(c) / d;
+  const uint4* rr = res ? reinterpret_cast<const uint4*>(res + r * d) : nullptr;
+  uint4* orow = reinterpret_cast<uint4*>(out + r * d);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int j = threadIdx.x + k * blockDim.x;
+    float a[8], b[8], gg[8], o[8];
+    unpack8(dv[k], a);
+    unpack8(xv[k], b);
+    unpack8(gr[j], gg);
+    if (rr) unpack8(rr[j], o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float v = rs * (gg[e] * a[e] - b[e] * rs * c);
+      o[e] = rr ? o[e] + v : v;
+    }
+    orow[j] = pack8(o);
+  }
+}
+
 // dx = res + rstd * (g*dy - xhat * sum(g*dy*xhat)/d), xhat = x*rstd   (out may alias res)
 __global__ void rms_bwd_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                                const float* __restrict__ rstd, const bf16* __restrict__ g,
@@ -236,14 +327,33 @@ inline int grid_for(long long n) {
 }
 inline int row_threads(int d) { return std::max(32, std::min(1024, ((d / 8 + 31) / 32) * 32)); }
 
+// vectors per thread for the register-resident kernels: 4 when a row is a multiple of 128
+// threads x 4 vectors (d % 4096 == 0 -> 128+ threads), else 2 / 1 with >= 32 threads; 0 = none
+inline int rms_vpt(int d) {
+  if (d % 8) return 0;
+  const int v = d / 8;
+  for (int k : {4, 2, 1})
+    if (v % (32 * k) == 0 && v / k <= 1024) return k;
+  return 0;
+}
 void rms_fwd(const bf16* x, const bf16* g, long long rows, int d, float eps, bf16* y, float* rstd,
              cudaStream_t s) {
-  rms_fwd_kernel<<<(unsigned)rows, row_threads(d), 0, s>>>(x, g, d, eps, y, rstd);
+  const int k = rms_vpt(d);
+  const unsigned th = k ? static_cast<unsigned>(d / 8 / k) : 0;
+  if (k == 4) rms_fwd_reg_kernel<4><<<(unsigned)rows, th, 0, s>>>(x, g, d, eps, y, rstd);
+  else if (k == 2) rms_fwd_reg_kernel<2><<<(unsigned)rows, th, 0, s>>>(x, g, d, eps, y, rstd);
+  else if (k == 1) rms_fwd_reg_kernel<1><<<(unsigned)rows, th, 0, s>>>(x, g, d, eps, y, rstd);
+  else rms_fwd_kernel<<<(unsigned)rows, row_threads(d), 0, s>>>(x, g, d, eps, y, rstd);
   check_launch("rms_fwd");
 }
 void rms_bwd(const bf16* dy, const bf16* x, const float* rstd, const bf16* g, const bf16* res,
              long long rows, int d, bf16* out, cudaStream_t s) {
-  rms_bwd_kernel<<<(unsigned)rows, row_threads(d), 0, s>>>(dy, x, rstd, g, res, d, out);
+  const int k = rms_vpt(d);
+  const unsigned th = k ? static_cast<unsigned>(d / 8 / k) : 0;
+  if (k == 4) rms_bwd_reg_kernel<4><<<(unsigned)rows, th, 0, s>>>(dy, x, rstd, g, res, d, out);
+  else if (k == 2) rms_bwd_reg_kernel<2><<<(unsigned)rows, th, 0, s>>>(dy, x, rstd, g, res, d, out);
+  else if (k == 1) rms_bwd_reg_kernel<1><<<(unsigned)rows, th, 0, s>>>(dy, x, rstd, g, res, d, out);
+  else rms_bwd_kernel<<<(unsigned)rows, row_threads(d), 0, s>>>(dy, x, rstd, g, res, d, out);
   check_launch("rms_bwd");
 }
 void rms_dgamma(const bf16* dy, const bf16* x, const float* rstd, long long rows, int d,
