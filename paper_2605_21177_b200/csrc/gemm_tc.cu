@@ -390,7 +390,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = blockIdx.x; u < args.num_units; u += gridDim.x) {
       int tm, tn, sp;
       decode_unit(args, u, tm, tn, sp);
-      ptx::mbar_wait(&tfull[acc], acc_phase);
+      // one warp polls the accumulator barrier with sleeps, the other epilogue warps park on
+      // a named barrier (no issue slots, no wake-ups on every pipeline event)
+      if (warp == 2) ptx::mbar_wait_sleep(&tfull[acc], acc_phase, 256);
+      ptx::named_bar_sync(1, 32 * kEpiWarps);
       ptx::tc_fence_after();
       const int row = tm * BM + quarter * 32 + lane - args.row_skip;
       const bool row_ok = row >= 0 && row < args.M;
@@ -575,7 +578,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int u = pair; u < args.num_units; u += npairs) {
       int tm, tn, sp;
       decode_unit(args, u, tm, tn, sp);
-      ptx::mbar_wait(&tfull[acc], acc_phase);
+      // one warp polls the accumulator barrier with sleeps, the other epilogue warps park on
+      // a named barrier (no issue slots, no wake-ups on every pipeline event)
+      if (warp == 2) ptx::mbar_wait_sleep(&tfull[acc], acc_phase, 256);
+      ptx::named_bar_sync(1, 32 * kEpiWarps);
       ptx::tc_fence_after();
       const int row = tm * BMP + static_cast<int>(rank) * 128 + quarter * 32 + lane - args.row_skip;
       const bool row_ok = row >= 0 && row < args.M;

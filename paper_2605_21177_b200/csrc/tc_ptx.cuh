@@ -47,6 +47,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Poll without the hardware suspend: a suspended try_wait is woken by every mbarrier event in
+// the CTA (each TMA / MMA completion), so warps parked for a whole mainloop re-poll every
+// ~150 ns.  Callers that can tolerate wake-up latency sleep a fixed time between polls.
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 0;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, unsigned ns) {
+  long long polls = 0;
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(ns);
+    if (++polls > (20000000000LL / 64) / ns) __trap();  // ~20 s bound, like mbar_wait
+  }
+}
+// bar.sync on a named barrier for a subset of the CTA's warps (id 0 is __syncthreads)
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 // ---- TMA ----
 __device__ __forceinline__ void tma_prefetch(const void* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
