@@ -332,13 +332,19 @@ def run_ours(args, rank, world, local_rank):
     return res
 
 
+LLAMA70_WORKLOAD = ("llama3_70b_layer_stack_chunk_local_step (BASELINE configs[4]: Llama-3-70B "
+                    "layer shapes -- d=8192, 64/8 heads, ffn 28672, vocab 128256 -- in a stack of "
+                    "{layers} layers sized to one GPU's HBM, seq 1024, 8 sequences = 8192 tokens "
+                    "per GPU per step, 2 GiB byte-budget chunks rotating every step with optimizer "
+                    "state offloaded to pinned host memory and prefetched; flat-memory check)")
+
 LLAMA_WORKLOAD = ("llama3_8b_chunk_local_step (BASELINE configs[2]: Llama-3-8B-shaped decoder, 32 "
                   "layers, d=4096, 32/8 heads, ffn 14336, vocab 128256, seq 1024, 8 sequences = "
                   "8192 tokens per GPU per step, byte-budget chunks of 2 GiB -> K=60 rotating every "
                   "step (T=1) over all layers, bf16 operands / fp32 accumulate + state)")
 
 
-def reference_llama_cpu(rows: int = 16, K: int = 60):
+def reference_llama_cpu(rows: int = 16, K: int = 60, model=None):
     """The reference CPU path (oracle/_ref, OpenMP on all host cores) for the configs[2] step,
     EXTRAPOLATED per SURVEY.md 8(d): one decoder layer's seven Linear shapes (forward + dX,
     which the reference always forms) timed at `rows` tokens, x 32 layers, + the lm_head
@@ -350,9 +356,13 @@ def reference_llama_cpu(rows: int = 16, K: int = 60):
         return None
     R.set_backend(True)
     rng = np.random.default_rng(3)
-    d, ffn, kv, vocab, L = 4096, 14336, 1024, 128256, 32
-    P = 8_030_261_248
-    shapes = [(d, d), (kv, d), (kv, d), (d, d), (ffn, d), (ffn, d), (d, ffn)]
+    if model is None:
+        from paper_2605_21177_b200.engine import LlamaModel
+        model = LlamaModel.llama3_8b()
+    d, ffn, vocab, L = model.d, model.ffn, model.vocab, model.layers
+    q, kv = model.heads * model.head_dim, model.kv_heads * model.head_dim
+    P = model.num_params()
+    shapes = [(q, d), (kv, d), (kv, d), (d, q), (ffn, d), (ffn, d), (d, ffn)]
 
     def timed(fn):
         t0 = time.perf_counter()
@@ -383,10 +393,24 @@ def reference_llama_cpu(rows: int = 16, K: int = 60):
     step_s = L * t_layer + t_head + t_dw + t_adam
     return dict(value=rows / step_s, unit="tokens/s", cores=R.openmp_threads(), kind="reference",
                 sample=f"EXTRAPOLATED: reference kernels (oracle/_ref, OpenMP) at {rows} tokens: one "
-                       f"decoder layer's 7 Linear fwd+dX ({t_layer:.2f} s) x 32 + lm_head fwd+dX "
+                       f"decoder layer's 7 Linear fwd+dX ({t_layer:.2f} s) x {L} + lm_head fwd+dX "
                        f"({t_head:.2f} s) + dW on one chunk ({t_dw:.2f} s) + AdamW on one chunk "
                        f"({t_adam:.2f} s); attention/norm/SwiGLU not charged",
                 step_s=step_s)
+
+
+def llama_setup(args):
+    """(model, K of the 2 GiB byte-budget plan, workload string) for the llama workloads."""
+    from paper_2605_21177_b200.engine import LlamaModel
+    from paper_2605_21177_b200.plan import TensorInfo, partition_by_budget
+    if args.workload == "llama70b":
+        model = LlamaModel.llama3_70b(layers=args.layers if args.layers != 32 else 12)
+        name = LLAMA70_WORKLOAD.format(layers=model.layers)
+    else:
+        model = LlamaModel.llama3_8b(layers=args.layers)
+        name = LLAMA_WORKLOAD
+    infos = [TensorInfo(i, n, r, c) for i, (n, r, c) in enumerate(model.tensors())]
+    return model, partition_by_budget(infos, 2 << 30).K, name
 
 
 def host_ram_bytes():
@@ -409,7 +433,7 @@ def run_llama(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     peaks = load_peaks()
-    model = LlamaModel.llama3_8b(layers=args.layers)
+    model, _, workload_name = llama_setup(args)
     B = 8
     tokens_per_gpu = B * model.seq
     budget = 2 << 30
@@ -419,7 +443,8 @@ def run_llama(args, rank, world, local_rank):
     W = args.warmup
     S = args.steps if args.steps > 0 else K  # default: one full rotation = rotation average
     E2E = 0 if args.no_e2e else S
-    total = W + 2 * S + (W + E2E if E2E else 0) + 2
+    FM = min(K, 16)  # flat-memory probe: per-step device memory in use (untimed, synced)
+    total = W + 2 * S + (W + E2E if E2E else 0) + FM + 2
     # optimizer state (12 B/param fp32 master+m+v) in pinned host memory when the host has
     # room for every local rank's copy, else resident in HBM (still flat, no rotation copies)
     # N > 1: optimizer state sharded 1/world per rank (reduce-scatter -> shard AdamW ->
@@ -522,9 +547,19 @@ def run_llama(args, rank, world, local_rank):
             f1.record(stream)
             barrier()
             e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+    # flat-memory check: device bytes in use after each of FM rotation steps
+    used = []
+    for i in range(FM):
+        one_step(dev_b[i % 4])
+        torch.cuda.synchronize()
+        free, tot = torch.cuda.mem_get_info()
+        used.append(tot - free)
     eng.finish()
     tr = eng.trajectory()
     finite = bool(np.all(np.isfinite(tr["loss"])))
+    flat = {"steps": FM, "used_bytes_min": int(min(used)), "used_bytes_max": int(max(used)),
+            "jitter": (max(used) - min(used)) / (sum(used) / len(used)),
+            "engine_device_bytes": int(eng.device_bytes())}
 
     value = tokens_per_gpu * world * S / (ms / 1e3)
     gemm_flops = phases["fwd_gemm"][2] + phases["dgrad"][2] + phases["wgrad"][2]
@@ -542,7 +577,7 @@ def run_llama(args, rank, world, local_rank):
             "warmup": W, "ms_per_step": ms / S, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded uniform token ids; random-init weights, U(-0.5,0.5)/sqrt(fan-in))",
-            "config": {"workload": LLAMA_WORKLOAD, "layers": args.layers, "params": model.num_params(),
+            "config": {"workload": workload_name, "layers": model.layers, "params": model.num_params(),
                        "tokens_per_gpu_per_step": tokens_per_gpu,
                        "global_batch_tokens": tokens_per_gpu * world, "seq_len": model.seq,
                        "K": K, "T": 1, "budget_bytes": budget, "plan_hash": f"{plan.hash():016x}",
@@ -574,6 +609,7 @@ def run_llama(args, rank, world, local_rank):
             "unattributed_ms_per_step": (prof_wall_ms - prof_ms) / S,
             "gpu_launches": launches,
             "device_bytes": eng.device_bytes(),
+            "flat_memory": flat,
             "final_loss": float(tr["loss"][-1]),
             "clocks": clk.summary(),
         }
@@ -614,9 +650,11 @@ def main():
                     help="timed steps (default: one full rotation for llama8b, 200 for linear4096)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["llama8b", "linear4096"], default="llama8b",
-                    help="llama8b = BASELINE configs[2] (headline); linear4096 = configs[1]")
-    ap.add_argument("--layers", type=int, default=32, help="llama8b depth (32 = Llama-3-8B)")
+    ap.add_argument("--workload", choices=["llama8b", "llama70b", "linear4096"], default="llama8b",
+                    help="llama8b = BASELINE configs[2] (headline); llama70b = configs[4] layer "
+                         "shapes (12-layer stack by default); linear4096 = configs[1]")
+    ap.add_argument("--layers", type=int, default=32,
+                    help="decoder depth (32 = Llama-3-8B; llama70b defaults to 12)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicated-state", action="store_true",
                     help="N>1: keep the whole optimizer state on every rank (all-reduce exchange)")
@@ -637,9 +675,10 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        if args.workload == "llama8b":
-            cpu = reference_llama_cpu()
-            workload, sample_tokens, per_step_tokens = LLAMA_WORKLOAD, 16, 8192
+        if args.workload in ("llama8b", "llama70b"):
+            m, K, workload = llama_setup(args)
+            cpu = reference_llama_cpu(K=K, model=m)
+            sample_tokens, per_step_tokens = 16, 8192
         else:
             cpu = None
         if cpu is None:
@@ -662,7 +701,7 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if args.workload == "llama8b":
+    if args.workload in ("llama8b", "llama70b"):
         res = run_llama(args, rank, world, local_rank)
     else:
         res = run_ours(args, rank, world, local_rank)
@@ -670,7 +709,10 @@ def main():
         if not args.no_sweep:
             res.setdefault("sliced_dw", {})["configs1_sweep"] = slice_sweep(local_rank)
         if world == 1 and not args.no_cpu_baseline:
-            cpu = reference_llama_cpu() if args.workload == "llama8b" else None
+            cpu = None
+            if args.workload in ("llama8b", "llama70b"):
+                m, K, _ = llama_setup(args)
+                cpu = reference_llama_cpu(K=K, model=m)
             if cpu is None:
                 cpu = reference_cpu()
             res["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}

@@ -193,6 +193,13 @@ class LlamaModel:
         return LlamaModel(layers=layers, d=4096, heads=32, kv_heads=8, head_dim=128, ffn=14336,
                           vocab=128256, seq=1024)
 
+    @staticmethod
+    def llama3_70b(layers=80):
+        """Llama-3-70B layer shapes (d 8192, 64/8 heads, ffn 28672); BASELINE configs[4] runs
+        a shortened stack that fits one GPU's HBM."""
+        return LlamaModel(layers=layers, d=8192, heads=64, kv_heads=8, head_dim=128, ffn=28672,
+                          vocab=128256, seq=1024)
+
     def tensors(self):
         """[(name, rows, cols)] in registration order (= oracle/shapes.py)."""
         q, kv = self.heads * self.head_dim, self.kv_heads * self.head_dim
