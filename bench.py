@@ -527,6 +527,7 @@ def run_llama(args, rank, world, local_rank):
             one_step(dev_b[i % 4])
         p1.record(stream)
         phases = eng.phase_totals(with_work=True)
+        pbytes = eng.phase_bytes()
         prof_wall_ms = p0.elapsed_time(p1)
         eng.profile(False, 0)
         losses = [eng.wait_step(W + 2 * S - 1)[0]]
@@ -565,6 +566,17 @@ def run_llama(args, rank, world, local_rank):
     gemm_flops = phases["fwd_gemm"][2] + phases["dgrad"][2] + phases["wgrad"][2]
     gemm_ms = phases["fwd_gemm"][0] + phases["dgrad"][0] + phases["wgrad"][0]
     gemm_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12
+    gemm_launches = sum(phases[k][1] for k in ("fwd_gemm", "dgrad", "wgrad"))
+    alg_bytes_launch = sum(pbytes[k] for k in ("fwd_gemm", "dgrad", "wgrad")) / max(gemm_launches, 1)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_gemm_traffic.json")
+    if args.workload == "llama8b" and os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        traffic = tj["dram_bytes_per_launch"]
+        traffic_src = ("profiles/r1_gemm_traffic.json: ncu dram__bytes_read+write per GEMM launch "
+                       f"over one step ({tj['gemm_launches']} launches, L2 flushed per kernel); "
+                       f"{tj['ratio']:.2f}x the algorithmic bytes")
     wg_tflops = phases["wgrad"][2] / max(phases["wgrad"][0], 1e-9) / 1e9
     adam_gbs = phases["update"][2] / max(phases["update"][0], 1e-9) / 1e6
     launches = int(sum(v[1] for k, v in phases.items()
@@ -594,7 +606,9 @@ def run_llama(args, rank, world, local_rank):
             "roofline": {"bound": "tensor",
                          "kernel": "gemm_bf16_2sm_kernel / gemm_bf16_kernel (tcgen05 fwd + dgrad + sliced wgrad)",
                          "achieved": gemm_tflops, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
-                         "frac": gemm_tflops / peaks["bf16_sustained"], "traffic": None,
+                         "frac": gemm_tflops / peaks["bf16_sustained"], "traffic": traffic,
+                         "traffic_unit": "bytes per GEMM launch", "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": alg_bytes_launch,
                          "peak_source": peaks["source"] + " sustained bf16 (MEASURED_PEAKS.json)",
                          "algorithmic_flops_per_step": gemm_flops / S,
                          "share_of_step": gemm_ms / ms,

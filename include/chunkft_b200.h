@@ -409,6 +409,10 @@ int cft_engine_phase_totals(cft_engine* e, float* ms, int64_t* counts, double* w
 /* Host-side submission time per profiler category (CFT_NUM_PHASES entries, ms) accumulated
  * since the previous call -- shows whether the step is launch-bound. */
 int cft_engine_host_phase_ms(cft_engine* e, double* ms);
+/* Algorithmic bytes per profiler category since the previous call (GEMMs: every operand read
+ * once and the result written once, plus fused-epilogue traffic) -- the roofline's numerator
+ * for a bandwidth view of the GEMM family. */
+int cft_engine_phase_bytes(cft_engine* e, double* bytes);
 /* Block the host until step t's loss / grad_norm_sq reached host memory (t within the last
  * 4 steps) -- a per-step result read that does not drain the device queue. */
 int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq);

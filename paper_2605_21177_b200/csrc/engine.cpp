@@ -397,6 +397,13 @@ void Engine::mark(int phase, cudaStream_t s, bool begin) {
   }
 }
 
+void Engine::phase_bytes(double* b) {
+  for (int i = 0; i < kNumPhases; ++i) {
+    b[i] = bytes_[i];
+    bytes_[i] = 0.0;
+  }
+}
+
 void Engine::host_phase_ms(double* ms) {
   for (int i = 0; i < kNumPhases; ++i) {
     ms[i] = host_ms_[i];

@@ -137,6 +137,7 @@ class Engine {
   // statistics / update passes); resets the marks
   void phase_totals(float* ms, int64_t* counts, double* work);
   void host_phase_ms(double* ms);  // host (submission) time per phase since the last call
+  void phase_bytes(double* b);    // algorithmic bytes per phase since the last call
   void wait_step(int64_t t, double* loss, double* gsq);  // host waits for step t's result only
 
   // CKFT v1 checkpoints (optimizer.cpp:210-251, FORMATS.md:176-194): one chunk_NNNN.bin per
@@ -275,6 +276,10 @@ class Engine {
   void pb(int phase);
   void mark(int phase, cudaStream_t s, bool begin);  // copy-stream marks
   double work_[16] = {};
+  double bytes_[16] = {};  // algorithmic bytes per phase (GEMM operands once + result once)
+  void add_bytes(int phase, double b) {
+    if (profiling_) bytes_[phase] += b;
+  }
   double host_ms_[16] = {};
   std::chrono::steady_clock::time_point host_t0_;
   void add_work(int phase, double w) {

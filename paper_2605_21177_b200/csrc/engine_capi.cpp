@@ -188,6 +188,10 @@ int cft_engine_prepare_graphs(cft_engine* e) {
   return guarded([&] { e->p->prepare_graphs(); });
 }
 
+int cft_engine_phase_bytes(cft_engine* e, double* bytes) {
+  return guarded([&] { e->p->phase_bytes(bytes); });
+}
+
 int cft_engine_host_phase_ms(cft_engine* e, double* ms) {
   return guarded([&] { e->p->host_phase_ms(ms); });
 }

@@ -229,6 +229,12 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     return nullptr;
   };
   auto aux_at = [&](const SliceRt* s) { return static_cast<float*>(aux_) + s->aux_off; };
+  // algorithmic work of a GEMM Y[M x Nn] = A[M x Kk] B^T: FLOPs, and bytes with every operand
+  // read once and the result written once (bf16; `extra` = fused epilogue traffic)
+  auto gemm_work = [&](int phase, double M, double Nn, double Kk, double out_bytes, double extra) {
+    add_work(phase, 2.0 * M * Nn * Kk);
+    add_bytes(phase, 2.0 * (M * Kk + Nn * Kk) + out_bytes + extra);
+  };
   // sliced weight gradient of a (possibly stacked) weight; `row0` = the tensor's first row
   // within the stacked operand
   auto wgrad = [&](int tensor, const void* dy, int64_t out_dim, const void* x, int64_t in_dim,
@@ -236,7 +242,9 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     const SliceRt* s = slice_of(tensor);
     if (!s) return;
     pb(kWgrad);
-    add_work(kWgrad, 2.0 * N * double(s->re - s->rb) * in_dim);
+    const double rows = double(s->re - s->rb);
+    add_work(kWgrad, 2.0 * N * rows * in_dim);
+    add_bytes(kWgrad, 2.0 * (N * rows + N * double(in_dim)) + 4.0 * rows * in_dim);
     tc::linear_wgrad_slice(dy, N, out_dim, x, in_dim, row0 + s->rb, row0 + s->re, aux_at(s), 1, st);
     pe();
   };
@@ -257,7 +265,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
                    static_cast<bf16*>(z.a), z.rstd1, st);
     pe();
     pb(kFwdGemm);
-    add_work(kFwdGemm, 2.0 * N * d * QKV);
+    gemm_work(kFwdGemm, N, QKV, d, 2.0 * N * QKV, 0);
     tc::linear_fwd(z.a, N, d, P(id(l, 1)), QKV, z.qkv, st);  // wq|wk|wv stacked
     pe();
     pb(kFwdOther);
@@ -268,7 +276,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     attn_->forward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, z.lse, st);
     pe();
     pb(kFwdGemm);
-    add_work(kFwdGemm, 2.0 * N * Q * d);
+    gemm_work(kFwdGemm, N, d, Q, 2.0 * N * d, 2.0 * N * d);  // + residual read
     tc::linear_fwd(z.o, N, Q, P(id(l, 4)), d, z.h, st, z.x);  // h = x + o Wo^T
     pe();
     pb(kFwdOther);
@@ -278,7 +286,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     // w1|w3 stacked with SwiGLU in the epilogue; [u | g] is kept only where the backward
     // suffix will read it
     pb(kFwdGemm);
-    add_work(kFwdGemm, 2.0 * N * d * 2 * F);
+    gemm_work(kFwdGemm, N, 2 * F, d, 2.0 * N * F, stop <= id(l, 7) ? 4.0 * N * F : 0.0);
     const bool fused = tc::linear_fwd_swiglu(z.m, N, d, P(id(l, 6)), F, z.s,
                                              stop <= id(l, 7) ? z.ug : nullptr, st);
     if (!fused) tc::linear_fwd(z.m, N, d, P(id(l, 6)), 2 * F, z.ug, st);
@@ -289,7 +297,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
       pe();
     }
     pb(kFwdGemm);
-    add_work(kFwdGemm, 2.0 * N * F * d);
+    gemm_work(kFwdGemm, N, d, F, 2.0 * N * d, 2.0 * N * d);  // + residual read
     tc::linear_fwd(z.s, N, F, P(id(l, 8)), d, lb_[l + 1].x, st, z.h);  // x' = h + s W2^T
     pe();
   }
@@ -298,7 +306,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
                  static_cast<bf16*>(l_xf_), l_rstdf_, st);
   pe();
   pb(kFwdGemm);
-  add_work(kFwdGemm, 2.0 * N * d * V);
+  gemm_work(kFwdGemm, N, V, d, 2.0 * N * V, 0);
   tc::linear_fwd(l_xf_, N, d, P(head_id), V, l_logits_, st);
   pe();
 
@@ -315,7 +323,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
   wgrad(head_id, dlog, V, l_xf_, d, 0);
   if (need(norm_id)) {
     pb(kDgrad);
-    add_work(kDgrad, 2.0 * N * V * d);
+    gemm_work(kDgrad, N, d, V, 2.0 * N * d, 0);
     tc::linear_dgrad(dlog, N, V, P(head_id), d, l_dxf_, 0, st);
     pe();
     if (const SliceRt* s = slice_of(norm_id)) {
@@ -337,7 +345,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     wgrad(id(l, 8), l_gx_, d, z.s, F, 0);
     if (!need(id(l, 7))) break;
     pb(kDgrad);  // dS = GX W2 with the SwiGLU backward in the epilogue -> [du | dg]
-    add_work(kDgrad, 2.0 * N * d * F);
+    gemm_work(kDgrad, N, F, d, 4.0 * N * F, 4.0 * N * F);  // [du|dg] out, [u|g] in
     const bool fused = tc::linear_dgrad_swiglu(l_gx_, N, d, P(id(l, 8)), F, z.ug, l_dug_, st);
     if (!fused) tc::linear_dgrad(l_gx_, N, d, P(id(l, 8)), F, l_ds_, 0, st);
     pe();
@@ -351,7 +359,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     wgrad(id(l, 7), l_dug_, 2 * F, z.m, d, F);  // w3 rows [F,2F)
     if (!need(id(l, 5))) break;
     pb(kDgrad);
-    add_work(kDgrad, 2.0 * N * 2 * F * d);
+    gemm_work(kDgrad, N, d, 2 * F, 2.0 * N * d, 0);
     tc::linear_dgrad(l_dug_, N, 2 * F, P(id(l, 6)), d, l_da_, 0, st);  // dM (reuses da buffer)
     pe();
     if (const SliceRt* s = slice_of(id(l, 5))) {
@@ -369,7 +377,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     wgrad(id(l, 4), l_gh_, d, z.o, Q, 0);
     if (!need(id(l, 3))) break;
     pb(kDgrad);
-    add_work(kDgrad, 2.0 * N * d * Q);
+    gemm_work(kDgrad, N, Q, d, 2.0 * N * Q, 0);
     tc::linear_dgrad(l_gh_, N, d, P(id(l, 4)), Q, l_do_, 0, st);
     pe();
     pb(kBwdOther);
@@ -384,7 +392,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     wgrad(id(l, 3), l_dqkv_, QKV, z.a, d, Q + KV);
     if (!need(id(l, 0))) break;
     pb(kDgrad);
-    add_work(kDgrad, 2.0 * N * QKV * d);
+    gemm_work(kDgrad, N, d, QKV, 2.0 * N * d, 0);
     tc::linear_dgrad(l_dqkv_, N, QKV, P(id(l, 1)), d, l_da_, 0, st);  // dA
     pe();
     if (const SliceRt* s = slice_of(id(l, 0))) {

@@ -76,6 +76,7 @@ for _n, _r, _a in [
     ("cft_engine_profile", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
     ("cft_engine_phase_totals", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("cft_engine_host_phase_ms", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("cft_engine_phase_bytes", C.c_int, [C.c_void_p, C.c_void_p]),
     ("cft_engine_prepare_graphs", C.c_int, [C.c_void_p]),
     ("cft_engine_shard_buffer", C.c_int, [C.c_void_p, _P(C.c_void_p), _P(C.c_int64), _P(C.c_int64)]),
     ("cft_engine_shard_stats", C.c_int, [C.c_void_p, _P(C.c_void_p)]),
@@ -455,6 +456,12 @@ class ChunkEngine:
     def prepare_graphs(self):
         """Capture every chunk's forward+backward CUDA graph now (Llama engine)."""
         N.check(_L.cft_engine_prepare_graphs(self._h), "prepare_graphs")
+
+    def phase_bytes(self):
+        """{phase: algorithmic bytes} accumulated since the previous call (profiling on)."""
+        b = np.zeros(len(self.PHASES), np.float64)
+        N.check(_L.cft_engine_phase_bytes(self._h, b.ctypes.data))
+        return {k: float(b[i]) for i, k in enumerate(self.PHASES)}
 
     def host_phase_ms(self):
         """{phase: host submission ms} accumulated since the previous call (profiling on)."""
