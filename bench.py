@@ -675,6 +675,8 @@ def main():
     ap.add_argument("--state", choices=["auto", "host", "hbm"], default="auto",
                     help="optimizer-state residency for llama8b (auto: pinned host when RAM allows)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fusion", type=int, default=3,
+                    help="A/B: epilogue fusion mask (1 SwiGLU, 2 RoPE; 0 = separate kernels)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[1] sliced-dW sweep")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -715,6 +717,9 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.fusion != 3:
+        from paper_2605_21177_b200 import ops
+        ops.set_fusion(args.fusion)
     if args.workload in ("llama8b", "llama70b"):
         res = run_llama(args, rank, world, local_rank)
     else:

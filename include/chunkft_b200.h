@@ -267,8 +267,9 @@ int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t
 /* bf16 GEMM tiling policy: 0 auto (CTA-pair 256x256 tcgen05 tiles when the tile space fills
  * the chip, single-CTA 128x256 otherwise), 1 force single-CTA, 2 force CTA pairs. */
 int cft_set_gemm_policy(int policy);
-/* Epilogue fusions of the Llama engine (SwiGLU in the w1|w3 forward and w2 dgrad GEMMs):
- * 1 on (default), 0 off -- results are bit-identical either way. */
+/* Epilogue fusions of the Llama engine, a bit mask: 1 = SwiGLU in the w1|w3 forward and w2
+ * dgrad GEMMs, 2 = RoPE in the QKV forward GEMM; default 3, 0 = separate kernels.  Results are
+ * bit-identical either way. */
 int cft_set_fusion(int enable);
 
 /* Element conversion (e.g. fp32 master -> bf16 params at init). */

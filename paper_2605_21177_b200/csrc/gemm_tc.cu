@@ -52,6 +52,10 @@ struct Args {
   //   writes [du | dg] to C (ld = 2 glu_F).  Both round exactly like the unfused kernels.
   int glu, glu_F;
   void* glu_ug;
+  // RoPE in the forward epilogue (QKV projection): columns < rope_cols are rotated per head of
+  // rope_hd columns with the (cos, sin) table rope_cs[pos * rope_hd/2 + i], pos = row % rope_seq
+  const float2* rope_cs;
+  int rope_seq, rope_hd, rope_cols;
   void* C;
   long long ldc;
   int epi;
@@ -265,6 +269,47 @@ __device__ __forceinline__ void glu_bwd_epilogue(const Args& args, uint32_t tacc
   }
 }
 
+// RoPE epilogue over this thread's columns [c0, c1) of a tile (whole heads): rounds the
+// accumulator to bf16 first and rotates with explicit roundings, exactly like rope_vec_kernel
+// on the stored projection.
+__device__ __forceinline__ void rope_epilogue(const Args& args, uint32_t tacc, int row,
+                                              bool row_ok, int colbase, int c0, int c1) {
+  const int hd = args.rope_hd, hh = hd / 2;
+  const int pos = row_ok ? row % args.rope_seq : 0;
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.C) + static_cast<long long>(row) * args.ldc;
+#pragma unroll 1
+  for (int hs = c0; hs < c1; hs += hd) {
+#pragma unroll 1
+    for (int c = 0; c < hh; c += 16) {
+      uint32_t ra[16], rb[16];
+      ptx::tmem_ld16(tacc + hs + c, ra);
+      ptx::tmem_ld16(tacc + hs + hh + c, rb);
+      ptx::tmem_wait_ld();
+      if (!row_ok) continue;
+      const float4* cs4 = reinterpret_cast<const float4*>(args.rope_cs + static_cast<long long>(pos) * hh + c);
+      float y1[16], y2[16];
+#pragma unroll
+      for (int e2 = 0; e2 < 8; ++e2) {
+        const float4 q = cs4[e2];  // (cos, sin) of pairs 2*e2 and 2*e2 + 1
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int e = 2 * e2 + k;
+          const float co = k ? q.z : q.x, sn = k ? q.w : q.y;
+          const float x1 = bf16_round(__uint_as_float(ra[e])), x2 = bf16_round(__uint_as_float(rb[e]));
+          y1[e] = __fsub_rn(__fmul_rn(x1, co), __fmul_rn(x2, sn));
+          y2[e] = __fadd_rn(__fmul_rn(x2, co), __fmul_rn(x1, sn));
+        }
+      }
+      uint4* p1 = reinterpret_cast<uint4*>(out + colbase + hs + c);
+      uint4* p2 = reinterpret_cast<uint4*>(out + colbase + hs + hh + c);
+      p1[0] = pack8_bf16(y1);
+      p1[1] = pack8_bf16(y1 + 8);
+      p2[0] = pack8_bf16(y2);
+      p2[1] = pack8_bf16(y2 + 8);
+    }
+  }
+}
+
 template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -401,6 +446,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tacc = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
       if (args.glu == 2) {
         glu_bwd_epilogue<BN>(args, tacc, row, row_ok, tn, half * (BN / 2), (half + 1) * (BN / 2));
+      } else if (args.rope_cs && tn * BN + half * (BN / 2) < args.rope_cols) {
+        rope_epilogue(args, tacc, row, row_ok, tn * BN, half * (BN / 2), (half + 1) * (BN / 2));
       } else {
 #pragma unroll 1
         for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
@@ -600,6 +647,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       } else if (args.glu == 2) {
         glu_bwd_epilogue<BNP>(args, tacc, row, row_ok, tn, half * (BNP / 2),
                               (half + 1) * (BNP / 2));
+      } else if (args.rope_cs && tn * BNP + half * (BNP / 2) < args.rope_cols) {
+        rope_epilogue(args, tacc, row, row_ok, tn * BNP, half * (BNP / 2), (half + 1) * (BNP / 2));
       } else {
 #pragma unroll 1
         for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 16) {
@@ -750,7 +799,7 @@ bool use_pairs(int M, int N, int K, bool allow_split) {
 void set_policy(int p) { g_policy = p; }
 
 namespace {
-int g_fuse = 1;
+int g_fuse = 3;  // bit 0: SwiGLU epilogues, bit 1: RoPE epilogue
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
 void set_fusion(int on) { g_fuse = on; }
@@ -760,7 +809,7 @@ void set_fusion(int on) { g_fuse = on; }
 // policy does not allow the fusion (the caller runs linear_fwd + swiglu_fwd).
 bool linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void* w13, int64_t F,
                        void* s, void* ug, cudaStream_t stream) {
-  if (!g_fuse || g_policy == 1 || F % 128 != 0 || in_dim % 8 != 0 || n_tok < 1 ||
+  if (!(g_fuse & 1) || g_policy == 1 || F % 128 != 0 || in_dim % 8 != 0 || n_tok < 1 ||
       !aligned16(s) || (ug && !aligned16(ug)))
     return false;
   Args a{};
@@ -784,7 +833,7 @@ bool linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void*
 // (dY: n_tok x out_dim, W2: out_dim x F, ug / dug: n_tok x 2F).  False when not applicable.
 bool linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2, int64_t F,
                          const void* ug, void* dug, cudaStream_t stream) {
-  if (!g_fuse || F % 32 != 0 || !aligned16(ug) || !aligned16(dug)) return false;
+  if (!(g_fuse & 1) || F % 32 != 0 || !aligned16(ug) || !aligned16(dug)) return false;
   Args a{};
   a.M = static_cast<int>(n_tok);
   a.N = static_cast<int>(F);
@@ -810,10 +859,13 @@ bool linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const v
   return true;
 }
 
-// Y = X W^T, bf16 out (epi kEpiBf16) -- forward.
-void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
-                void* y, cudaStream_t stream, const void* residual) {
+namespace {
+// Y = X W^T, bf16 out (epi kEpiBf16); `rope` (nullable) adds the rotary epilogue.  Returns the
+// tile width used (the rotary epilogue needs whole heads per half tile).
+void linear_fwd_impl(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
+                     void* y, cudaStream_t stream, const void* residual, const Args* rope) {
   Args a{};
+  if (rope) a = *rope;
   a.M = static_cast<int>(n_tok);
   a.N = static_cast<int>(out_dim);
   a.K = static_cast<int>(in_dim);
@@ -835,6 +887,30 @@ void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int
     const CUtensorMap tb = cached_map(w, in_dim, out_dim, in_dim, 64, 128);
     launch<false, false, 128>(ta, tb, a, stream);
   }
+}
+}  // namespace
+
+void linear_fwd(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
+                void* y, cudaStream_t stream, const void* residual) {
+  linear_fwd_impl(x, n_tok, in_dim, w, out_dim, y, stream, residual, nullptr);
+}
+
+bool linear_fwd_rope(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
+                     void* y, const float2* cs, int seq, int hd, int64_t rope_cols,
+                     cudaStream_t stream) {
+  // every tiling's half tile is 128 columns except the narrow single-CTA one (64)
+  const int half_cols = (out_dim >= 256 || use_pairs(static_cast<int>(n_tok), static_cast<int>(out_dim),
+                                                     static_cast<int>(in_dim), false)) ? 128 : 64;
+  if (!(g_fuse & 2) || !cs || seq <= 0 || (hd != 32 && hd != 64 && hd != 128) || half_cols % hd != 0 ||
+      rope_cols % half_cols != 0 || rope_cols > out_dim || out_dim % 8 != 0 || !aligned16(y))
+    return false;
+  Args r{};
+  r.rope_cs = cs;
+  r.rope_seq = seq;
+  r.rope_hd = hd;
+  r.rope_cols = static_cast<int>(rope_cols);
+  linear_fwd_impl(x, n_tok, in_dim, w, out_dim, y, stream, nullptr, &r);
+  return true;
 }
 
 // dX (+)= dY W -- dgrad; bf16 out.

@@ -22,6 +22,12 @@ bool linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void*
                        void* s, void* ug, cudaStream_t stream);
 bool linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2, int64_t F,
                          const void* ug, void* dug, cudaStream_t stream);
+// Y = X W^T with rotary embedding applied in the epilogue to columns [0, rope_cols) (heads of
+// hd columns, rotate-half pairs; position = row % seq); false: not eligible (run linear_fwd +
+// rope).  Bit-identical to the unfused pair.
+bool linear_fwd_rope(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
+                     void* y, const float2* cs, int seq, int hd, int64_t rope_cols,
+                     cudaStream_t stream);
 void set_fusion(int on);
 }  // namespace tc
 
@@ -106,6 +112,8 @@ void rms_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd,
 void rms_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd,
                 long long rows, int d, long long rb, long long re, float* out, cudaStream_t s);
 void rope_prepare(int seq, int hd, float theta);  // build the cos/sin table (not capturable)
+// the device (cos, sin) table [seq x hd/2] (built on first use)
+const float2* rope_cos_sin(int seq, int hd, float theta);
 void rope(__nv_bfloat16* qkv, long long tokens, int seq, int heads, int hd, int ld, float theta,
           bool backward, cudaStream_t s);
 void swiglu_fwd(const __nv_bfloat16* ug, long long rows, int F, __nv_bfloat16* out, cudaStream_t s);

@@ -266,13 +266,20 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     pe();
     pb(kFwdGemm);
     gemm_work(kFwdGemm, N, QKV, d, 2.0 * N * QKV, 0);
-    tc::linear_fwd(z.a, N, d, P(id(l, 1)), QKV, z.qkv, st);  // wq|wk|wv stacked
+    // wq|wk|wv stacked, RoPE on the q and k heads in the epilogue
+    const bool roped = tc::linear_fwd_rope(
+        z.a, N, d, P(id(l, 1)), QKV, z.qkv,
+        llama::rope_cos_sin(S.seq, S.head_dim, static_cast<float>(S.rope_theta)), S.seq,
+        S.head_dim, Q + KV, st);
+    if (!roped) tc::linear_fwd(z.a, N, d, P(id(l, 1)), QKV, z.qkv, st);
     pe();
     pb(kFwdOther);
-    llama::rope(static_cast<bf16*>(z.qkv), N, S.seq, S.heads, S.head_dim, ld, (float)S.rope_theta,
-                false, st);
-    llama::rope(static_cast<bf16*>(z.qkv) + Q, N, S.seq, S.kv_heads, S.head_dim, ld,
-                (float)S.rope_theta, false, st);
+    if (!roped) {
+      llama::rope(static_cast<bf16*>(z.qkv), N, S.seq, S.heads, S.head_dim, ld,
+                  (float)S.rope_theta, false, st);
+      llama::rope(static_cast<bf16*>(z.qkv) + Q, N, S.seq, S.kv_heads, S.head_dim, ld,
+                  (float)S.rope_theta, false, st);
+    }
     attn_->forward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, z.lse, st);
     pe();
     pb(kFwdGemm);

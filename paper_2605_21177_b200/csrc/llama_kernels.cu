@@ -394,10 +394,12 @@ __global__ void rope_vec_kernel(bf16* qkv, long long tokens, int seq, int heads,
     float y1[8], y2[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
+      // explicit roundings (no FMA contraction): the QKV GEMM epilogue applies the same
+      // rotation bit for bit (gemm_tc.cu rope_epilogue)
       const float2 q = c[e];
       const float sn = sign * q.y;
-      y1[e] = x1[e] * q.x - x2[e] * sn;
-      y2[e] = x2[e] * q.x + x1[e] * sn;
+      y1[e] = __fsub_rn(__fmul_rn(x1[e], q.x), __fmul_rn(x2[e], sn));
+      y2[e] = __fadd_rn(__fmul_rn(x2[e], q.x), __fmul_rn(x1[e], sn));
     }
     *reinterpret_cast<uint4*>(p) = pack8(y1);
     *reinterpret_cast<uint4*>(p + half) = pack8(y2);
@@ -426,6 +428,7 @@ float2* rope_table(int seq, int hd, float theta) {
 }  // namespace
 
 void rope_prepare(int seq, int hd, float theta) { rope_table(seq, hd, theta); }
+const float2* rope_cos_sin(int seq, int hd, float theta) { return rope_table(seq, hd, theta); }
 
 void rope(bf16* qkv, long long tokens, int seq, int heads, int hd, int ld, float theta,
           bool backward, cudaStream_t s) {

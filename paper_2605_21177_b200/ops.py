@@ -183,9 +183,10 @@ def linear_dgrad_swiglu(dy: torch.Tensor, w2: torch.Tensor, ug: torch.Tensor, st
     return dug
 
 
-def set_fusion(enable: bool) -> None:
-    """SwiGLU epilogue fusions in the Llama engine's MLP GEMMs (bit-identical on/off)."""
-    N.check(N.lib.cft_set_fusion(int(enable)))
+def set_fusion(enable) -> None:
+    """Llama-engine epilogue fusions: True/3 all, False/0 none, or a mask (1 SwiGLU, 2 RoPE);
+    results are bit-identical either way."""
+    N.check(N.lib.cft_set_fusion(3 if enable is True else int(enable)))
 
 
 def set_gemm_policy(policy: int) -> None:
