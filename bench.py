@@ -687,6 +687,11 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the N>1 code path on a 1-GPU box (never a timing): every rank on
+    # device 0, host-mediated gloo collectives (no kernel waits on another rank's kernel)
+    check_backend = os.environ.get("CFT_BENCH_DIST_CHECK", "")
+    if check_backend:
+        local_rank = 0
 
     if args.impl == "reference":
         if rank != 0:
@@ -716,7 +721,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if check_backend:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.fusion != 3:
         from paper_2605_21177_b200 import ops
         ops.set_fusion(args.fusion)
