@@ -17,6 +17,10 @@ class Context {
 
   // Build (and cache) the forward and backward graphs for a shape.
   void prepare(int batch, int hq, int hkv, int seq, int head_dim);
+  // Time every engine configuration cuDNN offers for the shape on the given buffers and keep
+  // the fastest forward and backward plan (overwrites the buffers' contents).
+  void autotune(int batch, int hq, int hkv, int seq, int head_dim, void* qkv, void* o,
+                float* stats, void* dout, void* dqkv, cudaStream_t stream);
   // qkv: [batch*seq][(hq + 2 hkv) * head_dim] bf16; o: [batch*seq][hq * head_dim] bf16;
   // stats: [batch][hq][seq] fp32 (row log-sum-exp, saved for the backward).
   void forward(int batch, int hq, int hkv, int seq, int head_dim, const void* qkv, void* o,
