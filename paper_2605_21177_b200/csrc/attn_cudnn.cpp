@@ -98,6 +98,9 @@ Compiled build(cudnnHandle_t h, const Key& k) {
     c.candidates.push_back(i);
     c.workspace = std::max(c.workspace, ws);
   }
+  // with every plan built, execute() would run an arbitrary one: pin the heuristic's first
+  // choice (plan 0) until autotune() finds a clearly faster plan
+  if (!c.candidates.empty()) c.best = c.candidates.front();
   return c;
 }
 
@@ -173,7 +176,7 @@ void Context::autotune(int b, int hq, int hk, int s, int d, void* qkv, void* o, 
     c.best = (best >= 0 && best != c.candidates.front() && default_ms > 0.05f * 3 &&
               best_ms < 0.95f * default_ms)
                  ? best
-                 : -1;
+                 : c.candidates.front();
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

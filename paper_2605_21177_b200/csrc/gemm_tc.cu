@@ -760,7 +760,15 @@ void fill_units(Args& a, int bm, int bn, int slots, double us_per_kb, bool allow
   // 4096-wide GEMMs.
   const int concurrent = std::max(1, slots / a.splits);
   int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(concurrent) * bn / bm)));
-  if (bm == 256) g = (a.tiles_n > 20 || a.K > 8192) ? 16 : 2;
+  static const int g_longk = [] {
+    const char* e = std::getenv("CFT_GEMM_GROUP_LONGK");
+    return e ? std::atoi(e) : 16;
+  }();
+  static const int g_wide = [] {
+    const char* e = std::getenv("CFT_GEMM_GROUP_WIDE");
+    return e ? std::atoi(e) : 16;
+  }();
+  if (bm == 256) g = a.K > 8192 ? g_longk : a.tiles_n > 20 ? g_wide : 2;
   static const int forced = [] {
     const char* e = std::getenv("CFT_GEMM_GROUP_M");  // experiments: fixed group size
     return e ? std::atoi(e) : 0;

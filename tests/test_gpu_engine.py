@@ -315,7 +315,11 @@ def test_llama_sharded_states_match_replicated(cuda):
         ps = [e.params(from_masters=False) for e in engs]
         assert np.array_equal(ps[0], ps[1])
         out[sharded] = ps[0]
-    assert rel(out[True], out[False]) < 1e-3
+    # not bitwise: the fp32 atomics in the step (RMSNorm dgamma, embedding scatter, split-K)
+    # make each run's gradient differ in the last bits, and AdamW's first steps turn those into
+    # +-lr flips for near-zero gradients; a sharding bug (wrong offsets, stale gathers) shows up
+    # as O(1) differences
+    assert rel(out[True], out[False]) < 2e-2
 
 
 CKPT = os.path.join(os.path.dirname(__file__), "golden", "checkpoints.json")
