@@ -250,13 +250,17 @@ int cft_grad_stats(cft_dtype state_dtype, const void* grad, int64_t n, double gr
  *   precond_dev[0..1] receive min/max of 1/(sqrt(vhat)+eps) (float, or double for F64).
  *   zero_grad 1 (fp32 state): the consumed gradient is overwritten with zeros in the same
  *   pass (+4 B/elem), so the next step's wgrad can red-add into it without a memset.
+ *   clip_max_norm > 0: global-norm clipping (the build's addition; the reference has none,
+ *   parity unpinned): the mean gradient is scaled by min(1, clip_max_norm / sqrt(stats_dev[0]))
+ *   on the device -- stats_dev[0] is the chunk's sum g^2 from cft_grad_stats (all-reduced
+ *   first when states are sharded), so no host round trip.  0 = off.
  * state_dtype: CFT_F32 (fp32 master/m/v/grad) or CFT_F64.  param_dtype: CFT_BF16, CFT_F32
  * or CFT_F64. */
 int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void* grad,
                     int64_t n, double grad_scale, const cft_adamw_hyper* hyper, double bc1,
                     double bc2, cft_dtype param_dtype, void* param_base,
                     const cft_segment* segments_dev, int32_t n_segments, const void* stats_dev,
-                    void* precond_dev, int zero_grad, cft_stream_t stream);
+                    void* precond_dev, int zero_grad, double clip_max_norm, cft_stream_t stream);
 
 /* Plain block descent (optimizer.cpp:200-208), same segment write-back. */
 int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t n,
@@ -318,6 +322,8 @@ typedef struct {
   int32_t shard_rank;    /* sharded optimizer state: this rank's index and the */
   int32_t shard_world;   /* number of ranks; 0 or 1 = every rank keeps the whole chunk state */
   int32_t pad_;
+  double clip_max_norm;  /* > 0: clip the chunk's mean gradient to this global L2 norm inside the
+                            fused AdamW (no reference counterpart); 0 = off */
 } cft_engine_config;
 
 /* One micro-batch (model.hpp:52-60).  x / target in the compute dtype; host pointers should

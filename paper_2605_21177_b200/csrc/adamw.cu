@@ -154,8 +154,13 @@ __global__ void __launch_bounds__(kThreads)
                      float* __restrict__ grad, long long n, float gscale, float eta, float b1,
                      float b2, float eps, float wd, float bc1, float bc2, P* __restrict__ param,
                      const cft_segment* __restrict__ segs, int nseg,
-                     const double* __restrict__ stats, float* __restrict__ precond, int zero_grad) {
+                     const double* __restrict__ stats, float* __restrict__ precond, int zero_grad,
+                     double clip) {
   if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
+  if (clip > 0.0 && stats) {  // global-norm clip from the statistics pass, on the device
+    const double nrm = sqrt(stats[0]);
+    if (nrm > clip) gscale = static_cast<float>(static_cast<double>(gscale) * (clip / nrm));
+  }
   __shared__ cft_segment s_segs[kSmemSegs];
   __shared__ float s_min[kThreads / 32], s_max[kThreads / 32];
   const bool in_smem = nseg <= kSmemSegs;
@@ -267,8 +272,12 @@ __global__ void __launch_bounds__(kThreads)
     adamw_f64_kernel(double* master, double* m, double* v, const double* grad, long long n,
                      double gscale, double eta, double b1, double b2, double eps, double wd,
                      double bc1, double bc2, P* param, const cft_segment* segs, int nseg,
-                     const double* stats, double* precond) {
+                     const double* stats, double* precond, double clip) {
   if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
+  if (clip > 0.0 && stats) {
+    const double nrm = __dsqrt_rn(stats[0]);
+    if (nrm > clip) gscale = __dmul_rn(gscale, __ddiv_rn(clip, nrm));
+  }
   double pmin = INFINITY, pmax = 0.0;
   const double omb1 = __dsub_rn(1.0, b1), omb2 = __dsub_rn(1.0, b2);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -380,11 +389,13 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
                     int64_t n, double grad_scale, const cft_adamw_hyper* h, double bc1, double bc2,
                     cft_dtype param_dtype, void* param_base, const cft_segment* segs,
                     int32_t n_segments, const void* stats_dev, void* precond_dev, int zero_grad,
-                    cft_stream_t stream) {
+                    double clip_max_norm, cft_stream_t stream) {
   return cft::guarded([&] {
     auto s = static_cast<cudaStream_t>(stream);
     if (n <= 0) return;
     CFT_CHECK(h != nullptr, "cft_adamw_slice: null hyper");
+    CFT_CHECK(clip_max_norm <= 0.0 || stats_dev != nullptr,
+              "cft_adamw_slice: clipping needs the statistics row (cft_grad_stats)");
     CFT_CHECK(!param_base || (segs && n_segments > 0), "cft_adamw_slice: missing segments");
     const double* st = static_cast<const double*>(stats_dev);
     if (state_dtype == CFT_F32) {
@@ -398,7 +409,7 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
             static_cast<float*>(master), static_cast<float*>(m), static_cast<float*>(v),
             static_cast<float*>(grad), n, (float)grad_scale, (float)h->eta, (float)h->beta1,
             (float)h->beta2, (float)h->epsilon, (float)h->weight_decay, (float)bc1, (float)bc2, p,
-            segs, n_segments, st, static_cast<float*>(precond_dev), zero_grad);
+            segs, n_segments, st, static_cast<float*>(precond_dev), zero_grad, clip_max_norm);
       };
       if (param_dtype == CFT_BF16) go(static_cast<__nv_bfloat16*>(param_base));
       else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));
@@ -409,7 +420,8 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
         adamw_f64_kernel<<<grid, kThreads, 0, s>>>(
             static_cast<double*>(master), static_cast<double*>(m), static_cast<double*>(v),
             static_cast<const double*>(grad), n, grad_scale, h->eta, h->beta1, h->beta2, h->epsilon,
-            h->weight_decay, bc1, bc2, p, segs, n_segments, st, static_cast<double*>(precond_dev));
+            h->weight_decay, bc1, bc2, p, segs, n_segments, st, static_cast<double*>(precond_dev),
+            clip_max_norm);
       };
       if (param_dtype == CFT_F64) go(static_cast<double*>(param_base));
       else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));

@@ -876,7 +876,7 @@ void Engine::step_end() {
       const double bc2 = 1.0 - std::pow(cfg_.hyper.beta2, static_cast<double>(n_local_[c]));
       if (cft_adamw_slice(sdt, master, m, v, grad, gn, scale, &cfg_.hyper, bc1, bc2,
                           static_cast<cft_dtype>(cfg_.dtype), pbase, segs, nseg, st, precond_,
-                          sdt == CFT_F32 ? 1 : 0, s) != CFT_OK)
+                          sdt == CFT_F32 ? 1 : 0, cfg_.clip_max_norm, s) != CFT_OK)
         throw Error(last_error());
     } else {
       if (cft_sgd_slice(sdt, master, grad, gn, scale, cfg_.hyper.eta,

@@ -146,7 +146,7 @@ def grad_stats(grad: torch.Tensor, grad_scale: float = 1.0, stats=None, stream=N
 
 def adamw_slice(master, m, v, grad, hyper, n_local: int, param=None, segments=None,
                 grad_scale: float = 1.0, stats=None, precond=None, zero_grad: bool = False,
-                stream=None):
+                clip_max_norm: float = 0.0, stream=None):
     """One fused AdamW update on a chunk (optimizer.cpp:163-198); n_local already incremented."""
     bc1 = 1.0 - hyper.beta1 ** float(n_local)
     bc2 = 1.0 - hyper.beta2 ** float(n_local)
@@ -156,7 +156,7 @@ def adamw_slice(master, m, v, grad, hyper, n_local: int, param=None, segments=No
                                   grad.data_ptr(), master.numel(), grad_scale, C.byref(h), bc1, bc2,
                                   _dtype(param) if param is not None else N.CFT_F32,
                                   _ptr(param), _ptr(segments), nseg, _ptr(stats), _ptr(precond),
-                                  int(zero_grad), _stream(stream)), "adamw_slice")
+                                  int(zero_grad), float(clip_max_norm), _stream(stream)), "adamw_slice")
 
 
 def linear_fwd_swiglu(x: torch.Tensor, w13: torch.Tensor, keep_ug: bool = True, stream=None):

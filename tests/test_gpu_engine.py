@@ -393,3 +393,55 @@ def test_checkpoint_resume_continues_bit_identically(cuda, tmp_path):
     c = ChunkEngine(model_of(case), np.array(case["init_params"]), bsz, other)
     with pytest.raises(Error, match="plan hash mismatch"):
         c.read_checkpoints(str(tmp_path))
+
+
+@pytest.mark.parametrize("clip_rel", [0.25, 1e6])
+def test_fp64_engine_gradient_clipping(cuda, clip_rel):
+    """Global-norm clipping inside the fused AdamW (the build's addition; the reference has no
+    clip, parity unpinned): the fp64 engine equals a CPU restatement that scales each step's mean
+    gradient by min(1, c / ||g||) before the reference AdamW (oracle arithmetic), to 1e-12; a
+    huge clip leaves the run bit-identical to the reference trajectory."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_dp import OracleEngine
+    from paper_2605_21177_b200 import plan as P
+    from paper_2605_21177_b200.engine import run_training
+    case = CASES["linear_dp2"]
+    gsq0 = case["traj_gsq"][0]
+    clip = clip_rel * gsq0 ** 0.5
+    opts = options_of(case, "fp64")
+    opts.clip_max_norm = clip
+    r = run_training(model_of(case), np.array(case["init_params"]), batches_of(case), opts)
+    if clip_rel > 1e3:
+        assert np.array_equal(r.params, np.array(case["final_params"]))
+        return
+
+    class ClipOracle(OracleEngine):
+        def step_end(self):
+            g = self.grad.numpy() * (self.scale * (1.0 / self.mb))
+            nrm = float(np.sqrt(np.sum(g * g)))
+            if nrm > clip:
+                self.grad = torch.from_numpy(self.grad.numpy() * (clip / nrm))
+            super().step_end()
+
+    layers = case["layers"]
+    tensors = []
+    for li, L in enumerate(layers):
+        tensors.append((f"linear{li}.weight", L[2], L[1]))
+        if L[3]:
+            tensors.append((f"linear{li}.bias", L[2], 1))
+    infos = [P.TensorInfo(i, n, r_, c) for i, (n, r_, c) in enumerate(tensors)]
+    plan = P.partition(infos, case["K"])
+    sched = P.RotationScheduler(P.ScheduleConfig(case["K"], case["T"], case["steps"]), plan)
+    mb = case["micro_batches"]
+    eng = ClipOracle(layers, case["init_params"], plan, sched, tuple(case["hyper"]), mb)
+    bs = batches_of(case)
+    cursor = 0
+    for _ in range(case["steps"]):
+        eng.step_begin()
+        for m in range(mb):
+            eng.forward_backward(bs[cursor], m)
+            cursor = (cursor + 1) % len(bs)
+        eng.step_end()
+    assert rel(r.params, eng.params) < 1e-12
+    assert not np.array_equal(r.params, np.array(case["final_params"]))  # the clip did act
