@@ -656,14 +656,16 @@ def slice_sweep(local_rank):
         s = D // f
         rb = (12376 % D) if f > 1 else 0
         rb = min(rb, D - s)
-        buf = torch.empty(s, D, device=dev)
+        # accumulate into a zeroed fp32 buffer: the engine's path (its gradient accumulator is
+        # kept zero between steps), i.e. the reference's dw += (kernels_serial.cpp:39-49)
+        buf = torch.zeros(s, D, device=dev)
         for _ in range(3):
-            ops.linear_wgrad_slice(dy, x, rb, rb + s, out=buf)
+            ops.linear_wgrad_slice(dy, x, rb, rb + s, out=buf, accumulate=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
         for _ in range(10):
-            ops.linear_wgrad_slice(dy, x, rb, rb + s, out=buf)
+            ops.linear_wgrad_slice(dy, x, rb, rb + s, out=buf, accumulate=True)
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 10

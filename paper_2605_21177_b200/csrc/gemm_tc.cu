@@ -44,6 +44,11 @@ struct Args {
   int row_skip;   // row_begin - m_off: leading tile rows that belong to the previous slice
   int tiles_m, tiles_n, splits, kb_per_split, total_kb, num_units;
   int group_m;    // row-blocks per rasterisation group (see decode_unit)
+  // stream-K (pair kernel, red-add epilogue): > 0 = every CTA pair takes a contiguous run of
+  // sk_len k-blocks of the linearised (tile, k-block) space, cut at tile boundaries into
+  // segments whose partial tiles are red-added -- balanced work for narrow slices where whole
+  // split-K units leave SMs idle in the last wave
+  long long sk_len;
   // SwiGLU fusion (Llama MLP).  glu 1 (forward, pair kernel): B is the stacked [w1; w3] with
   //   w3 at row glu_F; CTA rank 0 stages w1 rows, rank 1 the matching w3 rows, so accumulator
   //   columns [0,128) hold u and [128,256) g for output features tn*128..; the epilogue writes
@@ -85,6 +90,39 @@ __device__ __forceinline__ void decode_unit(const Args& a, int u, int& tm, int& 
   const int rows = min(a.group_m, a.tiles_m - g * a.group_m);
   tm = g * a.group_m + r % rows;
   tn = r / rows;
+}
+
+// The work a CTA pair walks: whole (tile, split) units, or stream-K segments.
+struct WorkIter {
+  int u;
+  long long pos, end;
+};
+__device__ __forceinline__ WorkIter work_begin(const Args& a, int pair) {
+  WorkIter it;
+  it.u = pair;
+  const long long total = static_cast<long long>(a.tiles_m) * a.tiles_n * a.total_kb;
+  it.pos = a.sk_len > 0 ? min(total, pair * a.sk_len) : 0;
+  it.end = a.sk_len > 0 ? min(total, (pair + 1) * a.sk_len) : 0;
+  return it;
+}
+__device__ __forceinline__ bool work_next(const Args& a, WorkIter& it, int npairs, int& tm,
+                                          int& tn, int& kb0, int& kb1) {
+  int sp;
+  if (a.sk_len > 0) {
+    if (it.pos >= it.end) return false;
+    const long long tile = it.pos / a.total_kb;
+    kb0 = static_cast<int>(it.pos - tile * a.total_kb);
+    kb1 = static_cast<int>(min(static_cast<long long>(a.total_kb), kb0 + (it.end - it.pos)));
+    it.pos += kb1 - kb0;
+    decode_unit(a, static_cast<int>(tile), tm, tn, sp);  // splits == 1 in stream-K mode
+    return true;
+  }
+  if (it.u >= a.num_units) return false;
+  decode_unit(a, it.u, tm, tn, sp);
+  kb0 = sp * a.kb_per_split;
+  kb1 = min(kb0 + a.kb_per_split, a.total_kb);
+  it.u += npairs;
+  return true;
 }
 
 // Epilogue store of 16 consecutive accumulator columns of one output row (one thread).
@@ -542,11 +580,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < args.num_units; u += npairs) {
-        int tm, tn, sp;
-        decode_unit(args, u, tm, tn, sp);
-        const int kb0 = sp * args.kb_per_split;
-        const int kb1 = min(kb0 + args.kb_per_split, args.total_kb);
+      WorkIter it = work_begin(args, pair);
+      int tm, tn, kb0, kb1;
+      while (work_next(args, it, npairs, tm, tn, kb0, kb1)) {
         const int m0 = args.m_off + tm * BMP + static_cast<int>(rank) * 128;
         const int n0 = args.glu == 1 ? tn * (BNP / 2) + static_cast<int>(rank) * args.glu_F
                                      : tn * BNP + static_cast<int>(rank) * (BNP / 2);
@@ -583,11 +619,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = pair; u < args.num_units; u += npairs) {
-        int tm, tn, sp;
-        decode_unit(args, u, tm, tn, sp);
-        const int kb0 = sp * args.kb_per_split;
-        const int kb1 = min(kb0 + args.kb_per_split, args.total_kb);
+      WorkIter it = work_begin(args, pair);
+      int tm, tn, kb0, kb1;
+      while (work_next(args, it, npairs, tm, tn, kb0, kb1)) {
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BNP;
@@ -622,9 +656,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                    tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty[1]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = pair; u < args.num_units; u += npairs) {
-      int tm, tn, sp;
-      decode_unit(args, u, tm, tn, sp);
+    WorkIter it = work_begin(args, pair);
+    int tm, tn, kb0_, kb1_;
+    while (work_next(args, it, npairs, tm, tn, kb0_, kb1_)) {
       // one warp polls the accumulator barrier with sleeps, the other epilogue warps park on
       // a named barrier (no issue slots, no wake-ups on every pipeline event)
       if (warp == 2) ptx::mbar_wait_sleep(&tfull[acc], acc_phase, 256);
@@ -970,13 +1004,35 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
     Args a256 = a, a128 = a;
     fill_units(a256, 256, 256, num_sms() / 2, 0.40, true);
     fill_units(a128, 256, 128, num_sms() / 2, 0.38, true);
-    auto cost = [](const Args& x, double us_per_kb) {
+    // measured (tools/probe_wgrad.py): fp32 red.add of partial outputs sustains ~1.2 TB/s
+    // chip-wide and is largely exposed for these short kernels, so every pass over the output
+    // (one per split, one per stream-K segment) is charged
+    constexpr double kRedBytesPerUs = 1.2e6;
+    auto cost = [&](const Args& x, double us_per_kb) {
       const int waves = (x.num_units + num_sms() / 2 - 1) / (num_sms() / 2);
       double t = waves * x.kb_per_split * us_per_kb;
-      if (x.splits > 1) t += (x.splits + 1) * static_cast<double>(x.M) * x.N * 4.0 / 2.0e6;
+      t += x.splits * static_cast<double>(x.M) * x.N * 4.0 / kRedBytesPerUs;
       return t;
     };
-    if (g_policy == 0 && cost(a128, 0.38) < cost(a256, 0.40)) {
+    // stream-K over 256x256 tiles: every pair gets ceil(W / pairs) k-blocks of the linearised
+    // (tile, k-block) space; partial tiles (about one per pair boundary) are red-added
+    Args ask = a;
+    fill_units(ask, 256, 256, num_sms() / 2, 0.40, false);
+    const int P = num_sms() / 2;
+    const long long W = static_cast<long long>(ask.tiles_m) * ask.tiles_n * ask.total_kb;
+    ask.sk_len = (W + P - 1) / P;
+    ask.num_units = static_cast<int>(std::min<long long>(P, (W + ask.sk_len - 1) / ask.sk_len));
+    const double segs = static_cast<double>(ask.tiles_m) * ask.tiles_n + ask.num_units - 1;
+    const double cost_sk = ask.sk_len * 0.40 + segs * 256.0 * 256.0 * 4.0 / kRedBytesPerUs;
+    static const int sk_mode = [] {  // experiments: 1 force stream-K, 2 never
+      const char* e = std::getenv("CFT_WGRAD_STREAMK");
+      return e ? std::atoi(e) : 0;
+    }();
+    const double c128 = cost(a128, 0.38), c256 = cost(a256, 0.40);
+    if (g_policy == 0 && sk_mode != 2 &&
+        (sk_mode == 1 || cost_sk < 0.95 * std::min(c128, c256))) {
+      a = ask;
+    } else if (g_policy == 0 && c128 < c256) {
       a = a128;
       pair_bn = 128;
     } else {
@@ -989,7 +1045,7 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
     // dw += result: fire-and-forget red.add for any split count (the engine keeps its
     // gradient accumulator zeroed between steps, so this is also its overwrite path)
     a.epi = kEpiF32Red;
-  } else if (a.splits > 1) {
+  } else if (a.splits > 1 || a.sk_len > 0) {
     // partial sums race into dw: zero it first
     CFT_CUDA(cudaMemset2DAsync(dw, sizeof(float) * in_dim, 0, sizeof(float) * in_dim, a.M,
                                stream));
