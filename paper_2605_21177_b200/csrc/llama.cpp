@@ -283,12 +283,9 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     if (!roped) tc::linear_fwd(z.a, N, d, P(id(l, 1)), QKV, z.qkv, st);
     pe();
     pb(kFwdOther);
-    if (!roped) {
-      llama::rope(static_cast<bf16*>(z.qkv), N, S.seq, S.heads, S.head_dim, ld,
+    if (!roped)
+      llama::rope(static_cast<bf16*>(z.qkv), N, S.seq, S.heads + S.kv_heads, S.head_dim, ld,
                   (float)S.rope_theta, false, st);
-      llama::rope(static_cast<bf16*>(z.qkv) + Q, N, S.seq, S.kv_heads, S.head_dim, ld,
-                  (float)S.rope_theta, false, st);
-    }
     attn_->forward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, z.lse, st);
     pe();
     pb(kFwdGemm);
@@ -398,9 +395,8 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     pe();
     pb(kBwdOther);
     attn_->backward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, l_do_, z.lse, l_dqkv_, st);
-    llama::rope(static_cast<bf16*>(l_dqkv_), N, S.seq, S.heads, S.head_dim, ld, (float)S.rope_theta,
-                true, st);
-    llama::rope(static_cast<bf16*>(l_dqkv_) + Q, N, S.seq, S.kv_heads, S.head_dim, ld,
+    // q and k heads are adjacent in the fused row: one inverse-rotation launch covers both
+    llama::rope(static_cast<bf16*>(l_dqkv_), N, S.seq, S.heads + S.kv_heads, S.head_dim, ld,
                 (float)S.rope_theta, true, st);
     pe();
     wgrad(id(l, 1), l_dqkv_, QKV, z.a, d, 0);
