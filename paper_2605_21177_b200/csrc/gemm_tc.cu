@@ -164,7 +164,30 @@ __device__ __forceinline__ void store16(const Args& args, long long rbase, int c
                : (args.epi == kEpiBf16Add ? out : nullptr);
     const bool vec = full16 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(res) & 15) == 0);
-    if (vec) {
+    const bool v32 = full16 && (((reinterpret_cast<uintptr_t>(out) |
+                                  reinterpret_cast<uintptr_t>(res)) & 31) == 0);
+    if (v32) {  // one 32-byte sector per thread: 256-bit load of the residual, 256-bit store
+      uint32_t w[8];
+      if (res) {
+        uint32_t old[8];
+        ptx::ld_global_256(res, old);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float2 of = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&old[q]));
+          __nv_bfloat162 v = __floats2bfloat162_rn(of.x + __uint_as_float(r[2 * q]),
+                                                   of.y + __uint_as_float(r[2 * q + 1]));
+          w[q] = *reinterpret_cast<uint32_t*>(&v);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[2 * q]),
+                                                   __uint_as_float(r[2 * q + 1]));
+          w[q] = *reinterpret_cast<uint32_t*>(&v);
+        }
+      }
+      ptx::st_global_256(out, w);
+    } else if (vec) {
 #pragma unroll
       for (int j = 0; j < 16; j += 8) {
         uint4 pk;
@@ -226,6 +249,22 @@ __device__ __forceinline__ void unpack8_bf16(const uint4& pk, float* f) {
   }
 }
 
+// 16 bf16 values from floats: one 256-bit store when 32-byte aligned, else two 128-bit ones
+__device__ __forceinline__ void store16_bf16(__nv_bfloat16* p, const float* f) {
+  if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      __nv_bfloat162 v = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
+      w[q] = *reinterpret_cast<uint32_t*>(&v);
+    }
+    ptx::st_global_256(p, w);
+  } else {
+    reinterpret_cast<uint4*>(p)[0] = pack8_bf16(f);
+    reinterpret_cast<uint4*>(p)[1] = pack8_bf16(f + 8);
+  }
+}
+
 // glu 1: 16 output features of one row from the u / g accumulator columns (F % 128 == 0, so a
 // chunk is never partial).  Same math as swiglu_fwd_kernel on the bf16-rounded u, g.
 __device__ __forceinline__ void glu_fwd_store16(const Args& args, long long row, int col,
@@ -239,15 +278,11 @@ __device__ __forceinline__ void glu_fwd_store16(const Args& args, long long row,
     g[j] = bf16_round(__uint_as_float(rg[j]));
     o[j] = u[j] * glu_sigm(u[j]) * g[j];
   }
-  uint4* out = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + row * F + col);
-  out[0] = pack8_bf16(o);
-  out[1] = pack8_bf16(o + 8);
+  store16_bf16(static_cast<__nv_bfloat16*>(args.C) + row * F + col, o);
   if (args.glu_ug) {
     __nv_bfloat16* ug = static_cast<__nv_bfloat16*>(args.glu_ug) + row * 2 * F + col;
-    reinterpret_cast<uint4*>(ug)[0] = pack8_bf16(u);
-    reinterpret_cast<uint4*>(ug)[1] = pack8_bf16(u + 8);
-    reinterpret_cast<uint4*>(ug + F)[0] = pack8_bf16(g);
-    reinterpret_cast<uint4*>(ug + F)[1] = pack8_bf16(g + 8);
+    store16_bf16(ug, u);
+    store16_bf16(ug + F, g);
   }
 }
 
@@ -258,19 +293,20 @@ __device__ __forceinline__ void glu_fwd_store16(const Args& args, long long row,
 template <int BN>
 __device__ __forceinline__ void glu_bwd_epilogue(const Args& args, uint32_t tacc, int row,
                                                  bool row_ok, int tn, int c0, int c1) {
+  // (F % 32 == 0 and 256-byte aligned buffers, checked by the host: every 32-feature chunk of u,
+  // g, du, dg is two 32-byte sectors -> 256-bit streaming loads / stores)
   const long long F = args.glu_F;
   const __nv_bfloat16* ugr =
       static_cast<const __nv_bfloat16*>(args.glu_ug) + static_cast<long long>(row) * 2 * F;
   __nv_bfloat16* outr = static_cast<__nv_bfloat16*>(args.C) + static_cast<long long>(row) * 2 * F;
-  uint4 cu[4], cg[4], nu[4], ng[4];
-  auto load = [&](int c, uint4 (&U)[4], uint4 (&G)[4]) {
+  uint32_t cu[16], cg[16], nu[16], ng[16];
+  auto load = [&](int c, uint32_t (&U)[16], uint32_t (&G)[16]) {
     const int col = tn * BN + c;
     if (row_ok && col < args.N) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {  // streaming: keep the GEMM operands in L2
-        U[i] = __ldcs(reinterpret_cast<const uint4*>(ugr + col) + i);
-        G[i] = __ldcs(reinterpret_cast<const uint4*>(ugr + F + col) + i);
-      }
+      ptx::ld_global_cs_256(ugr + col, *reinterpret_cast<uint32_t(*)[8]>(U));
+      ptx::ld_global_cs_256(ugr + col + 16, *reinterpret_cast<uint32_t(*)[8]>(U + 8));
+      ptx::ld_global_cs_256(ugr + F + col, *reinterpret_cast<uint32_t(*)[8]>(G));
+      ptx::ld_global_cs_256(ugr + F + col + 16, *reinterpret_cast<uint32_t(*)[8]>(G + 8));
     }
   };
   load(c0, cu, cg);
@@ -284,23 +320,32 @@ __device__ __forceinline__ void glu_bwd_epilogue(const Args& args, uint32_t tacc
     const int col = tn * BN + c;
     if (row_ok && col < args.N) {
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        float u[8], g[8], du[8], dg[8];
-        unpack8_bf16(cu[h], u);
-        unpack8_bf16(cg[h], g);
+      for (int h = 0; h < 2; ++h) {  // 16 features per half: one sector of du and one of dg
+        uint32_t wdu[8], wdg[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float d = bf16_round(__uint_as_float(r[8 * h + j]));
-          const float sg = glu_sigm(u[j]);
-          du[j] = d * g[j] * sg * (1.f + u[j] * (1.f - sg));
-          dg[j] = d * u[j] * sg;
+        for (int q = 0; q < 8; ++q) {
+          const float2 u2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cu[8 * h + q]));
+          const float2 g2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cg[8 * h + q]));
+          float du[2], dg[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float u = e ? u2.y : u2.x, g = e ? g2.y : g2.x;
+            const float d = bf16_round(__uint_as_float(r[16 * h + 2 * q + e]));
+            const float sg = glu_sigm(u);
+            du[e] = d * g * sg * (1.f + u * (1.f - sg));
+            dg[e] = d * u * sg;
+          }
+          __nv_bfloat162 a = __floats2bfloat162_rn(du[0], du[1]);
+          __nv_bfloat162 b = __floats2bfloat162_rn(dg[0], dg[1]);
+          wdu[q] = *reinterpret_cast<uint32_t*>(&a);
+          wdg[q] = *reinterpret_cast<uint32_t*>(&b);
         }
-        __stcs(reinterpret_cast<uint4*>(outr + col) + h, pack8_bf16(du));
-        __stcs(reinterpret_cast<uint4*>(outr + F + col) + h, pack8_bf16(dg));
+        ptx::st_global_cs_256(outr + col + 16 * h, wdu);
+        ptx::st_global_cs_256(outr + F + col + 16 * h, wdg);
       }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 16; ++i) {
       cu[i] = nu[i];
       cg[i] = ng[i];
     }
@@ -338,12 +383,8 @@ __device__ __forceinline__ void rope_epilogue(const Args& args, uint32_t tacc, i
           y2[e] = __fadd_rn(__fmul_rn(x2, co), __fmul_rn(x1, sn));
         }
       }
-      uint4* p1 = reinterpret_cast<uint4*>(out + colbase + hs + c);
-      uint4* p2 = reinterpret_cast<uint4*>(out + colbase + hs + hh + c);
-      p1[0] = pack8_bf16(y1);
-      p1[1] = pack8_bf16(y1 + 8);
-      p2[0] = pack8_bf16(y2);
-      p2[1] = pack8_bf16(y2 + 8);
+      store16_bf16(out + colbase + hs + c, y1);
+      store16_bf16(out + colbase + hs + hh + c, y2);
     }
   }
 }
@@ -875,7 +916,9 @@ bool linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void*
 // (dY: n_tok x out_dim, W2: out_dim x F, ug / dug: n_tok x 2F).  False when not applicable.
 bool linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2, int64_t F,
                          const void* ug, void* dug, cudaStream_t stream) {
-  if (!(g_fuse & 1) || F % 32 != 0 || !aligned16(ug) || !aligned16(dug)) return false;
+  if (!(g_fuse & 1) || F % 32 != 0 || ((reinterpret_cast<uintptr_t>(ug) |
+                                          reinterpret_cast<uintptr_t>(dug)) & 31) != 0)
+    return false;
   Args a{};
   a.M = static_cast<int>(n_tok);
   a.N = static_cast<int>(F);
