@@ -216,6 +216,16 @@ int cft_embedding_scatter_slice(cft_dtype dtype, const void* dy, int64_t dim,
                                 int64_t row_end, void* dtable_slice, int64_t* matched_dev,
                                 cft_stream_t stream);
 
+/* Softmax cross-entropy over rows (eval_loss softmax_ce, autodiff.cpp:205-225):
+ *   loss_dev[0] += mean over rows of -log softmax(y[r])[labels[r]]  (fp64 accumulator)
+ *   dy[r, c] = (softmax(y[r])[c] - [c == labels[r]]) / rows          (dy may alias y)
+ * Rows whose label is outside [0, cols) are skipped (dy untouched) and counted in
+ * bad_label_dev[0] (uint64), the device-side form of the reference's throw.  dtype BF16
+ * (the 128k-vocabulary path: one HBM read + one write per logit) or F32. */
+int cft_softmax_ce(cft_dtype dtype, const void* y, const int32_t* labels, int64_t rows,
+                   int64_t cols, void* dy, double* loss_dev, uint64_t* bad_label_dev,
+                   cft_stream_t stream);
+
 /* Hyper-parameters (AdamWHyper, optimizer.hpp:15-22). */
 typedef struct {
   double eta;

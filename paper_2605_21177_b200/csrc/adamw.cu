@@ -15,8 +15,11 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "cft_common.h"
+#include "tc_ptx.cuh"
 
 namespace cft::opt {
 
@@ -56,7 +59,7 @@ __global__ void __launch_bounds__(kThreads) grad_stats_kernel(const T* __restric
   unsigned nbad = 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   if constexpr (std::is_same_v<T, float>) {
-    const long long n4 = n / 4;
+    const long long n4 = (reinterpret_cast<uintptr_t>(g) & 15) == 0 ? n / 4 : 0;
     const float4* g4 = reinterpret_cast<const float4*>(g);
     const float fs = static_cast<float>(scale);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -174,7 +177,9 @@ __global__ void __launch_bounds__(kThreads)
   const float inv_bc1 = 1.f / bc1, inv_bc2 = 1.f / bc2;
   float pmin = INFINITY, pmax = 0.f;
   const long long n4 = (n + 3) / 4;
-  const bool vec_ok = (n % 4) == 0;
+  const bool vec_ok = (n % 4) == 0 &&
+                      ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(m) |
+                        reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long q0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; q0 < n4;
        q0 += kGroups * stride) {
@@ -257,6 +262,184 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int i = 1; i < kThreads / 32; ++i) {
+        pmin = fminf(pmin, s_min[i]);
+        pmax = fmaxf(pmax, s_max[i]);
+      }
+      if (pmax > 0.f) {
+        atomic_min_pos(&precond[0], pmin);
+        atomic_max_pos(&precond[1], pmax);
+      }
+    }
+  }
+}
+
+// ---- fp32-state AdamW, TMA-staged: the same per-element arithmetic as adamw_f32_kernel, but
+// the four input streams (g, m, v, master) arrive through 1-D bulk copies into a ring of
+// shared-memory stages, so each SM keeps kBulkStages x 32 KB of loads in flight regardless of
+// what its compute warps are doing.  One producer lane per CTA (warp kBulkWarps) walks the
+// CTA's tiles; eight consumer warps read a stage (conflict-free float4 LDS), update, and store
+// m, v, master, the zeroed gradient and the bf16 parameter straight from registers (stores
+// need no latency hiding).  Persistent grid: one CTA per SM.  Needs 16-byte-aligned state
+// arrays (the engine's slots and shards are); the register kernel covers anything else. ----
+// (in-step the SM clock sits at ~1.3 GHz under the power cap: 8 consumer warps ran
+// 5.2 TB/s alone at 1.95 GHz but fell to 3.5 TB/s in the step -- the per-tile dependent chain
+// LDS -> update -> STG needs more warps in flight, so 16 consumer warps, one float4 each)
+constexpr int kBulkWarps = 16;                     // consumer warps
+constexpr int kBulkGroups = 1;                     // float4 groups per consumer thread per tile
+constexpr int kBulkThreads = (kBulkWarps + 1) * 32;
+constexpr int kBulkTile = kBulkWarps * 32 * 4 * kBulkGroups;  // elements per stage
+constexpr int kBulkStages = 6;
+constexpr int kBulkSegs = 512;
+constexpr size_t kBulkSmem =
+    (size_t)kBulkStages * 4 * kBulkTile * sizeof(float) + 2 * kBulkStages * sizeof(uint64_t) +
+    kBulkSegs * sizeof(cft_segment);
+
+template <typename P>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    adamw_f32_bulk_kernel(float* __restrict__ master, float* __restrict__ m,
+                          float* __restrict__ v, float* __restrict__ grad, long long n,
+                          float gscale, float eta, float b1, float b2, float eps, float wd,
+                          float bc1, float bc2, P* __restrict__ param,
+                          const cft_segment* __restrict__ segs, int nseg,
+                          const double* __restrict__ stats, float* __restrict__ precond,
+                          int zero_grad, double clip) {
+  using namespace cft::ptx;
+  if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
+  if (clip > 0.0 && stats) {
+    const double nrm = sqrt(stats[0]);
+    if (nrm > clip) gscale = static_cast<float>(static_cast<double>(gscale) * (clip / nrm));
+  }
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);  // [stage][g, m, v, w][kBulkTile]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)kBulkStages * 4 * kBulkTile);
+  uint64_t* empty = full + kBulkStages;
+  cft_segment* s_segs = reinterpret_cast<cft_segment*>(empty + kBulkStages);
+  __shared__ float s_min[kBulkWarps], s_max[kBulkWarps];
+
+  const bool in_smem = nseg <= kBulkSegs;
+  if (in_smem)
+    for (int i = threadIdx.x; i < nseg; i += blockDim.x) s_segs[i] = segs[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBulkStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBulkWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const long long ntiles = (n + kBulkTile - 1) / kBulkTile;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+
+  if (warp == kBulkWarps) {  // producer
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      int it = 0;
+      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it % kBulkStages;
+        mbar_wait(&empty[s], ((it / kBulkStages) & 1) ^ 1);
+        const long long e0 = t * kBulkTile;
+        const long long cnt = min((long long)kBulkTile, n - e0);
+        const uint32_t bytes = static_cast<uint32_t>(cnt / 4) * 16u;
+        if (bytes == 0) {
+          mbar_arrive(&full[s]);
+          continue;
+        }
+        mbar_expect_tx(&full[s], 4 * bytes);
+        float* st = ring + (size_t)s * 4 * kBulkTile;
+        bulk_load_1d(st, grad + e0, bytes, &full[s], pol);
+        bulk_load_1d(st + kBulkTile, m + e0, bytes, &full[s], pol);
+        bulk_load_1d(st + 2 * kBulkTile, v + e0, bytes, &full[s], pol);
+        bulk_load_1d(st + 3 * kBulkTile, master + e0, bytes, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  const cft_segment* sg = in_smem ? s_segs : segs;
+  const float omb1 = 1.f - b1, omb2 = 1.f - b2;
+  const float inv_bc1 = 1.f / bc1, inv_bc2 = 1.f / bc2;
+  float pmin = INFINITY, pmax = 0.f;
+  int it = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % kBulkStages;
+    mbar_wait(&full[s], (it / kBulkStages) & 1);
+    const long long e0 = t * kBulkTile;
+    const long long cnt = min((long long)kBulkTile, n - e0);
+    const long long full4 = cnt / 4;  // groups delivered by the bulk copy
+    const float* st = ring + (size_t)s * 4 * kBulkTile;
+#pragma unroll
+    for (int k = 0; k < kBulkGroups; ++k) {
+      const int q = threadIdx.x + k * kBulkWarps * 32;
+      if (4LL * q >= cnt) break;
+      const long long i0 = e0 + 4LL * q;
+      float g[4], mm[4], vv[4], w[4];
+      if (q < full4) {
+        const float4 g4 = reinterpret_cast<const float4*>(st)[q];
+        const float4 m4 = reinterpret_cast<const float4*>(st + kBulkTile)[q];
+        const float4 v4 = reinterpret_cast<const float4*>(st + 2 * kBulkTile)[q];
+        const float4 w4 = reinterpret_cast<const float4*>(st + 3 * kBulkTile)[q];
+        g[0] = g4.x; g[1] = g4.y; g[2] = g4.z; g[3] = g4.w;
+        mm[0] = m4.x; mm[1] = m4.y; mm[2] = m4.z; mm[3] = m4.w;
+        vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
+        w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+      } else {  // the last 1-3 elements of the chunk: straight from global
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const long long i = i0 + e;
+          g[e] = i < n ? grad[i] : 0.f;
+          mm[e] = i < n ? m[i] : 0.f;
+          vv[e] = i < n ? v[i] : 0.f;
+          w[e] = i < n ? master[i] : 0.f;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float ge = g[e] * gscale;
+        mm[e] = b1 * mm[e] + omb1 * ge;
+        vv[e] = b2 * vv[e] + omb2 * ge * ge;
+        const float mhat = mm[e] * inv_bc1;
+        const float vhat = vv[e] * inv_bc2;
+        const float pc = __frcp_rn(sqrtf(vhat) + eps);
+        w[e] = w[e] - eta * (mhat * pc + wd * w[e]);
+        if (i0 + e < n) {
+          pmin = fminf(pmin, pc);
+          pmax = fmaxf(pmax, pc);
+        }
+      }
+      if (q < full4) {
+        __stcs(reinterpret_cast<float4*>(m + i0), make_float4(mm[0], mm[1], mm[2], mm[3]));
+        __stcs(reinterpret_cast<float4*>(v + i0), make_float4(vv[0], vv[1], vv[2], vv[3]));
+        __stcs(reinterpret_cast<float4*>(master + i0), make_float4(w[0], w[1], w[2], w[3]));
+        if (zero_grad) __stcs(reinterpret_cast<float4*>(grad + i0), make_float4(0.f, 0.f, 0.f, 0.f));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const long long i = i0 + e;
+          if (i < n) {
+            m[i] = mm[e];
+            v[i] = vv[e];
+            master[i] = w[e];
+            if (zero_grad) grad[i] = 0.f;
+          }
+        }
+      }
+      if (param) write_back4(param, sg, nseg, i0, n, w);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (precond) {
+    for (int o = 16; o > 0; o >>= 1) {
+      pmin = fminf(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+      pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+    }
+    if (lane == 0) {
+      s_min[warp] = pmin;
+      s_max[warp] = pmax;
+    }
+    named_bar_sync(1, kBulkWarps * 32);
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < kBulkWarps; ++i) {
         pmin = fminf(pmin, s_min[i]);
         pmax = fmaxf(pmax, s_max[i]);
       }
@@ -358,6 +541,15 @@ __global__ void convert_kernel(const S* src, D* dst, long long n) {
   }
 }
 
+// CFT_ADAMW_KERNEL=reg selects the register kernel everywhere (A/B experiments)
+inline bool adamw_bulk_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CFT_ADAMW_KERNEL");
+    return !(e && std::string(e) == "reg");
+  }();
+  return on;
+}
+
 inline int grid_for(long long work) {
   const long long cap = (long long)num_sms() * 8;
   return static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (work + kThreads - 1) / kThreads)));
@@ -400,7 +592,30 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
               "cft_adamw_slice: clipping needs the statistics row (cft_grad_stats)");
     CFT_CHECK(!param_base || (segs && n_segments > 0), "cft_adamw_slice: missing segments");
     const double* st = static_cast<const double*>(stats_dev);
-    if (state_dtype == CFT_F32) {
+    const auto aligned16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (state_dtype == CFT_F32 && adamw_bulk_enabled() && n >= kBulkTile &&
+        aligned16(master) && aligned16(m) && aligned16(v) && aligned16(grad)) {
+      const long long tiles = (n + kBulkTile - 1) / kBulkTile;
+      const int grid = static_cast<int>(std::min<long long>(tiles, cft::num_sms()));
+      auto go = [&](auto* p) {
+        using PT = std::remove_pointer_t<decltype(p)>;
+        static bool attr = [] {
+          CFT_CUDA(cudaFuncSetAttribute(adamw_f32_bulk_kernel<PT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kBulkSmem));
+          return true;
+        }();
+        (void)attr;
+        adamw_f32_bulk_kernel<<<grid, kBulkThreads, kBulkSmem, s>>>(
+            static_cast<float*>(master), static_cast<float*>(m), static_cast<float*>(v),
+            static_cast<float*>(grad), n, (float)grad_scale, (float)h->eta, (float)h->beta1,
+            (float)h->beta2, (float)h->epsilon, (float)h->weight_decay, (float)bc1, (float)bc2, p,
+            segs, n_segments, st, static_cast<float*>(precond_dev), zero_grad, clip_max_norm);
+      };
+      if (param_dtype == CFT_BF16) go(static_cast<__nv_bfloat16*>(param_base));
+      else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));
+      else throw cft::Error("cft_adamw_slice: fp32 state needs BF16 or F32 params");
+    } else if (state_dtype == CFT_F32) {
       // one pass: every thread owns kGroups float4 groups (no grid-stride tail for sizes up
       // to num_sms * 16 blocks)
       const long long groups = (n + 3) / 4;

@@ -7,8 +7,11 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "cft_common.h"
+#include "tc_ptx.cuh"
 
 namespace cft::layers {
 
@@ -278,6 +281,139 @@ __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels
   if (threadIdx.x == 0) atomicAdd(loss, static_cast<double>(-(ylab - logz)) * inv_rows);
 }
 
+// Softmax cross-entropy with the row held on chip: a cluster of kCeCluster CTAs owns one
+// row at a time, each CTA a contiguous part of <= kCePart columns that a 1-D bulk copy (TMA)
+// brings into shared memory.  Each CTA reduces its part to an online (max, sum-exp) pair,
+// the cluster exchanges the pairs through distributed shared memory, and every CTA writes
+// its part of dlogits from shared memory -- so HBM sees exactly one read and one write of
+// each logit (the two-pass kernel above re-reads a 256 KB row that no longer sits in L2 at
+// full occupancy).  Two stages per CTA: row r+1 streams in while row r is reduced/written.
+// The row may be overwritten in place (dy == y): the label logit is read from shared memory.
+constexpr int kCeCluster = 4;
+constexpr int kCeThreads = 512;
+constexpr int kCePart = 32768;  // bf16 columns per CTA and stage (64 KB)
+constexpr size_t kCeSmem = 2ull * kCePart * sizeof(__nv_bfloat16);
+
+__global__ void __cluster_dims__(kCeCluster, 1, 1) __launch_bounds__(kCeThreads, 1)
+    loss_ce_cluster_kernel(const __nv_bfloat16* y, const int32_t* labels, long long rows,
+                           long long cols, int part, float inv_rows, __nv_bfloat16* dy,
+                           double* loss, unsigned long long* bad_label) {
+  using namespace cft::ptx;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[2];
+  __shared__ float2 slot[2];  // this CTA's (max, sum) of the row in flight, by row parity
+  __shared__ float sm[32], ss[32];
+  const uint32_t rank = cluster_ctarank();
+  const long long cid = blockIdx.x / kCeCluster, ncl = gridDim.x / kCeCluster;
+  const long long c0 = (long long)rank * part;
+  const int my = static_cast<int>(max(0LL, min((long long)part, cols - c0)));  // % 8 == 0
+  __nv_bfloat16* buf0 = reinterpret_cast<__nv_bfloat16*>(smem);
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  uint64_t pol = 0;
+  auto issue = [&](long long r, int b) {
+    if (my > 0) {
+      mbar_expect_tx(&full[b], static_cast<uint32_t>(my) * 2u);
+      bulk_load_1d(buf0 + (size_t)b * kCePart, y + r * cols + c0, static_cast<uint32_t>(my) * 2u,
+                   &full[b], pol);
+    } else {
+      mbar_arrive(&full[b]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    pol = l2_policy_evict_first();
+    if (cid < rows) issue(cid, 0);
+    if (cid + ncl < rows) issue(cid + ncl, 1);
+  }
+  const int nv = my / 8;
+  int it = 0;
+  for (long long r = cid; r < rows; r += ncl, ++it) {
+    const int b = it & 1;
+    mbar_wait(&full[b], (it >> 1) & 1);
+    const __nv_bfloat16* row = buf0 + (size_t)b * kCePart;
+    float m = -INFINITY, s = 0.f;
+    for (int j = threadIdx.x; j < nv; j += kCeThreads) {
+      const uint4 u = reinterpret_cast<const uint4*>(row)[j];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(h[q]);
+        v[2 * q] = f.x;
+        v[2 * q + 1] = f.y;
+      }
+      float lm = v[0];
+#pragma unroll
+      for (int e = 1; e < 8; ++e) lm = fmaxf(lm, v[e]);
+      float ls = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ls += __expf(v[e] - lm);
+      online_merge(m, s, lm, ls);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      online_merge(m, s, m2, s2);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sm[threadIdx.x / 32] = m;
+      ss[threadIdx.x / 32] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      m = -INFINITY;
+      s = 0.f;
+      for (int i = 0; i < kCeThreads / 32; ++i) online_merge(m, s, sm[i], ss[i]);
+      slot[b] = make_float2(m, s);
+    }
+    cluster_sync();  // every CTA's pair for row r is visible cluster-wide
+    m = -INFINITY;
+    s = 0.f;
+    const uint32_t my_slot = smem_u32(&slot[b]);
+#pragma unroll
+    for (int k = 0; k < kCeCluster; ++k) {  // same order in every CTA -> same logZ
+      float2 p;
+      asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];"
+                   : "=f"(p.x), "=f"(p.y)
+                   : "r"(mapa(my_slot, k)));
+      online_merge(m, s, p.x, p.y);
+    }
+    const float logz = m + logf(s);
+    const int label = labels[r];
+    if (label < 0 || label >= cols) {
+      if (rank == 0 && threadIdx.x == 0) atomicAdd(bad_label, 1ull);
+    } else {
+      __nv_bfloat16* out = dy + r * cols + c0;
+      for (int j = threadIdx.x; j < nv; j += kCeThreads) {
+        const uint4 u = reinterpret_cast<const uint4*>(row)[j];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+        uint4 o;
+        __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(h[q]);
+          const long long c = c0 + 8 * j + 2 * q;
+          const float p0 = __expf(f.x - logz) - (c == label ? 1.f : 0.f);
+          const float p1 = __expf(f.y - logz) - (c + 1 == label ? 1.f : 0.f);
+          oh[q] = __floats2bfloat162_rn(p0 * inv_rows, p1 * inv_rows);
+        }
+        __stcs(reinterpret_cast<uint4*>(out) + j, o);
+      }
+      if (threadIdx.x == 0 && label >= c0 && label < c0 + my) {
+        const float ylab = __bfloat162float(row[label - c0]);
+        atomicAdd(loss, static_cast<double>(-(ylab - logz)) * inv_rows);
+      }
+    }
+    __syncthreads();  // every thread is done with this stage
+    if (threadIdx.x == 0 && r + 2 * ncl < rows) issue(r + 2 * ncl, b);
+  }
+  cluster_sync();  // peers may still read this CTA's slot
+}
+
 // fp64 losses for the fp64 engine path (exp/log are CUDA's: <= 1-2 ulp from glibc).
 __global__ void loss_elem_f64_kernel(int kind, const double* y, const double* target, long long n,
                                      double* dy, double* partial) {
@@ -373,8 +509,32 @@ void loss(int kind, const T* y, const T* target, const int32_t* labels, long lon
           long long cols, T* dy, double* loss_acc, unsigned long long* bad_label, cudaStream_t s) {
   if (kind == 3) {
     if constexpr (std::is_same_v<T, __nv_bfloat16>) {
-      if (cols % 8 == 0 &&
-          ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0) {
+      const bool vec = cols % 8 == 0 &&
+          ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0;
+      static const bool cluster_on = [] {  // CFT_CE_KERNEL=vec: two-pass kernel (A/B runs)
+        const char* e = std::getenv("CFT_CE_KERNEL");
+        return !(e && std::string(e) == "vec");
+      }();
+      if (vec && cluster_on && rows >= kCeCluster && cols <= (long long)kCeCluster * kCePart) {
+        static int max_clusters = [] {
+          CFT_CUDA(cudaFuncSetAttribute(loss_ce_cluster_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCeSmem));
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(kCeCluster * num_sms());
+          cfg.blockDim = dim3(kCeThreads);
+          cfg.dynamicSmemBytes = kCeSmem;
+          int n = 0;
+          CFT_CUDA(cudaOccupancyMaxActiveClusters(&n, loss_ce_cluster_kernel, &cfg));
+          return std::max(1, n);
+        }();
+        const int part = static_cast<int>(((cols + kCeCluster - 1) / kCeCluster + 7) / 8 * 8);
+        const long long ncl = std::min<long long>(rows, max_clusters);
+        loss_ce_cluster_kernel<<<(unsigned)(ncl * kCeCluster), kCeThreads, kCeSmem, s>>>(
+            y, labels, rows, cols, part, 1.f / rows, dy, loss_acc, bad_label);
+        check_launch("loss_ce_cluster");
+        return;
+      }
+      if (vec) {
         loss_ce_vec_kernel<<<(unsigned)rows, 512, 0, s>>>(y, labels, cols, 1.f / rows, dy, loss_acc,
                                                           bad_label);
         check_launch("loss_ce_vec");

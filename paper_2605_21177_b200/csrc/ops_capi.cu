@@ -8,6 +8,7 @@
 #include <algorithm>
 
 #include "cft_common.h"
+#include "kernels.h"
 
 namespace cft {
 namespace tc {
@@ -228,6 +229,25 @@ int cft_linear_dbias_slice(cft_dtype dtype, const void* dy, int64_t n_tok, int64
       f64::linear_dbias(static_cast<const double*>(dy), (int)n_tok, (int)out_dim, rb, re,
                         static_cast<double*>(db), s);
     }
+  });
+}
+
+int cft_softmax_ce(cft_dtype dtype, const void* y, const int32_t* labels, int64_t rows,
+                   int64_t cols, void* dy, double* loss_dev, uint64_t* bad_label_dev,
+                   cft_stream_t stream) {
+  return guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    if (rows <= 0 || cols <= 0) return;
+    auto* bad = reinterpret_cast<unsigned long long*>(bad_label_dev);
+    if (dtype == CFT_BF16)
+      cft::layers::loss<__nv_bfloat16>(3, static_cast<const __nv_bfloat16*>(y), nullptr, labels,
+                                       rows, cols, static_cast<__nv_bfloat16*>(dy), loss_dev, bad,
+                                       s);
+    else if (dtype == CFT_F32)
+      cft::layers::loss<float>(3, static_cast<const float*>(y), nullptr, labels, rows, cols,
+                               static_cast<float*>(dy), loss_dev, bad, s);
+    else
+      throw cft::Error("cft_softmax_ce: dtype must be BF16 or F32");
   });
 }
 

@@ -134,6 +134,21 @@ def segments_tensor(segments, device) -> torch.Tensor:
     return t.to(device)
 
 
+def softmax_ce(y: torch.Tensor, labels: torch.Tensor, dy: torch.Tensor | None = None, stream=None):
+    """Mean softmax cross-entropy over rows (autodiff.cpp:205-225).  Returns (loss, dy, bad):
+    loss a float64 device scalar, dy = (softmax - onehot) / rows (pass dy=y to overwrite the
+    logits in place), bad the count of rows whose label is out of range (skipped)."""
+    _contig(y, labels)
+    rows, cols = y.shape
+    dy = torch.empty_like(y) if dy is None else dy
+    loss = torch.zeros(1, dtype=torch.float64, device=y.device)
+    bad = torch.zeros(1, dtype=torch.int64, device=y.device)
+    N.check(N.lib.cft_softmax_ce(_dtype(y), y.data_ptr(), labels.data_ptr(), rows, cols,
+                                 dy.data_ptr(), loss.data_ptr(), bad.data_ptr(), _stream(stream)),
+            "softmax_ce")
+    return loss, dy, bad
+
+
 def grad_stats(grad: torch.Tensor, grad_scale: float = 1.0, stats=None, stream=None):
     """Returns a float64 device tensor [sumsq, nonfinite_count(bits), first_bad(bits)]."""
     if stats is None:

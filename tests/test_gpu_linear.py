@@ -179,3 +179,65 @@ def test_adamw_fp32_vs_oracle_and_zero_grad(cuda):
     assert np.allclose(p[6100:6100 + E - 6000], ref[0][6000:], rtol=1e-2, atol=1e-3)
     assert float(tg.abs().max()) == 0.0  # accumulator left zeroed
     assert abs(pre[0].item() - ref[4]) <= 1e-5 * ref[4] and abs(pre[1].item() - ref[5]) <= 1e-5 * ref[5]
+
+
+@pytest.mark.parametrize("E", [2048, 2051, 148 * 2048 * 3 + 4093])
+def test_adamw_tma_staged_matches_register_kernel(cuda, E):
+    """The TMA-staged AdamW (16-byte-aligned state) and the register kernel (the same state one
+    element off alignment) are the same arithmetic: bit-identical m, v, master, parameters and
+    preconditioner range, over several tiles per CTA, a ragged last tile and a 1-3 element tail."""
+    from paper_2605_21177_b200 import ops
+    from paper_2605_21177_b200.engine import AdamWHyper
+    g = torch.Generator(device=cuda).manual_seed(E)
+    h = AdamWHyper(1e-3, 0.9, 0.999, 1e-8, 0.01)
+    init = [torch.rand(E, device=cuda, generator=g) - 0.5, torch.rand(E, device=cuda, generator=g) * 1e-3,
+            torch.rand(E, device=cuda, generator=g) * 1e-6, torch.rand(E, device=cuda, generator=g) - 0.5]
+    cut = E // 3
+    outs = []
+    for off in (0, 1):  # off=1: misaligned views -> register kernel
+        bufs = [torch.zeros(E + 4, device=cuda) for _ in range(4)]
+        views = [b[off:off + E] for b in bufs]
+        for vw, src in zip(views, init):
+            vw.copy_(src)
+        param = torch.zeros(E + 64, dtype=torch.bfloat16, device=cuda)
+        segs = ops.segments_tensor([(0, 8, cut), (cut, cut + 40, E - cut)], cuda)  # (state, param, count)
+        pre = torch.tensor([float("inf"), 0.0], device=cuda)
+        stats = ops.grad_stats(views[3], 0.25)
+        ops.adamw_slice(*views, h, 7, param=param, segments=segs, grad_scale=0.25, stats=stats,
+                        precond=pre, zero_grad=True)
+        torch.cuda.synchronize()
+        outs.append([t.clone() for t in views] + [param, pre, stats.clone()])
+    for a, b in zip(outs[0][:-1], outs[1][:-1]):
+        assert torch.equal(a, b)
+    want = float(((init[3].double() * 0.25) ** 2).sum())
+    for o in outs:  # statistics pass: vector path (aligned) and scalar path (misaligned)
+        assert abs(o[-1][0].item() - want) <= 1e-9 * want and o[-1].view(torch.int64)[1].item() == 0
+    assert float(outs[0][3].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("rows,cols,inplace", [(64, 128256, False), (37, 128256, True), (16, 1000, False),
+                                               (3, 4096, False), (8, 1003, False)])
+def test_softmax_ce_vs_torch_fp32(cuda, rows, cols, inplace):
+    """Softmax CE (autodiff.cpp:205-225) on bf16 logits vs torch fp32 on the same values:
+    the cluster kernel (row parts in shared memory, DSMEM (max, sum) exchange; 128k vocab, ragged
+    last part), the two-pass vector kernel (rows < cluster) and the scalar kernel (cols % 8);
+    in place; an out-of-range label skips its row and is counted."""
+    from paper_2605_21177_b200 import ops
+    g = torch.Generator(device=cuda).manual_seed(rows * cols)
+    y = ((torch.rand(rows, cols, device=cuda, generator=g) - 0.5) * 8).to(torch.bfloat16)
+    lab = torch.randint(0, cols, (rows,), device=cuda, generator=g, dtype=torch.int32)
+    lab[rows // 2] = cols - 1  # the last column of the last part
+    lab[0] = -1 if rows > 4 else 0
+    keep = lab >= 0
+    yf = y.float()
+    want = torch.nn.functional.cross_entropy(yf[keep], lab[keep].long(), reduction="sum") / rows
+    want_dy = (torch.softmax(yf, 1) - torch.nn.functional.one_hot(lab.clamp(min=0).long(), cols)) / rows
+    y0 = y.clone()
+    loss, dy, bad = ops.softmax_ce(y, lab, dy=y if inplace else None)
+    torch.cuda.synchronize()
+    assert bad.item() == int((~keep).sum())
+    assert abs(loss.item() - want.item()) <= 1e-5 * abs(want.item())
+    err = (dy[keep].float() - want_dy[keep]).norm() / want_dy[keep].norm()
+    assert err.item() < 4e-3, err.item()
+    if inplace and not keep.all():  # the skipped row is untouched
+        assert torch.equal(dy[~keep], y0[~keep])

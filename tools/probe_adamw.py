@@ -22,6 +22,10 @@ class H:
     eta, beta1, beta2, epsilon, weight_decay = 1e-3, 0.9, 0.999, 1e-8, 0.0
 
 
+# ramp the clocks first (an idle B200 sits at ~120 MHz; a few ms of work is not enough)
+timeit(lambda: ops.adamw_slice(master, m, v, g, H, 3, param=param, segments=segs, stats=stats,
+                               zero_grad=True), iters=400)
 t = min(timeit(lambda: ops.adamw_slice(master, m, v, g, H, 3, param=param, segments=segs,
-                                       stats=stats, zero_grad=True), iters=5) for _ in range(4))
-print(f"adamw 134M: {t:.3f} ms  {34 * E / t / 1e6:.0f} GB/s (34 B/elem)  {30 * E / t / 1e6:.0f} GB/s (30 B/elem)")
+                                       stats=stats, zero_grad=True), iters=20) for _ in range(5))
+import os
+print(f"adamw 134M [{os.environ.get('CFT_ADAMW_KERNEL', 'bulk')}]: {t:.3f} ms  {34 * E / t / 1e6:.0f} GB/s (34 B/elem)  {30 * E / t / 1e6:.0f} GB/s (30 B/elem)")
