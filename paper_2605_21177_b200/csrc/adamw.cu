@@ -284,18 +284,23 @@ __global__ void __launch_bounds__(kThreads)
 // (in-step the SM clock sits at ~1.3 GHz under the power cap: 8 consumer warps ran
 // 5.2 TB/s alone at 1.95 GHz but fell to 3.5 TB/s in the step -- the per-tile dependent chain
 // LDS -> update -> STG needs more warps in flight, so 16 consumer warps, one float4 each)
-constexpr int kBulkWarps = 16;                     // consumer warps
-constexpr int kBulkGroups = 1;                     // float4 groups per consumer thread per tile
-constexpr int kBulkThreads = (kBulkWarps + 1) * 32;
-constexpr int kBulkTile = kBulkWarps * 32 * 4 * kBulkGroups;  // elements per stage
-constexpr int kBulkStages = 6;
-constexpr int kBulkSegs = 512;
-constexpr size_t kBulkSmem =
-    (size_t)kBulkStages * 4 * kBulkTile * sizeof(float) + 2 * kBulkStages * sizeof(uint64_t) +
-    kBulkSegs * sizeof(cft_segment);
+template <int W, int G, int ST>
+struct BulkCfg {
+  static constexpr int kWarps = W;                        // consumer warps
+  static constexpr int kGroups = G;                       // float4 groups per thread per tile
+  static constexpr int kThreads = (W + 1) * 32;           // + one producer warp
+  static constexpr int kTile = W * 32 * 4 * G;            // elements per stage
+  static constexpr int kStages = ST;
+  static constexpr int kSegs = 512;
+  static constexpr size_t kSmem = (size_t)ST * 4 * kTile * sizeof(float) +
+                                  2 * ST * sizeof(uint64_t) + kSegs * sizeof(cft_segment);
+};
+using Bulk8 = BulkCfg<8, 2, 5>;
+using Bulk16 = BulkCfg<16, 1, 6>;
+using Bulk24 = BulkCfg<24, 1, 4>;
 
-template <typename P>
-__global__ void __launch_bounds__(kBulkThreads, 1)
+template <typename Cfg, typename P>
+__global__ void __launch_bounds__(Cfg::kThreads, 1)
     adamw_f32_bulk_kernel(float* __restrict__ master, float* __restrict__ m,
                           float* __restrict__ v, float* __restrict__ grad, long long n,
                           float gscale, float eta, float b1, float b2, float eps, float wd,
@@ -310,46 +315,46 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     if (nrm > clip) gscale = static_cast<float>(static_cast<double>(gscale) * (clip / nrm));
   }
   extern __shared__ __align__(128) unsigned char smem[];
-  float* ring = reinterpret_cast<float*>(smem);  // [stage][g, m, v, w][kBulkTile]
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)kBulkStages * 4 * kBulkTile);
-  uint64_t* empty = full + kBulkStages;
-  cft_segment* s_segs = reinterpret_cast<cft_segment*>(empty + kBulkStages);
-  __shared__ float s_min[kBulkWarps], s_max[kBulkWarps];
+  float* ring = reinterpret_cast<float*>(smem);  // [stage][g, m, v, w][Cfg::kTile]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)Cfg::kStages * 4 * Cfg::kTile);
+  uint64_t* empty = full + Cfg::kStages;
+  cft_segment* s_segs = reinterpret_cast<cft_segment*>(empty + Cfg::kStages);
+  __shared__ float s_min[Cfg::kWarps], s_max[Cfg::kWarps];
 
-  const bool in_smem = nseg <= kBulkSegs;
+  const bool in_smem = nseg <= Cfg::kSegs;
   if (in_smem)
     for (int i = threadIdx.x; i < nseg; i += blockDim.x) s_segs[i] = segs[i];
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kBulkStages; ++s) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kBulkWarps);
+      mbar_init(&empty[s], Cfg::kWarps);
     }
     fence_barrier_init();
   }
   __syncthreads();
-  const long long ntiles = (n + kBulkTile - 1) / kBulkTile;
+  const long long ntiles = (n + Cfg::kTile - 1) / Cfg::kTile;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
 
-  if (warp == kBulkWarps) {  // producer
+  if (warp == Cfg::kWarps) {  // producer
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
       int it = 0;
       for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int s = it % kBulkStages;
-        mbar_wait(&empty[s], ((it / kBulkStages) & 1) ^ 1);
-        const long long e0 = t * kBulkTile;
-        const long long cnt = min((long long)kBulkTile, n - e0);
+        const int s = it % Cfg::kStages;
+        mbar_wait(&empty[s], ((it / Cfg::kStages) & 1) ^ 1);
+        const long long e0 = t * Cfg::kTile;
+        const long long cnt = min((long long)Cfg::kTile, n - e0);
         const uint32_t bytes = static_cast<uint32_t>(cnt / 4) * 16u;
         if (bytes == 0) {
           mbar_arrive(&full[s]);
           continue;
         }
         mbar_expect_tx(&full[s], 4 * bytes);
-        float* st = ring + (size_t)s * 4 * kBulkTile;
+        float* st = ring + (size_t)s * 4 * Cfg::kTile;
         bulk_load_1d(st, grad + e0, bytes, &full[s], pol);
-        bulk_load_1d(st + kBulkTile, m + e0, bytes, &full[s], pol);
-        bulk_load_1d(st + 2 * kBulkTile, v + e0, bytes, &full[s], pol);
-        bulk_load_1d(st + 3 * kBulkTile, master + e0, bytes, &full[s], pol);
+        bulk_load_1d(st + Cfg::kTile, m + e0, bytes, &full[s], pol);
+        bulk_load_1d(st + 2 * Cfg::kTile, v + e0, bytes, &full[s], pol);
+        bulk_load_1d(st + 3 * Cfg::kTile, master + e0, bytes, &full[s], pol);
       }
     }
     return;
@@ -361,23 +366,23 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   float pmin = INFINITY, pmax = 0.f;
   int it = 0;
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int s = it % kBulkStages;
-    mbar_wait(&full[s], (it / kBulkStages) & 1);
-    const long long e0 = t * kBulkTile;
-    const long long cnt = min((long long)kBulkTile, n - e0);
+    const int s = it % Cfg::kStages;
+    mbar_wait(&full[s], (it / Cfg::kStages) & 1);
+    const long long e0 = t * Cfg::kTile;
+    const long long cnt = min((long long)Cfg::kTile, n - e0);
     const long long full4 = cnt / 4;  // groups delivered by the bulk copy
-    const float* st = ring + (size_t)s * 4 * kBulkTile;
+    const float* st = ring + (size_t)s * 4 * Cfg::kTile;
 #pragma unroll
-    for (int k = 0; k < kBulkGroups; ++k) {
-      const int q = threadIdx.x + k * kBulkWarps * 32;
+    for (int k = 0; k < Cfg::kGroups; ++k) {
+      const int q = threadIdx.x + k * Cfg::kWarps * 32;
       if (4LL * q >= cnt) break;
       const long long i0 = e0 + 4LL * q;
       float g[4], mm[4], vv[4], w[4];
       if (q < full4) {
         const float4 g4 = reinterpret_cast<const float4*>(st)[q];
-        const float4 m4 = reinterpret_cast<const float4*>(st + kBulkTile)[q];
-        const float4 v4 = reinterpret_cast<const float4*>(st + 2 * kBulkTile)[q];
-        const float4 w4 = reinterpret_cast<const float4*>(st + 3 * kBulkTile)[q];
+        const float4 m4 = reinterpret_cast<const float4*>(st + Cfg::kTile)[q];
+        const float4 v4 = reinterpret_cast<const float4*>(st + 2 * Cfg::kTile)[q];
+        const float4 w4 = reinterpret_cast<const float4*>(st + 3 * Cfg::kTile)[q];
         g[0] = g4.x; g[1] = g4.y; g[2] = g4.z; g[3] = g4.w;
         mm[0] = m4.x; mm[1] = m4.y; mm[2] = m4.z; mm[3] = m4.w;
         vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
@@ -437,9 +442,9 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
       s_min[warp] = pmin;
       s_max[warp] = pmax;
     }
-    named_bar_sync(1, kBulkWarps * 32);
+    named_bar_sync(1, Cfg::kWarps * 32);
     if (threadIdx.x == 0) {
-      for (int i = 1; i < kBulkWarps; ++i) {
+      for (int i = 1; i < Cfg::kWarps; ++i) {
         pmin = fminf(pmin, s_min[i]);
         pmax = fmaxf(pmax, s_max[i]);
       }
@@ -541,14 +546,7 @@ __global__ void convert_kernel(const S* src, D* dst, long long n) {
   }
 }
 
-// CFT_ADAMW_KERNEL=reg selects the register kernel everywhere (A/B experiments)
-inline bool adamw_bulk_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("CFT_ADAMW_KERNEL");
-    return !(e && std::string(e) == "reg");
-  }();
-  return on;
-}
+inline int adamw_variant() { return cft::kernel_variant(0); }
 
 inline int grid_for(long long work) {
   const long long cap = (long long)num_sms() * 8;
@@ -593,24 +591,32 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
     CFT_CHECK(!param_base || (segs && n_segments > 0), "cft_adamw_slice: missing segments");
     const double* st = static_cast<const double*>(stats_dev);
     const auto aligned16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    if (state_dtype == CFT_F32 && adamw_bulk_enabled() && n >= kBulkTile &&
-        aligned16(master) && aligned16(m) && aligned16(v) && aligned16(grad)) {
-      const long long tiles = (n + kBulkTile - 1) / kBulkTile;
-      const int grid = static_cast<int>(std::min<long long>(tiles, cft::num_sms()));
-      auto go = [&](auto* p) {
+    const int variant = adamw_variant();
+    const long long min_n = Bulk24::kTile;
+    if (state_dtype == CFT_F32 && variant != 0 && n >= min_n && aligned16(master) &&
+        aligned16(m) && aligned16(v) && aligned16(grad)) {
+      auto launch = [&](auto cfg, auto* p) {
+        using C_ = decltype(cfg);
         using PT = std::remove_pointer_t<decltype(p)>;
         static bool attr = [] {
-          CFT_CUDA(cudaFuncSetAttribute(adamw_f32_bulk_kernel<PT>,
+          CFT_CUDA(cudaFuncSetAttribute(adamw_f32_bulk_kernel<C_, PT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kBulkSmem));
+                                        (int)C_::kSmem));
           return true;
         }();
         (void)attr;
-        adamw_f32_bulk_kernel<<<grid, kBulkThreads, kBulkSmem, s>>>(
+        const long long tiles = (n + C_::kTile - 1) / C_::kTile;
+        const int grid = static_cast<int>(std::min<long long>(tiles, cft::num_sms()));
+        adamw_f32_bulk_kernel<C_><<<grid, C_::kThreads, C_::kSmem, s>>>(
             static_cast<float*>(master), static_cast<float*>(m), static_cast<float*>(v),
             static_cast<float*>(grad), n, (float)grad_scale, (float)h->eta, (float)h->beta1,
             (float)h->beta2, (float)h->epsilon, (float)h->weight_decay, (float)bc1, (float)bc2, p,
             segs, n_segments, st, static_cast<float*>(precond_dev), zero_grad, clip_max_norm);
+      };
+      auto go = [&](auto* p) {
+        if (variant == 1) launch(Bulk8{}, p);
+        else if (variant == 2) launch(Bulk16{}, p);
+        else launch(Bulk24{}, p);
       };
       if (param_dtype == CFT_BF16) go(static_cast<__nv_bfloat16*>(param_base));
       else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));

@@ -2,6 +2,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -54,9 +55,33 @@ CUtensorMap make_tmap_bf16(const void* base, uint64_t inner, uint64_t outer,
   return m;
 }
 
+int& kernel_variant(int op) {
+  static int v[kNumVariantOps] = {
+      [] {
+        const char* e = std::getenv("CFT_ADAMW_KERNEL");
+        const std::string k = e ? e : "";
+        return k == "reg" ? 0 : k == "bulk8" ? 1 : k == "bulk16" ? 2 : 3;
+      }(),
+      [] {
+        const char* e = std::getenv("CFT_CE_KERNEL");
+        const std::string k = e ? e : "";
+        return k == "cluster" ? 1 : k == "cluster3" ? 2 : 0;
+      }(),
+  };
+  if (op < 0 || op >= kNumVariantOps) throw Error("kernel_variant: unknown operator");
+  return v[op];
+}
+
 }  // namespace cft
 
 extern "C" {
+int cft_set_kernel_variant(int op, int variant) {
+  return cft::guarded([&] {
+    CFT_CHECK(variant >= 0 && variant <= 3, "cft_set_kernel_variant: variant out of range");
+    cft::kernel_variant(op) = variant;
+  });
+}
+
 const char* cft_last_error(void) { return cft::t_err.c_str(); }
 int cft_last_status(void) {
   const int s = cft::t_status;

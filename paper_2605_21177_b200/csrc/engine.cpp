@@ -869,7 +869,9 @@ void Engine::step_end() {
   const cft_segment* segs = sharded() ? shard_segs_[c] : chunk_segs_[c];
   const int32_t nseg = sharded() ? 1 : static_cast<int32_t>(chunk_slices_[c].size());
   pb(kUpdate);
-  add_work(kUpdate, (cfg_.optim == 0 ? 30.0 : 14.0) * gn);
+  // AdamW: read g, m, v, master + write m, v, master, param + re-zero the accumulator (the
+  // reference's accumulate_grad fill, optimizer.cpp:136) = 34 B/elem at fp32 state, bf16 params
+  add_work(kUpdate, (cfg_.optim == 0 ? (sdt == CFT_F32 ? 30.0 + 4.0 : 30.0) : 14.0) * gn);
   if (gn > 0) {
     if (cfg_.optim == 0) {
       const double bc1 = 1.0 - std::pow(cfg_.hyper.beta1, static_cast<double>(n_local_[c]));

@@ -210,11 +210,25 @@ __global__ void loss_ce_kernel(const T* y, const int32_t* labels, long long cols
 
 // Softmax cross-entropy over wide bf16 rows (cols % 8 == 0, e.g. a 128k vocabulary): one
 // online pass for (max, sum of exp) with 16-byte loads, one pass writing dy (may alias y).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+constexpr float kL2e = 1.4426950408889634f;  // log2(e): exp(x - c) = ex2(x*kL2e - c*kL2e)
+
+// (one exp per merge: the larger maximum's sum is kept as is)
 __device__ __forceinline__ void online_merge(float& m, float& s, float m2, float s2) {
-  const float mn = fmaxf(m, m2);
-  if (mn == -INFINITY) return;
-  s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
-  m = mn;
+  if (m2 == -INFINITY) return;
+  if (m == -INFINITY) {
+    m = m2;
+    s = s2;
+  } else if (m2 > m) {
+    s = s * __expf(m - m2) + s2;
+    m = m2;
+  } else {
+    s = s + s2 * __expf(m2 - m);
+  }
 }
 
 __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels, long long cols,
@@ -245,8 +259,9 @@ __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels
 #pragma unroll
     for (int e = 1; e < 8; ++e) lm = fmaxf(lm, v[e]);
     float ls = 0.f;
+    const float lms = lm * kL2e;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ls += __expf(v[e] - lm);
+    for (int e = 0; e < 8; ++e) ls += ex2_approx(fmaf(v[e], kL2e, -lms));  // FFMA + EX2
     online_merge(m, s, lm, ls);
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -263,6 +278,7 @@ __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels
   s = 0.f;
   for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) online_merge(m, s, sm[i], ss[i]);
   const float logz = m + logf(s);
+  const float lzs = logz * kL2e;
   for (long long j = threadIdx.x; j < nv; j += blockDim.x) {
     const uint4 u = reinterpret_cast<const uint4*>(yr)[j];
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -272,8 +288,8 @@ __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels
     for (int q = 0; q < 4; ++q) {
       const float2 f = __bfloat1622float2(h[q]);
       const long long c0 = 8 * j + 2 * q;
-      const float p0 = __expf(f.x - logz) - (c0 == label ? 1.f : 0.f);
-      const float p1 = __expf(f.y - logz) - (c0 + 1 == label ? 1.f : 0.f);
+      const float p0 = ex2_approx(fmaf(f.x, kL2e, -lzs)) - (c0 == label ? 1.f : 0.f);
+      const float p1 = ex2_approx(fmaf(f.y, kL2e, -lzs)) - (c0 + 1 == label ? 1.f : 0.f);
       oh[q] = __floats2bfloat162_rn(p0 * inv_rows, p1 * inv_rows);
     }
     reinterpret_cast<uint4*>(dy + b * cols)[j] = o;
@@ -283,24 +299,36 @@ __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels
 
 // Softmax cross-entropy with the row held on chip: a cluster of kCeCluster CTAs owns one
 // row at a time, each CTA a contiguous part of <= kCePart columns that a 1-D bulk copy (TMA)
-// brings into shared memory.  Each CTA reduces its part to an online (max, sum-exp) pair,
-// the cluster exchanges the pairs through distributed shared memory, and every CTA writes
-// its part of dlogits from shared memory -- so HBM sees exactly one read and one write of
-// each logit (the two-pass kernel above re-reads a 256 KB row that no longer sits in L2 at
-// full occupancy).  Two stages per CTA: row r+1 streams in while row r is reduced/written.
+// brings into shared memory.  Each CTA reduces its part to a (max, sum-exp) pair, the cluster
+// exchanges the pairs through distributed shared memory, and every CTA writes its part of
+// dlogits from shared memory -- so HBM sees exactly one read and one write of each logit (the
+// two-pass kernel above re-reads a 256 KB row that no longer sits in L2 at full occupancy).
+// One MUFU exp per logit per pass: each thread takes the max of its own columns first (a
+// cheap extra pass over shared memory), then sums exp2(x*log2e - max*log2e) as FFMA + EX2.
+// STAGES row buffers per CTA and MINB CTAs per SM: rows in flight per SM = STAGES x MINB.
 // The row may be overwritten in place (dy == y): the label logit is read from shared memory.
 constexpr int kCeCluster = 4;
 constexpr int kCeThreads = 512;
 constexpr int kCePart = 32768;  // bf16 columns per CTA and stage (64 KB)
-constexpr size_t kCeSmem = 2ull * kCePart * sizeof(__nv_bfloat16);
 
-__global__ void __cluster_dims__(kCeCluster, 1, 1) __launch_bounds__(kCeThreads, 1)
+__device__ __forceinline__ void unpack8(const uint4& u, float (&v)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 f = __bfloat1622float2(h[q]);
+    v[2 * q] = f.x;
+    v[2 * q + 1] = f.y;
+  }
+}
+
+template <int STAGES, int MINB>
+__global__ void __cluster_dims__(kCeCluster, 1, 1) __launch_bounds__(kCeThreads, MINB)
     loss_ce_cluster_kernel(const __nv_bfloat16* y, const int32_t* labels, long long rows,
                            long long cols, int part, float inv_rows, __nv_bfloat16* dy,
                            double* loss, unsigned long long* bad_label) {
   using namespace cft::ptx;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t full[2];
+  __shared__ uint64_t full[STAGES];
   __shared__ float2 slot[2];  // this CTA's (max, sum) of the row in flight, by row parity
   __shared__ float sm[32], ss[32];
   const uint32_t rank = cluster_ctarank();
@@ -309,8 +337,7 @@ __global__ void __cluster_dims__(kCeCluster, 1, 1) __launch_bounds__(kCeThreads,
   const int my = static_cast<int>(max(0LL, min((long long)part, cols - c0)));  // % 8 == 0
   __nv_bfloat16* buf0 = reinterpret_cast<__nv_bfloat16*>(smem);
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int b = 0; b < STAGES; ++b) mbar_init(&full[b], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -326,33 +353,31 @@ __global__ void __cluster_dims__(kCeCluster, 1, 1) __launch_bounds__(kCeThreads,
   };
   if (threadIdx.x == 0) {
     pol = l2_policy_evict_first();
-    if (cid < rows) issue(cid, 0);
-    if (cid + ncl < rows) issue(cid + ncl, 1);
+    for (int b = 0; b < STAGES; ++b)
+      if (cid + b * ncl < rows) issue(cid + b * ncl, b);
   }
   const int nv = my / 8;
   int it = 0;
   for (long long r = cid; r < rows; r += ncl, ++it) {
-    const int b = it & 1;
-    mbar_wait(&full[b], (it >> 1) & 1);
-    const __nv_bfloat16* row = buf0 + (size_t)b * kCePart;
-    float m = -INFINITY, s = 0.f;
+    const int b = it % STAGES;
+    mbar_wait(&full[b], (it / STAGES) & 1);
+    const uint4* row = reinterpret_cast<const uint4*>(buf0 + (size_t)b * kCePart);
+    float m = -INFINITY;
     for (int j = threadIdx.x; j < nv; j += kCeThreads) {
-      const uint4 u = reinterpret_cast<const uint4*>(row)[j];
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
       float v[8];
+      unpack8(row[j], v);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 f = __bfloat1622float2(h[q]);
-        v[2 * q] = f.x;
-        v[2 * q + 1] = f.y;
+      for (int e = 0; e < 8; ++e) m = fmaxf(m, v[e]);
+    }
+    float s = 0.f;
+    if (m != -INFINITY) {
+      const float ms = m * kL2e;
+      for (int j = threadIdx.x; j < nv; j += kCeThreads) {
+        float v[8];
+        unpack8(row[j], v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += ex2_approx(fmaf(v[e], kL2e, -ms));
       }
-      float lm = v[0];
-#pragma unroll
-      for (int e = 1; e < 8; ++e) lm = fmaxf(lm, v[e]);
-      float ls = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) ls += __expf(v[e] - lm);
-      online_merge(m, s, lm, ls);
     }
     for (int o = 16; o > 0; o >>= 1) {
       const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
@@ -368,12 +393,12 @@ __global__ void __cluster_dims__(kCeCluster, 1, 1) __launch_bounds__(kCeThreads,
       m = -INFINITY;
       s = 0.f;
       for (int i = 0; i < kCeThreads / 32; ++i) online_merge(m, s, sm[i], ss[i]);
-      slot[b] = make_float2(m, s);
+      slot[it & 1] = make_float2(m, s);
     }
     cluster_sync();  // every CTA's pair for row r is visible cluster-wide
     m = -INFINITY;
     s = 0.f;
-    const uint32_t my_slot = smem_u32(&slot[b]);
+    const uint32_t my_slot = smem_u32(&slot[it & 1]);
 #pragma unroll
     for (int k = 0; k < kCeCluster; ++k) {  // same order in every CTA -> same logZ
       float2 p;
@@ -383,35 +408,59 @@ __global__ void __cluster_dims__(kCeCluster, 1, 1) __launch_bounds__(kCeThreads,
       online_merge(m, s, p.x, p.y);
     }
     const float logz = m + logf(s);
+    const float lzs = logz * kL2e;
     const int label = labels[r];
     if (label < 0 || label >= cols) {
       if (rank == 0 && threadIdx.x == 0) atomicAdd(bad_label, 1ull);
     } else {
-      __nv_bfloat16* out = dy + r * cols + c0;
+      uint4* out = reinterpret_cast<uint4*>(dy + r * cols + c0);
+      const long long lrel = label - c0;  // label column relative to this part
       for (int j = threadIdx.x; j < nv; j += kCeThreads) {
-        const uint4 u = reinterpret_cast<const uint4*>(row)[j];
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+        float v[8];
+        unpack8(row[j], v);
         uint4 o;
         __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float2 f = __bfloat1622float2(h[q]);
-          const long long c = c0 + 8 * j + 2 * q;
-          const float p0 = __expf(f.x - logz) - (c == label ? 1.f : 0.f);
-          const float p1 = __expf(f.y - logz) - (c + 1 == label ? 1.f : 0.f);
+          const long long c = 8LL * j + 2 * q;
+          const float p0 = ex2_approx(fmaf(v[2 * q], kL2e, -lzs)) - (c == lrel ? 1.f : 0.f);
+          const float p1 = ex2_approx(fmaf(v[2 * q + 1], kL2e, -lzs)) - (c + 1 == lrel ? 1.f : 0.f);
           oh[q] = __floats2bfloat162_rn(p0 * inv_rows, p1 * inv_rows);
         }
-        __stcs(reinterpret_cast<uint4*>(out) + j, o);
+        __stcs(out + j, o);
       }
-      if (threadIdx.x == 0 && label >= c0 && label < c0 + my) {
-        const float ylab = __bfloat162float(row[label - c0]);
+      if (threadIdx.x == 0 && lrel >= 0 && lrel < my) {
+        const float ylab = __bfloat162float(buf0[(size_t)b * kCePart + lrel]);
         atomicAdd(loss, static_cast<double>(-(ylab - logz)) * inv_rows);
       }
     }
     __syncthreads();  // every thread is done with this stage
-    if (threadIdx.x == 0 && r + 2 * ncl < rows) issue(r + 2 * ncl, b);
+    if (threadIdx.x == 0 && r + STAGES * ncl < rows) issue(r + STAGES * ncl, b);
   }
   cluster_sync();  // peers may still read this CTA's slot
+}
+
+template <int STAGES, int MINB>
+void launch_ce_cluster(const __nv_bfloat16* y, const int32_t* labels, long long rows,
+                       long long cols, __nv_bfloat16* dy, double* loss_acc,
+                       unsigned long long* bad_label, cudaStream_t s) {
+  constexpr size_t smem = (size_t)STAGES * kCePart * sizeof(__nv_bfloat16);
+  auto kern = loss_ce_cluster_kernel<STAGES, MINB>;
+  static int max_clusters = [&] {
+    CFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kCeCluster * num_sms() * MINB);
+    cfg.blockDim = dim3(kCeThreads);
+    cfg.dynamicSmemBytes = smem;
+    int n = 0;
+    CFT_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+    return std::max(1, n);
+  }();
+  const int part = static_cast<int>(((cols + kCeCluster - 1) / kCeCluster + 7) / 8 * 8);
+  const long long ncl = std::min<long long>(rows, max_clusters);
+  kern<<<(unsigned)(ncl * kCeCluster), kCeThreads, smem, s>>>(y, labels, rows, cols, part,
+                                                               1.f / rows, dy, loss_acc, bad_label);
+  check_launch("loss_ce_cluster");
 }
 
 // fp64 losses for the fp64 engine path (exp/log are CUDA's: <= 1-2 ulp from glibc).
@@ -511,27 +560,10 @@ void loss(int kind, const T* y, const T* target, const int32_t* labels, long lon
     if constexpr (std::is_same_v<T, __nv_bfloat16>) {
       const bool vec = cols % 8 == 0 &&
           ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0;
-      static const bool cluster_on = [] {  // CFT_CE_KERNEL=vec: two-pass kernel (A/B runs)
-        const char* e = std::getenv("CFT_CE_KERNEL");
-        return !(e && std::string(e) == "vec");
-      }();
-      if (vec && cluster_on && rows >= kCeCluster && cols <= (long long)kCeCluster * kCePart) {
-        static int max_clusters = [] {
-          CFT_CUDA(cudaFuncSetAttribute(loss_ce_cluster_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCeSmem));
-          cudaLaunchConfig_t cfg = {};
-          cfg.gridDim = dim3(kCeCluster * num_sms());
-          cfg.blockDim = dim3(kCeThreads);
-          cfg.dynamicSmemBytes = kCeSmem;
-          int n = 0;
-          CFT_CUDA(cudaOccupancyMaxActiveClusters(&n, loss_ce_cluster_kernel, &cfg));
-          return std::max(1, n);
-        }();
-        const int part = static_cast<int>(((cols + kCeCluster - 1) / kCeCluster + 7) / 8 * 8);
-        const long long ncl = std::min<long long>(rows, max_clusters);
-        loss_ce_cluster_kernel<<<(unsigned)(ncl * kCeCluster), kCeThreads, kCeSmem, s>>>(
-            y, labels, rows, cols, part, 1.f / rows, dy, loss_acc, bad_label);
-        check_launch("loss_ce_cluster");
+      const int variant = kernel_variant(1);  // 0: two-pass kernel (A/B runs)
+      if (vec && variant != 0 && rows >= kCeCluster && cols <= (long long)kCeCluster * kCePart) {
+        if (variant == 1) launch_ce_cluster<2, 1>(y, labels, rows, cols, dy, loss_acc, bad_label, s);
+        else launch_ce_cluster<1, 3>(y, labels, rows, cols, dy, loss_acc, bad_label, s);
         return;
       }
       if (vec) {
