@@ -65,7 +65,7 @@ int& kernel_variant(int op) {
       [] {
         const char* e = std::getenv("CFT_CE_KERNEL");
         const std::string k = e ? e : "";
-        return k == "cluster" ? 1 : k == "cluster3" ? 2 : 0;
+        return k == "cluster" ? 1 : k == "cluster3" ? 2 : k == "vec1024" ? 3 : 0;
       }(),
   };
   if (op < 0 || op >= kNumVariantOps) throw Error("kernel_variant: unknown operator");

@@ -86,7 +86,12 @@ Engine::Engine(const std::vector<LayerSpec>& specs, const EngineConfig& cfg,
         L.in_w = L.out_w = L.spec.a;
         break;
       case kTanh:
-        CFT_CHECK(width >= 0, "engine: tanh cannot be the first layer");
+        if (width < 0) {  // leading tanh (shape-agnostic in the reference): the input width is
+                          // the first later layer that fixes one (Linear in / LayerNorm dim)
+          for (size_t lj = li + 1; lj < specs.size() && width < 0; ++lj)
+            if (specs[lj].type == kLinear || specs[lj].type == kLayerNorm) width = specs[lj].a;
+          CFT_CHECK(width >= 0, "engine: cannot infer the input width of a leading tanh");
+        }
         L.in_w = L.out_w = width;
         break;
       default:

@@ -278,20 +278,25 @@ __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels
   s = 0.f;
   for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) online_merge(m, s, sm[i], ss[i]);
   const float logz = m + logf(s);
-  const float lzs = logz * kL2e;
-  for (long long j = threadIdx.x; j < nv; j += blockDim.x) {
+  // p / rows = ex2(x*log2e - (logZ*log2e - log2(1/rows))): the 1/rows scale rides in the
+  // exponent (one FFMA + one EX2 per logit); the one-hot term only touches the label's vector
+  const float lzs = logz * kL2e - log2f(inv_rows);
+  const int label_j = label >> 3;
+  for (int j = threadIdx.x; j < (int)nv; j += blockDim.x) {
     const uint4 u = reinterpret_cast<const uint4*>(yr)[j];
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
     uint4 o;
     __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+    float p[8];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const float2 f = __bfloat1622float2(h[q]);
-      const long long c0 = 8 * j + 2 * q;
-      const float p0 = ex2_approx(fmaf(f.x, kL2e, -lzs)) - (c0 == label ? 1.f : 0.f);
-      const float p1 = ex2_approx(fmaf(f.y, kL2e, -lzs)) - (c0 + 1 == label ? 1.f : 0.f);
-      oh[q] = __floats2bfloat162_rn(p0 * inv_rows, p1 * inv_rows);
+      p[2 * q] = ex2_approx(fmaf(f.x, kL2e, -lzs));
+      p[2 * q + 1] = ex2_approx(fmaf(f.y, kL2e, -lzs));
     }
+    if (j == label_j) p[label & 7] -= inv_rows;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) oh[q] = __floats2bfloat162_rn(p[2 * q], p[2 * q + 1]);
     reinterpret_cast<uint4*>(dy + b * cols)[j] = o;
   }
   if (threadIdx.x == 0) atomicAdd(loss, static_cast<double>(-(ylab - logz)) * inv_rows);
@@ -561,14 +566,18 @@ void loss(int kind, const T* y, const T* target, const int32_t* labels, long lon
       const bool vec = cols % 8 == 0 &&
           ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0;
       const int variant = kernel_variant(1);  // 0: two-pass kernel (A/B runs)
-      if (vec && variant != 0 && rows >= kCeCluster && cols <= (long long)kCeCluster * kCePart) {
+      if (vec && (variant == 1 || variant == 2) && rows >= kCeCluster && cols <= (long long)kCeCluster * kCePart) {
         if (variant == 1) launch_ce_cluster<2, 1>(y, labels, rows, cols, dy, loss_acc, bad_label, s);
         else launch_ce_cluster<1, 3>(y, labels, rows, cols, dy, loss_acc, bad_label, s);
         return;
       }
       if (vec) {
-        loss_ce_vec_kernel<<<(unsigned)rows, 512, 0, s>>>(y, labels, cols, 1.f / rows, dy, loss_acc,
-                                                          bad_label);
+        // variant 3: 1024 threads per row -> 2 CTAs (rows) per SM, 296 rows = 76 MB in flight,
+        // so the second pass over each 256 KB row still finds it in L2 (512 threads: 4 rows per
+        // SM, 152 MB in flight > L2, and the second pass re-reads from HBM)
+        const unsigned threads = variant == 3 ? 1024u : 512u;
+        loss_ce_vec_kernel<<<(unsigned)rows, threads, 0, s>>>(y, labels, cols, 1.f / rows, dy,
+                                                              loss_acc, bad_label);
         check_launch("loss_ce_vec");
         return;
       }

@@ -221,7 +221,7 @@ def test_adamw_tma_staged_matches_register_kernel(cuda, E, variant):
 
 @pytest.mark.parametrize("rows,cols,inplace", [(64, 128256, False), (37, 128256, True), (16, 1000, False),
                                                (3, 4096, False), (8, 1003, False)])
-@pytest.mark.parametrize("variant", [0, 1, 2], ids=["two_pass", "cluster2x1", "cluster1x3"])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3], ids=["two_pass", "cluster2x1", "cluster1x3", "two_pass1024"])
 def test_softmax_ce_vs_torch_fp32(cuda, rows, cols, inplace, variant):
     """Softmax CE (autodiff.cpp:205-225) on bf16 logits vs torch fp32 on the same values:
     the cluster kernel (row parts in shared memory, DSMEM (max, sum) exchange; 128k vocab, ragged
