@@ -215,7 +215,16 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-constexpr float kL2e = 1.4426950408889634f;  // log2(e): exp(x - c) = ex2(x*kL2e - c*kL2e)
+constexpr float kL2e = 1.4426950408889634f;
+__device__ __forceinline__ void unpack8(const uint4& u, float (&v)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 f = __bfloat1622float2(h[q]);
+    v[2 * q] = f.x;
+    v[2 * q + 1] = f.y;
+  }
+}  // log2(e): exp(x - c) = ex2(x*kL2e - c*kL2e)
 
 // (one exp per merge: the larger maximum's sum is kept as is)
 __device__ __forceinline__ void online_merge(float& m, float& s, float m2, float s2) {
@@ -245,24 +254,26 @@ __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels
   const float ylab = __bfloat162float(yr[label]);
   const long long nv = cols / 8;
   float m = -INFINITY, s = 0.f;
-  for (long long j = threadIdx.x; j < nv; j += blockDim.x) {
-    const uint4 u = reinterpret_cast<const uint4*>(yr)[j];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float2 f = __bfloat1622float2(h[q]);
-      v[2 * q] = f.x;
-      v[2 * q + 1] = f.y;
-    }
+  // 16 logits (two 16-byte loads blockDim apart, both coalesced) per online merge
+  const int nvi = static_cast<int>(nv), bd = blockDim.x;
+  for (int j = threadIdx.x; j < nvi; j += 2 * bd) {
+    const bool two = j + bd < nvi;
+    const uint4 u0 = reinterpret_cast<const uint4*>(yr)[j];
+    const uint4 u1 = two ? reinterpret_cast<const uint4*>(yr)[j + bd] : u0;
+    float v[16];
+    unpack8(u0, *reinterpret_cast<float(*)[8]>(v));
+    unpack8(u1, *reinterpret_cast<float(*)[8]>(v + 8));
     float lm = v[0];
 #pragma unroll
-    for (int e = 1; e < 8; ++e) lm = fmaxf(lm, v[e]);
-    float ls = 0.f;
+    for (int e = 1; e < 16; ++e) lm = fmaxf(lm, v[e]);  // a duplicated u1 leaves the max as is
     const float lms = lm * kL2e;
+    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ls += ex2_approx(fmaf(v[e], kL2e, -lms));  // FFMA + EX2
-    online_merge(m, s, lm, ls);
+    for (int e = 0; e < 8; ++e) {
+      s0 += ex2_approx(fmaf(v[e], kL2e, -lms));  // FFMA + EX2
+      s1 += ex2_approx(fmaf(v[e + 8], kL2e, -lms));
+    }
+    online_merge(m, s, lm, two ? s0 + s1 : s0);
   }
   for (int o = 16; o > 0; o >>= 1) {
     const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
@@ -316,15 +327,6 @@ constexpr int kCeCluster = 4;
 constexpr int kCeThreads = 512;
 constexpr int kCePart = 32768;  // bf16 columns per CTA and stage (64 KB)
 
-__device__ __forceinline__ void unpack8(const uint4& u, float (&v)[8]) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float2 f = __bfloat1622float2(h[q]);
-    v[2 * q] = f.x;
-    v[2 * q + 1] = f.y;
-  }
-}
 
 template <int STAGES, int MINB>
 __global__ void __cluster_dims__(kCeCluster, 1, 1) __launch_bounds__(kCeThreads, MINB)
