@@ -289,8 +289,7 @@ int cft_set_fusion(int enable);
  * CFT_CE_KERNEL).  op 0 fp32 AdamW: 0 register kernel, 1 / 2 / 3 TMA-staged with 8 / 16 /
  * 24 consumer warps.  op 1 bf16 softmax CE: 0 two-pass (512 threads per row), 1 cluster
  * (2 row stages, 1 CTA per SM), 2 cluster (1 stage, 3 CTAs per SM), 3 two-pass with 1024
- * threads per row.  op 2 fp32 wgrad red.add epilogue: 0 one row per lane (half-sector
- * requests), 1 quad-transposed (full 32-byte sectors). */
+ * threads per row. */
 int cft_set_kernel_variant(int op, int variant);
 
 /* Element conversion (e.g. fp32 master -> bf16 params at init). */

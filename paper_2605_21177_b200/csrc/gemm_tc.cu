@@ -36,8 +36,7 @@ constexpr int BK = 64;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
-enum Epi : int { kEpiBf16 = 0, kEpiBf16Add = 1, kEpiF32 = 2, kEpiF32Add = 3, kEpiF32Red = 4,
-                 kEpiF32RedQuad = 5 };  // 5: red.add with the quad transpose below
+enum Epi : int { kEpiBf16 = 0, kEpiBf16Add = 1, kEpiF32 = 2, kEpiF32Add = 3, kEpiF32Red = 4 };
 
 struct Args {
   int M, N, K;
@@ -126,43 +125,6 @@ __device__ __forceinline__ bool work_next(const Args& a, WorkIter& it, int npair
   return true;
 }
 
-// fp32 red.add of a warp's 32 rows x 16 columns with full 32-byte sectors: each lane holds one
-// row's 16 columns, so a plain red.v4 per lane touches 32 rows x 16 B -- 32 half-sector atomic
-// requests per instruction.  A 4 x 4 transpose of 16-byte chunks inside each lane quad (four
-// shuffle rounds) lets the quad's lanes cover one row's 64 contiguous bytes per instruction: 16
-// full-sector requests.  All 32 lanes must call it (warp-uniform col / alignment).
-__device__ __forceinline__ void red16_quad(const Args& args, long long rbase, bool row_ok, int col,
-                                           const uint32_t (&r)[16], int lane) {
-  const int q = lane & 3;
-  float c[4][4];  // c[k]: chunk q of quad row (q + k) & 3, received in round k
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int give = (q - k) & 3;  // the chunk this lane's reader in round k needs
-    const int src = (lane & ~3) | ((q + k) & 3);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t v = give == 0 ? r[e] : give == 1 ? r[4 + e] : give == 2 ? r[8 + e] : r[12 + e];
-      c[k][e] = __uint_as_float(__shfl_sync(0xffffffffu, v, src));
-    }
-  }
-  float* C = static_cast<float*>(args.C);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int srcl = (lane & ~3) | j;
-    const long long rb = __shfl_sync(0xffffffffu, rbase, srcl);
-    const int ok = __shfl_sync(0xffffffffu, static_cast<int>(row_ok), srcl);
-    const int k = (j - q) & 3;
-    float a[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) a[e] = k == 0 ? c[0][e] : k == 1 ? c[1][e] : k == 2 ? c[2][e] : c[3][e];
-    if (ok) ptx::red_add_v4(C + rb + col + 4 * q, a[0], a[1], a[2], a[3]);
-  }
-}
-__device__ __forceinline__ bool red_quad_ok(const Args& args, int col) {
-  return args.epi == kEpiF32RedQuad && col + 16 <= args.N && (args.ldc & 3) == 0 &&
-         (reinterpret_cast<uintptr_t>(args.C) & 15) == 0;
-}
-
 // Epilogue store of 16 consecutive accumulator columns of one output row (one thread).
 __device__ __forceinline__ void store16(const Args& args, long long rbase, int col,
                                         const uint32_t (&r)[16]) {
@@ -176,7 +138,7 @@ __device__ __forceinline__ void store16(const Args& args, long long rbase, int c
         const float a0 = __uint_as_float(r[j]), a1 = __uint_as_float(r[j + 1]);
         const float a2 = __uint_as_float(r[j + 2]), a3 = __uint_as_float(r[j + 3]);
         float4* p = reinterpret_cast<float4*>(out + j);
-        if (args.epi >= kEpiF32Red) {
+        if (args.epi == kEpiF32Red) {
           ptx::red_add_v4(out + j, a0, a1, a2, a3);
         } else if (args.epi == kEpiF32Add) {
           float4 o = *p;
@@ -190,7 +152,7 @@ __device__ __forceinline__ void store16(const Args& args, long long rbase, int c
       for (int j = 0; j < 16; ++j) {  // static indices keep r[] in registers
         if (col + j >= args.N) break;
         const float a0 = __uint_as_float(r[j]);
-        if (args.epi >= kEpiF32Red) atomicAdd(out + j, a0);
+        if (args.epi == kEpiF32Red) atomicAdd(out + j, a0);
         else if (args.epi == kEpiF32Add) out[j] += a0;
         else out[j] = a0;
       }
@@ -572,8 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_ld16(tacc + c, r);
           ptx::tmem_wait_ld();
           const int col = tn * BN + c;
-          if (red_quad_ok(args, col)) red16_quad(args, rbase, row_ok, col, r, lane);
-          else if (row_ok && col < args.N) store16(args, rbase, col, r);
+          if (row_ok && col < args.N) store16(args, rbase, col, r);
         }
       }
       ptx::tc_fence_before();
@@ -770,8 +731,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           ptx::tmem_ld16(tacc + c, r);
           ptx::tmem_wait_ld();
           const int col = tn * BNP + c;
-          if (red_quad_ok(args, col)) red16_quad(args, rbase, row_ok, col, r, lane);
-          else if (row_ok && col < args.N) store16(args, rbase, col, r);
+          if (row_ok && col < args.N) store16(args, rbase, col, r);
         }
       }
       ptx::tc_fence_before();
@@ -1124,16 +1084,15 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   } else {
     fill_units(a, BM, BN, num_sms(), 0.45 * BN / 256.0, true);
   }
-  const Epi red = kernel_variant(2) == 1 ? kEpiF32RedQuad : kEpiF32Red;
   if (accumulate) {
     // dw += result: fire-and-forget red.add for any split count (the engine keeps its
     // gradient accumulator zeroed between steps, so this is also its overwrite path)
-    a.epi = red;
+    a.epi = kEpiF32Red;
   } else if (a.splits > 1 || a.sk_len > 0) {
     // partial sums race into dw: zero it first
     CFT_CUDA(cudaMemset2DAsync(dw, sizeof(float) * in_dim, 0, sizeof(float) * in_dim, a.M,
                                stream));
-    a.epi = red;
+    a.epi = kEpiF32Red;
   } else {
     a.epi = kEpiF32;
   }

@@ -61,19 +61,22 @@ class H:
     eta, beta1, beta2, epsilon, weight_decay = 1e-3, 0.9, 0.999, 1e-8, 0.0
 
 
-for var in (2, 3):
+for var in (3,):
     N.check(N.lib.cft_set_kernel_variant(0, var), "variant")
     med, lo = measure(lambda: ops.adamw_slice(master, m, v, g, H, 3, param=param, segments=segs,
                                               stats=stats, zero_grad=True))
     print(json.dumps({"op": "adamw", "variant": var, "median_ms": round(med, 4), "min_ms": round(lo, 4),
                       "GBps_30B": round(30 * E / med / 1e6)}), flush=True)
 N.check(N.lib.cft_set_kernel_variant(0, 3), "variant")
+med, lo = measure(lambda: ops.grad_stats(g, 1.0, stats=stats))
+print(json.dumps({"op": "grad_stats", "median_ms": round(med, 4), "min_ms": round(lo, 4),
+                  "GBps_4B": round(4 * E / med / 1e6)}), flush=True)
 del master, m, v, g, param
 
 V = 128256
 logits = ((torch.rand(8192, V, device=dev) - 0.5) * 8).to(torch.bfloat16)
 labels = torch.randint(0, V, (8192,), device=dev, dtype=torch.int32)
-for var in (0, 3, 0, 3):
+for var in (0,):
     N.check(N.lib.cft_set_kernel_variant(1, var), "variant")
     med, lo = measure(lambda: ops.softmax_ce(logits, labels, dy=logits))
     print(json.dumps({"op": "softmax_ce", "variant": var, "median_ms": round(med, 4), "min_ms": round(lo, 4),
