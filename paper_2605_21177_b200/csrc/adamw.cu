@@ -62,27 +62,16 @@ __global__ void __launch_bounds__(kThreads) grad_stats_kernel(const T* __restric
     const long long n4 = (reinterpret_cast<uintptr_t>(g) & 15) == 0 ? n / 4 : 0;
     const float4* g4 = reinterpret_cast<const float4*>(g);
     const float fs = static_cast<float>(scale);
-    // four independent 16-byte loads in flight per thread before any use
-    constexpr int U = 4;
-    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n4; i0 += U * stride) {
-      float4 v[U];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+      const float4 v = g4[i];
+      const float e[4] = {v.x * fs, v.y * fs, v.z * fs, v.w * fs};
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const long long i = i0 + k * stride;
-        v[k] = i < n4 ? __ldcs(g4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const long long i = i0 + k * stride;
-        const float e[4] = {v[k].x * fs, v[k].y * fs, v[k].z * fs, v[k].w * fs};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (!isfinite(e[q])) {
-            ++nbad;
-            bad = min(bad, 4 * i + q);
-          } else {
-            acc += static_cast<double>(e[q]) * static_cast<double>(e[q]);
-          }
+      for (int q = 0; q < 4; ++q) {
+        if (!isfinite(e[q])) {
+          ++nbad;
+          bad = min(bad, 4 * i + q);
+        } else {
+          acc += static_cast<double>(e[q]) * static_cast<double>(e[q]);
         }
       }
     }

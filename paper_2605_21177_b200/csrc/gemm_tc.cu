@@ -528,13 +528,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (args.rope_cs && tn * BN + half * (BN / 2) < args.rope_cols) {
         rope_epilogue(args, tacc, row, row_ok, tn * BN, half * (BN / 2), (half + 1) * (BN / 2));
       } else {
+        // two TMEM loads in flight per wait: the epilogue of a single-wave GEMM (narrow
+        // slices, split-K) is exposed after the mainloop and latency-bound
 #pragma unroll 1
-        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
-          uint32_t r[16];
-          ptx::tmem_ld16(tacc + c, r);
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+          uint32_t r0[16], r1[16];
+          ptx::tmem_ld16(tacc + c, r0);
+          ptx::tmem_ld16(tacc + c + 16, r1);
           ptx::tmem_wait_ld();
           const int col = tn * BN + c;
-          if (row_ok && col < args.N) store16(args, rbase, col, r);
+          if (row_ok && col < args.N) store16(args, rbase, col, r0);
+          if (row_ok && col + 16 < args.N) store16(args, rbase, col + 16, r1);
         }
       }
       ptx::tc_fence_before();
@@ -725,13 +729,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       } else if (args.rope_cs && tn * BNP + half * (BNP / 2) < args.rope_cols) {
         rope_epilogue(args, tacc, row, row_ok, tn * BNP, half * (BNP / 2), (half + 1) * (BNP / 2));
       } else {
+        // two TMEM loads in flight per wait: the epilogue of a single-wave GEMM (narrow
+        // slices, split-K) is exposed after the mainloop and latency-bound
 #pragma unroll 1
-        for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 16) {
-          uint32_t r[16];
-          ptx::tmem_ld16(tacc + c, r);
+        for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 32) {
+          uint32_t r0[16], r1[16];
+          ptx::tmem_ld16(tacc + c, r0);
+          ptx::tmem_ld16(tacc + c + 16, r1);
           ptx::tmem_wait_ld();
           const int col = tn * BNP + c;
-          if (row_ok && col < args.N) store16(args, rbase, col, r);
+          if (row_ok && col < args.N) store16(args, rbase, col, r0);
+          if (row_ok && col + 16 < args.N) store16(args, rbase, col + 16, r1);
         }
       }
       ptx::tc_fence_before();
