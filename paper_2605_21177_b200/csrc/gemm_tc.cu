@@ -1080,7 +1080,16 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
       return e ? std::atoi(e) : 0;
     }();
     const double c128 = cost(a128, 0.38), c256 = cost(a256, 0.40);
-    if (g_policy == 0 && sk_mode != 2 &&
+    static const int forced_splits = [] {  // experiments: 256x256 pair tiles, this split count
+      const char* e = std::getenv("CFT_WGRAD_SPLITS");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (forced_splits > 0) {
+      a = a256;
+      a.kb_per_split = (a.total_kb + forced_splits - 1) / forced_splits;
+      a.splits = (a.total_kb + a.kb_per_split - 1) / a.kb_per_split;
+      a.num_units = a.tiles_m * a.tiles_n * a.splits;
+    } else if (g_policy == 0 && sk_mode != 2 &&
         (sk_mode == 1 || cost_sk < 0.95 * std::min(c128, c256))) {
       a = ask;
     } else if (g_policy == 0 && c128 < c256) {
