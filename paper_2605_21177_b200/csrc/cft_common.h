@@ -59,7 +59,7 @@ inline int num_sms() {
 
 // Kernel variant per operator, for A/B measurements inside one process (defaults from the
 // environment; see cft_set_kernel_variant and include/chunkft_b200.h for the variants).
-constexpr int kNumVariantOps = 2;
+constexpr int kNumVariantOps = 3;
 int& kernel_variant(int op);
 
 inline void check_launch(const char* what) {

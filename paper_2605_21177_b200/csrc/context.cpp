@@ -67,6 +67,10 @@ int& kernel_variant(int op) {
         const std::string k = e ? e : "";
         return k == "cluster" ? 1 : k == "cluster3" ? 2 : k == "vec1024" ? 3 : 0;
       }(),
+      [] {
+        const char* e = std::getenv("CFT_GEMM_PDL");
+        return e && std::string(e) == "0" ? 0 : 1;
+      }(),
 
   };
   if (op < 0 || op >= kNumVariantOps) throw Error("kernel_variant: unknown operator");

@@ -426,6 +426,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tslot;
+  // PDL: the prologue above (barriers, TMEM, descriptor prefetch) overlapped the previous
+  // kernel's tail; every global read / write below comes after its completion
+  ptx::grid_dep_wait();
+  ptx::grid_dep_launch();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -620,6 +624,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tslot;
+  ptx::grid_dep_wait();  // PDL, as in gemm_bf16_kernel
+  ptx::grid_dep_launch();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -787,6 +793,25 @@ CUtensorMap cached_map(const void* base, uint64_t inner, uint64_t outer, uint64_
   return m;
 }
 
+// GEMM launches carry the programmatic-stream-serialization attribute (kernel variant op 2,
+// default on): the GEMM's prologue overlaps the previous kernel's tail and it waits in
+// grid_dep_wait() before touching memory.
+template <typename K>
+void launch_pdl(K kern, int grid, size_t smem, cudaStream_t stream, const CUtensorMap& ta,
+                const CUtensorMap& tb, const Args& a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kernel_variant(2) ? 1 : 0;
+  CFT_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
+}
+
 template <bool A_MN, bool B_MN, int BN>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream_t stream) {
   using C_ = Cfg<BN>;
@@ -798,7 +823,7 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream_t s
     attr_done = true;
   }
   const int grid = std::min(a.num_units, num_sms());
-  kern<<<grid, kThreads, C_::SMEM, stream>>>(ta, tb, a);
+  launch_pdl(kern, grid, C_::SMEM, stream, ta, tb, a);
   check_launch("gemm_bf16_kernel");
 }
 
@@ -870,7 +895,7 @@ void launch_2sm(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream
     attr_done = true;
   }
   const int pairs = std::min(a.num_units, num_sms() / 2);
-  kern<<<2 * pairs, kThreads, PairCfg<BNP>::SMEM, stream>>>(ta, tb, a);
+  launch_pdl(kern, 2 * pairs, PairCfg<BNP>::SMEM, stream, ta, tb, a);
   check_launch("gemm_bf16_2sm_kernel");
 }
 

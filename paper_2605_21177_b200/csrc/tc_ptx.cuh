@@ -243,6 +243,17 @@ __device__ __forceinline__ void ld_global_cs_256(const void* addr, uint32_t (&w)
                : "l"(addr));
 }
 
+// Programmatic dependent launch: a kernel launched with programmatic stream serialization may
+// start (and run its prologue) while the previous kernel drains; it must wait here before its
+// first global-memory access.  launch_dependents lets the next such kernel start early.  Both
+// are no-ops for an ordinary launch.
+__device__ __forceinline__ void grid_dep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_dep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // 1-D bulk copy global -> shared (TMA engine, no tensor map), completion counted in bytes on
 // an mbarrier; the L2 evict-first policy keeps a streamed-once operand from displacing others
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {

@@ -121,3 +121,29 @@ def test_random_stack_matches_live_reference(cuda, trial):
     if exact:
         assert np.array_equal(got.params, want["params"]), (layers, loss, c)
         assert np.array_equal(got.loss, want["loss"]), (layers, loss, c)
+
+
+@pytest.mark.skipif(not _have_ref(), reason="oracle/_ref (the reference library build) is absent")
+@pytest.mark.parametrize("dtype,tol", [("fp32", 1e-5), ("bf16", 2e-2)])
+@pytest.mark.parametrize("trial", range(0, TRIALS, 3))
+def test_random_stack_reduced_precision(cuda, trial, dtype, tol):
+    """The same random stacks on the fp32 path (fp32 operands and state; SURVEY 8 tolerance 1e-5)
+    and the bf16 tensor-core path (bf16 operands, fp32 accumulation and state; 2e-2), normwise on
+    the loss trajectory and the final parameters against the live fp64 reference."""
+    from paper_2605_21177_b200.engine import AdamWHyper, TrainOptions, run_training
+    from paper_2605_21177_b200.plan import ScheduleConfig
+    layers, loss, batches, c = draw(trial)
+    init = R.init_params(layers, seed=c["seed"])
+    want = R.train(layers, loss, init, batches, K=c["K"], T=c["T"], steps=c["steps"],
+                   prefetch=c["prefetch"], micro_batches=c["micro_batches"])
+    o = TrainOptions()
+    o.schedule = ScheduleConfig(K=c["K"], T=c["T"], total_steps=c["steps"], prefetch=c["prefetch"])
+    o.hyper = AdamWHyper(1e-3, 0.9, 0.999, 1e-8, 0.0)
+    o.micro_batches = c["micro_batches"]
+    o.dtype = dtype
+    o.offload = c["offload"]
+    got = run_training(engine_model(layers, loss), init, batches, o)
+    assert got.plan_hash == want["plan_hash"]
+    assert got.chunk.tolist() == want["chunk"].tolist()
+    assert rel(got.loss, want["loss"]) <= tol, (layers, loss, c)
+    assert rel(got.params, want["params"]) <= tol, (layers, loss, c)
