@@ -1,8 +1,5 @@
 # scratch GPU session script (run via gpurun; outputs under gpurun_out/)
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/s21_pytest.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/s21_pytest.log
-summ='import json,sys;d=json.load(open(sys.argv[1]));p=d["phases_ms_per_step"];print(sys.argv[1],round(d["value"]),round(d["ms_per_step"],2),"e2e",round(d["e2e"]["value"]),"clk",d["clocks"]["sm_mhz"])'
-B="python bench.py --no-cpu-baseline --no-sweep"
-for r in 1 2; do
-CFT_GEMM_PDL=0 timeout 900 $B > gpurun_out/s21_nopdl_$r.json 2>/dev/null; python -c "$summ" gpurun_out/s21_nopdl_$r.json
-timeout 900 $B > gpurun_out/s21_pdl_$r.json 2>/dev/null; python -c "$summ" gpurun_out/s21_pdl_$r.json
-done
+timeout 900 python bench.py > gpurun_out/s23_bench.json 2> gpurun_out/s23_bench.err; echo "bench exit $?"
+timeout 900 python bench.py --workload llama70b > gpurun_out/s23_bench70b.json 2> gpurun_out/s23_bench70b.err; echo "bench70b exit $?"
+timeout 600 python bench.py --workload linear4096 > gpurun_out/s23_bench_linear.json 2> gpurun_out/s23_bench_linear.err; echo "bench linear exit $?"
+python tools/gemm_traffic_step.py 30 > /dev/null 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/s23_launches.csv python tools/gemm_traffic_step.py 30 > gpurun_out/s23_traffic.json 2> gpurun_out/s23_ncu.err; echo "ncu exit $?"
