@@ -468,7 +468,8 @@ def run_llama(args, rank, world, local_rank):
     opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=total, prefetch=True),
                         dtype="bf16", plan="budget", budget_bytes=budget, offload=offload,
                         check_every_step=False,
-                        shard_rank=rank if sharded else 0, shard_world=world if sharded else 1)
+                        shard_rank=rank if sharded else 0, shard_world=world if sharded else 1,
+                        remat=args.remat)
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
         eng = ChunkEngine(model, None, B, opts, stream=stream, seed=1234)
@@ -599,7 +600,9 @@ def run_llama(args, rank, world, local_rank):
             "warmup": W, "ms_per_step": ms / S, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded uniform token ids; random-init weights, U(-0.5,0.5)/sqrt(fan-in))",
-            "config": {"workload": workload_name, "layers": model.layers, "params": model.num_params(),
+            "config": {"workload": workload_name + (", activations re-materialised per suffix layer"
+                                                    if args.remat else ""),
+                       "layers": model.layers, "params": model.num_params(), "remat": bool(args.remat),
                        "tokens_per_gpu_per_step": tokens_per_gpu,
                        "global_batch_tokens": tokens_per_gpu * world, "seq_len": model.seq,
                        "K": K, "T": 1, "budget_bytes": budget, "plan_hash": f"{plan.hash():016x}",
@@ -699,6 +702,9 @@ def main():
     ap.add_argument("--fusion", type=int, default=3,
                     help="A/B: epilogue fusion mask (1 SwiGLU, 2 RoPE; 0 = separate kernels)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[1] sliced-dW sweep")
+    ap.add_argument("--remat", action="store_true",
+                    help="llama workloads: keep only layer inputs, re-materialise the backward "
+                         "suffix layer by layer (fits e.g. the full 80-layer 70B shape on 1 GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -338,7 +338,9 @@ typedef struct {
                             (Llama engine; captured on the chunk's first step) */
   int32_t shard_rank;    /* sharded optimizer state: this rank's index and the */
   int32_t shard_world;   /* number of ranks; 0 or 1 = every rank keeps the whole chunk state */
-  int32_t pad_;
+  int32_t remat;         /* Llama engine, 1: keep only each layer's input; the layers of the
+                            active chunk's backward suffix are re-materialised one at a time
+                            (north star item 4) -- ~35 GB less HBM for the 8B shape */
   double clip_max_norm;  /* > 0: clip the chunk's mean gradient to this global L2 norm inside the
                             fused AdamW (no reference counterpart); 0 = off */
 } cft_engine_config;

@@ -33,6 +33,7 @@ static cft::EngineConfig to_config(const cft_engine_config* c) {
   cfg.shard_rank = c->shard_rank;
   cfg.shard_world = c->shard_world > 1 ? c->shard_world : 1;
   cfg.clip_max_norm = c->clip_max_norm;
+  cfg.remat = c->remat;
   return cfg;
 }
 

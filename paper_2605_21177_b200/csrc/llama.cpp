@@ -79,6 +79,12 @@ void Engine::llama_alloc() {
     LlamaLayerBufs& b = lb_[l];
     b.x = A(N * d);
     if (l == s.layers) break;  // x[L] only
+    if (cfg_.remat && l > 0) {  // one set of layer internals, shared (re-materialised)
+      const void* x = b.x;
+      b = lb_[0];
+      b.x = const_cast<void*>(x);
+      continue;
+    }
     b.a = A(N * d);
     b.qkv = A(N * qkv);
     b.o = A(N * q);
@@ -267,7 +273,9 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
   if (cft_embedding_gather(CFT_BF16, P(0), d, tok, N, lb_[0].x, st) != CFT_OK)
     throw Error(last_error());
   pe();
-  for (int l = 0; l < L; ++l) {
+  // one decoder layer's forward from its input x_l; `keep_ug`: also store [u | g] (the SwiGLU
+  // backward reads it); `out`: run the w2 GEMM into x_{l+1} (a re-materialisation stops before)
+  auto layer_fwd = [&](int l, bool keep_ug, bool out) {
     LlamaLayerBufs& z = lb_[l];
     pb(kFwdOther);
     llama::rms_fwd(static_cast<bf16*>(z.x), P(id(l, 0)), N, S.d, (float)S.eps,
@@ -299,9 +307,9 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     // w1|w3 stacked with SwiGLU in the epilogue; [u | g] is kept only where the backward
     // suffix will read it
     pb(kFwdGemm);
-    gemm_work(kFwdGemm, N, 2 * F, d, 2.0 * N * F, stop <= id(l, 7) ? 4.0 * N * F : 0.0);
+    gemm_work(kFwdGemm, N, 2 * F, d, 2.0 * N * F, keep_ug ? 4.0 * N * F : 0.0);
     const bool fused = tc::linear_fwd_swiglu(z.m, N, d, P(id(l, 6)), F, z.s,
-                                             stop <= id(l, 7) ? z.ug : nullptr, st);
+                                             keep_ug ? z.ug : nullptr, st);
     if (!fused) tc::linear_fwd(z.m, N, d, P(id(l, 6)), 2 * F, z.ug, st);
     pe();
     if (!fused) {
@@ -309,11 +317,17 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
       llama::swiglu_fwd(static_cast<bf16*>(z.ug), N, S.ffn, static_cast<bf16*>(z.s), st);
       pe();
     }
+    if (!out) return;
     pb(kFwdGemm);
     gemm_work(kFwdGemm, N, d, F, 2.0 * N * d, 2.0 * N * d);  // + residual read
     tc::linear_fwd(z.s, N, F, P(id(l, 8)), d, lb_[l + 1].x, st, z.h);  // x' = h + s W2^T
     pe();
-  }
+  };
+  // [u | g] is kept only where the backward suffix will read it; with re-materialisation the
+  // top layer's internals are still in the shared buffers when the backward starts, every
+  // other suffix layer is recomputed there
+  for (int l = 0; l < L; ++l)
+    layer_fwd(l, stop <= id(l, 7) && (!cfg_.remat || l == L - 1), true);
   pb(kFwdOther);
   llama::rms_fwd(static_cast<bf16*>(lb_[L].x), P(norm_id), N, S.d, (float)S.eps,
                  static_cast<bf16*>(l_xf_), l_rstdf_, st);
@@ -354,6 +368,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
   }
   for (int l = L - 1; l >= 0 && below(id(l, 8) + 1); --l) {
     LlamaLayerBufs& z = lb_[l];
+    if (cfg_.remat && l < L - 1) layer_fwd(l, stop <= id(l, 7), false);  // re-materialise
     // x_{l+1} = h + s W2^T      (GX = dL/dx_{l+1})
     wgrad(id(l, 8), l_gx_, d, z.s, F, 0);
     if (!need(id(l, 7))) break;

@@ -37,7 +37,7 @@ class EngineConfigC(C.Structure):
                 ("hyper", N.AdamWHyperC), ("full_backward", C.c_int32),
                 ("check_every_step", C.c_int32), ("grad_scale", C.c_double),
                 ("cuda_graphs", C.c_int32), ("shard_rank", C.c_int32),
-                ("shard_world", C.c_int32), ("pad_", C.c_int32), ("clip_max_norm", C.c_double)]
+                ("shard_world", C.c_int32), ("remat", C.c_int32), ("clip_max_norm", C.c_double)]
 
 
 class BatchC(C.Structure):
@@ -238,6 +238,7 @@ class TrainOptions:
     shard_rank: int = 0           # sharded optimizer state; world 1 = unsharded
     shard_world: int = 1
     clip_max_norm: float = 0.0    # > 0: global-norm gradient clip inside the fused AdamW
+    remat: bool = False           # Llama engine: keep layer inputs only, re-materialise the suffix
 
 
 class ChunkEngine:
@@ -266,6 +267,7 @@ class ChunkEngine:
         cfg.shard_rank = o.shard_rank
         cfg.shard_world = o.shard_world
         cfg.clip_max_norm = o.clip_max_norm
+        cfg.remat = int(o.remat)
         cfg.bandwidth_bytes_per_step = o.schedule.bandwidth_bytes_per_step
         cfg.budget_bytes = o.budget_bytes
         h = o.hyper

@@ -1,5 +1,7 @@
 # scratch GPU session script (run via gpurun; outputs under gpurun_out/)
-timeout 900 python bench.py > gpurun_out/s23_bench.json 2> gpurun_out/s23_bench.err; echo "bench exit $?"
-timeout 900 python bench.py --workload llama70b > gpurun_out/s23_bench70b.json 2> gpurun_out/s23_bench70b.err; echo "bench70b exit $?"
-timeout 600 python bench.py --workload linear4096 > gpurun_out/s23_bench_linear.json 2> gpurun_out/s23_bench_linear.err; echo "bench linear exit $?"
-python tools/gemm_traffic_step.py 30 > /dev/null 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/s23_launches.csv python tools/gemm_traffic_step.py 30 > gpurun_out/s23_traffic.json 2> gpurun_out/s23_ncu.err; echo "ncu exit $?"
+free -g | head -2; nproc
+timeout 900 python -m pytest tests/test_gpu_llama.py -q -x > gpurun_out/s24_pytest.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/s24_pytest.log
+timeout 900 python bench.py --remat --no-cpu-baseline --no-sweep --no-e2e > gpurun_out/s24_bench_remat.json 2> gpurun_out/s24_bench_remat.err; echo "bench exit $?"
+python -c "
+import json;d=json.load(open('gpurun_out/s24_bench_remat.json'))
+print(round(d['value']), round(d['ms_per_step'],2), d['device_bytes'], d['flat_memory'], d['clocks'])"
