@@ -136,6 +136,8 @@ int64_t cft_scheduler_transfer_inflight_bytes(cft_scheduler* s, int64_t step);
 int64_t cft_scheduler_noop_loads(const cft_scheduler* s);
 int64_t cft_scheduler_num_events(const cft_scheduler* s);
 int cft_scheduler_get_events(const cft_scheduler* s, cft_transfer_event* out, int64_t cap);
+/* write_transfer_log_csv (schedule.cpp:137-154) of this scheduler's events. */
+int cft_scheduler_write_transfer_log_csv(const cft_scheduler* s, const char* path);
 
 /* ===================================================================== */
 /* 2. Parity kernels: chunkft::kernels (include/chunkft/kernels.hpp:20-65) */
@@ -417,6 +419,11 @@ int64_t cft_engine_device_bytes(const cft_engine* e);
 uint64_t cft_engine_plan_hash(const cft_engine* e);
 int cft_engine_plan_json(cft_engine* e, char* buf, int64_t cap, int64_t* needed);
 int64_t cft_engine_transfer_events(cft_engine* e, cft_transfer_event* out, int64_t cap);
+/* The reference's artifact files (FORMATS.md), byte-compatible: trajectory.csv
+ * (write_trajectory_csv, trainer.cpp:103-114; loss and grad_norm_sq as "%.17g") and
+ * transfer_log.csv (write_transfer_log_csv, schedule.cpp:137-154).  Errors name the path. */
+int cft_engine_write_trajectory_csv(cft_engine* e, const char* path);
+int cft_engine_write_transfer_log_csv(cft_engine* e, const char* path);
 int cft_engine_chunk_counters(cft_engine* e, uint64_t* n_out);
 /* CUDA-event times of the last step: inputs, forward, backward, stats+update (ms). */
 int cft_engine_phase_ms(cft_engine* e, float* ms4);

@@ -35,6 +35,7 @@ if REF is not None:
        vp, vp, vp, i64, vp, vp, vp, vp, vp, CT.c_char_p, i64)
     _s("ref_schedule", i64, CT.c_int, CT.c_int, i64, CT.c_int, i64, vp, vp, vp, vp, vp, vp, vp, i64,
        vp, vp, vp)
+    _s("ref_schedule_csv", CT.c_int, CT.c_int, CT.c_int, i64, CT.c_int, i64, vp, CT.c_char_p)
     _s("ref_openmp_threads", CT.c_int)
     _s("ref_set_backend", None, CT.c_int)
     _s("ref_linear_forward", None, vp, CT.c_int, CT.c_int, vp, CT.c_int, vp, vp)
@@ -106,6 +107,14 @@ def schedule(K, T, total_steps, chunk_elems, prefetch=False, bw=0):
                 events=[(int(ev[0][i]), int(ev[1][i]), int(ev[2][i]), int(ev[3][i]), int(ev[4][i]))
                         for i in range(ne)],
                 device_bytes=dev.tolist(), inflight=infl.tolist(), noop_loads=int(noop[0]))
+
+
+def schedule_csv(K, T, total_steps, chunk_elems, path, prefetch=False, bw=0):
+    """The reference's write_transfer_log_csv of a dry-run schedule (schedule.cpp:137-154)."""
+    _need()
+    ce = np.asarray(chunk_elems, np.int64)
+    if REF.ref_schedule_csv(K, T, total_steps, int(prefetch), bw, _p(ce), str(path).encode()) != 0:
+        raise ValueError(_err())
 
 
 def set_backend(openmp: bool):

@@ -176,6 +176,33 @@ int64_t ref_schedule(int K, int T, int64_t total_steps, int prefetch, int64_t bw
   }
 }
 
+// The same dry run, written by the reference's own write_transfer_log_csv (schedule.cpp:137-154).
+int ref_schedule_csv(int K, int T, int64_t total_steps, int prefetch, int64_t bw,
+                     const int64_t* chunk_elems, const char* path) {
+  try {
+    ChunkPlan plan;
+    plan.chunks.resize(static_cast<size_t>(K));
+    for (int c = 0; c < K; ++c) plan.chunks[c].elements = chunk_elems[c];
+    ScheduleConfig cfg;
+    cfg.K = K;
+    cfg.T = T;
+    cfg.total_steps = total_steps;
+    cfg.prefetch = prefetch != 0;
+    cfg.bandwidth_bytes_per_step = bw;
+    RotationScheduler sched(cfg, &plan, nullptr);
+    for (int64_t t = 0; t < total_steps; ++t) {
+      sched.step_begin();
+      sched.step_end();
+    }
+    sched.finish();
+    write_transfer_log_csv(sched.events(), path);
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(e.what());
+    return -1;
+  }
+}
+
 // ---- kernels (backend 0 serial, 1 openmp) ----
 int ref_openmp_threads() { return kernels::openmp_max_threads(); }
 void ref_set_backend(int b) {
@@ -371,12 +398,14 @@ int ref_train(const int32_t* layers, int n_layers, int loss_kind, const double* 
     *plan_hash_out = plan_hash(plan);
     if (chunk_n_out)
       for (int c = 0; c < plan.K(); ++c) chunk_n_out[c] = r.states[c].n;
-    if (ckpt_dir) {  // runner.cpp:182-187 naming
+    if (ckpt_dir) {  // runner.cpp:177-187 naming: checkpoints plus the artifact CSVs
       for (int c = 0; c < plan.K(); ++c) {
         char name[32];
         std::snprintf(name, sizeof(name), "chunk_%04d.bin", c);
         write_chunk_checkpoint(r.states[c], plan_hash(plan), std::filesystem::path(ckpt_dir) / name);
       }
+      write_trajectory_csv(r.trajectory, std::filesystem::path(ckpt_dir) / "trajectory.csv");
+      write_transfer_log_csv(r.transfers, std::filesystem::path(ckpt_dir) / "transfer_log.csv");
     }
     return 0;
   } catch (const std::exception& e) {

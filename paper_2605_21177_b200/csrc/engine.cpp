@@ -899,6 +899,7 @@ void Engine::step_end() {
   CFT_CUDA(cudaEventRecord(stats_ev_[t_ % 4], s));
   traj_step_.push_back(t_);
   traj_chunk_.push_back(c);
+  traj_epoch_.push_back(sched_->active_index_counter() / cfg_.K);  // trainer.cpp:69
 
   const int off = sched_->step_end();
   if (off >= 0) offload_chunk(off);
@@ -953,6 +954,24 @@ void Engine::trajectory(int64_t* step, int32_t* chunk, double* loss, double* gsq
     if (gsq) gsq[i] = h[0];
   }
   *n = k;
+}
+
+// The reference's artifact files (FORMATS.md): trajectory.csv (trainer.cpp:103-114) and
+// transfer_log.csv (schedule.cpp:137-154), byte-compatible.
+void Engine::write_trajectory_csv(const std::string& path) const {
+  const int64_t k = static_cast<int64_t>(traj_step_.size());
+  std::vector<int64_t> step(k);
+  std::vector<int32_t> chunk(k);
+  std::vector<double> loss(k), gsq(k);
+  int64_t n = 0;
+  trajectory(step.data(), chunk.data(), loss.data(), gsq.data(), &n);
+  std::vector<host::TrajectoryRow> rows(n);
+  for (int64_t i = 0; i < n; ++i)
+    rows[i] = {step[i], traj_epoch_[i], static_cast<int>(step[i] % cfg_.T), chunk[i], loss[i], gsq[i]};
+  host::write_trajectory_csv(rows, path);
+}
+void Engine::write_transfer_log_csv(const std::string& path) const {
+  host::write_transfer_log_csv(sched_->events(), path);
 }
 
 void Engine::stats_for_step(int64_t t, double* loss, double* gsq) {

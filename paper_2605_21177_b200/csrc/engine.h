@@ -112,6 +112,8 @@ class Engine {
 
   // results
   void trajectory(int64_t* step, int32_t* chunk, double* loss, double* gsq, int64_t* n) const;
+  void write_trajectory_csv(const std::string& path) const;
+  void write_transfer_log_csv(const std::string& path) const;
   void params_from_masters(double* out);            // fp64 copy of the authoritative params
   void params_device(double* out);                  // the compute-dtype params (widened)
   void grad_buffer(void** ptr, int64_t* n, int* dtype);
@@ -294,6 +296,7 @@ class Engine {
   int mb_done_ = 0;
   bool finished_ = false;
   std::vector<int32_t> traj_chunk_;
+  std::vector<int64_t> traj_epoch_;
   std::vector<int64_t> traj_step_;
 };
 

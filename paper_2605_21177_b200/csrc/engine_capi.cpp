@@ -153,6 +153,20 @@ int64_t cft_engine_transfer_events(cft_engine* e, cft_transfer_event* out, int64
   return n;
 }
 
+int cft_engine_write_trajectory_csv(cft_engine* e, const char* path) {
+  return guarded([&] {
+    CFT_CHECK(path != nullptr, "write_trajectory_csv: null path");
+    e->p->write_trajectory_csv(path);
+  });
+}
+
+int cft_engine_write_transfer_log_csv(cft_engine* e, const char* path) {
+  return guarded([&] {
+    CFT_CHECK(path != nullptr, "write_transfer_log_csv: null path");
+    e->p->write_transfer_log_csv(path);
+  });
+}
+
 int cft_engine_chunk_counters(cft_engine* e, uint64_t* n) {
   return guarded([&] { e->p->chunk_counters(n); });
 }

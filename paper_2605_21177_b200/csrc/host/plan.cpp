@@ -6,6 +6,8 @@
 #include "host/plan.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <fstream>
 #include <cmath>
 #include <map>
 
@@ -350,6 +352,41 @@ int64_t RotationScheduler::transfer_inflight_bytes(int64_t step) {
   for (const auto& w : windows_)
     if (w.begin <= step && step < w.end) sum += w.bytes;
   return sum;
+}
+
+}  // namespace cft::host
+
+namespace cft::host {
+
+void write_transfer_log_csv(const std::vector<TransferEvent>& events, const std::string& path) {
+  std::vector<TransferEvent> sorted = events;
+  std::stable_sort(sorted.begin(), sorted.end(), [](const TransferEvent& a, const TransferEvent& b) {
+    if (a.step != b.step) return a.step < b.step;
+    if (a.chunk != b.chunk) return a.chunk < b.chunk;
+    return a.dir < b.dir;
+  });
+  std::ofstream out(path);
+  if (!out) throw PlanError("cannot open '" + path + "' for writing");
+  out << "step,chunk,direction,bytes,latency_steps\n";
+  for (const auto& e : sorted)
+    out << e.step << ',' << e.chunk << ',' << (e.dir == 0 ? "load" : "offload") << ',' << e.bytes
+        << ',' << e.latency_steps << '\n';
+  if (!out) throw PlanError("write failed for '" + path + "'");
+}
+
+void write_trajectory_csv(const std::vector<TrajectoryRow>& rows, const std::string& path) {
+  auto fmt = [](double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof(buf), "%.17g", v);
+    return std::string(buf);
+  };
+  std::ofstream out(path);
+  if (!out) throw PlanError("cannot open '" + path + "' for writing");
+  out << "step,chunk_epoch,inner_step,chunk,loss,grad_norm_sq\n";
+  for (const auto& r : rows)
+    out << r.step << ',' << r.chunk_epoch << ',' << r.inner_step << ',' << r.chunk << ','
+        << fmt(r.loss) << ',' << fmt(r.grad_norm_sq) << '\n';
+  if (!out) throw PlanError("write failed for '" + path + "'");
 }
 
 }  // namespace cft::host

@@ -89,6 +89,22 @@ struct TransferEvent {
   int64_t latency_steps = 0;
 };
 
+// transfer_log.csv (schedule.cpp:137-154, FORMATS.md): stable-sorted by (step, chunk, dir),
+// header "step,chunk,direction,bytes,latency_steps".
+void write_transfer_log_csv(const std::vector<TransferEvent>& events, const std::string& path);
+
+// TrainTrajectoryEntry (trainer.hpp:26-33) and trajectory.csv (trainer.cpp:103-114): doubles
+// printed with "%.17g" (csvio.cpp:13-17).
+struct TrajectoryRow {
+  int64_t step = 0;
+  int64_t chunk_epoch = 0;  // active_index_counter / K while the step runs (trainer.cpp:69)
+  int inner_step = 0;       // t mod T
+  int chunk = -1;
+  double loss = 0.0;
+  double grad_norm_sq = 0.0;
+};
+void write_trajectory_csv(const std::vector<TrajectoryRow>& rows, const std::string& path);
+
 // What the caller must physically do at a boundary.
 struct BeginActions {
   int active = -1;

@@ -210,4 +210,11 @@ int cft_scheduler_get_events(const cft_scheduler* s, cft_transfer_event* out, in
   });
 }
 
+int cft_scheduler_write_transfer_log_csv(const cft_scheduler* s, const char* path) {
+  return guard([&] {
+    if (!path) throw PlanError("write_transfer_log_csv: null path");
+    write_transfer_log_csv(s->sched.events(), path);
+  });
+}
+
 }  // extern "C"

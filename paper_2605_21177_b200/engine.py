@@ -71,6 +71,8 @@ for _n, _r, _a in [
     ("cft_engine_plan_hash", C.c_uint64, [C.c_void_p]),
     ("cft_engine_plan_json", C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, _P(C.c_int64)]),
     ("cft_engine_transfer_events", C.c_int64, [C.c_void_p, _P(N.TransferEventC), C.c_int64]),
+    ("cft_engine_write_trajectory_csv", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("cft_engine_write_transfer_log_csv", C.c_int, [C.c_void_p, C.c_char_p]),
     ("cft_engine_chunk_counters", C.c_int, [C.c_void_p, C.c_void_p]),
     ("cft_engine_phase_ms", C.c_int, [C.c_void_p, C.c_void_p]),
     ("cft_engine_profile", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
@@ -379,6 +381,14 @@ class ChunkEngine:
         tdt = {N.CFT_BF16: torch.bfloat16, N.CFT_F32: torch.float32, N.CFT_F64: torch.float64}[dt.value]
         world = self.opt.shard_world
         return _wrap_device(p.value, n.value, tdt), off.value, n.value // world
+
+    def write_trajectory_csv(self, path) -> None:
+        """trajectory.csv exactly as the reference's write_trajectory_csv (trainer.cpp:103-114)."""
+        N.check(_L.cft_engine_write_trajectory_csv(self._h, str(path).encode()), "write_trajectory_csv")
+
+    def write_transfer_log_csv(self, path) -> None:
+        """transfer_log.csv exactly as the reference's write_transfer_log_csv (schedule.cpp:137-154)."""
+        N.check(_L.cft_engine_write_transfer_log_csv(self._h, str(path).encode()), "write_transfer_log_csv")
 
     def gather_end(self):
         N.check(_L.cft_engine_gather_end(self._h), "gather_end")

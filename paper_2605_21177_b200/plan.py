@@ -44,6 +44,7 @@ for _name, _res, _args in [
     ("cft_scheduler_noop_loads", C.c_int64, [C.c_void_p]),
     ("cft_scheduler_num_events", C.c_int64, [C.c_void_p]),
     ("cft_scheduler_get_events", C.c_int, [C.c_void_p, _P(N.TransferEventC), C.c_int64]),
+    ("cft_scheduler_write_transfer_log_csv", C.c_int, [C.c_void_p, C.c_char_p]),
 ]:
     _fn = getattr(_L, _name)
     _fn.restype = _res
@@ -286,6 +287,10 @@ class RotationScheduler:
 
     def noop_loads(self):
         return _L.cft_scheduler_noop_loads(self._h)
+
+    def write_transfer_log_csv(self, path) -> None:
+        """transfer_log.csv exactly as the reference's write_transfer_log_csv (schedule.cpp:137-154)."""
+        N.check(_L.cft_scheduler_write_transfer_log_csv(self._h, str(path).encode()))
 
     def events(self) -> List[TransferEvent]:
         n = _L.cft_scheduler_num_events(self._h)

@@ -445,3 +445,53 @@ def test_fp64_engine_gradient_clipping(cuda, clip_rel):
         eng.step_end()
     assert rel(r.params, eng.params) < 1e-12
     assert not np.array_equal(r.params, np.array(case["final_params"]))  # the clip did act
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_artifact_csvs_match_reference(cuda, name, tmp_path):
+    """trajectory.csv and transfer_log.csv (FORMATS.md) written by the fp64 engine vs the files
+    the LIVE reference library writes after the same run_training (write_trajectory_csv,
+    trainer.cpp:103-114; write_transfer_log_csv, schedule.cpp:137-154): the transfer log and
+    every non-float column byte-identical; the loss text identical for the bit-exact Linear
+    cases; loss / grad_norm_sq within 1e-12 otherwise (tanh / exp / log, parallel fp64 sums)."""
+    from oracle import ref as R
+    from paper_2605_21177_b200.engine import ChunkEngine
+    try:
+        R._need()
+    except Exception:
+        pytest.skip("oracle/_ref (the reference library build) is absent")
+    case = CASES[name]
+    batches = batches_of(case)
+    layers = [tuple(L) for L in case["layers"]]
+    ref_dir = tmp_path / "ref"
+    ref_dir.mkdir()
+    R.train(layers, case["loss"], np.array(case["init_params"]), batches, K=case["K"], T=case["T"],
+            steps=case["steps"], budget=case["budget"], prefetch=case["prefetch"], bw=case["bw"],
+            optim=case["optim"], micro_batches=case["micro_batches"], hyper=tuple(case["hyper"]),
+            ckpt_dir=str(ref_dir))
+    eng = ChunkEngine(model_of(case), np.array(case["init_params"]), batches[0][next(iter(batches[0]))].shape[0],
+                      options_of(case, "fp64"))
+    bs = [eng.stage(b, device=True) for b in batches]
+    cursor = 0
+    for _ in range(case["steps"]):
+        mbs = []
+        for _ in range(case["micro_batches"]):
+            mbs.append(bs[cursor])
+            cursor = (cursor + 1) % len(bs)
+        eng.step(mbs)
+    eng.finish()
+    eng.write_trajectory_csv(tmp_path / "trajectory.csv")
+    eng.write_transfer_log_csv(tmp_path / "transfer_log.csv")
+    assert (tmp_path / "transfer_log.csv").read_bytes() == (ref_dir / "transfer_log.csv").read_bytes()
+    got = (tmp_path / "trajectory.csv").read_text().splitlines()
+    want = (ref_dir / "trajectory.csv").read_text().splitlines()
+    assert got[0] == want[0] == "step,chunk_epoch,inner_step,chunk,loss,grad_norm_sq"
+    assert len(got) == len(want) == case["steps"] + 1
+    exact = name in ("linear_exact", "quadratic_k2")
+    for g, w in zip(got[1:], want[1:]):
+        gs, ws = g.split(","), w.split(",")
+        assert gs[:4] == ws[:4]
+        if exact:  # the loss is bit-exact; grad_norm_sq is a parallel fp64 sum on the GPU
+            assert gs[4] == ws[4]
+        for a, b in zip(gs[4:], ws[4:]):
+            assert abs(float(a) - float(b)) <= 1e-12 * max(abs(float(b)), 1e-300)

@@ -197,3 +197,25 @@ def test_scheduler_errors():
     s.step_end()
     with pytest.raises(P.Error, match="past total_steps"):
         s.step_begin()
+
+
+def test_transfer_log_csv_byte_identical_to_reference(tmp_path):
+    """transfer_log.csv (FORMATS.md; write_transfer_log_csv, schedule.cpp:137-154): our scheduler's
+    file equals the reference library's own writer byte for byte, over the golden schedules
+    (prefetch on/off, bandwidth windows, no-op loads) and random ones."""
+    recs = [(r["elems"], r["K"], r["T"], r["steps"], r["prefetch"], r["bw"]) for r in gold("schedules.json")]
+    rng = np.random.default_rng(11)
+    for _ in range(10):
+        K = int(rng.integers(1, 7))
+        recs.append(([int(rng.integers(1, 500)) for _ in range(K)], K, int(rng.integers(1, 4)),
+                     int(rng.integers(1, 25)), bool(rng.random() < 0.5), int(rng.integers(0, 3000))))
+    for i, (elems, K, T, steps, prefetch, bw) in enumerate(recs):
+        infos = infos_of([(j, 1, e) for j, e in enumerate(elems)])
+        plan = P.partition_per_tensor(infos)
+        s, *_ = drive(P.ScheduleConfig(K, T, steps, prefetch, bw), plan, steps)
+        ours, ref = tmp_path / f"ours_{i}.csv", tmp_path / f"ref_{i}.csv"
+        s.write_transfer_log_csv(ours)
+        R.schedule_csv(K, T, steps, elems, ref, prefetch=prefetch, bw=bw)
+        assert ours.read_bytes() == ref.read_bytes(), (elems, K, T, steps, prefetch, bw)
+    with pytest.raises(P.Error, match="cannot open"):
+        s.write_transfer_log_csv(tmp_path / "no_such_dir" / "x.csv")
