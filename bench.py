@@ -476,6 +476,24 @@ def run_llama(args, rank, world, local_rank):
     eng.prepare_graphs()  # one forward+backward CUDA graph per chunk, captured before timing
     if world > 1:
         eng.set_grad_scale(1.0 / world)
+    p2p = sharded and args.exchange != "collectives"
+    if p2p:  # publish this rank's accumulator / gather buffer, open every peer's (CUDA IPC)
+        handles = [None] * world
+        dist.all_gather_object(handles, eng.ipc_handles())
+        ok = torch.ones(1, device=dev)
+        try:
+            eng.connect_peers(handles, rank)
+        except Exception as e:  # e.g. no peer access: every rank falls back to the collectives
+            if args.exchange == "p2p":
+                raise
+            print(f"rank {rank}: peer exchange unavailable ({e}); using NCCL collectives",
+                  file=sys.stderr)
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        p2p = bool(ok.item())
+        if not p2p:
+            eng.clear_peers()
+        token = torch.zeros(1, device=dev)
     rng = np.random.default_rng(100 + rank)
     dev_b, host_b = [], []
     for i in range(4):
@@ -495,6 +513,13 @@ def run_llama(args, rank, world, local_rank):
             if not sharded:
                 dist.all_reduce(eng.grad_tensor())
                 eng.step_end()
+                return
+            if p2p:
+                dist.all_reduce(token)            # barrier: every accumulator complete
+                dist.all_reduce(eng.shard_stats())  # pulls this rank's shard over NVLink
+                eng.step_end()                    # AdamW stores into every rank's gather buffer
+                dist.all_reduce(token)            # barrier: every store landed
+                eng.gather_end()
                 return
             dist.reduce_scatter_tensor(eng.shard_grad_tensor(), eng.grad_tensor())
             dist.all_reduce(eng.shard_stats())
@@ -608,7 +633,8 @@ def run_llama(args, rank, world, local_rank):
                        "K": K, "T": 1, "budget_bytes": budget, "plan_hash": f"{plan.hash():016x}",
                        "prefetch": True,
                        "state_residency": ("pinned host + 3 HBM slots" if offload else "HBM (host RAM too small for all ranks)")
-                       + (f", sharded 1/{world} per rank (reduce-scatter / shard AdamW / all-gather)" if sharded else ""),
+                       + (f", sharded 1/{world} per rank (reduce-scatter / shard AdamW / all-gather"
+                          + (" over peer memory)" if p2p else ")") if sharded else ""),
                        "parallelism": f"dp{world}",
                        "l2": "step working set >> L2 (16 GB of bf16 weights streamed per step)",
                        "timed_steps_cover": "one full rotation (every chunk once)" if S % K == 0 else f"{S} steps"},
@@ -702,6 +728,10 @@ def main():
     ap.add_argument("--fusion", type=int, default=3,
                     help="A/B: epilogue fusion mask (1 SwiGLU, 2 RoPE; 0 = separate kernels)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[1] sliced-dW sweep")
+    ap.add_argument("--exchange", choices=["auto", "collectives", "p2p"], default="auto",
+                    help="N>1 sharded state: the exchange over peer memory (P2P pull "
+                         "reduce-scatter + AdamW stores into every rank; auto = when every rank "
+                         "can open every peer's buffers) or NCCL reduce-scatter/all-gather")
     ap.add_argument("--remat", action="store_true",
                     help="llama workloads: keep only layer inputs, re-materialise the backward "
                          "suffix layer by layer (fits e.g. the full 80-layer 70B shape on 1 GPU)")

@@ -409,6 +409,24 @@ int cft_engine_shard_stats(cft_engine* e, double** red3_dev);
 int cft_engine_gather_buffer(cft_engine* e, void** ptr, int64_t* n_total, int64_t* my_offset,
                              int32_t* dtype);
 int cft_engine_gather_end(cft_engine* e);
+/* The same exchange over peer memory (NVLink P2P) instead of NCCL data collectives.  Each rank
+ * publishes its gradient accumulator and gather buffer (cft_engine_ipc_handles: two 64-byte
+ * cudaIpcMemHandle_t; or cft_engine_p2p_buffers for ranks in one process), opens the others'
+ * (cft_ipc_open) and passes all shard_world pointers, in rank order, to cft_engine_set_peers.
+ * Per step, on the engine stream:
+ *   forward_backward -> barrier -> cft_engine_shard_stats (pulls and sums this rank's shard from
+ *   every accumulator: the reduce-scatter) -> all-reduce of its 3 doubles -> step_end (AdamW
+ *   writes the updated values into every rank's gather buffer: the all-gather) -> barrier ->
+ *   gather_end.
+ * "barrier" = any stream-ordered all-rank barrier (e.g. a 1-element ncclAllReduce).  fp64: the
+ * pull sums ranks in order, the reference's accumulate order for micro_batches = world.
+ * cft_engine_set_peers(e, NULL, NULL) returns to the collectives protocol. */
+int cft_engine_p2p_buffers(cft_engine* e, void** aux, void** gather);
+int cft_engine_ipc_handles(cft_engine* e, void* aux_handle, void* gather_handle);
+int cft_engine_set_peers(cft_engine* e, const void* const* aux, const void* const* gather);
+int cft_ipc_open(const void* handle, void** ptr);
+int cft_ipc_close(void* ptr);
+
 /* TrainTrajectoryEntry (trainer.hpp:26-33): step, chunk, loss (pre-update mean), grad_norm_sq. */
 int64_t cft_engine_trajectory(cft_engine* e, int64_t* step, int32_t* chunk, double* loss,
                               double* gsq, int64_t cap);

@@ -19,6 +19,7 @@
 #include <type_traits>
 
 #include "cft_common.h"
+#include "kernels.h"
 #include "tc_ptx.cuh"
 
 namespace cft::opt {
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kThreads)
                      float b2, float eps, float wd, float bc1, float bc2, P* __restrict__ param,
                      const cft_segment* __restrict__ segs, int nseg,
                      const double* __restrict__ stats, float* __restrict__ precond, int zero_grad,
-                     double clip) {
+                     double clip, P* const* __restrict__ peers, int npeers) {
   if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
   if (clip > 0.0 && stats) {  // global-norm clip from the statistics pass, on the device
     const double nrm = sqrt(stats[0]);
@@ -247,7 +248,11 @@ __global__ void __launch_bounds__(kThreads)
         }
       }
       // write-back through the segment table (optimizer.cpp:124-132)
-      if (param) write_back4(param, sg, nseg, i0, n, w[k]);
+      if (npeers) {  // sharded state over peer memory: the all-gather is these stores
+        for (int r = 0; r < npeers; ++r) write_back4(peers[r], sg, nseg, i0, n, w[k]);
+      } else if (param) {
+        write_back4(param, sg, nseg, i0, n, w[k]);
+      }
     }
   }
   if (precond) {
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                           float bc1, float bc2, P* __restrict__ param,
                           const cft_segment* __restrict__ segs, int nseg,
                           const double* __restrict__ stats, float* __restrict__ precond,
-                          int zero_grad, double clip) {
+                          int zero_grad, double clip, P* const* __restrict__ peers, int npeers) {
   using namespace cft::ptx;
   if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
   if (clip > 0.0 && stats) {
@@ -428,7 +433,11 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
           }
         }
       }
-      if (param) write_back4(param, sg, nseg, i0, n, w);
+      if (npeers) {
+        for (int r = 0; r < npeers; ++r) write_back4(peers[r], sg, nseg, i0, n, w);
+      } else if (param) {
+        write_back4(param, sg, nseg, i0, n, w);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -462,7 +471,8 @@ __global__ void __launch_bounds__(kThreads)
     adamw_f64_kernel(double* master, double* m, double* v, const double* grad, long long n,
                      double gscale, double eta, double b1, double b2, double eps, double wd,
                      double bc1, double bc2, P* param, const cft_segment* segs, int nseg,
-                     const double* stats, double* precond, double clip) {
+                     const double* stats, double* precond, double clip, P* const* peers,
+                     int npeers) {
   if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
   if (clip > 0.0 && stats) {
     const double nrm = __dsqrt_rn(stats[0]);
@@ -487,11 +497,14 @@ __global__ void __launch_bounds__(kThreads)
     const double pc = __ddiv_rn(1.0, denom);
     pmin = fmin(pmin, pc);
     pmax = fmax(pmax, pc);
-    if (param) {
+    if (param || npeers) {
       const int s = find_segment(segs, nseg, i);
-      P* dst = param + segs[s].param_off + (i - segs[s].state_off);
-      if constexpr (std::is_same_v<P, __nv_bfloat16>) *dst = __double2bfloat16(nw);
-      else *dst = static_cast<P>(nw);
+      const long long off = segs[s].param_off + (i - segs[s].state_off);
+      for (int r = 0; r < (npeers ? npeers : 1); ++r) {
+        P* dst = (npeers ? peers[r] : param) + off;
+        if constexpr (std::is_same_v<P, __nv_bfloat16>) *dst = __double2bfloat16(nw);
+        else *dst = static_cast<P>(nw);
+      }
     }
   }
   if (precond) {
@@ -503,6 +516,47 @@ __global__ void __launch_bounds__(kThreads)
       atomicMin(reinterpret_cast<long long*>(&precond[0]), __double_as_longlong(pmin));
       atomicMax(reinterpret_cast<long long*>(&precond[1]), __double_as_longlong(pmax));
     }
+  }
+}
+
+// ---- reduce-scatter over peer memory: this rank's shard of the chunk gradient is the sum of
+// every rank's accumulator over [lo, lo + n), read straight from the peers' HBM (NVLink P2P
+// loads; UVA pointers), in rank order -- for fp64 exactly the reference's accumulate order
+// (accum = 0; accum += bag_0; accum += bag_1 ..., optimizer.cpp:134-146). ----
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    pull_sum_kernel(const T* const* __restrict__ peers, int world, long long lo, long long n,
+                    T* __restrict__ out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if constexpr (std::is_same_v<T, float>) {
+    if ((lo & 3) == 0) {
+      const long long n4 = n / 4;
+      for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 acc = reinterpret_cast<const float4*>(peers[0] + lo)[i];
+        for (int r = 1; r < world; ++r) {
+          const float4 v = reinterpret_cast<const float4*>(peers[r] + lo)[i];
+          acc.x += v.x;
+          acc.y += v.y;
+          acc.z += v.z;
+          acc.w += v.w;
+        }
+        reinterpret_cast<float4*>(out)[i] = acc;
+      }
+      for (long long i = 4 * n4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+        float acc = peers[0][lo + i];
+        for (int r = 1; r < world; ++r) acc += peers[r][lo + i];
+        out[i] = acc;
+      }
+      return;
+    }
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    T acc = T(0);
+    for (int r = 0; r < world; ++r) {
+      if constexpr (std::is_same_v<T, double>) acc = __dadd_rn(acc, peers[r][lo + i]);
+      else acc += peers[r][lo + i];
+    }
+    out[i] = acc;
   }
 }
 
@@ -553,6 +607,18 @@ inline int grid_for(long long work) {
   return static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (work + kThreads - 1) / kThreads)));
 }
 
+void pull_shard(cft_dtype state_dtype, void* const* peers_dev, int world, int64_t lo, int64_t n,
+                void* out, cudaStream_t s) {
+  if (n <= 0) return;
+  if (state_dtype == CFT_F32)
+    pull_sum_kernel<float><<<grid_for(n / 4 + 1), kThreads, 0, s>>>(
+        reinterpret_cast<const float* const*>(peers_dev), world, lo, n, static_cast<float*>(out));
+  else
+    pull_sum_kernel<double><<<grid_for(n), kThreads, 0, s>>>(
+        reinterpret_cast<const double* const*>(peers_dev), world, lo, n, static_cast<double*>(out));
+  cft::check_launch("pull_shard");
+}
+
 }  // namespace cft::opt
 
 using namespace cft::opt;
@@ -582,6 +648,21 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
                     cft_dtype param_dtype, void* param_base, const cft_segment* segs,
                     int32_t n_segments, const void* stats_dev, void* precond_dev, int zero_grad,
                     double clip_max_norm, cft_stream_t stream) {
+  return cft::opt::adamw_slice_peers(state_dtype, master, m, v, grad, n, grad_scale, h, bc1, bc2,
+                                     param_dtype, param_base, segs, n_segments, stats_dev,
+                                     precond_dev, zero_grad, clip_max_norm, nullptr, 0, stream);
+}
+
+}  // extern "C"
+
+// cft_adamw_slice with the parameter write-back sent to `npeers` destinations (device array of
+// bases, same segment offsets in each): the sharded engine's all-gather over peer memory.
+int cft::opt::adamw_slice_peers(cft_dtype state_dtype, void* master, void* m, void* v, void* grad,
+                                int64_t n, double grad_scale, const cft_adamw_hyper* h, double bc1,
+                                double bc2, cft_dtype param_dtype, void* param_base,
+                                const cft_segment* segs, int32_t n_segments, const void* stats_dev,
+                                void* precond_dev, int zero_grad, double clip_max_norm,
+                                void* const* peers, int npeers, cft_stream_t stream) {
   return cft::guarded([&] {
     auto s = static_cast<cudaStream_t>(stream);
     if (n <= 0) return;
@@ -611,7 +692,8 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
             static_cast<float*>(master), static_cast<float*>(m), static_cast<float*>(v),
             static_cast<float*>(grad), n, (float)grad_scale, (float)h->eta, (float)h->beta1,
             (float)h->beta2, (float)h->epsilon, (float)h->weight_decay, (float)bc1, (float)bc2, p,
-            segs, n_segments, st, static_cast<float*>(precond_dev), zero_grad, clip_max_norm);
+            segs, n_segments, st, static_cast<float*>(precond_dev), zero_grad, clip_max_norm,
+            reinterpret_cast<PT* const*>(peers), npeers);
       };
       auto go = [&](auto* p) {
         if (variant == 1) launch(Bulk8{}, p);
@@ -628,11 +710,13 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
       const long long want = (groups + kThreads * kGroups - 1) / (kThreads * kGroups);
       const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(want, (long long)cft::num_sms() * 16)));
       auto go = [&](auto* p) {
+        using PT = std::remove_pointer_t<decltype(p)>;
         adamw_f32_kernel<<<grid, kThreads, 0, s>>>(
             static_cast<float*>(master), static_cast<float*>(m), static_cast<float*>(v),
             static_cast<float*>(grad), n, (float)grad_scale, (float)h->eta, (float)h->beta1,
             (float)h->beta2, (float)h->epsilon, (float)h->weight_decay, (float)bc1, (float)bc2, p,
-            segs, n_segments, st, static_cast<float*>(precond_dev), zero_grad, clip_max_norm);
+            segs, n_segments, st, static_cast<float*>(precond_dev), zero_grad, clip_max_norm,
+            reinterpret_cast<PT* const*>(peers), npeers);
       };
       if (param_dtype == CFT_BF16) go(static_cast<__nv_bfloat16*>(param_base));
       else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));
@@ -640,11 +724,12 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
     } else if (state_dtype == CFT_F64) {
       const int grid = grid_for(n);
       auto go = [&](auto* p) {
+        using PT = std::remove_pointer_t<decltype(p)>;
         adamw_f64_kernel<<<grid, kThreads, 0, s>>>(
             static_cast<double*>(master), static_cast<double*>(m), static_cast<double*>(v),
             static_cast<const double*>(grad), n, grad_scale, h->eta, h->beta1, h->beta2, h->epsilon,
             h->weight_decay, bc1, bc2, p, segs, n_segments, st, static_cast<double*>(precond_dev),
-            clip_max_norm);
+            clip_max_norm, reinterpret_cast<PT* const*>(peers), npeers);
       };
       if (param_dtype == CFT_F64) go(static_cast<double*>(param_base));
       else if (param_dtype == CFT_F32) go(static_cast<float*>(param_base));
@@ -655,6 +740,8 @@ int cft_adamw_slice(cft_dtype state_dtype, void* master, void* m, void* v, void*
     cft::check_launch("adamw_slice");
   });
 }
+
+extern "C" {
 
 int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t n,
                   double grad_scale, double eta, cft_dtype param_dtype, void* param_base,

@@ -881,9 +881,12 @@ void Engine::step_end() {
     if (cfg_.optim == 0) {
       const double bc1 = 1.0 - std::pow(cfg_.hyper.beta1, static_cast<double>(n_local_[c]));
       const double bc2 = 1.0 - std::pow(cfg_.hyper.beta2, static_cast<double>(n_local_[c]));
-      if (cft_adamw_slice(sdt, master, m, v, grad, gn, scale, &cfg_.hyper, bc1, bc2,
-                          static_cast<cft_dtype>(cfg_.dtype), pbase, segs, nseg, st, precond_,
-                          sdt == CFT_F32 ? 1 : 0, cfg_.clip_max_norm, s) != CFT_OK)
+      // p2p: the updated values go straight into every rank's gather buffer (the all-gather)
+      if (opt::adamw_slice_peers(sdt, master, m, v, grad, gn, scale, &cfg_.hyper, bc1, bc2,
+                                 static_cast<cft_dtype>(cfg_.dtype), pbase, segs, nseg, st,
+                                 precond_, sdt == CFT_F32 ? 1 : 0, cfg_.clip_max_norm,
+                                 p2p_ ? peer_tbl_ + cfg_.shard_world : nullptr,
+                                 p2p_ ? cfg_.shard_world : 0, s) != CFT_OK)
         throw Error(last_error());
     } else {
       if (cft_sgd_slice(sdt, master, grad, gn, scale, cfg_.hyper.eta,
@@ -1039,6 +1042,13 @@ double* Engine::shard_stats() {
   const cft_dtype sdt = cfg_.dtype == CFT_F64 ? CFT_F64 : CFT_F32;
   const double scale = cfg_.grad_scale * (1.0 / cfg_.micro_batches);
   double* st = stats_ + t_ * 4;
+  if (p2p_) {  // the reduce-scatter: sum this rank's shard over every rank's accumulator (P2P)
+    pb(kStats);
+    add_work(kStats, 4.0 * sn * (cfg_.shard_world + 1));
+    opt::pull_shard(sdt, peer_tbl_, cfg_.shard_world, int64_t(cfg_.shard_rank) * sh_size_[active_],
+                    sn, gshard_, s);
+    pe();
+  }
   pb(kStats);
   add_work(kStats, 4.0 * sn);
   if (sn > 0 && cft_grad_stats(sdt, gshard_, sn, scale, st, s) != CFT_OK) throw Error(last_error());
@@ -1047,6 +1057,35 @@ double* Engine::shard_stats() {
   pe();
   stats_done_ = true;
   return red_;
+}
+
+// ---- sharded exchange over peer memory (NVLink P2P; UVA pointers from cudaIpc handles or, for
+// ranks in one process, the peers' own allocations) ----
+void Engine::p2p_buffers(void** aux, void** gather) const {
+  CFT_CHECK(sharded(), "engine: states are not sharded");
+  *aux = aux_;
+  *gather = gather_;
+}
+void Engine::ipc_handles(void* aux_handle, void* gather_handle) const {
+  CFT_CHECK(sharded(), "engine: states are not sharded");
+  CFT_CUDA(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(aux_handle), aux_));
+  CFT_CUDA(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(gather_handle), gather_));
+}
+void Engine::set_peers(const void* const* aux, const void* const* gather) {
+  CFT_CHECK(sharded(), "engine: peer exchange needs sharded optimizer state");
+  CFT_CHECK(cfg_.optim == 0, "engine: peer exchange supports the AdamW update");
+  const int w = cfg_.shard_world;
+  CFT_CHECK(aux[cfg_.shard_rank] == aux_ && gather[cfg_.shard_rank] == gather_,
+            "engine: set_peers: this rank's entries must be its own buffers");
+  std::vector<void*> tbl(2 * w);
+  for (int r = 0; r < w; ++r) {
+    CFT_CHECK(aux[r] && gather[r], "engine: set_peers: null peer buffer");
+    tbl[r] = const_cast<void*>(aux[r]);
+    tbl[w + r] = const_cast<void*>(gather[r]);
+  }
+  if (!peer_tbl_) alloc(reinterpret_cast<void**>(&peer_tbl_), 2 * w * sizeof(void*));
+  CFT_CUDA(cudaMemcpy(peer_tbl_, tbl.data(), 2 * w * sizeof(void*), cudaMemcpyHostToDevice));
+  p2p_ = true;
 }
 
 void Engine::gather_buffer(void** ptr, int64_t* n_total, int64_t* my_offset, int* dtype) {

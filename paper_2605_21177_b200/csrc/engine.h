@@ -108,6 +108,14 @@ class Engine {
   double* shard_stats();
   void gather_buffer(void** ptr, int64_t* n_total, int64_t* my_offset, int* dtype);
   void gather_end();
+  // the same exchange over peer memory instead of NCCL: set_peers() once with every rank's
+  // accumulator and gather buffer (own entries = this engine's); then per step
+  //   forward_backward -> [barrier] -> shard_stats (pulls the reduce-scatter) -> all-reduce of
+  //   its 3 doubles -> step_end (AdamW stores into every gather buffer) -> [barrier] -> gather_end
+  void p2p_buffers(void** aux, void** gather) const;
+  void ipc_handles(void* aux_handle, void* gather_handle) const;  // 2 x cudaIpcMemHandle_t
+  void set_peers(const void* const* aux, const void* const* gather);
+  void clear_peers() { p2p_ = false; }
   void prepare_graphs();  // capture every chunk's forward+backward graph now (Llama engine)
 
   // results
@@ -230,6 +238,8 @@ class Engine {
   int64_t max_state_ = 0, max_padded_ = 0;
   void* gshard_ = nullptr;                  // reduce-scatter output (this rank's mean-grad part)
   void* gather_ = nullptr;                  // packed chunk params in the compute dtype
+  void** peer_tbl_ = nullptr;               // device: [aux of ranks 0..w-1, gather of 0..w-1]
+  bool p2p_ = false;
   double* red_ = nullptr;                   // {sumsq, nonfinite, loss} for the all-reduce
   std::vector<cft_segment*> shard_segs_;    // per chunk: {0, rank * padded, st_n}
   bool stats_done_ = false;

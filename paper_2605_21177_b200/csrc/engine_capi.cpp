@@ -167,6 +167,34 @@ int cft_engine_write_transfer_log_csv(cft_engine* e, const char* path) {
   });
 }
 
+int cft_engine_p2p_buffers(cft_engine* e, void** aux, void** gather) {
+  return guarded([&] { e->p->p2p_buffers(aux, gather); });
+}
+
+int cft_engine_ipc_handles(cft_engine* e, void* aux_handle, void* gather_handle) {
+  return guarded([&] { e->p->ipc_handles(aux_handle, gather_handle); });
+}
+
+int cft_engine_set_peers(cft_engine* e, const void* const* aux, const void* const* gather) {
+  return guarded([&] {
+    CFT_CHECK((aux == nullptr) == (gather == nullptr), "cft_engine_set_peers: null table");
+    if (!aux) e->p->clear_peers();  // back to the collectives protocol
+    else e->p->set_peers(aux, gather);
+  });
+}
+
+int cft_ipc_open(const void* handle, void** ptr) {
+  return guarded([&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    CFT_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int cft_ipc_close(void* ptr) {
+  return guarded([&] { CFT_CUDA(cudaIpcCloseMemHandle(ptr)); });
+}
+
 int cft_engine_chunk_counters(cft_engine* e, uint64_t* n) {
   return guarded([&] { e->p->chunk_counters(n); });
 }

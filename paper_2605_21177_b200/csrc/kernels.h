@@ -7,6 +7,8 @@
 
 #include <cstdint>
 
+#include "chunkft_b200.h"
+
 namespace cft {
 
 namespace tc {  // gemm_tc.cu: bf16 tcgen05/TMEM GEMMs
@@ -122,5 +124,18 @@ void swiglu_bwd(const __nv_bfloat16* ds, const __nv_bfloat16* ug, long long rows
 void init_slice(float* master, __nv_bfloat16* param, long long count, uint64_t seed, int tensor,
                 long long elem0, long long cols, bool is_gain, cudaStream_t s);
 }  // namespace llama
+
+namespace opt {  // adamw.cu: the sharded-state exchange over peer memory
+// cft_adamw_slice whose parameter write-back goes to `npeers` bases (device array; the same
+// segment offsets in each) -- the all-gather as stores into every rank's gather buffer
+int adamw_slice_peers(cft_dtype state_dtype, void* master, void* m, void* v, void* grad, int64_t n,
+                      double grad_scale, const cft_adamw_hyper* h, double bc1, double bc2,
+                      cft_dtype param_dtype, void* param_base, const cft_segment* segs,
+                      int32_t n_segments, const void* stats_dev, void* precond_dev, int zero_grad,
+                      double clip_max_norm, void* const* peers, int npeers, cft_stream_t stream);
+// out[i] = sum over ranks r (in order) of peers[r][lo + i], i < n -- the reduce-scatter
+void pull_shard(cft_dtype state_dtype, void* const* peers_dev, int world, int64_t lo, int64_t n,
+                void* out, cudaStream_t s);
+}  // namespace opt
 
 }  // namespace cft

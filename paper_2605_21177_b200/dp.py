@@ -26,11 +26,19 @@ class DataParallelStep:
     shard_grad_tensor(), shard_stats(), gather_tensor(), gather_end().  The exchange is then
     reduce-scatter of the gradient, an all-reduce of three statistics and an all-gather of the
     updated compute-dtype parameters: the same bytes on the wire as the all-reduce, 1/world
-    of the AdamW work, host memory and PCIe rotation traffic per rank."""
+    of the AdamW work, host memory and PCIe rotation traffic per rank.
+
+    ``exchange="p2p"`` (with ``sharded=True``, one node): the reduce-scatter and all-gather move
+    over peer memory instead of collectives -- every rank publishes its accumulator and gather
+    buffer (CUDA IPC handles, exchanged once with all_gather_object), shard_stats() pulls and
+    sums its shard from every rank's accumulator and the AdamW in step_end() stores the updated
+    values into every rank's gather buffer.  What stays collective is the 3-double statistics
+    all-reduce and two 1-element stream-ordered barriers."""
 
     def __init__(self, engine, group=None, all_reduce: Optional[Callable] = None,
                  world_size: Optional[int] = None, sharded: bool = False,
-                 reduce_scatter: Optional[Callable] = None, all_gather: Optional[Callable] = None):
+                 reduce_scatter: Optional[Callable] = None, all_gather: Optional[Callable] = None,
+                 exchange: str = "collectives", barrier: Optional[Callable] = None):
         import torch.distributed as dist
         self.engine = engine
         self.group = group
@@ -47,6 +55,23 @@ class DataParallelStep:
                 dist.all_gather_into_tensor(out, inp, group=group)
         self.all_reduce, self.reduce_scatter, self.all_gather = all_reduce, reduce_scatter, all_gather
         self.engine.set_grad_scale(1.0 / self.world)
+        if exchange not in ("collectives", "p2p"):
+            raise ValueError(f"unknown exchange '{exchange}'")
+        self.p2p = exchange == "p2p"
+        if self.p2p:
+            if not sharded:
+                raise ValueError("exchange='p2p' needs sharded=True")
+            if barrier is None:
+                import torch
+                token = torch.zeros(1, device="cuda")
+
+                def barrier():  # stream-ordered: a 1-element all-reduce
+                    dist.all_reduce(token, group=group)
+            self.barrier = barrier
+            if self.world > 1:  # (bench.py shows the agreed fallback to the collectives)
+                handles = [None] * self.world
+                dist.all_gather_object(handles, engine.ipc_handles(), group=group)
+                engine.connect_peers(handles, dist.get_rank(group))
 
     def step(self, batches: List) -> int:
         """One optimizer step over this rank's micro-batches; returns the active chunk."""
@@ -57,6 +82,13 @@ class DataParallelStep:
             if self.world > 1:
                 self.all_reduce(self.engine.grad_tensor())
             self.engine.step_end()
+            return active
+        if self.p2p:
+            self.barrier()                              # every accumulator complete
+            self.all_reduce(self.engine.shard_stats())  # (pulls the shard; also a barrier)
+            self.engine.step_end()                      # AdamW stores into every gather buffer
+            self.barrier()                              # every rank's stores landed
+            self.engine.gather_end()
             return active
         self.reduce_scatter(self.engine.shard_grad_tensor(), self.engine.grad_tensor())
         self.all_reduce(self.engine.shard_stats())

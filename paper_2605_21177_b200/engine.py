@@ -72,6 +72,11 @@ for _n, _r, _a in [
     ("cft_engine_plan_json", C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, _P(C.c_int64)]),
     ("cft_engine_transfer_events", C.c_int64, [C.c_void_p, _P(N.TransferEventC), C.c_int64]),
     ("cft_engine_write_trajectory_csv", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("cft_engine_p2p_buffers", C.c_int, [C.c_void_p, _P(C.c_void_p), _P(C.c_void_p)]),
+    ("cft_engine_ipc_handles", C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p]),
+    ("cft_engine_set_peers", C.c_int, [C.c_void_p, _P(C.c_void_p), _P(C.c_void_p)]),
+    ("cft_ipc_open", C.c_int, [C.c_char_p, _P(C.c_void_p)]),
+    ("cft_ipc_close", C.c_int, [C.c_void_p]),
     ("cft_engine_write_transfer_log_csv", C.c_int, [C.c_void_p, C.c_char_p]),
     ("cft_engine_chunk_counters", C.c_int, [C.c_void_p, C.c_void_p]),
     ("cft_engine_phase_ms", C.c_int, [C.c_void_p, C.c_void_p]),
@@ -389,6 +394,46 @@ class ChunkEngine:
     def write_transfer_log_csv(self, path) -> None:
         """transfer_log.csv exactly as the reference's write_transfer_log_csv (schedule.cpp:137-154)."""
         N.check(_L.cft_engine_write_transfer_log_csv(self._h, str(path).encode()), "write_transfer_log_csv")
+
+    # ---- the sharded exchange over peer memory (include/chunkft_b200.h: cft_engine_set_peers) ----
+    def p2p_buffers(self):
+        """(accumulator, gather buffer) device pointers of this engine, for peers in one process."""
+        a, g = C.c_void_p(), C.c_void_p()
+        N.check(_L.cft_engine_p2p_buffers(self._h, C.byref(a), C.byref(g)), "p2p_buffers")
+        return a.value, g.value
+
+    def ipc_handles(self) -> bytes:
+        """128 bytes: the cudaIpcMemHandle_t of the accumulator and of the gather buffer."""
+        a, g = C.create_string_buffer(64), C.create_string_buffer(64)
+        N.check(_L.cft_engine_ipc_handles(self._h, a, g), "ipc_handles")
+        return a.raw + g.raw
+
+    def set_peers(self, aux_ptrs, gather_ptrs):
+        """Every rank's accumulator / gather buffer (rank order; own entries from p2p_buffers)."""
+        w = len(aux_ptrs)
+        a = (C.c_void_p * w)(*aux_ptrs)
+        g = (C.c_void_p * w)(*gather_ptrs)
+        N.check(_L.cft_engine_set_peers(self._h, a, g), "set_peers")
+
+    def clear_peers(self):
+        """Back to the collectives protocol (reduce-scatter / all-gather by the caller)."""
+        N.check(_L.cft_engine_set_peers(self._h, None, None), "set_peers")
+
+    def connect_peers(self, handles, rank):
+        """Open the other ranks' ipc_handles() (list in rank order) and set_peers."""
+        aux, gat = [], []
+        own = self.p2p_buffers()
+        for r, h in enumerate(handles):
+            if r == rank:
+                aux.append(own[0])
+                gat.append(own[1])
+                continue
+            pa, pg = C.c_void_p(), C.c_void_p()
+            N.check(_L.cft_ipc_open(h[:64], C.byref(pa)), "ipc_open")
+            N.check(_L.cft_ipc_open(h[64:128], C.byref(pg)), "ipc_open")
+            aux.append(pa.value)
+            gat.append(pg.value)
+        self.set_peers(aux, gat)
 
     def gather_end(self):
         N.check(_L.cft_engine_gather_end(self._h), "gather_end")

@@ -247,3 +247,75 @@ def test_dp_sharded_states_world2_matches_reference_micro_batches():
     assert c0 == c1 == case["traj_chunk"]
     assert p0 == p1
     assert np.array_equal(np.array(p0), np.array(case["final_params"]))
+
+
+class _RecordingEngine:
+    """Protocol stand-in for the peer-memory exchange: records the DataParallelStep calls."""
+
+    def __init__(self, rank):
+        self.rank, self.calls, self.peers = rank, [], None
+
+    def set_grad_scale(self, s):
+        self.calls.append(("scale", s))
+
+    def ipc_handles(self):
+        return bytes([self.rank]) * 128
+
+    def connect_peers(self, handles, rank):
+        self.peers = ([h[0] for h in handles], rank)
+
+    def step_begin(self):
+        self.calls.append("step_begin")
+        return 0
+
+    def forward_backward(self, b, mb):
+        self.calls.append("forward_backward")
+
+    def shard_stats(self):
+        self.calls.append("shard_stats")
+        return torch.ones(3, dtype=torch.float64)
+
+    def step_end(self):
+        self.calls.append("step_end")
+
+    def gather_end(self):
+        self.calls.append("gather_end")
+
+
+def _p2p_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_21177_b200.dp import DataParallelStep
+        eng = _RecordingEngine(rank)
+        token = torch.zeros(1)
+
+        def barrier():
+            eng.calls.append("barrier")
+            dist.all_reduce(token)
+
+        step = DataParallelStep(eng, sharded=True, exchange="p2p", barrier=barrier)
+        step.step([None])
+        red = eng.shard_stats()
+        out[rank] = (eng.peers, eng.calls[:-1], float(red.sum()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dp_p2p_exchange_protocol_world2():
+    """exchange='p2p' (sharded state over peer memory): every rank receives all ranks' IPC
+    handles in rank order, and a step runs forward_backward -> barrier -> shard_stats (the pull)
+    all-reduced -> step_end (AdamW stores into every rank) -> barrier -> gather_end."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = 33500 + (os.getpid() % 2000)
+    mp.spawn(_p2p_worker, args=(2, port, out), nprocs=2, join=True)
+    for rank in range(2):
+        peers, calls, _ = out[rank]
+        assert peers == ([0, 1], rank)
+        assert calls == [("scale", 0.5), "step_begin", "forward_backward", "barrier", "shard_stats",
+                         "step_end", "barrier", "gather_end"]
+    with pytest.raises(ValueError, match="needs sharded"):
+        from paper_2605_21177_b200.dp import DataParallelStep
+        DataParallelStep(_RecordingEngine(0), world_size=1, exchange="p2p")

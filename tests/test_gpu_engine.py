@@ -240,8 +240,33 @@ def _sharded_exchange(engs):
         e.gather_end()
 
 
+def _p2p_exchange(engs):
+    """The peer-memory exchange (cft_engine_set_peers protocol) across engines standing in for
+    ranks on one GPU: each engine pulls its shard from every accumulator, the stats all-reduce
+    is done by hand, and step_end's AdamW stores into every engine's gather buffer."""
+    torch.cuda.synchronize()  # barrier: every accumulator complete
+    reds = [e.shard_stats() for e in engs]
+    torch.cuda.synchronize()
+    red = sum(reds)
+    for x in reds:
+        x.copy_(red)
+    torch.cuda.synchronize()  # (the all-reduce is also the barrier before the accumulators reset)
+    for e in engs:
+        e.step_end()
+    torch.cuda.synchronize()  # barrier: every rank's stores landed
+    for e in engs:
+        e.gather_end()
+
+
+def _connect(engs):
+    bufs = [e.p2p_buffers() for e in engs]
+    for e in engs:
+        e.set_peers([b[0] for b in bufs], [b[1] for b in bufs])
+
+
+@pytest.mark.parametrize("exchange", ["collectives", "p2p"])
 @pytest.mark.parametrize("offload", [True, False])
-def test_engine_sharded_states_match_reference_micro_batches(cuda, offload):
+def test_engine_sharded_states_match_reference_micro_batches(cuda, offload, exchange):
     """Sharded optimizer state: two engines standing in for two ranks, each
     holding master/m/v for its half of every chunk; reduce-scatter -> shard AdamW ->
     all-gather reproduces the reference with micro_batches = 2 bit for bit (fp64 path)."""
@@ -257,13 +282,15 @@ def test_engine_sharded_states_match_reference_micro_batches(cuda, offload):
         engs.append(e)
     bs = batches_of(case)
     staged = [[e.stage(b, device=True) for b in bs] for e in engs]
+    if exchange == "p2p":
+        _connect(engs)
     cursor = 0
     for t in range(case["steps"]):
         for r, e in enumerate(engs):
             e.step_begin()
             e.forward_backward(staged[r][(cursor + r) % len(bs)], 0)
         cursor = (cursor + 2) % len(bs)
-        _sharded_exchange(engs)
+        (_p2p_exchange if exchange == "p2p" else _sharded_exchange)(engs)
     for e in engs:
         e.finish()
     p0, p1 = engs[0].params(from_masters=False), engs[1].params(from_masters=False)
@@ -272,7 +299,8 @@ def test_engine_sharded_states_match_reference_micro_batches(cuda, offload):
     assert engs[0].trajectory()["chunk"].tolist() == case["traj_chunk"]
 
 
-def test_llama_sharded_states_match_replicated(cuda):
+@pytest.mark.parametrize("exchange", ["collectives", "p2p"])
+def test_llama_sharded_states_match_replicated(cuda, exchange):
     """bf16 Llama decoder, 2 stand-in ranks: sharded states + reduce-scatter/all-gather give
     the replicated-state all-reduce run (same per-element AdamW; the all-gather moves the
     exact bf16 values), with half the optimizer state per rank.  Replicas stay bit-identical;
@@ -296,12 +324,14 @@ def test_llama_sharded_states_match_replicated(cuda):
             engs.append(e)
         staged = [e.stage({"tokens": seqs[r][:, :-1].copy(), "labels": seqs[r][:, 1:].copy()},
                           device=True) for r, e in enumerate(engs)]
+        if sharded and exchange == "p2p":
+            _connect(engs)
         for t in range(2 * K):
             for r, e in enumerate(engs):
                 e.step_begin()
                 e.forward_backward(staged[r], 0)
             if sharded:
-                _sharded_exchange(engs)
+                (_p2p_exchange if exchange == "p2p" else _sharded_exchange)(engs)
             else:
                 torch.cuda.synchronize()
                 g = engs[0].grad_tensor() + engs[1].grad_tensor()
