@@ -284,8 +284,9 @@ int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t
  * the chip, single-CTA 128x256 otherwise), 1 force single-CTA, 2 force CTA pairs. */
 int cft_set_gemm_policy(int policy);
 /* Epilogue fusions of the Llama engine, a bit mask: 1 = SwiGLU in the w1|w3 forward and w2
- * dgrad GEMMs, 2 = RoPE in the QKV forward GEMM; default 3, 0 = separate kernels.  Results are
- * bit-identical either way. */
+ * dgrad GEMMs, 2 = RoPE in the QKV forward GEMM, 4 = the softmax CE's (max, sum-exp) pass in
+ * the lm_head forward GEMM; default 7, 0 = separate kernels.  1 and 2 are bit-identical to the
+ * separate kernels; 4 sums exp() in a different order (loss / dlogits to fp32 rounding). */
 int cft_set_fusion(int enable);
 /* Kernel variant per operator, for A/B measurements (defaults: CFT_ADAMW_KERNEL /
  * CFT_CE_KERNEL).  op 0 fp32 AdamW: 0 register kernel, 1 / 2 / 3 TMA-staged with 8 / 16 /

@@ -210,6 +210,7 @@ class Engine {
   };
   std::vector<LlamaLayerBufs> lb_;
   void *l_xf_ = nullptr, *l_logits_ = nullptr;
+  float2* l_cepart_ = nullptr;  // lm_head epilogue's per-row CE partials
   float* l_rstdf_ = nullptr;
   void *l_gx_ = nullptr, *l_gh_ = nullptr, *l_da_ = nullptr, *l_do_ = nullptr, *l_dxf_ = nullptr,
        *l_ds_ = nullptr, *l_dug_ = nullptr, *l_dqkv_ = nullptr;

@@ -65,7 +65,43 @@ struct Args {
   long long ldc;
   int epi;
   const void* R;  // bf16 residual added in the epilogue (same layout as C; may alias C)
+  // softmax-CE first pass in the epilogue (pair kernel, bf16 out): per row and 128-column half
+  // tile, (max, sum exp(v - max)) of the rounded outputs v -> ce_part[row * ce_stride + 2 tn + half]
+  float2* ce_part;
+  int ce_stride;
 };
+
+// online (max, sum-exp) over 16 accumulator columns, on the bf16-rounded values the epilogue
+// stores (so log Z matches the logits the CE's second pass reads)
+__device__ __forceinline__ void ce_accum16(const uint32_t (&r)[16], int col, int N, float& m,
+                                           float& s) {
+  constexpr float kL2e = 1.4426950408889634f;
+  float v[16];
+  float lm = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    v[j] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[j])));
+    if (col + j < N) lm = fmaxf(lm, v[j]);
+  }
+  if (lm == -INFINITY) return;
+  const float lms = lm * kL2e;
+  float ls = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(v[j], kL2e, -lms)));
+    if (col + j < N) ls += e;
+  }
+  if (m == -INFINITY) {
+    m = lm;
+    s = ls;
+  } else if (lm > m) {
+    s = s * __expf(m - lm) + ls;
+    m = lm;
+  } else {
+    s += ls * __expf(lm - m);
+  }
+}
 
 template <int BN>
 struct Cfg {
@@ -737,6 +773,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       } else {
         // two TMEM loads in flight per wait: the epilogue of a single-wave GEMM (narrow
         // slices, split-K) is exposed after the mainloop and latency-bound
+        float ce_m = -INFINITY, ce_s = 0.f;
 #pragma unroll 1
         for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 32) {
           uint32_t r0[16], r1[16];
@@ -744,9 +781,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           ptx::tmem_ld16(tacc + c + 16, r1);
           ptx::tmem_wait_ld();
           const int col = tn * BNP + c;
+          if (args.ce_part) {
+            ce_accum16(r0, col, args.N, ce_m, ce_s);
+            ce_accum16(r1, col + 16, args.N, ce_m, ce_s);
+          }
           if (row_ok && col < args.N) store16(args, rbase, col, r0);
           if (row_ok && col + 16 < args.N) store16(args, rbase, col + 16, r1);
         }
+        if (args.ce_part && row_ok)
+          args.ce_part[static_cast<long long>(row) * args.ce_stride + 2 * tn + half] =
+              make_float2(ce_m, ce_s);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -915,7 +959,7 @@ bool use_pairs(int M, int N, int K, bool allow_split) {
 void set_policy(int p) { g_policy = p; }
 
 namespace {
-int g_fuse = 3;  // bit 0: SwiGLU epilogues, bit 1: RoPE epilogue
+int g_fuse = 7;  // bit 0: SwiGLU epilogues, bit 1: RoPE epilogue, bit 2: CE first pass
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
 void set_fusion(int on) { g_fuse = on; }
@@ -1028,6 +1072,18 @@ bool linear_fwd_rope(const void* x, int64_t n_tok, int64_t in_dim, const void* w
   r.rope_hd = hd;
   r.rope_cols = static_cast<int>(rope_cols);
   linear_fwd_impl(x, n_tok, in_dim, w, out_dim, y, stream, nullptr, &r);
+  return true;
+}
+
+bool linear_fwd_ce(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
+                   void* y, float2* parts, cudaStream_t stream) {
+  if (!(g_fuse & 4) || !parts ||
+      !use_pairs(static_cast<int>(n_tok), static_cast<int>(out_dim), static_cast<int>(in_dim), false))
+    return false;
+  Args c{};
+  c.ce_part = parts;
+  c.ce_stride = static_cast<int>((out_dim + 127) / 128);
+  linear_fwd_impl(x, n_tok, in_dim, w, out_dim, y, stream, nullptr, &c);
   return true;
 }
 

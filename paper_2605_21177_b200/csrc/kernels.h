@@ -24,6 +24,11 @@ bool linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void*
                        void* s, void* ug, cudaStream_t stream);
 bool linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2, int64_t F,
                          const void* ug, void* dug, cudaStream_t stream);
+// Y = X W^T (bf16) whose epilogue also writes, per row and 128-column half tile, the (max,
+// sum-exp) of the rounded outputs to parts[row * ceil(out_dim / 128) + j] -- the softmax CE's
+// first pass (layers::loss_ce_from_parts); false: not eligible (run linear_fwd + the 2-pass CE)
+bool linear_fwd_ce(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
+                   void* y, float2* parts, cudaStream_t stream);
 // Y = X W^T with rotary embedding applied in the epilogue to columns [0, rope_cols) (heads of
 // hd columns, rotate-half pairs; position = row % seq); false: not eligible (run linear_fwd +
 // rope).  Bit-identical to the unfused pair.
@@ -88,6 +93,10 @@ void tanh_bwd(const T*, const T*, long long, T*, cudaStream_t);
 template <typename T>
 void loss(int kind, const T* y, const T* target, const int32_t* labels, long long rows,
           long long cols, T* dy, double* loss_acc, unsigned long long* bad_label, cudaStream_t);
+// softmax CE whose log Z comes from per-row (max, sum-exp) partials (tc::linear_fwd_ce)
+void loss_ce_from_parts(const __nv_bfloat16* y, const int32_t* labels, long long rows,
+                        long long cols, const float2* parts, int nparts, __nv_bfloat16* dy,
+                        double* loss_acc, unsigned long long* bad_label, cudaStream_t s);
 void loss_f64(int kind, const double* y, const double* target, const int32_t* labels,
               long long rows, long long cols, double* dy, double* loss_acc, double* scratch,
               unsigned long long* bad_label, cudaStream_t);

@@ -240,6 +240,34 @@ __device__ __forceinline__ void online_merge(float& m, float& s, float m2, float
   }
 }
 
+// dlogits of one row given log Z, and the row's loss term (shared by the CE kernels):
+// p / rows = ex2(x*log2e - (logZ*log2e - log2(1/rows))): the 1/rows scale rides in the exponent
+// (one FFMA + one EX2 per logit); the one-hot term only touches the label's vector
+__device__ __forceinline__ void ce_write_dy(const __nv_bfloat16* yr, __nv_bfloat16* dyr, long long nv,
+                                            int label, float ylab, float logz, float inv_rows,
+                                            double* loss) {
+  const float lzs = logz * kL2e - log2f(inv_rows);
+  const int label_j = label >> 3;
+  for (int j = threadIdx.x; j < (int)nv; j += blockDim.x) {
+    const uint4 u = reinterpret_cast<const uint4*>(yr)[j];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    uint4 o;
+    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+    float p[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(h[q]);
+      p[2 * q] = ex2_approx(fmaf(f.x, kL2e, -lzs));
+      p[2 * q + 1] = ex2_approx(fmaf(f.y, kL2e, -lzs));
+    }
+    if (j == label_j) p[label & 7] -= inv_rows;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) oh[q] = __floats2bfloat162_rn(p[2 * q], p[2 * q + 1]);
+    reinterpret_cast<uint4*>(dyr)[j] = o;
+  }
+  if (threadIdx.x == 0) atomicAdd(loss, static_cast<double>(-(ylab - logz)) * inv_rows);
+}
+
 __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels, long long cols,
                                    float inv_rows, __nv_bfloat16* dy, double* loss,
                                    unsigned long long* bad_label) {
@@ -288,29 +316,45 @@ __global__ void loss_ce_vec_kernel(const __nv_bfloat16* y, const int32_t* labels
   m = -INFINITY;
   s = 0.f;
   for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) online_merge(m, s, sm[i], ss[i]);
-  const float logz = m + logf(s);
-  // p / rows = ex2(x*log2e - (logZ*log2e - log2(1/rows))): the 1/rows scale rides in the
-  // exponent (one FFMA + one EX2 per logit); the one-hot term only touches the label's vector
-  const float lzs = logz * kL2e - log2f(inv_rows);
-  const int label_j = label >> 3;
-  for (int j = threadIdx.x; j < (int)nv; j += blockDim.x) {
-    const uint4 u = reinterpret_cast<const uint4*>(yr)[j];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-    uint4 o;
-    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
-    float p[8];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float2 f = __bfloat1622float2(h[q]);
-      p[2 * q] = ex2_approx(fmaf(f.x, kL2e, -lzs));
-      p[2 * q + 1] = ex2_approx(fmaf(f.y, kL2e, -lzs));
-    }
-    if (j == label_j) p[label & 7] -= inv_rows;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) oh[q] = __floats2bfloat162_rn(p[2 * q], p[2 * q + 1]);
-    reinterpret_cast<uint4*>(dy + b * cols)[j] = o;
+  ce_write_dy(yr, dy + b * cols, cols / 8, label, ylab, m + logf(s), inv_rows, loss);
+}
+
+// CE from the lm_head GEMM's per-row (max, sum-exp) partials (one per 128-column half tile,
+// computed in its epilogue from the rounded bf16 logits): log Z costs a read of the partials,
+// so the logits are read once (for dlogits) instead of twice.
+__global__ void loss_ce_parts_kernel(const __nv_bfloat16* y, const int32_t* labels, long long cols,
+                                     const float2* __restrict__ parts, int nparts, float inv_rows,
+                                     __nv_bfloat16* dy, double* loss,
+                                     unsigned long long* bad_label) {
+  __shared__ float sm[32], ss[32];
+  const long long b = blockIdx.x;
+  const __nv_bfloat16* yr = y + b * cols;
+  const int label = labels[b];
+  if (label < 0 || label >= cols) {
+    if (threadIdx.x == 0) atomicAdd(bad_label, 1ull);
+    return;
   }
-  if (threadIdx.x == 0) atomicAdd(loss, static_cast<double>(-(ylab - logz)) * inv_rows);
+  const float ylab = __bfloat162float(yr[label]);
+  float m = -INFINITY, s = 0.f;
+  const float2* pr = parts + b * nparts;
+  for (int j = threadIdx.x; j < nparts; j += blockDim.x) {
+    const float2 p = pr[j];
+    online_merge(m, s, p.x, p.y);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    online_merge(m, s, m2, s2);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sm[threadIdx.x / 32] = m;
+    ss[threadIdx.x / 32] = s;
+  }
+  __syncthreads();
+  m = -INFINITY;
+  s = 0.f;
+  for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) online_merge(m, s, sm[i], ss[i]);
+  ce_write_dy(yr, dy + b * cols, cols / 8, label, ylab, m + logf(s), inv_rows, loss);
 }
 
 // Softmax cross-entropy with the row held on chip: a cluster of kCeCluster CTAs owns one
@@ -590,6 +634,15 @@ void loss(int kind, const T* y, const T* target, const int32_t* labels, long lon
     loss_elem_kernel<T><<<grid_n(rows * cols), 256, 0, s>>>(kind, y, target, rows * cols, dy, loss_acc);
   }
   check_launch("loss");
+}
+void loss_ce_from_parts(const __nv_bfloat16* y, const int32_t* labels, long long rows,
+                        long long cols, const float2* parts, int nparts, __nv_bfloat16* dy,
+                        double* loss_acc, unsigned long long* bad_label, cudaStream_t s) {
+  CFT_CHECK(cols % 8 == 0 && ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0,
+            "loss_ce_from_parts: 16-byte rows required");
+  loss_ce_parts_kernel<<<(unsigned)rows, 512, 0, s>>>(y, labels, cols, parts, nparts, 1.f / rows, dy,
+                                                      loss_acc, bad_label);
+  check_launch("loss_ce_parts");
 }
 void loss_f64(int kind, const double* y, const double* target, const int32_t* labels,
               long long rows, long long cols, double* dy, double* loss_acc, double* scratch,

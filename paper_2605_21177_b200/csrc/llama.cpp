@@ -99,6 +99,7 @@ void Engine::llama_alloc() {
   l_xf_ = A(N * d);
   l_rstdf_ = static_cast<float*>(A(N, 4));
   l_logits_ = A(N * int64_t(s.vocab));
+  l_cepart_ = static_cast<float2*>(A(N * ((int64_t(s.vocab) + 127) / 128), 8));
   l_gx_ = A(N * d);
   l_gh_ = A(N * d);
   l_da_ = A(N * d);
@@ -334,13 +335,20 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
   pe();
   pb(kFwdGemm);
   gemm_work(kFwdGemm, N, V, d, 2.0 * N * V, 0);
-  tc::linear_fwd(l_xf_, N, d, P(head_id), V, l_logits_, st);
+  // the lm_head epilogue also forms the CE's per-row (max, sum-exp) partials
+  const bool ce_fused = tc::linear_fwd_ce(l_xf_, N, d, P(head_id), V, l_logits_, l_cepart_, st);
+  if (!ce_fused) tc::linear_fwd(l_xf_, N, d, P(head_id), V, l_logits_, st);
   pe();
 
   // ---- next-token CE (autodiff.cpp:205-225); dlogits written in place ----
   pb(kLoss);
-  layers::loss<bf16>(3, static_cast<bf16*>(l_logits_), nullptr, lab, N, V,
-                     static_cast<bf16*>(l_logits_), loss_cell, flags_, st);
+  if (ce_fused)
+    layers::loss_ce_from_parts(static_cast<bf16*>(l_logits_), lab, N, V, l_cepart_,
+                               static_cast<int>((V + 127) / 128), static_cast<bf16*>(l_logits_),
+                               loss_cell, flags_, st);
+  else
+    layers::loss<bf16>(3, static_cast<bf16*>(l_logits_), nullptr, lab, N, V,
+                       static_cast<bf16*>(l_logits_), loss_cell, flags_, st);
   pe();
 
   // ---- chunk-masked backward over the suffix ----

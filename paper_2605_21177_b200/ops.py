@@ -199,9 +199,9 @@ def linear_dgrad_swiglu(dy: torch.Tensor, w2: torch.Tensor, ug: torch.Tensor, st
 
 
 def set_fusion(enable) -> None:
-    """Llama-engine epilogue fusions: True/3 all, False/0 none, or a mask (1 SwiGLU, 2 RoPE);
-    results are bit-identical either way."""
-    N.check(N.lib.cft_set_fusion(3 if enable is True else int(enable)))
+    """Llama-engine epilogue fusions: True/7 all, False/0 none, or a mask (1 SwiGLU, 2 RoPE,
+    4 CE first pass in the lm_head epilogue); 1 and 2 are bit-identical to the separate kernels."""
+    N.check(N.lib.cft_set_fusion(7 if enable is True else int(enable)))
 
 
 def set_gemm_policy(policy: int) -> None:

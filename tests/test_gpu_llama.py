@@ -147,7 +147,7 @@ def test_llama_swiglu_fusion_bit_identical(cuda, policy):
     ops.set_gemm_policy(policy)
     try:
         for fuse in (False, True):
-            ops.set_fusion(fuse)
+            ops.set_fusion(3 if fuse else 0)  # SwiGLU + RoPE epilogues (bit-identical fusions)
             opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=K), dtype="bf16",
                                 cuda_graphs=False)
             eng = ChunkEngine(model, flat, B, opts)
@@ -309,3 +309,39 @@ def test_llama_rematerialisation_matches_resident(cuda, graphs):
         assert np.linalg.norm(b - a) <= 1e-5 * np.linalg.norm(a)
     np.testing.assert_allclose(res[True][1], res[False][1], rtol=1e-6)
     assert res[True][2] < res[False][2]
+
+
+def test_llama_ce_first_pass_in_lm_head_epilogue(cuda):
+    """Fusion bit 4: the lm_head GEMM's epilogue forms each row's (max, sum-exp) over 128-column
+    half tiles from the rounded bf16 logits and the CE kernel only reads those plus one pass over
+    the logits.  Same math, another summation order: the loss and the full-depth gradient of the
+    first step (embedding chunk: the dlogits feed every layer's backward) agree with the
+    two-pass kernel to fp32 rounding propagated through the bf16 dlogits."""
+    from paper_2605_21177_b200 import ops
+    from paper_2605_21177_b200.engine import ChunkEngine, LlamaModel, TrainOptions
+    from paper_2605_21177_b200.plan import ScheduleConfig
+    model = LlamaModel(layers=2)
+    B, K = 4, 6
+    flat = init_params(model, seed=13)
+    rng = np.random.default_rng(3)
+    seqs = rng.integers(0, model.vocab, (B, model.seq + 1)).astype(np.int32)
+    res = {}
+    try:
+        for mask in (3, 7):
+            ops.set_fusion(mask)
+            opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=1), dtype="bf16",
+                                cuda_graphs=False)
+            eng = ChunkEngine(model, flat, B, opts)
+            batch = eng.stage({"tokens": seqs[:, :-1].copy(), "labels": seqs[:, 1:].copy()},
+                              device=True)
+            eng.step_begin()
+            eng.forward_backward(batch, 0)
+            g = eng.grad_tensor().cpu().numpy().copy()
+            eng.step_end()
+            eng.finish()
+            res[mask] = (g, eng.trajectory()["loss"][0])
+    finally:
+        ops.set_fusion(7)
+    (g3, l3), (g7, l7) = res[3], res[7]
+    assert abs(l7 - l3) <= 1e-5 * abs(l3)
+    assert np.linalg.norm(g7 - g3) <= 1e-3 * np.linalg.norm(g3)
