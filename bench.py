@@ -659,11 +659,11 @@ def run_llama(args, rank, world, local_rank):
                           "frac_of_spec_2250": wg_tflops / 2250.0,
                           "flops_per_step": phases["wgrad"][2] / S},
             "adamw": {"GBps_in_step": adam_gbs, "frac_of_measured_hbm": adam_gbs / peaks["hbm"],
-                      "frac_of_spec_8000": adam_gbs / 8000.0, "bytes_per_elem": 34,
+                      "frac_of_spec_8000": adam_gbs / 8000.0, "bytes_per_elem": 30,
                       "bytes_note": "read g, m, v, master fp32 (16) + write m, v, master fp32 (12) + "
-                                    "bf16 param write-back (2) + the accumulator re-zeroing the "
-                                    "reference does in accumulate_grad (optimizer.cpp:136) (4)",
-                      "GBps_in_step_30B": adam_gbs * 30.0 / 34.0,
+                                    "bf16 param write-back (2); the accumulator re-zeroing (the "
+                                    "reference's accumulate_grad fill, optimizer.cpp:136) runs on a "
+                                    "side branch of the next step's graph, overlapping its forward",
                       "kernel": "adamw_f32_bulk_kernel (TMA bulk loads into a 4-stage ring, 24 consumer warps)",
                       "elements_per_chunk": model.num_params() / K},
             "phases_ms_per_step": {k: v[0] / S for k, v in phases.items()},

@@ -234,6 +234,13 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
     CFT_CUDA(cudaEventCreateWithFlags(&in_free_[k], cudaEventDisableTiming));
   }
   CFT_CUDA(cudaStreamCreateWithFlags(&in_stream_, cudaStreamNonBlocking));
+  zero_in_body_ = kind_ == kLlamaModel && cfg_.dtype != CFT_F64 && !sharded() &&
+                  cfg_.micro_batches == 1;
+  if (zero_in_body_) {
+    CFT_CUDA(cudaStreamCreateWithFlags(&zero_stream_, cudaStreamNonBlocking));
+    CFT_CUDA(cudaEventCreateWithFlags(&zero_fork_, cudaEventDisableTiming));
+    CFT_CUDA(cudaEventCreateWithFlags(&zero_join_, cudaEventDisableTiming));
+  }
   {
     void* p;
     alloc(&p, static_cast<size_t>(std::max<int64_t>(cfg_.total_steps, 1)) * 4 * sizeof(double));
@@ -468,6 +475,9 @@ Engine::~Engine() {
   if (step_done_) cudaEventDestroy(step_done_);
   if (h2d_) cudaStreamDestroy(h2d_);
   if (in_stream_) cudaStreamDestroy(in_stream_);
+  if (zero_stream_) cudaStreamDestroy(zero_stream_);
+  if (zero_fork_) cudaEventDestroy(zero_fork_);
+  if (zero_join_) cudaEventDestroy(zero_join_);
   for (int k = 0; k < 2; ++k) {
     if (in_ready_[k]) cudaEventDestroy(in_ready_[k]);
     if (in_free_[k]) cudaEventDestroy(in_free_[k]);
@@ -876,7 +886,7 @@ void Engine::step_end() {
   pb(kUpdate);
   // AdamW: read g, m, v, master + write m, v, master, param + re-zero the accumulator (the
   // reference's accumulate_grad fill, optimizer.cpp:136) = 34 B/elem at fp32 state, bf16 params
-  add_work(kUpdate, (cfg_.optim == 0 ? (sdt == CFT_F32 ? 30.0 + 4.0 : 30.0) : 14.0) * gn);
+  add_work(kUpdate, (cfg_.optim == 0 ? (sdt == CFT_F32 && !zero_in_body_ ? 30.0 + 4.0 : 30.0) : 14.0) * gn);
   if (gn > 0) {
     if (cfg_.optim == 0) {
       const double bc1 = 1.0 - std::pow(cfg_.hyper.beta1, static_cast<double>(n_local_[c]));
@@ -884,7 +894,8 @@ void Engine::step_end() {
       // p2p: the updated values go straight into every rank's gather buffer (the all-gather)
       if (opt::adamw_slice_peers(sdt, master, m, v, grad, gn, scale, &cfg_.hyper, bc1, bc2,
                                  static_cast<cft_dtype>(cfg_.dtype), pbase, segs, nseg, st,
-                                 precond_, sdt == CFT_F32 ? 1 : 0, cfg_.clip_max_norm,
+                                 precond_, sdt == CFT_F32 && !zero_in_body_ ? 1 : 0,
+                                 cfg_.clip_max_norm,
                                  p2p_ ? peer_tbl_ + cfg_.shard_world : nullptr,
                                  p2p_ ? cfg_.shard_world : 0, s) != CFT_OK)
         throw Error(last_error());

@@ -261,6 +261,11 @@ class Engine {
   int32_t* in_tokens_[2] = {nullptr, nullptr};
   int32_t* in_labels_[2] = {nullptr, nullptr};
   cudaStream_t in_stream_ = nullptr;
+  // Llama step, one micro-batch, replicated state: the accumulator is re-zeroed at the start of
+  // the next forward on a side branch (overlapping the forward) instead of inside AdamW
+  bool zero_in_body_ = false;
+  cudaStream_t zero_stream_ = nullptr;
+  cudaEvent_t zero_fork_ = nullptr, zero_join_ = nullptr;
   cudaEvent_t in_ready_[2] = {nullptr, nullptr};
   cudaEvent_t in_free_[2] = {nullptr, nullptr};
   int64_t uploads_ = 0;

@@ -268,6 +268,14 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
   pb(kInputs);
   layers::count_in_range(tok, N, 0, V, reinterpret_cast<long long*>(flags_ + 1), st);
   pe();
+  // re-zero the gradient accumulator (the reference's accumulate_grad fill, optimizer.cpp:136)
+  // on a side branch that overlaps the forward; joined before the first dW slice below
+  if (zero_in_body_) {
+    CFT_CUDA(cudaEventRecord(zero_fork_, st));
+    CFT_CUDA(cudaStreamWaitEvent(zero_stream_, zero_fork_, 0));
+    CFT_CUDA(cudaMemsetAsync(aux_, 0, plan_.chunks[active_].elements * sizeof(float), zero_stream_));
+    CFT_CUDA(cudaEventRecord(zero_join_, zero_stream_));
+  }
 
   // ---- forward ----
   pb(kFwdOther);
@@ -355,6 +363,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
   auto need = [&](int tensor) { return stop <= tensor; };    // gradient at/above `tensor`
   auto below = [&](int tensor) { return stop < tensor; };    // something below `tensor`
   const bf16* dlog = static_cast<const bf16*>(l_logits_);
+  if (zero_in_body_) CFT_CUDA(cudaStreamWaitEvent(st, zero_join_, 0));
   wgrad(head_id, dlog, V, l_xf_, d, 0);
   if (need(norm_id)) {
     pb(kDgrad);
