@@ -24,6 +24,7 @@
 #include <tuple>
 
 #include "cft_common.h"
+#include "kernels.h"
 #include "tc_ptx.cuh"
 
 namespace cft::tc {
@@ -1082,7 +1083,7 @@ bool linear_fwd_ce(const void* x, int64_t n_tok, int64_t in_dim, const void* w, 
     return false;
   Args c{};
   c.ce_part = parts;
-  c.ce_stride = static_cast<int>((out_dim + 127) / 128);
+  c.ce_stride = ce_parts_per_row(out_dim);  // every (256-column tile, half) entry is written
   linear_fwd_impl(x, n_tok, in_dim, w, out_dim, y, stream, nullptr, &c);
   return true;
 }

@@ -25,10 +25,13 @@ bool linear_fwd_swiglu(const void* x, int64_t n_tok, int64_t in_dim, const void*
 bool linear_dgrad_swiglu(const void* dy, int64_t n_tok, int64_t out_dim, const void* w2, int64_t F,
                          const void* ug, void* dug, cudaStream_t stream);
 // Y = X W^T (bf16) whose epilogue also writes, per row and 128-column half tile, the (max,
-// sum-exp) of the rounded outputs to parts[row * ceil(out_dim / 128) + j] -- the softmax CE's
+// sum-exp) of the rounded outputs to parts[row * ce_parts_per_row(out_dim) + j] -- the softmax CE's
 // first pass (layers::loss_ce_from_parts); false: not eligible (run linear_fwd + the 2-pass CE)
 bool linear_fwd_ce(const void* x, int64_t n_tok, int64_t in_dim, const void* w, int64_t out_dim,
                    void* y, float2* parts, cudaStream_t stream);
+// partials per row: one per 128-column half of every 256-column tile (halves past out_dim hold
+// an empty (-inf, 0) entry)
+inline int ce_parts_per_row(int64_t out_dim) { return static_cast<int>(2 * ((out_dim + 255) / 256)); }
 // Y = X W^T with rotary embedding applied in the epilogue to columns [0, rope_cols) (heads of
 // hd columns, rotate-half pairs; position = row % seq); false: not eligible (run linear_fwd +
 // rope).  Bit-identical to the unfused pair.

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "attn.h"
@@ -99,7 +100,7 @@ void Engine::llama_alloc() {
   l_xf_ = A(N * d);
   l_rstdf_ = static_cast<float*>(A(N, 4));
   l_logits_ = A(N * int64_t(s.vocab));
-  l_cepart_ = static_cast<float2*>(A(N * ((int64_t(s.vocab) + 127) / 128), 8));
+  l_cepart_ = static_cast<float2*>(A(N * tc::ce_parts_per_row(s.vocab), 8));
   l_gx_ = A(N * d);
   l_gh_ = A(N * d);
   l_da_ = A(N * d);
@@ -352,7 +353,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
   pb(kLoss);
   if (ce_fused)
     layers::loss_ce_from_parts(static_cast<bf16*>(l_logits_), lab, N, V, l_cepart_,
-                               static_cast<int>((V + 127) / 128), static_cast<bf16*>(l_logits_),
+                               tc::ce_parts_per_row(V), static_cast<bf16*>(l_logits_),
                                loss_cell, flags_, st);
   else
     layers::loss<bf16>(3, static_cast<bf16*>(l_logits_), nullptr, lab, N, V,
