@@ -308,6 +308,9 @@ class ChunkEngine:
         if h is not None and h.value:
             _L.cft_engine_destroy(h)
             self._h = None
+        for p in getattr(self, "_ipc_opened", []):  # peers' mappings from connect_peers
+            _L.cft_ipc_close(p)
+        self._ipc_opened = []
 
     # ---- batches ----
     def stage(self, batch: dict, device: bool = False) -> BatchC:
@@ -430,7 +433,9 @@ class ChunkEngine:
                 continue
             pa, pg = C.c_void_p(), C.c_void_p()
             N.check(_L.cft_ipc_open(h[:64], C.byref(pa)), "ipc_open")
+            self._ipc_opened = getattr(self, "_ipc_opened", []) + [pa.value]
             N.check(_L.cft_ipc_open(h[64:128], C.byref(pg)), "ipc_open")
+            self._ipc_opened.append(pg.value)
             aux.append(pa.value)
             gat.append(pg.value)
         self.set_peers(aux, gat)
