@@ -664,7 +664,7 @@ def run_llama(args, rank, world, local_rank):
                                     "bf16 param write-back (2); the accumulator re-zeroing (the "
                                     "reference's accumulate_grad fill, optimizer.cpp:136) runs on a "
                                     "side branch of the next step's graph, overlapping its forward",
-                      "kernel": "adamw_f32_bulk_kernel (TMA bulk loads into a 4-stage ring, 24 consumer warps)",
+                      "kernel": "adamw_f32_bulk_kernel (TMA bulk loads into a 3-stage ring of 62 KB, 31 consumer warps)",
                       "elements_per_chunk": model.num_params() / K},
             "phases_ms_per_step": {k: v[0] / S for k, v in phases.items()},
             "profiled_step_ms": prof_wall_ms / S,

@@ -289,8 +289,8 @@ int cft_set_gemm_policy(int policy);
  * separate kernels; 4 sums exp() in a different order (loss / dlogits to fp32 rounding). */
 int cft_set_fusion(int enable);
 /* Kernel variant per operator, for A/B measurements (defaults: CFT_ADAMW_KERNEL /
- * CFT_CE_KERNEL).  op 0 fp32 AdamW: 0 register kernel, 1 / 2 / 3 TMA-staged with 8 / 16 /
- * 24 consumer warps.  op 1 bf16 softmax CE: 0 two-pass (512 threads per row), 1 cluster
+ * CFT_CE_KERNEL).  op 0 fp32 AdamW: 0 register kernel, 1 / 2 / 3 / 4 TMA-staged with 8 / 16 /
+ * 24 / 31 consumer warps (default 4).  op 1 bf16 softmax CE: 0 two-pass (512 threads per row), 1 cluster
  * (2 row stages, 1 CTA per SM), 2 cluster (1 stage, 3 CTAs per SM), 3 two-pass with 1024
  * threads per row.  op 2 tcgen05 GEMM launches: 0 ordinary, 1 programmatic dependent launch
  * (prologue overlaps the previous kernel's tail). */

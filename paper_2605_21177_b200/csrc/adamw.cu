@@ -303,6 +303,7 @@ struct BulkCfg {
 using Bulk8 = BulkCfg<8, 2, 5>;
 using Bulk16 = BulkCfg<16, 1, 6>;
 using Bulk24 = BulkCfg<24, 1, 4>;
+using Bulk31 = BulkCfg<31, 1, 3>;
 
 template <typename Cfg, typename P>
 __global__ void __launch_bounds__(Cfg::kThreads, 1)
@@ -673,7 +674,8 @@ int cft::opt::adamw_slice_peers(cft_dtype state_dtype, void* master, void* m, vo
     const double* st = static_cast<const double*>(stats_dev);
     const auto aligned16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     const int variant = adamw_variant();
-    const long long min_n = Bulk24::kTile;
+    const long long min_n = variant == 1 ? Bulk8::kTile : variant == 2 ? Bulk16::kTile
+                            : variant == 3 ? Bulk24::kTile : Bulk31::kTile;  // >= one full tile
     if (state_dtype == CFT_F32 && variant != 0 && n >= min_n && aligned16(master) &&
         aligned16(m) && aligned16(v) && aligned16(grad)) {
       auto launch = [&](auto cfg, auto* p) {
@@ -698,6 +700,7 @@ int cft::opt::adamw_slice_peers(cft_dtype state_dtype, void* master, void* m, vo
       auto go = [&](auto* p) {
         if (variant == 1) launch(Bulk8{}, p);
         else if (variant == 2) launch(Bulk16{}, p);
+        else if (variant == 4) launch(Bulk31{}, p);
         else launch(Bulk24{}, p);
       };
       if (param_dtype == CFT_BF16) go(static_cast<__nv_bfloat16*>(param_base));

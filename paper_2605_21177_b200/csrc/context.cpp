@@ -60,7 +60,7 @@ int& kernel_variant(int op) {
       [] {
         const char* e = std::getenv("CFT_ADAMW_KERNEL");
         const std::string k = e ? e : "";
-        return k == "reg" ? 0 : k == "bulk8" ? 1 : k == "bulk16" ? 2 : 3;
+        return k == "reg" ? 0 : k == "bulk8" ? 1 : k == "bulk16" ? 2 : k == "bulk24" ? 3 : 4;
       }(),
       [] {
         const char* e = std::getenv("CFT_CE_KERNEL");
@@ -82,7 +82,7 @@ int& kernel_variant(int op) {
 extern "C" {
 int cft_set_kernel_variant(int op, int variant) {
   return cft::guarded([&] {
-    CFT_CHECK(variant >= 0 && variant <= 3, "cft_set_kernel_variant: variant out of range");
+    CFT_CHECK(variant >= 0 && variant <= 4, "cft_set_kernel_variant: variant out of range");
     cft::kernel_variant(op) = variant;
   });
 }

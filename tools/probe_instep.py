@@ -61,13 +61,13 @@ class H:
     eta, beta1, beta2, epsilon, weight_decay = 1e-3, 0.9, 0.999, 1e-8, 0.0
 
 
-for var in (3,):
+for var in (3, 4, 3, 4):
     N.check(N.lib.cft_set_kernel_variant(0, var), "variant")
     med, lo = measure(lambda: ops.adamw_slice(master, m, v, g, H, 3, param=param, segments=segs,
                                               stats=stats, zero_grad=True))
     print(json.dumps({"op": "adamw", "variant": var, "median_ms": round(med, 4), "min_ms": round(lo, 4),
                       "GBps_30B": round(30 * E / med / 1e6)}), flush=True)
-N.check(N.lib.cft_set_kernel_variant(0, 3), "variant")
+N.check(N.lib.cft_set_kernel_variant(0, 4), "variant")
 med, lo = measure(lambda: ops.grad_stats(g, 1.0, stats=stats))
 print(json.dumps({"op": "grad_stats", "median_ms": round(med, 4), "min_ms": round(lo, 4),
                   "GBps_4B": round(4 * E / med / 1e6)}), flush=True)
