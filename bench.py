@@ -47,9 +47,20 @@ def load_peaks():
             p = json.load(f)
         return dict(hbm=float(p["hbm_gbs"]), bf16=float(p["bf16_tflops"]),
                     bf16_sustained=float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                    sm_mhz=(p.get("clocks_under_load") or {}).get("sm_mhz_median"),
                     source="measured")
     except Exception:
-        return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, source="fallback")
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, sm_mhz=None, source="fallback")
+
+
+def clock_normalised(frac, peaks, clocks):
+    """frac rescaled to the SM clock the peak was measured at: under the 1000 W cap the clock
+    depends on the power the workload draws, so a step whose GEMMs draw less than cuBLAS's
+    back-to-back 8192^3 run clocks higher and can exceed the sustained peak (frac > 1)."""
+    run = (clocks or {}).get("sm_mhz")
+    if not run or not peaks.get("sm_mhz"):
+        return None
+    return frac * peaks["sm_mhz"] / run
 
 
 class ClockSampler:
@@ -319,6 +330,8 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "tensor", "kernel": "gemm_bf16_kernel (tcgen05: fwd+dgrad+sliced wgrad)",
                          "achieved": gemm_tflops, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
                          "frac": gemm_tflops / peaks["bf16_sustained"], "traffic": traffic,
+                         "frac_clock_normalised": clock_normalised(gemm_tflops / peaks["bf16_sustained"],
+                                                                   peaks, clocks),
                          "peak_source": peaks["source"] + " sustained bf16 (MEASURED_PEAKS.json)",
                          "algorithmic_flops_per_step": fl_fwd + fl_dgrad + fl_wgrad},
             "sliced_dw": {"tflops": wgrad_tflops, "frac_of_measured_peak": wgrad_tflops / peaks["bf16"],
@@ -620,6 +633,7 @@ def run_llama(args, rank, world, local_rank):
     prof_ms = sum(v[0] for k, v in phases.items() if k not in ("h2d", "d2h"))
     res = None
     if rank == 0:
+        clocks = clk.summary()
         res = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": S,
             "warmup": W, "ms_per_step": ms / S, "higher_is_better": True, "scaling": "weak",
@@ -646,6 +660,9 @@ def run_llama(args, rank, world, local_rank):
                          "kernel": "gemm_bf16_2sm_kernel / gemm_bf16_kernel (tcgen05 fwd + dgrad + sliced wgrad)",
                          "achieved": gemm_tflops, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
                          "frac": gemm_tflops / peaks["bf16_sustained"], "traffic": traffic,
+                         "frac_clock_normalised": clock_normalised(gemm_tflops / peaks["bf16_sustained"],
+                                                                   peaks, clocks),
+                         "peak_sm_mhz": peaks["sm_mhz"],
                          "frac_of_burst_peak": gemm_tflops / peaks["bf16"],
                          "frac_of_spec_2250": gemm_tflops / 2250.0,
                          "traffic_unit": "bytes per GEMM launch", "traffic_source": traffic_src,
@@ -673,7 +690,7 @@ def run_llama(args, rank, world, local_rank):
             "device_bytes": eng.device_bytes(),
             "flat_memory": flat,
             "final_loss": float(tr["loss"][-1]),
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
     return res
 
