@@ -357,73 +357,188 @@ LLAMA_WORKLOAD = ("llama3_8b_chunk_local_step (BASELINE configs[2]: Llama-3-8B-s
                   "step (T=1) over all layers, bf16 operands / fp32 accumulate + state)")
 
 
-def reference_llama_cpu(rows: int = 16, K: int = 60, model=None):
-    """The reference CPU path (oracle/_ref, OpenMP on all host cores) for the configs[2] step,
-    EXTRAPOLATED per SURVEY.md 8(d): one decoder layer's seven Linear shapes (forward + dX,
-    which the reference always forms) timed at `rows` tokens, x 32 layers, + the lm_head
-    (forward + dX), + dW on one chunk's worth of rows (the active slice), + adamw_chunk_step on
-    one chunk.  Attention / RMSNorm / SwiGLU (absent from the reference) are not charged, so
-    the figure is optimistic for the reference."""
+def llama_chunk_flops(m, chunks, n_tok, remat=False, attention_only=False):
+    """Algorithmic FLOPs of one training step for every chunk of a Llama plan, following the
+    engine's backward-suffix rule (csrc/llama.cpp, llama_body): the full forward, then -- from
+    the top -- dgrad / attention backward only down to the chunk's lowest tensor, and dW only on
+    the chunk's rows.  `m`: any object with layers, d, heads, kv_heads, head_dim, ffn, vocab,
+    seq; `chunks`: per chunk a list of (tensor_id, row_begin, row_end).  Causal attention counts
+    2*S^2*dh per (sequence, head) forward (two half-masked matmuls) and 2.5x that backward."""
+    L, d, F, V = m.layers, m.d, m.ffn, m.vocab
+    Q, KV = m.heads * m.head_dim, m.kv_heads * m.head_dim
+    QKV = Q + 2 * KV
+    N = float(n_tok)
+    seqs = n_tok // m.seq
+    attn_f = 2.0 * m.seq * m.seq * m.head_dim * m.heads * seqs
+    attn_b = 2.5 * attn_f
+    layer_fwd = 2 * N * (QKV * d + d * Q + 2 * F * d + d * F) + attn_f
+    fwd = L * layer_fwd + 2 * N * V * d
+    cols = {0: d}
+    for l in range(L):
+        b = 1 + 9 * l
+        cols.update({b: 1, b + 1: d, b + 2: d, b + 3: d, b + 4: Q, b + 5: 1, b + 6: d, b + 7: d,
+                     b + 8: F})
+    cols[1 + 9 * L], cols[2 + 9 * L] = 1, d
+    out = []
+    for ch in chunks:
+        stop = min(t for t, _, _ in ch)
+        wg = sum(2 * N * (re - rb) * cols[t] for t, rb, re in ch if cols[t] > 1 and t != 0)
+        bwd = 0.0
+        att = L * attn_f
+        if stop <= 1 + 9 * L:
+            bwd += 2 * N * d * V  # lm_head dgrad
+        for l in range(L - 1, -1, -1):
+            i = lambda k: 1 + 9 * l + k  # noqa: E731
+            if not stop <= i(8):
+                break
+            if remat and l < L - 1:  # re-materialised layer (no w2 GEMM)
+                bwd += layer_fwd - 2 * N * d * F
+                att += attn_f
+            if not stop <= i(7):
+                break
+            bwd += 2 * N * F * d  # w2 dgrad
+            if not stop <= i(5):
+                break
+            bwd += 2 * N * d * 2 * F  # w1|w3 dgrad
+            if not stop < i(5):
+                break
+            if not stop <= i(3):
+                break
+            bwd += 2 * N * Q * d + attn_b  # wo dgrad + attention backward
+            att += attn_b
+            if not stop <= i(0):
+                break
+            bwd += 2 * N * d * QKV  # wq|wk|wv dgrad
+            if not stop < i(0):
+                break
+        out.append(att if attention_only else fwd + bwd + wg)
+    return out
+
+
+def representative_window(flops, steps):
+    """First chunk of the `steps`-long window (consecutive chunks mod K, T=1) whose mean
+    per-step FLOPs is nearest the rotation mean -- a --steps S < K run then estimates the
+    full-rotation rate; S a multiple of K covers whole rotations from chunk 0."""
+    K = len(flops)
+    if steps % K == 0:
+        return 0
+    mean = sum(flops) / K
+    best, best_err = 0, None
+    for c0 in range(K):
+        w = sum(flops[(c0 + i) % K] for i in range(steps)) / steps
+        err = abs(w - mean)
+        if best_err is None or err < best_err * (1 - 1e-12):
+            best, best_err = c0, err
+    return best
+
+
+class _Shape:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def llama_shape(workload, layers):
+    """Model shape for the llama workloads WITHOUT importing the package (the reference arm
+    must not load the product library): the numbers of LlamaModel.llama3_8b / llama3_70b."""
+    if workload == "llama70b":
+        L = layers if layers != 32 else 12
+        return _Shape(layers=L, d=8192, heads=64, kv_heads=8, head_dim=128, ffn=28672,
+                      vocab=128256, seq=1024)
+    return _Shape(layers=layers, d=4096, heads=32, kv_heads=8, head_dim=128, ffn=14336,
+                  vocab=128256, seq=1024)
+
+
+def reference_llama_sampler(m, K, rows=None, seed=3):
+    """The reference CPU path (oracle/_ref = the unmodified reference library, OpenMP on all
+    host cores) for the configs[2]/[4] step, as a BOUNDED SAMPLE: one sample step = 1/L of the
+    reference's step work at `rows` tokens -- one decoder layer's seven Linear forward + dX
+    (the reference always forms dX), 1/L of the lm_head rows forward + dX, dW on 1/L of one
+    chunk's rows and adamw_chunk_step on 1/L of one chunk.  A full step is L sample steps
+    (EXTRAPOLATED); attention / RMSNorm / SwiGLU (absent from the reference)
+    are not charged, so the figure is optimistic for the reference.  Returns (step_fn, info)."""
     from oracle import ref as R
     if not R.available:
-        return None
+        return None, None
     R.set_backend(True)
-    rng = np.random.default_rng(3)
-    if model is None:
-        from paper_2605_21177_b200.engine import LlamaModel
-        model = LlamaModel.llama3_8b()
-    d, ffn, vocab, L = model.d, model.ffn, model.vocab, model.layers
-    q, kv = model.heads * model.head_dim, model.kv_heads * model.head_dim
-    P = model.num_params()
+    if rows is None:  # the OpenMP kernels split the token rows across threads: one row per thread
+        rows = max(8, R.openmp_threads())
+    rng = np.random.default_rng(seed)
+    d, ffn, vocab, L = m.d, m.ffn, m.vocab, m.layers
+    q, kv = m.heads * m.head_dim, m.kv_heads * m.head_dim
+    P = sum(r * c for r, c in _tensor_shapes(m))
     shapes = [(q, d), (kv, d), (kv, d), (d, q), (ffn, d), (ffn, d), (d, ffn)]
-
-    def timed(fn):
-        t0 = time.perf_counter()
-        fn()
-        return time.perf_counter() - t0
-
-    t_layer = 0.0
+    ops = []
     for out_dim, in_dim in shapes:
         x = rng.uniform(-1, 1, (rows, in_dim))
         w = rng.uniform(-0.5, 0.5, (out_dim, in_dim)) / np.sqrt(in_dim)
         dy = rng.uniform(-1, 1, (rows, out_dim))
-        t_layer += timed(lambda: R.linear_forward(x, w)) + timed(lambda: R.linear_dinput(dy, w))
-    # lm_head: time a 1/8 row block and scale (forward + dX are linear in the row count)
-    hb = vocab // 8
+        ops.append(lambda x=x, w=w: R.linear_forward(x, w))
+        ops.append(lambda dy=dy, w=w: R.linear_dinput(dy, w))
+    hb = -(-vocab // L)
     xh = rng.uniform(-1, 1, (rows, d))
     wh = rng.uniform(-0.5, 0.5, (hb, d)) / np.sqrt(d)
     dyh = rng.uniform(-1, 1, (rows, hb))
-    t_head = 8 * (timed(lambda: R.linear_forward(xh, wh)) + timed(lambda: R.linear_dinput(dyh, wh)))
-    # dW on one chunk (P/K elements): time dW for 2048 rows of w1 and scale by element count
+    ops.append(lambda: R.linear_forward(xh, wh))
+    ops.append(lambda: R.linear_dinput(dyh, wh))
+    chunk = P / K
+    dw_rows = max(1, int(round(chunk / L / d)))  # 1/L of a chunk, as rows of a d-wide weight
     x1 = rng.uniform(-1, 1, (rows, d))
-    dy1 = rng.uniform(-1, 1, (rows, ffn))
-    t_dw = timed(lambda: R.linear_dweight(dy1, x1, 0, 2048)) * (P / K) / (2048 * d)
-    # adamw_chunk_step on 8.4 M elements, scaled to a chunk
-    E = 1 << 23
+    dy1 = rng.uniform(-1, 1, (rows, dw_rows))
+    ops.append(lambda: R.linear_dweight(dy1, x1, 0, dw_rows))
+    E = max(1, int(round(chunk / L)))
     st = [rng.uniform(-1, 1, E) * 0.01, np.zeros(E), np.zeros(E)]
     g = rng.uniform(-1, 1, E)
-    t_adam = timed(lambda: R.adamw(*st, g, 0)) * (P / K) / E
-    step_s = L * t_layer + t_head + t_dw + t_adam
-    # Backend::serial on one shape (wq forward + dX): the per-core rate beside the OpenMP one
-    xq = rng.uniform(-1, 1, (rows, d))
-    wq = rng.uniform(-0.5, 0.5, (q, d)) / np.sqrt(d)
-    dyq = rng.uniform(-1, 1, (rows, q))
-    t_omp = timed(lambda: R.linear_forward(xq, wq)) + timed(lambda: R.linear_dinput(dyq, wq))
-    R.set_backend(False)
-    t_ser = timed(lambda: R.linear_forward(xq, wq)) + timed(lambda: R.linear_dinput(dyq, wq))
-    R.set_backend(True)
-    serial_value = rows / (step_s * t_ser / max(t_omp, 1e-9))
-    return dict(value=rows / step_s, unit="tokens/s", cores=R.openmp_threads(), kind="reference",
-                value_1core_serial=serial_value,
-                sample=f"EXTRAPOLATED: reference kernels (oracle/_ref, OpenMP) at {rows} tokens: one "
-                       f"decoder layer's 7 Linear fwd+dX ({t_layer:.2f} s) x {L} + lm_head fwd+dX "
-                       f"({t_head:.2f} s) + dW on one chunk ({t_dw:.2f} s) + AdamW on one chunk "
-                       f"({t_adam:.2f} s); attention/norm/SwiGLU not charged",
+    ops.append(lambda: R.adamw(*st, g, 0))
+
+    def step():
+        for op in ops:
+            op()
+
+    info = dict(cores=R.openmp_threads(), rows=rows, sample_fraction=L,
+                sample=f"reference kernels (oracle/_ref, OpenMP, {R.openmp_threads()} threads) at "
+                       f"{rows} tokens; one sample step = 1/{L} of the step: one decoder layer's 7 "
+                       f"Linear fwd+dX, lm_head rows [0,{hb}) fwd+dX, dW on {dw_rows}x{d} and "
+                       f"adamw_chunk_step on {E} elements (1/{L} of a K={K} chunk); "
+                       f"EXTRAPOLATED tokens/s = {rows} / ({L} x sample-step time); attention / "
+                       f"norm / SwiGLU not charged")
+    return step, info
+
+
+def _tensor_shapes(m):
+    q, kv = m.heads * m.head_dim, m.kv_heads * m.head_dim
+    out = [(m.vocab, m.d)]
+    for _ in range(m.layers):
+        out += [(m.d, 1), (q, m.d), (kv, m.d), (kv, m.d), (m.d, q), (m.d, 1), (m.ffn, m.d),
+                (m.ffn, m.d), (m.d, m.ffn)]
+    return out + [(m.d, 1), (m.vocab, m.d)]
+
+
+def reference_llama_cpu(m, K, samples=2):
+    """cpu_baseline leg of our own arm: a few sample steps of reference_llama_sampler."""
+    step, info = reference_llama_sampler(m, K)
+    if step is None:
+        return None
+    step()  # warm-up (first-touch of the operands)
+    t0 = time.perf_counter()
+    for _ in range(samples):
+        step()
+    sample_s = (time.perf_counter() - t0) / samples
+    step_s = sample_s * info["sample_fraction"]
+    return dict(value=info["rows"] / step_s, unit="tokens/s", cores=info["cores"],
+                kind="reference", sample=info["sample"] + f"; {samples} sample steps timed",
                 step_s=step_s)
 
 
+def reference_plan_K(m, budget=2 << 30):
+    """K of the 2 GiB byte-budget plan from the reference's own partition_by_budget
+    (oracle/_ref), so the reference arm never imports the product package."""
+    from oracle import ref as R
+    shapes = _tensor_shapes(m)
+    return R.partition([(i, r, c) for i, (r, c) in enumerate(shapes)], budget=budget)["K"]
+
+
 def llama_setup(args):
-    """(model, K of the 2 GiB byte-budget plan, workload string) for the llama workloads."""
+    """(model, 2 GiB byte-budget plan, workload string) for the llama workloads (our arm)."""
     from paper_2605_21177_b200.engine import LlamaModel
     from paper_2605_21177_b200.plan import TensorInfo, partition_by_budget
     if args.workload == "llama70b":
@@ -433,7 +548,7 @@ def llama_setup(args):
         model = LlamaModel.llama3_8b(layers=args.layers)
         name = LLAMA_WORKLOAD
     infos = [TensorInfo(i, n, r, c) for i, (n, r, c) in enumerate(model.tensors())]
-    return model, partition_by_budget(infos, 2 << 30).K, name
+    return model, partition_by_budget(infos, 2 << 30), name
 
 
 def host_ram_bytes():
@@ -456,18 +571,22 @@ def run_llama(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     peaks = load_peaks()
-    model, _, workload_name = llama_setup(args)
+    model, plan, workload_name = llama_setup(args)
     B = 8
     tokens_per_gpu = B * model.seq
     budget = 2 << 30
-    infos = [TensorInfo(i, n, r, c) for i, (n, r, c) in enumerate(model.tensors())]
-    plan = partition_by_budget(infos, budget)
     K = plan.K
     W = args.warmup
     S = args.steps if args.steps > 0 else K  # default: one full rotation = rotation average
     E2E = 0 if args.no_e2e else S
     FM = min(K, 16)  # flat-memory probe: per-step device memory in use (untimed, synced)
-    total = W + 2 * S + (W + E2E if E2E else 0) + FM + 2
+    # every timed leg (device-resident value, profiled, e2e) covers the SAME chunk window:
+    # chunks c0 .. c0+S-1 (mod K; T = 1 so step t runs chunk t mod K), untimed steps in between
+    chunk_fl = llama_chunk_flops(model, [[(s.tensor_id, s.row_begin, s.row_end) for s in ch.slices]
+                                         for ch in plan.chunks], tokens_per_gpu, args.remat)
+    c0 = representative_window(chunk_fl, S)
+    window = [(c0 + i) % K for i in range(S)]
+    total = W + 3 * (K + S) + W + FM + 4
     # optimizer state (12 B/param fp32 master+m+v) in pinned host memory when the host has
     # room for every local rank's copy, else resident in HBM (still flat, no rotation copies)
     # N > 1: optimizer state sharded 1/world per rank (reduce-scatter -> shard AdamW ->
@@ -554,53 +673,70 @@ def run_llama(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    t_next = [0]  # index of the next step (its chunk is t mod K)
+
+    def run(b):
+        one_step(b)
+        t_next[0] += 1
+
+    def align(batches):
+        """untimed steps until the next step runs chunk c0"""
+        i = 0
+        while t_next[0] % K != c0:
+            run(batches[i % len(batches)])
+            i += 1
+
     for i in range(W):
-        one_step(dev_b[i % 4])
+        run(dev_b[i % 4])
+    align(dev_b)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         barrier()
         e0.record(stream)
         for i in range(S):
-            one_step(dev_b[i % 4])
+            run(dev_b[i % 4])
         e1.record(stream)
         barrier()
         ms = max_over_ranks(e0.elapsed_time(e1))
-        # second rotation with the kernel-category profiler on (CUDA events around every
+        # the same window again with the kernel-category profiler on (CUDA events around every
         # launch; kept out of the headline timing because the ~800 extra event records per
         # step cost ~8%): per-kernel times for the roofline and the phase split
+        align(dev_b)
+        barrier()
         eng.profile(True, 2048 * (S + 2))
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         p0.record(stream)
         for i in range(S):
-            one_step(dev_b[i % 4])
+            run(dev_b[i % 4])
         p1.record(stream)
         phases = eng.phase_totals(with_work=True)
         pbytes = eng.phase_bytes()
         prof_wall_ms = p0.elapsed_time(p1)
         eng.profile(False, 0)
-        losses = [eng.wait_step(W + 2 * S - 1)[0]]
+        losses = [eng.wait_step(t_next[0] - 1)[0]]
         e2e_ms = None
         if E2E:
-            base = W + 2 * S
-            for i in range(W):
-                one_step(host_b[i % 4])
-                eng.wait_step(base + i)
+            for i in range(W):  # host-batch warm-up, then the same window from pinned host
+                run(host_b[i % 4])
+                eng.wait_step(t_next[0] - 1)
+            align(host_b)
             barrier()
+            base = t_next[0]
             f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             f0.record(stream)
             for i in range(E2E):
-                one_step(host_b[i % 4])
+                run(host_b[i % 4])
                 if i > 0:
-                    losses.append(eng.wait_step(base + W + i - 1)[0])
-            losses.append(eng.wait_step(base + W + E2E - 1)[0])
+                    losses.append(eng.wait_step(base + i - 1)[0])
+            losses.append(eng.wait_step(base + E2E - 1)[0])
             f1.record(stream)
             barrier()
             e2e_ms = max_over_ranks(f0.elapsed_time(f1))
     # flat-memory check (SURVEY 8(d) cfg5): device bytes in use after each of FM rotation steps
     used = []
     for i in range(FM):
-        one_step(dev_b[i % 4])
+        run(dev_b[i % 4])
         torch.cuda.synchronize()
         free, tot = torch.cuda.mem_get_info()
         used.append(tot - free)
@@ -612,6 +748,14 @@ def run_llama(args, rank, world, local_rank):
             "engine_device_bytes": int(eng.device_bytes())}
 
     value = tokens_per_gpu * world * S / (ms / 1e3)
+    # step-level roofline over the timed window: algorithmic FLOPs (GEMMs + causal attention,
+    # from the plan) / time, against the sustained tensor peak
+    win_fl = sum(chunk_fl[c] for c in window)
+    rot_fl = sum(chunk_fl) / K
+    step_tflops = win_fl * world / (ms / 1e3) / 1e12
+    att_fl = llama_chunk_flops(model, [[(s.tensor_id, s.row_begin, s.row_end) for s in ch.slices]
+                                       for ch in plan.chunks], tokens_per_gpu, args.remat, True)
+    win_att = sum(att_fl[c] for c in window)
     gemm_flops = phases["fwd_gemm"][2] + phases["dgrad"][2] + phases["wgrad"][2]
     gemm_ms = phases["fwd_gemm"][0] + phases["dgrad"][0] + phases["wgrad"][0]
     gemm_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12
@@ -651,7 +795,14 @@ def run_llama(args, rank, world, local_rank):
                           + (" over peer memory)" if p2p else ")") if sharded else ""),
                        "parallelism": f"dp{world}",
                        "l2": "step working set >> L2 (16 GB of bf16 weights streamed per step)",
-                       "timed_steps_cover": "one full rotation (every chunk once)" if S % K == 0 else f"{S} steps"},
+                       "timed_steps_cover": "one full rotation (every chunk once)" if S % K == 0 else f"{S} steps",
+                       "chunk_window": {"first": c0, "last": window[-1], "steps": S,
+                                        "same_window_every_leg": True,
+                                        "gflop_per_token": win_fl / S / tokens_per_gpu / 1e9,
+                                        "rotation_avg_gflop_per_token": rot_fl / tokens_per_gpu / 1e9,
+                                        "choice": "whole rotations from chunk 0" if S % K == 0 else
+                                        "window whose mean algorithmic GFLOP/token is nearest the "
+                                        "rotation average (value then estimates the full-rotation rate)"}},
             "e2e": {"value": (tokens_per_gpu * world * E2E / (e2e_ms / 1e3)) if E2E else None,
                     "unit": "tokens/s", "h2d_bytes_per_step": 2 * 4 * tokens_per_gpu,
                     "d2h_bytes_per_step": 32,
@@ -671,6 +822,15 @@ def run_llama(args, rank, world, local_rank):
                          "algorithmic_flops_per_step": gemm_flops / S,
                          "share_of_step": gemm_ms / ms,
                          "timing": "per-launch CUDA events on the engine stream, profiled rotation"},
+            "step_roofline": {"bound": "tensor", "achieved": step_tflops, "unit": "TFLOP/s",
+                              "peak": peaks["bf16_sustained"], "frac": step_tflops / peaks["bf16_sustained"],
+                              "frac_of_burst_peak": step_tflops / peaks["bf16"],
+                              "algorithmic_flops_per_step": win_fl / S,
+                              "gemm_flops_per_step_engine_counted": gemm_flops / S,
+                              "attention_flops_per_step": win_att / S,
+                              "note": "tokens x window GFLOP/token / device time (fwd + suffix dgrad + "
+                                      "sliced dW GEMMs and causal attention, 2.5x fwd backward); "
+                              "the engine's own per-launch work counters give the GEMM part"},
             "sliced_dw": {"tflops_in_step": wg_tflops, "frac_of_measured_peak": wg_tflops / peaks["bf16"],
                           "frac_of_measured_sustained": wg_tflops / peaks["bf16_sustained"],
                           "frac_of_spec_2250": wg_tflops / 2250.0,
@@ -724,6 +884,54 @@ def slice_sweep(local_rank):
     return out
 
 
+def run_reference_arm(args):
+    """--impl reference: the unmodified reference library (oracle/_ref) on the host cores, on
+    our arm's workload, metric and unit.  It never imports the product package.  Every step is
+    a bounded sample of the workload (llama: 1/L of a step, see reference_llama_sampler);
+    W untimed + S timed sample steps run, ms_per_step is the measured sample-step time and
+    `value` the EXTRAPOLATED full-step tokens/s."""
+    if args.workload in ("llama8b", "llama70b"):
+        m = llama_shape(args.workload, args.layers)
+        K = reference_plan_K(m)
+        step, info = reference_llama_sampler(m, K)
+        workload = (LLAMA70_WORKLOAD.format(layers=m.layers) if args.workload == "llama70b"
+                    else LLAMA_WORKLOAD)
+        if step is not None:
+            S = args.steps if args.steps > 0 else 10
+            for _ in range(args.warmup):
+                step()
+            t0 = time.perf_counter()
+            for _ in range(S):
+                step()
+            sample_s = (time.perf_counter() - t0) / S
+            value = info["rows"] / (sample_s * info["sample_fraction"])
+            return {
+                "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+                "n_gpus": args.gpus, "steps": S, "warmup": args.warmup,
+                "ms_per_step": sample_s * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload, "K": K, "plan": "reference partition_by_budget "
+                           "(2 GiB) from oracle/_ref", "reference_sample_tokens": info["rows"],
+                           "ms_per_step_is": "measured time of one SAMPLE step (1/%d of a full "
+                           "step at %d tokens)" % (info["sample_fraction"], info["rows"]),
+                           "extrapolated_full_step_ms": sample_s * info["sample_fraction"] * 1e3
+                           * (8 * m.seq) / info["rows"]},
+                "extrapolated": True,
+                "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": info["cores"],
+                                 "kind": "reference", "sample": info["sample"]},
+                "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+    cpu = reference_cpu()
+    return {
+        "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": 2, "warmup": 1, "ms_per_step": cpu["step_s"] * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "reference_sample_tokens": 64},
+        "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample") if k in cpu},
+        "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -771,27 +979,21 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        if args.workload in ("llama8b", "llama70b"):
-            m, K, workload = llama_setup(args)
-            cpu = reference_llama_cpu(K=K, model=m)
-            sample_tokens, per_step_tokens = 16, 8192
-        else:
-            cpu = None
-        if cpu is None:
-            cpu = reference_cpu()
-            workload, sample_tokens, per_step_tokens = WORKLOAD, 64, N_TOK
-        print(json.dumps({
-            "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": cpu["step_s"] * 1e3 * per_step_tokens / sample_tokens,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": workload, "reference_sample_tokens": sample_tokens},
-            "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample",
-                                                 "value_1core_serial") if k in cpu},
-            "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}))
+        print(json.dumps(run_reference_arm(args)))
         return
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without torchrun: re-launch as N ranks on this node
+        import socket
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if world != args.gpus and not check_backend:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if world > 1:
         import torch
@@ -814,8 +1016,8 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cpu = None
             if args.workload in ("llama8b", "llama70b"):
-                m, K, _ = llama_setup(args)
-                cpu = reference_llama_cpu(K=K, model=m)
+                m = llama_shape(args.workload, args.layers)
+                cpu = reference_llama_cpu(m, reference_plan_K(m))
             if cpu is None:
                 cpu = reference_cpu()
             res["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample",
