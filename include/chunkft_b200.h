@@ -207,9 +207,13 @@ int cft_linear_dbias_slice(cft_dtype dtype, const void* dy, int64_t n_tok, int64
                            int64_t row_begin, int64_t row_end, void* db_slice, int accumulate,
                            cft_stream_t stream);
 
-/* y[p,:] = table[tokens[p],:].                           kernels.hpp:35-37 */
-int cft_embedding_gather(cft_dtype dtype, const void* table, int64_t dim, const int32_t* tokens,
-                         int64_t positions, void* y, cft_stream_t stream);
+/* y[p,:] = table[tokens[p],:] for a table of table_rows rows.    kernels.hpp:35-37
+ * An id outside [0, table_rows) reads nothing: its output row is zeroed and counted in
+ * *bad_dev (device uint64, may be NULL) -- the device-side form of the range check the
+ * reference's ops layer throws on (ops.cpp:53-54). */
+int cft_embedding_gather(cft_dtype dtype, const void* table, int64_t table_rows, int64_t dim,
+                         const int32_t* tokens, int64_t positions, void* y,
+                         unsigned long long* bad_dev, cft_stream_t stream);
 
 /* dtable_slice[tok-rb,:] += dy[p,:] for rb <= tok < re; matched count added to
  * *matched_dev (device int64, may be NULL).  fp32 out (fp64 for CFT_F64). kernels.hpp:39-44 */

@@ -81,7 +81,7 @@ _sig("cft_linear_fwd_swiglu", C.c_int, vp, i64, i64, vp, i64, vp, vp, vp)
 _sig("cft_linear_dgrad_swiglu", C.c_int, vp, i64, i64, vp, i64, vp, vp, vp)
 _sig("cft_linear_wgrad_slice", C.c_int, C.c_int, vp, i64, i64, vp, i64, i64, i64, vp, C.c_int, vp)
 _sig("cft_linear_dbias_slice", C.c_int, C.c_int, vp, i64, i64, i64, i64, vp, C.c_int, vp)
-_sig("cft_embedding_gather", C.c_int, C.c_int, vp, i64, vp, i64, vp, vp)
+_sig("cft_embedding_gather", C.c_int, C.c_int, vp, i64, i64, vp, i64, vp, vp, vp)
 _sig("cft_embedding_scatter_slice", C.c_int, C.c_int, vp, i64, vp, i64, i64, i64, vp, vp, vp)
 _sig("cft_grad_stats", C.c_int, C.c_int, vp, i64, f64, vp, vp)
 _sig("cft_set_kernel_variant", C.c_int, C.c_int, C.c_int)

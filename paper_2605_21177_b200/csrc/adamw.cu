@@ -152,6 +152,19 @@ __device__ __forceinline__ void write_back4(P* __restrict__ param, const cft_seg
   }
 }
 
+// a rejected step (non-finite gradient or loss flagged in stats[1]) updates nothing, but the
+// accumulator is still re-zeroed when this kernel owns that (zero_grad): the next step's
+// red-add wgrad must not fold the rejected gradient in
+__device__ __forceinline__ bool rejected_step(const double* stats, float* grad, long long n,
+                                              int zero_grad) {
+  if (!stats || reinterpret_cast<const unsigned long long*>(stats)[1] == 0) return false;
+  if (zero_grad)
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+      grad[i] = 0.f;
+  return true;
+}
+
 // (measured, tools/probe_adamw.py: forcing 4 resident blocks (64 registers, spills) or 4 float4
 // groups per thread both ran slower than 2 groups at 86 registers)
 template <typename P>
@@ -162,7 +175,7 @@ __global__ void __launch_bounds__(kThreads)
                      const cft_segment* __restrict__ segs, int nseg,
                      const double* __restrict__ stats, float* __restrict__ precond, int zero_grad,
                      double clip, P* const* __restrict__ peers, int npeers) {
-  if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
+  if (rejected_step(stats, grad, n, zero_grad)) return;
   if (clip > 0.0 && stats) {  // global-norm clip from the statistics pass, on the device
     const double nrm = sqrt(stats[0]);
     if (nrm > clip) gscale = static_cast<float>(static_cast<double>(gscale) * (clip / nrm));
@@ -315,7 +328,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
                           const double* __restrict__ stats, float* __restrict__ precond,
                           int zero_grad, double clip, P* const* __restrict__ peers, int npeers) {
   using namespace cft::ptx;
-  if (stats && reinterpret_cast<const unsigned long long*>(stats)[1] != 0) return;
+  if (rejected_step(stats, grad, n, zero_grad)) return;
   if (clip > 0.0 && stats) {
     const double nrm = sqrt(stats[0]);
     if (nrm > clip) gscale = static_cast<float>(static_cast<double>(gscale) * (clip / nrm));

@@ -448,6 +448,35 @@ void Engine::wait_step(int64_t t, double* loss, double* gsq) {
   CFT_CUDA(cudaEventSynchronize(stats_ev_[t % 4]));
   if (loss) *loss = host_stats_[t * 4 + 3] / cfg_.micro_batches;
   if (gsq) *gsq = host_stats_[t * 4];
+  scan_results(t);
+  if (!sticky_error_.empty()) throw Error(sticky_error_);
+}
+
+// The rejection check of an unchecked run, on the statistics rows the host already holds
+// (steps < = upto have completed).  The reference throws at the rejected step and never
+// advances n (optimizer.cpp:169-173); here the step's update was skipped on the device, so
+// the host undoes its n increment and records the error, raised from then on.
+void Engine::scan_results(int64_t upto) {
+  for (; scanned_ <= upto && scanned_ < t_; ++scanned_) {
+    const int64_t t = scanned_;
+    const double* h = host_stats_ + t * 4;
+    uint64_t nbad;
+    std::memcpy(&nbad, &h[1], 8);
+    if (!nbad && std::isfinite(h[3])) continue;
+    const int c = traj_chunk_[t];
+    n_local_[c] -= 1;
+    if (!sticky_error_.empty()) continue;
+    const std::string ctx = "step " + std::to_string(t) + ", chunk " + std::to_string(c) + ": ";
+    if (!std::isfinite(h[3])) {
+      sticky_error_ = ctx + "non-finite loss";
+    } else {
+      int64_t bad;
+      std::memcpy(&bad, &h[2], 8);
+      sticky_error_ = ctx + "step: non-finite gradient at element " + std::to_string(bad) +
+                      " (chunk " + std::to_string(c) + ", local step " +
+                      std::to_string(n_local_[c] + 1) + ")";
+    }
+  }
 }
 
 Engine::~Engine() {
@@ -562,6 +591,7 @@ void Engine::offload_chunk(int chunk) {
 
 int Engine::step_begin() {
   CFT_CHECK(!finished_, "engine: finished");
+  if (!sticky_error_.empty()) throw Error(sticky_error_);
   CFT_CHECK(t_ < cfg_.total_steps, "scheduler: step_begin past total_steps");
   const host::BeginActions a = sched_->step_begin();
   active_ = a.active;
@@ -647,8 +677,8 @@ void Engine::forward_backward(const Batch& b, int mb) {
     if (L.spec.type == kLinear) add_work(kFwdGemm, 2.0 * rows * L.in_w * L.out_w);
     switch (L.spec.type) {
       case kEmbedding:
-        if (cft_embedding_gather(static_cast<cft_dtype>(dt), param_ptr(L.w), L.spec.b, tok,
-                                 rows * std::max(1, L.spec.c), out, s) != CFT_OK)
+        if (cft_embedding_gather(static_cast<cft_dtype>(dt), param_ptr(L.w), L.spec.a, L.spec.b,
+                                 tok, rows * std::max(1, L.spec.c), out, nullptr, s) != CFT_OK)
           throw Error(last_error());
         break;
       case kLinear:
@@ -944,6 +974,7 @@ void Engine::step_end() {
       throw Error(ctx + "step: non-finite gradient at element " + std::to_string(bad) + " (chunk " +
                   std::to_string(c) + ", local step " + std::to_string(n_local_[c] + 1) + ")");
     }
+    scanned_ = t_ + 1;
   }
   ++t_;
 }
@@ -955,6 +986,13 @@ void Engine::finish() {
   CFT_CUDA(cudaStreamSynchronize(d2h_));
   CFT_CUDA(cudaStreamSynchronize(h2d_));
   finished_ = true;
+  scan_results(t_ - 1);
+  if (!cfg_.check_every_step) {  // input range errors counted on the device by unchecked steps
+    CFT_CUDA(cudaMemcpy(host_flags_, flags_, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    if (sticky_error_.empty() && host_flags_[1]) sticky_error_ = "embedding: token id out of range";
+    if (sticky_error_.empty() && host_flags_[0]) sticky_error_ = "loss: label out of range";
+  }
+  if (!sticky_error_.empty()) throw Error(sticky_error_);
 }
 
 void Engine::trajectory(int64_t* step, int32_t* chunk, double* loss, double* gsq, int64_t* n) const {

@@ -311,6 +311,11 @@ class Engine {
   int64_t t_ = 0;
   int mb_done_ = 0;
   bool finished_ = false;
+  // unchecked runs (check_every_step = 0): steps whose statistics row the host has read, and
+  // the first rejection found there -- sticky, raised by wait_step / finish / step_begin
+  int64_t scanned_ = 0;
+  std::string sticky_error_;
+  void scan_results(int64_t upto);
   std::vector<int32_t> traj_chunk_;
   std::vector<int64_t> traj_epoch_;
   std::vector<int64_t> traj_step_;

@@ -65,7 +65,8 @@ void linear_dinput(const double*, int, int, const double*, int, double*, cudaStr
 void linear_dweight(const double*, int, int, const double*, int, long long, long long, double*,
                     cudaStream_t);
 void linear_dbias(const double*, int, int, long long, long long, double*, cudaStream_t);
-void embedding_gather(const double*, int, const int*, int, double*, cudaStream_t);
+// ids outside [0, rows) produce a zero row (no read)
+void embedding_gather(const double*, long long rows, int, const int*, int, double*, cudaStream_t);
 void embedding_scatter(const double*, int, const int*, int, long long, long long, double*,
                        unsigned long long*, cudaStream_t);
 void layernorm_forward(const double*, int, int, const double*, const double*, double, double*,

@@ -73,12 +73,13 @@ __global__ void k_linear_dbias(const double* dy, int batch, int out_dim, long lo
 }
 
 // kernels_serial.cpp:60-67
-__global__ void k_embedding_gather(const double* table, int dim, const int* tokens, int positions,
-                                   double* y) {
+__global__ void k_embedding_gather(const double* table, long long rows, int dim, const int* tokens,
+                                   int positions, double* y) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= (long long)positions * dim) return;
   const int p = static_cast<int>(t / dim), j = static_cast<int>(t % dim);
-  y[t] = table[(size_t)tokens[p] * dim + j];
+  const long long tok = tokens[p];
+  y[t] = (tok >= 0 && tok < rows) ? table[(size_t)tok * dim + j] : 0.0;
 }
 
 // kernels_serial.cpp:69-85: per target row, positions ascending
@@ -210,11 +211,11 @@ void linear_dbias(const double* dy, int batch, int out_dim, long long rb, long l
   k_linear_dbias<<<GRID(re - rb), 0, s>>>(dy, batch, out_dim, rb, re, db);
   check_launch("f64 linear_dbias");
 }
-void embedding_gather(const double* table, int dim, const int* tokens, int positions, double* y,
-                      cudaStream_t s) {
+void embedding_gather(const double* table, long long rows, int dim, const int* tokens, int positions,
+                      double* y, cudaStream_t s) {
   const long long n = (long long)positions * dim;
   if (n == 0) return;
-  k_embedding_gather<<<GRID(n), 0, s>>>(table, dim, tokens, positions, y);
+  k_embedding_gather<<<GRID(n), 0, s>>>(table, rows, dim, tokens, positions, y);
   check_launch("f64 embedding_gather");
 }
 void embedding_scatter(const double* dy, int dim, const int* tokens, int positions, long long rb,
@@ -357,11 +358,14 @@ void cft_kernels_embedding_gather(const double* table, int dim, const int* token
                                   double* y) {
   if (positions <= 0) return;
   run_void([&] {
-    int max_tok = 0;
+    // only rows [0, max id] are staged; a negative id (undefined in the reference's kernel,
+    // which the ops layer never lets through, ops.cpp:53-54) yields a zero row, never a read
+    int max_tok = -1;
     for (int p = 0; p < positions; ++p) max_tok = std::max(max_tok, tokens[p]);
     Dev d_t(table, sizeof(double) * (size_t)(max_tok + 1) * dim);
     Dev d_tok(tokens, sizeof(int) * positions), d_y(nullptr, sizeof(double) * positions * dim);
-    cft::f64::embedding_gather(d_t.as<double>(), dim, d_tok.as<int>(), positions, d_y.as<double>(), 0);
+    cft::f64::embedding_gather(d_t.as<double>(), max_tok + 1, dim, d_tok.as<int>(), positions,
+                               d_y.as<double>(), 0);
     d_y.back(y);
   });
 }

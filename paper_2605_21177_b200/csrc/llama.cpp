@@ -280,7 +280,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
 
   // ---- forward ----
   pb(kFwdOther);
-  if (cft_embedding_gather(CFT_BF16, P(0), d, tok, N, lb_[0].x, st) != CFT_OK)
+  if (cft_embedding_gather(CFT_BF16, P(0), V, d, tok, N, lb_[0].x, nullptr, st) != CFT_OK)
     throw Error(last_error());
   pe();
   // one decoder layer's forward from its input x_l; `keep_ug`: also store [u | g] (the SwiGLU

@@ -48,7 +48,7 @@ void linear_dinput(const double*, int, int, const double*, int, double*, cudaStr
 void linear_dweight(const double*, int, int, const double*, int, long long, long long, double*,
                     cudaStream_t);
 void linear_dbias(const double*, int, int, long long, long long, double*, cudaStream_t);
-void embedding_gather(const double*, int, const int*, int, double*, cudaStream_t);
+void embedding_gather(const double*, long long, int, const int*, int, double*, cudaStream_t);
 void embedding_scatter(const double*, int, const int*, int, long long, long long, double*,
                        unsigned long long*, cudaStream_t);
 }  // namespace f64
@@ -60,15 +60,23 @@ bool tma_ok(const void* p, int64_t row_elems) {
   return row_elems > 0 && (row_elems % 8) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
 }
 
-// y[p,:] = table[tok[p],:]  (16-byte vectorised rows when possible)
+// y[p,:] = table[tok[p],:]  (16-byte vectorised rows when possible).  An id outside
+// [0, rows) reads nothing: its row is zeroed and counted (the reference's ops layer throws
+// before the gather, ops.cpp:53-54; here the count is the device-side form of that throw).
 template <typename T>
-__global__ void gather_kernel(const T* __restrict__ table, long long dim,
+__global__ void gather_kernel(const T* __restrict__ table, long long rows, long long dim,
                               const int32_t* __restrict__ tokens, long long positions,
-                              T* __restrict__ y) {
+                              T* __restrict__ y, unsigned long long* bad) {
   const long long p = blockIdx.x;
   if (p >= positions) return;
-  const T* src = table + (long long)tokens[p] * dim;
+  const long long tok = tokens[p];
   T* dst = y + p * dim;
+  if (tok < 0 || tok >= rows) {
+    if (bad && threadIdx.x == 0) atomicAdd(bad, 1ull);
+    for (long long j = threadIdx.x; j < dim; j += blockDim.x) dst[j] = T(0.f);
+    return;
+  }
+  const T* src = table + tok * dim;
   constexpr int V = 16 / sizeof(T);
   if (dim % V == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -251,22 +259,24 @@ int cft_softmax_ce(cft_dtype dtype, const void* y, const int32_t* labels, int64_
   });
 }
 
-int cft_embedding_gather(cft_dtype dtype, const void* table, int64_t dim, const int32_t* tokens,
-                         int64_t positions, void* y, cft_stream_t stream) {
+int cft_embedding_gather(cft_dtype dtype, const void* table, int64_t table_rows, int64_t dim,
+                         const int32_t* tokens, int64_t positions, void* y,
+                         unsigned long long* bad_dev, cft_stream_t stream) {
   return guarded([&] {
     auto s = static_cast<cudaStream_t>(stream);
     if (positions <= 0 || dim <= 0) return;
     const int threads = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, dim / 8)));
     if (dtype == CFT_BF16)
       gather_kernel<<<(unsigned)positions, threads, 0, s>>>(
-          static_cast<const __nv_bfloat16*>(table), dim, tokens, positions,
-          static_cast<__nv_bfloat16*>(y));
+          static_cast<const __nv_bfloat16*>(table), table_rows, dim, tokens, positions,
+          static_cast<__nv_bfloat16*>(y), bad_dev);
     else if (dtype == CFT_F32)
-      gather_kernel<<<(unsigned)positions, threads, 0, s>>>(static_cast<const float*>(table), dim,
-                                                            tokens, positions, static_cast<float*>(y));
+      gather_kernel<<<(unsigned)positions, threads, 0, s>>>(static_cast<const float*>(table),
+                                                            table_rows, dim, tokens, positions,
+                                                            static_cast<float*>(y), bad_dev);
     else
-      f64::embedding_gather(static_cast<const double*>(table), (int)dim, tokens, (int)positions,
-                            static_cast<double*>(y), s);
+      f64::embedding_gather(static_cast<const double*>(table), table_rows, (int)dim, tokens,
+                            (int)positions, static_cast<double*>(y), s);
     check_launch("embedding_gather");
   });
 }

@@ -102,14 +102,18 @@ def linear_dbias_slice(dy: torch.Tensor, row_begin: int, row_end: int,
     return out
 
 
-def embedding_gather(table: torch.Tensor, tokens: torch.Tensor, out=None, stream=None):
+def embedding_gather(table: torch.Tensor, tokens: torch.Tensor, out=None, bad=None, stream=None):
+    """y[p] = table[tokens[p]]; ids outside [0, rows) give a zero row and are counted in `bad`
+    (a 1-element int64 device tensor) when given."""
     _contig(table, tokens)
     positions = tokens.numel()
-    dim = table.shape[1]
+    rows, dim = table.shape
     if out is None:
         out = torch.empty(positions, dim, dtype=table.dtype, device=table.device)
-    N.check(N.lib.cft_embedding_gather(_dtype(table), table.data_ptr(), dim, tokens.data_ptr(),
-                                       positions, out.data_ptr(), _stream(stream)),
+    N.check(N.lib.cft_embedding_gather(_dtype(table), table.data_ptr(), rows, dim,
+                                       tokens.data_ptr(), positions, out.data_ptr(),
+                                       bad.data_ptr() if bad is not None else None,
+                                       _stream(stream)),
             "embedding_gather")
     return out
 

@@ -164,6 +164,30 @@ def test_nonfinite_gradient_is_rejected_without_advancing(cuda):
     assert eng.chunk_counters()[1] == 0
 
 
+def test_unchecked_run_raises_rejection_at_wait_and_keeps_accumulator_zero(cuda):
+    """check_every_step = 0: a rejected step is detected from its statistics row at the next
+    wait_step / finish (sticky), its n increment is undone, and the fp32 accumulator is still
+    re-zeroed by the skipped AdamW so no later step folds the rejected gradient in."""
+    import dataclasses
+    from paper_2605_21177_b200.engine import ChunkEngine, Error
+    case = CASES["linear_exact"]
+    opts = dataclasses.replace(options_of(case, "fp32"), check_every_step=False)
+    eng = ChunkEngine(model_of(case), np.array(case["init_params"]), 12, opts)
+    b = batches_of(case)[0]
+    bad = dict(b)
+    bad["x"] = b["x"].copy()
+    bad["x"][0, 0] = np.inf
+    eng.step([eng.stage(b, device=True)])
+    eng.step([eng.stage(bad, device=True)])  # rejected on the device, not raised yet
+    torch.cuda.synchronize()
+    assert float(eng.grad_tensor().abs().max()) == 0.0
+    with pytest.raises(Error, match=r"step 1, chunk 1: (non-finite loss|step: non-finite gradient)"):
+        eng.wait_step(1)
+    assert eng.chunk_counters()[1] == 0
+    with pytest.raises(Error, match=r"step 1, chunk 1"):  # sticky
+        eng.step([eng.stage(b, device=True)])
+
+
 @pytest.mark.parametrize("name", ["linear_exact", "emb_ln_mb"])
 def test_host_batches_match_device_batches(cuda, name):
     """Pinned-host batches go through the double-buffered upload stream; results must be
