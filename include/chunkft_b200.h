@@ -232,6 +232,19 @@ int cft_softmax_ce(cft_dtype dtype, const void* y, const int32_t* labels, int64_
                    int64_t cols, void* dy, double* loss_dev, uint64_t* bad_label_dev,
                    cft_stream_t stream);
 
+/* Causal GQA flash attention over the fused qkv projection buffer (the Llama decoder's
+ * attention; the reference has none).  bf16, tcgen05.
+ *   qkv  [batch*seq][(hq + 2 hkv) * head_dim]: q heads | k heads | v heads per token row
+ *   o    [batch*seq][hq * head_dim]
+ *   lse  [batch][hq][seq] fp32: log2-sum-exp of the scaled scores (forward output, backward input)
+ *   dqkv gets dQ | dK | dV in the qkv layout; scratch = batch*hq*seq floats (rowsum(dO*O)).
+ * head_dim 64 or 128, seq a multiple of 128, hq / hkv even.  No allocation. */
+int cft_attention_fwd(const void* qkv, int batch, int hq, int hkv, int seq, int head_dim,
+                      void* o, float* lse, cft_stream_t stream);
+int cft_attention_bwd(const void* qkv, const void* o, const void* dout, const float* lse,
+                      int batch, int hq, int hkv, int seq, int head_dim, void* dqkv,
+                      float* scratch, cft_stream_t stream);
+
 /* Hyper-parameters (AdamWHyper, optimizer.hpp:15-22). */
 typedef struct {
   double eta;

@@ -1,4 +1,5 @@
-// attn.h -- causal GQA attention (cuDNN fused SDPA) over the fused qkv projection buffer.
+// attn.h -- causal GQA flash attention (own tcgen05 kernels, attn_fa.cu) over the fused qkv
+// projection buffer.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -15,14 +16,11 @@ class Context {
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
 
-  // Build (and cache) the forward and backward graphs for a shape.
+  // Check the shape (head_dim 64 / 128, seq % 128 == 0, an even number of query heads per KV
+  // head) and allocate the backward's scratch; nothing is allocated in forward / backward.
   void prepare(int batch, int hq, int hkv, int seq, int head_dim);
-  // Time every engine configuration cuDNN offers for the shape on the given buffers and keep
-  // the fastest forward and backward plan (overwrites the buffers' contents).
-  void autotune(int batch, int hq, int hkv, int seq, int head_dim, void* qkv, void* o,
-                float* stats, void* dout, void* dqkv, cudaStream_t stream);
   // qkv: [batch*seq][(hq + 2 hkv) * head_dim] bf16; o: [batch*seq][hq * head_dim] bf16;
-  // stats: [batch][hq][seq] fp32 (row log-sum-exp, saved for the backward).
+  // stats: [batch][hq][seq] fp32 (row log2-sum-exp of the scaled scores, for the backward).
   void forward(int batch, int hq, int hkv, int seq, int head_dim, const void* qkv, void* o,
                float* stats, cudaStream_t stream);
   // dqkv gets dQ | dK | dV in the same fused layout.

@@ -1,0 +1,886 @@
+// attn_fa.cu -- causal GQA flash attention, forward and backward, on sm_100a tensor cores.
+//
+// The Llama decoder's attention (the reference has none) over
+// the fused qkv projection buffer [token][q heads | k heads | v heads] (row pitch
+// (Hq + 2 Hkv) * hd), read in place by TMA -- no transposes, no library.
+//
+// Tiles: 128 query rows x 128 (forward) / 64 (backward) key rows; head_dim 64 or 128.  Every
+// operand is staged by TMA in the 128-byte-swizzled K-major layout, and the same smem bytes
+// serve as the MN-major operand where a GEMM needs the transpose (V in O += P.V, K in
+// dQ += dS.K, Q / dO in dK / dV): rows of a swizzled tile are the K dimension there, 16 rows
+// = one 2048-byte UMMA_K step, and the leading-byte offset is the distance between 64-column
+// blocks.  Accumulators (S, dP, O, dQ, dK, dV) live in TMEM; one elected thread issues
+// tcgen05.mma; softmax / gradient warps own one TMEM lane = one row each.
+//
+//  forward   one CTA = two query heads of one GQA group x one 128-row query tile: the heads
+//            share every K / V tile, and their softmax warp groups ping-pong with the tensor
+//            pipe (head A's softmax overlaps head B's MMAs).  Online softmax in the exp2
+//            domain; the O accumulator (TMEM) is rescaled only when a row's running max grows
+//            by more than 2^8 (the final 1/l is exact for any reference max).  Writes O (bf16)
+//            and the row log2-sum-exp (fp32, consumed only by the backward here).
+//  backward  D = rowsum(dO * O); then two deterministic kernels, no atomics:
+//            dK/dV: one CTA = one 128-row key tile of one KV head, looping over all the
+//                   group's query heads and 64-row query blocks, so the GQA head reduction
+//                   of dK / dV happens in TMEM; S^T / dP^T double-buffered in TMEM.
+//            dQ:    one CTA = one 128-row query tile of one head, looping over 64-row key
+//                   blocks; S / dP double-buffered, dQ accumulated in TMEM.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "attn.h"
+#include "cft_common.h"
+#include "tc_ptx.cuh"
+
+namespace cft::attn {
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+using namespace cft::ptx;
+
+constexpr uint32_t kBlk128 = 128 * 128;  // one 64-column block of a 128-row tile (16 KB)
+constexpr uint32_t kBlk64 = 64 * 128;    // one 64-column block of a 64-row tile (8 KB)
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// generic-proxy smem writes (P, dS) -> visible to the tensor pipe's async proxy
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float f32(uint32_t u) { return __uint_as_float(u); }
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// UMMA descriptors over 128B-swizzled tiles whose 64-column blocks are `blk` bytes apart.
+// K-major operand, K step k (16 columns): block k/4, 32 bytes per step inside the 128 B row.
+__device__ __forceinline__ uint64_t desc_k(const void* base, int k, uint32_t blk) {
+  return smem_desc_sw128(smem_u32(base) + (k >> 2) * blk + (k & 3) * 32, 16, 1024);
+}
+// MN-major operand (the K dimension runs down the tile's rows): K step k = 16 rows = 2048 B;
+// the MN dimension's 64-column blocks are `blk` bytes apart (leading-byte offset).
+__device__ __forceinline__ uint64_t desc_mn(const void* base, int k, uint32_t blk) {
+  return smem_desc_sw128(smem_u32(base) + k * 2048, blk, 1024);
+}
+// 16-byte chunk c (0..7) of row r in a [rows][128 B] SW128 block (TMA's 128B swizzle)
+__device__ __forceinline__ void st_swz(uint8_t* blk, int r, int c, const uint32_t* w) {
+  *reinterpret_cast<uint4*>(blk + r * 128 + ((c ^ (r & 7)) << 4)) =
+      make_uint4(w[0], w[1], w[2], w[3]);
+}
+// 32 fp32 values -> 32 bf16 in four swizzled chunks starting at chunk c0 of row r
+__device__ __forceinline__ void st_swz32(uint8_t* blk, int r, int c0, const float* v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t w[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) w[t] = pack_bf16(v[q * 8 + 2 * t], v[q * 8 + 2 * t + 1]);
+    st_swz(blk, r, c0 + q, w);
+  }
+}
+// 32 fp32 (scaled) -> 32 bf16 to global (two 32-byte stores)
+__device__ __forceinline__ void st_row32(bf16* p, const uint32_t (&r)[32], float s) {
+  uint32_t w[8];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      w[t] = pack_bf16(f32(r[h * 16 + 2 * t]) * s, f32(r[h * 16 + 2 * t + 1]) * s);
+    st_global_256(p + h * 16, w);
+  }
+}
+
+struct FwdArgs {
+  int B, H, KVH, S, ld;  // ld = qkv row pitch (elements)
+  bf16* o;
+  int ldo;
+  float* lse;  // [B][H][S] log2-sum-exp of the scaled scores
+  float scale_log2;
+};
+
+// ------------------------------------------------------------------------------------------
+// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax of head A, 6-9 of B
+template <int HD>
+struct FwdSmem {
+  static constexpr uint32_t TILE = 128 * HD * 2;
+  static constexpr uint32_t PT = 128 * 128 * 2;
+  static constexpr uint32_t Q0 = 0, K = 2 * TILE, V0 = 3 * TILE, P0 = 5 * TILE,
+                            BAR = 5 * TILE + 2 * PT;
+  static constexpr size_t BYTES = 1024 + BAR + 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(320, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, const FwdArgs a) {
+  using L = FwdSmem<HD>;
+  constexpr int NB = HD / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* qfull = bar;
+  uint64_t* kfull = bar + 1;
+  uint64_t* kempty = bar + 2;
+  uint64_t* vfull = bar + 3;   // [2]
+  uint64_t* vempty = bar + 5;  // [2]
+  uint64_t* sfull = bar + 7;   // [2] per head
+  uint64_t* pfull = bar + 9;   // [2]
+  uint64_t* ofull = bar + 11;  // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 13);
+
+  const int nq = a.S / 128, G = a.H / a.KVH, G2 = G / 2;
+  const int per_i = a.B * a.KVH * G2;
+  const int i = nq - 1 - static_cast<int>(blockIdx.x) / per_i;  // longest rows first
+  const int rest = static_cast<int>(blockIdx.x) % per_i;
+  const int b = rest / (a.KVH * G2), kvh = (rest / G2) % a.KVH, pr = rest % G2;
+  const int h0 = kvh * G + 2 * pr;
+  const int n = i + 1;
+  const int qrow = b * a.S + i * 128, krow = b * a.S;
+  const int kcol = a.H * HD + kvh * HD, vcol = (a.H + a.KVH) * HD + kvh * HD;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm);
+    mbar_init(qfull, 1);
+    mbar_init(kfull, 1);
+    mbar_init(kempty, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&vfull[t], 1);
+      mbar_init(&vempty[t], 1);
+      mbar_init(&sfull[t], 1);
+      mbar_init(&pfull[t], 128);
+      mbar_init(&ofull[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(qfull, 2 * L::TILE);
+      for (int t = 0; t < 2; ++t)
+        for (int kb = 0; kb < NB; ++kb)
+          tma_load_2d(sm + L::Q0 + t * L::TILE + kb * kBlk128, &tm, qfull,
+                      (h0 + t) * HD + kb * 64, qrow);
+      for (int j = 0; j < n; ++j) {
+        mbar_wait(kempty, (j & 1) ^ 1);
+        mbar_expect_tx(kfull, L::TILE);
+        for (int kb = 0; kb < NB; ++kb)
+          tma_load_2d(sm + L::K + kb * kBlk128, &tm, kfull, kcol + kb * 64, krow + j * 128);
+        const int vb = j & 1;
+        mbar_wait(&vempty[vb], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&vfull[vb], L::TILE);
+        for (int kb = 0; kb < NB; ++kb)
+          tma_load_2d(sm + L::V0 + vb * L::TILE + kb * kBlk128, &tm, &vfull[vb], vcol + kb * 64,
+                      krow + j * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_S = idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t ID_O = idesc_bf16_f32(128, HD, false, true);
+      auto issue_s = [&](int t) {
+        const uint8_t* q = sm + L::Q0 + t * L::TILE;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16(tbase + t * 128, desc_k(q, k, kBlk128), desc_k(sm + L::K, k, kBlk128), ID_S,
+                    k > 0);
+        umma_commit(&sfull[t]);
+      };
+      auto issue_pv = [&](int t, int vb, int j) {
+        const uint8_t* p = sm + L::P0 + t * L::PT;
+        const uint8_t* v = sm + L::V0 + vb * L::TILE;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_bf16(tbase + 256 + t * HD, desc_k(p, k, kBlk128), desc_mn(v, k, kBlk128), ID_O,
+                    (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&ofull[t]);
+      };
+      mbar_wait(qfull, 0);
+      mbar_wait(kfull, 0);
+      tc_fence_after();
+      issue_s(0);
+      issue_s(1);
+      umma_commit(kempty);
+      for (int j = 0; j < n; ++j) {
+        const int vb = j & 1;
+        mbar_wait(&vfull[vb], (j >> 1) & 1);
+        mbar_wait(&pfull[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, vb, j);
+        if (j + 1 < n) {
+          mbar_wait(kfull, (j + 1) & 1);
+          tc_fence_after();
+          issue_s(0);
+        }
+        mbar_wait(&pfull[1], j & 1);
+        tc_fence_after();
+        issue_pv(1, vb, j);
+        umma_commit(&vempty[vb]);
+        if (j + 1 < n) {
+          issue_s(1);
+          umma_commit(kempty);
+        }
+      }
+    }
+  } else {
+    const int t = (warp - 2) / 4;
+    const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
+    const int r = quarter * 32 + lane;
+    const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tbase + lo + t * 128, tO = tbase + lo + 256 + t * HD;
+    uint8_t* sP = sm + L::P0 + t * L::PT;
+    const float c = a.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(&sfull[t], j & 1);
+      tc_fence_after();
+      const bool diag = j == i;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tS + cc * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (!diag || cc * 32 + e <= r) mx = fmaxf(mx, f32(v[e]));
+      }
+      const float m_new = fmaxf(m, mx * c);
+      if (j > 0) {  // PV of the previous block done: P buffer and O free
+        mbar_wait(&ofull[t], (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (j == 0) {
+        m = m_new;
+      } else if (__any_sync(0xffffffffu, m_new > m + 8.f)) {
+        const float alpha = ex2(m - m_new);
+        l *= alpha;
+        m = m_new;
+#pragma unroll
+        for (int cc = 0; cc < HD / 32; ++cc) {
+          uint32_t v[32];
+          tmem_ld32(tO + cc * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(f32(v[e]) * alpha);
+          tmem_st32(tO + cc * 32, v);
+        }
+        tmem_wait_st();
+      }
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tS + cc * 32, v);
+        tmem_wait_ld();
+        float p[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          p[e] = (diag && cc * 32 + e > r) ? 0.f : ex2(fmaf(f32(v[e]), c, -m));
+          l += p[e];
+        }
+        st_swz32(sP + (cc >> 1) * kBlk128, r, (cc & 1) * 4, p);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&pfull[t]);
+    }
+    mbar_wait(&ofull[t], (n - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    bf16* out = a.o + static_cast<long long>(qrow + r) * a.ldo + (h0 + t) * HD;
+#pragma unroll
+    for (int cc = 0; cc < HD / 32; ++cc) {
+      uint32_t v[32];
+      tmem_ld32(tO + cc * 32, v);
+      tmem_wait_ld();
+      st_row32(out + cc * 32, v, inv);
+    }
+    a.lse[(static_cast<long long>(b) * a.H + h0 + t) * a.S + i * 128 + r] = m + __log2f(l);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tbase);
+}
+
+// ------------------------------------------------------------------------------------------
+// backward preprocessing: D[b][h][s] = sum_d dO * O (fp32), one warp per (token, head)
+__global__ void attn_bwd_dot_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout,
+                                    int ldo, int N, int H, int S, int HD, float* __restrict__ D) {
+  const long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= static_cast<long long>(N) * H) return;
+  const int row = static_cast<int>(w / H), h = static_cast<int>(w % H);
+  const bf16* po = o + static_cast<long long>(row) * ldo + h * HD;
+  const bf16* pd = dout + static_cast<long long>(row) * ldo + h * HD;
+  float acc = 0.f;
+  for (int e = lane * 2; e < HD; e += 64) {
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(po + e));
+    const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(pd + e));
+    acc = fmaf(a.x, g.x, fmaf(a.y, g.y, acc));
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (lane == 0) D[(static_cast<long long>(row / S) * H + h) * S + row % S] = acc;
+}
+
+struct BwdArgs {
+  int B, H, KVH, S, ld;  // qkv / dqkv row pitch
+  int ldo;               // dO row pitch (H * hd)
+  const float* lse;      // [B][H][S] log2-sum-exp from the forward
+  const float* D;        // [B][H][S]
+  bf16* dqkv;
+  float scale_log2, scale;
+};
+
+// ------------------------------------------------------------------------------------------
+// dK / dV: warp 0 TMA, warp 1 MMA, warps 2-5 one key row each
+template <int HD>
+struct KvSmem {
+  static constexpr uint32_t TILE = 128 * HD * 2;  // K or V tile (128 rows)
+  static constexpr uint32_t QB = 64 * HD * 2;     // Q or dO block (64 rows)
+  static constexpr uint32_t PB = 128 * 64 * 2;    // P^T or dS^T block (128 kv x 64 q)
+  static constexpr uint32_t K = 0, V = TILE, Q0 = 2 * TILE, DO0 = Q0 + 2 * QB,
+                            P0 = DO0 + 2 * QB, DS0 = P0 + 2 * PB, LSE0 = DS0 + 2 * PB,
+                            D0 = LSE0 + 2 * 256, BAR = D0 + 2 * 256;
+  static constexpr size_t BYTES = 1024 + BAR + 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm128,
+                         const __grid_constant__ CUtensorMap tm64,
+                         const __grid_constant__ CUtensorMap tmdo, const BwdArgs a) {
+  using L = KvSmem<HD>;
+  constexpr int NB = HD / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* kvfull = bar;
+  uint64_t* qfull = bar + 1;   // [2] Q, dO, lse, D of a query block
+  uint64_t* sfree = bar + 3;   // [2] smem stage (Q, dO, P^T, dS^T) consumed by the MMAs
+  uint64_t* tfull = bar + 5;   // [2] S^T, dP^T in TMEM
+  uint64_t* pfull = bar + 7;   // [2] P^T, dS^T written
+  uint64_t* done = bar + 9;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 10);
+
+  const int nk = a.S / 128, G = a.H / a.KVH;
+  const int per_j = a.B * a.KVH;
+  const int j = static_cast<int>(blockIdx.x) / per_j;  // ascending: most query blocks first
+  const int rest = static_cast<int>(blockIdx.x) % per_j;
+  const int b = rest / a.KVH, kvh = rest % a.KVH;
+  (void)nk;
+  const int nper = a.S / 64 - 2 * j;  // query blocks at or after this key tile, per head
+  const int n_it = G * nper;
+  const int kvrow = b * a.S + j * 128;
+  const int kcol = a.H * HD + kvh * HD, vcol = (a.H + a.KVH) * HD + kvh * HD;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm128);
+    tma_prefetch(&tm64);
+    tma_prefetch(&tmdo);
+    mbar_init(kvfull, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qfull[s], 1);
+      mbar_init(&sfree[s], 1);
+      mbar_init(&tfull[s], 1);
+      mbar_init(&pfull[s], 128);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  // TMEM: dV [0, HD), dK [HD, 2HD), stage s: S^T [2HD + 128 s, +64), dP^T [+64, +128)
+  auto tst = [&](int s) { return tbase + 2 * HD + 128 * s; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      mbar_expect_tx(kvfull, 2 * L::TILE);
+      for (int kb = 0; kb < NB; ++kb) {
+        tma_load_2d(sm + L::K + kb * kBlk128, &tm128, kvfull, kcol + kb * 64, kvrow);
+        tma_load_2d(sm + L::V + kb * kBlk128, &tm128, kvfull, vcol + kb * 64, kvrow);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it & 1, u = it >> 1;
+        const int h = kvh * G + it / nper, qb = 2 * j + it % nper;
+        const int qr = b * a.S + qb * 64;
+        mbar_wait(&sfree[s], (u & 1) ^ 1);
+        mbar_expect_tx(&qfull[s], 2 * L::QB + 512);
+        for (int kb = 0; kb < NB; ++kb) {
+          tma_load_2d(sm + L::Q0 + s * L::QB + kb * kBlk64, &tm64, &qfull[s], h * HD + kb * 64, qr);
+          tma_load_2d(sm + L::DO0 + s * L::QB + kb * kBlk64, &tmdo, &qfull[s], h * HD + kb * 64, qr);
+        }
+        const long long st = (static_cast<long long>(b) * a.H + h) * a.S + qb * 64;
+        bulk_load_1d(sm + L::LSE0 + s * 256, a.lse + st, 256, &qfull[s], pol);
+        bulk_load_1d(sm + L::D0 + s * 256, a.D + st, 256, &qfull[s], pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
+      constexpr uint32_t ID_A = idesc_bf16_f32(128, HD, false, true);
+      auto issue_s = [&](int it) {
+        const int s = it & 1, u = it >> 1;
+        mbar_wait(&qfull[s], u & 1);
+        tc_fence_after();
+        const uint8_t* q = sm + L::Q0 + s * L::QB;
+        const uint8_t* d = sm + L::DO0 + s * L::QB;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          umma_bf16(tst(s), desc_k(sm + L::K, k, kBlk128), desc_k(q, k, kBlk64), ID_S, k > 0);
+          umma_bf16(tst(s) + 64, desc_k(sm + L::V, k, kBlk128), desc_k(d, k, kBlk64), ID_S, k > 0);
+        }
+        umma_commit(&tfull[s]);
+      };
+      mbar_wait(kvfull, 0);
+      issue_s(0);
+      if (n_it > 1) issue_s(1);
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it & 1, u = it >> 1;
+        mbar_wait(&pfull[s], u & 1);
+        tc_fence_after();
+        const uint8_t* q = sm + L::Q0 + s * L::QB;
+        const uint8_t* d = sm + L::DO0 + s * L::QB;
+        const uint8_t* p = sm + L::P0 + s * L::PB;
+        const uint8_t* ds = sm + L::DS0 + s * L::PB;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
+          umma_bf16(tbase, desc_k(p, k, kBlk128), desc_mn(d, k, kBlk64), ID_A, acc);        // dV
+          umma_bf16(tbase + HD, desc_k(ds, k, kBlk128), desc_mn(q, k, kBlk64), ID_A, acc);  // dK
+        }
+        umma_commit(&sfree[s]);
+        if (it + 2 < n_it) issue_s(it + 2);
+      }
+      umma_commit(done);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
+    const int kvi = j * 128 + r;  // key position within the sequence
+    const float c = a.scale_log2;
+    for (int it = 0; it < n_it; ++it) {
+      const int s = it & 1, u = it >> 1;
+      const int qb = 2 * j + it % nper;
+      mbar_wait(&tfull[s], u & 1);
+      mbar_wait(&qfull[s], u & 1);  // lse / D of the block
+      if (it >= 2) mbar_wait(&sfree[s], (u & 1) ^ 1);  // P^T / dS^T stage free
+      tc_fence_after();
+      const float* sl = reinterpret_cast<const float*>(sm + L::LSE0 + s * 256);
+      const float* sd = reinterpret_cast<const float*>(sm + L::D0 + s * 256);
+      uint8_t* p = sm + L::P0 + s * L::PB;
+      uint8_t* ds = sm + L::DS0 + s * L::PB;
+      const bool diag = qb * 64 < j * 128 + 128;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t vs[32], vp[32];
+        tmem_ld32(lo + tst(s) + cc * 32, vs);
+        tmem_ld32(lo + tst(s) + 64 + cc * 32, vp);
+        tmem_wait_ld();
+        float pv[32], dv[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int qc = cc * 32 + e;
+          const float pe = (diag && qb * 64 + qc < kvi) ? 0.f : ex2(fmaf(f32(vs[e]), c, -sl[qc]));
+          pv[e] = pe;
+          dv[e] = pe * (f32(vp[e]) - sd[qc]);
+        }
+        st_swz32(p, r, cc * 4, pv);
+        st_swz32(ds, r, cc * 4, dv);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&pfull[s]);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    bf16* drow = a.dqkv + static_cast<long long>(kvrow + r) * a.ld;
+#pragma unroll
+    for (int cc = 0; cc < HD / 32; ++cc) {
+      uint32_t v[32];
+      tmem_ld32(tbase + lo + cc * 32, v);
+      tmem_wait_ld();
+      st_row32(drow + vcol + cc * 32, v, 1.f);  // dV
+      tmem_ld32(tbase + lo + HD + cc * 32, v);
+      tmem_wait_ld();
+      st_row32(drow + kcol + cc * 32, v, a.scale);  // dK
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tbase);
+}
+
+// ------------------------------------------------------------------------------------------
+// dQ: warp 0 TMA, warp 1 MMA, warps 2-5 one query row each
+template <int HD>
+struct QSmem {
+  static constexpr uint32_t TILE = 128 * HD * 2;  // Q or dO tile (128 rows)
+  static constexpr uint32_t KB = 64 * HD * 2;     // K or V block (64 rows)
+  static constexpr uint32_t SB = 128 * 64 * 2;    // dS block (128 q x 64 kv)
+  static constexpr uint32_t Q = 0, DO = TILE, K0 = 2 * TILE, V0 = K0 + 2 * KB, DS0 = V0 + 2 * KB,
+                            BAR = DS0 + 2 * SB;
+  static constexpr size_t BYTES = 1024 + BAR + 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm128,
+                       const __grid_constant__ CUtensorMap tm64,
+                       const __grid_constant__ CUtensorMap tmdo, const BwdArgs a) {
+  using L = QSmem<HD>;
+  constexpr int NB = HD / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* qfull = bar;
+  uint64_t* kvfull = bar + 1;  // [2]
+  uint64_t* sfree = bar + 3;   // [2] K, V, dS stage consumed
+  uint64_t* tfull = bar + 5;   // [2] S, dP in TMEM
+  uint64_t* pfull = bar + 7;   // [2] dS written
+  uint64_t* done = bar + 9;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 10);
+
+  const int nq = a.S / 128;
+  const int per_i = a.B * a.H;
+  const int i = nq - 1 - static_cast<int>(blockIdx.x) / per_i;  // longest rows first
+  const int rest = static_cast<int>(blockIdx.x) % per_i;
+  const int b = rest / a.H, h = rest % a.H;
+  const int kvh = h / (a.H / a.KVH);
+  const int n = 2 * i + 2;  // 64-row key blocks up to the diagonal
+  const int qrow = b * a.S + i * 128;
+  const int kcol = a.H * HD + kvh * HD, vcol = (a.H + a.KVH) * HD + kvh * HD;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm128);
+    tma_prefetch(&tm64);
+    tma_prefetch(&tmdo);
+    mbar_init(qfull, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kvfull[s], 1);
+      mbar_init(&sfree[s], 1);
+      mbar_init(&tfull[s], 1);
+      mbar_init(&pfull[s], 128);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  // TMEM: dQ [0, HD), stage s: S [HD + 128 s, +64), dP [+64, +128)
+  auto tst = [&](int s) { return tbase + HD + 128 * s; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(qfull, 2 * L::TILE);
+      for (int kb = 0; kb < NB; ++kb) {
+        tma_load_2d(sm + L::Q + kb * kBlk128, &tm128, qfull, h * HD + kb * 64, qrow);
+        tma_load_2d(sm + L::DO + kb * kBlk128, &tmdo, qfull, h * HD + kb * 64, qrow);
+      }
+      for (int jj = 0; jj < n; ++jj) {
+        const int s = jj & 1, u = jj >> 1;
+        const int kr = b * a.S + jj * 64;
+        mbar_wait(&sfree[s], (u & 1) ^ 1);
+        mbar_expect_tx(&kvfull[s], 2 * L::KB);
+        for (int kb = 0; kb < NB; ++kb) {
+          tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], kcol + kb * 64, kr);
+          tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], vcol + kb * 64, kr);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
+      constexpr uint32_t ID_Q = idesc_bf16_f32(128, HD, false, true);
+      auto issue_s = [&](int jj) {
+        const int s = jj & 1, u = jj >> 1;
+        mbar_wait(&kvfull[s], u & 1);
+        tc_fence_after();
+        const uint8_t* k = sm + L::K0 + s * L::KB;
+        const uint8_t* v = sm + L::V0 + s * L::KB;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          umma_bf16(tst(s), desc_k(sm + L::Q, kk, kBlk128), desc_k(k, kk, kBlk64), ID_S, kk > 0);
+          umma_bf16(tst(s) + 64, desc_k(sm + L::DO, kk, kBlk128), desc_k(v, kk, kBlk64), ID_S,
+                    kk > 0);
+        }
+        umma_commit(&tfull[s]);
+      };
+      mbar_wait(qfull, 0);
+      issue_s(0);
+      if (n > 1) issue_s(1);
+      for (int jj = 0; jj < n; ++jj) {
+        const int s = jj & 1, u = jj >> 1;
+        mbar_wait(&pfull[s], u & 1);
+        tc_fence_after();
+        const uint8_t* k = sm + L::K0 + s * L::KB;
+        const uint8_t* ds = sm + L::DS0 + s * L::SB;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tbase, desc_k(ds, kk, kBlk128), desc_mn(k, kk, kBlk64), ID_Q,
+                    (jj > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&sfree[s]);
+        if (jj + 2 < n) issue_s(jj + 2);
+      }
+      umma_commit(done);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
+    const int qi = i * 128 + r;
+    const long long st = (static_cast<long long>(b) * a.H + h) * a.S + qi;
+    const float lse = a.lse[st], dd = a.D[st];
+    const float c = a.scale_log2;
+    for (int jj = 0; jj < n; ++jj) {
+      const int s = jj & 1, u = jj >> 1;
+      mbar_wait(&tfull[s], u & 1);
+      if (jj >= 2) mbar_wait(&sfree[s], (u & 1) ^ 1);  // dS stage free
+      tc_fence_after();
+      uint8_t* ds = sm + L::DS0 + s * L::SB;
+      const bool diag = jj * 64 + 63 > i * 128;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t vs[32], vp[32];
+        tmem_ld32(lo + tst(s) + cc * 32, vs);
+        tmem_ld32(lo + tst(s) + 64 + cc * 32, vp);
+        tmem_wait_ld();
+        float dv[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int kc = jj * 64 + cc * 32 + e;
+          const float pe = (diag && kc > qi) ? 0.f : ex2(fmaf(f32(vs[e]), c, -lse));
+          dv[e] = pe * (f32(vp[e]) - dd);
+        }
+        st_swz32(ds, r, cc * 4, dv);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&pfull[s]);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD;
+#pragma unroll
+    for (int cc = 0; cc < HD / 32; ++cc) {
+      uint32_t v[32];
+      tmem_ld32(tbase + lo + cc * 32, v);
+      tmem_wait_ld();
+      st_row32(drow + cc * 32, v, a.scale);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tbase);
+}
+
+// ------------------------------------------------------------------------------------------
+
+}  // namespace
+
+namespace {
+CUtensorMap tmap(const void* base, uint64_t cols, uint64_t rows, uint64_t pitch, uint32_t box_rows) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint32_t>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(base, cols, rows, pitch, box_rows);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cache.size() > 1024) cache.clear();
+  CUtensorMap m = make_tmap_bf16(base, cols, rows, pitch, 64, box_rows);
+  cache.emplace(key, m);
+  return m;
+}
+
+// every kernel holds all 512 TMEM columns: request enough shared memory that two CTAs can
+// never share an SM (a second one would stall in tcgen05.alloc)
+constexpr size_t kMinSmem = 120 * 1024;
+template <typename K>
+void set_smem(K kern, size_t bytes) {
+  CFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(std::max(bytes, kMinSmem))));
+}
+
+}  // namespace
+
+void check_shape(int hq, int hkv, int seq, int hd) {
+  CFT_CHECK(hd == 64 || hd == 128, "attention: head_dim must be 64 or 128");
+  CFT_CHECK(seq % 128 == 0, "attention: seq must be a multiple of 128");
+  CFT_CHECK(hkv > 0 && hq % hkv == 0 && (hq / hkv) % 2 == 0,
+            "attention: query heads per KV head must be even");
+}
+
+namespace {
+template <int HD>
+void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* lse,
+                cudaStream_t st) {
+  const int ld = (H + 2 * KVH) * HD;
+  const int N = B * S;
+  const CUtensorMap m = tmap(qkv, ld, N, ld, 128);
+  FwdArgs a{B, H, KVH, S, ld, static_cast<bf16*>(o), H * HD, lse,
+            1.4426950408889634f / sqrtf(static_cast<float>(HD))};
+  static bool attr = false;
+  if (!attr) {
+    set_smem(attn_fwd_kernel<HD>, FwdSmem<HD>::BYTES);
+    attr = true;
+  }
+  const int grid = (S / 128) * B * KVH * (H / KVH / 2);
+  attn_fwd_kernel<HD><<<grid, 320, std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(m, a);
+  check_launch("attn_fwd_kernel");
+}
+
+template <int HD>
+void bwd_launch(int B, int H, int KVH, int S, const void* qkv, const void* o, const void* dout,
+                const float* lse, float* D, void* dqkv, cudaStream_t st) {
+  const int ld = (H + 2 * KVH) * HD, ldo = H * HD;
+  const int N = B * S;
+  {
+    const long long warps = static_cast<long long>(N) * H;
+    attn_bwd_dot_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
+        static_cast<const bf16*>(o), static_cast<const bf16*>(dout), ldo, N, H, S, HD, D);
+    check_launch("attn_bwd_dot_kernel");
+  }
+  const CUtensorMap m128 = tmap(qkv, ld, N, ld, 128);
+  const CUtensorMap m64 = tmap(qkv, ld, N, ld, 64);
+  const float sc = 1.f / sqrtf(static_cast<float>(HD));
+  BwdArgs a{B, H, KVH, S, ld, ldo, lse, D, static_cast<bf16*>(dqkv), 1.4426950408889634f * sc, sc};
+  static bool attr = false;
+  if (!attr) {
+    set_smem(attn_bwd_dkdv_kernel<HD>, KvSmem<HD>::BYTES);
+    set_smem(attn_bwd_dq_kernel<HD>, QSmem<HD>::BYTES);
+    attr = true;
+  }
+  {
+    const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 64);
+    attn_bwd_dkdv_kernel<HD><<<(S / 128) * B * KVH, 192, std::max(KvSmem<HD>::BYTES, kMinSmem), st>>>(m128, m64, mdo, a);
+    check_launch("attn_bwd_dkdv_kernel");
+  }
+  {
+    const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 128);
+    attn_bwd_dq_kernel<HD><<<(S / 128) * B * H, 192, std::max(QSmem<HD>::BYTES, kMinSmem), st>>>(m128, m64, mdo, a);
+    check_launch("attn_bwd_dq_kernel");
+  }
+}
+
+}  // namespace
+
+struct Context::Impl {
+  float* D = nullptr;  // [B][H][S] rowsum(dO * O) scratch
+  size_t d_elems = 0;
+};
+
+Context::Context() : impl_(std::make_unique<Impl>()) {}
+Context::~Context() {
+  if (impl_ && impl_->D) cudaFree(impl_->D);
+}
+
+void Context::prepare(int batch, int hq, int hkv, int seq, int head_dim) {
+  check_shape(hq, hkv, seq, head_dim);
+  const size_t need = static_cast<size_t>(batch) * hq * seq;
+  if (need > impl_->d_elems) {
+    if (impl_->D) CFT_CUDA(cudaFree(impl_->D));
+    CFT_CUDA(cudaMalloc(&impl_->D, need * sizeof(float)));
+    impl_->d_elems = need;
+  }
+}
+
+void Context::forward(int batch, int hq, int hkv, int seq, int head_dim, const void* qkv, void* o,
+                      float* stats, cudaStream_t stream) {
+  check_shape(hq, hkv, seq, head_dim);
+  if (head_dim == 128) fwd_launch<128>(batch, hq, hkv, seq, qkv, o, stats, stream);
+  else fwd_launch<64>(batch, hq, hkv, seq, qkv, o, stats, stream);
+}
+
+void Context::backward(int batch, int hq, int hkv, int seq, int head_dim, const void* qkv,
+                       const void* o, const void* dout, const float* stats, void* dqkv,
+                       cudaStream_t stream) {
+  check_shape(hq, hkv, seq, head_dim);
+  CFT_CHECK(impl_->D && impl_->d_elems >= static_cast<size_t>(batch) * hq * seq,
+            "attention: prepare() before backward");
+  if (head_dim == 128)
+    bwd_launch<128>(batch, hq, hkv, seq, qkv, o, dout, stats, impl_->D, dqkv, stream);
+  else
+    bwd_launch<64>(batch, hq, hkv, seq, qkv, o, dout, stats, impl_->D, dqkv, stream);
+}
+
+}  // namespace cft::attn
+
+// ---- C ABI (include/chunkft_b200.h) ----
+using namespace cft;
+
+extern "C" int cft_attention_fwd(const void* qkv, int batch, int hq, int hkv, int seq,
+                                 int head_dim, void* o, float* lse, cft_stream_t stream) {
+  return guarded([&] {
+    attn::check_shape(hq, hkv, seq, head_dim);
+    if (batch <= 0) return;
+    auto st = static_cast<cudaStream_t>(stream);
+    if (head_dim == 128) attn::fwd_launch<128>(batch, hq, hkv, seq, qkv, o, lse, st);
+    else attn::fwd_launch<64>(batch, hq, hkv, seq, qkv, o, lse, st);
+  });
+}
+
+extern "C" int cft_attention_bwd(const void* qkv, const void* o, const void* dout,
+                                 const float* lse, int batch, int hq, int hkv, int seq,
+                                 int head_dim, void* dqkv, float* scratch, cft_stream_t stream) {
+  return guarded([&] {
+    attn::check_shape(hq, hkv, seq, head_dim);
+    if (batch <= 0) return;
+    auto st = static_cast<cudaStream_t>(stream);
+    if (head_dim == 128)
+      attn::bwd_launch<128>(batch, hq, hkv, seq, qkv, o, dout, lse, scratch, dqkv, st);
+    else
+      attn::bwd_launch<64>(batch, hq, hkv, seq, qkv, o, dout, lse, scratch, dqkv, st);
+  });
+}

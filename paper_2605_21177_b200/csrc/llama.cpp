@@ -117,19 +117,10 @@ void Engine::llama_alloc() {
   g_lab_ = static_cast<int32_t*>(A(N, 4));
   g_loss_ = static_cast<double*>(A(1, 8));
   CFT_CUDA(cudaStreamCreateWithFlags(&cap_, cudaStreamNonBlocking));
-  // everything a capture may not do (allocation, first-use tables, cuDNN plan builds and
-  // workspace) happens here, before any step
+  // everything a capture may not do (allocation, first-use tables) happens here, before any
+  // step
   attn_ = std::make_unique<attn::Context>();
   attn_->prepare(cfg_.batch_rows, s.heads, s.kv_heads, s.seq, s.head_dim);
-  {  // pick the fastest cuDNN SDPA plans on zeroed stand-in activations
-    LlamaLayerBufs& z = lb_[0];
-    CFT_CUDA(cudaMemset(z.qkv, 0, N * qkv * 2));
-    CFT_CUDA(cudaMemset(z.o, 0, N * int64_t(s.heads) * s.head_dim * 2));
-    CFT_CUDA(cudaMemset(l_do_, 0, N * int64_t(s.heads) * s.head_dim * 2));
-    attn_->autotune(cfg_.batch_rows, s.heads, s.kv_heads, s.seq, s.head_dim, z.qkv, z.o, z.lse,
-                    l_do_, l_dqkv_, nullptr);
-    CFT_CUDA(cudaDeviceSynchronize());
-  }
   llama::rope_prepare(s.seq, s.head_dim, static_cast<float>(s.rope_theta));
 }
 

@@ -153,6 +153,30 @@ def softmax_ce(y: torch.Tensor, labels: torch.Tensor, dy: torch.Tensor | None = 
     return loss, dy, bad
 
 
+def attention_fwd(qkv: torch.Tensor, batch: int, hq: int, hkv: int, seq: int, head_dim: int,
+                  stream=None):
+    """Causal GQA flash attention over the fused qkv buffer [batch*seq, (hq+2hkv)*hd] (bf16).
+    Returns (o [batch*seq, hq*hd] bf16, lse [batch, hq, seq] fp32 log2-sum-exp)."""
+    _contig(qkv)
+    o = torch.empty(batch * seq, hq * head_dim, dtype=qkv.dtype, device=qkv.device)
+    lse = torch.empty(batch, hq, seq, dtype=torch.float32, device=qkv.device)
+    N.check(N.lib.cft_attention_fwd(qkv.data_ptr(), batch, hq, hkv, seq, head_dim, o.data_ptr(),
+                                    lse.data_ptr(), _stream(stream)), "attention_fwd")
+    return o, lse
+
+
+def attention_bwd(qkv, o, dout, lse, batch: int, hq: int, hkv: int, seq: int, head_dim: int,
+                  stream=None):
+    """dqkv (dQ | dK | dV in the qkv layout) of the causal GQA attention."""
+    _contig(qkv, o, dout, lse)
+    dqkv = torch.empty_like(qkv)
+    scratch = torch.empty(batch * hq * seq, dtype=torch.float32, device=qkv.device)
+    N.check(N.lib.cft_attention_bwd(qkv.data_ptr(), o.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                                    batch, hq, hkv, seq, head_dim, dqkv.data_ptr(),
+                                    scratch.data_ptr(), _stream(stream)), "attention_bwd")
+    return dqkv
+
+
 def grad_stats(grad: torch.Tensor, grad_scale: float = 1.0, stats=None, stream=None):
     """Returns a float64 device tensor [sumsq, nonfinite_count(bits), first_bad(bits)]."""
     if stats is None:

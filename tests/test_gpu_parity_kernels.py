@@ -32,6 +32,11 @@ def libs(cuda):
     R.set_backend(True)
 
 
+@pytest.fixture(autouse=True)
+def _clear_status(libs):
+    libs[0].cft_last_status()  # reading resets the thread's sticky status
+
+
 def d(a):
     return a.ctypes.data_as(D)
 
