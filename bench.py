@@ -831,6 +831,13 @@ def run_llama(args, rank, world, local_rank):
                               "note": "tokens x window GFLOP/token / device time (fwd + suffix dgrad + "
                                       "sliced dW GEMMs and causal attention, 2.5x fwd backward); "
                               "the engine's own per-launch work counters give the GEMM part"},
+            "attention": {"kernel": "attn_fwd_kernel / attn_bwd_dkdv_kernel + attn_bwd_dq_kernel "
+                                    "(own tcgen05 causal GQA flash attention)",
+                          "fwd_ms_per_step": phases["attn_fwd"][0] / S,
+                          "bwd_ms_per_step": phases["attn_bwd"][0] / S,
+                          "fwd_tflops_in_step": phases["attn_fwd"][2] / max(phases["attn_fwd"][0], 1e-9) / 1e9,
+                          "bwd_tflops_in_step": phases["attn_bwd"][2] / max(phases["attn_bwd"][0], 1e-9) / 1e9,
+                          "flops_note": "causal algorithmic: fwd 2*S^2*hd per (sequence, head), bwd 2.5x"},
             "sliced_dw": {"tflops_in_step": wg_tflops, "frac_of_measured_peak": wg_tflops / peaks["bf16"],
                           "frac_of_measured_sustained": wg_tflops / peaks["bf16_sustained"],
                           "frac_of_spec_2250": wg_tflops / 2250.0,

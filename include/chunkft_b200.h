@@ -467,12 +467,13 @@ int cft_engine_phase_ms(cft_engine* e, float* ms4);
  * category (0 inputs, 1 forward GEMM, 2 other forward, 3 loss, 4 slice wgrad, 5 dgrad,
  * 6 other backward, 7 gradient statistics, 8 AdamW/SGD update, 9 engine stream waiting for
  * the active chunk's state upload, 10 / 11 state H2D / D2H time on the copy streams, 12 a
- * replayed forward+backward graph).  enable: 0 off, 1 per-category marks (the Llama engine
+ * replayed forward+backward graph, 13 / 14 attention forward / backward).  enable: 0 off, 1 per-category marks (the Llama engine
  * then launches eagerly), 2 coarse marks only (CUDA graphs stay on).
  * max_marks bounds the preallocated event pool.  phase_totals synchronises, returns summed ms,
- * launch counts and algorithmic work (GEMM FLOPs for 1/4/5; bytes for 7/8) per category
+ * launch counts and algorithmic work (GEMM FLOPs for 1/4/5, causal attention FLOPs for
+ * 13/14; bytes for 7/8) per category
  * (CFT_NUM_PHASES entries each; any pointer may be NULL) and clears the marks. */
-#define CFT_NUM_PHASES 13
+#define CFT_NUM_PHASES 15
 int cft_engine_profile(cft_engine* e, int enable, int64_t max_marks);
 int cft_engine_phase_totals(cft_engine* e, float* ms, int64_t* counts, double* work);
 /* Host-side submission time per profiler category (CFT_NUM_PHASES entries, ms) accumulated

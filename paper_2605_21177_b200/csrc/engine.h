@@ -142,7 +142,7 @@ class Engine {
   // kRotWait is non-zero)
   // kGraph: a replayed forward+backward graph (coarse profiling keeps graphs on)
   enum Phase { kInputs = 0, kFwdGemm, kFwdOther, kLoss, kWgrad, kDgrad, kBwdOther, kStats,
-               kUpdate, kRotWait, kH2D, kD2H, kGraph, kNumPhases };
+               kUpdate, kRotWait, kH2D, kD2H, kGraph, kAttnFwd, kAttnBwd, kNumPhases };
   // mode 0 off, 1 per-kernel-category marks (eager launches), 2 coarse marks (graphs stay on)
   void profile(int mode, int64_t max_marks);
   // syncs; per phase: summed ms, launch count, algorithmic work (GEMM FLOPs; bytes for the

@@ -291,10 +291,14 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
         S.head_dim, Q + KV, st);
     if (!roped) tc::linear_fwd(z.a, N, d, P(id(l, 1)), QKV, z.qkv, st);
     pe();
-    pb(kFwdOther);
-    if (!roped)
+    if (!roped) {
+      pb(kFwdOther);
       llama::rope(static_cast<bf16*>(z.qkv), N, S.seq, S.heads + S.kv_heads, S.head_dim, ld,
                   (float)S.rope_theta, false, st);
+      pe();
+    }
+    pb(kAttnFwd);  // causal: two half-masked S x S x hd matmuls per (sequence, head)
+    add_work(kAttnFwd, 2.0 * S.seq * double(S.seq) * S.head_dim * S.heads * B);
     attn_->forward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, z.lse, st);
     pe();
     pb(kFwdGemm);
@@ -417,8 +421,11 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     gemm_work(kDgrad, N, Q, d, 2.0 * N * Q, 0);
     tc::linear_dgrad(l_gh_, N, d, P(id(l, 4)), Q, l_do_, 0, st);
     pe();
-    pb(kBwdOther);
+    pb(kAttnBwd);  // algorithmic 2.5x the forward (dV, dP, dS.K, dS^T.Q + the S recompute)
+    add_work(kAttnBwd, 5.0 * S.seq * double(S.seq) * S.head_dim * S.heads * B);
     attn_->backward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, l_do_, z.lse, l_dqkv_, st);
+    pe();
+    pb(kBwdOther);
     // q and k heads are adjacent in the fused row: one inverse-rotation launch covers both
     llama::rope(static_cast<bf16*>(l_dqkv_), N, S.seq, S.heads + S.kv_heads, S.head_dim, ld,
                 (float)S.rope_theta, true, st);

@@ -497,7 +497,7 @@ class ChunkEngine:
         return out
 
     PHASES = ("inputs", "fwd_gemm", "fwd_other", "loss", "wgrad", "dgrad", "bwd_other", "stats",
-              "update", "rot_wait", "h2d", "d2h", "graph")
+              "update", "rot_wait", "h2d", "d2h", "graph", "attn_fwd", "attn_bwd")
 
     def profile(self, enable=True, max_marks: int = 1 << 14):
         """enable: False/0 off, True/1 per-kernel-category marks (eager launches), 2 coarse
