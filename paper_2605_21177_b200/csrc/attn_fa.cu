@@ -4,7 +4,7 @@
 // the fused qkv projection buffer [token][q heads | k heads | v heads] (row pitch
 // (Hq + 2 Hkv) * hd), read in place by TMA -- no transposes, no library.
 //
-// Tiles: 128 query rows x 128 (forward) / 64 (backward) key rows; head_dim 64 or 128.  Every
+// Tiles: 128 rows x 64-row blocks of the other side; head_dim 64 or 128.  Every
 // operand is staged by TMA in the 128-byte-swizzled K-major layout, and the same smem bytes
 // serve as the MN-major operand where a GEMM needs the transpose (V in O += P.V, K in
 // dQ += dS.K, Q / dO in dK / dV): rows of a swizzled tile are the K dimension there, 16 rows
@@ -12,18 +12,20 @@
 // blocks.  Accumulators (S, dP, O, dQ, dK, dV) live in TMEM; one elected thread issues
 // tcgen05.mma; softmax / gradient warps own one TMEM lane = one row each.
 //
-//  forward   one CTA = two query heads of one GQA group x one 128-row query tile: the heads
+//  forward   one CTA = two query heads of one GQA group x one 128-row query tile (64-row key
+//            blocks in a 3-deep TMA ring): the heads
 //            share every K / V tile, and their softmax warp groups ping-pong with the tensor
 //            pipe (head A's softmax overlaps head B's MMAs).  Online softmax in the exp2
 //            domain; the O accumulator (TMEM) is rescaled only when a row's running max grows
 //            by more than 2^8 (the final 1/l is exact for any reference max).  Writes O (bf16)
 //            and the row log2-sum-exp (fp32, consumed only by the backward here).
-//  backward  D = rowsum(dO * O); then two deterministic kernels, no atomics:
+//  backward  two deterministic kernels, no atomics:
+//            dQ:    one CTA = one 128-row query tile of one head, looping over 64-row key
+//                   blocks; S / dP double-buffered, dQ accumulated in TMEM; it also forms
+//                   D = rowsum(dO * O) of its rows from the staged tiles (no separate pass).
 //            dK/dV: one CTA = one 128-row key tile of one KV head, looping over all the
 //                   group's query heads and 64-row query blocks, so the GQA head reduction
 //                   of dK / dV happens in TMEM; S^T / dP^T double-buffered in TMEM.
-//            dQ:    one CTA = one 128-row query tile of one head, looping over 64-row key
-//                   blocks; S / dP double-buffered, dQ accumulated in TMEM.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -125,6 +127,24 @@ __device__ __forceinline__ void st_row32(bf16* p, const uint32_t (&r)[32], float
   }
 }
 
+
+// 2^x on the FMA pipe (degree-3 minimax of 2^f on [-1/2, 1/2], rel. error 7.5e-5 -- far below
+// the bf16 rounding of P): the MUFU unit (16 ex2 / clock / SM) would otherwise bound the
+// softmax; a quarter of the exponentials go this way.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: rounds x to an integer in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.0551716685f, f, 0.2426111251f), f, 0.6932609677f), f,
+                       0.9999280572f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+template <int E>
+__device__ __forceinline__ float ex2_mix(float x) {
+  if constexpr ((E & 3) == 3) return ex2_poly(x);
+  else return ex2(x);
+}
+
 struct FwdArgs {
   int B, H, KVH, S, ld;  // ld = qkv row pitch (elements)
   bf16* o;
@@ -134,33 +154,36 @@ struct FwdArgs {
 };
 
 // ------------------------------------------------------------------------------------------
-// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax of head A, 6-9 of B
+// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax of head A, 6-9 of B.
+// Key / value blocks of 64 rows in a 3-deep ring; S of each head 128 x 64 in TMEM.
 template <int HD>
 struct FwdSmem {
-  static constexpr uint32_t TILE = 128 * HD * 2;
-  static constexpr uint32_t PT = 128 * 128 * 2;
-  static constexpr uint32_t Q0 = 0, K = 2 * TILE, V0 = 3 * TILE, P0 = 5 * TILE,
-                            BAR = 5 * TILE + 2 * PT;
+  static constexpr int NS = 3;
+  static constexpr uint32_t QT = 128 * HD * 2;  // query tile
+  static constexpr uint32_t KB = 64 * HD * 2;   // key or value block
+  static constexpr uint32_t PB = 128 * 64 * 2;  // P block (bf16)
+  static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NS * KB, P0 = V0 + NS * KB,
+                            BAR = P0 + 2 * PB;
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
 template <int HD>
 __global__ void __launch_bounds__(320, 1)
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, const FwdArgs a) {
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv,
+                    const FwdArgs a) {
   using L = FwdSmem<HD>;
-  constexpr int NB = HD / 64;
+  constexpr int NB = HD / 64, NS = L::NS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* qfull = bar;
-  uint64_t* kfull = bar + 1;
-  uint64_t* kempty = bar + 2;
-  uint64_t* vfull = bar + 3;   // [2]
-  uint64_t* vempty = bar + 5;  // [2]
-  uint64_t* sfull = bar + 7;   // [2] per head
-  uint64_t* pfull = bar + 9;   // [2]
-  uint64_t* ofull = bar + 11;  // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 13);
+  uint64_t* kfull = bar + 1;            // [NS]
+  uint64_t* vfull = bar + 1 + NS;       // [NS]
+  uint64_t* kvempty = bar + 1 + 2 * NS; // [NS]
+  uint64_t* sfull = bar + 1 + 3 * NS;   // [2] per head
+  uint64_t* pfull = sfull + 2;          // [2]
+  uint64_t* ofull = sfull + 4;          // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfull + 6);
 
   const int nq = a.S / 128, G = a.H / a.KVH, G2 = G / 2;
   const int per_i = a.B * a.KVH * G2;
@@ -168,19 +191,21 @@ __global__ void __launch_bounds__(320, 1)
   const int rest = static_cast<int>(blockIdx.x) % per_i;
   const int b = rest / (a.KVH * G2), kvh = (rest / G2) % a.KVH, pr = rest % G2;
   const int h0 = kvh * G + 2 * pr;
-  const int n = i + 1;
+  const int nb = 2 * i + 2;  // 64-row key blocks up to the diagonal
   const int qrow = b * a.S + i * 128, krow = b * a.S;
   const int kcol = a.H * HD + kvh * HD, vcol = (a.H + a.KVH) * HD + kvh * HD;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (threadIdx.x == 0) {
-    tma_prefetch(&tm);
+    tma_prefetch(&tmq);
+    tma_prefetch(&tmkv);
     mbar_init(qfull, 1);
-    mbar_init(kfull, 1);
-    mbar_init(kempty, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&kfull[s], 1);
+      mbar_init(&vfull[s], 1);
+      mbar_init(&kvempty[s], 1);
+    }
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&vfull[t], 1);
-      mbar_init(&vempty[t], 1);
       mbar_init(&sfull[t], 1);
       mbar_init(&pfull[t], 128);
       mbar_init(&ofull[t], 1);
@@ -192,73 +217,71 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  // TMEM: S_A [0, 64), S_B [64, 128), O_A [128, 128 + HD), O_B [128 + HD, 128 + 2 HD)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(qfull, 2 * L::TILE);
+      mbar_expect_tx(qfull, 2 * L::QT);
       for (int t = 0; t < 2; ++t)
         for (int kb = 0; kb < NB; ++kb)
-          tma_load_2d(sm + L::Q0 + t * L::TILE + kb * kBlk128, &tm, qfull,
-                      (h0 + t) * HD + kb * 64, qrow);
-      for (int j = 0; j < n; ++j) {
-        mbar_wait(kempty, (j & 1) ^ 1);
-        mbar_expect_tx(kfull, L::TILE);
+          tma_load_2d(sm + L::Q0 + t * L::QT + kb * kBlk128, &tmq, qfull, (h0 + t) * HD + kb * 64,
+                      qrow);
+      for (int j = 0; j < nb; ++j) {
+        const int s = j % NS, u = j / NS;
+        mbar_wait(&kvempty[s], (u & 1) ^ 1);
+        mbar_expect_tx(&kfull[s], L::KB);
         for (int kb = 0; kb < NB; ++kb)
-          tma_load_2d(sm + L::K + kb * kBlk128, &tm, kfull, kcol + kb * 64, krow + j * 128);
-        const int vb = j & 1;
-        mbar_wait(&vempty[vb], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&vfull[vb], L::TILE);
+          tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tmkv, &kfull[s], kcol + kb * 64,
+                      krow + j * 64);
+        mbar_expect_tx(&vfull[s], L::KB);
         for (int kb = 0; kb < NB; ++kb)
-          tma_load_2d(sm + L::V0 + vb * L::TILE + kb * kBlk128, &tm, &vfull[vb], vcol + kb * 64,
-                      krow + j * 128);
+          tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tmkv, &vfull[s], vcol + kb * 64,
+                      krow + j * 64);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t ID_S = idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_O = idesc_bf16_f32(128, HD, false, true);
-      auto issue_s = [&](int t) {
-        const uint8_t* q = sm + L::Q0 + t * L::TILE;
+      auto issue_s = [&](int t, int s) {
+        const uint8_t* q = sm + L::Q0 + t * L::QT;
+        const uint8_t* k = sm + L::K0 + s * L::KB;
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tbase + t * 128, desc_k(q, k, kBlk128), desc_k(sm + L::K, k, kBlk128), ID_S,
-                    k > 0);
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_bf16(tbase + t * 64, desc_k(q, kk, kBlk128), desc_k(k, kk, kBlk64), ID_S, kk > 0);
         umma_commit(&sfull[t]);
       };
-      auto issue_pv = [&](int t, int vb, int j) {
-        const uint8_t* p = sm + L::P0 + t * L::PT;
-        const uint8_t* v = sm + L::V0 + vb * L::TILE;
+      auto issue_pv = [&](int t, int s, int j) {
+        const uint8_t* p = sm + L::P0 + t * L::PB;
+        const uint8_t* v = sm + L::V0 + s * L::KB;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          umma_bf16(tbase + 256 + t * HD, desc_k(p, k, kBlk128), desc_mn(v, k, kBlk128), ID_O,
-                    (j > 0 || k > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tbase + 128 + t * HD, desc_k(p, kk, kBlk128), desc_mn(v, kk, kBlk64), ID_O,
+                    (j > 0 || kk > 0) ? 1u : 0u);
         umma_commit(&ofull[t]);
       };
       mbar_wait(qfull, 0);
-      mbar_wait(kfull, 0);
+      mbar_wait(&kfull[0], 0);
       tc_fence_after();
-      issue_s(0);
-      issue_s(1);
-      umma_commit(kempty);
-      for (int j = 0; j < n; ++j) {
-        const int vb = j & 1;
-        mbar_wait(&vfull[vb], (j >> 1) & 1);
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nb; ++j) {
+        const int s = j % NS, u = j / NS;
+        const int s1 = (j + 1) % NS, u1 = (j + 1) / NS;
+        mbar_wait(&vfull[s], u & 1);
         mbar_wait(&pfull[0], j & 1);
         tc_fence_after();
-        issue_pv(0, vb, j);
-        if (j + 1 < n) {
-          mbar_wait(kfull, (j + 1) & 1);
+        issue_pv(0, s, j);
+        if (j + 1 < nb) {
+          mbar_wait(&kfull[s1], u1 & 1);
           tc_fence_after();
-          issue_s(0);
+          issue_s(0, s1);
         }
         mbar_wait(&pfull[1], j & 1);
         tc_fence_after();
-        issue_pv(1, vb, j);
-        umma_commit(&vempty[vb]);
-        if (j + 1 < n) {
-          issue_s(1);
-          umma_commit(kempty);
-        }
+        issue_pv(1, s, j);
+        umma_commit(&kvempty[s]);
+        if (j + 1 < nb) issue_s(1, s1);
       }
     }
   } else {
@@ -266,23 +289,28 @@ __global__ void __launch_bounds__(320, 1)
     const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tS = tbase + lo + t * 128, tO = tbase + lo + 256 + t * HD;
-    uint8_t* sP = sm + L::P0 + t * L::PT;
+    const uint32_t tS = tbase + lo + t * 64, tO = tbase + lo + 128 + t * HD;
+    uint8_t* sP = sm + L::P0 + t * L::PB;
     const float c = a.scale_log2;
+    const int qpos = i * 128 + r;
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < n; ++j) {
+    for (int j = 0; j < nb; ++j) {
       mbar_wait(&sfull[t], j & 1);
       tc_fence_after();
-      const bool diag = j == i;
+      uint32_t v[64];
+      tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(v));
+      tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      tmem_wait_ld();
+      const bool diag = j * 64 + 63 > i * 128;  // block reaches past this tile's first row
+      const int lim = qpos - j * 64;             // columns e <= lim are visible
       float mx = -INFINITY;
+      if (!diag) {
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(tS + cc * 32, v);
-        tmem_wait_ld();
+        for (int e = 0; e < 64; ++e) mx = fmaxf(mx, f32(v[e]));
+      } else {
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (!diag || cc * 32 + e <= r) mx = fmaxf(mx, f32(v[e]));
+        for (int e = 0; e < 64; ++e)
+          if (e <= lim) mx = fmaxf(mx, f32(v[e]));
       }
       const float m_new = fmaxf(m, mx * c);
       if (j > 0) {  // PV of the previous block done: P buffer and O free
@@ -297,44 +325,267 @@ __global__ void __launch_bounds__(320, 1)
         m = m_new;
 #pragma unroll
         for (int cc = 0; cc < HD / 32; ++cc) {
-          uint32_t v[32];
-          tmem_ld32(tO + cc * 32, v);
+          uint32_t o[32];
+          tmem_ld32(tO + cc * 32, o);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(f32(v[e]) * alpha);
-          tmem_st32(tO + cc * 32, v);
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(f32(o[e]) * alpha);
+          tmem_st32(tO + cc * 32, o);
         }
         tmem_wait_st();
       }
+      float p[64];
+      const float nm = -m;
+      if (!diag) {
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(tS + cc * 32, v);
-        tmem_wait_ld();
-        float p[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          p[e] = (diag && cc * 32 + e > r) ? 0.f : ex2(fmaf(f32(v[e]), c, -m));
-          l += p[e];
+        for (int e = 0; e < 64; e += 4) {
+          p[e] = ex2_mix<0>(fmaf(f32(v[e]), c, nm));
+          p[e + 1] = ex2_mix<1>(fmaf(f32(v[e + 1]), c, nm));
+          p[e + 2] = ex2_mix<2>(fmaf(f32(v[e + 2]), c, nm));
+          p[e + 3] = ex2_mix<3>(fmaf(f32(v[e + 3]), c, nm));
         }
-        st_swz32(sP + (cc >> 1) * kBlk128, r, (cc & 1) * 4, p);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) p[e] = e <= lim ? ex2(fmaf(f32(v[e]), c, nm)) : 0.f;
       }
+#pragma unroll
+      for (int e = 0; e < 64; ++e) l += p[e];
+      st_swz32(sP, r, 0, p);
+      st_swz32(sP, r, 4, p + 32);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&pfull[t]);
     }
-    mbar_wait(&ofull[t], (n - 1) & 1);
+    mbar_wait(&ofull[t], (nb - 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l;
     bf16* out = a.o + static_cast<long long>(qrow + r) * a.ldo + (h0 + t) * HD;
 #pragma unroll
     for (int cc = 0; cc < HD / 32; ++cc) {
-      uint32_t v[32];
-      tmem_ld32(tO + cc * 32, v);
+      uint32_t o[32];
+      tmem_ld32(tO + cc * 32, o);
       tmem_wait_ld();
-      st_row32(out + cc * 32, v, inv);
+      st_row32(out + cc * 32, o, inv);
     }
-    a.lse[(static_cast<long long>(b) * a.H + h0 + t) * a.S + i * 128 + r] = m + __log2f(l);
+    a.lse[(static_cast<long long>(b) * a.H + h0 + t) * a.S + qpos] = m + __log2f(l);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tbase);
+}
+
+struct BwdArgs {
+  int B, H, KVH, S, ld;  // qkv / dqkv row pitch
+  int ldo;               // o / dO row pitch (H * hd)
+  const float* lse;      // [B][H][S] log2-sum-exp from the forward
+  float* D;              // [B][H][S] rowsum(dO * O): written by the dQ kernel, read by dK/dV
+  bf16* dqkv;
+  float scale_log2, scale;
+};
+
+// ------------------------------------------------------------------------------------------
+// dQ (runs first; also forms D = rowsum(dO * O) of its rows): warp 0 TMA, warp 1 MMA,
+// warps 2-5 one query row each.  Key / value blocks of 64 rows in a 4-deep ring; S and dP
+// double-buffered in TMEM; the O tile is staged once in the dS buffers before the loop.
+template <int HD>
+struct QSmem {
+  static constexpr int NS = 4;
+  static constexpr uint32_t TILE = 128 * HD * 2;  // Q / dO / O tile (128 rows)
+  static constexpr uint32_t KB = 64 * HD * 2;     // K or V block (64 rows)
+  static constexpr uint32_t SB = 128 * 64 * 2;    // dS block (128 q x 64 kv)
+  static constexpr uint32_t Q = 0, DO = TILE, K0 = 2 * TILE, V0 = K0 + NS * KB, DS0 = V0 + NS * KB,
+                            BAR = DS0 + 2 * SB;
+  static_assert(TILE <= 2 * SB, "the O tile is staged in the dS buffers");
+  static constexpr size_t BYTES = 1024 + BAR + 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm128,
+                       const __grid_constant__ CUtensorMap tm64,
+                       const __grid_constant__ CUtensorMap tmdo,
+                       const __grid_constant__ CUtensorMap tmo, const BwdArgs a) {
+  using L = QSmem<HD>;
+  constexpr int NB = HD / 64, NS = L::NS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* qfull = bar;
+  uint64_t* kvfull = bar + 1;            // [NS]
+  uint64_t* kvempty = bar + 1 + NS;      // [NS] K / V block consumed
+  uint64_t* tfull = bar + 1 + 2 * NS;    // [2] S, dP in TMEM
+  uint64_t* pfull = tfull + 2;           // [2] dS written
+  uint64_t* pfree = tfull + 4;           // [2] dS consumed
+  uint64_t* done = tfull + 6;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 7);
+
+  const int nq = a.S / 128;
+  const int per_i = a.B * a.H;
+  const int i = nq - 1 - static_cast<int>(blockIdx.x) / per_i;  // longest rows first
+  const int rest = static_cast<int>(blockIdx.x) % per_i;
+  const int b = rest / a.H, h = rest % a.H;
+  const int kvh = h / (a.H / a.KVH);
+  const int n = 2 * i + 2;  // 64-row key blocks up to the diagonal
+  const int qrow = b * a.S + i * 128;
+  const int kcol = a.H * HD + kvh * HD, vcol = (a.H + a.KVH) * HD + kvh * HD;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm128);
+    tma_prefetch(&tm64);
+    tma_prefetch(&tmdo);
+    tma_prefetch(&tmo);
+    mbar_init(qfull, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&kvfull[s], 1);
+      mbar_init(&kvempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&pfull[s], 128);
+      mbar_init(&pfree[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  // TMEM: dQ [0, HD), stage s: S [HD + 128 s, +64), dP [+64, +128)
+  auto tst = [&](int s) { return tbase + HD + 128 * s; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(qfull, 3 * L::TILE);
+      for (int kb = 0; kb < NB; ++kb) {
+        tma_load_2d(sm + L::Q + kb * kBlk128, &tm128, qfull, h * HD + kb * 64, qrow);
+        tma_load_2d(sm + L::DO + kb * kBlk128, &tmdo, qfull, h * HD + kb * 64, qrow);
+        tma_load_2d(sm + L::DS0 + kb * kBlk128, &tmo, qfull, h * HD + kb * 64, qrow);
+      }
+      for (int jj = 0; jj < n; ++jj) {
+        const int s = jj % NS, u = jj / NS;
+        const int kr = b * a.S + jj * 64;
+        mbar_wait(&kvempty[s], (u & 1) ^ 1);
+        mbar_expect_tx(&kvfull[s], 2 * L::KB);
+        for (int kb = 0; kb < NB; ++kb) {
+          tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], kcol + kb * 64, kr);
+          tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], vcol + kb * 64, kr);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
+      constexpr uint32_t ID_Q = idesc_bf16_f32(128, HD, false, true);
+      auto issue_s = [&](int jj) {
+        const int s = jj % NS, u = jj / NS, ts = jj & 1;
+        mbar_wait(&kvfull[s], u & 1);
+        tc_fence_after();
+        const uint8_t* k = sm + L::K0 + s * L::KB;
+        const uint8_t* v = sm + L::V0 + s * L::KB;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          umma_bf16(tst(ts), desc_k(sm + L::Q, kk, kBlk128), desc_k(k, kk, kBlk64), ID_S, kk > 0);
+          umma_bf16(tst(ts) + 64, desc_k(sm + L::DO, kk, kBlk128), desc_k(v, kk, kBlk64), ID_S,
+                    kk > 0);
+        }
+        umma_commit(&tfull[ts]);
+      };
+      mbar_wait(qfull, 0);
+      issue_s(0);
+      if (n > 1) issue_s(1);
+      for (int jj = 0; jj < n; ++jj) {
+        const int s = jj % NS, ts = jj & 1, v = jj >> 1;
+        mbar_wait(&pfull[ts], v & 1);
+        tc_fence_after();
+        const uint8_t* k = sm + L::K0 + s * L::KB;
+        const uint8_t* ds = sm + L::DS0 + ts * L::SB;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tbase, desc_k(ds, kk, kBlk128), desc_mn(k, kk, kBlk64), ID_Q,
+                    (jj > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&kvempty[s]);
+        umma_commit(&pfree[ts]);
+        if (jj + 2 < n) issue_s(jj + 2);
+      }
+      umma_commit(done);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
+    const int qi = i * 128 + r;
+    const long long st = (static_cast<long long>(b) * a.H + h) * a.S + qi;
+    const float lse = a.lse[st];
+    const float c = a.scale_log2;
+    // D of this row from the staged dO and O tiles (own row only: the dS writes below reuse
+    // the O staging bytes of this same row)
+    mbar_wait(qfull, 0);
+    float dd = 0.f;
+#pragma unroll
+    for (int kb = 0; kb < NB; ++kb) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t off = kb * kBlk128 + r * 128 + ((q ^ (r & 7)) << 4);
+        const uint4 x = *reinterpret_cast<const uint4*>(sm + L::DO + off);
+        const uint4 y = *reinterpret_cast<const uint4*>(sm + L::DS0 + off);
+        const __nv_bfloat162* xa = reinterpret_cast<const __nv_bfloat162*>(&x);
+        const __nv_bfloat162* ya = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 p = __bfloat1622float2(xa[e]), o = __bfloat1622float2(ya[e]);
+          dd = fmaf(p.x, o.x, fmaf(p.y, o.y, dd));
+        }
+      }
+    }
+    a.D[st] = dd;
+    for (int jj = 0; jj < n; ++jj) {
+      const int ts = jj & 1, v = jj >> 1;
+      mbar_wait(&tfull[ts], v & 1);
+      if (jj >= 2) mbar_wait(&pfree[ts], (v & 1) ^ 1);  // dS stage free
+      tc_fence_after();
+      uint8_t* ds = sm + L::DS0 + ts * L::SB;
+      uint32_t vs[64], vp[64];
+      tmem_ld32(lo + tst(ts), *reinterpret_cast<uint32_t(*)[32]>(vs));
+      tmem_ld32(lo + tst(ts) + 32, *reinterpret_cast<uint32_t(*)[32]>(vs + 32));
+      tmem_ld32(lo + tst(ts) + 64, *reinterpret_cast<uint32_t(*)[32]>(vp));
+      tmem_ld32(lo + tst(ts) + 96, *reinterpret_cast<uint32_t(*)[32]>(vp + 32));
+      tmem_wait_ld();
+      const bool diag = jj * 64 + 63 > i * 128;
+      const int lim = qi - jj * 64;
+      float dv[64];
+      if (!diag) {
+#pragma unroll
+        for (int e = 0; e < 64; e += 4) {
+          dv[e] = ex2_mix<0>(fmaf(f32(vs[e]), c, -lse)) * (f32(vp[e]) - dd);
+          dv[e + 1] = ex2_mix<1>(fmaf(f32(vs[e + 1]), c, -lse)) * (f32(vp[e + 1]) - dd);
+          dv[e + 2] = ex2_mix<2>(fmaf(f32(vs[e + 2]), c, -lse)) * (f32(vp[e + 2]) - dd);
+          dv[e + 3] = ex2_mix<3>(fmaf(f32(vs[e + 3]), c, -lse)) * (f32(vp[e + 3]) - dd);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 64; ++e)
+          dv[e] = e <= lim ? ex2(fmaf(f32(vs[e]), c, -lse)) * (f32(vp[e]) - dd) : 0.f;
+      }
+      st_swz32(ds, r, 0, dv);
+      st_swz32(ds, r, 4, dv + 32);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&pfull[ts]);
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD;
+#pragma unroll
+    for (int cc = 0; cc < HD / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(tbase + lo + cc * 32, o);
+      tmem_wait_ld();
+      st_row32(drow + cc * 32, o, a.scale);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -343,45 +594,18 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ------------------------------------------------------------------------------------------
-// backward preprocessing: D[b][h][s] = sum_d dO * O (fp32), one warp per (token, head)
-__global__ void attn_bwd_dot_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout,
-                                    int ldo, int N, int H, int S, int HD, float* __restrict__ D) {
-  const long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  if (w >= static_cast<long long>(N) * H) return;
-  const int row = static_cast<int>(w / H), h = static_cast<int>(w % H);
-  const bf16* po = o + static_cast<long long>(row) * ldo + h * HD;
-  const bf16* pd = dout + static_cast<long long>(row) * ldo + h * HD;
-  float acc = 0.f;
-  for (int e = lane * 2; e < HD; e += 64) {
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(po + e));
-    const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(pd + e));
-    acc = fmaf(a.x, g.x, fmaf(a.y, g.y, acc));
-  }
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-  if (lane == 0) D[(static_cast<long long>(row / S) * H + h) * S + row % S] = acc;
-}
-
-struct BwdArgs {
-  int B, H, KVH, S, ld;  // qkv / dqkv row pitch
-  int ldo;               // dO row pitch (H * hd)
-  const float* lse;      // [B][H][S] log2-sum-exp from the forward
-  const float* D;        // [B][H][S]
-  bf16* dqkv;
-  float scale_log2, scale;
-};
-
-// ------------------------------------------------------------------------------------------
-// dK / dV: warp 0 TMA, warp 1 MMA, warps 2-5 one key row each
+// dK / dV: warp 0 TMA, warp 1 MMA, warps 2-5 one key row each.  Query / dO blocks of 64 rows
+// (+ their lse / D) in a 3-deep ring; S^T, dP^T double-buffered in TMEM; P^T / dS^T in two
+// smem stages.
 template <int HD>
 struct KvSmem {
+  static constexpr int NS = 3;
   static constexpr uint32_t TILE = 128 * HD * 2;  // K or V tile (128 rows)
   static constexpr uint32_t QB = 64 * HD * 2;     // Q or dO block (64 rows)
   static constexpr uint32_t PB = 128 * 64 * 2;    // P^T or dS^T block (128 kv x 64 q)
-  static constexpr uint32_t K = 0, V = TILE, Q0 = 2 * TILE, DO0 = Q0 + 2 * QB,
-                            P0 = DO0 + 2 * QB, DS0 = P0 + 2 * PB, LSE0 = DS0 + 2 * PB,
-                            D0 = LSE0 + 2 * 256, BAR = D0 + 2 * 256;
+  static constexpr uint32_t K = 0, V = TILE, Q0 = 2 * TILE, DO0 = Q0 + NS * QB,
+                            P0 = DO0 + NS * QB, DS0 = P0 + 2 * PB, LSE0 = DS0 + 2 * PB,
+                            D0 = LSE0 + NS * 256, BAR = D0 + NS * 256;
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
@@ -391,24 +615,24 @@ __global__ void __launch_bounds__(192, 1)
                          const __grid_constant__ CUtensorMap tm64,
                          const __grid_constant__ CUtensorMap tmdo, const BwdArgs a) {
   using L = KvSmem<HD>;
-  constexpr int NB = HD / 64;
+  constexpr int NB = HD / 64, NS = L::NS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* kvfull = bar;
-  uint64_t* qfull = bar + 1;   // [2] Q, dO, lse, D of a query block
-  uint64_t* sfree = bar + 3;   // [2] smem stage (Q, dO, P^T, dS^T) consumed by the MMAs
-  uint64_t* tfull = bar + 5;   // [2] S^T, dP^T in TMEM
-  uint64_t* pfull = bar + 7;   // [2] P^T, dS^T written
-  uint64_t* done = bar + 9;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 10);
+  uint64_t* qfull = bar + 1;             // [NS] Q, dO, lse, D of a query block
+  uint64_t* qempty = bar + 1 + NS;       // [NS] consumed by the dV / dK MMAs
+  uint64_t* tfull = bar + 1 + 2 * NS;    // [2] S^T, dP^T in TMEM
+  uint64_t* pfull = tfull + 2;           // [2] P^T, dS^T written
+  uint64_t* pfree = tfull + 4;           // [2] P^T, dS^T consumed
+  uint64_t* done = tfull + 6;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 7);
 
-  const int nk = a.S / 128, G = a.H / a.KVH;
+  const int G = a.H / a.KVH;
   const int per_j = a.B * a.KVH;
   const int j = static_cast<int>(blockIdx.x) / per_j;  // ascending: most query blocks first
   const int rest = static_cast<int>(blockIdx.x) % per_j;
   const int b = rest / a.KVH, kvh = rest % a.KVH;
-  (void)nk;
   const int nper = a.S / 64 - 2 * j;  // query blocks at or after this key tile, per head
   const int n_it = G * nper;
   const int kvrow = b * a.S + j * 128;
@@ -420,11 +644,14 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tm64);
     tma_prefetch(&tmdo);
     mbar_init(kvfull, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&qfull[s], 1);
-      mbar_init(&sfree[s], 1);
+      mbar_init(&qempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&pfull[s], 128);
+      mbar_init(&pfree[s], 1);
     }
     mbar_init(done, 1);
     fence_barrier_init();
@@ -446,10 +673,10 @@ __global__ void __launch_bounds__(192, 1)
         tma_load_2d(sm + L::V + kb * kBlk128, &tm128, kvfull, vcol + kb * 64, kvrow);
       }
       for (int it = 0; it < n_it; ++it) {
-        const int s = it & 1, u = it >> 1;
+        const int s = it % NS, u = it / NS;
         const int h = kvh * G + it / nper, qb = 2 * j + it % nper;
         const int qr = b * a.S + qb * 64;
-        mbar_wait(&sfree[s], (u & 1) ^ 1);
+        mbar_wait(&qempty[s], (u & 1) ^ 1);
         mbar_expect_tx(&qfull[s], 2 * L::QB + 512);
         for (int kb = 0; kb < NB; ++kb) {
           tma_load_2d(sm + L::Q0 + s * L::QB + kb * kBlk64, &tm64, &qfull[s], h * HD + kb * 64, qr);
@@ -465,36 +692,37 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_A = idesc_bf16_f32(128, HD, false, true);
       auto issue_s = [&](int it) {
-        const int s = it & 1, u = it >> 1;
+        const int s = it % NS, u = it / NS, ts = it & 1;
         mbar_wait(&qfull[s], u & 1);
         tc_fence_after();
         const uint8_t* q = sm + L::Q0 + s * L::QB;
         const uint8_t* d = sm + L::DO0 + s * L::QB;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
-          umma_bf16(tst(s), desc_k(sm + L::K, k, kBlk128), desc_k(q, k, kBlk64), ID_S, k > 0);
-          umma_bf16(tst(s) + 64, desc_k(sm + L::V, k, kBlk128), desc_k(d, k, kBlk64), ID_S, k > 0);
+          umma_bf16(tst(ts), desc_k(sm + L::K, k, kBlk128), desc_k(q, k, kBlk64), ID_S, k > 0);
+          umma_bf16(tst(ts) + 64, desc_k(sm + L::V, k, kBlk128), desc_k(d, k, kBlk64), ID_S, k > 0);
         }
-        umma_commit(&tfull[s]);
+        umma_commit(&tfull[ts]);
       };
       mbar_wait(kvfull, 0);
       issue_s(0);
       if (n_it > 1) issue_s(1);
       for (int it = 0; it < n_it; ++it) {
-        const int s = it & 1, u = it >> 1;
-        mbar_wait(&pfull[s], u & 1);
+        const int s = it % NS, ts = it & 1, v = it >> 1;
+        mbar_wait(&pfull[ts], v & 1);
         tc_fence_after();
         const uint8_t* q = sm + L::Q0 + s * L::QB;
         const uint8_t* d = sm + L::DO0 + s * L::QB;
-        const uint8_t* p = sm + L::P0 + s * L::PB;
-        const uint8_t* ds = sm + L::DS0 + s * L::PB;
+        const uint8_t* p = sm + L::P0 + ts * L::PB;
+        const uint8_t* ds = sm + L::DS0 + ts * L::PB;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
           umma_bf16(tbase, desc_k(p, k, kBlk128), desc_mn(d, k, kBlk64), ID_A, acc);        // dV
           umma_bf16(tbase + HD, desc_k(ds, k, kBlk128), desc_mn(q, k, kBlk64), ID_A, acc);  // dK
         }
-        umma_commit(&sfree[s]);
+        umma_commit(&qempty[s]);
+        umma_commit(&pfree[ts]);
         if (it + 2 < n_it) issue_s(it + 2);
       }
       umma_commit(done);
@@ -506,50 +734,59 @@ __global__ void __launch_bounds__(192, 1)
     const int kvi = j * 128 + r;  // key position within the sequence
     const float c = a.scale_log2;
     for (int it = 0; it < n_it; ++it) {
-      const int s = it & 1, u = it >> 1;
+      const int s = it % NS, u = it / NS, ts = it & 1, v = it >> 1;
       const int qb = 2 * j + it % nper;
-      mbar_wait(&tfull[s], u & 1);
+      mbar_wait(&tfull[ts], v & 1);
       mbar_wait(&qfull[s], u & 1);  // lse / D of the block
-      if (it >= 2) mbar_wait(&sfree[s], (u & 1) ^ 1);  // P^T / dS^T stage free
+      if (it >= 2) mbar_wait(&pfree[ts], (v & 1) ^ 1);  // P^T / dS^T stage free
       tc_fence_after();
       const float* sl = reinterpret_cast<const float*>(sm + L::LSE0 + s * 256);
       const float* sd = reinterpret_cast<const float*>(sm + L::D0 + s * 256);
-      uint8_t* p = sm + L::P0 + s * L::PB;
-      uint8_t* ds = sm + L::DS0 + s * L::PB;
+      uint8_t* p = sm + L::P0 + ts * L::PB;
+      uint8_t* ds = sm + L::DS0 + ts * L::PB;
+      uint32_t vs[64], vp[64];
+      tmem_ld32(lo + tst(ts), *reinterpret_cast<uint32_t(*)[32]>(vs));
+      tmem_ld32(lo + tst(ts) + 32, *reinterpret_cast<uint32_t(*)[32]>(vs + 32));
+      tmem_ld32(lo + tst(ts) + 64, *reinterpret_cast<uint32_t(*)[32]>(vp));
+      tmem_ld32(lo + tst(ts) + 96, *reinterpret_cast<uint32_t(*)[32]>(vp + 32));
+      tmem_wait_ld();
       const bool diag = qb * 64 < j * 128 + 128;
+      const int lim = kvi - qb * 64;  // query columns e < lim are masked (q < kv)
+      float pv[64];
+      if (!diag) {
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t vs[32], vp[32];
-        tmem_ld32(lo + tst(s) + cc * 32, vs);
-        tmem_ld32(lo + tst(s) + 64 + cc * 32, vp);
-        tmem_wait_ld();
-        float pv[32], dv[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int qc = cc * 32 + e;
-          const float pe = (diag && qb * 64 + qc < kvi) ? 0.f : ex2(fmaf(f32(vs[e]), c, -sl[qc]));
-          pv[e] = pe;
-          dv[e] = pe * (f32(vp[e]) - sd[qc]);
+        for (int e = 0; e < 64; e += 4) {
+          pv[e] = ex2_mix<0>(fmaf(f32(vs[e]), c, -sl[e]));
+          pv[e + 1] = ex2_mix<1>(fmaf(f32(vs[e + 1]), c, -sl[e + 1]));
+          pv[e + 2] = ex2_mix<2>(fmaf(f32(vs[e + 2]), c, -sl[e + 2]));
+          pv[e + 3] = ex2_mix<3>(fmaf(f32(vs[e + 3]), c, -sl[e + 3]));
         }
-        st_swz32(p, r, cc * 4, pv);
-        st_swz32(ds, r, cc * 4, dv);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) pv[e] = e < lim ? 0.f : ex2(fmaf(f32(vs[e]), c, -sl[e]));
       }
+      st_swz32(p, r, 0, pv);
+      st_swz32(p, r, 4, pv + 32);
+#pragma unroll
+      for (int e = 0; e < 64; ++e) pv[e] *= f32(vp[e]) - sd[e];
+      st_swz32(ds, r, 0, pv);
+      st_swz32(ds, r, 4, pv + 32);
       fence_async_smem();
       tc_fence_before();
-      mbar_arrive(&pfull[s]);
+      mbar_arrive(&pfull[ts]);
     }
     mbar_wait(done, 0);
     tc_fence_after();
     bf16* drow = a.dqkv + static_cast<long long>(kvrow + r) * a.ld;
 #pragma unroll
     for (int cc = 0; cc < HD / 32; ++cc) {
-      uint32_t v[32];
-      tmem_ld32(tbase + lo + cc * 32, v);
+      uint32_t o[32];
+      tmem_ld32(tbase + lo + cc * 32, o);
       tmem_wait_ld();
-      st_row32(drow + vcol + cc * 32, v, 1.f);  // dV
-      tmem_ld32(tbase + lo + HD + cc * 32, v);
+      st_row32(drow + vcol + cc * 32, o, 1.f);  // dV
+      tmem_ld32(tbase + lo + HD + cc * 32, o);
       tmem_wait_ld();
-      st_row32(drow + kcol + cc * 32, v, a.scale);  // dK
+      st_row32(drow + kcol + cc * 32, o, a.scale);  // dK
     }
   }
   tc_fence_before();
@@ -557,176 +794,6 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   if (warp == 1) tmem_dealloc<512>(tbase);
 }
-
-// ------------------------------------------------------------------------------------------
-// dQ: warp 0 TMA, warp 1 MMA, warps 2-5 one query row each
-template <int HD>
-struct QSmem {
-  static constexpr uint32_t TILE = 128 * HD * 2;  // Q or dO tile (128 rows)
-  static constexpr uint32_t KB = 64 * HD * 2;     // K or V block (64 rows)
-  static constexpr uint32_t SB = 128 * 64 * 2;    // dS block (128 q x 64 kv)
-  static constexpr uint32_t Q = 0, DO = TILE, K0 = 2 * TILE, V0 = K0 + 2 * KB, DS0 = V0 + 2 * KB,
-                            BAR = DS0 + 2 * SB;
-  static constexpr size_t BYTES = 1024 + BAR + 256;
-};
-
-template <int HD>
-__global__ void __launch_bounds__(192, 1)
-    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm128,
-                       const __grid_constant__ CUtensorMap tm64,
-                       const __grid_constant__ CUtensorMap tmdo, const BwdArgs a) {
-  using L = QSmem<HD>;
-  constexpr int NB = HD / 64;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t* qfull = bar;
-  uint64_t* kvfull = bar + 1;  // [2]
-  uint64_t* sfree = bar + 3;   // [2] K, V, dS stage consumed
-  uint64_t* tfull = bar + 5;   // [2] S, dP in TMEM
-  uint64_t* pfull = bar + 7;   // [2] dS written
-  uint64_t* done = bar + 9;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 10);
-
-  const int nq = a.S / 128;
-  const int per_i = a.B * a.H;
-  const int i = nq - 1 - static_cast<int>(blockIdx.x) / per_i;  // longest rows first
-  const int rest = static_cast<int>(blockIdx.x) % per_i;
-  const int b = rest / a.H, h = rest % a.H;
-  const int kvh = h / (a.H / a.KVH);
-  const int n = 2 * i + 2;  // 64-row key blocks up to the diagonal
-  const int qrow = b * a.S + i * 128;
-  const int kcol = a.H * HD + kvh * HD, vcol = (a.H + a.KVH) * HD + kvh * HD;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-  if (threadIdx.x == 0) {
-    tma_prefetch(&tm128);
-    tma_prefetch(&tm64);
-    tma_prefetch(&tmdo);
-    mbar_init(qfull, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&kvfull[s], 1);
-      mbar_init(&sfree[s], 1);
-      mbar_init(&tfull[s], 1);
-      mbar_init(&pfull[s], 128);
-    }
-    mbar_init(done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tslot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tslot;
-  // TMEM: dQ [0, HD), stage s: S [HD + 128 s, +64), dP [+64, +128)
-  auto tst = [&](int s) { return tbase + HD + 128 * s; };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(qfull, 2 * L::TILE);
-      for (int kb = 0; kb < NB; ++kb) {
-        tma_load_2d(sm + L::Q + kb * kBlk128, &tm128, qfull, h * HD + kb * 64, qrow);
-        tma_load_2d(sm + L::DO + kb * kBlk128, &tmdo, qfull, h * HD + kb * 64, qrow);
-      }
-      for (int jj = 0; jj < n; ++jj) {
-        const int s = jj & 1, u = jj >> 1;
-        const int kr = b * a.S + jj * 64;
-        mbar_wait(&sfree[s], (u & 1) ^ 1);
-        mbar_expect_tx(&kvfull[s], 2 * L::KB);
-        for (int kb = 0; kb < NB; ++kb) {
-          tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], kcol + kb * 64, kr);
-          tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], vcol + kb * 64, kr);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
-      constexpr uint32_t ID_Q = idesc_bf16_f32(128, HD, false, true);
-      auto issue_s = [&](int jj) {
-        const int s = jj & 1, u = jj >> 1;
-        mbar_wait(&kvfull[s], u & 1);
-        tc_fence_after();
-        const uint8_t* k = sm + L::K0 + s * L::KB;
-        const uint8_t* v = sm + L::V0 + s * L::KB;
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          umma_bf16(tst(s), desc_k(sm + L::Q, kk, kBlk128), desc_k(k, kk, kBlk64), ID_S, kk > 0);
-          umma_bf16(tst(s) + 64, desc_k(sm + L::DO, kk, kBlk128), desc_k(v, kk, kBlk64), ID_S,
-                    kk > 0);
-        }
-        umma_commit(&tfull[s]);
-      };
-      mbar_wait(qfull, 0);
-      issue_s(0);
-      if (n > 1) issue_s(1);
-      for (int jj = 0; jj < n; ++jj) {
-        const int s = jj & 1, u = jj >> 1;
-        mbar_wait(&pfull[s], u & 1);
-        tc_fence_after();
-        const uint8_t* k = sm + L::K0 + s * L::KB;
-        const uint8_t* ds = sm + L::DS0 + s * L::SB;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_bf16(tbase, desc_k(ds, kk, kBlk128), desc_mn(k, kk, kBlk64), ID_Q,
-                    (jj > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&sfree[s]);
-        if (jj + 2 < n) issue_s(jj + 2);
-      }
-      umma_commit(done);
-    }
-  } else {
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;
-    const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
-    const int qi = i * 128 + r;
-    const long long st = (static_cast<long long>(b) * a.H + h) * a.S + qi;
-    const float lse = a.lse[st], dd = a.D[st];
-    const float c = a.scale_log2;
-    for (int jj = 0; jj < n; ++jj) {
-      const int s = jj & 1, u = jj >> 1;
-      mbar_wait(&tfull[s], u & 1);
-      if (jj >= 2) mbar_wait(&sfree[s], (u & 1) ^ 1);  // dS stage free
-      tc_fence_after();
-      uint8_t* ds = sm + L::DS0 + s * L::SB;
-      const bool diag = jj * 64 + 63 > i * 128;
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t vs[32], vp[32];
-        tmem_ld32(lo + tst(s) + cc * 32, vs);
-        tmem_ld32(lo + tst(s) + 64 + cc * 32, vp);
-        tmem_wait_ld();
-        float dv[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int kc = jj * 64 + cc * 32 + e;
-          const float pe = (diag && kc > qi) ? 0.f : ex2(fmaf(f32(vs[e]), c, -lse));
-          dv[e] = pe * (f32(vp[e]) - dd);
-        }
-        st_swz32(ds, r, cc * 4, dv);
-      }
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(&pfull[s]);
-    }
-    mbar_wait(done, 0);
-    tc_fence_after();
-    bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD;
-#pragma unroll
-    for (int cc = 0; cc < HD / 32; ++cc) {
-      uint32_t v[32];
-      tmem_ld32(tbase + lo + cc * 32, v);
-      tmem_wait_ld();
-      st_row32(drow + cc * 32, v, a.scale);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 1) tmem_dealloc<512>(tbase);
-}
-
-// ------------------------------------------------------------------------------------------
 
 }  // namespace
 
@@ -768,7 +835,8 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
                 cudaStream_t st) {
   const int ld = (H + 2 * KVH) * HD;
   const int N = B * S;
-  const CUtensorMap m = tmap(qkv, ld, N, ld, 128);
+  const CUtensorMap mq = tmap(qkv, ld, N, ld, 128);
+  const CUtensorMap mkv = tmap(qkv, ld, N, ld, 64);
   FwdArgs a{B, H, KVH, S, ld, static_cast<bf16*>(o), H * HD, lse,
             1.4426950408889634f / sqrtf(static_cast<float>(HD))};
   static bool attr = false;
@@ -777,21 +845,16 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
     attr = true;
   }
   const int grid = (S / 128) * B * KVH * (H / KVH / 2);
-  attn_fwd_kernel<HD><<<grid, 320, std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(m, a);
+  attn_fwd_kernel<HD><<<grid, 320, std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(mq, mkv, a);
   check_launch("attn_fwd_kernel");
 }
 
+// dQ first (it also writes D), then dK / dV (reads D)
 template <int HD>
 void bwd_launch(int B, int H, int KVH, int S, const void* qkv, const void* o, const void* dout,
                 const float* lse, float* D, void* dqkv, cudaStream_t st) {
   const int ld = (H + 2 * KVH) * HD, ldo = H * HD;
   const int N = B * S;
-  {
-    const long long warps = static_cast<long long>(N) * H;
-    attn_bwd_dot_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
-        static_cast<const bf16*>(o), static_cast<const bf16*>(dout), ldo, N, H, S, HD, D);
-    check_launch("attn_bwd_dot_kernel");
-  }
   const CUtensorMap m128 = tmap(qkv, ld, N, ld, 128);
   const CUtensorMap m64 = tmap(qkv, ld, N, ld, 64);
   const float sc = 1.f / sqrtf(static_cast<float>(HD));
@@ -803,14 +866,17 @@ void bwd_launch(int B, int H, int KVH, int S, const void* qkv, const void* o, co
     attr = true;
   }
   {
-    const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 64);
-    attn_bwd_dkdv_kernel<HD><<<(S / 128) * B * KVH, 192, std::max(KvSmem<HD>::BYTES, kMinSmem), st>>>(m128, m64, mdo, a);
-    check_launch("attn_bwd_dkdv_kernel");
+    const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 128);
+    const CUtensorMap mo = tmap(o, ldo, N, ldo, 128);
+    attn_bwd_dq_kernel<HD><<<(S / 128) * B * H, 192, std::max(QSmem<HD>::BYTES, kMinSmem), st>>>(
+        m128, m64, mdo, mo, a);
+    check_launch("attn_bwd_dq_kernel");
   }
   {
-    const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 128);
-    attn_bwd_dq_kernel<HD><<<(S / 128) * B * H, 192, std::max(QSmem<HD>::BYTES, kMinSmem), st>>>(m128, m64, mdo, a);
-    check_launch("attn_bwd_dq_kernel");
+    const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 64);
+    attn_bwd_dkdv_kernel<HD><<<(S / 128) * B * KVH, 192, std::max(KvSmem<HD>::BYTES, kMinSmem),
+                               st>>>(m128, m64, mdo, a);
+    check_launch("attn_bwd_dkdv_kernel");
   }
 }
 
