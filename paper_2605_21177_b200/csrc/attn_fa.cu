@@ -154,7 +154,7 @@ struct FwdArgs {
 };
 
 // ------------------------------------------------------------------------------------------
-// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax of head A, 6-9 of B.
+// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-9 softmax of head A, 10-17 of B.
 // Key / value blocks of 64 rows in a 3-deep ring; S of each head 128 x 64 in TMEM.
 template <int HD>
 struct FwdSmem {
@@ -163,12 +163,14 @@ struct FwdSmem {
   static constexpr uint32_t KB = 64 * HD * 2;   // key or value block
   static constexpr uint32_t PB = 128 * 64 * 2;  // P block (bf16)
   static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NS * KB, P0 = V0 + NS * KB,
-                            BAR = P0 + 2 * PB;
+                            XCH = P0 + 2 * PB, BAR = XCH + 8 * 128 * 4;
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
+constexpr int kFwdThreads = 64 + 16 * 32;  // TMA warp, MMA warp, 16 softmax warps
+
 template <int HD>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __maxnreg__(112)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv,
                     const FwdArgs a) {
   using L = FwdSmem<HD>;
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&sfull[t], 1);
-      mbar_init(&pfull[t], 128);
+      mbar_init(&pfull[t], 256);
       mbar_init(&ofull[t], 1);
     }
     fence_barrier_init();
@@ -285,33 +287,42 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else {
-    const int t = (warp - 2) / 4;
+    // softmax: 8 warps per head, two per TMEM lane quarter; a thread owns half a row (32 of
+    // the block's 64 columns, half of O's columns).  The two halves of a row agree on the
+    // running max through a double-buffered smem exchange and a named barrier per head.
+    const int idx = warp - 2;
+    const int t = idx / 8, hf = (idx / 4) & 1;
     const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tS = tbase + lo + t * 64, tO = tbase + lo + 128 + t * HD;
+    const uint32_t tS = tbase + lo + t * 64 + hf * 32;
+    const uint32_t tO = tbase + lo + 128 + t * HD + hf * (HD / 2);
     uint8_t* sP = sm + L::P0 + t * L::PB;
+    float* xch = reinterpret_cast<float*>(sm + L::XCH);  // [2 parity][2 heads][2 halves][128]
+    auto slot = [&](int par, int half) { return xch + ((par * 2 + t) * 2 + half) * 128 + r; };
     const float c = a.scale_log2;
     const int qpos = i * 128 + r;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nb; ++j) {
       mbar_wait(&sfull[t], j & 1);
       tc_fence_after();
-      uint32_t v[64];
-      tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(v));
-      tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      uint32_t v[32];
+      tmem_ld32(tS, v);
       tmem_wait_ld();
       const bool diag = j * 64 + 63 > i * 128;  // block reaches past this tile's first row
-      const int lim = qpos - j * 64;             // columns e <= lim are visible
+      const int lim = qpos - j * 64 - hf * 32;   // columns e <= lim are visible
       float mx = -INFINITY;
       if (!diag) {
 #pragma unroll
-        for (int e = 0; e < 64; ++e) mx = fmaxf(mx, f32(v[e]));
+        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, f32(v[e]));
       } else {
 #pragma unroll
-        for (int e = 0; e < 64; ++e)
+        for (int e = 0; e < 32; ++e)
           if (e <= lim) mx = fmaxf(mx, f32(v[e]));
       }
+      *slot(j & 1, hf) = mx;
+      named_bar_sync(1 + t, 256);
+      mx = fmaxf(mx, *slot(j & 1, hf ^ 1));
       const float m_new = fmaxf(m, mx * c);
       if (j > 0) {  // PV of the previous block done: P buffer and O free
         mbar_wait(&ofull[t], (j - 1) & 1);
@@ -324,7 +335,7 @@ __global__ void __launch_bounds__(320, 1)
         l *= alpha;
         m = m_new;
 #pragma unroll
-        for (int cc = 0; cc < HD / 32; ++cc) {
+        for (int cc = 0; cc < HD / 64; ++cc) {
           uint32_t o[32];
           tmem_ld32(tO + cc * 32, o);
           tmem_wait_ld();
@@ -334,40 +345,53 @@ __global__ void __launch_bounds__(320, 1)
         }
         tmem_wait_st();
       }
-      float p[64];
-      const float nm = -m;
+      tmem_ld32(tS, v);  // reload (S is still in TMEM): keeps v dead across the rescale
+      tmem_wait_ld();
+      float pr[32];
+      const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const float2 x = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
+        pr[e] = x.x;
+        pr[e + 1] = x.y;
+      }
       if (!diag) {
 #pragma unroll
-        for (int e = 0; e < 64; e += 4) {
-          p[e] = ex2_mix<0>(fmaf(f32(v[e]), c, nm));
-          p[e + 1] = ex2_mix<1>(fmaf(f32(v[e + 1]), c, nm));
-          p[e + 2] = ex2_mix<2>(fmaf(f32(v[e + 2]), c, nm));
-          p[e + 3] = ex2_mix<3>(fmaf(f32(v[e + 3]), c, nm));
+        for (int e = 0; e < 32; e += 4) {
+          pr[e] = ex2_mix<0>(pr[e]);
+          pr[e + 1] = ex2_mix<1>(pr[e + 1]);
+          pr[e + 2] = ex2_mix<2>(pr[e + 2]);
+          pr[e + 3] = ex2_mix<3>(pr[e + 3]);
         }
       } else {
 #pragma unroll
-        for (int e = 0; e < 64; ++e) p[e] = e <= lim ? ex2(fmaf(f32(v[e]), c, nm)) : 0.f;
+        for (int e = 0; e < 32; ++e) pr[e] = e <= lim ? ex2(pr[e]) : 0.f;
       }
+      float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int e = 0; e < 64; ++e) l += p[e];
-      st_swz32(sP, r, 0, p);
-      st_swz32(sP, r, 4, p + 32);
+      for (int e = 0; e < 32; e += 2) acc = __fadd2_rn(acc, make_float2(pr[e], pr[e + 1]));
+      l += acc.x + acc.y;
+      st_swz32(sP, r, hf * 4, pr);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&pfull[t]);
     }
+    // l of the whole row = the two halves' sums (same running max)
+    *slot(nb & 1, hf) = l;
+    named_bar_sync(1 + t, 256);
+    l += *slot(nb & 1, hf ^ 1);
     mbar_wait(&ofull[t], (nb - 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l;
-    bf16* out = a.o + static_cast<long long>(qrow + r) * a.ldo + (h0 + t) * HD;
+    bf16* out = a.o + static_cast<long long>(qrow + r) * a.ldo + (h0 + t) * HD + hf * (HD / 2);
 #pragma unroll
-    for (int cc = 0; cc < HD / 32; ++cc) {
+    for (int cc = 0; cc < HD / 64; ++cc) {
       uint32_t o[32];
       tmem_ld32(tO + cc * 32, o);
       tmem_wait_ld();
       st_row32(out + cc * 32, o, inv);
     }
-    a.lse[(static_cast<long long>(b) * a.H + h0 + t) * a.S + qpos] = m + __log2f(l);
+    if (hf == 0) a.lse[(static_cast<long long>(b) * a.H + h0 + t) * a.S + qpos] = m + __log2f(l);
   }
   tc_fence_before();
   __syncthreads();
@@ -386,7 +410,7 @@ struct BwdArgs {
 
 // ------------------------------------------------------------------------------------------
 // dQ (runs first; also forms D = rowsum(dO * O) of its rows): warp 0 TMA, warp 1 MMA,
-// warps 2-5 one query row each.  Key / value blocks of 64 rows in a 4-deep ring; S and dP
+// warps 2-9 half a query row each.  Key / value blocks of 64 rows in a 4-deep ring; S and dP
 // double-buffered in TMEM; the O tile is staged once in the dS buffers before the loop.
 template <int HD>
 struct QSmem {
@@ -400,8 +424,10 @@ struct QSmem {
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
+constexpr int kBwdThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 gradient warps
+
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm128,
                        const __grid_constant__ CUtensorMap tm64,
                        const __grid_constant__ CUtensorMap tmdo,
@@ -443,7 +469,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&pfull[s], 128);
+      mbar_init(&pfull[s], 256);
       mbar_init(&pfree[s], 1);
     }
     mbar_init(done, 1);
@@ -514,15 +540,17 @@ __global__ void __launch_bounds__(192, 1)
       umma_commit(done);
     }
   } else {
-    const int quarter = warp & 3;
+    // 8 warps, two per TMEM lane quarter: a thread owns half a row (32 of the block's 64 key
+    // columns of S / dP, half of dQ's columns)
+    const int quarter = warp & 3, hf = (warp - 2) / 4;
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
     const int qi = i * 128 + r;
     const long long st = (static_cast<long long>(b) * a.H + h) * a.S + qi;
     const float lse = a.lse[st];
     const float c = a.scale_log2;
-    // D of this row from the staged dO and O tiles (own row only: the dS writes below reuse
-    // the O staging bytes of this same row)
+    // D of this row from the staged dO and O tiles (both halves form it; the dS writes below
+    // reuse the O staging bytes, so the row's two threads sync before the first one)
     mbar_wait(qfull, 0);
     float dd = 0.f;
 #pragma unroll
@@ -541,48 +569,59 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-    a.D[st] = dd;
+    if (hf == 0) a.D[st] = dd;
+    named_bar_sync(1, 256);
+    const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse, -lse), nd2 = make_float2(-dd, -dd);
     for (int jj = 0; jj < n; ++jj) {
       const int ts = jj & 1, v = jj >> 1;
       mbar_wait(&tfull[ts], v & 1);
       if (jj >= 2) mbar_wait(&pfree[ts], (v & 1) ^ 1);  // dS stage free
       tc_fence_after();
       uint8_t* ds = sm + L::DS0 + ts * L::SB;
-      uint32_t vs[64], vp[64];
-      tmem_ld32(lo + tst(ts), *reinterpret_cast<uint32_t(*)[32]>(vs));
-      tmem_ld32(lo + tst(ts) + 32, *reinterpret_cast<uint32_t(*)[32]>(vs + 32));
-      tmem_ld32(lo + tst(ts) + 64, *reinterpret_cast<uint32_t(*)[32]>(vp));
-      tmem_ld32(lo + tst(ts) + 96, *reinterpret_cast<uint32_t(*)[32]>(vp + 32));
+      uint32_t vs[32], vp[32];
+      tmem_ld32(lo + tst(ts) + hf * 32, vs);
+      tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
       tmem_wait_ld();
       const bool diag = jj * 64 + 63 > i * 128;
-      const int lim = qi - jj * 64;
-      float dv[64];
+      const int lim = qi - jj * 64 - hf * 32;
+      float dv[32];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const float2 x = __ffma2_rn(make_float2(f32(vs[e]), f32(vs[e + 1])), c2, nl2);
+        dv[e] = x.x;
+        dv[e + 1] = x.y;
+      }
       if (!diag) {
 #pragma unroll
-        for (int e = 0; e < 64; e += 4) {
-          dv[e] = ex2_mix<0>(fmaf(f32(vs[e]), c, -lse)) * (f32(vp[e]) - dd);
-          dv[e + 1] = ex2_mix<1>(fmaf(f32(vs[e + 1]), c, -lse)) * (f32(vp[e + 1]) - dd);
-          dv[e + 2] = ex2_mix<2>(fmaf(f32(vs[e + 2]), c, -lse)) * (f32(vp[e + 2]) - dd);
-          dv[e + 3] = ex2_mix<3>(fmaf(f32(vs[e + 3]), c, -lse)) * (f32(vp[e + 3]) - dd);
+        for (int e = 0; e < 32; e += 4) {
+          dv[e] = ex2_mix<0>(dv[e]);
+          dv[e + 1] = ex2_mix<1>(dv[e + 1]);
+          dv[e + 2] = ex2_mix<2>(dv[e + 2]);
+          dv[e + 3] = ex2_mix<3>(dv[e + 3]);
         }
       } else {
 #pragma unroll
-        for (int e = 0; e < 64; ++e)
-          dv[e] = e <= lim ? ex2(fmaf(f32(vs[e]), c, -lse)) * (f32(vp[e]) - dd) : 0.f;
+        for (int e = 0; e < 32; ++e) dv[e] = e <= lim ? ex2(dv[e]) : 0.f;
       }
-      st_swz32(ds, r, 0, dv);
-      st_swz32(ds, r, 4, dv + 32);
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {  // dS = P (dP - D)
+        const float2 x = __fmul2_rn(make_float2(dv[e], dv[e + 1]),
+                                    __fadd2_rn(make_float2(f32(vp[e]), f32(vp[e + 1])), nd2));
+        dv[e] = x.x;
+        dv[e + 1] = x.y;
+      }
+      st_swz32(ds, r, hf * 4, dv);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&pfull[ts]);
     }
     mbar_wait(done, 0);
     tc_fence_after();
-    bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD;
+    bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD + hf * (HD / 2);
 #pragma unroll
-    for (int cc = 0; cc < HD / 32; ++cc) {
+    for (int cc = 0; cc < HD / 64; ++cc) {
       uint32_t o[32];
-      tmem_ld32(tbase + lo + cc * 32, o);
+      tmem_ld32(tbase + lo + hf * (HD / 2) + cc * 32, o);
       tmem_wait_ld();
       st_row32(drow + cc * 32, o, a.scale);
     }
@@ -594,7 +633,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ------------------------------------------------------------------------------------------
-// dK / dV: warp 0 TMA, warp 1 MMA, warps 2-5 one key row each.  Query / dO blocks of 64 rows
+// dK / dV: warp 0 TMA, warp 1 MMA, warps 2-9 half a key row each.  Query / dO blocks of 64 rows
 // (+ their lse / D) in a 3-deep ring; S^T, dP^T double-buffered in TMEM; P^T / dS^T in two
 // smem stages.
 template <int HD>
@@ -610,7 +649,7 @@ struct KvSmem {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm128,
                          const __grid_constant__ CUtensorMap tm64,
                          const __grid_constant__ CUtensorMap tmdo, const BwdArgs a) {
@@ -650,7 +689,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&pfull[s], 128);
+      mbar_init(&pfull[s], 256);
       mbar_init(&pfree[s], 1);
     }
     mbar_init(done, 1);
@@ -728,11 +767,14 @@ __global__ void __launch_bounds__(192, 1)
       umma_commit(done);
     }
   } else {
-    const int quarter = warp & 3;
+    // 8 warps, two per TMEM lane quarter: a thread owns half a key row (32 of the block's 64
+    // query columns of S^T / dP^T, half of dK's / dV's columns)
+    const int quarter = warp & 3, hf = (warp - 2) / 4;
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
     const int kvi = j * 128 + r;  // key position within the sequence
     const float c = a.scale_log2;
+    const float2 c2 = make_float2(c, c);
     for (int it = 0; it < n_it; ++it) {
       const int s = it % NS, u = it / NS, ts = it & 1, v = it >> 1;
       const int qb = 2 * j + it % nper;
@@ -740,51 +782,60 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&qfull[s], u & 1);  // lse / D of the block
       if (it >= 2) mbar_wait(&pfree[ts], (v & 1) ^ 1);  // P^T / dS^T stage free
       tc_fence_after();
-      const float* sl = reinterpret_cast<const float*>(sm + L::LSE0 + s * 256);
-      const float* sd = reinterpret_cast<const float*>(sm + L::D0 + s * 256);
+      const float* sl = reinterpret_cast<const float*>(sm + L::LSE0 + s * 256) + hf * 32;
+      const float* sd = reinterpret_cast<const float*>(sm + L::D0 + s * 256) + hf * 32;
       uint8_t* p = sm + L::P0 + ts * L::PB;
       uint8_t* ds = sm + L::DS0 + ts * L::PB;
-      uint32_t vs[64], vp[64];
-      tmem_ld32(lo + tst(ts), *reinterpret_cast<uint32_t(*)[32]>(vs));
-      tmem_ld32(lo + tst(ts) + 32, *reinterpret_cast<uint32_t(*)[32]>(vs + 32));
-      tmem_ld32(lo + tst(ts) + 64, *reinterpret_cast<uint32_t(*)[32]>(vp));
-      tmem_ld32(lo + tst(ts) + 96, *reinterpret_cast<uint32_t(*)[32]>(vp + 32));
+      uint32_t vs[32], vp[32];
+      tmem_ld32(lo + tst(ts) + hf * 32, vs);
+      tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
       tmem_wait_ld();
       const bool diag = qb * 64 < j * 128 + 128;
-      const int lim = kvi - qb * 64;  // query columns e < lim are masked (q < kv)
-      float pv[64];
+      const int lim = kvi - qb * 64 - hf * 32;  // query columns e < lim are masked (q < kv)
+      float pv[32];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const float2 x = __ffma2_rn(make_float2(f32(vs[e]), f32(vs[e + 1])), c2,
+                                    make_float2(-sl[e], -sl[e + 1]));
+        pv[e] = x.x;
+        pv[e + 1] = x.y;
+      }
       if (!diag) {
 #pragma unroll
-        for (int e = 0; e < 64; e += 4) {
-          pv[e] = ex2_mix<0>(fmaf(f32(vs[e]), c, -sl[e]));
-          pv[e + 1] = ex2_mix<1>(fmaf(f32(vs[e + 1]), c, -sl[e + 1]));
-          pv[e + 2] = ex2_mix<2>(fmaf(f32(vs[e + 2]), c, -sl[e + 2]));
-          pv[e + 3] = ex2_mix<3>(fmaf(f32(vs[e + 3]), c, -sl[e + 3]));
+        for (int e = 0; e < 32; e += 4) {
+          pv[e] = ex2_mix<0>(pv[e]);
+          pv[e + 1] = ex2_mix<1>(pv[e + 1]);
+          pv[e + 2] = ex2_mix<2>(pv[e + 2]);
+          pv[e + 3] = ex2_mix<3>(pv[e + 3]);
         }
       } else {
 #pragma unroll
-        for (int e = 0; e < 64; ++e) pv[e] = e < lim ? 0.f : ex2(fmaf(f32(vs[e]), c, -sl[e]));
+        for (int e = 0; e < 32; ++e) pv[e] = e < lim ? 0.f : ex2(pv[e]);
       }
-      st_swz32(p, r, 0, pv);
-      st_swz32(p, r, 4, pv + 32);
+      st_swz32(p, r, hf * 4, pv);
 #pragma unroll
-      for (int e = 0; e < 64; ++e) pv[e] *= f32(vp[e]) - sd[e];
-      st_swz32(ds, r, 0, pv);
-      st_swz32(ds, r, 4, pv + 32);
+      for (int e = 0; e < 32; e += 2) {  // dS^T = P^T (dP^T - D)
+        const float2 x = __fmul2_rn(make_float2(pv[e], pv[e + 1]),
+                                    __fadd2_rn(make_float2(f32(vp[e]), f32(vp[e + 1])),
+                                               make_float2(-sd[e], -sd[e + 1])));
+        pv[e] = x.x;
+        pv[e + 1] = x.y;
+      }
+      st_swz32(ds, r, hf * 4, pv);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&pfull[ts]);
     }
     mbar_wait(done, 0);
     tc_fence_after();
-    bf16* drow = a.dqkv + static_cast<long long>(kvrow + r) * a.ld;
+    bf16* drow = a.dqkv + static_cast<long long>(kvrow + r) * a.ld + hf * (HD / 2);
 #pragma unroll
-    for (int cc = 0; cc < HD / 32; ++cc) {
+    for (int cc = 0; cc < HD / 64; ++cc) {
       uint32_t o[32];
-      tmem_ld32(tbase + lo + cc * 32, o);
+      tmem_ld32(tbase + lo + hf * (HD / 2) + cc * 32, o);
       tmem_wait_ld();
       st_row32(drow + vcol + cc * 32, o, 1.f);  // dV
-      tmem_ld32(tbase + lo + HD + cc * 32, o);
+      tmem_ld32(tbase + lo + HD + hf * (HD / 2) + cc * 32, o);
       tmem_wait_ld();
       st_row32(drow + kcol + cc * 32, o, a.scale);  // dK
     }
@@ -845,7 +896,7 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
     attr = true;
   }
   const int grid = (S / 128) * B * KVH * (H / KVH / 2);
-  attn_fwd_kernel<HD><<<grid, 320, std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(mq, mkv, a);
+  attn_fwd_kernel<HD><<<grid, kFwdThreads, std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(mq, mkv, a);
   check_launch("attn_fwd_kernel");
 }
 
@@ -868,13 +919,13 @@ void bwd_launch(int B, int H, int KVH, int S, const void* qkv, const void* o, co
   {
     const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 128);
     const CUtensorMap mo = tmap(o, ldo, N, ldo, 128);
-    attn_bwd_dq_kernel<HD><<<(S / 128) * B * H, 192, std::max(QSmem<HD>::BYTES, kMinSmem), st>>>(
+    attn_bwd_dq_kernel<HD><<<(S / 128) * B * H, kBwdThreads, std::max(QSmem<HD>::BYTES, kMinSmem), st>>>(
         m128, m64, mdo, mo, a);
     check_launch("attn_bwd_dq_kernel");
   }
   {
     const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 64);
-    attn_bwd_dkdv_kernel<HD><<<(S / 128) * B * KVH, 192, std::max(KvSmem<HD>::BYTES, kMinSmem),
+    attn_bwd_dkdv_kernel<HD><<<(S / 128) * B * KVH, kBwdThreads, std::max(KvSmem<HD>::BYTES, kMinSmem),
                                st>>>(m128, m64, mdo, a);
     check_launch("attn_bwd_dkdv_kernel");
   }
