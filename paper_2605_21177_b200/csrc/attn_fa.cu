@@ -170,7 +170,7 @@ struct FwdSmem {
 constexpr int kFwdThreads = 64 + 16 * 32;  // TMA warp, MMA warp, 16 softmax warps
 
 template <int HD>
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 32 <= 16K registers
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv,
                     const FwdArgs a) {
   using L = FwdSmem<HD>;
