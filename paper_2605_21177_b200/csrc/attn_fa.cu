@@ -145,6 +145,16 @@ __device__ __forceinline__ float ex2_mix(float x) {
   else return ex2(x);
 }
 
+// Spin wait (no suspend hint): the attention pipelines hand off every ~0.1-0.3 us between
+// the softmax warps and the MMA thread, so wake-up latency is on the critical path.
+__device__ __forceinline__ void spin_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_test(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_test(bar, parity)) {
+    if (clock64() - t0 > 20000000000LL) __trap();
+  }
+}
+
 struct FwdArgs {
   int B, H, KVH, S, ld;  // ld = qkv row pitch (elements)
   bf16* o;
@@ -169,39 +179,53 @@ struct FwdSmem {
 
 constexpr int kFwdThreads = 64 + 16 * 32;  // TMA warp, MMA warp, 16 softmax warps
 
+// Work item = (query tile, batch, KV head, head pair), longest query tiles first; a persistent
+// CTA walks items blockIdx.x, +gridDim.x, ...  The next item's Q tiles load while the current
+// item's last blocks run, and its first S MMAs overlap the current item's O epilogue.
+struct FwdItem {
+  int i, b, kvh, h0, nb;
+};
+__device__ __forceinline__ FwdItem fwd_item(const FwdArgs& a, int item) {
+  const int nq = a.S / 128, G = a.H / a.KVH, G2 = G / 2;
+  const int per_i = a.B * a.KVH * G2;
+  FwdItem w;
+  w.i = nq - 1 - item / per_i;
+  const int rest = item % per_i;
+  w.b = rest / (a.KVH * G2);
+  w.kvh = (rest / G2) % a.KVH;
+  w.h0 = w.kvh * G + 2 * (rest % G2);
+  w.nb = 2 * w.i + 2;  // 64-row key blocks up to the diagonal
+  return w;
+}
+
 template <int HD>
 __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 32 <= 16K registers
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv,
-                    const FwdArgs a) {
+                    const FwdArgs a, int n_items) {
   using L = FwdSmem<HD>;
   constexpr int NB = HD / 64, NS = L::NS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* qfull = bar;
-  uint64_t* kfull = bar + 1;            // [NS]
-  uint64_t* vfull = bar + 1 + NS;       // [NS]
-  uint64_t* kvempty = bar + 1 + 2 * NS; // [NS]
-  uint64_t* sfull = bar + 1 + 3 * NS;   // [2] per head
+  uint64_t* qempty = bar + 1;
+  uint64_t* kfull = bar + 2;            // [NS]
+  uint64_t* vfull = bar + 2 + NS;       // [NS]
+  uint64_t* kvempty = bar + 2 + 2 * NS; // [NS]
+  uint64_t* sfull = bar + 2 + 3 * NS;   // [2] per head
   uint64_t* pfull = sfull + 2;          // [2]
   uint64_t* ofull = sfull + 4;          // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfull + 6);
+  uint64_t* oempty = sfull + 6;         // [2] O read out by the epilogue
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfull + 8);
 
-  const int nq = a.S / 128, G = a.H / a.KVH, G2 = G / 2;
-  const int per_i = a.B * a.KVH * G2;
-  const int i = nq - 1 - static_cast<int>(blockIdx.x) / per_i;  // longest rows first
-  const int rest = static_cast<int>(blockIdx.x) % per_i;
-  const int b = rest / (a.KVH * G2), kvh = (rest / G2) % a.KVH, pr = rest % G2;
-  const int h0 = kvh * G + 2 * pr;
-  const int nb = 2 * i + 2;  // 64-row key blocks up to the diagonal
-  const int qrow = b * a.S + i * 128, krow = b * a.S;
-  const int kcol = a.H * HD + kvh * HD, vcol = (a.H + a.KVH) * HD + kvh * HD;
+  const int krow_of = a.S;  // rows per sequence
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmq);
     tma_prefetch(&tmkv);
     mbar_init(qfull, 1);
+    mbar_init(qempty, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kfull[s], 1);
       mbar_init(&vfull[s], 1);
@@ -211,6 +235,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
       mbar_init(&sfull[t], 1);
       mbar_init(&pfull[t], 256);
       mbar_init(&ofull[t], 1);
+      mbar_init(&oempty[t], 256);
     }
     fence_barrier_init();
   }
@@ -223,22 +248,29 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(qfull, 2 * L::QT);
-      for (int t = 0; t < 2; ++t)
-        for (int kb = 0; kb < NB; ++kb)
-          tma_load_2d(sm + L::Q0 + t * L::QT + kb * kBlk128, &tmq, qfull, (h0 + t) * HD + kb * 64,
-                      qrow);
-      for (int j = 0; j < nb; ++j) {
-        const int s = j % NS, u = j / NS;
-        mbar_wait(&kvempty[s], (u & 1) ^ 1);
-        mbar_expect_tx(&kfull[s], L::KB);
-        for (int kb = 0; kb < NB; ++kb)
-          tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tmkv, &kfull[s], kcol + kb * 64,
-                      krow + j * 64);
-        mbar_expect_tx(&vfull[s], L::KB);
-        for (int kb = 0; kb < NB; ++kb)
-          tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tmkv, &vfull[s], vcol + kb * 64,
-                      krow + j * 64);
+      int g = 0, n = 0;  // blocks / items this CTA has loaded
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
+        const FwdItem w = fwd_item(a, item);
+        const int qrow = w.b * krow_of + w.i * 128, krow = w.b * krow_of;
+        const int kcol = a.H * HD + w.kvh * HD, vcol = (a.H + a.KVH) * HD + w.kvh * HD;
+        spin_wait(qempty, (n & 1) ^ 1);
+        mbar_expect_tx(qfull, 2 * L::QT);
+        for (int t = 0; t < 2; ++t)
+          for (int kb = 0; kb < NB; ++kb)
+            tma_load_2d(sm + L::Q0 + t * L::QT + kb * kBlk128, &tmq, qfull,
+                        (w.h0 + t) * HD + kb * 64, qrow);
+        for (int j = 0; j < w.nb; ++j, ++g) {
+          const int s = g % NS, u = g / NS;
+          spin_wait(&kvempty[s], (u & 1) ^ 1);
+          mbar_expect_tx(&kfull[s], L::KB);
+          for (int kb = 0; kb < NB; ++kb)
+            tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tmkv, &kfull[s], kcol + kb * 64,
+                        krow + j * 64);
+          mbar_expect_tx(&vfull[s], L::KB);
+          for (int kb = 0; kb < NB; ++kb)
+            tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tmkv, &vfull[s], vcol + kb * 64,
+                        krow + j * 64);
+        }
       }
     }
   } else if (warp == 1) {
@@ -262,28 +294,36 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
                     (j > 0 || kk > 0) ? 1u : 0u);
         umma_commit(&ofull[t]);
       };
-      mbar_wait(qfull, 0);
-      mbar_wait(&kfull[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      for (int j = 0; j < nb; ++j) {
-        const int s = j % NS, u = j / NS;
-        const int s1 = (j + 1) % NS, u1 = (j + 1) / NS;
-        mbar_wait(&vfull[s], u & 1);
-        mbar_wait(&pfull[0], j & 1);
+      int g = 0, n = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
+        const int nb = fwd_item(a, item).nb;
+        spin_wait(qfull, n & 1);
+        spin_wait(&kfull[g % NS], (g / NS) & 1);
         tc_fence_after();
-        issue_pv(0, s, j);
-        if (j + 1 < nb) {
-          mbar_wait(&kfull[s1], u1 & 1);
+        // S of block 0: the S buffers were released by the previous item's last pfull waits
+        issue_s(0, g % NS);
+        issue_s(1, g % NS);
+        for (int j = 0; j < nb; ++j, ++g) {
+          const int s = g % NS, u = g / NS;
+          const int s1 = (g + 1) % NS, u1 = (g + 1) / NS;
+          spin_wait(&vfull[s], u & 1);
+          if (j == 0 && n > 0) spin_wait(&oempty[0], (n - 1) & 1);  // O_A read out
+          spin_wait(&pfull[0], g & 1);
           tc_fence_after();
-          issue_s(0, s1);
+          issue_pv(0, s, j);
+          if (j + 1 < nb) {
+            spin_wait(&kfull[s1], u1 & 1);
+            tc_fence_after();
+            issue_s(0, s1);
+          }
+          if (j == 0 && n > 0) spin_wait(&oempty[1], (n - 1) & 1);  // O_B read out
+          spin_wait(&pfull[1], g & 1);
+          tc_fence_after();
+          issue_pv(1, s, j);
+          umma_commit(&kvempty[s]);
+          if (j + 1 < nb) issue_s(1, s1);
+          if (j + 2 == nb) umma_commit(qempty);  // the item's last S MMAs were just issued
         }
-        mbar_wait(&pfull[1], j & 1);
-        tc_fence_after();
-        issue_pv(1, s, j);
-        umma_commit(&kvempty[s]);
-        if (j + 1 < nb) issue_s(1, s1);
       }
     }
   } else {
@@ -301,97 +341,107 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     float* xch = reinterpret_cast<float*>(sm + L::XCH);  // [2 parity][2 heads][2 halves][128]
     auto slot = [&](int par, int half) { return xch + ((par * 2 + t) * 2 + half) * 128 + r; };
     const float c = a.scale_log2;
-    const int qpos = i * 128 + r;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nb; ++j) {
-      mbar_wait(&sfull[t], j & 1);
-      tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(tS, v);
-      tmem_wait_ld();
-      const bool diag = j * 64 + 63 > i * 128;  // block reaches past this tile's first row
-      const int lim = qpos - j * 64 - hf * 32;   // columns e <= lim are visible
-      float mx = -INFINITY;
-      if (!diag) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, f32(v[e]));
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (e <= lim) mx = fmaxf(mx, f32(v[e]));
-      }
-      *slot(j & 1, hf) = mx;
-      named_bar_sync(1 + t, 256);
-      mx = fmaxf(mx, *slot(j & 1, hf ^ 1));
-      const float m_new = fmaxf(m, mx * c);
-      if (j > 0) {  // PV of the previous block done: P buffer and O free
-        mbar_wait(&ofull[t], (j - 1) & 1);
+    int g = 0, xp = 0;  // blocks seen, exchange parity
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const FwdItem w = fwd_item(a, item);
+      const int qpos = w.i * 128 + r;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < w.nb; ++j, ++g) {
+        spin_wait(&sfull[t], g & 1);
         tc_fence_after();
-      }
-      if (j == 0) {
-        m = m_new;
-      } else if (__any_sync(0xffffffffu, m_new > m + 8.f)) {
-        const float alpha = ex2(m - m_new);
-        l *= alpha;
-        m = m_new;
+        uint32_t v[32];
+        tmem_ld32(tS, v);
+        tmem_wait_ld();
+        const bool diag = j * 64 + 63 > w.i * 128;  // block reaches past this tile's first row
+        const int lim = qpos - j * 64 - hf * 32;     // columns e <= lim are visible
+        float mx = -INFINITY;
+        if (!diag) {
 #pragma unroll
-        for (int cc = 0; cc < HD / 64; ++cc) {
-          uint32_t o[32];
-          tmem_ld32(tO + cc * 32, o);
-          tmem_wait_ld();
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, f32(v[e]));
+        } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(f32(o[e]) * alpha);
-          tmem_st32(tO + cc * 32, o);
+          for (int e = 0; e < 32; ++e)
+            if (e <= lim) mx = fmaxf(mx, f32(v[e]));
         }
-        tmem_wait_st();
-      }
-      tmem_ld32(tS, v);  // reload (S is still in TMEM): keeps v dead across the rescale
-      tmem_wait_ld();
-      float pr[32];
-      const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
-#pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        const float2 x = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
-        pr[e] = x.x;
-        pr[e + 1] = x.y;
-      }
-      if (!diag) {
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          pr[e] = ex2_mix<0>(pr[e]);
-          pr[e + 1] = ex2_mix<1>(pr[e + 1]);
-          pr[e + 2] = ex2_mix<2>(pr[e + 2]);
-          pr[e + 3] = ex2_mix<3>(pr[e + 3]);
+        *slot(xp, hf) = mx;
+        named_bar_sync(1 + t, 256);
+        mx = fmaxf(mx, *slot(xp, hf ^ 1));
+        xp ^= 1;
+        const float m_new = fmaxf(m, mx * c);
+        if (g > 0) {  // the previous block's PV done: P buffer (and, within an item, O) free
+          spin_wait(&ofull[t], (g - 1) & 1);
+          tc_fence_after();
         }
-      } else {
+        if (j == 0) {
+          m = m_new;
+        } else if (__any_sync(0xffffffffu, m_new > m + 8.f)) {
+          const float alpha = ex2(m - m_new);
+          l *= alpha;
+          m = m_new;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) pr[e] = e <= lim ? ex2(pr[e]) : 0.f;
+          for (int cc = 0; cc < HD / 64; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(tO + cc * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(f32(o[e]) * alpha);
+            tmem_st32(tO + cc * 32, o);
+          }
+          tmem_wait_st();
+        }
+        tmem_ld32(tS, v);  // reload (S is still in TMEM): keeps v dead across the rescale
+        tmem_wait_ld();
+        float pr[32];
+        const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float2 x = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
+          pr[e] = x.x;
+          pr[e + 1] = x.y;
+        }
+        if (!diag) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            pr[e] = ex2_mix<0>(pr[e]);
+            pr[e + 1] = ex2_mix<1>(pr[e + 1]);
+            pr[e + 2] = ex2_mix<2>(pr[e + 2]);
+            pr[e + 3] = ex2_mix<3>(pr[e + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) pr[e] = e <= lim ? ex2(pr[e]) : 0.f;
+        }
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) acc = __fadd2_rn(acc, make_float2(pr[e], pr[e + 1]));
+        l += acc.x + acc.y;
+        st_swz32(sP, r, hf * 4, pr);
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(&pfull[t]);
       }
-      float2 acc = make_float2(0.f, 0.f);
+      // l of the whole row = the two halves' sums (same running max)
+      *slot(xp, hf) = l;
+      named_bar_sync(1 + t, 256);
+      l += *slot(xp, hf ^ 1);
+      xp ^= 1;
+      spin_wait(&ofull[t], (g - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      bf16* out = a.o + static_cast<long long>(w.b * krow_of + qpos) * a.ldo + (w.h0 + t) * HD +
+                  hf * (HD / 2);
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) acc = __fadd2_rn(acc, make_float2(pr[e], pr[e + 1]));
-      l += acc.x + acc.y;
-      st_swz32(sP, r, hf * 4, pr);
-      fence_async_smem();
+      for (int cc = 0; cc < HD / 64; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(tO + cc * 32, o);
+        tmem_wait_ld();
+        st_row32(out + cc * 32, o, inv);
+      }
       tc_fence_before();
-      mbar_arrive(&pfull[t]);
+      mbar_arrive(&oempty[t]);
+      if (hf == 0)
+        a.lse[(static_cast<long long>(w.b) * a.H + w.h0 + t) * a.S + qpos] = m + __log2f(l);
     }
-    // l of the whole row = the two halves' sums (same running max)
-    *slot(nb & 1, hf) = l;
-    named_bar_sync(1 + t, 256);
-    l += *slot(nb & 1, hf ^ 1);
-    mbar_wait(&ofull[t], (nb - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    bf16* out = a.o + static_cast<long long>(qrow + r) * a.ldo + (h0 + t) * HD + hf * (HD / 2);
-#pragma unroll
-    for (int cc = 0; cc < HD / 64; ++cc) {
-      uint32_t o[32];
-      tmem_ld32(tO + cc * 32, o);
-      tmem_wait_ld();
-      st_row32(out + cc * 32, o, inv);
-    }
-    if (hf == 0) a.lse[(static_cast<long long>(b) * a.H + h0 + t) * a.S + qpos] = m + __log2f(l);
   }
   tc_fence_before();
   __syncthreads();
@@ -494,7 +544,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int jj = 0; jj < n; ++jj) {
         const int s = jj % NS, u = jj / NS;
         const int kr = b * a.S + jj * 64;
-        mbar_wait(&kvempty[s], (u & 1) ^ 1);
+        spin_wait(&kvempty[s], (u & 1) ^ 1);
         mbar_expect_tx(&kvfull[s], 2 * L::KB);
         for (int kb = 0; kb < NB; ++kb) {
           tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], kcol + kb * 64, kr);
@@ -508,7 +558,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t ID_Q = idesc_bf16_f32(128, HD, false, true);
       auto issue_s = [&](int jj) {
         const int s = jj % NS, u = jj / NS, ts = jj & 1;
-        mbar_wait(&kvfull[s], u & 1);
+        spin_wait(&kvfull[s], u & 1);
         tc_fence_after();
         const uint8_t* k = sm + L::K0 + s * L::KB;
         const uint8_t* v = sm + L::V0 + s * L::KB;
@@ -520,12 +570,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         umma_commit(&tfull[ts]);
       };
-      mbar_wait(qfull, 0);
+      spin_wait(qfull, 0);
       issue_s(0);
       if (n > 1) issue_s(1);
       for (int jj = 0; jj < n; ++jj) {
         const int s = jj % NS, ts = jj & 1, v = jj >> 1;
-        mbar_wait(&pfull[ts], v & 1);
+        spin_wait(&pfull[ts], v & 1);
         tc_fence_after();
         const uint8_t* k = sm + L::K0 + s * L::KB;
         const uint8_t* ds = sm + L::DS0 + ts * L::SB;
@@ -551,7 +601,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const float c = a.scale_log2;
     // D of this row from the staged dO and O tiles (both halves form it; the dS writes below
     // reuse the O staging bytes, so the row's two threads sync before the first one)
-    mbar_wait(qfull, 0);
+    spin_wait(qfull, 0);
     float dd = 0.f;
 #pragma unroll
     for (int kb = 0; kb < NB; ++kb) {
@@ -574,8 +624,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse, -lse), nd2 = make_float2(-dd, -dd);
     for (int jj = 0; jj < n; ++jj) {
       const int ts = jj & 1, v = jj >> 1;
-      mbar_wait(&tfull[ts], v & 1);
-      if (jj >= 2) mbar_wait(&pfree[ts], (v & 1) ^ 1);  // dS stage free
+      spin_wait(&tfull[ts], v & 1);
+      if (jj >= 2) spin_wait(&pfree[ts], (v & 1) ^ 1);  // dS stage free
       tc_fence_after();
       uint8_t* ds = sm + L::DS0 + ts * L::SB;
       uint32_t vs[32], vp[32];
@@ -615,7 +665,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&pfull[ts]);
     }
-    mbar_wait(done, 0);
+    spin_wait(done, 0);
     tc_fence_after();
     bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD + hf * (HD / 2);
 #pragma unroll
@@ -715,7 +765,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int s = it % NS, u = it / NS;
         const int h = kvh * G + it / nper, qb = 2 * j + it % nper;
         const int qr = b * a.S + qb * 64;
-        mbar_wait(&qempty[s], (u & 1) ^ 1);
+        spin_wait(&qempty[s], (u & 1) ^ 1);
         mbar_expect_tx(&qfull[s], 2 * L::QB + 512);
         for (int kb = 0; kb < NB; ++kb) {
           tma_load_2d(sm + L::Q0 + s * L::QB + kb * kBlk64, &tm64, &qfull[s], h * HD + kb * 64, qr);
@@ -732,7 +782,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t ID_A = idesc_bf16_f32(128, HD, false, true);
       auto issue_s = [&](int it) {
         const int s = it % NS, u = it / NS, ts = it & 1;
-        mbar_wait(&qfull[s], u & 1);
+        spin_wait(&qfull[s], u & 1);
         tc_fence_after();
         const uint8_t* q = sm + L::Q0 + s * L::QB;
         const uint8_t* d = sm + L::DO0 + s * L::QB;
@@ -743,12 +793,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         umma_commit(&tfull[ts]);
       };
-      mbar_wait(kvfull, 0);
+      spin_wait(kvfull, 0);
       issue_s(0);
       if (n_it > 1) issue_s(1);
       for (int it = 0; it < n_it; ++it) {
         const int s = it % NS, ts = it & 1, v = it >> 1;
-        mbar_wait(&pfull[ts], v & 1);
+        spin_wait(&pfull[ts], v & 1);
         tc_fence_after();
         const uint8_t* q = sm + L::Q0 + s * L::QB;
         const uint8_t* d = sm + L::DO0 + s * L::QB;
@@ -778,9 +828,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int it = 0; it < n_it; ++it) {
       const int s = it % NS, u = it / NS, ts = it & 1, v = it >> 1;
       const int qb = 2 * j + it % nper;
-      mbar_wait(&tfull[ts], v & 1);
-      mbar_wait(&qfull[s], u & 1);  // lse / D of the block
-      if (it >= 2) mbar_wait(&pfree[ts], (v & 1) ^ 1);  // P^T / dS^T stage free
+      spin_wait(&tfull[ts], v & 1);
+      spin_wait(&qfull[s], u & 1);  // lse / D of the block
+      if (it >= 2) spin_wait(&pfree[ts], (v & 1) ^ 1);  // P^T / dS^T stage free
       tc_fence_after();
       const float* sl = reinterpret_cast<const float*>(sm + L::LSE0 + s * 256) + hf * 32;
       const float* sd = reinterpret_cast<const float*>(sm + L::D0 + s * 256) + hf * 32;
@@ -826,7 +876,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&pfull[ts]);
     }
-    mbar_wait(done, 0);
+    spin_wait(done, 0);
     tc_fence_after();
     bf16* drow = a.dqkv + static_cast<long long>(kvrow + r) * a.ld + hf * (HD / 2);
 #pragma unroll
@@ -895,8 +945,9 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
     set_smem(attn_fwd_kernel<HD>, FwdSmem<HD>::BYTES);
     attr = true;
   }
-  const int grid = (S / 128) * B * KVH * (H / KVH / 2);
-  attn_fwd_kernel<HD><<<grid, kFwdThreads, std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(mq, mkv, a);
+  const int items = (S / 128) * B * KVH * (H / KVH / 2);
+  attn_fwd_kernel<HD><<<std::min(items, num_sms()), kFwdThreads,
+                        std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(mq, mkv, a, items);
   check_launch("attn_fwd_kernel");
 }
 
