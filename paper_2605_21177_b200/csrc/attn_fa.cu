@@ -212,11 +212,11 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
   uint64_t* kfull = bar + 2;            // [NS]
   uint64_t* vfull = bar + 2 + NS;       // [NS]
   uint64_t* kvempty = bar + 2 + 2 * NS; // [NS]
-  uint64_t* sfull = bar + 2 + 3 * NS;   // [2] per head
-  uint64_t* pfull = sfull + 2;          // [2]
-  uint64_t* ofull = sfull + 4;          // [2]
-  uint64_t* oempty = sfull + 6;         // [2] O read out by the epilogue
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfull + 8);
+  uint64_t* sfull = bar + 2 + 3 * NS;   // [2 heads][2 buffers]
+  uint64_t* pfull = sfull + 4;          // [2]
+  uint64_t* ofull = sfull + 6;          // [2]
+  uint64_t* oempty = sfull + 8;         // [2] O read out by the epilogue
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfull + 10);
 
   const int krow_of = a.S;  // rows per sequence
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -232,7 +232,8 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
       mbar_init(&kvempty[s], 1);
     }
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&sfull[t], 1);
+      mbar_init(&sfull[2 * t], 1);
+      mbar_init(&sfull[2 * t + 1], 1);
       mbar_init(&pfull[t], 256);
       mbar_init(&ofull[t], 1);
       mbar_init(&oempty[t], 256);
@@ -244,7 +245,8 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: S_A [0, 64), S_B [64, 128), O_A [128, 128 + HD), O_B [128 + HD, 128 + 2 HD)
+  // TMEM: S of head t, buffer u at [64 (2 t + u), +64) -- the MMA runs two key blocks ahead of
+  // the softmax; O_A [256, 256 + HD), O_B [256 + HD, 256 + 2 HD)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -277,52 +279,56 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     if (lane == 0) {
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_O = idesc_bf16_f32(128, HD, false, true);
-      auto issue_s = [&](int t, int s) {
+      // S of block g (head t) into buffer g & 1
+      auto issue_s = [&](int t, int g) {
         const uint8_t* q = sm + L::Q0 + t * L::QT;
-        const uint8_t* k = sm + L::K0 + s * L::KB;
+        const uint8_t* k = sm + L::K0 + (g % NS) * L::KB;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
-          umma_bf16(tbase + t * 64, desc_k(q, kk, kBlk128), desc_k(k, kk, kBlk64), ID_S, kk > 0);
-        umma_commit(&sfull[t]);
+          umma_bf16(tbase + (2 * t + (g & 1)) * 64, desc_k(q, kk, kBlk128), desc_k(k, kk, kBlk64),
+                    ID_S, kk > 0);
+        umma_commit(&sfull[2 * t + (g & 1)]);
       };
       auto issue_pv = [&](int t, int s, int j) {
         const uint8_t* p = sm + L::P0 + t * L::PB;
         const uint8_t* v = sm + L::V0 + s * L::KB;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          umma_bf16(tbase + 128 + t * HD, desc_k(p, kk, kBlk128), desc_mn(v, kk, kBlk64), ID_O,
+          umma_bf16(tbase + 256 + t * HD, desc_k(p, kk, kBlk128), desc_mn(v, kk, kBlk64), ID_O,
                     (j > 0 || kk > 0) ? 1u : 0u);
         umma_commit(&ofull[t]);
       };
       int g = 0, n = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
-        const int nb = fwd_item(a, item).nb;
+        const int nb = fwd_item(a, item).nb;  // >= 2
         spin_wait(qfull, n & 1);
-        spin_wait(&kfull[g % NS], (g / NS) & 1);
-        tc_fence_after();
-        // S of block 0: the S buffers were released by the previous item's last pfull waits
-        issue_s(0, g % NS);
-        issue_s(1, g % NS);
+        // S of blocks 0 and 1: their buffers were released by the previous item's pfull waits
+        for (int q = 0; q < 2; ++q) {
+          spin_wait(&kfull[(g + q) % NS], ((g + q) / NS) & 1);
+          tc_fence_after();
+          issue_s(0, g + q);
+          issue_s(1, g + q);
+        }
+        const int q_last = nb >= 3 ? nb - 3 : 0;  // iteration that issues the item's last S
         for (int j = 0; j < nb; ++j, ++g) {
           const int s = g % NS, u = g / NS;
-          const int s1 = (g + 1) % NS, u1 = (g + 1) / NS;
           spin_wait(&vfull[s], u & 1);
           if (j == 0 && n > 0) spin_wait(&oempty[0], (n - 1) & 1);  // O_A read out
           spin_wait(&pfull[0], g & 1);
           tc_fence_after();
           issue_pv(0, s, j);
-          if (j + 1 < nb) {
-            spin_wait(&kfull[s1], u1 & 1);
+          if (j + 2 < nb) {  // softmax A is done with buffer g & 1
+            spin_wait(&kfull[(g + 2) % NS], ((g + 2) / NS) & 1);
             tc_fence_after();
-            issue_s(0, s1);
+            issue_s(0, g + 2);
           }
           if (j == 0 && n > 0) spin_wait(&oempty[1], (n - 1) & 1);  // O_B read out
           spin_wait(&pfull[1], g & 1);
           tc_fence_after();
           issue_pv(1, s, j);
           umma_commit(&kvempty[s]);
-          if (j + 1 < nb) issue_s(1, s1);
-          if (j + 2 == nb) umma_commit(qempty);  // the item's last S MMAs were just issued
+          if (j + 2 < nb) issue_s(1, g + 2);
+          if (j == q_last) umma_commit(qempty);
         }
       }
     }
@@ -335,8 +341,8 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tS = tbase + lo + t * 64 + hf * 32;
-    const uint32_t tO = tbase + lo + 128 + t * HD + hf * (HD / 2);
+    const uint32_t tS0 = tbase + lo + 2 * t * 64 + hf * 32;
+    const uint32_t tO = tbase + lo + 256 + t * HD + hf * (HD / 2);
     uint8_t* sP = sm + L::P0 + t * L::PB;
     float* xch = reinterpret_cast<float*>(sm + L::XCH);  // [2 parity][2 heads][2 halves][128]
     auto slot = [&](int par, int half) { return xch + ((par * 2 + t) * 2 + half) * 128 + r; };
@@ -347,8 +353,9 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
       const int qpos = w.i * 128 + r;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < w.nb; ++j, ++g) {
-        spin_wait(&sfull[t], g & 1);
+        spin_wait(&sfull[2 * t + (g & 1)], (g >> 1) & 1);
         tc_fence_after();
+        const uint32_t tS = tS0 + (g & 1) * 64;
         uint32_t v[32];
         tmem_ld32(tS, v);
         tmem_wait_ld();
