@@ -165,15 +165,18 @@ struct FwdArgs {
 
 // ------------------------------------------------------------------------------------------
 // forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-9 softmax of head A, 10-17 of B.
-// Key / value blocks of 64 rows in a 3-deep ring; S of each head 128 x 64 in TMEM.
+// 64-row key blocks.  K ring of 2 (freed by the S MMAs), V ring of 3 (freed by the PV MMAs),
+// P double-buffered per head, S double-buffered per head in TMEM: the MMA thread issues S two
+// blocks ahead of the softmax, so a softmax warp waits only for its own previous block's P
+// buffer (two blocks back) and, rarely, for the O rescale.
 template <int HD>
 struct FwdSmem {
-  static constexpr int NS = 3;
+  static constexpr int NK = 2, NV = 3;
   static constexpr uint32_t QT = 128 * HD * 2;  // query tile
   static constexpr uint32_t KB = 64 * HD * 2;   // key or value block
   static constexpr uint32_t PB = 128 * 64 * 2;  // P block (bf16)
-  static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NS * KB, P0 = V0 + NS * KB,
-                            XCH = P0 + 2 * PB, BAR = XCH + 8 * 128 * 4;
+  static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NK * KB, P0 = V0 + NV * KB,
+                            XCH = P0 + 4 * PB, BAR = XCH + 8 * 128 * 4;
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
@@ -194,7 +197,7 @@ __device__ __forceinline__ FwdItem fwd_item(const FwdArgs& a, int item) {
   w.b = rest / (a.KVH * G2);
   w.kvh = (rest / G2) % a.KVH;
   w.h0 = w.kvh * G + 2 * (rest % G2);
-  w.nb = 2 * w.i + 2;  // 64-row key blocks up to the diagonal
+  w.nb = 2 * w.i + 2;  // 64-row key blocks up to the diagonal (>= 2)
   return w;
 }
 
@@ -203,22 +206,22 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv,
                     const FwdArgs a, int n_items) {
   using L = FwdSmem<HD>;
-  constexpr int NB = HD / 64, NS = L::NS;
+  constexpr int NB = HD / 64, NK = L::NK, NV = L::NV;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* qfull = bar;
   uint64_t* qempty = bar + 1;
-  uint64_t* kfull = bar + 2;            // [NS]
-  uint64_t* vfull = bar + 2 + NS;       // [NS]
-  uint64_t* kvempty = bar + 2 + 2 * NS; // [NS]
-  uint64_t* sfull = bar + 2 + 3 * NS;   // [2 heads][2 buffers]
-  uint64_t* pfull = sfull + 4;          // [2]
-  uint64_t* ofull = sfull + 6;          // [2]
-  uint64_t* oempty = sfull + 8;         // [2] O read out by the epilogue
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfull + 10);
+  uint64_t* kfull = bar + 2;             // [NK]
+  uint64_t* kempty = kfull + NK;         // [NK]
+  uint64_t* vfull = kempty + NK;         // [NV]
+  uint64_t* vempty = vfull + NV;         // [NV]
+  uint64_t* sfull = vempty + NV;         // [2 heads][2 buffers]
+  uint64_t* pfull = sfull + 4;           // [2][2]
+  uint64_t* ofull = sfull + 8;           // [2][2] PV of the block using P buffer u done
+  uint64_t* oempty = sfull + 12;         // [2] O read out by the epilogue
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfull + 14);
 
-  const int krow_of = a.S;  // rows per sequence
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (threadIdx.x == 0) {
@@ -226,18 +229,21 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     tma_prefetch(&tmkv);
     mbar_init(qfull, 1);
     mbar_init(qempty, 1);
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < NK; ++s) {
       mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
+    }
+    for (int s = 0; s < NV; ++s) {
       mbar_init(&vfull[s], 1);
-      mbar_init(&kvempty[s], 1);
+      mbar_init(&vempty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&sfull[2 * t], 1);
-      mbar_init(&sfull[2 * t + 1], 1);
-      mbar_init(&pfull[t], 256);
-      mbar_init(&ofull[t], 1);
-      mbar_init(&oempty[t], 256);
+    for (int k = 0; k < 4; ++k) {
+      mbar_init(&sfull[k], 1);
+      mbar_init(&pfull[k], 256);
+      mbar_init(&ofull[k], 1);
     }
+    mbar_init(&oempty[0], 256);
+    mbar_init(&oempty[1], 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -245,33 +251,42 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: S of head t, buffer u at [64 (2 t + u), +64) -- the MMA runs two key blocks ahead of
-  // the softmax; O_A [256, 256 + HD), O_B [256 + HD, 256 + 2 HD)
+  // TMEM: S of head t, buffer u at [64 (2 t + u), +64); O_A [256, 256 + HD), O_B [256 + HD, +HD)
 
   if (warp == 0) {
     if (lane == 0) {
-      int g = 0, n = 0;  // blocks / items this CTA has loaded
+      // issue order per item: Q, K0, K1, V0, K2, V1, ... (keys one block ahead of values)
+      int gk = 0, gv = 0, n = 0;
+      auto load_k = [&](const FwdItem& w, int j) {
+        const int s = gk % NK;
+        spin_wait(&kempty[s], ((gk / NK) & 1) ^ 1);
+        mbar_expect_tx(&kfull[s], L::KB);
+        for (int kb = 0; kb < NB; ++kb)
+          tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tmkv, &kfull[s],
+                      a.H * HD + w.kvh * HD + kb * 64, w.b * a.S + j * 64);
+        ++gk;
+      };
+      auto load_v = [&](const FwdItem& w, int j) {
+        const int s = gv % NV;
+        spin_wait(&vempty[s], ((gv / NV) & 1) ^ 1);
+        mbar_expect_tx(&vfull[s], L::KB);
+        for (int kb = 0; kb < NB; ++kb)
+          tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tmkv, &vfull[s],
+                      (a.H + a.KVH) * HD + w.kvh * HD + kb * 64, w.b * a.S + j * 64);
+        ++gv;
+      };
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
         const FwdItem w = fwd_item(a, item);
-        const int qrow = w.b * krow_of + w.i * 128, krow = w.b * krow_of;
-        const int kcol = a.H * HD + w.kvh * HD, vcol = (a.H + a.KVH) * HD + w.kvh * HD;
         spin_wait(qempty, (n & 1) ^ 1);
         mbar_expect_tx(qfull, 2 * L::QT);
         for (int t = 0; t < 2; ++t)
           for (int kb = 0; kb < NB; ++kb)
             tma_load_2d(sm + L::Q0 + t * L::QT + kb * kBlk128, &tmq, qfull,
-                        (w.h0 + t) * HD + kb * 64, qrow);
-        for (int j = 0; j < w.nb; ++j, ++g) {
-          const int s = g % NS, u = g / NS;
-          spin_wait(&kvempty[s], (u & 1) ^ 1);
-          mbar_expect_tx(&kfull[s], L::KB);
-          for (int kb = 0; kb < NB; ++kb)
-            tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tmkv, &kfull[s], kcol + kb * 64,
-                        krow + j * 64);
-          mbar_expect_tx(&vfull[s], L::KB);
-          for (int kb = 0; kb < NB; ++kb)
-            tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tmkv, &vfull[s], vcol + kb * 64,
-                        krow + j * 64);
+                        (w.h0 + t) * HD + kb * 64, w.b * a.S + w.i * 128);
+        load_k(w, 0);
+        for (int j = 0; j < w.nb; ++j) {
+          if (j + 1 < w.nb) load_k(w, j + 1);
+          load_v(w, j);
         }
       }
     }
@@ -279,54 +294,56 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     if (lane == 0) {
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_O = idesc_bf16_f32(128, HD, false, true);
-      // S of block g (head t) into buffer g & 1
+      // S of block g (head t) into buffer g & 1; the K slot is released after head B's S
       auto issue_s = [&](int t, int g) {
         const uint8_t* q = sm + L::Q0 + t * L::QT;
-        const uint8_t* k = sm + L::K0 + (g % NS) * L::KB;
+        const uint8_t* k = sm + L::K0 + (g % NK) * L::KB;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
           umma_bf16(tbase + (2 * t + (g & 1)) * 64, desc_k(q, kk, kBlk128), desc_k(k, kk, kBlk64),
                     ID_S, kk > 0);
         umma_commit(&sfull[2 * t + (g & 1)]);
+        if (t == 1) umma_commit(&kempty[g % NK]);
       };
-      auto issue_pv = [&](int t, int s, int j) {
-        const uint8_t* p = sm + L::P0 + t * L::PB;
-        const uint8_t* v = sm + L::V0 + s * L::KB;
+      auto issue_pv = [&](int t, int g, int j) {
+        const uint8_t* p = sm + L::P0 + (2 * t + (g & 1)) * L::PB;
+        const uint8_t* v = sm + L::V0 + (g % NV) * L::KB;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           umma_bf16(tbase + 256 + t * HD, desc_k(p, kk, kBlk128), desc_mn(v, kk, kBlk64), ID_O,
                     (j > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&ofull[t]);
+        umma_commit(&ofull[2 * t + (g & 1)]);
+        if (t == 1) umma_commit(&vempty[g % NV]);
+      };
+      auto wait_k = [&](int g) {
+        spin_wait(&kfull[g % NK], (g / NK) & 1);
+        tc_fence_after();
       };
       int g = 0, n = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
-        const int nb = fwd_item(a, item).nb;  // >= 2
+        const int nb = fwd_item(a, item).nb;
         spin_wait(qfull, n & 1);
-        // S of blocks 0 and 1: their buffers were released by the previous item's pfull waits
+        // S of blocks 0 and 1 (their S buffers were released by the previous item's pfull)
         for (int q = 0; q < 2; ++q) {
-          spin_wait(&kfull[(g + q) % NS], ((g + q) / NS) & 1);
-          tc_fence_after();
+          wait_k(g + q);
           issue_s(0, g + q);
           issue_s(1, g + q);
         }
         const int q_last = nb >= 3 ? nb - 3 : 0;  // iteration that issues the item's last S
         for (int j = 0; j < nb; ++j, ++g) {
-          const int s = g % NS, u = g / NS;
-          spin_wait(&vfull[s], u & 1);
+          spin_wait(&vfull[g % NV], (g / NV) & 1);
           if (j == 0 && n > 0) spin_wait(&oempty[0], (n - 1) & 1);  // O_A read out
-          spin_wait(&pfull[0], g & 1);
+          spin_wait(&pfull[g & 1], (g >> 1) & 1);
           tc_fence_after();
-          issue_pv(0, s, j);
-          if (j + 2 < nb) {  // softmax A is done with buffer g & 1
-            spin_wait(&kfull[(g + 2) % NS], ((g + 2) / NS) & 1);
-            tc_fence_after();
+          issue_pv(0, g, j);
+          if (j + 2 < nb) {  // softmax A is done with S buffer g & 1
+            wait_k(g + 2);
             issue_s(0, g + 2);
           }
           if (j == 0 && n > 0) spin_wait(&oempty[1], (n - 1) & 1);  // O_B read out
-          spin_wait(&pfull[1], g & 1);
+          spin_wait(&pfull[2 + (g & 1)], (g >> 1) & 1);
           tc_fence_after();
-          issue_pv(1, s, j);
-          umma_commit(&kvempty[s]);
+          issue_pv(1, g, j);
           if (j + 2 < nb) issue_s(1, g + 2);
           if (j == q_last) umma_commit(qempty);
         }
@@ -343,7 +360,6 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t tS0 = tbase + lo + 2 * t * 64 + hf * 32;
     const uint32_t tO = tbase + lo + 256 + t * HD + hf * (HD / 2);
-    uint8_t* sP = sm + L::P0 + t * L::PB;
     float* xch = reinterpret_cast<float*>(sm + L::XCH);  // [2 parity][2 heads][2 halves][128]
     auto slot = [&](int par, int half) { return xch + ((par * 2 + t) * 2 + half) * 128 + r; };
     const float c = a.scale_log2;
@@ -353,9 +369,10 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
       const int qpos = w.i * 128 + r;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < w.nb; ++j, ++g) {
-        spin_wait(&sfull[2 * t + (g & 1)], (g >> 1) & 1);
+        const int u = g & 1;
+        spin_wait(&sfull[2 * t + u], (g >> 1) & 1);
         tc_fence_after();
-        const uint32_t tS = tS0 + (g & 1) * 64;
+        const uint32_t tS = tS0 + u * 64;
         uint32_t v[32];
         tmem_ld32(tS, v);
         tmem_wait_ld();
@@ -375,13 +392,12 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
         mx = fmaxf(mx, *slot(xp, hf ^ 1));
         xp ^= 1;
         const float m_new = fmaxf(m, mx * c);
-        if (g > 0) {  // the previous block's PV done: P buffer (and, within an item, O) free
-          spin_wait(&ofull[t], (g - 1) & 1);
-          tc_fence_after();
-        }
         if (j == 0) {
           m = m_new;
         } else if (__any_sync(0xffffffffu, m_new > m + 8.f)) {
+          // O must hold every PV up to the previous block before it is rescaled
+          spin_wait(&ofull[2 * t + (u ^ 1)], ((g - 1) >> 1) & 1);
+          tc_fence_after();
           const float alpha = ex2(m - m_new);
           l *= alpha;
           m = m_new;
@@ -422,20 +438,22 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
 #pragma unroll
         for (int e = 0; e < 32; e += 2) acc = __fadd2_rn(acc, make_float2(pr[e], pr[e + 1]));
         l += acc.x + acc.y;
-        st_swz32(sP, r, hf * 4, pr);
+        // P buffer u was last read by the PV two blocks back
+        if (g >= 2) spin_wait(&ofull[2 * t + u], ((g - 2) >> 1) & 1);
+        st_swz32(sm + L::P0 + (2 * t + u) * L::PB, r, hf * 4, pr);
         fence_async_smem();
         tc_fence_before();
-        mbar_arrive(&pfull[t]);
+        mbar_arrive(&pfull[2 * t + u]);
       }
       // l of the whole row = the two halves' sums (same running max)
       *slot(xp, hf) = l;
       named_bar_sync(1 + t, 256);
       l += *slot(xp, hf ^ 1);
       xp ^= 1;
-      spin_wait(&ofull[t], (g - 1) & 1);
+      spin_wait(&ofull[2 * t + ((g - 1) & 1)], ((g - 1) >> 1) & 1);
       tc_fence_after();
       const float inv = 1.f / l;
-      bf16* out = a.o + static_cast<long long>(w.b * krow_of + qpos) * a.ldo + (w.h0 + t) * HD +
+      bf16* out = a.o + static_cast<long long>(w.b * a.S + qpos) * a.ldo + (w.h0 + t) * HD +
                   hf * (HD / 2);
 #pragma unroll
       for (int cc = 0; cc < HD / 64; ++cc) {
