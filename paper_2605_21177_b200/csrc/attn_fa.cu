@@ -72,6 +72,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -163,24 +172,34 @@ struct FwdArgs {
   float scale_log2;
 };
 
+// A operand from TMEM (the "ts" form): P is written by the softmax warps into the S columns
+// of its own rows (row m = lane m, two bf16 per 32-bit column, K order), so P.V reads no
+// shared memory for its A side.
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+}
+
 // ------------------------------------------------------------------------------------------
-// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-9 softmax of head A, 10-17 of B.
-// 64-row key blocks.  K ring of 2 (freed by the S MMAs), V ring of 3 (freed by the PV MMAs),
-// P double-buffered per head, S double-buffered per head in TMEM: the MMA thread issues S two
-// blocks ahead of the softmax, so a softmax warp waits only for its own previous block's P
-// buffer (two blocks back) and, rarely, for the O rescale.
+// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax of head A, 6-9 of B.
+// 128-row key blocks (K ring of 2, V ring of 3).  TMEM: S_A, S_B (128 columns each), O_A, O_B;
+// the softmax thread of a row reads its 128 scores, writes P (bf16) into the first 64
+// columns of its own S row, and P.V runs with A from TMEM.  The tensor pipe executes
+// PV_A(j), S_A(j+1), PV_B(j), S_B(j+1): head A's softmax overlaps head B's MMAs and vice versa,
+// and S_t(j+1) completing implies PV_t(j) did (O is safe to rescale, P to overwrite).
 template <int HD>
 struct FwdSmem {
   static constexpr int NK = 2, NV = 3;
-  static constexpr uint32_t QT = 128 * HD * 2;  // query tile
-  static constexpr uint32_t KB = 64 * HD * 2;   // key or value block
-  static constexpr uint32_t PB = 128 * 64 * 2;  // P block (bf16)
-  static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NK * KB, P0 = V0 + NV * KB,
-                            XCH = P0 + 4 * PB, BAR = XCH + 8 * 128 * 4;
+  static constexpr uint32_t QT = 128 * HD * 2;  // query tile / key or value block (128 rows)
+  static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NK * QT, BAR = V0 + NV * QT;
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
-constexpr int kFwdThreads = 64 + 16 * 32;  // TMA warp, MMA warp, 16 softmax warps
+constexpr int kFwdThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 softmax warps
 
 // Work item = (query tile, batch, KV head, head pair), longest query tiles first; a persistent
 // CTA walks items blockIdx.x, +gridDim.x, ...  The next item's Q tiles load while the current
@@ -197,14 +216,13 @@ __device__ __forceinline__ FwdItem fwd_item(const FwdArgs& a, int item) {
   w.b = rest / (a.KVH * G2);
   w.kvh = (rest / G2) % a.KVH;
   w.h0 = w.kvh * G + 2 * (rest % G2);
-  w.nb = 2 * w.i + 2;  // 64-row key blocks up to the diagonal (>= 2)
+  w.nb = w.i + 1;  // 128-row key blocks up to the diagonal
   return w;
 }
 
 template <int HD>
-__global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 32 <= 16K registers
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv,
-                    const FwdArgs a, int n_items) {
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq, const FwdArgs a, int n_items) {
   using L = FwdSmem<HD>;
   constexpr int NB = HD / 64, NK = L::NK, NV = L::NV;
   extern __shared__ uint8_t smem_raw[];
@@ -216,17 +234,16 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
   uint64_t* kempty = kfull + NK;         // [NK]
   uint64_t* vfull = kempty + NK;         // [NV]
   uint64_t* vempty = vfull + NV;         // [NV]
-  uint64_t* sfull = vempty + NV;         // [2 heads][2 buffers]
-  uint64_t* pfull = sfull + 4;           // [2][2]
-  uint64_t* ofull = sfull + 8;           // [2][2] PV of the block using P buffer u done
-  uint64_t* oempty = sfull + 12;         // [2] O read out by the epilogue
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfull + 14);
+  uint64_t* sfull = vempty + NV;         // [2] S_t(j) done (and every earlier MMA)
+  uint64_t* pfull = sfull + 2;           // [2] P_t(j) in TMEM
+  uint64_t* ofull = sfull + 4;           // [2] last PV of an item done
+  uint64_t* oempty = sfull + 6;          // [2] O read out by the epilogue
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfull + 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmq);
-    tma_prefetch(&tmkv);
     mbar_init(qfull, 1);
     mbar_init(qempty, 1);
     for (int s = 0; s < NK; ++s) {
@@ -237,13 +254,12 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
       mbar_init(&vfull[s], 1);
       mbar_init(&vempty[s], 1);
     }
-    for (int k = 0; k < 4; ++k) {
-      mbar_init(&sfull[k], 1);
-      mbar_init(&pfull[k], 256);
-      mbar_init(&ofull[k], 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&sfull[t], 1);
+      mbar_init(&pfull[t], 128);
+      mbar_init(&ofull[t], 1);
+      mbar_init(&oempty[t], 128);
     }
-    mbar_init(&oempty[0], 256);
-    mbar_init(&oempty[1], 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -251,68 +267,57 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: S of head t, buffer u at [64 (2 t + u), +64); O_A [256, 256 + HD), O_B [256 + HD, +HD)
+  // TMEM: S_t at [128 t, +128) (P_t in its first 64 columns), O_t at [256 + HD t, +HD)
 
   if (warp == 0) {
     if (lane == 0) {
       // issue order per item: Q, K0, K1, V0, K2, V1, ... (keys one block ahead of values)
       int gk = 0, gv = 0, n = 0;
-      auto load_k = [&](const FwdItem& w, int j) {
-        const int s = gk % NK;
-        spin_wait(&kempty[s], ((gk / NK) & 1) ^ 1);
-        mbar_expect_tx(&kfull[s], L::KB);
+      auto load_kv = [&](int& gc, int nslots, uint64_t* full, uint64_t* empty, uint32_t base,
+                         int col, int row) {
+        const int s = gc % nslots;
+        spin_wait(&empty[s], ((gc / nslots) & 1) ^ 1);
+        mbar_expect_tx(&full[s], L::QT);
         for (int kb = 0; kb < NB; ++kb)
-          tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tmkv, &kfull[s],
-                      a.H * HD + w.kvh * HD + kb * 64, w.b * a.S + j * 64);
-        ++gk;
-      };
-      auto load_v = [&](const FwdItem& w, int j) {
-        const int s = gv % NV;
-        spin_wait(&vempty[s], ((gv / NV) & 1) ^ 1);
-        mbar_expect_tx(&vfull[s], L::KB);
-        for (int kb = 0; kb < NB; ++kb)
-          tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tmkv, &vfull[s],
-                      (a.H + a.KVH) * HD + w.kvh * HD + kb * 64, w.b * a.S + j * 64);
-        ++gv;
+          tma_load_2d(sm + base + s * L::QT + kb * kBlk128, &tmq, &full[s], col + kb * 64, row);
+        ++gc;
       };
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
         const FwdItem w = fwd_item(a, item);
+        const int kcol = a.H * HD + w.kvh * HD, vcol = (a.H + a.KVH) * HD + w.kvh * HD;
+        const int krow = w.b * a.S;
         spin_wait(qempty, (n & 1) ^ 1);
         mbar_expect_tx(qfull, 2 * L::QT);
         for (int t = 0; t < 2; ++t)
           for (int kb = 0; kb < NB; ++kb)
             tma_load_2d(sm + L::Q0 + t * L::QT + kb * kBlk128, &tmq, qfull,
-                        (w.h0 + t) * HD + kb * 64, w.b * a.S + w.i * 128);
-        load_k(w, 0);
+                        (w.h0 + t) * HD + kb * 64, krow + w.i * 128);
+        load_kv(gk, NK, kfull, kempty, L::K0, kcol, krow);
         for (int j = 0; j < w.nb; ++j) {
-          if (j + 1 < w.nb) load_k(w, j + 1);
-          load_v(w, j);
+          if (j + 1 < w.nb) load_kv(gk, NK, kfull, kempty, L::K0, kcol, krow + (j + 1) * 128);
+          load_kv(gv, NV, vfull, vempty, L::V0, vcol, krow + j * 128);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
+      constexpr uint32_t ID_S = idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t ID_O = idesc_bf16_f32(128, HD, false, true);
-      // S of block g (head t) into buffer g & 1; the K slot is released after head B's S
-      auto issue_s = [&](int t, int g) {
+      auto issue_s = [&](int t, int g) {  // S_t of key block g (K slot g % NK)
         const uint8_t* q = sm + L::Q0 + t * L::QT;
-        const uint8_t* k = sm + L::K0 + (g % NK) * L::KB;
+        const uint8_t* k = sm + L::K0 + (g % NK) * L::QT;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
-          umma_bf16(tbase + (2 * t + (g & 1)) * 64, desc_k(q, kk, kBlk128), desc_k(k, kk, kBlk64),
-                    ID_S, kk > 0);
-        umma_commit(&sfull[2 * t + (g & 1)]);
+          umma_bf16(tbase + 128 * t, desc_k(q, kk, kBlk128), desc_k(k, kk, kBlk128), ID_S, kk > 0);
+        umma_commit(&sfull[t]);
         if (t == 1) umma_commit(&kempty[g % NK]);
       };
-      auto issue_pv = [&](int t, int g, int j) {
-        const uint8_t* p = sm + L::P0 + (2 * t + (g & 1)) * L::PB;
-        const uint8_t* v = sm + L::V0 + (g % NV) * L::KB;
+      auto issue_pv = [&](int t, int g, int j) {  // O_t += P_t V(g)
+        const uint8_t* v = sm + L::V0 + (g % NV) * L::QT;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_bf16(tbase + 256 + t * HD, desc_k(p, kk, kBlk128), desc_mn(v, kk, kBlk64), ID_O,
-                    (j > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&ofull[2 * t + (g & 1)]);
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16_ts(tbase + 256 + HD * t, tbase + 128 * t + kk * 8, desc_mn(v, kk, kBlk128),
+                       ID_O, (j > 0 || kk > 0) ? 1u : 0u);
         if (t == 1) umma_commit(&vempty[g % NV]);
       };
       auto wait_k = [&](int g) {
@@ -323,140 +328,114 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
         const int nb = fwd_item(a, item).nb;
         spin_wait(qfull, n & 1);
-        // S of blocks 0 and 1 (their S buffers were released by the previous item's pfull)
-        for (int q = 0; q < 2; ++q) {
-          wait_k(g + q);
-          issue_s(0, g + q);
-          issue_s(1, g + q);
-        }
-        const int q_last = nb >= 3 ? nb - 3 : 0;  // iteration that issues the item's last S
+        wait_k(g);
+        // S buffers: the previous item's last PV (issued before these) consumed its P
+        issue_s(0, g);
+        issue_s(1, g);
+        if (nb == 1) umma_commit(qempty);
         for (int j = 0; j < nb; ++j, ++g) {
           spin_wait(&vfull[g % NV], (g / NV) & 1);
           if (j == 0 && n > 0) spin_wait(&oempty[0], (n - 1) & 1);  // O_A read out
-          spin_wait(&pfull[g & 1], (g >> 1) & 1);
+          spin_wait(&pfull[0], g & 1);
           tc_fence_after();
           issue_pv(0, g, j);
-          if (j + 2 < nb) {  // softmax A is done with S buffer g & 1
-            wait_k(g + 2);
-            issue_s(0, g + 2);
+          if (j + 1 == nb) umma_commit(&ofull[0]);
+          if (j + 1 < nb) {
+            wait_k(g + 1);
+            issue_s(0, g + 1);
           }
           if (j == 0 && n > 0) spin_wait(&oempty[1], (n - 1) & 1);  // O_B read out
-          spin_wait(&pfull[2 + (g & 1)], (g >> 1) & 1);
+          spin_wait(&pfull[1], g & 1);
           tc_fence_after();
           issue_pv(1, g, j);
-          if (j + 2 < nb) issue_s(1, g + 2);
-          if (j == q_last) umma_commit(qempty);
+          if (j + 1 == nb) umma_commit(&ofull[1]);
+          if (j + 1 < nb) issue_s(1, g + 1);
+          if (j + 2 == nb) umma_commit(qempty);  // the item's last S MMAs were just issued
         }
       }
     }
   } else {
-    // softmax: 8 warps per head, two per TMEM lane quarter; a thread owns half a row (32 of
-    // the block's 64 columns, half of O's columns).  The two halves of a row agree on the
-    // running max through a double-buffered smem exchange and a named barrier per head.
-    const int idx = warp - 2;
-    const int t = idx / 8, hf = (idx / 4) & 1;
+    const int t = (warp - 2) / 4;
     const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tS0 = tbase + lo + 2 * t * 64 + hf * 32;
-    const uint32_t tO = tbase + lo + 256 + t * HD + hf * (HD / 2);
-    float* xch = reinterpret_cast<float*>(sm + L::XCH);  // [2 parity][2 heads][2 halves][128]
-    auto slot = [&](int par, int half) { return xch + ((par * 2 + t) * 2 + half) * 128 + r; };
+    const uint32_t tS = tbase + lo + 128 * t, tO = tbase + lo + 256 + HD * t;
     const float c = a.scale_log2;
-    int g = 0, xp = 0;  // blocks seen, exchange parity
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    int g = 0, n = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
       const FwdItem w = fwd_item(a, item);
       const int qpos = w.i * 128 + r;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < w.nb; ++j, ++g) {
-        const int u = g & 1;
-        spin_wait(&sfull[2 * t + u], (g >> 1) & 1);
+        spin_wait(&sfull[t], g & 1);
         tc_fence_after();
-        const uint32_t tS = tS0 + u * 64;
-        uint32_t v[32];
-        tmem_ld32(tS, v);
+        uint32_t v[128];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+          tmem_ld32(tS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cc * 32));
         tmem_wait_ld();
-        const bool diag = j * 64 + 63 > w.i * 128;  // block reaches past this tile's first row
-        const int lim = qpos - j * 64 - hf * 32;     // columns e <= lim are visible
+        const bool diag = j == w.i;  // columns e > r are masked
         float mx = -INFINITY;
         if (!diag) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, f32(v[e]));
+          for (int e = 0; e < 128; ++e) mx = fmaxf(mx, f32(v[e]));
         } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (e <= lim) mx = fmaxf(mx, f32(v[e]));
+          for (int e = 0; e < 128; ++e)
+            if (e <= r) mx = fmaxf(mx, f32(v[e]));
         }
-        *slot(xp, hf) = mx;
-        named_bar_sync(1 + t, 256);
-        mx = fmaxf(mx, *slot(xp, hf ^ 1));
-        xp ^= 1;
         const float m_new = fmaxf(m, mx * c);
         if (j == 0) {
           m = m_new;
         } else if (__any_sync(0xffffffffu, m_new > m + 8.f)) {
-          // O must hold every PV up to the previous block before it is rescaled
-          spin_wait(&ofull[2 * t + (u ^ 1)], ((g - 1) >> 1) & 1);
-          tc_fence_after();
+          // S_t(j) done => PV_t(j-1) done: O holds every earlier block
           const float alpha = ex2(m - m_new);
           l *= alpha;
           m = m_new;
-#pragma unroll
-          for (int cc = 0; cc < HD / 64; ++cc) {
-            uint32_t o[32];
-            tmem_ld32(tO + cc * 32, o);
+#pragma unroll 1
+          for (int cc = 0; cc < HD / 16; ++cc) {  // 16 columns at a time: v[] stays live
+            uint32_t o[16];
+            tmem_ld16(tO + cc * 16, o);
             tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(f32(o[e]) * alpha);
-            tmem_st32(tO + cc * 32, o);
+            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(f32(o[e]) * alpha);
+            tmem_st16(tO + cc * 16, o);
           }
-          tmem_wait_st();
         }
-        tmem_ld32(tS, v);  // reload (S is still in TMEM): keeps v dead across the rescale
-        tmem_wait_ld();
-        float pr[32];
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float2 x = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
-          pr[e] = x.x;
-          pr[e + 1] = x.y;
-        }
-        if (!diag) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            pr[e] = ex2_mix<0>(pr[e]);
-            pr[e + 1] = ex2_mix<1>(pr[e + 1]);
-            pr[e + 2] = ex2_mix<2>(pr[e + 2]);
-            pr[e + 3] = ex2_mix<3>(pr[e + 3]);
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) pr[e] = e <= lim ? ex2(pr[e]) : 0.f;
-        }
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) acc = __fadd2_rn(acc, make_float2(pr[e], pr[e + 1]));
+        for (int e = 0; e < 128; e += 4) {  // P packed in place: word e/2 holds columns e, e+1
+          float2 x0 = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
+          float2 x1 = __ffma2_rn(make_float2(f32(v[e + 2]), f32(v[e + 3])), c2, nm2);
+          if (!diag) {
+            x0.x = ex2_mix<0>(x0.x);
+            x0.y = ex2_mix<1>(x0.y);
+            x1.x = ex2_mix<2>(x1.x);
+            x1.y = ex2_mix<3>(x1.y);
+          } else {
+            x0.x = e <= r ? ex2(x0.x) : 0.f;
+            x0.y = e + 1 <= r ? ex2(x0.y) : 0.f;
+            x1.x = e + 2 <= r ? ex2(x1.x) : 0.f;
+            x1.y = e + 3 <= r ? ex2(x1.y) : 0.f;
+          }
+          acc = __fadd2_rn(acc, __fadd2_rn(x0, x1));
+          v[e / 2] = pack_bf16(x0.x, x0.y);
+          v[e / 2 + 1] = pack_bf16(x1.x, x1.y);
+        }
         l += acc.x + acc.y;
-        // P buffer u was last read by the PV two blocks back
-        if (g >= 2) spin_wait(&ofull[2 * t + u], ((g - 2) >> 1) & 1);
-        st_swz32(sm + L::P0 + (2 * t + u) * L::PB, r, hf * 4, pr);
-        fence_async_smem();
+        tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(v));
+        tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(v + 32));
+        tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&pfull[2 * t + u]);
+        mbar_arrive(&pfull[t]);
       }
-      // l of the whole row = the two halves' sums (same running max)
-      *slot(xp, hf) = l;
-      named_bar_sync(1 + t, 256);
-      l += *slot(xp, hf ^ 1);
-      xp ^= 1;
-      spin_wait(&ofull[2 * t + ((g - 1) & 1)], ((g - 1) >> 1) & 1);
+      spin_wait(&ofull[t], n & 1);
       tc_fence_after();
       const float inv = 1.f / l;
-      bf16* out = a.o + static_cast<long long>(w.b * a.S + qpos) * a.ldo + (w.h0 + t) * HD +
-                  hf * (HD / 2);
+      bf16* out = a.o + static_cast<long long>(w.b * a.S + qpos) * a.ldo + (w.h0 + t) * HD;
 #pragma unroll
-      for (int cc = 0; cc < HD / 64; ++cc) {
+      for (int cc = 0; cc < HD / 32; ++cc) {
         uint32_t o[32];
         tmem_ld32(tO + cc * 32, o);
         tmem_wait_ld();
@@ -464,8 +443,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
       }
       tc_fence_before();
       mbar_arrive(&oempty[t]);
-      if (hf == 0)
-        a.lse[(static_cast<long long>(w.b) * a.H + w.h0 + t) * a.S + qpos] = m + __log2f(l);
+      a.lse[(static_cast<long long>(w.b) * a.H + w.h0 + t) * a.S + qpos] = m + __log2f(l);
     }
   }
   tc_fence_before();
@@ -962,7 +940,6 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
   const int ld = (H + 2 * KVH) * HD;
   const int N = B * S;
   const CUtensorMap mq = tmap(qkv, ld, N, ld, 128);
-  const CUtensorMap mkv = tmap(qkv, ld, N, ld, 64);
   FwdArgs a{B, H, KVH, S, ld, static_cast<bf16*>(o), H * HD, lse,
             1.4426950408889634f / sqrtf(static_cast<float>(HD))};
   static bool attr = false;
@@ -972,7 +949,7 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
   }
   const int items = (S / 128) * B * KVH * (H / KVH / 2);
   attn_fwd_kernel<HD><<<std::min(items, num_sms()), kFwdThreads,
-                        std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(mq, mkv, a, items);
+                        std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(mq, a, items);
   check_launch("attn_fwd_kernel");
 }
 
