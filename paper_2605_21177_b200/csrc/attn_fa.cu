@@ -154,6 +154,16 @@ __device__ __forceinline__ float ex2_mix(float x) {
   else return ex2(x);
 }
 
+// One lane of a converged warp (the MMA / commit issuer); the rest of the warp runs the same
+// loop, so descriptors and addresses stay warp-uniform (uniform registers, no per-MMA moves).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // Spin wait (no suspend hint): the attention pipelines hand off every ~0.1-0.3 us between
 // the softmax warps and the MMA thread, so wake-up latency is on the critical path.
 __device__ __forceinline__ void spin_wait(uint64_t* bar, uint32_t parity) {
@@ -193,7 +203,7 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
 // and S_t(j+1) completing implies PV_t(j) did (O is safe to rescale, P to overwrite).
 template <int HD>
 struct FwdSmem {
-  static constexpr int NK = 2, NV = 3;
+  static constexpr int NK = 3, NV = 2;
   static constexpr uint32_t QT = 128 * HD * 2;  // query tile / key or value block (128 rows)
   static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NK * QT, BAR = V0 + NV * QT;
   static constexpr size_t BYTES = 1024 + BAR + 256;
@@ -300,25 +310,35 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp walks the MMA program; one elected lane issues
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t ID_O = idesc_bf16_f32(128, HD, false, true);
       auto issue_s = [&](int t, int g) {  // S_t of key block g (K slot g % NK)
         const uint8_t* q = sm + L::Q0 + t * L::QT;
         const uint8_t* k = sm + L::K0 + (g % NK) * L::QT;
+        const uint64_t dq = desc_k(q, 0, kBlk128), dk = desc_k(k, 0, kBlk128);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          umma_bf16(tbase + 128 * t, desc_k(q, kk, kBlk128), desc_k(k, kk, kBlk128), ID_S, kk > 0);
-        umma_commit(&sfull[t]);
-        if (t == 1) umma_commit(&kempty[g % NK]);
+          for (int kk = 0; kk < HD / 16; ++kk) {  // +32 B per step, +16 KB per 64-column block
+            const uint64_t off = ((kk >> 2) * kBlk128 + (kk & 3) * 32) >> 4;
+            umma_bf16(tbase + 128 * t, dq + off, dk + off, ID_S, kk > 0);
+          }
+          umma_commit(&sfull[t]);
+          if (t == 1) umma_commit(&kempty[g % NK]);
+        }
+        __syncwarp();
       };
       auto issue_pv = [&](int t, int g, int j) {  // O_t += P_t V(g)
         const uint8_t* v = sm + L::V0 + (g % NV) * L::QT;
+        const uint64_t dv = desc_mn(v, 0, kBlk128);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16_ts(tbase + 256 + HD * t, tbase + 128 * t + kk * 8, desc_mn(v, kk, kBlk128),
-                       ID_O, (j > 0 || kk > 0) ? 1u : 0u);
-        if (t == 1) umma_commit(&vempty[g % NV]);
+          for (int kk = 0; kk < 8; ++kk)  // 16 key rows = 2048 B per step
+            umma_bf16_ts(tbase + 256 + HD * t, tbase + 128 * t + kk * 8, dv + kk * (2048 >> 4),
+                         ID_O, (j > 0 || kk > 0) ? 1u : 0u);
+          if (t == 1) umma_commit(&vempty[g % NV]);
+        }
+        __syncwarp();
       };
       auto wait_k = [&](int g) {
         spin_wait(&kfull[g % NK], (g / NK) & 1);
@@ -332,14 +352,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         // S buffers: the previous item's last PV (issued before these) consumed its P
         issue_s(0, g);
         issue_s(1, g);
-        if (nb == 1) umma_commit(qempty);
+        if (nb == 1 && elect_one()) umma_commit(qempty);
+        __syncwarp();
         for (int j = 0; j < nb; ++j, ++g) {
           spin_wait(&vfull[g % NV], (g / NV) & 1);
           if (j == 0 && n > 0) spin_wait(&oempty[0], (n - 1) & 1);  // O_A read out
           spin_wait(&pfull[0], g & 1);
           tc_fence_after();
           issue_pv(0, g, j);
-          if (j + 1 == nb) umma_commit(&ofull[0]);
+          if (j + 1 == nb && elect_one()) umma_commit(&ofull[0]);
+          __syncwarp();
           if (j + 1 < nb) {
             wait_k(g + 1);
             issue_s(0, g + 1);
@@ -348,9 +370,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           spin_wait(&pfull[1], g & 1);
           tc_fence_after();
           issue_pv(1, g, j);
-          if (j + 1 == nb) umma_commit(&ofull[1]);
+          if (j + 1 == nb && elect_one()) umma_commit(&ofull[1]);
+          __syncwarp();
           if (j + 1 < nb) issue_s(1, g + 1);
-          if (j + 2 == nb) umma_commit(qempty);  // the item's last S MMAs were just issued
+          if (j + 2 == nb && elect_one()) umma_commit(qempty);  // the item's last S MMAs issued
+          __syncwarp();
         }
       }
     }
@@ -375,15 +399,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tmem_ld32(tS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cc * 32));
         tmem_wait_ld();
         const bool diag = j == w.i;  // columns e > r are masked
-        float mx = -INFINITY;
+        float mk[8];  // eight independent max chains (ILP), folded at the end
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mk[q] = -INFINITY;
         if (!diag) {
 #pragma unroll
-          for (int e = 0; e < 128; ++e) mx = fmaxf(mx, f32(v[e]));
+          for (int e = 0; e < 128; ++e) mk[e & 7] = fmaxf(mk[e & 7], f32(v[e]));
         } else {
 #pragma unroll
           for (int e = 0; e < 128; ++e)
-            if (e <= r) mx = fmaxf(mx, f32(v[e]));
+            if (e <= r) mk[e & 7] = fmaxf(mk[e & 7], f32(v[e]));
         }
+        const float mx = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
+                               fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
         const float m_new = fmaxf(m, mx * c);
         if (j == 0) {
           m = m_new;
@@ -403,7 +431,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
-        float2 acc = make_float2(0.f, 0.f);
+        float2 accs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};
 #pragma unroll
         for (int e = 0; e < 128; e += 4) {  // P packed in place: word e/2 holds columns e, e+1
           float2 x0 = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
@@ -419,10 +448,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             x1.x = e + 2 <= r ? ex2(x1.x) : 0.f;
             x1.y = e + 3 <= r ? ex2(x1.y) : 0.f;
           }
-          acc = __fadd2_rn(acc, __fadd2_rn(x0, x1));
+          accs[(e >> 2) & 3] = __fadd2_rn(accs[(e >> 2) & 3], __fadd2_rn(x0, x1));
           v[e / 2] = pack_bf16(x0.x, x0.y);
           v[e / 2 + 1] = pack_bf16(x1.x, x1.y);
         }
+        const float2 acc = __fadd2_rn(__fadd2_rn(accs[0], accs[1]), __fadd2_rn(accs[2], accs[3]));
         l += acc.x + acc.y;
         tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(v));
         tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(v + 32));
