@@ -586,22 +586,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp walks the MMA program; one elected lane issues
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_Q = idesc_bf16_f32(128, HD, false, true);
+      const uint64_t dQ = desc_k(sm + L::Q, 0, kBlk128), dDO = desc_k(sm + L::DO, 0, kBlk128);
       auto issue_s = [&](int jj) {
         const int s = jj % NS, u = jj / NS, ts = jj & 1;
         spin_wait(&kvfull[s], u & 1);
         tc_fence_after();
-        const uint8_t* k = sm + L::K0 + s * L::KB;
-        const uint8_t* v = sm + L::V0 + s * L::KB;
+        const uint64_t dk = desc_k(sm + L::K0 + s * L::KB, 0, kBlk64);
+        const uint64_t dv = desc_k(sm + L::V0 + s * L::KB, 0, kBlk64);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          umma_bf16(tst(ts), desc_k(sm + L::Q, kk, kBlk128), desc_k(k, kk, kBlk64), ID_S, kk > 0);
-          umma_bf16(tst(ts) + 64, desc_k(sm + L::DO, kk, kBlk128), desc_k(v, kk, kBlk64), ID_S,
-                    kk > 0);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint64_t oa = ((kk >> 2) * kBlk128 + (kk & 3) * 32) >> 4;
+            const uint64_t ob = ((kk >> 2) * kBlk64 + (kk & 3) * 32) >> 4;
+            umma_bf16(tst(ts), dQ + oa, dk + ob, ID_S, kk > 0);
+            umma_bf16(tst(ts) + 64, dDO + oa, dv + ob, ID_S, kk > 0);
+          }
+          umma_commit(&tfull[ts]);
         }
-        umma_commit(&tfull[ts]);
+        __syncwarp();
       };
       spin_wait(qfull, 0);
       issue_s(0);
@@ -610,17 +615,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int s = jj % NS, ts = jj & 1, v = jj >> 1;
         spin_wait(&pfull[ts], v & 1);
         tc_fence_after();
-        const uint8_t* k = sm + L::K0 + s * L::KB;
-        const uint8_t* ds = sm + L::DS0 + ts * L::SB;
+        const uint64_t dk = desc_mn(sm + L::K0 + s * L::KB, 0, kBlk64);
+        const uint64_t dds = desc_k(sm + L::DS0 + ts * L::SB, 0, kBlk128);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_bf16(tbase, desc_k(ds, kk, kBlk128), desc_mn(k, kk, kBlk64), ID_Q,
-                    (jj > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&kvempty[s]);
-        umma_commit(&pfree[ts]);
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16(tbase, dds + ((kk * 32) >> 4), dk + ((kk * 2048) >> 4), ID_Q,
+                      (jj > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&kvempty[s]);
+          umma_commit(&pfree[ts]);
+        }
+        __syncwarp();
         if (jj + 2 < n) issue_s(jj + 2);
       }
-      umma_commit(done);
+      if (elect_one()) umma_commit(done);
+      __syncwarp();
     }
   } else {
     // 8 warps, two per TMEM lane quarter: a thread owns half a row (32 of the block's 64 key
@@ -810,21 +819,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp walks the MMA program; one elected lane issues
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_A = idesc_bf16_f32(128, HD, false, true);
+      const uint64_t dK = desc_k(sm + L::K, 0, kBlk128), dV = desc_k(sm + L::V, 0, kBlk128);
       auto issue_s = [&](int it) {
         const int s = it % NS, u = it / NS, ts = it & 1;
         spin_wait(&qfull[s], u & 1);
         tc_fence_after();
-        const uint8_t* q = sm + L::Q0 + s * L::QB;
-        const uint8_t* d = sm + L::DO0 + s * L::QB;
+        const uint64_t dq = desc_k(sm + L::Q0 + s * L::QB, 0, kBlk64);
+        const uint64_t dd = desc_k(sm + L::DO0 + s * L::QB, 0, kBlk64);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          umma_bf16(tst(ts), desc_k(sm + L::K, k, kBlk128), desc_k(q, k, kBlk64), ID_S, k > 0);
-          umma_bf16(tst(ts) + 64, desc_k(sm + L::V, k, kBlk128), desc_k(d, k, kBlk64), ID_S, k > 0);
+          for (int k = 0; k < HD / 16; ++k) {
+            const uint64_t oa = ((k >> 2) * kBlk128 + (k & 3) * 32) >> 4;
+            const uint64_t ob = ((k >> 2) * kBlk64 + (k & 3) * 32) >> 4;
+            umma_bf16(tst(ts), dK + oa, dq + ob, ID_S, k > 0);
+            umma_bf16(tst(ts) + 64, dV + oa, dd + ob, ID_S, k > 0);
+          }
+          umma_commit(&tfull[ts]);
         }
-        umma_commit(&tfull[ts]);
+        __syncwarp();
       };
       spin_wait(kvfull, 0);
       issue_s(0);
@@ -833,21 +848,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int s = it % NS, ts = it & 1, v = it >> 1;
         spin_wait(&pfull[ts], v & 1);
         tc_fence_after();
-        const uint8_t* q = sm + L::Q0 + s * L::QB;
-        const uint8_t* d = sm + L::DO0 + s * L::QB;
-        const uint8_t* p = sm + L::P0 + ts * L::PB;
-        const uint8_t* ds = sm + L::DS0 + ts * L::PB;
+        const uint64_t dq = desc_mn(sm + L::Q0 + s * L::QB, 0, kBlk64);
+        const uint64_t dd = desc_mn(sm + L::DO0 + s * L::QB, 0, kBlk64);
+        const uint64_t dp = desc_k(sm + L::P0 + ts * L::PB, 0, kBlk128);
+        const uint64_t dds = desc_k(sm + L::DS0 + ts * L::PB, 0, kBlk128);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
-          umma_bf16(tbase, desc_k(p, k, kBlk128), desc_mn(d, k, kBlk64), ID_A, acc);        // dV
-          umma_bf16(tbase + HD, desc_k(ds, k, kBlk128), desc_mn(q, k, kBlk64), ID_A, acc);  // dK
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
+            umma_bf16(tbase, dp + ((k * 32) >> 4), dd + ((k * 2048) >> 4), ID_A, acc);        // dV
+            umma_bf16(tbase + HD, dds + ((k * 32) >> 4), dq + ((k * 2048) >> 4), ID_A, acc);  // dK
+          }
+          umma_commit(&qempty[s]);
+          umma_commit(&pfree[ts]);
         }
-        umma_commit(&qempty[s]);
-        umma_commit(&pfree[ts]);
+        __syncwarp();
         if (it + 2 < n_it) issue_s(it + 2);
       }
-      umma_commit(done);
+      if (elect_one()) umma_commit(done);
+      __syncwarp();
     }
   } else {
     // 8 warps, two per TMEM lane quarter: a thread owns half a key row (32 of the block's 64
