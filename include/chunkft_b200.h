@@ -305,12 +305,10 @@ int cft_set_gemm_policy(int policy);
  * the lm_head forward GEMM; default 7, 0 = separate kernels.  1 and 2 are bit-identical to the
  * separate kernels; 4 sums exp() in a different order (loss / dlogits to fp32 rounding). */
 int cft_set_fusion(int enable);
-/* Kernel variant per operator, for A/B measurements (defaults: CFT_ADAMW_KERNEL /
- * CFT_CE_KERNEL).  op 0 fp32 AdamW: 0 register kernel, 1 / 2 / 3 / 4 TMA-staged with 8 / 16 /
- * 24 / 31 consumer warps (default 4).  op 1 bf16 softmax CE: 0 two-pass (512 threads per row), 1 cluster
- * (2 row stages, 1 CTA per SM), 2 cluster (1 stage, 3 CTAs per SM), 3 two-pass with 1024
- * threads per row.  op 2 tcgen05 GEMM launches: 0 ordinary, 1 programmatic dependent launch
- * (prologue overlaps the previous kernel's tail). */
+/* Kernel variant per operator, for A/B measurements (default from CFT_ADAMW_KERNEL /
+ * CFT_GEMM_PDL).  op 0 fp32 AdamW: 0 register kernel, 1 TMA-staged with 31 consumer warps
+ * (default).  op 2 tcgen05 GEMM launches: 0 ordinary, 1 programmatic dependent launch
+ * (default; the prologue overlaps the previous kernel's tail). */
 int cft_set_kernel_variant(int op, int variant);
 
 /* Element conversion (e.g. fp32 master -> bf16 params at init). */

@@ -60,13 +60,9 @@ int& kernel_variant(int op) {
       [] {
         const char* e = std::getenv("CFT_ADAMW_KERNEL");
         const std::string k = e ? e : "";
-        return k == "reg" ? 0 : k == "bulk8" ? 1 : k == "bulk16" ? 2 : k == "bulk24" ? 3 : 4;
+        return k == "reg" ? 0 : 1;
       }(),
-      [] {
-        const char* e = std::getenv("CFT_CE_KERNEL");
-        const std::string k = e ? e : "";
-        return k == "cluster" ? 1 : k == "cluster3" ? 2 : k == "vec1024" ? 3 : 0;
-      }(),
+      0,  // (retired: softmax CE variants; the two-pass kernel is the only one)
       [] {
         const char* e = std::getenv("CFT_GEMM_PDL");
         return e && std::string(e) == "0" ? 0 : 1;
@@ -82,7 +78,8 @@ int& kernel_variant(int op) {
 extern "C" {
 int cft_set_kernel_variant(int op, int variant) {
   return cft::guarded([&] {
-    CFT_CHECK(variant >= 0 && variant <= 4, "cft_set_kernel_variant: variant out of range");
+    CFT_CHECK(op != 1, "cft_set_kernel_variant: operator 1 (softmax CE) has one kernel");
+    CFT_CHECK(variant >= 0 && variant <= 1, "cft_set_kernel_variant: variant out of range");
     cft::kernel_variant(op) = variant;
   });
 }

@@ -357,163 +357,6 @@ __global__ void loss_ce_parts_kernel(const __nv_bfloat16* y, const int32_t* labe
   ce_write_dy(yr, dy + b * cols, cols / 8, label, ylab, m + logf(s), inv_rows, loss);
 }
 
-// Softmax cross-entropy with the row held on chip: a cluster of kCeCluster CTAs owns one
-// row at a time, each CTA a contiguous part of <= kCePart columns that a 1-D bulk copy (TMA)
-// brings into shared memory.  Each CTA reduces its part to a (max, sum-exp) pair, the cluster
-// exchanges the pairs through distributed shared memory, and every CTA writes its part of
-// dlogits from shared memory -- so HBM sees exactly one read and one write of each logit (the
-// two-pass kernel above re-reads a 256 KB row that no longer sits in L2 at full occupancy).
-// One MUFU exp per logit per pass: each thread takes the max of its own columns first (a
-// cheap extra pass over shared memory), then sums exp2(x*log2e - max*log2e) as FFMA + EX2.
-// STAGES row buffers per CTA and MINB CTAs per SM: rows in flight per SM = STAGES x MINB.
-// The row may be overwritten in place (dy == y): the label logit is read from shared memory.
-constexpr int kCeCluster = 4;
-constexpr int kCeThreads = 512;
-constexpr int kCePart = 32768;  // bf16 columns per CTA and stage (64 KB)
-
-
-template <int STAGES, int MINB>
-__global__ void __cluster_dims__(kCeCluster, 1, 1) __launch_bounds__(kCeThreads, MINB)
-    loss_ce_cluster_kernel(const __nv_bfloat16* y, const int32_t* labels, long long rows,
-                           long long cols, int part, float inv_rows, __nv_bfloat16* dy,
-                           double* loss, unsigned long long* bad_label) {
-  using namespace cft::ptx;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t full[STAGES];
-  __shared__ float2 slot[2];  // this CTA's (max, sum) of the row in flight, by row parity
-  __shared__ float sm[32], ss[32];
-  const uint32_t rank = cluster_ctarank();
-  const long long cid = blockIdx.x / kCeCluster, ncl = gridDim.x / kCeCluster;
-  const long long c0 = (long long)rank * part;
-  const int my = static_cast<int>(max(0LL, min((long long)part, cols - c0)));  // % 8 == 0
-  __nv_bfloat16* buf0 = reinterpret_cast<__nv_bfloat16*>(smem);
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < STAGES; ++b) mbar_init(&full[b], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  uint64_t pol = 0;
-  auto issue = [&](long long r, int b) {
-    if (my > 0) {
-      mbar_expect_tx(&full[b], static_cast<uint32_t>(my) * 2u);
-      bulk_load_1d(buf0 + (size_t)b * kCePart, y + r * cols + c0, static_cast<uint32_t>(my) * 2u,
-                   &full[b], pol);
-    } else {
-      mbar_arrive(&full[b]);
-    }
-  };
-  if (threadIdx.x == 0) {
-    pol = l2_policy_evict_first();
-    for (int b = 0; b < STAGES; ++b)
-      if (cid + b * ncl < rows) issue(cid + b * ncl, b);
-  }
-  const int nv = my / 8;
-  int it = 0;
-  for (long long r = cid; r < rows; r += ncl, ++it) {
-    const int b = it % STAGES;
-    mbar_wait(&full[b], (it / STAGES) & 1);
-    const uint4* row = reinterpret_cast<const uint4*>(buf0 + (size_t)b * kCePart);
-    float m = -INFINITY;
-    for (int j = threadIdx.x; j < nv; j += kCeThreads) {
-      float v[8];
-      unpack8(row[j], v);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) m = fmaxf(m, v[e]);
-    }
-    float s = 0.f;
-    if (m != -INFINITY) {
-      const float ms = m * kL2e;
-      for (int j = threadIdx.x; j < nv; j += kCeThreads) {
-        float v[8];
-        unpack8(row[j], v);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) s += ex2_approx(fmaf(v[e], kL2e, -ms));
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-      const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
-      online_merge(m, s, m2, s2);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      sm[threadIdx.x / 32] = m;
-      ss[threadIdx.x / 32] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      m = -INFINITY;
-      s = 0.f;
-      for (int i = 0; i < kCeThreads / 32; ++i) online_merge(m, s, sm[i], ss[i]);
-      slot[it & 1] = make_float2(m, s);
-    }
-    cluster_sync();  // every CTA's pair for row r is visible cluster-wide
-    m = -INFINITY;
-    s = 0.f;
-    const uint32_t my_slot = smem_u32(&slot[it & 1]);
-#pragma unroll
-    for (int k = 0; k < kCeCluster; ++k) {  // same order in every CTA -> same logZ
-      float2 p;
-      asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];"
-                   : "=f"(p.x), "=f"(p.y)
-                   : "r"(mapa(my_slot, k)));
-      online_merge(m, s, p.x, p.y);
-    }
-    const float logz = m + logf(s);
-    const float lzs = logz * kL2e;
-    const int label = labels[r];
-    if (label < 0 || label >= cols) {
-      if (rank == 0 && threadIdx.x == 0) atomicAdd(bad_label, 1ull);
-    } else {
-      uint4* out = reinterpret_cast<uint4*>(dy + r * cols + c0);
-      const long long lrel = label - c0;  // label column relative to this part
-      for (int j = threadIdx.x; j < nv; j += kCeThreads) {
-        float v[8];
-        unpack8(row[j], v);
-        uint4 o;
-        __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const long long c = 8LL * j + 2 * q;
-          const float p0 = ex2_approx(fmaf(v[2 * q], kL2e, -lzs)) - (c == lrel ? 1.f : 0.f);
-          const float p1 = ex2_approx(fmaf(v[2 * q + 1], kL2e, -lzs)) - (c + 1 == lrel ? 1.f : 0.f);
-          oh[q] = __floats2bfloat162_rn(p0 * inv_rows, p1 * inv_rows);
-        }
-        __stcs(out + j, o);
-      }
-      if (threadIdx.x == 0 && lrel >= 0 && lrel < my) {
-        const float ylab = __bfloat162float(buf0[(size_t)b * kCePart + lrel]);
-        atomicAdd(loss, static_cast<double>(-(ylab - logz)) * inv_rows);
-      }
-    }
-    __syncthreads();  // every thread is done with this stage
-    if (threadIdx.x == 0 && r + STAGES * ncl < rows) issue(r + STAGES * ncl, b);
-  }
-  cluster_sync();  // peers may still read this CTA's slot
-}
-
-template <int STAGES, int MINB>
-void launch_ce_cluster(const __nv_bfloat16* y, const int32_t* labels, long long rows,
-                       long long cols, __nv_bfloat16* dy, double* loss_acc,
-                       unsigned long long* bad_label, cudaStream_t s) {
-  constexpr size_t smem = (size_t)STAGES * kCePart * sizeof(__nv_bfloat16);
-  auto kern = loss_ce_cluster_kernel<STAGES, MINB>;
-  static int max_clusters = [&] {
-    CFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kCeCluster * num_sms() * MINB);
-    cfg.blockDim = dim3(kCeThreads);
-    cfg.dynamicSmemBytes = smem;
-    int n = 0;
-    CFT_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
-    return std::max(1, n);
-  }();
-  const int part = static_cast<int>(((cols + kCeCluster - 1) / kCeCluster + 7) / 8 * 8);
-  const long long ncl = std::min<long long>(rows, max_clusters);
-  kern<<<(unsigned)(ncl * kCeCluster), kCeThreads, smem, s>>>(y, labels, rows, cols, part,
-                                                               1.f / rows, dy, loss_acc, bad_label);
-  check_launch("loss_ce_cluster");
-}
-
 // fp64 losses for the fp64 engine path (exp/log are CUDA's: <= 1-2 ulp from glibc).
 __global__ void loss_elem_f64_kernel(int kind, const double* y, const double* target, long long n,
                                      double* dy, double* partial) {
@@ -611,17 +454,8 @@ void loss(int kind, const T* y, const T* target, const int32_t* labels, long lon
     if constexpr (std::is_same_v<T, __nv_bfloat16>) {
       const bool vec = cols % 8 == 0 &&
           ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0;
-      const int variant = kernel_variant(1);  // 0: two-pass kernel (A/B runs)
-      if (vec && (variant == 1 || variant == 2) && rows >= kCeCluster && cols <= (long long)kCeCluster * kCePart) {
-        if (variant == 1) launch_ce_cluster<2, 1>(y, labels, rows, cols, dy, loss_acc, bad_label, s);
-        else launch_ce_cluster<1, 3>(y, labels, rows, cols, dy, loss_acc, bad_label, s);
-        return;
-      }
       if (vec) {
-        // variant 3: 1024 threads per row -> 2 CTAs (rows) per SM, 296 rows = 76 MB in flight,
-        // so the second pass over each 256 KB row still finds it in L2 (512 threads: 4 rows per
-        // SM, 152 MB in flight > L2, and the second pass re-reads from HBM)
-        const unsigned threads = variant == 3 ? 1024u : 512u;
+        const unsigned threads = 512u;
         loss_ce_vec_kernel<<<(unsigned)rows, threads, 0, s>>>(y, labels, cols, 1.f / rows, dy,
                                                               loss_acc, bad_label);
         check_launch("loss_ce_vec");

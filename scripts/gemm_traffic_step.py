@@ -3,7 +3,7 @@
 gpu__time_duration.sum` captures exactly that step's kernels.  Prints the step's algorithmic
 GEMM bytes / FLOPs / launch counts (engine work counters) as one JSON line.
 
-usage: python tools/gemm_traffic_step.py [steps_before]   (the captured step's chunk = that)
+usage: python scripts/gemm_traffic_step.py [steps_before]   (the captured step's chunk = that)
 """
 import json
 import sys
@@ -11,7 +11,7 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
 from paper_2605_21177_b200.engine import ChunkEngine, LlamaModel, TrainOptions  # noqa: E402
 from paper_2605_21177_b200.plan import ScheduleConfig, TensorInfo, partition_by_budget  # noqa: E402
 
