@@ -1130,10 +1130,9 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   const CUtensorMap tb = cached_map(x, in_dim, n_tok, in_dim, 64, 64);
   // Candidate tilings for the (usually narrow) slice: CTA-pair 256x256 or 256x128 tiles, or
   // single-CTA 128xBN tiles; each with its best split count under the cost model.
-  bool pairs = use_pairs(a.M, a.N, a.K, true);
+  const bool pairs = use_pairs(a.M, a.N, a.K, true);
   const int BN = in_dim >= 256 ? 256 : 128;
   int pair_bn = 256;
-  bool single128 = false;
   if (pairs) {
     Args a256 = a, a128 = a;
     fill_units(a256, 256, 256, num_sms() / 2, 0.40, true);
@@ -1163,16 +1162,6 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
       return e ? std::atoi(e) : 0;
     }();
     const double c128 = cost(a128, 0.38), c256 = cost(a256, 0.40);
-    // single-CTA 128 x 128 tiles (M128 N128 MMAs run at the full per-SM rate): for a narrow
-    // slice they fill the chip without splitting K, and the unsplit tile's epilogue is a plain
-    // read-add-write (one writer per element) instead of an L2 red.add
-    Args as1 = a;
-    fill_units(as1, BM, 128, num_sms(), 0.20, true);
-    const int waves1 = (as1.num_units + num_sms() - 1) / num_sms();
-    const double c_s128 = waves1 * as1.kb_per_split * 0.20 +
-                          (as1.splits > 1 ? as1.splits * static_cast<double>(as1.M) * as1.N * 4.0 /
-                                                kRedBytesPerUs
-                                          : 0.0);
     static const int forced_splits = [] {  // experiments: 256x256 pair tiles, this split count
       const char* e = std::getenv("CFT_WGRAD_SPLITS");
       return e ? std::atoi(e) : 0;
@@ -1182,9 +1171,6 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
       a.kb_per_split = (a.total_kb + forced_splits - 1) / forced_splits;
       a.splits = (a.total_kb + a.kb_per_split - 1) / a.kb_per_split;
       a.num_units = a.tiles_m * a.tiles_n * a.splits;
-    } else if (g_policy == 0 && sk_mode != 1 && c_s128 < 0.95 * std::min({c128, c256, cost_sk})) {
-      a = as1;
-      single128 = true;
     } else if (g_policy == 0 && sk_mode != 2 &&
         (sk_mode == 1 || cost_sk < 0.95 * std::min(c128, c256))) {
       a = ask;
@@ -1197,12 +1183,9 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   } else {
     fill_units(a, BM, BN, num_sms(), 0.45 * BN / 256.0, true);
   }
-  if (single128) pairs = false;
-  if (accumulate && a.splits == 1 && a.sk_len == 0) {
-    a.epi = kEpiF32Add;  // dw += result, one writer per element: read-add-write
-  } else if (accumulate) {
-    // dw += partial results: fire-and-forget red.add (the engine keeps its gradient
-    // accumulator zeroed between steps, so this is also its overwrite path)
+  if (accumulate) {
+    // dw += result: fire-and-forget red.add for any split count (the engine keeps its
+    // gradient accumulator zeroed between steps, so this is also its overwrite path)
     a.epi = kEpiF32Red;
   } else if (a.splits > 1 || a.sk_len > 0) {
     // partial sums race into dw: zero it first
@@ -1214,7 +1197,7 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   }
   if (pairs && pair_bn == 128) launch_2sm<true, true, 128>(ta, tb, a, stream);
   else if (pairs) launch_2sm<true, true, 256>(ta, tb, a, stream);
-  else if (BN == 256 && !single128) launch<true, true, 256>(ta, tb, a, stream);
+  else if (BN == 256) launch<true, true, 256>(ta, tb, a, stream);
   else launch<true, true, 128>(ta, tb, a, stream);
 }
 
