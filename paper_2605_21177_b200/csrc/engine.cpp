@@ -109,7 +109,6 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
   const int64_t rows = cfg_.batch_rows;
   CFT_CHECK(init_params != nullptr || kind_ == kLlamaModel,
             "engine: initial parameters required for this model");
-  if (cfg_.dtype == CFT_BF16) tc::prepare_workspace();  // before any graph capture
 
   // ---- plan + scheduler (partition.cpp:125-198, schedule.cpp:17-26) ----
   std::vector<host::TensorInfo> infos;

@@ -70,12 +70,6 @@ struct Args {
   // tile, (max, sum exp(v - max)) of the rounded outputs v -> ce_part[row * ce_stride + 2 tn + half]
   float2* ce_part;
   int ce_stride;
-  // split-K fixup (pair kernel, splits > 1): the splits of a tile run in order through a
-  // per-(tile, CTA) running sum in `fix_ws` (plain stores to L2) guarded by `fix_flag`; only
-  // the last split writes C, so C sees one pass (red.add for accumulate, else a plain store)
-  // instead of one red.add pass per split.  Flags return to 0 after the last split.
-  float* fix_ws;
-  unsigned* fix_flag;
 };
 
 // online (max, sum-exp) over 16 accumulator columns, on the bf16-rounded values the epilogue
@@ -781,67 +775,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // two TMEM loads in flight per wait: the epilogue of a single-wave GEMM (narrow
         // slices, split-K) is exposed after the mainloop and latency-bound
         float ce_m = -INFINITY, ce_s = 0.f;
-        if (args.fix_ws) {  // split-K fixup: this unit's split of tile (tm, tn)
-          const int sp = kb0_ / args.kb_per_split;
-          const int tile = tm * args.tiles_n + tn;
-          unsigned* flag = args.fix_flag + tile * 2 + rank;
-          float* ws = args.fix_ws + (static_cast<long long>(tile) * 2 + rank) * 128 * BNP +
-                      (quarter * 32 + lane) * BNP;
-          const bool last = sp == args.splits - 1;
-          if (sp > 0) {  // the previous split's running sum is complete
-            unsigned f;
-            do {
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
-            } while (f != static_cast<unsigned>(sp));
-          }
 #pragma unroll 1
-          for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 16) {
-            uint32_t r0[16];
-            ptx::tmem_ld16(tacc + c, r0);
-            ptx::tmem_wait_ld();
-            if (sp > 0) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float4 w = __ldcg(reinterpret_cast<const float4*>(ws + c) + q);
-                r0[4 * q] = __float_as_uint(__uint_as_float(r0[4 * q]) + w.x);
-                r0[4 * q + 1] = __float_as_uint(__uint_as_float(r0[4 * q + 1]) + w.y);
-                r0[4 * q + 2] = __float_as_uint(__uint_as_float(r0[4 * q + 2]) + w.z);
-                r0[4 * q + 3] = __float_as_uint(__uint_as_float(r0[4 * q + 3]) + w.w);
-              }
-            }
-            if (!last) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                __stcg(reinterpret_cast<float4*>(ws + c) + q,
-                       make_float4(__uint_as_float(r0[4 * q]), __uint_as_float(r0[4 * q + 1]),
-                                   __uint_as_float(r0[4 * q + 2]), __uint_as_float(r0[4 * q + 3])));
-            } else {
-              const int col = tn * BNP + c;
-              if (row_ok && col < args.N) store16(args, rbase, col, r0);
-            }
+        for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 32) {
+          uint32_t r0[16], r1[16];
+          ptx::tmem_ld16(tacc + c, r0);
+          ptx::tmem_ld16(tacc + c + 16, r1);
+          ptx::tmem_wait_ld();
+          const int col = tn * BNP + c;
+          if (args.ce_part) {
+            ce_accum16(r0, col, args.N, ce_m, ce_s);
+            ce_accum16(r1, col + 16, args.N, ce_m, ce_s);
           }
-          // every epilogue thread of this CTA is done with the running sum: publish / reset
-          __threadfence();
-          ptx::named_bar_sync(2, 32 * kEpiWarps);
-          if (warp == 2 && lane == 0) {
-            const unsigned nf = last ? 0u : static_cast<unsigned>(sp + 1);
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(nf) : "memory");
-          }
-        } else {
-#pragma unroll 1
-          for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 32) {
-            uint32_t r0[16], r1[16];
-            ptx::tmem_ld16(tacc + c, r0);
-            ptx::tmem_ld16(tacc + c + 16, r1);
-            ptx::tmem_wait_ld();
-            const int col = tn * BNP + c;
-            if (args.ce_part) {
-              ce_accum16(r0, col, args.N, ce_m, ce_s);
-              ce_accum16(r1, col + 16, args.N, ce_m, ce_s);
-            }
-            if (row_ok && col < args.N) store16(args, rbase, col, r0);
-            if (row_ok && col + 16 < args.N) store16(args, rbase, col + 16, r1);
-          }
+          if (row_ok && col < args.N) store16(args, rbase, col, r0);
+          if (row_ok && col + 16 < args.N) store16(args, rbase, col + 16, r1);
         }
         if (args.ce_part && row_ok)
           args.ce_part[static_cast<long long>(row) * args.ce_stride + 2 * tn + half] =
@@ -1167,39 +1113,6 @@ void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w,
 }
 
 // dW_S (+)= dY[:, rb:re)^T X -- slice-aware wgrad, fp32 out.
-namespace {
-int fix_mode() {  // experiments: CFT_WGRAD_FIXUP=0 keeps one red.add pass per split
-  static const int m = [] {
-    const char* e = std::getenv("CFT_WGRAD_FIXUP");
-    return e ? std::atoi(e) : 1;
-  }();
-  return m;
-}
-struct FixWorkspace {
-  float* ws = nullptr;
-  unsigned* flags = nullptr;
-};
-constexpr size_t kFixWsFloats = size_t{16} << 20;  // 64 MB: 256 pair tiles of 256 x 256 fp32
-constexpr size_t kFixFlags = 512;
-FixWorkspace* fix_workspace(bool allocate) {
-  static std::mutex mu;
-  static std::map<int, FixWorkspace> per_dev;
-  int dev = 0;
-  CFT_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = per_dev.find(dev);
-  if (it != per_dev.end()) return &it->second;
-  if (!allocate) return nullptr;
-  FixWorkspace w;
-  CFT_CUDA(cudaMalloc(&w.ws, kFixWsFloats * sizeof(float)));
-  CFT_CUDA(cudaMalloc(&w.flags, kFixFlags * sizeof(unsigned)));
-  CFT_CUDA(cudaMemset(w.flags, 0, kFixFlags * sizeof(unsigned)));
-  return &per_dev.emplace(dev, w).first->second;
-}
-}  // namespace
-
-void prepare_workspace() { fix_workspace(true); }
-
 void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const void* x,
                         int64_t in_dim, int64_t rb, int64_t re, float* dw, int accumulate,
                         cudaStream_t stream) {
@@ -1270,23 +1183,7 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   } else {
     fill_units(a, BM, BN, num_sms(), 0.45 * BN / 256.0, true);
   }
-  // split-K fixup for CTA-pair split tiles: the splits chain through the workspace and only
-  // the last one writes dw (one output pass instead of one red.add pass per split)
-  if (pairs && a.splits > 1 && a.sk_len == 0 && fix_mode() != 0) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    CFT_CUDA(cudaStreamIsCapturing(stream, &cs));
-    FixWorkspace* w = fix_workspace(cs == cudaStreamCaptureStatusNone);
-    const int tiles = a.tiles_m * a.tiles_n;
-    const int bnp = pair_bn;
-    if (w && static_cast<size_t>(tiles) * 2 <= kFixFlags &&
-        static_cast<size_t>(tiles) * 2 * 128 * bnp <= kFixWsFloats) {
-      a.fix_ws = w->ws;
-      a.fix_flag = w->flags;
-    }
-  }
-  if (a.fix_ws) {
-    a.epi = accumulate ? kEpiF32Red : kEpiF32;  // one writer per element
-  } else if (accumulate) {
+  if (accumulate) {
     // dw += result: fire-and-forget red.add for any split count (the engine keeps its
     // gradient accumulator zeroed between steps, so this is also its overwrite path)
     a.epi = kEpiF32Red;

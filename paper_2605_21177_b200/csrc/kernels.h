@@ -39,9 +39,6 @@ bool linear_fwd_rope(const void* x, int64_t n_tok, int64_t in_dim, const void* w
                      void* y, const float2* cs, int seq, int hd, int64_t rope_cols,
                      cudaStream_t stream);
 void set_fusion(int on);
-// allocate this device's split-K fixup workspace now (engines call it before capturing graphs;
-// a wgrad launched inside a capture without it falls back to one red.add pass per split)
-void prepare_workspace();
 }  // namespace tc
 
 namespace simt {  // gemm_simt.cu: fp32 / bf16 CUDA-core GEMMs and column sums
