@@ -1182,23 +1182,64 @@ std::string chunk_file(const std::string& dir, int c) {
   std::snprintf(name, sizeof(name), "chunk_%04d.bin", c);
   return dir + "/" + name;
 }
+// sharded optimizer state: one file per (chunk, rank) holding that rank's contiguous part of
+// the chunk's master / m / v (the CKFT v1 header with E = the shard's element count); the
+// shards of a chunk concatenate to exactly the unsharded chunk file's three vectors
+std::string shard_file(const std::string& dir, int c, int rank, int world) {
+  char name[64];
+  std::snprintf(name, sizeof(name), "chunk_%04d.shard%03dof%03d.bin", c, rank, world);
+  return dir + "/" + name;
+}
+
+// CKFT v1 body reader: header checks with the reference's messages (optimizer.cpp:231-251)
+void read_ckft(const std::string& path, uint64_t want_hash, int32_t want_chunk, int64_t want_E,
+               uint64_t* nl, std::vector<double>* wide) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  CFT_CHECK(f != nullptr, "checkpoint: cannot open '" + path + "'");
+  char magic[4];
+  uint32_t version = 0;
+  uint64_t hash = 0;
+  int32_t chunk = -1;
+  int64_t E = -1;
+  const bool hdr = std::fread(magic, 1, 4, f) == 4;
+  if (!hdr || std::memcmp(magic, kMagic, 4) != 0) {
+    std::fclose(f);
+    throw Error("checkpoint: bad magic in '" + path + "'");
+  }
+  if (std::fread(&version, 4, 1, f) != 1 || version != kVersion) {
+    std::fclose(f);
+    throw Error("checkpoint: unsupported version");
+  }
+  if (std::fread(&hash, 8, 1, f) != 1 || hash != want_hash) {
+    std::fclose(f);
+    throw Error("checkpoint: plan hash mismatch (checkpoint belongs to a different plan)");
+  }
+  wide->assign(3 * std::max<int64_t>(want_E, 0), 0.0);
+  const bool body = std::fread(&chunk, 4, 1, f) == 1 && std::fread(nl, 8, 1, f) == 1 &&
+                    std::fread(&E, 8, 1, f) == 1 && E == want_E &&
+                    std::fread(wide->data(), 8, wide->size(), f) == wide->size();
+  std::fclose(f);
+  CFT_CHECK(body && chunk == want_chunk, "checkpoint: truncated payload");
+}
 }  // namespace
 
+// One file per chunk (optimizer.cpp:210-230), or per (chunk, rank) with sharded state.
 void Engine::write_checkpoints(const std::string& dir) {
   CFT_CHECK(finished_, "checkpoint: flush chunk to host tier first");
-  CFT_CHECK(!sharded(), "checkpoint: states are sharded across ranks");
   const uint64_t hash = host::plan_hash(plan_);
   const size_t S = ssz();
   for (int c = 0; c < cfg_.K; ++c) {
-    const int64_t n = plan_.chunks[c].elements;
+    const int64_t n = st_n_[c];  // the whole chunk, or this rank's shard
     std::vector<char> raw(n * 3 * S);
-    CFT_CUDA(cudaMemcpy(raw.data(), host_states_[c], raw.size(),
-                        cfg_.offload ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+    if (n > 0)
+      CFT_CUDA(cudaMemcpy(raw.data(), host_states_[c], raw.size(),
+                          cfg_.offload ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
     std::vector<double> wide(n * 3);
     for (int64_t i = 0; i < 3 * n; ++i)
       wide[i] = S == 8 ? reinterpret_cast<double*>(raw.data())[i]
                        : static_cast<double>(reinterpret_cast<float*>(raw.data())[i]);
-    const std::string path = chunk_file(dir, c);
+    const std::string path = sharded() ? shard_file(dir, c, cfg_.shard_rank, cfg_.shard_world)
+                                       : chunk_file(dir, c);
     FILE* f = std::fopen(path.c_str(), "wb");
     CFT_CHECK(f != nullptr, "checkpoint: cannot open '" + path + "' for writing");
     const int32_t chunk = c;
@@ -1213,66 +1254,65 @@ void Engine::write_checkpoints(const std::string& dir) {
   }
 }
 
+// Restore chunk by chunk: this rank's states from its file, and the chunk's parameters from
+// the chunk's masters (every shard of the chunk with sharded state) through a device staging
+// buffer of one chunk -- no full-model host or device copy.
 void Engine::read_checkpoints(const std::string& dir) {
   CFT_CHECK(t_ == 0 && !finished_, "checkpoint: restore before the first step");
-  CFT_CHECK(!sharded(), "checkpoint: states are sharded across ranks");
   const uint64_t want = host::plan_hash(plan_);
-  const size_t S = ssz();
-  std::vector<double> params(param_elems_);
-  params_device(params.data());  // start from the current values (frozen tensors keep theirs)
-  for (int c = 0; c < cfg_.K; ++c) {
-    const std::string path = chunk_file(dir, c);
-    FILE* f = std::fopen(path.c_str(), "rb");
-    CFT_CHECK(f != nullptr, "checkpoint: cannot open '" + path + "'");
-    char magic[4];
-    uint32_t version = 0;
-    uint64_t hash = 0, nl = 0;
-    int32_t chunk = -1;
-    int64_t E = -1;
-    const bool hdr = std::fread(magic, 1, 4, f) == 4;
-    if (!hdr || std::memcmp(magic, kMagic, 4) != 0) {
-      std::fclose(f);
-      throw Error("checkpoint: bad magic in '" + path + "'");
+  const size_t S = ssz(), E = esz();
+  const int W = cfg_.shard_world;
+  double* dev = nullptr;
+  CFT_CUDA(cudaMalloc(&dev, std::max<int64_t>(max_chunk_, 1) * 8));
+  try {
+    for (int c = 0; c < cfg_.K; ++c) {
+      const int64_t n = plan_.chunks[c].elements;
+      std::vector<double> masters(n), mine;
+      uint64_t nl = 0;
+      if (!sharded()) {
+        read_ckft(chunk_file(dir, c), want, c, n, &nl, &mine);
+        std::copy(mine.begin(), mine.begin() + n, masters.begin());
+      } else {
+        for (int r = 0; r < W; ++r) {
+          const int64_t lo = std::min(n, r * sh_size_[c]);
+          const int64_t sn = std::min(n - lo, sh_size_[c]);
+          std::vector<double> part;
+          uint64_t pnl = 0;
+          read_ckft(shard_file(dir, c, r, W), want, c, sn, &pnl, &part);
+          CFT_CHECK(r == 0 || pnl == nl, "checkpoint: shards disagree on the local step count");
+          nl = pnl;
+          std::copy(part.begin(), part.begin() + sn, masters.begin() + lo);
+          if (r == cfg_.shard_rank) mine.swap(part);
+        }
+      }
+      n_local_[c] = nl;
+      const int64_t sn = st_n_[c];
+      std::vector<char> raw(sn * 3 * S);
+      for (int64_t i = 0; i < 3 * sn; ++i) {
+        if (S == 8) reinterpret_cast<double*>(raw.data())[i] = mine[i];
+        else reinterpret_cast<float*>(raw.data())[i] = static_cast<float>(mine[i]);
+      }
+      if (sn > 0)
+        CFT_CUDA(cudaMemcpy(host_states_[c], raw.data(), raw.size(),
+                            cfg_.offload ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice));
+      // masters are the authoritative parameters: this chunk's slices, converted in place
+      CFT_CUDA(cudaMemcpy(dev, masters.data(), n * 8, cudaMemcpyHostToDevice));
+      for (const auto& s : chunk_slices_[c]) {
+        void* dst = static_cast<char*>(params_) + s.param_off * E;
+        if (cfg_.dtype == CFT_F64)
+          CFT_CUDA(cudaMemcpyAsync(dst, dev + s.aux_off, s.count * 8, cudaMemcpyDeviceToDevice,
+                                   stream_));
+        else if (cft_convert(CFT_F64, dev + s.aux_off, static_cast<cft_dtype>(cfg_.dtype), dst,
+                             s.count, stream_) != CFT_OK)
+          throw Error(last_error());
+      }
+      CFT_CUDA(cudaStreamSynchronize(stream_));
     }
-    if (std::fread(&version, 4, 1, f) != 1 || version != kVersion) {
-      std::fclose(f);
-      throw Error("checkpoint: unsupported version");
-    }
-    if (std::fread(&hash, 8, 1, f) != 1 || hash != want) {
-      std::fclose(f);
-      throw Error("checkpoint: plan hash mismatch (checkpoint belongs to a different plan)");
-    }
-    const int64_t n = plan_.chunks[c].elements;
-    std::vector<double> wide(3 * n);
-    const bool body = std::fread(&chunk, 4, 1, f) == 1 && std::fread(&nl, 8, 1, f) == 1 &&
-                      std::fread(&E, 8, 1, f) == 1 && E == n &&
-                      std::fread(wide.data(), 8, wide.size(), f) == wide.size();
-    std::fclose(f);
-    CFT_CHECK(body && chunk == c, "checkpoint: truncated payload");
-    n_local_[c] = nl;
-    std::vector<char> raw(n * 3 * S);
-    for (int64_t i = 0; i < 3 * n; ++i) {
-      if (S == 8) reinterpret_cast<double*>(raw.data())[i] = wide[i];
-      else reinterpret_cast<float*>(raw.data())[i] = static_cast<float>(wide[i]);
-    }
-    CFT_CUDA(cudaMemcpy(host_states_[c], raw.data(), raw.size(),
-                        cfg_.offload ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice));
-    for (const auto& s : chunk_slices_[c])  // masters are the authoritative parameters
-      std::memcpy(params.data() + s.param_off, wide.data() + s.aux_off, s.count * 8);
+  } catch (...) {
+    cudaFree(dev);
+    throw;
   }
-  // refresh the compute-dtype parameter arena from the restored masters
-  void* tmp;
-  CFT_CUDA(cudaMalloc(&tmp, param_elems_ * 8));
-  CFT_CUDA(cudaMemcpy(tmp, params.data(), param_elems_ * 8, cudaMemcpyHostToDevice));
-  if (cfg_.dtype == CFT_F64) {
-    CFT_CUDA(cudaMemcpy(params_, tmp, param_elems_ * 8, cudaMemcpyDeviceToDevice));
-  } else if (cft_convert(CFT_F64, tmp, static_cast<cft_dtype>(cfg_.dtype), params_, param_elems_,
-                         stream_) != CFT_OK) {
-    cudaFree(tmp);
-    throw Error(last_error());
-  }
-  CFT_CUDA(cudaStreamSynchronize(stream_));
-  cudaFree(tmp);
+  cudaFree(dev);
 }
 
 void Engine::chunk_counters(uint64_t* n) const {

@@ -124,6 +124,11 @@ void rms_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, long long rows, int
 void rms_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd,
              const __nv_bfloat16* g, const __nv_bfloat16* res, long long rows, int d,
              __nv_bfloat16* out, cudaStream_t s);
+// rms_bwd fused with the weight's gradient slice dgamma[j - rb] += ... (false: d not one of
+// the register kernels' widths -- run rms_bwd + rms_dgamma)
+bool rms_bwd_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd,
+                    const __nv_bfloat16* g, const __nv_bfloat16* res, long long rows, int d,
+                    __nv_bfloat16* out, long long rb, long long re, float* dgamma, cudaStream_t s);
 void rms_dgamma(const __nv_bfloat16* dy, const __nv_bfloat16* x, const float* rstd,
                 long long rows, int d, long long rb, long long re, float* out, cudaStream_t s);
 void rope_prepare(int seq, int hd, float theta);  // build the cos/sin table (not capturable)

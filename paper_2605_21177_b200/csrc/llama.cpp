@@ -366,19 +366,31 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     gemm_work(kDgrad, N, d, V, 2.0 * N * d, 0);
     tc::linear_dgrad(dlog, N, V, P(head_id), d, l_dxf_, 0, st);
     pe();
-    if (const SliceRt* s = slice_of(norm_id)) {
-      pb(kBwdOther);
-      llama::rms_dgamma(static_cast<bf16*>(l_dxf_), static_cast<bf16*>(lb_[L].x), l_rstdf_, N,
-                        S.d, s->rb, s->re, aux_at(s), st);
-      pe();
-    }
   }
-  if (below(norm_id)) {
+  // RMSNorm backward of `tensor` (dy -> out = res + dx), fused with the weight's gradient slice
+  // when the chunk holds one; false: nothing below needs dx (the dgamma slice still runs)
+  auto norm_bwd = [&](int tensor, const void* dy, const void* x, const float* rstd,
+                      const void* res, void* out) {
+    const SliceRt* s = slice_of(tensor);
+    const bool bwd = below(tensor);
     pb(kBwdOther);
-    llama::rms_bwd(static_cast<bf16*>(l_dxf_), static_cast<bf16*>(lb_[L].x), l_rstdf_, P(norm_id),
-                   nullptr, N, S.d, static_cast<bf16*>(l_gx_), st);
+    if (s && bwd &&
+        llama::rms_bwd_dgamma(static_cast<const bf16*>(dy), static_cast<const bf16*>(x), rstd,
+                              P(tensor), static_cast<const bf16*>(res), N, S.d,
+                              static_cast<bf16*>(out), s->rb, s->re, aux_at(s), st)) {
+      pe();
+      return true;
+    }
+    if (s)
+      llama::rms_dgamma(static_cast<const bf16*>(dy), static_cast<const bf16*>(x), rstd, N, S.d,
+                        s->rb, s->re, aux_at(s), st);
+    if (bwd)
+      llama::rms_bwd(static_cast<const bf16*>(dy), static_cast<const bf16*>(x), rstd, P(tensor),
+                     static_cast<const bf16*>(res), N, S.d, static_cast<bf16*>(out), st);
     pe();
-  }
+    return bwd;
+  };
+  if (need(norm_id)) norm_bwd(norm_id, l_dxf_, lb_[L].x, l_rstdf_, nullptr, l_gx_);
   for (int l = L - 1; l >= 0 && below(id(l, 8) + 1); --l) {
     LlamaLayerBufs& z = lb_[l];
     if (cfg_.remat && l < L - 1) layer_fwd(l, stop <= id(l, 7), false);  // re-materialise
@@ -403,17 +415,8 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     gemm_work(kDgrad, N, d, 2 * F, 2.0 * N * d, 0);
     tc::linear_dgrad(l_dug_, N, 2 * F, P(id(l, 6)), d, l_da_, 0, st);  // dM (reuses da buffer)
     pe();
-    if (const SliceRt* s = slice_of(id(l, 5))) {
-      pb(kBwdOther);
-      llama::rms_dgamma(static_cast<bf16*>(l_da_), static_cast<bf16*>(z.h), z.rstd2, N, S.d, s->rb,
-                        s->re, aux_at(s), st);
-      pe();
-    }
-    if (!below(id(l, 5))) break;
-    pb(kBwdOther);  // GH = GX + rms_bwd(dM)
-    llama::rms_bwd(static_cast<bf16*>(l_da_), static_cast<bf16*>(z.h), z.rstd2, P(id(l, 5)),
-                   static_cast<bf16*>(l_gx_), N, S.d, static_cast<bf16*>(l_gh_), st);
-    pe();
+    // GH = GX + rms_bwd(dM)
+    if (!norm_bwd(id(l, 5), l_da_, z.h, z.rstd2, l_gx_, l_gh_)) break;
     // h = x + o Wo^T
     wgrad(id(l, 4), l_gh_, d, z.o, Q, 0);
     if (!need(id(l, 3))) break;
@@ -438,17 +441,8 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     gemm_work(kDgrad, N, d, QKV, 2.0 * N * d, 0);
     tc::linear_dgrad(l_dqkv_, N, QKV, P(id(l, 1)), d, l_da_, 0, st);  // dA
     pe();
-    if (const SliceRt* s = slice_of(id(l, 0))) {
-      pb(kBwdOther);
-      llama::rms_dgamma(static_cast<bf16*>(l_da_), static_cast<bf16*>(z.x), z.rstd1, N, S.d, s->rb,
-                        s->re, aux_at(s), st);
-      pe();
-    }
-    if (!below(id(l, 0))) break;
-    pb(kBwdOther);  // GX = GH + rms_bwd(dA)
-    llama::rms_bwd(static_cast<bf16*>(l_da_), static_cast<bf16*>(z.x), z.rstd1, P(id(l, 0)),
-                   static_cast<bf16*>(l_gh_), N, S.d, static_cast<bf16*>(l_gx_), st);
-    pe();
+    // GX = GH + rms_bwd(dA)
+    if (!norm_bwd(id(l, 0), l_da_, z.x, z.rstd1, l_gh_, l_gx_)) break;
   }
   if (const SliceRt* s = slice_of(0)) {  // embedding rows: one pass over positions
     pb(kBwdOther);

@@ -170,6 +170,74 @@ __global__ void rms_bwd_reg_kernel(const bf16* __restrict__ dy, const bf16* __re
   }
 }
 
+// rms_bwd_reg_kernel over R consecutive rows per block, also forming the RMSNorm weight's
+// gradient slice dgamma[j - rb] += sum_b dy[b,j] * x[b,j] * rstd[b], j in [rb, re)
+// (kernels_serial.cpp:132-143 with mean = 0) from the same registers: one atomicAdd per
+// column per block instead of a second pass over dy and x
+template <int VPT, int R>
+__global__ void rms_bwd_dg_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                  const float* __restrict__ rstd, const bf16* __restrict__ g,
+                                  const bf16* res, int d, long long rows, bf16* out,
+                                  long long rb, long long re, float* dgamma) {
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  float acc[VPT][8];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[k][e] = 0.f;
+  const long long r0 = static_cast<long long>(blockIdx.x) * R;
+  for (int q = 0; q < R && r0 + q < rows; ++q) {
+    const long long r = r0 + q;
+    const float rs = rstd[r];
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + r * d);
+    const uint4* xr = reinterpret_cast<const uint4*>(x + r * d);
+    uint4 dv[VPT], xv[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      dv[k] = __ldcs(dyr + threadIdx.x + k * blockDim.x);
+      xv[k] = xr[threadIdx.x + k * blockDim.x];
+    }
+    float c = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      float a[8], b[8], gg[8];
+      unpack8(dv[k], a);
+      unpack8(xv[k], b);
+      unpack8(gr[threadIdx.x + k * blockDim.x], gg);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        c += gg[e] * a[e] * b[e] * rs;
+        acc[k][e] += a[e] * b[e] * rs;
+      }
+    }
+    c = block_sum_small<VPT>(c) / d;
+    const uint4* rr = res ? reinterpret_cast<const uint4*>(res + r * d) : nullptr;
+    uint4* orow = reinterpret_cast<uint4*>(out + r * d);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int j = threadIdx.x + k * blockDim.x;
+      float a[8], b[8], gg[8], o[8];
+      unpack8(dv[k], a);
+      unpack8(xv[k], b);
+      unpack8(gr[j], gg);
+      if (rr) unpack8(rr[j], o);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float v = rs * (gg[e] * a[e] - b[e] * rs * c);
+        o[e] = rr ? o[e] + v : v;
+      }
+      orow[j] = pack8(o);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const long long j0 = static_cast<long long>(threadIdx.x + k * blockDim.x) * 8;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (j0 + e >= rb && j0 + e < re) atomicAdd(dgamma + (j0 + e - rb), acc[k][e]);
+  }
+}
+
 // dx = res + rstd * (g*dy - xhat * sum(g*dy*xhat)/d), xhat = x*rstd   (out may alias res)
 __global__ void rms_bwd_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                                const float* __restrict__ rstd, const bf16* __restrict__ g,
@@ -355,6 +423,23 @@ void rms_bwd(const bf16* dy, const bf16* x, const float* rstd, const bf16* g, co
   else if (k == 1) rms_bwd_reg_kernel<1><<<(unsigned)rows, th, 0, s>>>(dy, x, rstd, g, res, d, out);
   else rms_bwd_kernel<<<(unsigned)rows, row_threads(d), 0, s>>>(dy, x, rstd, g, res, d, out);
   check_launch("rms_bwd");
+}
+bool rms_bwd_dgamma(const bf16* dy, const bf16* x, const float* rstd, const bf16* g,
+                    const bf16* res, long long rows, int d, bf16* out, long long rb,
+                    long long re, float* dgamma, cudaStream_t s) {
+  const int k = rms_vpt(d);
+  if (k == 0) return false;  // the register kernels' shapes only
+  const unsigned th = static_cast<unsigned>(d / 8 / k);
+  constexpr int R = 16;
+  const unsigned grid = static_cast<unsigned>((rows + R - 1) / R);
+  if (k == 4)
+    rms_bwd_dg_kernel<4, R><<<grid, th, 0, s>>>(dy, x, rstd, g, res, d, rows, out, rb, re, dgamma);
+  else if (k == 2)
+    rms_bwd_dg_kernel<2, R><<<grid, th, 0, s>>>(dy, x, rstd, g, res, d, rows, out, rb, re, dgamma);
+  else
+    rms_bwd_dg_kernel<1, R><<<grid, th, 0, s>>>(dy, x, rstd, g, res, d, rows, out, rb, re, dgamma);
+  check_launch("rms_bwd_dgamma");
+  return true;
 }
 void rms_dgamma(const bf16* dy, const bf16* x, const float* rstd, long long rows, int d,
                 long long rb, long long re, float* out, cudaStream_t s) {

@@ -534,11 +534,15 @@ class ChunkEngine:
         return {k: float(ms[i]) for i, k in enumerate(self.PHASES)}
 
     def write_checkpoints(self, directory: str):
-        """CKFT v1 files dir/chunk_NNNN.bin (optimizer.cpp:210-230); call after finish()."""
+        """CKFT v1 files dir/chunk_NNNN.bin (optimizer.cpp:210-230); call after finish().  With
+        sharded state every rank writes dir/chunk_NNNN.shardRRRofWWW.bin (its part of each
+        chunk's master / m / v; merge_shard_checkpoints joins them into reference files)."""
         N.check(_L.cft_engine_write_checkpoints(self._h, directory.encode()), "checkpoint")
 
     def read_checkpoints(self, directory: str):
-        """Resume from CKFT v1 files (optimizer.cpp:232-251) before the first step."""
+        """Resume from CKFT v1 files (optimizer.cpp:232-251) before the first step; with
+        sharded state from the per-rank shard files (each rank reads every shard's masters to
+        restore its replicated parameters, and its own shard's state)."""
         N.check(_L.cft_engine_read_checkpoints(self._h, directory.encode()), "checkpoint")
 
     def wait_step(self, t: int):
@@ -551,6 +555,31 @@ class ChunkEngine:
         N.check(_L.cft_engine_phase_ms(self._h, out.ctypes.data))
         return dict(inputs=float(out[0]), forward=float(out[1]), backward=float(out[2]),
                     update=float(out[3]))
+
+
+def merge_shard_checkpoints(directory: str, K: int, world: int) -> None:
+    """Join the per-rank shard files of a sharded-state run into the reference's per-chunk
+    CKFT v1 files (FORMATS.md:176-194): same header (n, plan hash), E = the chunk's elements,
+    master | m | v each the concatenation of the ranks' parts."""
+    import os
+    import struct
+    hdr = struct.Struct("<4sIQiQq")
+    for c in range(K):
+        parts, head = [], None
+        for r in range(world):
+            with open(os.path.join(directory, f"chunk_{c:04d}.shard{r:03d}of{world:03d}.bin"), "rb") as f:
+                raw = f.read()
+            magic, ver, h, chunk, n, E = hdr.unpack_from(raw)
+            if magic != b"CKFT" or chunk != c:
+                raise Error(f"checkpoint: bad shard file for chunk {c}")
+            if head is not None and (h, n) != head:
+                raise Error("checkpoint: shards disagree on the plan hash or local step count")
+            head = (h, n)
+            parts.append(np.frombuffer(raw, np.float64, 3 * E, hdr.size).reshape(3, E))
+        body = np.concatenate(parts, axis=1)
+        with open(os.path.join(directory, f"chunk_{c:04d}.bin"), "wb") as f:
+            f.write(hdr.pack(b"CKFT", 1, head[0], c, head[1], body.shape[1]))
+            f.write(np.ascontiguousarray(body).tobytes())
 
 
 def _wrap_device(ptr: int, n: int, dtype) -> torch.Tensor:

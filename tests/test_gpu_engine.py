@@ -449,6 +449,75 @@ def test_checkpoint_resume_continues_bit_identically(cuda, tmp_path):
         c.read_checkpoints(str(tmp_path))
 
 
+@pytest.mark.parametrize("offload", [True, False])
+def test_sharded_checkpoints_merge_to_reference_files_and_resume(cuda, offload, tmp_path):
+    """Sharded optimizer state (the configs[4] mode): two stand-in ranks write per-rank shard
+    files; merged, they are byte-identical to the unsharded DP run's CKFT files (which equal
+    the reference's micro_batches = 2 run, test above); two new sharded ranks resume from the
+    shards and continue bit-identically to the uninterrupted run (fp64)."""
+    from paper_2605_21177_b200.engine import ChunkEngine, merge_shard_checkpoints
+    case = CASES["linear_dp2"]
+    bs = batches_of(case)
+    steps = case["steps"]
+
+    def ranks(total, sharded):
+        engs = []
+        for r in range(2):
+            opts = options_of(case, "fp64", offload=offload)
+            opts.micro_batches = 1
+            opts.schedule.total_steps = total
+            if sharded:
+                opts.shard_rank, opts.shard_world = r, 2
+            e = ChunkEngine(model_of(case), np.array(case["init_params"]), 5, opts)
+            e.set_grad_scale(0.5)
+            engs.append(e)
+        return engs
+
+    def run(engs, t0, t1, sharded):
+        staged = [[e.stage(b, device=True) for b in bs] for e in engs]
+        for t in range(t0, t1):
+            for r, e in enumerate(engs):
+                e.step_begin()
+                e.forward_backward(staged[r][(2 * t + r) % len(bs)], 0)
+            if sharded:
+                _sharded_exchange(engs)
+            else:
+                torch.cuda.synchronize()
+                g0, g1 = engs[0].grad_tensor(), engs[1].grad_tensor()
+                s = g0 + g1
+                g0.copy_(s)
+                g1.copy_(s)
+                torch.cuda.synchronize()
+                for e in engs:
+                    e.step_end()
+        for e in engs:
+            e.finish()
+
+    half = steps // 2
+    rep = ranks(half, False)
+    run(rep, 0, half, False)
+    (tmp_path / "rep").mkdir()
+    rep[0].write_checkpoints(str(tmp_path / "rep"))
+    sh = ranks(half, True)
+    run(sh, 0, half, True)
+    (tmp_path / "sh").mkdir()
+    for e in sh:
+        e.write_checkpoints(str(tmp_path / "sh"))
+    K = case["K"]
+    merge_shard_checkpoints(str(tmp_path / "sh"), K, 2)
+    for c in range(K):
+        fn = f"chunk_{c:04d}.bin"
+        assert (tmp_path / "sh" / fn).read_bytes() == (tmp_path / "rep" / fn).read_bytes()
+    full = ranks(steps, True)
+    run(full, 0, steps, True)
+    res = ranks(steps - half, True)
+    for e in res:
+        e.read_checkpoints(str(tmp_path / "sh"))
+    run(res, half, steps, True)
+    assert np.array_equal(res[0].params(from_masters=False), full[0].params(from_masters=False))
+    assert np.array_equal(res[1].params(from_masters=False), full[1].params(from_masters=False))
+
+
 @pytest.mark.parametrize("clip_rel", [0.25, 1e6])
 def test_fp64_engine_gradient_clipping(cuda, clip_rel):
     """Global-norm clipping inside the fused AdamW (the build's addition; the reference has no
