@@ -275,6 +275,62 @@ def test_llama_production_shapes_chunk_gradients(cuda):
         assert err < 2e-2, (c, err)
 
 
+def test_llama_production_shapes_post_step_weights(cuda):
+    """eta > 0 at the Llama-3-8B layer shapes (2 layers, seq 1024, 2 sequences, K = 5): one
+    full rotation, every chunk updated once at the parameters the previous steps left.  The
+    restatement replays it: torch fp32 autograd at the bf16 parameters -> the chunk's slice of
+    the gradient -> the reference AdamW (oracle/chunkft_oracle.c, pinned to
+    src/optimizer.cpp:163-198) on fp32-rounded masters -> bf16 parameters.  Post-step masters
+    of every chunk within the north star's bf16 bar (normwise 2e-2), and the update itself
+    (master - init) agreeing in sign wherever the reference gradient is not tiny."""
+    from oracle import lib as orc
+    from paper_2605_21177_b200.engine import AdamWHyper, ChunkEngine, LlamaModel, TrainOptions
+    from paper_2605_21177_b200.plan import ScheduleConfig, TensorInfo, partition
+    model = LlamaModel.llama3_8b(layers=2)
+    B, K, eta = 2, 5, 1e-3
+    rng = np.random.default_rng(23)
+    flat = np.concatenate([np.ones(r) if c == 1 else
+                           (rng.random(r * c, dtype=np.float32) - 0.5) / math.sqrt(c)
+                           for _, r, c in model.tensors()])
+    seqs = rng.integers(0, model.vocab, (B, model.seq + 1)).astype(np.int32)
+    tokens, labels = seqs[:, :-1].copy(), seqs[:, 1:].copy()
+    infos = [TensorInfo(i, n, r, c) for i, (n, r, c) in enumerate(model.tensors())]
+    plan = partition(infos, K)
+    offs = np.cumsum([0] + [r * c for _, r, c in model.tensors()])
+    opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=K), dtype="bf16",
+                        hyper=AdamWHyper(eta, 0.9, 0.999, 1e-8, 0.0))
+    eng = ChunkEngine(model, flat, B, opts)
+    batch = eng.stage({"tokens": tokens, "labels": labels}, device=True)
+    for _ in range(K):
+        eng.step([batch])
+    eng.finish()
+    got = eng.params(from_masters=True)
+
+    def idx(c):
+        return np.concatenate([np.arange(offs[s.tensor_id] + s.row_begin * infos[s.tensor_id].cols,
+                                         offs[s.tensor_id] + s.row_end * infos[s.tensor_id].cols)
+                               for s in plan.chunks[c].slices])
+    masters = flat.astype(np.float32).astype(np.float64)
+    for c in range(K):
+        _, g = torch_reference(model, masters, tokens, labels)
+        ix = idx(c)
+        e = ix.size
+        new, _, _, n, _, _ = orc.adamw(masters[ix], np.zeros(e), np.zeros(e), g[ix], 0, eta=eta)
+        assert n == 1
+        want_g = g
+        masters = masters.copy()
+        masters[ix] = new
+        ref = masters[ix]
+        mine = got[ix]
+        err = np.linalg.norm(mine - ref) / np.linalg.norm(ref)
+        assert err < 2e-2, (c, err)
+        d_ref = ref - flat[ix].astype(np.float32)
+        d_got = mine - flat[ix].astype(np.float32)
+        big = np.abs(want_g[ix]) > 0.05 * np.abs(want_g[ix]).max()
+        agree = np.mean(np.sign(d_ref[big]) == np.sign(d_got[big]))
+        assert agree > 0.99, (c, agree)
+
+
 @pytest.mark.parametrize("graphs", [False, True], ids=["eager", "graphs"])
 def test_llama_rematerialisation_matches_resident(cuda, graphs):
     """remat = 1 keeps only each layer's input and recomputes the backward suffix's layers one at
