@@ -310,6 +310,13 @@ int cft_set_fusion(int enable);
  * (default).  op 2 tcgen05 GEMM launches: 0 ordinary, 1 programmatic dependent launch
  * (default; the prologue overlaps the previous kernel's tail). */
 int cft_set_kernel_variant(int op, int variant);
+/* Deterministic mode (process-wide, default off; env CFT_DETERMINISTIC=1): every reduction of
+ * the bf16 / fp32 paths runs in a fixed order -- no split-K or stream-K GEMMs, an embedding
+ * scatter that walks positions in ascending order per row block, a single-pass RMSNorm dgamma
+ * -- so gradients and parameters are bitwise reproducible run to run, as the reference's
+ * serial / OpenMP backends are (kernels.hpp:8-12).  Set it before an engine captures its
+ * graphs.  (Scalar loss / gradient-norm sums may still differ in the last bits.) */
+int cft_set_deterministic(int on);
 
 /* Element conversion (e.g. fp32 master -> bf16 params at init). */
 int cft_convert(cft_dtype src_dtype, const void* src, cft_dtype dst_dtype, void* dst, int64_t n,

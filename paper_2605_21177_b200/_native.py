@@ -85,6 +85,7 @@ _sig("cft_embedding_gather", C.c_int, C.c_int, vp, i64, i64, vp, i64, vp, vp, vp
 _sig("cft_embedding_scatter_slice", C.c_int, C.c_int, vp, i64, vp, i64, i64, i64, vp, vp, vp)
 _sig("cft_grad_stats", C.c_int, C.c_int, vp, i64, f64, vp, vp)
 _sig("cft_set_kernel_variant", C.c_int, C.c_int, C.c_int)
+_sig("cft_set_deterministic", C.c_int, C.c_int)
 _sig("cft_softmax_ce", C.c_int, C.c_int, vp, vp, i64, i64, vp, vp, vp, vp)
 _sig("cft_attention_fwd", C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp)
 _sig("cft_attention_bwd", C.c_int, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

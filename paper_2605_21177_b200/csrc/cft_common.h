@@ -62,6 +62,12 @@ inline int num_sms() {
 constexpr int kNumVariantOps = 3;
 int& kernel_variant(int op);
 
+// Deterministic mode (cft_set_deterministic): every reduction in a fixed order, so a step's
+// gradients and parameters are bitwise reproducible run to run (the reference's backends are,
+// kernels.hpp:8-12): no split-K / stream-K GEMMs, an ordered embedding scatter, a
+// single-pass RMSNorm dgamma.  Off by default (the faster atomic reductions).
+bool& deterministic();
+
 inline void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw Error(std::string(what) + ": " + cudaGetErrorString(e));

@@ -55,6 +55,14 @@ CUtensorMap make_tmap_bf16(const void* base, uint64_t inner, uint64_t outer,
   return m;
 }
 
+bool& deterministic() {
+  static bool d = [] {
+    const char* e = std::getenv("CFT_DETERMINISTIC");
+    return e && std::string(e) == "1";
+  }();
+  return d;
+}
+
 int& kernel_variant(int op) {
   static int v[kNumVariantOps] = {
       [] {
@@ -82,6 +90,11 @@ int cft_set_kernel_variant(int op, int variant) {
     CFT_CHECK(variant >= 0 && variant <= 1, "cft_set_kernel_variant: variant out of range");
     cft::kernel_variant(op) = variant;
   });
+}
+
+int cft_set_deterministic(int on) {
+  cft::deterministic() = on != 0;
+  return CFT_OK;
 }
 
 const char* cft_last_error(void) { return cft::t_err.c_str(); }

@@ -878,7 +878,7 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream_t s
 // s fp32 red-adds of the output through L2 (~2 TB/s measured for red.global.add.v4.f32).
 int choose_splits(int tiles, int slots, int total_kb, long long out_elems, double us_per_kb,
                   bool allow) {
-  if (!allow || tiles >= slots) return 1;
+  if (!allow || tiles >= slots || deterministic()) return 1;
   double best_t = 1e30;
   int best = 1;
   for (int s = 1; s <= 16; ++s) {
@@ -1171,7 +1171,7 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
       a.kb_per_split = (a.total_kb + forced_splits - 1) / forced_splits;
       a.splits = (a.total_kb + a.kb_per_split - 1) / a.kb_per_split;
       a.num_units = a.tiles_m * a.tiles_n * a.splits;
-    } else if (g_policy == 0 && sk_mode != 2 &&
+    } else if (g_policy == 0 && sk_mode != 2 && !deterministic() &&
         (sk_mode == 1 || cost_sk < 0.95 * std::min(c128, c256))) {
       a = ask;
     } else if (g_policy == 0 && c128 < c256) {

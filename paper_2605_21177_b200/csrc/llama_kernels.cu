@@ -428,7 +428,7 @@ bool rms_bwd_dgamma(const bf16* dy, const bf16* x, const float* rstd, const bf16
                     const bf16* res, long long rows, int d, bf16* out, long long rb,
                     long long re, float* dgamma, cudaStream_t s) {
   const int k = rms_vpt(d);
-  if (k == 0) return false;  // the register kernels' shapes only
+  if (k == 0 || deterministic()) return false;  // register shapes; atomics across row groups
   const unsigned th = static_cast<unsigned>(d / 8 / k);
   constexpr int R = 16;
   const unsigned grid = static_cast<unsigned>((rows + R - 1) / R);
@@ -445,7 +445,8 @@ void rms_dgamma(const bf16* dy, const bf16* x, const float* rstd, long long rows
                 long long rb, long long re, float* out, cudaStream_t s) {
   if (re <= rb) return;
   const unsigned cb = static_cast<unsigned>((re - rb + 31) / 32);
-  const unsigned rc = static_cast<unsigned>(std::max<long long>(1, std::min<long long>(
+  // deterministic: one block row per column strip, so each column is summed in a fixed order
+  const unsigned rc = deterministic() ? 1u : static_cast<unsigned>(std::max<long long>(1, std::min<long long>(
       rows / 64, (num_sms() * 8LL + cb - 1) / cb)));
   rms_dgamma_kernel<<<dim3(cb, rc), 256, 0, s>>>(dy, x, rstd, rows, d, rb, re, out);
   check_launch("rms_dgamma");

@@ -108,6 +108,60 @@ __global__ void scatter_slice_kernel(const T* __restrict__ dy, long long dim,
   }
 }
 
+// Deterministic form of the scatter: a block owns kRowsPerBlock consecutive table rows and
+// walks the positions in ascending order (the reference's order, kernels_serial.cpp:69-85),
+// compacting each 256-position window's matches in order, then adding their dy rows with plain
+// read-add-writes (the block is the rows' only writer).
+constexpr int kScatterRows = 64;
+template <typename T>
+__global__ void __launch_bounds__(256)
+    scatter_ordered_kernel(const T* __restrict__ dy, long long dim,
+                           const int32_t* __restrict__ tokens, long long positions, long long rb,
+                           long long re, float* dtable, unsigned long long* matched) {
+  __shared__ int list[256];
+  __shared__ int wcount[8];
+  __shared__ int total;
+  const long long lo = rb + static_cast<long long>(blockIdx.x) * kScatterRows;
+  const long long hi = min(re, lo + kScatterRows);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  unsigned long long hits = 0;
+  for (long long base = 0; base < positions; base += 256) {
+    const long long p = base + threadIdx.x;
+    const long long tok = p < positions ? tokens[p] : -1;
+    const bool m = tok >= lo && tok < hi;
+    const unsigned bal = __ballot_sync(0xffffffffu, m);
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int w = 0; w < 8; ++w) {
+        const int c = wcount[w];
+        wcount[w] = acc;
+        acc += c;
+      }
+      total = acc;
+    }
+    __syncthreads();
+    if (m) list[wcount[warp] + __popc(bal & ((1u << lane) - 1))] = static_cast<int>(threadIdx.x);
+    __syncthreads();
+    const int n = total;
+    hits += n;
+    for (int q = 0; q < n; ++q) {  // ascending positions
+      const long long pp = base + list[q];
+      const T* src = dy + pp * dim;
+      float* dst = dtable + (tokens[pp] - rb) * dim;
+      for (long long j = threadIdx.x; j < dim; j += blockDim.x) {
+        float v;
+        if constexpr (std::is_same_v<T, float>) v = src[j];
+        else v = __bfloat162float(src[j]);
+        dst[j] += v;
+      }
+    }
+    __syncthreads();
+  }
+  if (matched && threadIdx.x == 0 && hits) atomicAdd(matched, hits);
+}
+
 }  // namespace
 }  // namespace cft
 
@@ -289,7 +343,16 @@ int cft_embedding_scatter_slice(cft_dtype dtype, const void* dy, int64_t dim,
     if (positions <= 0 || re <= rb || dim <= 0) return;
     auto* matched = reinterpret_cast<unsigned long long*>(matched_dev);
     const int threads = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, dim)));
-    if (dtype == CFT_BF16)
+    const unsigned oblocks = static_cast<unsigned>((re - rb + kScatterRows - 1) / kScatterRows);
+    if (deterministic() && dtype == CFT_BF16)
+      scatter_ordered_kernel<<<oblocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dy), dim,
+                                                     tokens, positions, rb, re,
+                                                     static_cast<float*>(dtable), matched);
+    else if (deterministic() && dtype == CFT_F32)
+      scatter_ordered_kernel<<<oblocks, 256, 0, s>>>(static_cast<const float*>(dy), dim, tokens,
+                                                     positions, rb, re,
+                                                     static_cast<float*>(dtable), matched);
+    else if (dtype == CFT_BF16)
       scatter_slice_kernel<<<(unsigned)positions, threads, 0, s>>>(
           static_cast<const __nv_bfloat16*>(dy), dim, tokens, positions, rb, re,
           static_cast<float*>(dtable), matched);

@@ -153,6 +153,12 @@ def softmax_ce(y: torch.Tensor, labels: torch.Tensor, dy: torch.Tensor | None = 
     return loss, dy, bad
 
 
+def set_deterministic(on: bool) -> None:
+    """Process-wide deterministic mode (cft_set_deterministic): fixed-order reductions, bitwise
+    reproducible gradients and parameters; set before an engine captures its graphs."""
+    N.check(N.lib.cft_set_deterministic(int(bool(on))), "set_deterministic")
+
+
 def attention_fwd(qkv: torch.Tensor, batch: int, hq: int, hkv: int, seq: int, head_dim: int,
                   stream=None):
     """Causal GQA flash attention over the fused qkv buffer [batch*seq, (hq+2hkv)*hd] (bf16).
