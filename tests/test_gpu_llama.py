@@ -380,7 +380,7 @@ def test_llama_deterministic_mode_is_bitwise_reproducible(cuda, layers, B):
         assert np.array_equal(m1, m2) and np.array_equal(p1, p2)
     g3, _, _ = run(False)
     for a, b in zip(g1, g3):
-        assert (a - b).norm().item() <= 1e-2 * max(b.norm().item(), 1e-30)
+        assert (a - b).norm().item() <= 2e-2 * max(b.norm().item(), 1e-30)  # the bf16 bar
 
 
 @pytest.mark.parametrize("graphs", [False, True], ids=["eager", "graphs"])
