@@ -862,13 +862,16 @@ def run_llama(args, rank, world, local_rank):
     return res
 
 
-def slice_sweep(local_rank):
-    """sliced-dW TFLOP/s for active-slice widths 1/8 .. 1/1 (configs[1] sweep)."""
+def slice_sweep(local_rank, dtype="bf16", reps=10):
+    """sliced-dW TFLOP/s for active-slice widths 1/8 .. 1/1 (configs[1] sweep: d=4096,
+    N_tok=8192; bf16 on the tcgen05 GEMM, fp32 on the CUDA-core path -- the reference harness
+    times both precisions side by side, tools/bench_kernels.cpp:19-41)."""
     import torch
     from paper_2605_21177_b200 import ops
     dev = torch.device("cuda", local_rank)
-    x = (torch.rand(N_TOK, D, device=dev) * 2 - 1).to(torch.bfloat16)
-    dy = (torch.rand(N_TOK, D, device=dev) * 2 - 1).to(torch.bfloat16)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    x = (torch.rand(N_TOK, D, device=dev) * 2 - 1).to(tdt)
+    dy = (torch.rand(N_TOK, D, device=dev) * 2 - 1).to(tdt)
     out = {}
     for f in (8, 4, 2, 1):
         s = D // f
@@ -882,11 +885,11 @@ def slice_sweep(local_rank):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
-        for _ in range(10):
+        for _ in range(reps):
             ops.linear_wgrad_slice(dy, x, rb, rb + s, out=buf, accumulate=True)
         e1.record()
         torch.cuda.synchronize()
-        t = e0.elapsed_time(e1) / 10
+        t = e0.elapsed_time(e1) / reps
         out[f"1/{f}"] = {"rows": s, "row_begin": rb, "ms": t, "tflops": 2 * N_TOK * s * D / t / 1e9}
     return out
 
@@ -1019,7 +1022,9 @@ def main():
         res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_sweep:
-            res.setdefault("sliced_dw", {})["configs1_sweep"] = slice_sweep(local_rank)
+            sw = res.setdefault("sliced_dw", {})
+            sw["configs1_sweep"] = slice_sweep(local_rank)
+            sw["configs1_sweep_fp32"] = slice_sweep(local_rank, "fp32", reps=3)
         if world == 1 and not args.no_cpu_baseline:
             cpu = None
             if args.workload in ("llama8b", "llama70b"):
