@@ -514,31 +514,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm128,
                        const __grid_constant__ CUtensorMap tm64,
                        const __grid_constant__ CUtensorMap tmdo,
-                       const __grid_constant__ CUtensorMap tmo, const BwdArgs a) {
+                       const __grid_constant__ CUtensorMap tmo, const BwdArgs a, int n_items) {
+  // persistent: a CTA walks items (query tile, batch, head) blockIdx.x, +gridDim.x, ... (longest
+  // tiles first); the next item's Q / dO / O load overlaps this item's dQ epilogue
   using L = QSmem<HD>;
   constexpr int NB = HD / 64, NS = L::NS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* qfull = bar;
-  uint64_t* kvfull = bar + 1;            // [NS]
-  uint64_t* kvempty = bar + 1 + NS;      // [NS] K / V block consumed
-  uint64_t* tfull = bar + 1 + 2 * NS;    // [2] S, dP in TMEM
+  uint64_t* qempty = bar + 1;            // the item's MMAs are done with Q, dO and the dS area
+  uint64_t* kvfull = bar + 2;            // [NS]
+  uint64_t* kvempty = kvfull + NS;       // [NS] K / V block consumed
+  uint64_t* tfull = kvempty + NS;        // [2] S, dP in TMEM
   uint64_t* pfull = tfull + 2;           // [2] dS written
   uint64_t* pfree = tfull + 4;           // [2] dS consumed
-  uint64_t* done = tfull + 6;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 7);
+  uint64_t* done = tfull + 6;            // the item's dQ complete
+  uint64_t* qout = tfull + 7;            // the item's dQ read out of TMEM
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 8);
 
-  const int nq = a.S / 128;
-  const int per_i = a.B * a.H;
-  const int i = nq - 1 - static_cast<int>(blockIdx.x) / per_i;  // longest rows first
-  const int rest = static_cast<int>(blockIdx.x) % per_i;
-  const int b = rest / a.H, h = rest % a.H;
-  const int kvh = h / (a.H / a.KVH);
-  const int n = 2 * i + 2;  // 64-row key blocks up to the diagonal
-  const int qrow = b * a.S + i * 128;
-  const int kcol = a.H * HD + kvh * HD, vcol = (a.H + a.KVH) * HD + kvh * HD;
+  const int nq = a.S / 128, per_i = a.B * a.H, G = a.H / a.KVH;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  auto item_of = [&](int item, int& i, int& b, int& h) {
+    i = nq - 1 - item / per_i;
+    const int rest = item % per_i;
+    b = rest / a.H;
+    h = rest % a.H;
+  };
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tm128);
@@ -546,6 +548,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tma_prefetch(&tmdo);
     tma_prefetch(&tmo);
     mbar_init(qfull, 1);
+    mbar_init(qempty, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kvfull[s], 1);
       mbar_init(&kvempty[s], 1);
@@ -556,6 +559,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&pfree[s], 1);
     }
     mbar_init(done, 1);
+    mbar_init(qout, 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -568,20 +572,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(qfull, 3 * L::TILE);
-      for (int kb = 0; kb < NB; ++kb) {
-        tma_load_2d(sm + L::Q + kb * kBlk128, &tm128, qfull, h * HD + kb * 64, qrow);
-        tma_load_2d(sm + L::DO + kb * kBlk128, &tmdo, qfull, h * HD + kb * 64, qrow);
-        tma_load_2d(sm + L::DS0 + kb * kBlk128, &tmo, qfull, h * HD + kb * 64, qrow);
-      }
-      for (int jj = 0; jj < n; ++jj) {
-        const int s = jj % NS, u = jj / NS;
-        const int kr = b * a.S + jj * 64;
-        spin_wait(&kvempty[s], (u & 1) ^ 1);
-        mbar_expect_tx(&kvfull[s], 2 * L::KB);
+      int g = 0, it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        int i, b, h;
+        item_of(item, i, b, h);
+        const int kvh = h / G, n = 2 * i + 2, qrow = b * a.S + i * 128;
+        const int kcol = a.H * HD + kvh * HD, vcol = (a.H + a.KVH) * HD + kvh * HD;
+        spin_wait(qempty, (it & 1) ^ 1);
+        mbar_expect_tx(qfull, 3 * L::TILE);
         for (int kb = 0; kb < NB; ++kb) {
-          tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], kcol + kb * 64, kr);
-          tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], vcol + kb * 64, kr);
+          tma_load_2d(sm + L::Q + kb * kBlk128, &tm128, qfull, h * HD + kb * 64, qrow);
+          tma_load_2d(sm + L::DO + kb * kBlk128, &tmdo, qfull, h * HD + kb * 64, qrow);
+          tma_load_2d(sm + L::DS0 + kb * kBlk128, &tmo, qfull, h * HD + kb * 64, qrow);
+        }
+        for (int jj = 0; jj < n; ++jj, ++g) {
+          const int s = g % NS, u = g / NS;
+          const int kr = b * a.S + jj * 64;
+          spin_wait(&kvempty[s], (u & 1) ^ 1);
+          mbar_expect_tx(&kvfull[s], 2 * L::KB);
+          for (int kb = 0; kb < NB; ++kb) {
+            tma_load_2d(sm + L::K0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], kcol + kb * 64, kr);
+            tma_load_2d(sm + L::V0 + s * L::KB + kb * kBlk64, &tm64, &kvfull[s], vcol + kb * 64, kr);
+          }
         }
       }
     }
@@ -590,8 +602,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_Q = idesc_bf16_f32(128, HD, false, true);
       const uint64_t dQ = desc_k(sm + L::Q, 0, kBlk128), dDO = desc_k(sm + L::DO, 0, kBlk128);
-      auto issue_s = [&](int jj) {
-        const int s = jj % NS, u = jj / NS, ts = jj & 1;
+      auto issue_s = [&](int g) {
+        const int s = g % NS, u = g / NS, ts = g & 1;
         spin_wait(&kvfull[s], u & 1);
         tc_fence_after();
         const uint64_t dk = desc_k(sm + L::K0 + s * L::KB, 0, kBlk64);
@@ -608,28 +620,37 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         __syncwarp();
       };
-      spin_wait(qfull, 0);
-      issue_s(0);
-      if (n > 1) issue_s(1);
-      for (int jj = 0; jj < n; ++jj) {
-        const int s = jj % NS, ts = jj & 1, v = jj >> 1;
-        spin_wait(&pfull[ts], v & 1);
-        tc_fence_after();
-        const uint64_t dk = desc_mn(sm + L::K0 + s * L::KB, 0, kBlk64);
-        const uint64_t dds = desc_k(sm + L::DS0 + ts * L::SB, 0, kBlk128);
-        if (elect_one()) {
+      int g = 0, it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        int i, b, h;
+        item_of(item, i, b, h);
+        const int n = 2 * i + 2;  // >= 2
+        spin_wait(qfull, it & 1);
+        issue_s(g);
+        issue_s(g + 1);
+        for (int jj = 0; jj < n; ++jj, ++g) {
+          const int s = g % NS, ts = g & 1, v = g >> 1;
+          if (jj == 0 && it > 0) spin_wait(qout, (it - 1) & 1);  // previous dQ read out
+          spin_wait(&pfull[ts], v & 1);
+          tc_fence_after();
+          const uint64_t dk = desc_mn(sm + L::K0 + s * L::KB, 0, kBlk64);
+          const uint64_t dds = desc_k(sm + L::DS0 + ts * L::SB, 0, kBlk128);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_bf16(tbase, dds + ((kk * 32) >> 4), dk + ((kk * 2048) >> 4), ID_Q,
-                      (jj > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&kvempty[s]);
-          umma_commit(&pfree[ts]);
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16(tbase, dds + ((kk * 32) >> 4), dk + ((kk * 2048) >> 4), ID_Q,
+                        (jj > 0 || kk > 0) ? 1u : 0u);
+            umma_commit(&kvempty[s]);
+            umma_commit(&pfree[ts]);
+            if (jj + 1 == n) {
+              umma_commit(done);
+              umma_commit(qempty);
+            }
+          }
+          __syncwarp();
+          if (jj + 2 < n) issue_s(g + 2);
         }
-        __syncwarp();
-        if (jj + 2 < n) issue_s(jj + 2);
       }
-      if (elect_one()) umma_commit(done);
-      __syncwarp();
     }
   } else {
     // 8 warps, two per TMEM lane quarter: a thread owns half a row (32 of the block's 64 key
@@ -637,85 +658,94 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int quarter = warp & 3, hf = (warp - 2) / 4;
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
-    const int qi = i * 128 + r;
-    const long long st = (static_cast<long long>(b) * a.H + h) * a.S + qi;
-    const float lse = a.lse[st];
     const float c = a.scale_log2;
-    // D of this row from the staged dO and O tiles (both halves form it; the dS writes below
-    // reuse the O staging bytes, so the row's two threads sync before the first one)
-    spin_wait(qfull, 0);
-    float dd = 0.f;
+    const float2 c2 = make_float2(c, c);
+    int g = 0, it = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      int i, b, h;
+      item_of(item, i, b, h);
+      const int n = 2 * i + 2, qrow = b * a.S + i * 128;
+      const int qi = i * 128 + r;
+      const long long st = (static_cast<long long>(b) * a.H + h) * a.S + qi;
+      const float lse = a.lse[st];
+      // D of this row from the staged dO and O tiles (both halves form it; the dS writes below
+      // reuse the O staging bytes, so the row's two threads sync before the first one)
+      spin_wait(qfull, it & 1);
+      float dd = 0.f;
 #pragma unroll
-    for (int kb = 0; kb < NB; ++kb) {
+      for (int kb = 0; kb < NB; ++kb) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint32_t off = kb * kBlk128 + r * 128 + ((q ^ (r & 7)) << 4);
-        const uint4 x = *reinterpret_cast<const uint4*>(sm + L::DO + off);
-        const uint4 y = *reinterpret_cast<const uint4*>(sm + L::DS0 + off);
-        const __nv_bfloat162* xa = reinterpret_cast<const __nv_bfloat162*>(&x);
-        const __nv_bfloat162* ya = reinterpret_cast<const __nv_bfloat162*>(&y);
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t off = kb * kBlk128 + r * 128 + ((q ^ (r & 7)) << 4);
+          const uint4 x = *reinterpret_cast<const uint4*>(sm + L::DO + off);
+          const uint4 y = *reinterpret_cast<const uint4*>(sm + L::DS0 + off);
+          const __nv_bfloat162* xa = reinterpret_cast<const __nv_bfloat162*>(&x);
+          const __nv_bfloat162* ya = reinterpret_cast<const __nv_bfloat162*>(&y);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 p = __bfloat1622float2(xa[e]), o = __bfloat1622float2(ya[e]);
-          dd = fmaf(p.x, o.x, fmaf(p.y, o.y, dd));
+          for (int e = 0; e < 4; ++e) {
+            const float2 p = __bfloat1622float2(xa[e]), o = __bfloat1622float2(ya[e]);
+            dd = fmaf(p.x, o.x, fmaf(p.y, o.y, dd));
+          }
         }
       }
-    }
-    if (hf == 0) a.D[st] = dd;
-    named_bar_sync(1, 256);
-    const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse, -lse), nd2 = make_float2(-dd, -dd);
-    for (int jj = 0; jj < n; ++jj) {
-      const int ts = jj & 1, v = jj >> 1;
-      spin_wait(&tfull[ts], v & 1);
-      if (jj >= 2) spin_wait(&pfree[ts], (v & 1) ^ 1);  // dS stage free
+      if (hf == 0) a.D[st] = dd;
+      named_bar_sync(1, 256);
+      const float2 nl2 = make_float2(-lse, -lse), nd2 = make_float2(-dd, -dd);
+      for (int jj = 0; jj < n; ++jj, ++g) {
+        const int ts = g & 1, v = g >> 1;
+        spin_wait(&tfull[ts], v & 1);
+        if (g >= 2) spin_wait(&pfree[ts], (v & 1) ^ 1);  // dS stage free
+        tc_fence_after();
+        uint8_t* ds = sm + L::DS0 + ts * L::SB;
+        uint32_t vs[32], vp[32];
+        tmem_ld32(lo + tst(ts) + hf * 32, vs);
+        tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
+        tmem_wait_ld();
+        const bool diag = jj * 64 + 63 > i * 128;
+        const int lim = qi - jj * 64 - hf * 32;
+        float dv[32];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float2 x = __ffma2_rn(make_float2(f32(vs[e]), f32(vs[e + 1])), c2, nl2);
+          dv[e] = x.x;
+          dv[e + 1] = x.y;
+        }
+        if (!diag) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            dv[e] = ex2_mix<0>(dv[e]);
+            dv[e + 1] = ex2_mix<1>(dv[e + 1]);
+            dv[e + 2] = ex2_mix<2>(dv[e + 2]);
+            dv[e + 3] = ex2_mix<3>(dv[e + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) dv[e] = e <= lim ? ex2(dv[e]) : 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {  // dS = P (dP - D)
+          const float2 x = __fmul2_rn(make_float2(dv[e], dv[e + 1]),
+                                      __fadd2_rn(make_float2(f32(vp[e]), f32(vp[e + 1])), nd2));
+          dv[e] = x.x;
+          dv[e + 1] = x.y;
+        }
+        st_swz32(ds, r, hf * 4, dv);
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(&pfull[ts]);
+      }
+      spin_wait(done, it & 1);
       tc_fence_after();
-      uint8_t* ds = sm + L::DS0 + ts * L::SB;
-      uint32_t vs[32], vp[32];
-      tmem_ld32(lo + tst(ts) + hf * 32, vs);
-      tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
-      tmem_wait_ld();
-      const bool diag = jj * 64 + 63 > i * 128;
-      const int lim = qi - jj * 64 - hf * 32;
-      float dv[32];
+      bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD + hf * (HD / 2);
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        const float2 x = __ffma2_rn(make_float2(f32(vs[e]), f32(vs[e + 1])), c2, nl2);
-        dv[e] = x.x;
-        dv[e + 1] = x.y;
+      for (int cc = 0; cc < HD / 64; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(tbase + lo + hf * (HD / 2) + cc * 32, o);
+        tmem_wait_ld();
+        st_row32(drow + cc * 32, o, a.scale);
       }
-      if (!diag) {
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          dv[e] = ex2_mix<0>(dv[e]);
-          dv[e + 1] = ex2_mix<1>(dv[e + 1]);
-          dv[e + 2] = ex2_mix<2>(dv[e + 2]);
-          dv[e + 3] = ex2_mix<3>(dv[e + 3]);
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) dv[e] = e <= lim ? ex2(dv[e]) : 0.f;
-      }
-#pragma unroll
-      for (int e = 0; e < 32; e += 2) {  // dS = P (dP - D)
-        const float2 x = __fmul2_rn(make_float2(dv[e], dv[e + 1]),
-                                    __fadd2_rn(make_float2(f32(vp[e]), f32(vp[e + 1])), nd2));
-        dv[e] = x.x;
-        dv[e + 1] = x.y;
-      }
-      st_swz32(ds, r, hf * 4, dv);
-      fence_async_smem();
       tc_fence_before();
-      mbar_arrive(&pfull[ts]);
-    }
-    spin_wait(done, 0);
-    tc_fence_after();
-    bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD + hf * (HD / 2);
-#pragma unroll
-    for (int cc = 0; cc < HD / 64; ++cc) {
-      uint32_t o[32];
-      tmem_ld32(tbase + lo + hf * (HD / 2) + cc * 32, o);
-      tmem_wait_ld();
-      st_row32(drow + cc * 32, o, a.scale);
+      mbar_arrive(qout);
     }
   }
   tc_fence_before();
@@ -1021,8 +1051,10 @@ void bwd_launch(int B, int H, int KVH, int S, const void* qkv, const void* o, co
   {
     const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 128);
     const CUtensorMap mo = tmap(o, ldo, N, ldo, 128);
-    attn_bwd_dq_kernel<HD><<<(S / 128) * B * H, kBwdThreads, std::max(QSmem<HD>::BYTES, kMinSmem), st>>>(
-        m128, m64, mdo, mo, a);
+    const int items = (S / 128) * B * H;
+    attn_bwd_dq_kernel<HD><<<std::min(items, num_sms()), kBwdThreads,
+                             std::max(QSmem<HD>::BYTES, kMinSmem), st>>>(m128, m64, mdo, mo, a,
+                                                                         items);
     check_launch("attn_bwd_dq_kernel");
   }
   {
