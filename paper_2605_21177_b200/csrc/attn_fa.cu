@@ -760,13 +760,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // smem stages.
 template <int HD>
 struct KvSmem {
-  static constexpr int NS = 3;
+  static constexpr int NS = 4;  // P^T / dS^T live in TMEM: the smem holds K, V and the Q/dO ring
   static constexpr uint32_t TILE = 128 * HD * 2;  // K or V tile (128 rows)
   static constexpr uint32_t QB = 64 * HD * 2;     // Q or dO block (64 rows)
-  static constexpr uint32_t PB = 128 * 64 * 2;    // P^T or dS^T block (128 kv x 64 q)
   static constexpr uint32_t K = 0, V = TILE, Q0 = 2 * TILE, DO0 = Q0 + NS * QB,
-                            P0 = DO0 + NS * QB, DS0 = P0 + 2 * PB, LSE0 = DS0 + 2 * PB,
-                            D0 = LSE0 + NS * 256, BAR = D0 + NS * 256;
+                            LSE0 = DO0 + NS * QB, D0 = LSE0 + NS * 256, BAR = D0 + NS * 256;
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
@@ -784,10 +782,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* qfull = bar + 1;             // [NS] Q, dO, lse, D of a query block
   uint64_t* qempty = bar + 1 + NS;       // [NS] consumed by the dV / dK MMAs
   uint64_t* tfull = bar + 1 + 2 * NS;    // [2] S^T, dP^T in TMEM
-  uint64_t* pfull = tfull + 2;           // [2] P^T, dS^T written
-  uint64_t* pfree = tfull + 4;           // [2] P^T, dS^T consumed
-  uint64_t* done = tfull + 6;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 7);
+  uint64_t* pfull = tfull + 2;           // [2] P^T, dS^T written (into the stage's TMEM)
+  uint64_t* done = tfull + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 5);
 
   const int G = a.H / a.KVH;
   const int per_j = a.B * a.KVH;
@@ -812,7 +809,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&pfull[s], 256);
-      mbar_init(&pfree[s], 1);
     }
     mbar_init(done, 1);
     fence_barrier_init();
@@ -822,7 +818,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: dV [0, HD), dK [HD, 2HD), stage s: S^T [2HD + 128 s, +64), dP^T [+64, +128)
+  // TMEM: dV [0, HD), dK [HD, 2HD), stage s: S^T [2HD + 128 s, +64), dP^T [+64, +128); the
+  // compute threads overwrite each with its bf16 form (P^T, dS^T: 32 packed columns) and
+  // dV += P^T dO, dK += dS^T Q run with A from TMEM -- P^T and dS^T never touch smem
   auto tst = [&](int s) { return tbase + 2 * HD + 128 * s; };
 
   if (warp == 0) {
@@ -880,17 +878,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_after();
         const uint64_t dq = desc_mn(sm + L::Q0 + s * L::QB, 0, kBlk64);
         const uint64_t dd = desc_mn(sm + L::DO0 + s * L::QB, 0, kBlk64);
-        const uint64_t dp = desc_k(sm + L::P0 + ts * L::PB, 0, kBlk128);
-        const uint64_t dds = desc_k(sm + L::DS0 + ts * L::PB, 0, kBlk128);
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < 4; ++k) {  // 16 query columns = 8 packed TMEM columns per step
             const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
-            umma_bf16(tbase, dp + ((k * 32) >> 4), dd + ((k * 2048) >> 4), ID_A, acc);        // dV
-            umma_bf16(tbase + HD, dds + ((k * 32) >> 4), dq + ((k * 2048) >> 4), ID_A, acc);  // dK
+            umma_bf16_ts(tbase, tst(ts) + k * 8, dd + ((k * 2048) >> 4), ID_A, acc);            // dV
+            umma_bf16_ts(tbase + HD, tst(ts) + 64 + k * 8, dq + ((k * 2048) >> 4), ID_A, acc);  // dK
           }
           umma_commit(&qempty[s]);
-          umma_commit(&pfree[ts]);
         }
         __syncwarp();
         if (it + 2 < n_it) issue_s(it + 2);
@@ -912,16 +907,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int qb = 2 * j + it % nper;
       spin_wait(&tfull[ts], v & 1);
       spin_wait(&qfull[s], u & 1);  // lse / D of the block
-      if (it >= 2) spin_wait(&pfree[ts], (v & 1) ^ 1);  // P^T / dS^T stage free
       tc_fence_after();
       const float* sl = reinterpret_cast<const float*>(sm + L::LSE0 + s * 256) + hf * 32;
       const float* sd = reinterpret_cast<const float*>(sm + L::D0 + s * 256) + hf * 32;
-      uint8_t* p = sm + L::P0 + ts * L::PB;
-      uint8_t* ds = sm + L::DS0 + ts * L::PB;
       uint32_t vs[32], vp[32];
       tmem_ld32(lo + tst(ts) + hf * 32, vs);
       tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
       tmem_wait_ld();
+      // both halves of every row have read their scores before either overwrites the stage
+      tc_fence_before();
+      named_bar_sync(1, 256);
+      tc_fence_after();
       const bool diag = qb * 64 < j * 128 + 128;
       const int lim = kvi - qb * 64 - hf * 32;  // query columns e < lim are masked (q < kv)
       float pv[32];
@@ -944,17 +940,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) pv[e] = e < lim ? 0.f : ex2(pv[e]);
       }
-      st_swz32(p, r, hf * 4, pv);
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
+      tmem_st16(lo + tst(ts) + hf * 16, pk);  // P^T, query columns in K order
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {  // dS^T = P^T (dP^T - D)
         const float2 x = __fmul2_rn(make_float2(pv[e], pv[e + 1]),
                                     __fadd2_rn(make_float2(f32(vp[e]), f32(vp[e + 1])),
                                                make_float2(-sd[e], -sd[e + 1])));
-        pv[e] = x.x;
-        pv[e + 1] = x.y;
+        pk[e / 2] = pack_bf16(x.x, x.y);
       }
-      st_swz32(ds, r, hf * 4, pv);
-      fence_async_smem();
+      tmem_st16(lo + tst(ts) + 64 + hf * 16, pk);  // dS^T
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&pfull[ts]);
     }
@@ -997,6 +995,10 @@ CUtensorMap tmap(const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
 // every kernel holds all 512 TMEM columns: request enough shared memory that two CTAs can
 // never share an SM (a second one would stall in tcgen05.alloc)
 constexpr size_t kMinSmem = 120 * 1024;
+constexpr size_t kMaxSmem = 227 * 1024;  // sm_100 opt-in dynamic shared memory per block
+static_assert(FwdSmem<128>::BYTES <= kMaxSmem && QSmem<128>::BYTES <= kMaxSmem &&
+                  KvSmem<128>::BYTES <= kMaxSmem,
+              "attention smem layouts must fit one SM");
 template <typename K>
 void set_smem(K kern, size_t bytes) {
   CFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

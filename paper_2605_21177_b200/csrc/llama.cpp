@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <initializer_list>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -256,6 +257,42 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     tc::linear_wgrad_slice(dy, N, out_dim, x, in_dim, row0 + s->rb, row0 + s->re, aux_at(s), 1, st);
     pe();
   };
+  // the sliced dW of the tensors stacked in one operand (wq|wk|wv, w1|w3): a run of slices that
+  // is contiguous in the stack (a slice reaching its tensor's last row, the next starting at the
+  // following tensor's row 0) is contiguous in the chunk's gradient buffer too (plan order), so
+  // it is one wider GEMM instead of one launch per tensor
+  auto wgrad_stack = [&](std::initializer_list<int> ts, const void* dy, int64_t out_dim,
+                         const void* x, int64_t in_dim) {
+    int64_t row0 = 0, run_lo = 0, run_hi = 0;
+    const SliceRt* first = nullptr;
+    auto flush = [&] {
+      if (!first) return;
+      pb(kWgrad);
+      const double rows = double(run_hi - run_lo);
+      add_work(kWgrad, 2.0 * N * rows * in_dim);
+      add_bytes(kWgrad, 2.0 * (N * rows + N * double(in_dim)) + 4.0 * rows * in_dim);
+      tc::linear_wgrad_slice(dy, N, out_dim, x, in_dim, run_lo, run_hi, aux_at(first), 1, st);
+      pe();
+      first = nullptr;
+    };
+    for (int t : ts) {
+      const int64_t rows_t = tensors_[t].rows;
+      if (const SliceRt* s = slice_of(t)) {
+        const bool joins = first && run_hi == row0 + s->rb &&
+                           s->aux_off == first->aux_off + (run_hi - run_lo) * in_dim;
+        if (!joins) {
+          flush();
+          first = s;
+          run_lo = row0 + s->rb;
+        }
+        run_hi = row0 + s->re;
+      } else {
+        flush();
+      }
+      row0 += rows_t;
+    }
+    flush();
+  };
 
   pb(kInputs);
   layers::count_in_range(tok, N, 0, V, reinterpret_cast<long long*>(flags_ + 1), st);
@@ -408,8 +445,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
                         static_cast<bf16*>(l_dug_), st);
       pe();
     }
-    wgrad(id(l, 6), l_dug_, 2 * F, z.m, d, 0);  // w1 rows [0,F) of the stack
-    wgrad(id(l, 7), l_dug_, 2 * F, z.m, d, F);  // w3 rows [F,2F)
+    wgrad_stack({id(l, 6), id(l, 7)}, l_dug_, 2 * F, z.m, d);  // w1 | w3 rows of the stack
     if (!need(id(l, 5))) break;
     pb(kDgrad);
     gemm_work(kDgrad, N, d, 2 * F, 2.0 * N * d, 0);
@@ -433,9 +469,7 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     llama::rope(static_cast<bf16*>(l_dqkv_), N, S.seq, S.heads + S.kv_heads, S.head_dim, ld,
                 (float)S.rope_theta, true, st);
     pe();
-    wgrad(id(l, 1), l_dqkv_, QKV, z.a, d, 0);
-    wgrad(id(l, 2), l_dqkv_, QKV, z.a, d, Q);
-    wgrad(id(l, 3), l_dqkv_, QKV, z.a, d, Q + KV);
+    wgrad_stack({id(l, 1), id(l, 2), id(l, 3)}, l_dqkv_, QKV, z.a, d);  // wq | wk | wv
     if (!need(id(l, 0))) break;
     pb(kDgrad);
     gemm_work(kDgrad, N, d, QKV, 2.0 * N * d, 0);
