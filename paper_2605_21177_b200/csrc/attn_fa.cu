@@ -494,7 +494,8 @@ struct BwdArgs {
 // ------------------------------------------------------------------------------------------
 // dQ (runs first; also forms D = rowsum(dO * O) of its rows): warp 0 TMA, warp 1 MMA,
 // warps 2-9 half a query row each.  Key / value blocks of 64 rows in a 4-deep ring; S and dP
-// double-buffered in TMEM; the O tile is staged once in the dS buffers before the loop.
+// double-buffered in TMEM, dS written back over S in TMEM; the O tile is staged per item in a
+// 32 KB smem area (for D only).
 template <int HD>
 struct QSmem {
   static constexpr int NS = 4;
@@ -527,11 +528,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* kvfull = bar + 2;            // [NS]
   uint64_t* kvempty = kvfull + NS;       // [NS] K / V block consumed
   uint64_t* tfull = kvempty + NS;        // [2] S, dP in TMEM
-  uint64_t* pfull = tfull + 2;           // [2] dS written
-  uint64_t* pfree = tfull + 4;           // [2] dS consumed
-  uint64_t* done = tfull + 6;            // the item's dQ complete
-  uint64_t* qout = tfull + 7;            // the item's dQ read out of TMEM
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 8);
+  uint64_t* pfull = tfull + 2;           // [2] dS written (into the stage's TMEM)
+  uint64_t* done = tfull + 4;            // the item's dQ complete
+  uint64_t* qout = tfull + 5;            // the item's dQ read out of TMEM
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 6);
 
   const int nq = a.S / 128, per_i = a.B * a.H, G = a.H / a.KVH;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -556,7 +556,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&pfull[s], 256);
-      mbar_init(&pfree[s], 1);
     }
     mbar_init(done, 1);
     mbar_init(qout, 256);
@@ -567,7 +566,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: dQ [0, HD), stage s: S [HD + 128 s, +64), dP [+64, +128)
+  // TMEM: dQ [0, HD), stage s: S [HD + 128 s, +64), dP [+64, +128); the compute threads write
+  // dS (bf16, 32 packed columns) over the stage's S and dQ += dS K runs with A from TMEM
   auto tst = [&](int s) { return tbase + HD + 128 * s; };
 
   if (warp == 0) {
@@ -634,14 +634,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           spin_wait(&pfull[ts], v & 1);
           tc_fence_after();
           const uint64_t dk = desc_mn(sm + L::K0 + s * L::KB, 0, kBlk64);
-          const uint64_t dds = desc_k(sm + L::DS0 + ts * L::SB, 0, kBlk128);
           if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              umma_bf16(tbase, dds + ((kk * 32) >> 4), dk + ((kk * 2048) >> 4), ID_Q,
-                        (jj > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk)  // 16 key columns = 8 packed TMEM columns per step
+              umma_bf16_ts(tbase, tst(ts) + kk * 8, dk + ((kk * 2048) >> 4), ID_Q,
+                           (jj > 0 || kk > 0) ? 1u : 0u);
             umma_commit(&kvempty[s]);
-            umma_commit(&pfree[ts]);
             if (jj + 1 == n) {
               umma_commit(done);
               umma_commit(qempty);
@@ -694,13 +692,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int jj = 0; jj < n; ++jj, ++g) {
         const int ts = g & 1, v = g >> 1;
         spin_wait(&tfull[ts], v & 1);
-        if (g >= 2) spin_wait(&pfree[ts], (v & 1) ^ 1);  // dS stage free
         tc_fence_after();
-        uint8_t* ds = sm + L::DS0 + ts * L::SB;
         uint32_t vs[32], vp[32];
         tmem_ld32(lo + tst(ts) + hf * 32, vs);
         tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
         tmem_wait_ld();
+        // both halves of every row have read S before either overwrites it with dS
+        tc_fence_before();
+        named_bar_sync(1, 256);
+        tc_fence_after();
         const bool diag = jj * 64 + 63 > i * 128;
         const int lim = qi - jj * 64 - hf * 32;
         float dv[32];
@@ -729,8 +729,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dv[e] = x.x;
           dv[e + 1] = x.y;
         }
-        st_swz32(ds, r, hf * 4, dv);
-        fence_async_smem();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dv[2 * e], dv[2 * e + 1]);
+        tmem_st16(lo + tst(ts) + hf * 16, pk);  // dS, key columns in K order
+        tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&pfull[ts]);
       }
