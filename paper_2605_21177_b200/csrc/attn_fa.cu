@@ -195,7 +195,7 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
 }
 
 // ------------------------------------------------------------------------------------------
-// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax of head A, 6-9 of B.
+// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-9 softmax of head A, 10-17 of B.
 // 128-row key blocks (K ring of 2, V ring of 3).  TMEM: S_A, S_B (128 columns each), O_A, O_B;
 // the softmax thread of a row reads its 128 scores, writes P (bf16) into the first 64
 // columns of its own S row, and P.V runs with A from TMEM.  The tensor pipe executes
@@ -203,13 +203,14 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
 // and S_t(j+1) completing implies PV_t(j) did (O is safe to rescale, P to overwrite).
 template <int HD>
 struct FwdSmem {
-  static constexpr int NK = 3, NV = 2;
+  static constexpr int NK = 2, NV = 2;
   static constexpr uint32_t QT = 128 * HD * 2;  // query tile / key or value block (128 rows)
-  static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NK * QT, BAR = V0 + NV * QT;
+  static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NK * QT, XCH = V0 + NV * QT,
+                            BAR = XCH + 8 * 128 * 4;
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
-constexpr int kFwdThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 softmax warps
+constexpr int kFwdThreads = 64 + 16 * 32;  // TMA warp, MMA warp, 16 softmax warps
 
 // Work item = (query tile, batch, KV head, head pair), longest query tiles first; a persistent
 // CTA walks items blockIdx.x, +gridDim.x, ...  The next item's Q tiles load while the current
@@ -231,7 +232,7 @@ __device__ __forceinline__ FwdItem fwd_item(const FwdArgs& a, int item) {
 }
 
 template <int HD>
-__global__ void __launch_bounds__(kFwdThreads, 1)
+__global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 32 <= 16K registers
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq, const FwdArgs a, int n_items) {
   using L = FwdSmem<HD>;
   constexpr int NB = HD / 64, NK = L::NK, NV = L::NV;
@@ -266,9 +267,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&sfull[t], 1);
-      mbar_init(&pfull[t], 128);
+      mbar_init(&pfull[t], 256);
       mbar_init(&ofull[t], 1);
-      mbar_init(&oempty[t], 128);
+      mbar_init(&oempty[t], 256);
     }
     fence_barrier_init();
   }
@@ -379,13 +380,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
   } else {
-    const int t = (warp - 2) / 4;
+    // softmax: 8 warps per head, two per TMEM lane quarter; a thread owns half a row (64 of the
+    // block's 128 scores, half of O's columns).  The halves agree on the row max through a
+    // double-buffered smem exchange and a named barrier per head, which also orders both
+    // halves' score reads before either writes its P over the row's S columns.
+    const int idx = warp - 2;
+    const int t = idx / 8, hf = (idx / 4) & 1;
     const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tS = tbase + lo + 128 * t, tO = tbase + lo + 256 + HD * t;
+    const uint32_t tS = tbase + lo + 128 * t, tO = tbase + lo + 256 + HD * t + hf * (HD / 2);
+    float* xch = reinterpret_cast<float*>(sm + L::XCH);  // [2 parity][2 heads][2 halves][128]
+    auto slot = [&](int par, int half) { return xch + ((par * 2 + t) * 2 + half) * 128 + r; };
     const float c = a.scale_log2;
-    int g = 0, n = 0;
+    int g = 0, n = 0, xp = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
       const FwdItem w = fwd_item(a, item);
       const int qpos = w.i * 128 + r;
@@ -393,25 +401,30 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int j = 0; j < w.nb; ++j, ++g) {
         spin_wait(&sfull[t], g & 1);
         tc_fence_after();
-        uint32_t v[128];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          tmem_ld32(tS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cc * 32));
+        uint32_t v[64];
+        tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         tmem_wait_ld();
-        const bool diag = j == w.i;  // columns e > r are masked
-        float mk[8];  // eight independent max chains (ILP), folded at the end
+        const bool diag = j == w.i;   // columns > r are masked
+        const int lim = r - hf * 64;  // this half's columns e <= lim are visible
+        float mk[4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) mk[q] = -INFINITY;
+        for (int q = 0; q < 4; ++q) mk[q] = -INFINITY;
         if (!diag) {
 #pragma unroll
-          for (int e = 0; e < 128; ++e) mk[e & 7] = fmaxf(mk[e & 7], f32(v[e]));
+          for (int e = 0; e < 64; ++e) mk[e & 3] = fmaxf(mk[e & 3], f32(v[e]));
         } else {
 #pragma unroll
-          for (int e = 0; e < 128; ++e)
-            if (e <= r) mk[e & 7] = fmaxf(mk[e & 7], f32(v[e]));
+          for (int e = 0; e < 64; ++e)
+            if (e <= lim) mk[e & 3] = fmaxf(mk[e & 3], f32(v[e]));
         }
-        const float mx = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
-                               fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
+        float mx = fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3]));
+        *slot(xp, hf) = mx;
+        tc_fence_before();
+        named_bar_sync(1 + t, 256);
+        tc_fence_after();
+        mx = fmaxf(mx, *slot(xp, hf ^ 1));
+        xp ^= 1;
         const float m_new = fmaxf(m, mx * c);
         if (j == 0) {
           m = m_new;
@@ -421,7 +434,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           l *= alpha;
           m = m_new;
 #pragma unroll 1
-          for (int cc = 0; cc < HD / 16; ++cc) {  // 16 columns at a time: v[] stays live
+          for (int cc = 0; cc < HD / 32; ++cc) {  // this half's HD/2 columns, 16 at a time
             uint32_t o[16];
             tmem_ld16(tO + cc * 16, o);
             tmem_wait_ld();
@@ -431,10 +444,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
-        float2 accs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                          make_float2(0.f, 0.f)};
+        float2 accs[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int e = 0; e < 128; e += 4) {  // P packed in place: word e/2 holds columns e, e+1
+        for (int e = 0; e < 64; e += 4) {  // P packed in place: word e/2 holds columns e, e+1
           float2 x0 = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
           float2 x1 = __ffma2_rn(make_float2(f32(v[e + 2]), f32(v[e + 3])), c2, nm2);
           if (!diag) {
@@ -443,29 +455,35 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             x1.x = ex2_mix<2>(x1.x);
             x1.y = ex2_mix<3>(x1.y);
           } else {
-            x0.x = e <= r ? ex2(x0.x) : 0.f;
-            x0.y = e + 1 <= r ? ex2(x0.y) : 0.f;
-            x1.x = e + 2 <= r ? ex2(x1.x) : 0.f;
-            x1.y = e + 3 <= r ? ex2(x1.y) : 0.f;
+            x0.x = e <= lim ? ex2(x0.x) : 0.f;
+            x0.y = e + 1 <= lim ? ex2(x0.y) : 0.f;
+            x1.x = e + 2 <= lim ? ex2(x1.x) : 0.f;
+            x1.y = e + 3 <= lim ? ex2(x1.y) : 0.f;
           }
-          accs[(e >> 2) & 3] = __fadd2_rn(accs[(e >> 2) & 3], __fadd2_rn(x0, x1));
+          accs[(e >> 2) & 1] = __fadd2_rn(accs[(e >> 2) & 1], __fadd2_rn(x0, x1));
           v[e / 2] = pack_bf16(x0.x, x0.y);
           v[e / 2 + 1] = pack_bf16(x1.x, x1.y);
         }
-        const float2 acc = __fadd2_rn(__fadd2_rn(accs[0], accs[1]), __fadd2_rn(accs[2], accs[3]));
+        const float2 acc = __fadd2_rn(accs[0], accs[1]);
         l += acc.x + acc.y;
-        tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(v));
-        tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(v + 32));
+        // P words [32 hf, 32 hf + 32) of the row: columns 64 hf .. 64 hf + 63 in K order
+        tmem_st32(tS + hf * 32, *reinterpret_cast<const uint32_t(*)[32]>(v));
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&pfull[t]);
       }
+      // l of the whole row = the two halves' sums (same running max)
+      *slot(xp, hf) = l;
+      named_bar_sync(1 + t, 256);
+      l += *slot(xp, hf ^ 1);
+      xp ^= 1;
       spin_wait(&ofull[t], n & 1);
       tc_fence_after();
       const float inv = 1.f / l;
-      bf16* out = a.o + static_cast<long long>(w.b * a.S + qpos) * a.ldo + (w.h0 + t) * HD;
+      bf16* out = a.o + static_cast<long long>(w.b * a.S + qpos) * a.ldo + (w.h0 + t) * HD +
+                  hf * (HD / 2);
 #pragma unroll
-      for (int cc = 0; cc < HD / 32; ++cc) {
+      for (int cc = 0; cc < HD / 64; ++cc) {
         uint32_t o[32];
         tmem_ld32(tO + cc * 32, o);
         tmem_wait_ld();
@@ -473,7 +491,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&oempty[t]);
-      a.lse[(static_cast<long long>(w.b) * a.H + w.h0 + t) * a.S + qpos] = m + __log2f(l);
+      if (hf == 0)
+        a.lse[(static_cast<long long>(w.b) * a.H + w.h0 + t) * a.S + qpos] = m + __log2f(l);
     }
   }
   tc_fence_before();
