@@ -267,9 +267,9 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&sfull[t], 1);
-      mbar_init(&pfull[t], 256);
+      mbar_init(&pfull[t], 8);  // one arrival per softmax warp
       mbar_init(&ofull[t], 1);
-      mbar_init(&oempty[t], 256);
+      mbar_init(&oempty[t], 8);
     }
     fence_barrier_init();
   }
@@ -470,7 +470,8 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
         tmem_st32(tS + hf * 32, *reinterpret_cast<const uint32_t(*)[32]>(v));
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&pfull[t]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[t]);
       }
       // l of the whole row = the two halves' sums (same running max)
       *slot(xp, hf) = l;
@@ -490,7 +491,8 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
         st_row32(out + cc * 32, o, inv);
       }
       tc_fence_before();
-      mbar_arrive(&oempty[t]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&oempty[t]);
       if (hf == 0)
         a.lse[(static_cast<long long>(w.b) * a.H + w.h0 + t) * a.S + qpos] = m + __log2f(l);
     }
@@ -574,10 +576,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&pfull[s], 256);
+      mbar_init(&pfull[s], 8);  // one arrival per gradient warp
     }
     mbar_init(done, 1);
-    mbar_init(qout, 256);
+    mbar_init(qout, 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -754,7 +756,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_st16(lo + tst(ts) + hf * 16, pk);  // dS, key columns in K order
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&pfull[ts]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[ts]);
       }
       spin_wait(done, it & 1);
       tc_fence_after();
@@ -767,7 +770,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         st_row32(drow + cc * 32, o, a.scale);
       }
       tc_fence_before();
-      mbar_arrive(qout);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qout);
     }
   }
   tc_fence_before();
@@ -830,7 +834,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&pfull[s], 256);
+      mbar_init(&pfull[s], 8);  // one arrival per gradient warp
     }
     mbar_init(done, 1);
     fence_barrier_init();
@@ -976,7 +980,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_st16(lo + tst(ts) + 64 + hf * 16, pk);  // dS^T
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&pfull[ts]);
+      __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[ts]);
     }
     spin_wait(done, 0);
     tc_fence_after();
