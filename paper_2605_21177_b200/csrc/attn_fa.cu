@@ -141,6 +141,8 @@ __device__ __forceinline__ void st_row32(bf16* p, const uint32_t (&r)[32], float
 // the bf16 rounding of P): the MUFU unit (16 ex2 / clock / SM) would otherwise bound the
 // softmax; a quarter of the exponentials go this way.
 __device__ __forceinline__ float ex2_poly(float x) {
+  // clamped at 2^-126 (the exponent add must not underflow): masked (-inf) scores give
+  // ~6e-39 here against exactly 0 from MUFU -- far below any bf16 P the row sums with
   x = fmaxf(x, -126.f);
   const float t = x + 12582912.f;  // 1.5 * 2^23: rounds x to an integer in the low mantissa bits
   const float f = x - (t - 12582912.f);
@@ -148,9 +150,12 @@ __device__ __forceinline__ float ex2_poly(float x) {
                        0.9999280572f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+#ifndef CFT_POLY_SHARE
+#define CFT_POLY_SHARE 1  // exponentials on the FMA pipe per 4 (0..4)
+#endif
 template <int E>
 __device__ __forceinline__ float ex2_mix(float x) {
-  if constexpr ((E & 3) == 3) return ex2_poly(x);
+  if constexpr ((E & 3) >= 4 - CFT_POLY_SHARE) return ex2_poly(x);
   else return ex2(x);
 }
 
@@ -405,19 +410,19 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
         tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
         tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         tmem_wait_ld();
-        const bool diag = j == w.i;   // columns > r are masked
-        const int lim = r - hf * 64;  // this half's columns e <= lim are visible
+        // the diagonal block: masked scores become -inf, so one exp path serves every block
+        // (a separate masked path gets if-converted into predicated-off MUFU issue slots)
+        if (j == w.i) {
+          const int lim = r - hf * 64;  // this half's columns e <= lim are visible
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (e > lim) v[e] = __float_as_uint(-INFINITY);
+        }
         float mk[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) mk[q] = -INFINITY;
-        if (!diag) {
 #pragma unroll
-          for (int e = 0; e < 64; ++e) mk[e & 3] = fmaxf(mk[e & 3], f32(v[e]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e <= lim) mk[e & 3] = fmaxf(mk[e & 3], f32(v[e]));
-        }
+        for (int e = 0; e < 64; ++e) mk[e & 3] = fmaxf(mk[e & 3], f32(v[e]));
         float mx = fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3]));
         *slot(xp, hf) = mx;
         tc_fence_before();
@@ -449,17 +454,10 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
         for (int e = 0; e < 64; e += 4) {  // P packed in place: word e/2 holds columns e, e+1
           float2 x0 = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
           float2 x1 = __ffma2_rn(make_float2(f32(v[e + 2]), f32(v[e + 3])), c2, nm2);
-          if (!diag) {
-            x0.x = ex2_mix<0>(x0.x);
-            x0.y = ex2_mix<1>(x0.y);
-            x1.x = ex2_mix<2>(x1.x);
-            x1.y = ex2_mix<3>(x1.y);
-          } else {
-            x0.x = e <= lim ? ex2(x0.x) : 0.f;
-            x0.y = e + 1 <= lim ? ex2(x0.y) : 0.f;
-            x1.x = e + 2 <= lim ? ex2(x1.x) : 0.f;
-            x1.y = e + 3 <= lim ? ex2(x1.y) : 0.f;
-          }
+          x0.x = ex2_mix<0>(x0.x);
+          x0.y = ex2_mix<1>(x0.y);
+          x1.x = ex2_mix<2>(x1.x);
+          x1.y = ex2_mix<3>(x1.y);
           accs[(e >> 2) & 1] = __fadd2_rn(accs[(e >> 2) & 1], __fadd2_rn(x0, x1));
           v[e / 2] = pack_bf16(x0.x, x0.y);
           v[e / 2 + 1] = pack_bf16(x1.x, x1.y);
@@ -722,8 +720,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         named_bar_sync(1, 256);
         tc_fence_after();
-        const bool diag = jj * 64 + 63 > i * 128;
-        const int lim = qi - jj * 64 - hf * 32;
+        if (jj * 64 + 63 > i * 128) {  // diagonal block: masked scores -> -inf -> P = 0
+          const int lim = qi - jj * 64 - hf * 32;
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e > lim) vs[e] = __float_as_uint(-INFINITY);
+        }
         float dv[32];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
@@ -731,17 +733,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dv[e] = x.x;
           dv[e + 1] = x.y;
         }
-        if (!diag) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            dv[e] = ex2_mix<0>(dv[e]);
-            dv[e + 1] = ex2_mix<1>(dv[e + 1]);
-            dv[e + 2] = ex2_mix<2>(dv[e + 2]);
-            dv[e + 3] = ex2_mix<3>(dv[e + 3]);
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) dv[e] = e <= lim ? ex2(dv[e]) : 0.f;
+        for (int e = 0; e < 32; e += 4) {
+          dv[e] = ex2_mix<0>(dv[e]);
+          dv[e + 1] = ex2_mix<1>(dv[e + 1]);
+          dv[e + 2] = ex2_mix<2>(dv[e + 2]);
+          dv[e + 3] = ex2_mix<3>(dv[e + 3]);
         }
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {  // dS = P (dP - D)
@@ -944,8 +941,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       named_bar_sync(1, 256);
       tc_fence_after();
-      const bool diag = qb * 64 < j * 128 + 128;
-      const int lim = kvi - qb * 64 - hf * 32;  // query columns e < lim are masked (q < kv)
+      if (qb * 64 < j * 128 + 128) {  // diagonal: query columns e < lim (q < kv) -> P = 0
+        const int lim = kvi - qb * 64 - hf * 32;
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (e < lim) vs[e] = __float_as_uint(-INFINITY);
+      }
       float pv[32];
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {
@@ -954,17 +955,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         pv[e] = x.x;
         pv[e + 1] = x.y;
       }
-      if (!diag) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          pv[e] = ex2_mix<0>(pv[e]);
-          pv[e + 1] = ex2_mix<1>(pv[e + 1]);
-          pv[e + 2] = ex2_mix<2>(pv[e + 2]);
-          pv[e + 3] = ex2_mix<3>(pv[e + 3]);
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) pv[e] = e < lim ? 0.f : ex2(pv[e]);
+      for (int e = 0; e < 32; e += 4) {
+        pv[e] = ex2_mix<0>(pv[e]);
+        pv[e + 1] = ex2_mix<1>(pv[e + 1]);
+        pv[e + 2] = ex2_mix<2>(pv[e + 2]);
+        pv[e + 3] = ex2_mix<3>(pv[e + 3]);
       }
       uint32_t pk[16];
 #pragma unroll
