@@ -443,6 +443,13 @@ void Engine::phase_totals(float* ms, int64_t* counts, double* work) {
   pool_next_ = 0;
 }
 
+namespace {
+// the first non-finite element, chunk-global; with sharded state a rank only sees its shard
+std::string bad_element(int64_t bad) {
+  return bad == INT64_MAX ? std::string("<in another rank's shard>") : std::to_string(bad);
+}
+}  // namespace
+
 void Engine::wait_step(int64_t t, double* loss, double* gsq) {
   CFT_CHECK(t >= 0 && t < t_ && t >= t_ - 4, "engine: step result no longer tracked");
   CFT_CUDA(cudaEventSynchronize(stats_ev_[t % 4]));
@@ -472,7 +479,7 @@ void Engine::scan_results(int64_t upto) {
     } else {
       int64_t bad;
       std::memcpy(&bad, &h[2], 8);
-      sticky_error_ = ctx + "step: non-finite gradient at element " + std::to_string(bad) +
+      sticky_error_ = ctx + "step: non-finite gradient at element " + bad_element(bad) +
                       " (chunk " + std::to_string(c) + ", local step " +
                       std::to_string(n_local_[c] + 1) + ")";
     }
@@ -880,7 +887,7 @@ void Engine::step_end() {
   if (sharded()) {
     CFT_CHECK(stats_done_, "engine: sharded step_end needs shard_stats() and its all-reduce first");
     stats_done_ = false;
-    layers::unpack_shard_stats(red_, st, 1.0 / cfg_.shard_world, s);
+    layers::unpack_shard_stats(red_, st, 1.0 / cfg_.shard_world, st_lo_[c], s);
     grad = gshard_;
     gn = st_n_[c];
     if (sdt == CFT_F32) CFT_CUDA(cudaMemsetAsync(aux_, 0, n * 4, s));  // zero-accumulator invariant
@@ -971,7 +978,7 @@ void Engine::step_end() {
       std::memcpy(&bad, &h[2], 8);
       n_local_[c] -= 1;
       restore();
-      throw Error(ctx + "step: non-finite gradient at element " + std::to_string(bad) + " (chunk " +
+      throw Error(ctx + "step: non-finite gradient at element " + bad_element(bad) + " (chunk " +
                   std::to_string(c) + ", local step " + std::to_string(n_local_[c] + 1) + ")");
     }
     scanned_ = t_ + 1;

@@ -109,7 +109,8 @@ void add_f64(double* dst, const double* src, long long n, cudaStream_t s);
 void sm_copy(void* dst, const void* src, long long bytes, cudaStream_t s);
 bool host_pinned(const void* p);  // pinned + mapped at the same address (UVA)
 void pack_shard_stats(const double* st, double* red, cudaStream_t s);
-void unpack_shard_stats(const double* red, double* st, double inv_world, cudaStream_t s);
+void unpack_shard_stats(const double* red, double* st, double inv_world, long long shard_lo,
+                        cudaStream_t s);
 void copy_unless_flagged(void* dst, const void* src, long long elems, int esz, const double* st,
                          cudaStream_t s);
 void add_f32(float* dst, const float* src, long long n, cudaStream_t s);

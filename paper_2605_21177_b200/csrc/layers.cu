@@ -576,18 +576,28 @@ __global__ void pack_shard_stats_kernel(const double* st, double* red) {
   red[1] = static_cast<double>(nbad);
   red[2] = st[3];
 }
-__global__ void unpack_shard_stats_kernel(const double* red, double* st, double inv_world) {
+// st[2] (first non-finite element) is this rank's own, shard-local: made chunk-global here;
+// it stays INT64_MAX when the non-finite values were in another rank's shard
+__global__ void unpack_shard_stats_kernel(const double* red, double* st, double inv_world,
+                                          long long shard_lo) {
   const unsigned long long nbad = static_cast<unsigned long long>(red[1]);
   st[0] = red[0];
   memcpy(&st[1], &nbad, 8);
+  long long bad;
+  memcpy(&bad, &st[2], 8);
+  if (bad != 0x7fffffffffffffffLL) {
+    bad += shard_lo;
+    memcpy(&st[2], &bad, 8);
+  }
   st[3] = red[2] * inv_world;
 }
 void pack_shard_stats(const double* st, double* red, cudaStream_t s) {
   pack_shard_stats_kernel<<<1, 1, 0, s>>>(st, red);
   check_launch("pack_shard_stats");
 }
-void unpack_shard_stats(const double* red, double* st, double inv_world, cudaStream_t s) {
-  unpack_shard_stats_kernel<<<1, 1, 0, s>>>(red, st, inv_world);
+void unpack_shard_stats(const double* red, double* st, double inv_world, long long shard_lo,
+                        cudaStream_t s) {
+  unpack_shard_stats_kernel<<<1, 1, 0, s>>>(red, st, inv_world, shard_lo);
   check_launch("unpack_shard_stats");
 }
 
