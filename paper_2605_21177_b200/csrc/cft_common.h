@@ -77,5 +77,8 @@ inline void check_launch(const char* what) {
 // {inner (contiguous), outer} with the given box and 128B swizzle.
 CUtensorMap make_tmap_bf16(const void* base, uint64_t inner, uint64_t outer,
                            uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer);
+// the same for fp32 (the TMA reduce-add epilogue's output view)
+CUtensorMap make_tmap_f32_sw128(const void* base, uint64_t inner, uint64_t outer,
+                                uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer);
 
 }  // namespace cft

@@ -63,6 +63,22 @@ bool& deterministic() {
   return d;
 }
 
+CUtensorMap make_tmap_f32_sw128(const void* base, uint64_t inner, uint64_t outer,
+                                uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
+  CUtensorMap m{};
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_stride_elems * 4};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error("cuTensorMapEncodeTiled (f32) failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
 int& kernel_variant(int op) {
   static int v[kNumVariantOps] = {
       [] {

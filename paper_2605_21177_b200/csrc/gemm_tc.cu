@@ -70,6 +70,9 @@ struct Args {
   // tile, (max, sum exp(v - max)) of the rounded outputs v -> ce_part[row * ce_stride + 2 tn + half]
   float2* ce_part;
   int ce_stride;
+  // fp32 red-add epilogue through the TMA engine (pair kernel, one unit per CTA pair: the
+  // mainloop's stage buffers are free for staging): 32x32 fp32 boxes of C, 128B-swizzled in smem
+  int tma_red;
 };
 
 // online (max, sum-exp) over 16 accumulator columns, on the bf16-rounded values the epilogue
@@ -618,7 +621,8 @@ struct PairCfg {
 template <bool A_MN, bool B_MN, int BNP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                         const __grid_constant__ CUtensorMap tmap_b, const Args args) {
+                         const __grid_constant__ CUtensorMap tmap_b, const Args args,
+                         const __grid_constant__ CUtensorMap tmap_c) {
   using P_ = PairCfg<BNP>;
   constexpr int kPairStages = P_::STAGES;
   constexpr uint32_t kPairABytes = P_::A_BYTES;
@@ -775,19 +779,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // two TMEM loads in flight per wait: the epilogue of a single-wave GEMM (narrow
         // slices, split-K) is exposed after the mainloop and latency-bound
         float ce_m = -INFINITY, ce_s = 0.f;
+        // (a warp whose rows start before the slice -- row_skip -- keeps the v4 red.add path:
+        // the reduce form of the TMA takes no negative coordinates)
+        if (args.tma_red &&
+            tm * BMP + static_cast<int>(rank) * 128 + quarter * 32 - args.row_skip >= 0) {
+          // this warp's 32 rows x BNP/2 columns -> BNP/64 swizzled 32x32 fp32 boxes (4 KB each)
+          // in the (drained) stage buffers, then one TMA reduce-add per box; rows outside C
+          // (the slice's leading rows, ragged M) are clipped by the tensor map
+          uint8_t* stg = sa + (warp - 2) * (32 * (BNP / 2) * 4);
+          const int lr = lane;  // row within the warp's 32
 #pragma unroll 1
-        for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 32) {
-          uint32_t r0[16], r1[16];
-          ptx::tmem_ld16(tacc + c, r0);
-          ptx::tmem_ld16(tacc + c + 16, r1);
-          ptx::tmem_wait_ld();
-          const int col = tn * BNP + c;
-          if (args.ce_part) {
-            ce_accum16(r0, col, args.N, ce_m, ce_s);
-            ce_accum16(r1, col + 16, args.N, ce_m, ce_s);
+          for (int c = 0; c < BNP / 2; c += 32) {
+            uint32_t r0[16], r1[16];
+            ptx::tmem_ld16(tacc + half * (BNP / 2) + c, r0);
+            ptx::tmem_ld16(tacc + half * (BNP / 2) + c + 16, r1);
+            ptx::tmem_wait_ld();
+            uint8_t* box = stg + (c / 32) * 4096;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {  // 16-byte chunk q of this row: columns 4q..4q+3
+              const uint32_t* src = q < 4 ? r0 + 4 * q : r1 + 4 * (q - 4);
+              *reinterpret_cast<uint4*>(box + lr * 128 + ((q ^ (lr & 7)) << 4)) =
+                  make_uint4(src[0], src[1], src[2], src[3]);
+            }
           }
-          if (row_ok && col < args.N) store16(args, rbase, col, r0);
-          if (row_ok && col + 16 < args.N) store16(args, rbase, col + 16, r1);
+          ptx::fence_proxy_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            const int row0 = tm * BMP + static_cast<int>(rank) * 128 + quarter * 32 - args.row_skip;
+            for (int c = 0; c < BNP / 2; c += 32)
+              ptx::tma_reduce_add_2d(&tmap_c, stg + (c / 32) * 4096,
+                                     tn * BNP + half * (BNP / 2) + c, row0);
+            ptx::bulk_commit_group();
+            ptx::bulk_wait_group0();
+          }
+          __syncwarp();
+        } else {
+#pragma unroll 1
+          for (int c = half * (BNP / 2); c < (half + 1) * (BNP / 2); c += 32) {
+            uint32_t r0[16], r1[16];
+            ptx::tmem_ld16(tacc + c, r0);
+            ptx::tmem_ld16(tacc + c + 16, r1);
+            ptx::tmem_wait_ld();
+            const int col = tn * BNP + c;
+            if (args.ce_part) {
+              ce_accum16(r0, col, args.N, ce_m, ce_s);
+              ce_accum16(r1, col + 16, args.N, ce_m, ce_s);
+            }
+            if (row_ok && col < args.N) store16(args, rbase, col, r0);
+            if (row_ok && col + 16 < args.N) store16(args, rbase, col + 16, r1);
+          }
         }
         if (args.ce_part && row_ok)
           args.ce_part[static_cast<long long>(row) * args.ce_stride + 2 * tn + half] =
@@ -931,7 +971,8 @@ void fill_units(Args& a, int bm, int bn, int slots, double us_per_kb, bool allow
 }
 
 template <bool A_MN, bool B_MN, int BNP>
-void launch_2sm(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream_t stream) {
+void launch_2sm(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream_t stream,
+                const CUtensorMap* tc = nullptr) {
   auto kern = gemm_bf16_2sm_kernel<A_MN, B_MN, BNP>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -940,7 +981,19 @@ void launch_2sm(const CUtensorMap& ta, const CUtensorMap& tb, Args a, cudaStream
     attr_done = true;
   }
   const int pairs = std::min(a.num_units, num_sms() / 2);
-  launch_pdl(kern, 2 * pairs, PairCfg<BNP>::SMEM, stream, ta, tb, a);
+  if (!tc) a.tma_red = 0;
+  const CUtensorMap& mc = tc ? *tc : ta;  // unused unless a.tma_red
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = PairCfg<BNP>::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kernel_variant(2) ? 1 : 0;
+  CFT_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, a, mc));
   check_launch("gemm_bf16_2sm_kernel");
 }
 
@@ -1113,6 +1166,14 @@ void linear_dgrad(const void* dy, int64_t n_tok, int64_t out_dim, const void* w,
 }
 
 // dW_S (+)= dY[:, rb:re)^T X -- slice-aware wgrad, fp32 out.
+int tma_red_mode() {  // experiments: CFT_WGRAD_TMA_RED=0 keeps the v4 red.add epilogue
+  static const int m = [] {
+    const char* e = std::getenv("CFT_WGRAD_TMA_RED");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+
 void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const void* x,
                         int64_t in_dim, int64_t rb, int64_t re, float* dw, int accumulate,
                         cudaStream_t stream) {
@@ -1195,8 +1256,19 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   } else {
     a.epi = kEpiF32;
   }
-  if (pairs && pair_bn == 128) launch_2sm<true, true, 128>(ta, tb, a, stream);
-  else if (pairs) launch_2sm<true, true, 256>(ta, tb, a, stream);
+  // one unit per CTA pair (a single wave): its drained stage buffers stage the fp32 tile and
+  // the TMA engine red-adds it into dw (one bulk op per 32 x 32 box instead of v4 red.adds)
+  CUtensorMap tcm;
+  const bool tma_red = pairs && a.epi == kEpiF32Red && a.num_units <= num_sms() / 2 &&
+                       tma_red_mode() != 0 && (reinterpret_cast<uintptr_t>(dw) & 15) == 0 &&
+                       in_dim % 4 == 0;
+  if (tma_red) {
+    tcm = make_tmap_f32_sw128(dw, static_cast<uint64_t>(in_dim), static_cast<uint64_t>(a.M),
+                              static_cast<uint64_t>(in_dim), 32, 32);
+    a.tma_red = 1;
+  }
+  if (pairs && pair_bn == 128) launch_2sm<true, true, 128>(ta, tb, a, stream, tma_red ? &tcm : nullptr);
+  else if (pairs) launch_2sm<true, true, 256>(ta, tb, a, stream, tma_red ? &tcm : nullptr);
   else if (BN == 256) launch<true, true, 256>(ta, tb, a, stream);
   else launch<true, true, 128>(ta, tb, a, stream);
 }
