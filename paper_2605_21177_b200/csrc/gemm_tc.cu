@@ -70,8 +70,8 @@ struct Args {
   // tile, (max, sum exp(v - max)) of the rounded outputs v -> ce_part[row * ce_stride + 2 tn + half]
   float2* ce_part;
   int ce_stride;
-  // fp32 red-add epilogue through the TMA engine (pair kernel, one unit per CTA pair: the
-  // mainloop's stage buffers are free for staging): 32x32 fp32 boxes of C, 128B-swizzled in smem
+  // fp32 red-add epilogue through the TMA engine (pair kernel): 32x32 fp32 boxes of C, staged
+  // 128B-swizzled in a per-warp smem box, reduce-added by cp.reduce.async.bulk.tensor
   int tma_red;
 };
 
@@ -615,7 +615,11 @@ struct PairCfg {
   static constexpr uint32_t B_BYTES = (BNP / 2) * BK * 2;  // this CTA's BNP/2 columns of B
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = 2 * BNP;
-  static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+  // after the stages: 1 KB of barriers, then one 4 KB 32x32 fp32 staging box per epilogue warp
+  // (the TMA reduce-add epilogue)
+  static constexpr uint32_t STG = STAGES * STAGE_BYTES + 1024;
+  static constexpr size_t SMEM = 1024 + STG + kEpiWarps * 4096;
+  static_assert(SMEM <= 227 * 1024, "pair GEMM smem");
 };
 
 template <bool A_MN, bool B_MN, int BNP>
@@ -786,32 +790,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // this warp's 32 rows x BNP/2 columns -> BNP/64 swizzled 32x32 fp32 boxes (4 KB each)
           // in the (drained) stage buffers, then one TMA reduce-add per box; rows outside C
           // (the slice's leading rows, ragged M) are clipped by the tensor map
-          uint8_t* stg = sa + (warp - 2) * (32 * (BNP / 2) * 4);
+          uint8_t* box = smem + P_::STG + (warp - 2) * 4096;  // this warp's staging box
           const int lr = lane;  // row within the warp's 32
+          const int row0 = tm * BMP + static_cast<int>(rank) * 128 + quarter * 32 - args.row_skip;
 #pragma unroll 1
           for (int c = 0; c < BNP / 2; c += 32) {
             uint32_t r0[16], r1[16];
             ptx::tmem_ld16(tacc + half * (BNP / 2) + c, r0);
             ptx::tmem_ld16(tacc + half * (BNP / 2) + c + 16, r1);
             ptx::tmem_wait_ld();
-            uint8_t* box = stg + (c / 32) * 4096;
+            if (c > 0) {  // the previous box has been read out by the TMA engine
+              if (lane == 0) ptx::bulk_wait_group_read0();
+              __syncwarp();
+            }
 #pragma unroll
             for (int q = 0; q < 8; ++q) {  // 16-byte chunk q of this row: columns 4q..4q+3
               const uint32_t* src = q < 4 ? r0 + 4 * q : r1 + 4 * (q - 4);
               *reinterpret_cast<uint4*>(box + lr * 128 + ((q ^ (lr & 7)) << 4)) =
                   make_uint4(src[0], src[1], src[2], src[3]);
             }
+            ptx::fence_proxy_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_reduce_add_2d(&tmap_c, box, tn * BNP + half * (BNP / 2) + c, row0);
+              ptx::bulk_commit_group();
+            }
           }
-          ptx::fence_proxy_async_shared();
-          __syncwarp();
-          if (lane == 0) {
-            const int row0 = tm * BMP + static_cast<int>(rank) * 128 + quarter * 32 - args.row_skip;
-            for (int c = 0; c < BNP / 2; c += 32)
-              ptx::tma_reduce_add_2d(&tmap_c, stg + (c / 32) * 4096,
-                                     tn * BNP + half * (BNP / 2) + c, row0);
-            ptx::bulk_commit_group();
-            ptx::bulk_wait_group0();
-          }
+          if (lane == 0) ptx::bulk_wait_group_read0();
           __syncwarp();
         } else {
 #pragma unroll 1
@@ -1202,10 +1207,12 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
     // chip-wide and is largely exposed for these short kernels, so every pass over the output
     // (one per split, one per stream-K segment) is charged
     constexpr double kRedBytesPerUs = 1.2e6;
+    // partial tiles go through the TMA reduce-add (measured ~3x the v4 rate)
+    const double red_tma = tma_red_mode() != 0 ? 3.6e6 : kRedBytesPerUs;
     auto cost = [&](const Args& x, double us_per_kb) {
       const int waves = (x.num_units + num_sms() / 2 - 1) / (num_sms() / 2);
       double t = waves * x.kb_per_split * us_per_kb;
-      t += x.splits * static_cast<double>(x.M) * x.N * 4.0 / kRedBytesPerUs;
+      t += x.splits * static_cast<double>(x.M) * x.N * 4.0 / red_tma;
       return t;
     };
     // stream-K over 256x256 tiles: every pair gets ceil(W / pairs) k-blocks of the linearised
@@ -1217,7 +1224,7 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
     ask.sk_len = (W + P - 1) / P;
     ask.num_units = static_cast<int>(std::min<long long>(P, (W + ask.sk_len - 1) / ask.sk_len));
     const double segs = static_cast<double>(ask.tiles_m) * ask.tiles_n + ask.num_units - 1;
-    const double cost_sk = ask.sk_len * 0.40 + segs * 256.0 * 256.0 * 4.0 / kRedBytesPerUs;
+    const double cost_sk = ask.sk_len * 0.40 + segs * 256.0 * 256.0 * 4.0 / red_tma;
     static const int sk_mode = [] {  // experiments: 1 force stream-K, 2 never
       const char* e = std::getenv("CFT_WGRAD_STREAMK");
       return e ? std::atoi(e) : 0;
@@ -1233,7 +1240,13 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
       a.splits = (a.total_kb + a.kb_per_split - 1) / a.kb_per_split;
       a.num_units = a.tiles_m * a.tiles_n * a.splits;
     } else if (g_policy == 0 && sk_mode != 2 && !deterministic() &&
-        (sk_mode == 1 || cost_sk < 0.95 * std::min(c128, c256))) {
+        (sk_mode == 1 ||
+         // with the TMA reduce-add (measured, configs[1] sweep, 4096 x 8192 tokens): stream-K
+         // wins whenever the 256x256 tiles are under two waves (|S| = 512: 945, 1024: 1170,
+         // 2048: 1140 TFLOP/s), the dense split-free tiling from two waves up (4096: 1345 vs
+         // 1301); without it, the cost model
+         (tma_red_mode() != 0 ? ask.tiles_m * ask.tiles_n < 2 * P
+                              : cost_sk < 0.95 * std::min(c128, c256)))) {
       a = ask;
     } else if (g_policy == 0 && c128 < c256) {
       a = a128;
@@ -1256,10 +1269,12 @@ void linear_wgrad_slice(const void* dy, int64_t n_tok, int64_t out_dim, const vo
   } else {
     a.epi = kEpiF32;
   }
-  // one unit per CTA pair (a single wave): its drained stage buffers stage the fp32 tile and
-  // the TMA engine red-adds it into dw (one bulk op per 32 x 32 box instead of v4 red.adds)
+  // partial fp32 tiles are staged box by box (32 x 32, 4 KB per epilogue warp) and the TMA
+  // engine red-adds them into dw (one bulk op per box instead of 256 v4 red.adds)
   CUtensorMap tcm;
-  const bool tma_red = pairs && a.epi == kEpiF32Red && a.num_units <= num_sms() / 2 &&
+  // (split / stream-K partials only: an unsplit tile's v4 red.adds overlap the next tile's
+  // mainloop better than the staged boxes do)
+  const bool tma_red = pairs && a.epi == kEpiF32Red && (a.splits > 1 || a.sk_len > 0) &&
                        tma_red_mode() != 0 && (reinterpret_cast<uintptr_t>(dw) & 15) == 0 &&
                        in_dim % 4 == 0;
   if (tma_red) {
