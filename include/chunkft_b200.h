@@ -368,6 +368,9 @@ typedef struct {
                             (north star item 4) -- ~35 GB less HBM for the 8B shape */
   double clip_max_norm;  /* > 0: clip the chunk's mean gradient to this global L2 norm inside the
                             fused AdamW (no reference counterpart); 0 = off */
+  cft_cost_policy policy; /* plan cost policy (config.hpp:42); all zero = the default 2/4/4/4/4.
+                            Also the storage width of every tensor (config.cpp:368) */
+  int32_t pad_;
 } cft_engine_config;
 
 /* One micro-batch (model.hpp:52-60).  x / target in the compute dtype; host pointers should
@@ -498,6 +501,35 @@ int cft_engine_wait_step(cft_engine* e, int64_t t, double* loss, double* gsq);
  * compute-dtype parameters. */
 int cft_engine_write_checkpoints(cft_engine* e, const char* dir);
 int cft_engine_read_checkpoints(cft_engine* e, const char* dir);
+
+/* ---- experiments: configs, presets and the artifact bundle ----
+ * ExperimentConfig (include/chunkft/config.hpp:36-49) as an opaque handle.  The training runs
+ * on the GPU engine above; the host side restates the reference's data generators and inits
+ * (src/model.cpp:99-264, same std::mt19937_64 streams) and its accounting (src/accounting.cpp).
+ *   cft_experiment_preset  <- make_preset (src/runner.cpp:131-142); unknown names list the known
+ *   cft_experiment_parse   <- parse_config (src/config.cpp:138-298), same error text
+ *   cft_experiment_load    <- load_config_file (src/config.cpp:300-310)
+ *   cft_experiment_to_json <- config_to_json(...).dump(2) (src/config.cpp:312-352)
+ *   cft_experiment_run     <- run_experiment + summary_text (src/runner.cpp:144-212): with an
+ *                             out_dir it writes memory_trace.csv, transfer_log.csv,
+ *                             trajectory.csv, plan.json, effective_config.json, summary text
+ *                             (returned) and checkpoints/chunk_NNNN.bin.  dtype CFT_F64 is the
+ *                             reference's arithmetic.
+ *   cft_run_preset_checks  <- run_preset_checks (src/runner.cpp:214-260): report + failures.
+ * Text outputs follow cft_engine_plan_json: *needed = length + 1, truncated to cap - 1. */
+typedef struct cft_experiment cft_experiment;
+int cft_preset_names(char* buf, int64_t cap, int64_t* needed); /* newline-separated */
+int cft_experiment_preset(const char* name, cft_experiment** out);
+int cft_experiment_parse(const char* json_text, cft_experiment** out);
+int cft_experiment_load(const char* path, cft_experiment** out);
+void cft_experiment_destroy(cft_experiment* e);
+int cft_experiment_set_out_dir(cft_experiment* e, const char* dir);
+int cft_experiment_set_seed(cft_experiment* e, uint64_t seed); /* the CLI's --seed override */
+int cft_experiment_to_json(const cft_experiment* e, char* buf, int64_t cap, int64_t* needed);
+int cft_experiment_run(const cft_experiment* e, cft_dtype dtype, cft_stream_t stream,
+                       char* summary, int64_t cap, int64_t* needed);
+int cft_run_preset_checks(cft_dtype dtype, cft_stream_t stream, char* report, int64_t cap,
+                          int64_t* needed, int32_t* failures);
 
 #ifdef __cplusplus
 }

@@ -213,8 +213,41 @@ def checkpoints():
     return out
 
 
+def presets():
+    """The reference's own run_experiment bundle for every built-in preset (src/runner.cpp:40-192)
+    and its run_preset_checks report (runner.cpp:214-260).  effective_config.json's out_dir is
+    replaced by @OUT@; checkpoints are kept as sha256 + size."""
+    import hashlib
+    import tempfile
+    names = ["quadratic-k2", "mlp-imbalanced-layers", "mlp-imbalanced-layers-identity",
+             "dense-reduction", "classification-sanity"]
+    out = {"checks": ref.preset_checks()[0], "runs": {}}
+    for name in names:
+        d = tempfile.mkdtemp()
+        summary = ref.run_preset(name, d)
+        files = {}
+        for root, _, fns in os.walk(d):
+            for fn in sorted(fns):
+                path = os.path.join(root, fn)
+                rel = os.path.relpath(path, d)
+                with open(path, "rb") as f:
+                    data = f.read()
+                if fn.endswith(".bin"):
+                    files[rel] = {"sha256": hashlib.sha256(data).hexdigest(), "bytes": len(data)}
+                else:
+                    files[rel] = {"text": data.decode().replace(d, "@OUT@")}
+        out["runs"][name] = {"summary": summary, "files": files}
+    return out
+
+
 def main():
+    import sys
     os.makedirs(OUT, exist_ok=True)
+    if sys.argv[1:] == ["presets"]:
+        with open(os.path.join(OUT, "presets.json"), "w") as f:
+            json.dump(presets(), f, indent=0)
+        print("preset fixtures written to", OUT)
+        return
     with open(os.path.join(OUT, "checkpoints.json"), "w") as f:
         json.dump(checkpoints(), f)
     with open(os.path.join(OUT, "plans.json"), "w") as f:
@@ -225,6 +258,8 @@ def main():
         json.dump(adamw(), f)
     with open(os.path.join(OUT, "train.json"), "w") as f:
         json.dump(train_runs(), f)
+    with open(os.path.join(OUT, "presets.json"), "w") as f:
+        json.dump(presets(), f, indent=0)
     print("golden fixtures written to", OUT)
 
 

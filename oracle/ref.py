@@ -54,6 +54,37 @@ if REF is not None:
     _s("ref_init_params", i64, vp, CT.c_int, CT.c_int, u64, vp, i64)
     _s("ref_train", CT.c_int, vp, CT.c_int, CT.c_int, vp, CT.c_int, CT.c_int, CT.c_int, vp, CT.c_int,
        vp, CT.c_int, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, CT.c_char_p)
+    _s("ref_config_json", CT.c_int, CT.c_char_p, CT.c_char_p, CT.c_char_p, i64)
+    _s("ref_run_preset", CT.c_int, CT.c_char_p, CT.c_char_p, CT.c_char_p, i64)
+    _s("ref_run_preset_checks", CT.c_int, CT.c_char_p, i64)
+
+
+def config_json(text=None, preset=None):
+    """(True, config_to_json(cfg).dump(2)) or (False, the reference's error message) for
+    make_preset(preset) / parse_config(text) (src/config.cpp:138-352, src/runner.cpp:131-142)."""
+    _need()
+    buf = CT.create_string_buffer(1 << 16)
+    rc = REF.ref_config_json(None if text is None else text.encode(),
+                             None if preset is None else preset.encode(), buf, len(buf))
+    return (True, buf.value.decode()) if rc == 0 else (False, _err())
+
+
+def run_preset(name, out_dir):
+    """make_preset + run_experiment into out_dir (src/runner.cpp:144-192); summary_text.
+    ``name`` may also be a JSON config document (parse_config)."""
+    _need()
+    buf = CT.create_string_buffer(1 << 14)
+    if REF.ref_run_preset(name.encode(), str(out_dir).encode(), buf, len(buf)) != 0:
+        raise RuntimeError(_err())
+    return buf.value.decode()
+
+
+def preset_checks():
+    """run_preset_checks (src/runner.cpp:214-260): (report, failures)."""
+    _need()
+    buf = CT.create_string_buffer(1 << 14)
+    f = REF.ref_run_preset_checks(buf, len(buf))
+    return buf.value.decode(), f
 
 
 def partition(tensors, K=None, budget=None, per_tensor=False, policy=(2, 4, 4, 4, 4), names=None,

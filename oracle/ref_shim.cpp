@@ -9,6 +9,7 @@
 //   * the 12 kernels, serial or OpenMP (include/chunkft/kernels.hpp:13-65)
 //   * adamw_chunk_step                 (include/chunkft/optimizer.hpp:50-100)
 //   * run_training end to end          (include/chunkft/trainer.hpp:49-50)
+//   * presets / run_experiment / run_preset_checks (include/chunkft/runner.hpp:27-42)
 // Nothing here is product code and nothing in the product links it.
 #include <cstdio>
 #include <cstring>
@@ -25,6 +26,8 @@
 #include "chunkft/partition.hpp"
 #include "chunkft/schedule.hpp"
 #include "chunkft/trainer.hpp"
+#include "chunkft/runner.hpp"
+#include <sstream>
 
 using namespace chunkft;
 
@@ -408,6 +411,52 @@ int ref_train(const int32_t* layers, int n_layers, int loss_kind, const double* 
       write_transfer_log_csv(r.transfers, std::filesystem::path(ckpt_dir) / "transfer_log.csv");
     }
     return 0;
+  } catch (const std::exception& e) {
+    set_err(e.what());
+    return -1;
+  }
+}
+
+// config_to_json(...).dump(2) of make_preset(preset) (preset != NULL) or of
+// parse_config(json::parse(text)); -1 and ref_last_error() on any failure.
+int ref_config_json(const char* text, const char* preset, char* out, int64_t cap) {
+  try {
+    const ExperimentConfig cfg =
+        preset ? make_preset(preset) : parse_config(nlohmann::json::parse(text));
+    const std::string s = config_to_json(cfg).dump(2);
+    if (out && cap > 0) std::snprintf(out, static_cast<size_t>(cap), "%s", s.c_str());
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(e.what());
+    return -1;
+  }
+}
+
+// make_preset(name) + run_experiment with out_dir set (runner.cpp:144-192): writes the
+// artifact bundle and returns summary_text in `summary`.
+int ref_run_preset(const char* name, const char* out_dir, char* summary, int64_t cap) {
+  try {
+    // a name starting with '{' is a JSON config document (parse_config, config.cpp:138)
+    ExperimentConfig cfg =
+        name[0] == '{' ? parse_config(nlohmann::json::parse(name)) : make_preset(name);
+    cfg.out_dir = out_dir ? out_dir : "";
+    const RunArtifacts a = run_experiment(cfg);
+    const std::string s = summary_text(a);
+    if (summary && cap > 0) std::snprintf(summary, static_cast<size_t>(cap), "%s", s.c_str());
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(e.what());
+    return -1;
+  }
+}
+
+// run_preset_checks (runner.cpp:214-260): the report text, returns the failure count.
+int ref_run_preset_checks(char* report, int64_t cap) {
+  try {
+    std::ostringstream os;
+    const int f = run_preset_checks(os);
+    if (report && cap > 0) std::snprintf(report, static_cast<size_t>(cap), "%s", os.str().c_str());
+    return f;
   } catch (const std::exception& e) {
     set_err(e.what());
     return -1;

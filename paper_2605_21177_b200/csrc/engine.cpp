@@ -119,11 +119,12 @@ void Engine::setup(const double* init_params, uint64_t seed, cudaStream_t stream
     i.rows = t.rows;
     i.cols = t.cols;
     i.reg_order = t.id;
+    i.storage_precision = cfg_.policy.param_bytes;
     infos.push_back(i);
   }
-  if (cfg_.plan_mode == 1) plan_ = host::partition_by_budget(infos, cfg_.budget_bytes);
-  else if (cfg_.plan_mode == 2) plan_ = host::partition_per_tensor(infos);
-  else plan_ = host::partition(infos, cfg_.K);
+  if (cfg_.plan_mode == 1) plan_ = host::partition_by_budget(infos, cfg_.budget_bytes, cfg_.policy);
+  else if (cfg_.plan_mode == 2) plan_ = host::partition_per_tensor(infos, cfg_.policy);
+  else plan_ = host::partition(infos, cfg_.K, cfg_.policy);
   cfg_.K = plan_.K();
   host::ScheduleConfig sc;
   sc.K = cfg_.K;
@@ -1175,6 +1176,7 @@ std::string Engine::plan_json() const {
     i.rows = t.rows;
     i.cols = t.cols;
     i.reg_order = t.id;
+    i.storage_precision = cfg_.policy.param_bytes;
     infos.push_back(i);
   }
   return host::plan_to_json(plan_, infos);

@@ -64,6 +64,7 @@ struct EngineConfig {
   // and all-gathers the updated parameters (see include/chunkft_b200.h).
   int shard_rank = 0, shard_world = 1;
   double clip_max_norm = 0.0;  // > 0: global-norm clip of the chunk's mean gradient (no ref.)
+  host::CostPolicy policy;  // plan decisions + per-tensor storage width (config.hpp:42)
   int remat = 0;  // Llama engine: keep layer inputs only, recompute suffix layers in backward
 };
 

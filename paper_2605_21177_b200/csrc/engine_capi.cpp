@@ -34,6 +34,14 @@ static cft::EngineConfig to_config(const cft_engine_config* c) {
   cfg.shard_world = c->shard_world > 1 ? c->shard_world : 1;
   cfg.clip_max_norm = c->clip_max_norm;
   cfg.remat = c->remat;
+  if (c->policy.param_bytes != 0 || c->policy.grad_bytes != 0 || c->policy.master_bytes != 0 ||
+      c->policy.moment1_bytes != 0 || c->policy.moment2_bytes != 0) {
+    cfg.policy.param_bytes = c->policy.param_bytes;
+    cfg.policy.grad_bytes = c->policy.grad_bytes;
+    cfg.policy.master_bytes = c->policy.master_bytes;
+    cfg.policy.moment1_bytes = c->policy.moment1_bytes;
+    cfg.policy.moment2_bytes = c->policy.moment2_bytes;
+  }
   return cfg;
 }
 

@@ -37,7 +37,8 @@ class EngineConfigC(C.Structure):
                 ("hyper", N.AdamWHyperC), ("full_backward", C.c_int32),
                 ("check_every_step", C.c_int32), ("grad_scale", C.c_double),
                 ("cuda_graphs", C.c_int32), ("shard_rank", C.c_int32),
-                ("shard_world", C.c_int32), ("remat", C.c_int32), ("clip_max_norm", C.c_double)]
+                ("shard_world", C.c_int32), ("remat", C.c_int32), ("clip_max_norm", C.c_double),
+                ("policy", N.CostPolicy), ("pad_", C.c_int32)]
 
 
 class BatchC(C.Structure):
