@@ -453,6 +453,33 @@ int cft_engine_set_peers(cft_engine* e, const void* const* aux, const void* cons
 int cft_ipc_open(const void* handle, void** ptr);
 int cft_ipc_close(void* ptr);
 
+/* One data-parallel step driven from C / C++ (trainer.cpp:45-58 with micro_batches = world;
+ * the same exchange order as paper_2605_21177_b200/dp.py, so both hosts produce the same
+ * bits).  The host brings its communication as callbacks -- NCCL on the engine's stream for a
+ * multi-GPU job, anything else in tests.  Each callback returns 0 on success and must order its
+ * work on `stream` (or complete it before returning):
+ *   all_reduce      in-place SUM over ranks of n elements (dtype CFT_F32 / CFT_F64);
+ *   reduce_scatter  out[0, n) = SUM over ranks of in[rank * n, rank * n + n);
+ *   all_gather      in place: buf[r * n, r * n + n) <- rank r's part, every r;
+ *   barrier         work queued before it on every rank is complete (and visible through peer
+ *                   memory) before work queued after it on any rank.
+ * Protocols, chosen by the engine's configuration: replicated state -> one all_reduce of the
+ * active chunk's gradient; sharded -> reduce_scatter, all_reduce of 3 statistics, AdamW on the
+ * shard, all_gather; sharded with peers set (cft_engine_set_peers) -> barrier, the pull
+ * reduce-scatter over peer memory, all_reduce of 3 statistics, AdamW storing into every rank's
+ * gather buffer, barrier.  grad_scale is set to 1 / world.  `batches` holds micro_batches
+ * entries. */
+typedef struct {
+  void* ctx;
+  int32_t world, rank;
+  int (*all_reduce)(void* ctx, void* buf, int64_t n, int32_t dtype, cft_stream_t stream);
+  int (*reduce_scatter)(void* ctx, const void* in, void* out, int64_t n, int32_t dtype,
+                        cft_stream_t stream);
+  int (*all_gather)(void* ctx, void* buf, int64_t n, int32_t dtype, cft_stream_t stream);
+  int (*barrier)(void* ctx, cft_stream_t stream);
+} cft_comm;
+int cft_engine_step_dp(cft_engine* e, const cft_batch* batches, const cft_comm* comm);
+
 /* TrainTrajectoryEntry (trainer.hpp:26-33): step, chunk, loss (pre-update mean), grad_norm_sq. */
 int64_t cft_engine_trajectory(cft_engine* e, int64_t* step, int32_t* chunk, double* loss,
                               double* gsq, int64_t cap);

@@ -117,6 +117,7 @@ class Engine {
   void ipc_handles(void* aux_handle, void* gather_handle) const;  // 2 x cudaIpcMemHandle_t
   void set_peers(const void* const* aux, const void* const* gather);
   void clear_peers() { p2p_ = false; }
+  bool peers_set() const { return p2p_; }
   void prepare_graphs();  // capture every chunk's forward+backward graph now (Llama engine)
 
   // results

@@ -104,6 +104,60 @@ int cft_engine_step(cft_engine* e, const cft_batch* batches) {
   });
 }
 
+// One data-parallel step with the host's communication as callbacks (dp.py's DataParallelStep
+// in C; trainer.cpp:45-58 with micro_batches = world).  The order of exchanges is the Python
+// driver's, so both hosts produce the same bits.
+int cft_engine_step_dp(cft_engine* e, const cft_batch* batches, const cft_comm* comm) {
+  return guarded([&] {
+    CFT_CHECK(comm && comm->world >= 1, "engine: step_dp needs a communicator");
+    cft::Engine& g = *e->p;
+    cudaStream_t s = g.stream();
+    auto call = [&](int rc, const char* what) {
+      if (rc != 0) throw cft::Error(std::string("engine: step_dp: ") + what + " callback failed");
+    };
+    const int world = comm->world;
+    g.set_grad_scale(1.0 / world);
+    g.step_begin();
+    for (int mb = 0; mb < g.micro_batches(); ++mb) g.forward_backward(to_batch(batches + mb), mb);
+    void* aux = nullptr;
+    int64_t n = 0;
+    int dt = 0;
+    g.grad_buffer(&aux, &n, &dt);
+    if (!g.sharded()) {  // replicated state: one all-reduce of the active chunk's gradient
+      if (world > 1) {
+        CFT_CHECK(comm->all_reduce, "engine: step_dp: all_reduce callback missing");
+        call(comm->all_reduce(comm->ctx, aux, n, dt, s), "all_reduce");
+      }
+      g.step_end();
+      return;
+    }
+    CFT_CHECK(comm->all_reduce, "engine: step_dp: all_reduce callback missing");
+    if (g.peers_set()) {  // peer-memory exchange: pull reduce-scatter, AdamW stores everywhere
+      CFT_CHECK(comm->barrier, "engine: step_dp: barrier callback missing");
+      call(comm->barrier(comm->ctx, s), "barrier");  // every accumulator complete
+      call(comm->all_reduce(comm->ctx, g.shard_stats(), 3, CFT_F64, s), "all_reduce");
+      g.step_end();
+      call(comm->barrier(comm->ctx, s), "barrier");  // every rank's stores landed
+      g.gather_end();
+      return;
+    }
+    CFT_CHECK(comm->reduce_scatter && comm->all_gather,
+              "engine: step_dp: reduce_scatter / all_gather callbacks missing");
+    void* shard = nullptr;
+    int64_t padded = 0, valid = 0;
+    g.shard_buffer(&shard, &padded, &valid);
+    call(comm->reduce_scatter(comm->ctx, aux, shard, padded, dt, s), "reduce_scatter");
+    call(comm->all_reduce(comm->ctx, g.shard_stats(), 3, CFT_F64, s), "all_reduce");
+    g.step_end();
+    void* buf = nullptr;
+    int64_t total = 0, off = 0;
+    int gdt = 0;
+    g.gather_buffer(&buf, &total, &off, &gdt);
+    call(comm->all_gather(comm->ctx, buf, total / world, gdt, s), "all_gather");
+    g.gather_end();
+  });
+}
+
 int cft_engine_finish(cft_engine* e) {
   return guarded([&] { e->p->finish(); });
 }

@@ -1,9 +1,9 @@
 # ncu evidence for round 2 (one gpurun call; each ncu after the same command exited 0):
 #   /usr/local/graft/bin/gpurun --timeout 3000 -- 'bash scripts/gpu_profiles.sh'
 mkdir -p gpurun_out
-# 1. launch list of one 8B step (2 layers to bound the capture; same kernels as the 32-layer step)
+# 1. launch list of the whole 8B bench run (warm-up + 2 timed steps + the profiled leg)
 python bench.py --layers 32 --steps 2 --warmup 3 --no-sweep --no-cpu-baseline --no-e2e > gpurun_out/prof_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 3000 -c 1400 --csv \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 4000 --csv \
     --log-file gpurun_out/r2_launches.csv python bench.py --layers 32 --steps 2 --warmup 3 --no-sweep --no-cpu-baseline --no-e2e > gpurun_out/prof_ncu1.log 2>&1; echo "launch list exit $?"
 # 2. full captures: attention forward / backward kernels at the 8B layer shape
 python scripts/attn_probe.py 3 > gpurun_out/attn_plain.log 2>&1 && \
