@@ -629,6 +629,8 @@ int64_t grad_macs(const std::vector<LayerCfg>& layers, const std::vector<TensorD
   return macs;
 }
 
+std::string summary_text(const struct Result& R);
+
 Result run_experiment(const Experiment& cfg, int dtype, cudaStream_t stream) {
   Result R;
   R.cfg = cfg;
@@ -772,6 +774,7 @@ Result run_experiment(const Experiment& cfg, int dtype, cudaStream_t stream) {
     write(out / "plan.json", eng.plan_json() + "\n");
     write(out / "effective_config.json", to_json(R.cfg).dump(2) + "\n");
     eng.write_checkpoints((out / "checkpoints").string());
+    write(out / "summary.txt", summary_text(R));
   }
   return R;
 }
