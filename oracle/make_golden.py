@@ -216,7 +216,7 @@ def checkpoints():
 def presets():
     """The reference's own run_experiment bundle for every built-in preset (src/runner.cpp:40-192)
     and its run_preset_checks report (runner.cpp:214-260).  effective_config.json's out_dir is
-    replaced by @OUT@; checkpoints are kept as sha256 + size."""
+    replaced by @OUT@; checkpoints are kept as sha256 + size + the 36-byte CKFT v1 header."""
     import hashlib
     import tempfile
     names = ["quadratic-k2", "mlp-imbalanced-layers", "mlp-imbalanced-layers-identity",
@@ -233,7 +233,8 @@ def presets():
                 with open(path, "rb") as f:
                     data = f.read()
                 if fn.endswith(".bin"):
-                    files[rel] = {"sha256": hashlib.sha256(data).hexdigest(), "bytes": len(data)}
+                    files[rel] = {"sha256": hashlib.sha256(data).hexdigest(), "bytes": len(data),
+                                  "header": data[:36].hex()}
                 else:
                     files[rel] = {"text": data.decode().replace(d, "@OUT@")}
         out["runs"][name] = {"summary": summary, "files": files}

@@ -121,6 +121,40 @@ __global__ void __launch_bounds__(kThreads) grad_stats_kernel(const T* __restric
   }
 }
 
+// ---- fp64 statistics in the reference's order: take_mean_grad then `gsq += g * g` element by
+// element (src/trainer.cpp:58-60), so grad_norm_sq is bit-identical, not just within an ulp.
+// One warp: coalesced loads of 32 elements, then every lane folds them in index order (the sum
+// is warp-uniform).  The fp64 path is the parity path; its chunks are small. ----
+__global__ void __launch_bounds__(32) grad_stats_seq_f64_kernel(const double* __restrict__ g,
+                                                                 long long n, double scale,
+                                                                 double* stats) {
+  double acc = 0.0;
+  long long bad = LLONG_MAX;
+  unsigned long long nbad = 0;
+  const int lane = threadIdx.x;
+  for (long long base = 0; base < n; base += 32) {
+    const long long i = base + lane;
+    const double e = i < n ? __dmul_rn(g[i], scale) : 0.0;
+    const int cnt = n - base < 32 ? static_cast<int>(n - base) : 32;
+    for (int k = 0; k < cnt; ++k) {
+      const double ek = __shfl_sync(0xffffffffu, e, k);
+      if (!isfinite(ek)) {
+        ++nbad;
+        bad = min(bad, base + k);
+      } else {
+        acc = __dadd_rn(acc, __dmul_rn(ek, ek));
+      }
+    }
+  }
+  if (lane == 0) {
+    stats[0] = __dadd_rn(stats[0], acc);
+    if (nbad) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stats[1]), nbad);
+      atomicMin(reinterpret_cast<long long*>(&stats[2]), bad);
+    }
+  }
+}
+
 // ---- fp32-state AdamW: 2 x 4 elements per thread with all 8 vector loads issued up front
 // (memory-level parallelism for the small chunks of narrow plans); block-level min/max of
 // 1/denom so only one atomic pair per block reaches L2; optionally leaves the gradient
@@ -647,8 +681,8 @@ int cft_grad_stats(cft_dtype state_dtype, const void* grad, int64_t n, double gr
       grad_stats_kernel<float><<<grid_for(n / 4 + 1), kThreads, 0, s>>>(
           static_cast<const float*>(grad), n, grad_scale, static_cast<double*>(stats_dev));
     } else if (state_dtype == CFT_F64) {
-      grad_stats_kernel<double><<<grid_for(n), kThreads, 0, s>>>(
-          static_cast<const double*>(grad), n, grad_scale, static_cast<double*>(stats_dev));
+      grad_stats_seq_f64_kernel<<<1, 32, 0, s>>>(static_cast<const double*>(grad), n, grad_scale,
+                                                  static_cast<double*>(stats_dev));
     } else {
       throw cft::Error("cft_grad_stats: state dtype must be F32 or F64");
     }

@@ -678,19 +678,47 @@ Result run_experiment(const Experiment& cfg, int dtype, cudaStream_t stream) {
   int64_t resident_param_bytes = 0;
   for (const TensorDesc& t : ts) resident_param_bytes += t.rows * t.cols * cfg.policy.param_bytes;
 
+  // the engine reads host batches in its compute dtype: fp64 as generated, fp32 / bf16 rounded
+  // to nearest (the bf16 through fp32, like the Python binding's torch conversion)
+  auto narrow = [dtype](const std::vector<double>& v) {
+    const size_t w = dtype == CFT_F64 ? 8 : dtype == CFT_F32 ? 4 : 2;
+    std::vector<char> out(v.size() * w);
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (w == 8) {
+        std::memcpy(out.data() + 8 * i, &v[i], 8);
+        continue;
+      }
+      const float f = static_cast<float>(v[i]);
+      if (w == 4) {
+        std::memcpy(out.data() + 4 * i, &f, 4);
+        continue;
+      }
+      uint32_t u;
+      std::memcpy(&u, &f, 4);
+      const uint16_t h = std::isnan(f) ? uint16_t(0x7fc0)
+                                       : uint16_t((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+      std::memcpy(out.data() + 2 * i, &h, 2);
+    }
+    return out;
+  };
+  std::vector<std::vector<char>> xs, ys;
+  for (const HostBatch& hb : batches) {
+    xs.push_back(narrow(hb.x));
+    ys.push_back(narrow(hb.target));
+  }
+
   host::RotationScheduler& sched = eng.scheduler();
   size_t cursor = 0;
   int64_t rotation_macs = 0;
-  std::vector<std::unique_ptr<HostBatch>> keep;
   for (int64_t t = 0; t < cfg.steps; ++t) {
     const int active = eng.step_begin();
     for (int mb = 0; mb < cfg.micro_batches; ++mb) {
       const HostBatch& hb = batches[cursor];
-      cursor = (cursor + 1) % batches.size();
       Batch b;
-      b.x = hb.x.empty() ? nullptr : hb.x.data();
+      b.x = hb.x.empty() ? nullptr : xs[cursor].data();
       b.tokens = hb.tokens.empty() ? nullptr : hb.tokens.data();
-      b.target = hb.target.empty() ? nullptr : hb.target.data();
+      b.target = hb.target.empty() ? nullptr : ys[cursor].data();
+      cursor = (cursor + 1) % batches.size();
       b.labels = hb.labels.empty() ? nullptr : hb.labels.data();
       b.on_device = 0;
       eng.forward_backward(b, mb);

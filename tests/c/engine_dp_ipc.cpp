@@ -11,7 +11,7 @@
 // calls cft_engine_set_peers -- the gradient then moves through peer memory and only the three
 // statistics and two barriers go through the callbacks.  No kernel ever waits on the other
 // process: every barrier synchronises the stream on the host first.  Each rank writes its final
-// parameters (from the masters, %.17g) to <out dir>/rank<r>.txt.
+// parameters (%.17g; the device copy when sharded) to <out dir>/rank<r>.txt.
 //
 // Case file (whitespace-separated): n_layers, then per layer type a b c bias; loss rows K T steps
 // n_batches in_dim out_dim; the initial parameters; then n_batches x (rows*in_dim x values,
@@ -222,7 +222,8 @@ int run_rank(const Case& c, const std::string& mode, Link L, const std::string& 
   }
   check(cft_engine_finish(e), "finish");
   std::vector<double> p(c.init.size());
-  check(cft_engine_params(e, p.data(), 1), "params");
+  // sharded ranks hold only their shard of the masters: read the (fp64) device parameters
+  check(cft_engine_params(e, p.data(), sharded ? 0 : 1), "params");
   const std::string path = out_dir + "/rank" + std::to_string(L.rank) + ".txt";
   FILE* f = std::fopen(path.c_str(), "w");
   if (!f) die("open", path.c_str());
