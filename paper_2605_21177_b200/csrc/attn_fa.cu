@@ -29,9 +29,12 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "attn.h"
 #include "cft_common.h"
@@ -185,7 +188,29 @@ struct FwdArgs {
   int ldo;
   float* lse;  // [B][H][S] log2-sum-exp of the scaled scores
   float scale_log2;
+  unsigned long long* trace;  // development timeline of CTA 0 (CFT_ATTN_TRACE=<file>), or null
 };
+
+// Timeline events (trace builds, CTA 0 only, when a.trace is set): three regions of 8192
+// {clock64, code} records -- role 0 the MMA issuer, 1 / 2 the first softmax warp of head A / B --
+// each filled by one thread with a register counter (plain stores, no atomics on the path).
+// code = event | head << 8 | block << 16.  Off (null) in every normal run.
+enum TraceEv : unsigned { kEvSIssue = 1, kEvPvWait, kEvPvIssue, kEvSfull, kEvLdDone, kEvBarDone,
+                          kEvExpDone, kEvPfull, kEvEpiStart, kEvEpiEnd, kEvItem };
+constexpr int kTraceRecs = 8192;
+__device__ __forceinline__ void trace_ev(unsigned long long* tr, int role, int& cnt, unsigned ev,
+                                         int head, int blk) {
+#ifndef CFT_ATTN_TRACE  // compiled in only for timeline builds (make ATTN_TRACE=1)
+  return;
+#endif
+  if (tr == nullptr || blockIdx.x != 0) return;
+  const int i = cnt++;
+  if (i < kTraceRecs) {
+    unsigned long long* r = tr + 2 * (static_cast<size_t>(role) * kTraceRecs + i);
+    r[0] = clock64();
+    r[1] = ev | (unsigned(head) << 8) | (unsigned(blk) << 16);
+  }
+}
 
 // A operand from TMEM (the "ts" form): P is written by the softmax warps into the S columns
 // of its own rows (row m = lane m, two bf16 per 32-bit column, K order), so P.V reads no
@@ -200,7 +225,7 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
 }
 
 // ------------------------------------------------------------------------------------------
-// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-9 softmax of head A, 10-17 of B.
+// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax of head A, 6-9 of B.
 // 128-row key blocks (K ring of 2, V ring of 3).  TMEM: S_A, S_B (128 columns each), O_A, O_B;
 // the softmax thread of a row reads its 128 scores, writes P (bf16) into the first 64
 // columns of its own S row, and P.V runs with A from TMEM.  The tensor pipe executes
@@ -210,12 +235,11 @@ template <int HD>
 struct FwdSmem {
   static constexpr int NK = 2, NV = 2;
   static constexpr uint32_t QT = 128 * HD * 2;  // query tile / key or value block (128 rows)
-  static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NK * QT, XCH = V0 + NV * QT,
-                            BAR = XCH + 8 * 128 * 4;
+  static constexpr uint32_t Q0 = 0, K0 = 2 * QT, V0 = K0 + NK * QT, BAR = V0 + NV * QT;
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
-constexpr int kFwdThreads = 64 + 16 * 32;  // TMA warp, MMA warp, 16 softmax warps
+constexpr int kFwdThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 softmax warps
 
 // Work item = (query tile, batch, KV head, head pair), longest query tiles first; a persistent
 // CTA walks items blockIdx.x, +gridDim.x, ...  The next item's Q tiles load while the current
@@ -237,7 +261,7 @@ __device__ __forceinline__ FwdItem fwd_item(const FwdArgs& a, int item) {
 }
 
 template <int HD>
-__global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 32 <= 16K registers
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmq, const FwdArgs a, int n_items) {
   using L = FwdSmem<HD>;
   constexpr int NB = HD / 64, NK = L::NK, NV = L::NV;
@@ -272,9 +296,9 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&sfull[t], 1);
-      mbar_init(&pfull[t], 8);  // one arrival per softmax warp
+      mbar_init(&pfull[t], 4);  // one arrival per softmax warp
       mbar_init(&ofull[t], 1);
-      mbar_init(&oempty[t], 8);
+      mbar_init(&oempty[t], 4);
     }
     fence_barrier_init();
   }
@@ -317,9 +341,11 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
     }
   } else if (warp == 1) {
     {  // the whole warp walks the MMA program; one elected lane issues
+      int tcnt = 0;  // trace records (trace builds)
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t ID_O = idesc_bf16_f32(128, HD, false, true);
       auto issue_s = [&](int t, int g) {  // S_t of key block g (K slot g % NK)
+        if (lane == 0) trace_ev(a.trace, 0, tcnt, kEvSIssue, t, g);
         const uint8_t* q = sm + L::Q0 + t * L::QT;
         const uint8_t* k = sm + L::K0 + (g % NK) * L::QT;
         const uint64_t dq = desc_k(q, 0, kBlk128), dk = desc_k(k, 0, kBlk128);
@@ -335,6 +361,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
         __syncwarp();
       };
       auto issue_pv = [&](int t, int g, int j) {  // O_t += P_t V(g)
+        if (lane == 0) trace_ev(a.trace, 0, tcnt, kEvPvIssue, t, g);
         const uint8_t* v = sm + L::V0 + (g % NV) * L::QT;
         const uint64_t dv = desc_mn(v, 0, kBlk128);
         if (elect_one()) {
@@ -364,6 +391,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
           spin_wait(&vfull[g % NV], (g / NV) & 1);
           if (j == 0 && n > 0) spin_wait(&oempty[0], (n - 1) & 1);  // O_A read out
           spin_wait(&pfull[0], g & 1);
+          if (lane == 0) trace_ev(a.trace, 0, tcnt, kEvPvWait, 0, g);
           tc_fence_after();
           issue_pv(0, g, j);
           if (j + 1 == nb && elect_one()) umma_commit(&ofull[0]);
@@ -374,6 +402,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
           }
           if (j == 0 && n > 0) spin_wait(&oempty[1], (n - 1) & 1);  // O_B read out
           spin_wait(&pfull[1], g & 1);
+          if (lane == 0) trace_ev(a.trace, 0, tcnt, kEvPvWait, 1, g);
           tc_fence_after();
           issue_pv(1, g, j);
           if (j + 1 == nb && elect_one()) umma_commit(&ofull[1]);
@@ -385,51 +414,47 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
       }
     }
   } else {
-    // softmax: 8 warps per head, two per TMEM lane quarter; a thread owns half a row (64 of the
-    // block's 128 scores, half of O's columns).  The halves agree on the row max through a
-    // double-buffered smem exchange and a named barrier per head, which also orders both
-    // halves' score reads before either writes its P over the row's S columns.
+    // softmax: 4 warps per head, one per TMEM lane quarter; a thread owns a whole row (the
+    // block's 128 scores and O's HD columns), so the row max needs no exchange between warps.
     const int idx = warp - 2;
-    const int t = idx / 8, hf = (idx / 4) & 1;
+    const int t = idx / 4;
     const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tS = tbase + lo + 128 * t, tO = tbase + lo + 256 + HD * t + hf * (HD / 2);
-    float* xch = reinterpret_cast<float*>(sm + L::XCH);  // [2 parity][2 heads][2 halves][128]
-    auto slot = [&](int par, int half) { return xch + ((par * 2 + t) * 2 + half) * 128 + r; };
+    const uint32_t tS = tbase + lo + 128 * t, tO = tbase + lo + 256 + HD * t;
     const float c = a.scale_log2;
-    int g = 0, n = 0, xp = 0;
+    unsigned long long* const tr = (idx & 3) == 0 && lane == 0 ? a.trace : nullptr;
+    int tcnt = 0;
+    int g = 0, n = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++n) {
       const FwdItem w = fwd_item(a, item);
       const int qpos = w.i * 128 + r;
       float m = -INFINITY, l = 0.f;
+      trace_ev(tr, 1 + t, tcnt, kEvItem, t, w.nb);
       for (int j = 0; j < w.nb; ++j, ++g) {
         spin_wait(&sfull[t], g & 1);
+        trace_ev(tr, 1 + t, tcnt, kEvSfull, t, g);
         tc_fence_after();
-        uint32_t v[64];
-        tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-        tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        uint32_t v[128];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tmem_ld32(tS + q * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * q));
         tmem_wait_ld();
+        trace_ev(tr, 1 + t, tcnt, kEvLdDone, t, g);
         // the diagonal block: masked scores become -inf, so one exp path serves every block
         // (a separate masked path gets if-converted into predicated-off MUFU issue slots)
         if (j == w.i) {
-          const int lim = r - hf * 64;  // this half's columns e <= lim are visible
 #pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e > lim) v[e] = __float_as_uint(-INFINITY);
+          for (int e = 0; e < 128; ++e)
+            if (e > r) v[e] = __float_as_uint(-INFINITY);
         }
         float mk[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) mk[q] = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < 64; ++e) mk[e & 3] = fmaxf(mk[e & 3], f32(v[e]));
-        float mx = fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3]));
-        *slot(xp, hf) = mx;
-        tc_fence_before();
-        named_bar_sync(1 + t, 256);
-        tc_fence_after();
-        mx = fmaxf(mx, *slot(xp, hf ^ 1));
-        xp ^= 1;
+        for (int e = 0; e < 128; ++e) mk[e & 3] = fmaxf(mk[e & 3], f32(v[e]));
+        const float mx = fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3]));
+        trace_ev(tr, 1 + t, tcnt, kEvBarDone, t, g);
         const float m_new = fmaxf(m, mx * c);
         if (j == 0) {
           m = m_new;
@@ -439,7 +464,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
           l *= alpha;
           m = m_new;
 #pragma unroll 1
-          for (int cc = 0; cc < HD / 32; ++cc) {  // this half's HD/2 columns, 16 at a time
+          for (int cc = 0; cc < HD / 16; ++cc) {  // the row's HD columns, 16 at a time
             uint32_t o[16];
             tmem_ld16(tO + cc * 16, o);
             tmem_wait_ld();
@@ -451,7 +476,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
         float2 accs[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int e = 0; e < 64; e += 4) {  // P packed in place: word e/2 holds columns e, e+1
+        for (int e = 0; e < 128; e += 4) {  // P packed in place: word e/2 holds columns e, e+1
           float2 x0 = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
           float2 x1 = __ffma2_rn(make_float2(f32(v[e + 2]), f32(v[e + 3])), c2, nm2);
           x0.x = ex2_mix<0>(x0.x);
@@ -464,25 +489,23 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
         }
         const float2 acc = __fadd2_rn(accs[0], accs[1]);
         l += acc.x + acc.y;
-        // P words [32 hf, 32 hf + 32) of the row: columns 64 hf .. 64 hf + 63 in K order
-        tmem_st32(tS + hf * 32, *reinterpret_cast<const uint32_t(*)[32]>(v));
+        trace_ev(tr, 1 + t, tcnt, kEvExpDone, t, g);
+        // P words [0, 64) of the row: columns 0 .. 127 in K order, over the row's S columns
+        tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(v));
+        tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(v + 32));
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[t]);
+        trace_ev(tr, 1 + t, tcnt, kEvPfull, t, g);
       }
-      // l of the whole row = the two halves' sums (same running max)
-      *slot(xp, hf) = l;
-      named_bar_sync(1 + t, 256);
-      l += *slot(xp, hf ^ 1);
-      xp ^= 1;
       spin_wait(&ofull[t], n & 1);
+      trace_ev(tr, 1 + t, tcnt, kEvEpiStart, t, n);
       tc_fence_after();
       const float inv = 1.f / l;
-      bf16* out = a.o + static_cast<long long>(w.b * a.S + qpos) * a.ldo + (w.h0 + t) * HD +
-                  hf * (HD / 2);
+      bf16* out = a.o + static_cast<long long>(w.b * a.S + qpos) * a.ldo + (w.h0 + t) * HD;
 #pragma unroll
-      for (int cc = 0; cc < HD / 64; ++cc) {
+      for (int cc = 0; cc < HD / 32; ++cc) {
         uint32_t o[32];
         tmem_ld32(tO + cc * 32, o);
         tmem_wait_ld();
@@ -491,8 +514,8 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SM sub-partition x 96 x 3
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&oempty[t]);
-      if (hf == 0)
-        a.lse[(static_cast<long long>(w.b) * a.H + w.h0 + t) * a.S + qpos] = m + __log2f(l);
+      trace_ev(tr, 1 + t, tcnt, kEvEpiEnd, t, n);
+      a.lse[(static_cast<long long>(w.b) * a.H + w.h0 + t) * a.S + qpos] = m + __log2f(l);
     }
   }
   tc_fence_before();
@@ -618,6 +641,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp == 1) {
     {  // the whole warp walks the MMA program; one elected lane issues
+      int tcnt = 0;  // trace records (trace builds)
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_Q = idesc_bf16_f32(128, HD, false, true);
       const uint64_t dQ = desc_k(sm + L::Q, 0, kBlk128), dDO = desc_k(sm + L::DO, 0, kBlk128);
@@ -871,6 +895,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp == 1) {
     {  // the whole warp walks the MMA program; one elected lane issues
+      int tcnt = 0;  // trace records (trace builds)
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_A = idesc_bf16_f32(128, HD, false, true);
       const uint64_t dK = desc_k(sm + L::K, 0, kBlk128), dV = desc_k(sm + L::V, 0, kBlk128);
@@ -1045,7 +1070,24 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
   const int N = B * S;
   const CUtensorMap mq = tmap(qkv, ld, N, ld, 128);
   FwdArgs a{B, H, KVH, S, ld, static_cast<bf16*>(o), H * HD, lse,
-            1.4426950408889634f / sqrtf(static_cast<float>(HD))};
+            1.4426950408889634f / sqrtf(static_cast<float>(HD)), nullptr};
+  // development timeline (trace builds only): CFT_ATTN_TRACE=<file> records CTA 0's events of
+  // the next launch
+#ifdef CFT_ATTN_TRACE
+  static const char* trace_path = std::getenv("CFT_ATTN_TRACE");
+#else
+  static const char* trace_path = nullptr;
+#endif
+  static unsigned long long* trace_buf = nullptr;
+  constexpr size_t kTraceWords = 2 * 3 * size_t(kTraceRecs);
+  static int trace_skip = trace_path && std::getenv("CFT_ATTN_TRACE_SKIP")
+                              ? std::atoi(std::getenv("CFT_ATTN_TRACE_SKIP")) : 0;
+  if (trace_path && trace_skip > 0) --trace_skip;
+  else if (trace_path && !trace_buf) {
+    CFT_CUDA(cudaMalloc(&trace_buf, kTraceWords * 8));
+    CFT_CUDA(cudaMemsetAsync(trace_buf, 0, kTraceWords * 8, st));
+    a.trace = trace_buf;
+  }
   static bool attr = false;
   if (!attr) {
     set_smem(attn_fwd_kernel<HD>, FwdSmem<HD>::BYTES);
@@ -1055,6 +1097,16 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
   attn_fwd_kernel<HD><<<std::min(items, num_sms()), kFwdThreads,
                         std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(mq, a, items);
   check_launch("attn_fwd_kernel");
+  if (a.trace) {  // write once, then stay off
+    std::vector<unsigned long long> h(kTraceWords);
+    CFT_CUDA(cudaMemcpyAsync(h.data(), trace_buf, kTraceWords * 8, cudaMemcpyDeviceToHost, st));
+    CFT_CUDA(cudaStreamSynchronize(st));
+    if (FILE* f = std::fopen(trace_path, "wb")) {
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+    trace_path = nullptr;
+  }
 }
 
 // dQ first (it also writes D), then dK / dV (reads D)
