@@ -172,8 +172,12 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
-// Spin wait (no suspend hint): the attention pipelines hand off every ~0.1-0.3 us between
-// the softmax warps and the MMA thread, so wake-up latency is on the critical path.
+// Wait with the hardware suspend hint: a waiting warp parks instead of polling, so the TMA /
+// MMA warps and the idle head's softmax warps leave the issue slots of their SM sub-partitions
+// to the warps doing the exponentials (a polling warp took about half of them).
+#ifndef CFT_ATTN_SPIN
+__device__ __forceinline__ void spin_wait(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
+#else
 __device__ __forceinline__ void spin_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_test(bar, parity)) return;
   const long long t0 = clock64();
@@ -181,6 +185,7 @@ __device__ __forceinline__ void spin_wait(uint64_t* bar, uint32_t parity) {
     if (clock64() - t0 > 20000000000LL) __trap();
   }
 }
+#endif
 
 struct FwdArgs {
   int B, H, KVH, S, ld;  // ld = qkv row pitch (elements)
