@@ -613,8 +613,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: dQ [0, HD), stage s: S [HD + 128 s, +64), dP [+64, +128); the compute threads write
-  // dS (bf16, 32 packed columns) over the stage's S and dQ += dS K runs with A from TMEM
+  // TMEM: dQ [0, HD), stage s: S [HD + 128 s, +64), dP [+64, +128); each compute thread writes
+  // its dS (bf16, 16 packed columns) over its own S columns and dQ += dS K runs with A from TMEM
   auto tst = [&](int s) { return tbase + HD + 128 * s; };
 
   if (warp == 0) {
@@ -685,8 +685,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)  // 16 key columns = 8 packed TMEM columns per step
-              umma_bf16_ts(tbase, tst(ts) + kk * 8, dk + ((kk * 2048) >> 4), ID_Q,
-                           (jj > 0 || kk > 0) ? 1u : 0u);
+              umma_bf16_ts(tbase, tst(ts) + 32 * (kk >> 1) + 8 * (kk & 1),
+                           dk + ((kk * 2048) >> 4), ID_Q, (jj > 0 || kk > 0) ? 1u : 0u);
             umma_commit(&kvempty[s]);
             if (jj + 1 == n) {
               umma_commit(done);
@@ -745,10 +745,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_ld32(lo + tst(ts) + hf * 32, vs);
         tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
         tmem_wait_ld();
-        // both halves of every row have read S before either overwrites it with dS
-        tc_fence_before();
-        named_bar_sync(1, 256);
-        tc_fence_after();
         if (jj * 64 + 63 > i * 128) {  // diagonal block: masked scores -> -inf -> P = 0
           const int lim = qi - jj * 64 - hf * 32;
 #pragma unroll
@@ -779,7 +775,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(dv[2 * e], dv[2 * e + 1]);
-        tmem_st16(lo + tst(ts) + hf * 16, pk);  // dS, key columns in K order
+        // dS over this half's own S columns (no other thread reads them): key columns
+        // 32 hf .. 32 hf + 31 as 16 packed columns at 32 hf
+        tmem_st16(lo + tst(ts) + hf * 32, pk);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -935,8 +933,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // 16 query columns = 8 packed TMEM columns per step
             const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
-            umma_bf16_ts(tbase, tst(ts) + k * 8, dd + ((k * 2048) >> 4), ID_A, acc);            // dV
-            umma_bf16_ts(tbase + HD, tst(ts) + 64 + k * 8, dq + ((k * 2048) >> 4), ID_A, acc);  // dK
+            const uint32_t ca = 32 * (k >> 1) + 8 * (k & 1);  // this step's packed columns
+            umma_bf16_ts(tbase, tst(ts) + ca, dd + ((k * 2048) >> 4), ID_A, acc);            // dV
+            umma_bf16_ts(tbase + HD, tst(ts) + 64 + ca, dq + ((k * 2048) >> 4), ID_A, acc);  // dK
           }
           umma_commit(&qempty[s]);
         }
@@ -967,10 +966,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_ld32(lo + tst(ts) + hf * 32, vs);
       tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
       tmem_wait_ld();
-      // both halves of every row have read their scores before either overwrites the stage
-      tc_fence_before();
-      named_bar_sync(1, 256);
-      tc_fence_after();
       if (qb * 64 < j * 128 + 128) {  // diagonal: query columns e < lim (q < kv) -> P = 0
         const int lim = kvi - qb * 64 - hf * 32;
 #pragma unroll
@@ -995,7 +990,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       uint32_t pk[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
-      tmem_st16(lo + tst(ts) + hf * 16, pk);  // P^T, query columns in K order
+      // P^T / dS^T over this half's own S^T / dP^T columns (no other thread reads them):
+      // query columns 32 hf .. 32 hf + 31 as 16 packed columns at 32 hf
+      tmem_st16(lo + tst(ts) + hf * 32, pk);
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {  // dS^T = P^T (dP^T - D)
         const float2 x = __fmul2_rn(make_float2(pv[e], pv[e + 1]),
@@ -1003,7 +1000,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                                make_float2(-sd[e], -sd[e + 1])));
         pk[e / 2] = pack_bf16(x.x, x.y);
       }
-      tmem_st16(lo + tst(ts) + 64 + hf * 16, pk);  // dS^T
+      tmem_st16(lo + tst(ts) + 64 + hf * 32, pk);  // dS^T
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
