@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -536,22 +537,24 @@ struct BwdArgs {
   float* D;              // [B][H][S] rowsum(dO * O): written by the dQ kernel, read by dK/dV
   bf16* dqkv;
   float scale_log2, scale;
+  unsigned long long* trace = nullptr;  // development timeline (see FwdArgs)
 };
 
 // ------------------------------------------------------------------------------------------
 // dQ (runs first; also forms D = rowsum(dO * O) of its rows): warp 0 TMA, warp 1 MMA,
-// warps 2-9 half a query row each.  Key / value blocks of 64 rows in a 4-deep ring; S and dP
-// double-buffered in TMEM, dS written back over S in TMEM; the O tile is staged per item in a
-// 32 KB smem area (for D only).
+// warps 2-9 half a query row each.  Key / value blocks of 64 rows in a 4-deep smem ring.
+// Q and dO of the item live in TMEM (bf16, copied there once per item by the row threads), so
+// S = Q K^T and dP = dO V^T take A from TMEM and read only the 64-row K / V block from shared
+// memory: with N = 64 an SS MMA would be shared-memory bound (6 KB of operands per 32 clocks).
+// S and dP in TMEM stages (S committed before dP), dS written back over S in TMEM; the Q, dO
+// and O tiles are staged per item in smem (read once by the row threads, for TMEM and D).
 template <int HD>
 struct QSmem {
   static constexpr int NS = 4;
   static constexpr uint32_t TILE = 128 * HD * 2;  // Q / dO / O tile (128 rows)
   static constexpr uint32_t KB = 64 * HD * 2;     // K or V block (64 rows)
-  static constexpr uint32_t SB = 128 * 64 * 2;    // dS block (128 q x 64 kv)
-  static constexpr uint32_t Q = 0, DO = TILE, K0 = 2 * TILE, V0 = K0 + NS * KB, DS0 = V0 + NS * KB,
-                            BAR = DS0 + 2 * SB;
-  static_assert(TILE <= 2 * SB, "the O tile is staged in the dS buffers");
+  static constexpr uint32_t Q = 0, DO = TILE, O = 2 * TILE, K0 = 3 * TILE, V0 = K0 + NS * KB,
+                            BAR = V0 + NS * KB;
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
@@ -564,21 +567,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                        const __grid_constant__ CUtensorMap tmdo,
                        const __grid_constant__ CUtensorMap tmo, const BwdArgs a, int n_items) {
   // persistent: a CTA walks items (query tile, batch, head) blockIdx.x, +gridDim.x, ... (longest
-  // tiles first); the next item's Q / dO / O load overlaps this item's dQ epilogue
+  // tiles first); the next item's Q / dO / O load overlaps this item's blocks, and its TMEM
+  // copy overlaps this item's dQ epilogue
   using L = QSmem<HD>;
   constexpr int NB = HD / 64, NS = L::NS;
+  constexpr int NT = (512 - 2 * HD) / 128;  // S / dP stages left in TMEM (2 for HD 128, 3 for 64)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* qfull = bar;
-  uint64_t* qempty = bar + 1;            // the item's MMAs are done with Q, dO and the dS area
-  uint64_t* kvfull = bar + 2;            // [NS]
+  uint64_t* qempty = bar + 1;            // the row threads have read the Q / dO / O tiles
+  uint64_t* qtfull = bar + 2;            // Q, dO of the item in TMEM
+  uint64_t* kvfull = bar + 3;            // [NS]
   uint64_t* kvempty = kvfull + NS;       // [NS] K / V block consumed
-  uint64_t* tfull = kvempty + NS;        // [2] S, dP in TMEM
-  uint64_t* pfull = tfull + 2;           // [2] dS written (into the stage's TMEM)
-  uint64_t* done = tfull + 4;            // the item's dQ complete
-  uint64_t* qout = tfull + 5;            // the item's dQ read out of TMEM
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 6);
+  uint64_t* tfull = kvempty + NS;        // [NT] S in TMEM
+  uint64_t* dpfull = tfull + NT;         // [NT] dP in TMEM
+  uint64_t* pfull = dpfull + NT;         // [NT] dS written (into the stage's TMEM)
+  uint64_t* done = pfull + NT;           // the item's MMAs complete
+  uint64_t* qout = done + 1;             // the item's dQ read out of TMEM
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(qout + 1);
 
   const int nq = a.S / 128, per_i = a.B * a.H, G = a.H / a.KVH;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -595,14 +602,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tma_prefetch(&tmdo);
     tma_prefetch(&tmo);
     mbar_init(qfull, 1);
-    mbar_init(qempty, 1);
+    mbar_init(qempty, 8);  // one arrival per row warp
+    mbar_init(qtfull, 8);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kvfull[s], 1);
       mbar_init(&kvempty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NT; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&pfull[s], 8);  // one arrival per gradient warp
+      mbar_init(&dpfull[s], 1);
+      mbar_init(&pfull[s], 8);
     }
     mbar_init(done, 1);
     mbar_init(qout, 8);
@@ -613,9 +622,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  // TMEM: dQ [0, HD), stage s: S [HD + 128 s, +64), dP [+64, +128); each compute thread writes
-  // its dS (bf16, 16 packed columns) over its own S columns and dQ += dS K runs with A from TMEM
-  auto tst = [&](int s) { return tbase + HD + 128 * s; };
+  // TMEM: dQ [0, HD) fp32; Q [HD, HD + HD/2) and dO [HD + HD/2, 2 HD) bf16 (row = lane, two
+  // per column, K order); stage s: S [2 HD + 128 s, +64), dP [+64, +128).  Each row thread
+  // writes its dS (16 packed columns) over its own S columns; dQ += dS K takes A from TMEM.
+  const uint32_t tQ = tbase + HD, tDO = tbase + HD + HD / 2;
+  auto tst = [&](int s) { return tbase + 2 * HD + 128 * s; };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -630,7 +641,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int kb = 0; kb < NB; ++kb) {
           tma_load_2d(sm + L::Q + kb * kBlk128, &tm128, qfull, h * HD + kb * 64, qrow);
           tma_load_2d(sm + L::DO + kb * kBlk128, &tmdo, qfull, h * HD + kb * 64, qrow);
-          tma_load_2d(sm + L::DS0 + kb * kBlk128, &tmo, qfull, h * HD + kb * 64, qrow);
+          tma_load_2d(sm + L::O + kb * kBlk128, &tmo, qfull, h * HD + kb * 64, qrow);
         }
         for (int jj = 0; jj < n; ++jj, ++g) {
           const int s = g % NS, u = g / NS;
@@ -649,22 +660,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       int tcnt = 0;  // trace records (trace builds)
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_Q = idesc_bf16_f32(128, HD, false, true);
-      const uint64_t dQ = desc_k(sm + L::Q, 0, kBlk128), dDO = desc_k(sm + L::DO, 0, kBlk128);
       auto issue_s = [&](int g) {
-        const int s = g % NS, u = g / NS, ts = g & 1;
+        const int s = g % NS, u = g / NS, ts = g % NT;
         spin_wait(&kvfull[s], u & 1);
+        if (lane == 0) trace_ev(a.trace, 0, tcnt, kEvSIssue, 0, g);
         tc_fence_after();
         const uint64_t dk = desc_k(sm + L::K0 + s * L::KB, 0, kBlk64);
         const uint64_t dv = desc_k(sm + L::V0 + s * L::KB, 0, kBlk64);
-        if (elect_one()) {
+        if (elect_one()) {  // S first: its exponentials overlap the dP MMAs
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint64_t oa = ((kk >> 2) * kBlk128 + (kk & 3) * 32) >> 4;
+          for (int kk = 0; kk < HD / 16; ++kk) {  // 16 head-dim columns = 8 TMEM columns of Q
             const uint64_t ob = ((kk >> 2) * kBlk64 + (kk & 3) * 32) >> 4;
-            umma_bf16(tst(ts), dQ + oa, dk + ob, ID_S, kk > 0);
-            umma_bf16(tst(ts) + 64, dDO + oa, dv + ob, ID_S, kk > 0);
+            umma_bf16_ts(tst(ts), tQ + kk * 8, dk + ob, ID_S, kk > 0 ? 1u : 0u);
           }
           umma_commit(&tfull[ts]);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint64_t ob = ((kk >> 2) * kBlk64 + (kk & 3) * 32) >> 4;
+            umma_bf16_ts(tst(ts) + 64, tDO + kk * 8, dv + ob, ID_S, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&dpfull[ts]);
         }
         __syncwarp();
       };
@@ -673,13 +688,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         int i, b, h;
         item_of(item, i, b, h);
         const int n = 2 * i + 2;  // >= 2
-        spin_wait(qfull, it & 1);
-        issue_s(g);
-        issue_s(g + 1);
+        spin_wait(qtfull, it & 1);  // this item's Q / dO in TMEM (the previous item's MMAs done)
+        for (int k = 0; k < NT && k < n; ++k) issue_s(g + k);
         for (int jj = 0; jj < n; ++jj, ++g) {
-          const int s = g % NS, ts = g & 1, v = g >> 1;
+          const int s = g % NS, ts = g % NT, v = g / NT;
           if (jj == 0 && it > 0) spin_wait(qout, (it - 1) & 1);  // previous dQ read out
           spin_wait(&pfull[ts], v & 1);
+          if (lane == 0) trace_ev(a.trace, 0, tcnt, kEvPvWait, 0, g);
           tc_fence_after();
           const uint64_t dk = desc_mn(sm + L::K0 + s * L::KB, 0, kBlk64);
           if (elect_one()) {
@@ -688,43 +703,37 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               umma_bf16_ts(tbase, tst(ts) + 32 * (kk >> 1) + 8 * (kk & 1),
                            dk + ((kk * 2048) >> 4), ID_Q, (jj > 0 || kk > 0) ? 1u : 0u);
             umma_commit(&kvempty[s]);
-            if (jj + 1 == n) {
-              umma_commit(done);
-              umma_commit(qempty);
-            }
+            if (jj + 1 == n) umma_commit(done);
           }
           __syncwarp();
-          if (jj + 2 < n) issue_s(g + 2);
+          if (jj + NT < n) issue_s(g + NT);
         }
       }
     }
   } else {
     // 8 warps, two per TMEM lane quarter: a thread owns half a row (32 of the block's 64 key
-    // columns of S / dP, half of dQ's columns)
+    // columns of S / dP, half of dQ's, Q's and dO's columns)
     const int quarter = warp & 3, hf = (warp - 2) / 4;
     const int r = quarter * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quarter * 32) << 16;
     const float c = a.scale_log2;
     const float2 c2 = make_float2(c, c);
-    int g = 0, it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      int i, b, h;
-      item_of(item, i, b, h);
-      const int n = 2 * i + 2, qrow = b * a.S + i * 128;
-      const int qi = i * 128 + r;
-      const long long st = (static_cast<long long>(b) * a.H + h) * a.S + qi;
-      const float lse = a.lse[st];
-      // D of this row from the staged dO and O tiles (both halves form it; the dS writes below
-      // reuse the O staging bytes, so the row's two threads sync before the first one)
+    unsigned long long* const tr = warp == 2 && lane == 0 ? a.trace : nullptr;
+    int tcnt = 0;
+    // item prologue: D of the row from the staged dO and O (both halves form the whole row's
+    // sum), and this half's Q / dO columns into TMEM
+    auto prologue = [&](int it, int b, int h, int i, float& dd, float& lse) {
+      const long long st = (static_cast<long long>(b) * a.H + h) * a.S + i * 128 + r;
+      lse = a.lse[st];
       spin_wait(qfull, it & 1);
-      float dd = 0.f;
+      dd = 0.f;
 #pragma unroll
       for (int kb = 0; kb < NB; ++kb) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint32_t off = kb * kBlk128 + r * 128 + ((q ^ (r & 7)) << 4);
           const uint4 x = *reinterpret_cast<const uint4*>(sm + L::DO + off);
-          const uint4 y = *reinterpret_cast<const uint4*>(sm + L::DS0 + off);
+          const uint4 y = *reinterpret_cast<const uint4*>(sm + L::O + off);
           const __nv_bfloat162* xa = reinterpret_cast<const __nv_bfloat162*>(&x);
           const __nv_bfloat162* ya = reinterpret_cast<const __nv_bfloat162*>(&y);
 #pragma unroll
@@ -735,16 +744,55 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
       if (hf == 0) a.D[st] = dd;
-      named_bar_sync(1, 256);
+      // this half's HD/2 columns of Q and dO: 16-byte chunks [hf * HD/16, +HD/16) of the row
+      constexpr int CH = HD / 16;  // 16-byte chunks per half row
+      uint32_t wq[4 * CH], wd[4 * CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int cq = hf * CH + q;  // chunk index over the whole row (8 per 64-column block)
+        const uint32_t off = (cq >> 3) * kBlk128 + r * 128 + (((cq & 7) ^ (r & 7)) << 4);
+        const uint4 x = *reinterpret_cast<const uint4*>(sm + L::Q + off);
+        const uint4 y = *reinterpret_cast<const uint4*>(sm + L::DO + off);
+        wq[4 * q] = x.x; wq[4 * q + 1] = x.y; wq[4 * q + 2] = x.z; wq[4 * q + 3] = x.w;
+        wd[4 * q] = y.x; wd[4 * q + 1] = y.y; wd[4 * q + 2] = y.z; wd[4 * q + 3] = y.w;
+      }
+      if constexpr (HD == 128) {
+        tmem_st32(lo + tQ + hf * 32, *reinterpret_cast<const uint32_t(*)[32]>(wq));
+        tmem_st32(lo + tDO + hf * 32, *reinterpret_cast<const uint32_t(*)[32]>(wd));
+      } else {
+        tmem_st16(lo + tQ + hf * 16, *reinterpret_cast<const uint32_t(*)[16]>(wq));
+        tmem_st16(lo + tDO + hf * 16, *reinterpret_cast<const uint32_t(*)[16]>(wd));
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(qempty);  // the staged tiles are free for the next item's loads
+        mbar_arrive(qtfull);
+      }
+    };
+    int g = 0, it = 0;
+    float dd = 0.f, lse = 0.f;
+    if (static_cast<int>(blockIdx.x) < n_items) {
+      int i, b, h;
+      item_of(blockIdx.x, i, b, h);
+      prologue(0, b, h, i, dd, lse);
+    }
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      int i, b, h;
+      item_of(item, i, b, h);
+      const int n = 2 * i + 2, qrow = b * a.S + i * 128;
+      const int qi = i * 128 + r;
       const float2 nl2 = make_float2(-lse, -lse), nd2 = make_float2(-dd, -dd);
       for (int jj = 0; jj < n; ++jj, ++g) {
-        const int ts = g & 1, v = g >> 1;
+        const int ts = g % NT, v = g / NT;
         spin_wait(&tfull[ts], v & 1);
+        trace_ev(tr, 1, tcnt, kEvSfull, 0, g);
         tc_fence_after();
         uint32_t vs[32], vp[32];
         tmem_ld32(lo + tst(ts) + hf * 32, vs);
-        tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
         tmem_wait_ld();
+        trace_ev(tr, 1, tcnt, kEvLdDone, 0, g);
         if (jj * 64 + 63 > i * 128) {  // diagonal block: masked scores -> -inf -> P = 0
           const int lim = qi - jj * 64 - hf * 32;
 #pragma unroll
@@ -765,6 +813,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dv[e + 2] = ex2_mix<2>(dv[e + 2]);
           dv[e + 3] = ex2_mix<3>(dv[e + 3]);
         }
+        trace_ev(tr, 1, tcnt, kEvExpDone, 0, g);
+        spin_wait(&dpfull[ts], v & 1);
+        trace_ev(tr, 1, tcnt, kEvBarDone, 0, g);
+        tc_fence_after();
+        tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
+        tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {  // dS = P (dP - D)
           const float2 x = __fmul2_rn(make_float2(dv[e], dv[e + 1]),
@@ -782,9 +836,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[ts]);
+        trace_ev(tr, 1, tcnt, kEvPfull, 0, g);
       }
-      spin_wait(done, it & 1);
+      spin_wait(done, it & 1);  // every MMA of the item: Q / dO in TMEM and dQ final
+      trace_ev(tr, 1, tcnt, kEvEpiStart, 0, it);
       tc_fence_after();
+      {  // the next item's TMEM copy first, so its S / dP MMAs overlap this dQ read-out
+        const int nxt = item + gridDim.x;
+        if (nxt < n_items) {
+          int i2, b2, h2;
+          item_of(nxt, i2, b2, h2);
+          prologue(it + 1, b2, h2, i2, dd, lse);
+        }
+      }
       bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD + hf * (HD / 2);
 #pragma unroll
       for (int cc = 0; cc < HD / 64; ++cc) {
@@ -831,10 +895,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* kvfull = bar;
   uint64_t* qfull = bar + 1;             // [NS] Q, dO, lse, D of a query block
   uint64_t* qempty = bar + 1 + NS;       // [NS] consumed by the dV / dK MMAs
-  uint64_t* tfull = bar + 1 + 2 * NS;    // [2] S^T, dP^T in TMEM
-  uint64_t* pfull = tfull + 2;           // [2] P^T, dS^T written (into the stage's TMEM)
-  uint64_t* done = tfull + 4;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 5);
+  uint64_t* tfull = bar + 1 + 2 * NS;    // [2] S^T in TMEM
+  uint64_t* dpfull = tfull + 2;          // [2] dP^T in TMEM
+  uint64_t* pfull = tfull + 4;           // [2] P^T written (over the stage's S^T)
+  uint64_t* dsfull = tfull + 6;          // [2] dS^T written (over the stage's dP^T)
+  uint64_t* done = tfull + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 9);
 
   const int G = a.H / a.KVH;
   const int per_j = a.B * a.KVH;
@@ -858,7 +924,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
+      mbar_init(&dpfull[s], 1);
       mbar_init(&pfull[s], 8);  // one arrival per gradient warp
+      mbar_init(&dsfull[s], 8);
     }
     mbar_init(done, 1);
     fence_barrier_init();
@@ -908,15 +976,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_after();
         const uint64_t dq = desc_k(sm + L::Q0 + s * L::QB, 0, kBlk64);
         const uint64_t dd = desc_k(sm + L::DO0 + s * L::QB, 0, kBlk64);
-        if (elect_one()) {
+        if (elect_one()) {  // S^T first (its exponentials overlap the dP^T MMAs)
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k) {
             const uint64_t oa = ((k >> 2) * kBlk128 + (k & 3) * 32) >> 4;
             const uint64_t ob = ((k >> 2) * kBlk64 + (k & 3) * 32) >> 4;
             umma_bf16(tst(ts), dK + oa, dq + ob, ID_S, k > 0);
-            umma_bf16(tst(ts) + 64, dV + oa, dd + ob, ID_S, k > 0);
           }
           umma_commit(&tfull[ts]);
+#pragma unroll
+          for (int k = 0; k < HD / 16; ++k) {
+            const uint64_t oa = ((k >> 2) * kBlk128 + (k & 3) * 32) >> 4;
+            const uint64_t ob = ((k >> 2) * kBlk64 + (k & 3) * 32) >> 4;
+            umma_bf16(tst(ts) + 64, dV + oa, dd + ob, ID_S, k > 0);
+          }
+          umma_commit(&dpfull[ts]);
         }
         __syncwarp();
       };
@@ -925,17 +999,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (n_it > 1) issue_s(1);
       for (int it = 0; it < n_it; ++it) {
         const int s = it % NS, ts = it & 1, v = it >> 1;
-        spin_wait(&pfull[ts], v & 1);
-        tc_fence_after();
         const uint64_t dq = desc_mn(sm + L::Q0 + s * L::QB, 0, kBlk64);
         const uint64_t dd = desc_mn(sm + L::DO0 + s * L::QB, 0, kBlk64);
+        const uint32_t acc0 = it > 0 ? 1u : 0u;
+        spin_wait(&pfull[ts], v & 1);  // dV += P^T dO while the threads form dS^T
+        tc_fence_after();
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // 16 query columns = 8 packed TMEM columns per step
-            const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
             const uint32_t ca = 32 * (k >> 1) + 8 * (k & 1);  // this step's packed columns
-            umma_bf16_ts(tbase, tst(ts) + ca, dd + ((k * 2048) >> 4), ID_A, acc);            // dV
-            umma_bf16_ts(tbase + HD, tst(ts) + 64 + ca, dq + ((k * 2048) >> 4), ID_A, acc);  // dK
+            umma_bf16_ts(tbase, tst(ts) + ca, dd + ((k * 2048) >> 4), ID_A, acc0 | (k > 0));
+          }
+        }
+        __syncwarp();
+        spin_wait(&dsfull[ts], v & 1);  // dK += dS^T Q
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t ca = 32 * (k >> 1) + 8 * (k & 1);
+            umma_bf16_ts(tbase + HD, tst(ts) + 64 + ca, dq + ((k * 2048) >> 4), ID_A,
+                         acc0 | (k > 0));
           }
           umma_commit(&qempty[s]);
         }
@@ -964,7 +1048,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const float* sd = reinterpret_cast<const float*>(sm + L::D0 + s * 256) + hf * 32;
       uint32_t vs[32], vp[32];
       tmem_ld32(lo + tst(ts) + hf * 32, vs);
-      tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
       tmem_wait_ld();
       if (qb * 64 < j * 128 + 128) {  // diagonal: query columns e < lim (q < kv) -> P = 0
         const int lim = kvi - qb * 64 - hf * 32;
@@ -993,6 +1076,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // P^T / dS^T over this half's own S^T / dP^T columns (no other thread reads them):
       // query columns 32 hf .. 32 hf + 31 as 16 packed columns at 32 hf
       tmem_st16(lo + tst(ts) + hf * 32, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[ts]);
+      spin_wait(&dpfull[ts], v & 1);
+      tc_fence_after();
+      tmem_ld32(lo + tst(ts) + 64 + hf * 32, vp);
+      tmem_wait_ld();
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {  // dS^T = P^T (dP^T - D)
         const float2 x = __fmul2_rn(make_float2(pv[e], pv[e + 1]),
@@ -1004,7 +1095,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-        if (lane == 0) mbar_arrive(&pfull[ts]);
+      if (lane == 0) mbar_arrive(&dsfull[ts]);
     }
     spin_wait(done, 0);
     tc_fence_after();
@@ -1065,6 +1156,42 @@ void check_shape(int hq, int hkv, int seq, int hd) {
 }
 
 namespace {
+// Development timeline (trace builds only): CFT_ATTN_TRACE=<file> records CTA 0's events of one
+// launch of the kernel CFT_ATTN_TRACE_KERNEL (fwd | dq | dkdv; default fwd) after skipping
+// CFT_ATTN_TRACE_SKIP launches of it.
+unsigned long long* trace_arm(const char* kernel, cudaStream_t st) {
+#ifdef CFT_ATTN_TRACE
+  static const char* path = std::getenv("CFT_ATTN_TRACE");
+  static const char* which = std::getenv("CFT_ATTN_TRACE_KERNEL");
+  static int skip = std::getenv("CFT_ATTN_TRACE_SKIP") ? std::atoi(std::getenv("CFT_ATTN_TRACE_SKIP")) : 0;
+  static bool used = false;
+  if (!path || used || std::strcmp(kernel, which ? which : "fwd") != 0) return nullptr;
+  if (skip > 0) {
+    --skip;
+    return nullptr;
+  }
+  used = true;
+  unsigned long long* buf = nullptr;
+  CFT_CUDA(cudaMalloc(&buf, 2 * 3 * size_t(kTraceRecs) * 8));
+  CFT_CUDA(cudaMemsetAsync(buf, 0, 2 * 3 * size_t(kTraceRecs) * 8, st));
+  return buf;
+#else
+  (void)kernel;
+  (void)st;
+  return nullptr;
+#endif
+}
+void trace_dump(unsigned long long* buf, cudaStream_t st) {
+  if (!buf) return;
+  std::vector<unsigned long long> h(2 * 3 * size_t(kTraceRecs));
+  CFT_CUDA(cudaMemcpyAsync(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost, st));
+  CFT_CUDA(cudaStreamSynchronize(st));
+  if (FILE* f = std::fopen(std::getenv("CFT_ATTN_TRACE"), "wb")) {
+    std::fwrite(h.data(), 8, h.size(), f);
+    std::fclose(f);
+  }
+}
+
 template <int HD>
 void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* lse,
                 cudaStream_t st) {
@@ -1073,23 +1200,7 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
   const CUtensorMap mq = tmap(qkv, ld, N, ld, 128);
   FwdArgs a{B, H, KVH, S, ld, static_cast<bf16*>(o), H * HD, lse,
             1.4426950408889634f / sqrtf(static_cast<float>(HD)), nullptr};
-  // development timeline (trace builds only): CFT_ATTN_TRACE=<file> records CTA 0's events of
-  // the next launch
-#ifdef CFT_ATTN_TRACE
-  static const char* trace_path = std::getenv("CFT_ATTN_TRACE");
-#else
-  static const char* trace_path = nullptr;
-#endif
-  static unsigned long long* trace_buf = nullptr;
-  constexpr size_t kTraceWords = 2 * 3 * size_t(kTraceRecs);
-  static int trace_skip = trace_path && std::getenv("CFT_ATTN_TRACE_SKIP")
-                              ? std::atoi(std::getenv("CFT_ATTN_TRACE_SKIP")) : 0;
-  if (trace_path && trace_skip > 0) --trace_skip;
-  else if (trace_path && !trace_buf) {
-    CFT_CUDA(cudaMalloc(&trace_buf, kTraceWords * 8));
-    CFT_CUDA(cudaMemsetAsync(trace_buf, 0, kTraceWords * 8, st));
-    a.trace = trace_buf;
-  }
+  a.trace = trace_arm("fwd", st);
   static bool attr = false;
   if (!attr) {
     set_smem(attn_fwd_kernel<HD>, FwdSmem<HD>::BYTES);
@@ -1099,16 +1210,7 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
   attn_fwd_kernel<HD><<<std::min(items, num_sms()), kFwdThreads,
                         std::max(FwdSmem<HD>::BYTES, kMinSmem), st>>>(mq, a, items);
   check_launch("attn_fwd_kernel");
-  if (a.trace) {  // write once, then stay off
-    std::vector<unsigned long long> h(kTraceWords);
-    CFT_CUDA(cudaMemcpyAsync(h.data(), trace_buf, kTraceWords * 8, cudaMemcpyDeviceToHost, st));
-    CFT_CUDA(cudaStreamSynchronize(st));
-    if (FILE* f = std::fopen(trace_path, "wb")) {
-      std::fwrite(h.data(), 8, h.size(), f);
-      std::fclose(f);
-    }
-    trace_path = nullptr;
-  }
+  trace_dump(a.trace, st);
 }
 
 // dQ first (it also writes D), then dK / dV (reads D)
@@ -1131,16 +1233,20 @@ void bwd_launch(int B, int H, int KVH, int S, const void* qkv, const void* o, co
     const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 128);
     const CUtensorMap mo = tmap(o, ldo, N, ldo, 128);
     const int items = (S / 128) * B * H;
+    a.trace = trace_arm("dq", st);
     attn_bwd_dq_kernel<HD><<<std::min(items, num_sms()), kBwdThreads,
                              std::max(QSmem<HD>::BYTES, kMinSmem), st>>>(m128, m64, mdo, mo, a,
                                                                          items);
     check_launch("attn_bwd_dq_kernel");
+    trace_dump(a.trace, st);
   }
   {
     const CUtensorMap mdo = tmap(dout, ldo, N, ldo, 64);
+    a.trace = trace_arm("dkdv", st);
     attn_bwd_dkdv_kernel<HD><<<(S / 128) * B * KVH, kBwdThreads, std::max(KvSmem<HD>::BYTES, kMinSmem),
                                st>>>(m128, m64, mdo, a);
     check_launch("attn_bwd_dkdv_kernel");
+    trace_dump(a.trace, st);
   }
 }
 
