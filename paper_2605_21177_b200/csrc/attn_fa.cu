@@ -88,10 +88,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
-// generic-proxy smem writes (P, dS) -> visible to the tensor pipe's async proxy
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -112,21 +108,6 @@ __device__ __forceinline__ uint64_t desc_k(const void* base, int k, uint32_t blk
 // the MN dimension's 64-column blocks are `blk` bytes apart (leading-byte offset).
 __device__ __forceinline__ uint64_t desc_mn(const void* base, int k, uint32_t blk) {
   return smem_desc_sw128(smem_u32(base) + k * 2048, blk, 1024);
-}
-// 16-byte chunk c (0..7) of row r in a [rows][128 B] SW128 block (TMA's 128B swizzle)
-__device__ __forceinline__ void st_swz(uint8_t* blk, int r, int c, const uint32_t* w) {
-  *reinterpret_cast<uint4*>(blk + r * 128 + ((c ^ (r & 7)) << 4)) =
-      make_uint4(w[0], w[1], w[2], w[3]);
-}
-// 32 fp32 values -> 32 bf16 in four swizzled chunks starting at chunk c0 of row r
-__device__ __forceinline__ void st_swz32(uint8_t* blk, int r, int c0, const float* v) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t w[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) w[t] = pack_bf16(v[q * 8 + 2 * t], v[q * 8 + 2 * t + 1]);
-    st_swz(blk, r, c0 + q, w);
-  }
 }
 // 32 fp32 (scaled) -> 32 bf16 to global (two 32-byte stores)
 __device__ __forceinline__ void st_row32(bf16* p, const uint32_t (&r)[32], float s) {
@@ -966,7 +947,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp == 1) {
     {  // the whole warp walks the MMA program; one elected lane issues
-      int tcnt = 0;  // trace records (trace builds)
       constexpr uint32_t ID_S = idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t ID_A = idesc_bf16_f32(128, HD, false, true);
       const uint64_t dK = desc_k(sm + L::K, 0, kBlk128), dV = desc_k(sm + L::V, 0, kBlk128);
