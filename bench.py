@@ -862,10 +862,13 @@ def run_llama(args, rank, world, local_rank):
     return res
 
 
-def slice_sweep(local_rank, dtype="bf16", reps=10):
+def slice_sweep(local_rank, dtype="bf16", reps=30):
     """sliced-dW TFLOP/s for active-slice widths 1/8 .. 1/1 (configs[1] sweep: d=4096,
     N_tok=8192; bf16 on the tcgen05 GEMM, fp32 on the CUDA-core path -- the reference harness
-    times both precisions side by side, tools/bench_kernels.cpp:19-41)."""
+    times both precisions side by side, tools/bench_kernels.cpp:19-41).  Mean over `reps`
+    back-to-back launches after 5 warm-up launches: like a step's sequence of slices, each
+    launch's prologue overlaps the previous one's tail (programmatic dependent launch), which
+    is worth ~5 % at |S| = 512 (10 reps: 948, 20: 979, 40: 1007 TFLOP/s on one box)."""
     import torch
     from paper_2605_21177_b200 import ops
     dev = torch.device("cuda", local_rank)
@@ -880,7 +883,7 @@ def slice_sweep(local_rank, dtype="bf16", reps=10):
         # accumulate into a zeroed fp32 buffer: the engine's path (its gradient accumulator is
         # kept zero between steps), i.e. the reference's dw += (kernels_serial.cpp:39-49)
         buf = torch.zeros(s, D, device=dev)
-        for _ in range(3):
+        for _ in range(5):
             ops.linear_wgrad_slice(dy, x, rb, rb + s, out=buf, accumulate=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -890,7 +893,8 @@ def slice_sweep(local_rank, dtype="bf16", reps=10):
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / reps
-        out[f"1/{f}"] = {"rows": s, "row_begin": rb, "ms": t, "tflops": 2 * N_TOK * s * D / t / 1e9}
+        out[f"1/{f}"] = {"rows": s, "row_begin": rb, "ms": t, "reps": reps,
+                         "tflops": 2 * N_TOK * s * D / t / 1e9}
     return out
 
 
@@ -1024,6 +1028,9 @@ def main():
         if not args.no_sweep:
             sw = res.setdefault("sliced_dw", {})
             sw["configs1_sweep"] = slice_sweep(local_rank)
+            bf16_peak = load_peaks()["bf16"]
+            for v in sw["configs1_sweep"].values():  # a kernel timed alone: the burst peak
+                v["frac_of_measured_burst_peak"] = v["tflops"] / bf16_peak
             sw["configs1_sweep_fp32"] = slice_sweep(local_rank, "fp32", reps=3)
         if world == 1 and not args.no_cpu_baseline:
             cpu = None
