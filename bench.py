@@ -964,10 +964,9 @@ def main():
     ap.add_argument("--state", choices=["auto", "host", "hbm"], default="auto",
                     help="optimizer-state residency for llama8b (auto: pinned host when RAM allows)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--fusion", type=int, default=15,
+    ap.add_argument("--fusion", type=int, default=7,
                     help="A/B: epilogue fusion mask (1 SwiGLU, 2 RoPE, 4 CE first pass in the "
-                         "lm_head epilogue, 8 RoPE inverse in the attention backward; 0 = "
-                         "separate kernels)")
+                         "lm_head epilogue; 0 = separate kernels)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[1] sliced-dW sweep")
     ap.add_argument("--exchange", choices=["auto", "collectives", "p2p"], default="auto",
                     help="N>1 sharded state: the exchange over peer memory (P2P pull "
@@ -1018,7 +1017,7 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if args.fusion != 15:
+    if args.fusion != 7:
         from paper_2605_21177_b200 import ops
         ops.set_fusion(args.fusion)
     if args.workload in ("llama8b", "llama70b"):

@@ -244,13 +244,6 @@ int cft_attention_fwd(const void* qkv, int batch, int hq, int hkv, int seq, int 
 int cft_attention_bwd(const void* qkv, const void* o, const void* dout, const float* lse,
                       int batch, int hq, int hkv, int seq, int head_dim, void* dqkv,
                       float* scratch, cft_stream_t stream);
-/* The same backward with RoPE (rotate-half, base rope_theta, position = row % seq) folded in:
- * dQ and dK come out rotated back through the inverse rotation, i.e. the gradient w.r.t. the
- * pre-RoPE q / k -- what cft_attention_bwd followed by the inverse rotation gives, rounded to
- * bf16 once instead of twice. */
-int cft_attention_bwd_rope(const void* qkv, const void* o, const void* dout, const float* lse,
-                           int batch, int hq, int hkv, int seq, int head_dim, double rope_theta,
-                           void* dqkv, float* scratch, cft_stream_t stream);
 
 /* Hyper-parameters (AdamWHyper, optimizer.hpp:15-22). */
 typedef struct {
@@ -309,10 +302,8 @@ int cft_sgd_slice(cft_dtype state_dtype, void* master, const void* grad, int64_t
 int cft_set_gemm_policy(int policy);
 /* Epilogue fusions of the Llama engine, a bit mask: 1 = SwiGLU in the w1|w3 forward and w2
  * dgrad GEMMs, 2 = RoPE in the QKV forward GEMM, 4 = the softmax CE's (max, sum-exp) pass in
- * the lm_head forward GEMM, 8 = RoPE's inverse rotation of dQ / dK in the attention backward
- * epilogues; default 15, 0 = separate kernels.  1 and 2 are bit-identical to the separate
- * kernels; 4 sums exp() in a different order (loss / dlogits to fp32 rounding); 8 rounds dQ / dK
- * to bf16 once instead of twice. */
+ * the lm_head forward GEMM; default 7, 0 = separate kernels.  1 and 2 are bit-identical to the
+ * separate kernels; 4 sums exp() in a different order (loss / dlogits to fp32 rounding). */
 int cft_set_fusion(int enable);
 /* Kernel variant per operator, for A/B measurements (default from CFT_ADAMW_KERNEL /
  * CFT_GEMM_PDL).  op 0 fp32 AdamW: 0 register kernel, 1 TMA-staged with 31 consumer warps

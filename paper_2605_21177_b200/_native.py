@@ -90,8 +90,6 @@ _sig("cft_softmax_ce", C.c_int, C.c_int, vp, vp, i64, i64, vp, vp, vp, vp)
 _sig("cft_attention_fwd", C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp)
 _sig("cft_attention_bwd", C.c_int, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
      vp, vp, vp)
-_sig("cft_attention_bwd_rope", C.c_int, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-     f64, vp, vp, vp)
 _sig("cft_adamw_slice", C.c_int, C.c_int, vp, vp, vp, vp, i64, f64, P(AdamWHyperC), f64, f64,
      C.c_int, vp, vp, i32, vp, vp, C.c_int, f64, vp)
 _sig("cft_set_gemm_policy", C.c_int, C.c_int)

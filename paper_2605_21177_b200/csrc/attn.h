@@ -23,12 +23,9 @@ class Context {
   // stats: [batch][hq][seq] fp32 (row log2-sum-exp of the scaled scores, for the backward).
   void forward(int batch, int hq, int hkv, int seq, int head_dim, const void* qkv, void* o,
                float* stats, cudaStream_t stream);
-  // dqkv gets dQ | dK | dV in the same fused layout.  rope_cs (cos, sin per position and pair;
-  // llama::rope_cos_sin) non-null: dQ and dK come out rotated back through RoPE's inverse, the
-  // gradient of the pre-rotation q / k (the separate rope backward pass folded in).
+  // dqkv gets dQ | dK | dV in the same fused layout.
   void backward(int batch, int hq, int hkv, int seq, int head_dim, const void* qkv, const void* o,
-                const void* dout, const float* stats, void* dqkv, cudaStream_t stream,
-                const float2* rope_cs = nullptr);
+                const void* dout, const float* stats, void* dqkv, cudaStream_t stream);
 
   struct Impl;
 

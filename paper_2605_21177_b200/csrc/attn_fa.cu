@@ -39,7 +39,6 @@
 
 #include "attn.h"
 #include "cft_common.h"
-#include "kernels.h"
 #include "tc_ptx.cuh"
 
 namespace cft::attn {
@@ -520,47 +519,7 @@ struct BwdArgs {
   bf16* dqkv;
   float scale_log2, scale;
   unsigned long long* trace = nullptr;  // development timeline (see FwdArgs)
-  // RoPE (rotate-half) cos / sin per (position, pair) or null: dQ and dK leave the kernels
-  // rotated back to the pre-RoPE q / k (the inverse rotation fused into their epilogues)
-  const float2* rope = nullptr;
 };
-
-// One row's dQ or dK with the inverse RoPE rotation: pairs i in [i0, i0 + W) of a head_dim HD
-// row, x1 = acc[i], x2 = acc[i + HD/2] (TMEM columns `t1`, `t2`), out = (x1 c + x2 s,
-// x2 c - x1 s) * scale, rounded once to bf16 and stored at row[i0..] and row[HD/2 + i0..].
-template <int W>
-__device__ __forceinline__ void rope_bwd_store(uint32_t t1, uint32_t t2, const float2* cs,
-                                               bf16* row, int i0, int half, float scale) {
-  static_assert(W == 16 || W == 32, "rope_bwd_store: 16 or 32 pairs");
-  uint32_t x1[32], x2[32];
-  if constexpr (W == 32) {
-    tmem_ld32(t1, x1);
-    tmem_ld32(t2, x2);
-  } else {
-    tmem_ld16(t1, *reinterpret_cast<uint32_t(*)[16]>(x1));
-    tmem_ld16(t2, *reinterpret_cast<uint32_t(*)[16]>(x2));
-  }
-  tmem_wait_ld();
-  uint32_t y1[W], y2[W];
-#pragma unroll
-  for (int e = 0; e < W; e += 2) {
-    float a1[2], a2[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const float2 c = cs[i0 + e + q];
-      const float u = f32(x1[e + q]) * scale, w = f32(x2[e + q]) * scale;
-      a1[q] = u * c.x + w * c.y;
-      a2[q] = w * c.x - u * c.y;
-    }
-    y1[e / 2] = pack_bf16(a1[0], a1[1]);
-    y2[e / 2] = pack_bf16(a2[0], a2[1]);
-  }
-#pragma unroll
-  for (int q = 0; q < W / 16; ++q) {
-    st_global_256(row + i0 + 16 * q, *reinterpret_cast<const uint32_t(*)[8]>(y1 + 8 * q));
-    st_global_256(row + half + i0 + 16 * q, *reinterpret_cast<const uint32_t(*)[8]>(y2 + 8 * q));
-  }
-}
 
 // ------------------------------------------------------------------------------------------
 // dQ (runs first; also forms D = rowsum(dO * O) of its rows): warp 0 TMA, warp 1 MMA,
@@ -871,20 +830,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           prologue(it + 1, b2, h2, i2, dd, lse);
         }
       }
-      if (a.rope) {  // this half's HD/4 rotation pairs: columns [hf HD/4, +HD/4) and +HD/2
-        bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD;
-        rope_bwd_store<HD / 4>(tbase + lo + hf * (HD / 4), tbase + lo + HD / 2 + hf * (HD / 4),
-                               a.rope + static_cast<long long>(i * 128 + r) * (HD / 2), drow,
-                               hf * (HD / 4), HD / 2, a.scale);
-      } else {
-        bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD + hf * (HD / 2);
+      bf16* drow = a.dqkv + static_cast<long long>(qrow + r) * a.ld + h * HD + hf * (HD / 2);
 #pragma unroll
-        for (int cc = 0; cc < HD / 64; ++cc) {
-          uint32_t o[32];
-          tmem_ld32(tbase + lo + hf * (HD / 2) + cc * 32, o);
-          tmem_wait_ld();
-          st_row32(drow + cc * 32, o, a.scale);
-        }
+      for (int cc = 0; cc < HD / 64; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(tbase + lo + hf * (HD / 2) + cc * 32, o);
+        tmem_wait_ld();
+        st_row32(drow + cc * 32, o, a.scale);
       }
       tc_fence_before();
       __syncwarp();
@@ -1134,17 +1086,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_ld32(tbase + lo + hf * (HD / 2) + cc * 32, o);
       tmem_wait_ld();
       st_row32(drow + vcol + cc * 32, o, 1.f);  // dV
-      if (!a.rope) {
-        tmem_ld32(tbase + lo + HD + hf * (HD / 2) + cc * 32, o);
-        tmem_wait_ld();
-        st_row32(drow + kcol + cc * 32, o, a.scale);  // dK
-      }
+      tmem_ld32(tbase + lo + HD + hf * (HD / 2) + cc * 32, o);
+      tmem_wait_ld();
+      st_row32(drow + kcol + cc * 32, o, a.scale);  // dK
     }
-    if (a.rope)  // dK rotated back: this half's HD/4 pairs, as in the dQ kernel
-      rope_bwd_store<HD / 4>(tbase + lo + HD + hf * (HD / 4), tbase + lo + HD + HD / 2 + hf * (HD / 4),
-                             a.rope + static_cast<long long>(j * 128 + r) * (HD / 2),
-                             a.dqkv + static_cast<long long>(kvrow + r) * a.ld + kcol,
-                             hf * (HD / 4), HD / 2, a.scale);
   }
   tc_fence_before();
   __syncthreads();
@@ -1251,15 +1196,13 @@ void fwd_launch(int B, int H, int KVH, int S, const void* qkv, void* o, float* l
 // dQ first (it also writes D), then dK / dV (reads D)
 template <int HD>
 void bwd_launch(int B, int H, int KVH, int S, const void* qkv, const void* o, const void* dout,
-                const float* lse, float* D, void* dqkv, cudaStream_t st,
-                const float2* rope = nullptr) {
+                const float* lse, float* D, void* dqkv, cudaStream_t st) {
   const int ld = (H + 2 * KVH) * HD, ldo = H * HD;
   const int N = B * S;
   const CUtensorMap m128 = tmap(qkv, ld, N, ld, 128);
   const CUtensorMap m64 = tmap(qkv, ld, N, ld, 64);
   const float sc = 1.f / sqrtf(static_cast<float>(HD));
   BwdArgs a{B, H, KVH, S, ld, ldo, lse, D, static_cast<bf16*>(dqkv), 1.4426950408889634f * sc, sc};
-  a.rope = rope;
   static bool attr = false;
   if (!attr) {
     set_smem(attn_bwd_dkdv_kernel<HD>, KvSmem<HD>::BYTES);
@@ -1318,14 +1261,14 @@ void Context::forward(int batch, int hq, int hkv, int seq, int head_dim, const v
 
 void Context::backward(int batch, int hq, int hkv, int seq, int head_dim, const void* qkv,
                        const void* o, const void* dout, const float* stats, void* dqkv,
-                       cudaStream_t stream, const float2* rope_cs) {
+                       cudaStream_t stream) {
   check_shape(hq, hkv, seq, head_dim);
   CFT_CHECK(impl_->D && impl_->d_elems >= static_cast<size_t>(batch) * hq * seq,
             "attention: prepare() before backward");
   if (head_dim == 128)
-    bwd_launch<128>(batch, hq, hkv, seq, qkv, o, dout, stats, impl_->D, dqkv, stream, rope_cs);
+    bwd_launch<128>(batch, hq, hkv, seq, qkv, o, dout, stats, impl_->D, dqkv, stream);
   else
-    bwd_launch<64>(batch, hq, hkv, seq, qkv, o, dout, stats, impl_->D, dqkv, stream, rope_cs);
+    bwd_launch<64>(batch, hq, hkv, seq, qkv, o, dout, stats, impl_->D, dqkv, stream);
 }
 
 }  // namespace cft::attn
@@ -1355,21 +1298,5 @@ extern "C" int cft_attention_bwd(const void* qkv, const void* o, const void* dou
       attn::bwd_launch<128>(batch, hq, hkv, seq, qkv, o, dout, lse, scratch, dqkv, st);
     else
       attn::bwd_launch<64>(batch, hq, hkv, seq, qkv, o, dout, lse, scratch, dqkv, st);
-  });
-}
-
-extern "C" int cft_attention_bwd_rope(const void* qkv, const void* o, const void* dout,
-                                      const float* lse, int batch, int hq, int hkv, int seq,
-                                      int head_dim, double rope_theta, void* dqkv, float* scratch,
-                                      cft_stream_t stream) {
-  return guarded([&] {
-    attn::check_shape(hq, hkv, seq, head_dim);
-    if (batch <= 0) return;
-    auto st = static_cast<cudaStream_t>(stream);
-    const float2* cs = llama::rope_cos_sin(seq, head_dim, static_cast<float>(rope_theta));
-    if (head_dim == 128)
-      attn::bwd_launch<128>(batch, hq, hkv, seq, qkv, o, dout, lse, scratch, dqkv, st, cs);
-    else
-      attn::bwd_launch<64>(batch, hq, hkv, seq, qkv, o, dout, lse, scratch, dqkv, st, cs);
   });
 }

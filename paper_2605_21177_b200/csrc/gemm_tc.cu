@@ -1018,12 +1018,10 @@ bool use_pairs(int M, int N, int K, bool allow_split) {
 void set_policy(int p) { g_policy = p; }
 
 namespace {
-int g_fuse = 15;  // bit 0: SwiGLU epilogues, bit 1: RoPE epilogue, bit 2: CE first pass,
-                  // bit 3: RoPE inverse in the attention backward epilogues
+int g_fuse = 7;  // bit 0: SwiGLU epilogues, bit 1: RoPE epilogue, bit 2: CE first pass
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
 void set_fusion(int on) { g_fuse = on; }
-int fusion() { return g_fuse; }
 
 // s = silu(X W1^T) * (X W3^T) with W13 = [w1; w3] (2F x in) in one CTA-pair GEMM; [u | g] is
 // also written to ug when non-null (the backward needs it).  Returns false when the shape or

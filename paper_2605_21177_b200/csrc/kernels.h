@@ -39,7 +39,6 @@ bool linear_fwd_rope(const void* x, int64_t n_tok, int64_t in_dim, const void* w
                      void* y, const float2* cs, int seq, int hd, int64_t rope_cols,
                      cudaStream_t stream);
 void set_fusion(int on);
-int fusion();  // the current fusion bits (set_fusion)
 }  // namespace tc
 
 namespace simt {  // gemm_simt.cu: fp32 / bf16 CUDA-core GEMMs and column sums

@@ -462,19 +462,13 @@ void Engine::llama_body(const int32_t* tok, const int32_t* lab, double* loss_cel
     pe();
     pb(kAttnBwd);  // algorithmic 2.5x the forward (dV, dP, dS.K, dS^T.Q + the S recompute)
     add_work(kAttnBwd, 5.0 * S.seq * double(S.seq) * S.head_dim * S.heads * B);
-    // RoPE's inverse rotation of dQ / dK folded into the attention epilogues (fusion bit 3),
-    // else one launch over the adjacent q and k heads of the fused row
-    const bool rope_fused = (tc::fusion() & 8) != 0;
-    attn_->backward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, l_do_, z.lse, l_dqkv_, st,
-                    rope_fused ? llama::rope_cos_sin(S.seq, S.head_dim, (float)S.rope_theta)
-                               : nullptr);
+    attn_->backward(B, S.heads, S.kv_heads, S.seq, S.head_dim, z.qkv, z.o, l_do_, z.lse, l_dqkv_, st);
     pe();
-    if (!rope_fused) {
-      pb(kBwdOther);
-      llama::rope(static_cast<bf16*>(l_dqkv_), N, S.seq, S.heads + S.kv_heads, S.head_dim, ld,
-                  (float)S.rope_theta, true, st);
-      pe();
-    }
+    pb(kBwdOther);
+    // q and k heads are adjacent in the fused row: one inverse-rotation launch covers both
+    llama::rope(static_cast<bf16*>(l_dqkv_), N, S.seq, S.heads + S.kv_heads, S.head_dim, ld,
+                (float)S.rope_theta, true, st);
+    pe();
     wgrad_stack({id(l, 1), id(l, 2), id(l, 3)}, l_dqkv_, QKV, z.a, d);  // wq | wk | wv
     if (!need(id(l, 0))) break;
     pb(kDgrad);

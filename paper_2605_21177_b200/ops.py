@@ -172,24 +172,14 @@ def attention_fwd(qkv: torch.Tensor, batch: int, hq: int, hkv: int, seq: int, he
 
 
 def attention_bwd(qkv, o, dout, lse, batch: int, hq: int, hkv: int, seq: int, head_dim: int,
-                  stream=None, rope_theta=None):
-    """dqkv (dQ | dK | dV in the qkv layout) of the causal GQA attention.  With ``rope_theta``
-    dQ and dK come out rotated back through RoPE's inverse (the gradient of the pre-RoPE q / k,
-    rotate-half convention, position = row % seq)."""
+                  stream=None):
+    """dqkv (dQ | dK | dV in the qkv layout) of the causal GQA attention."""
     _contig(qkv, o, dout, lse)
     dqkv = torch.empty_like(qkv)
     scratch = torch.empty(batch * hq * seq, dtype=torch.float32, device=qkv.device)
-    if rope_theta is None:
-        N.check(N.lib.cft_attention_bwd(qkv.data_ptr(), o.data_ptr(), dout.data_ptr(),
-                                        lse.data_ptr(), batch, hq, hkv, seq, head_dim,
-                                        dqkv.data_ptr(), scratch.data_ptr(), _stream(stream)),
-                "attention_bwd")
-    else:
-        N.check(N.lib.cft_attention_bwd_rope(qkv.data_ptr(), o.data_ptr(), dout.data_ptr(),
-                                             lse.data_ptr(), batch, hq, hkv, seq, head_dim,
-                                             float(rope_theta), dqkv.data_ptr(),
-                                             scratch.data_ptr(), _stream(stream)),
-                "attention_bwd")
+    N.check(N.lib.cft_attention_bwd(qkv.data_ptr(), o.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                                    batch, hq, hkv, seq, head_dim, dqkv.data_ptr(),
+                                    scratch.data_ptr(), _stream(stream)), "attention_bwd")
     return dqkv
 
 
@@ -243,11 +233,9 @@ def linear_dgrad_swiglu(dy: torch.Tensor, w2: torch.Tensor, ug: torch.Tensor, st
 
 
 def set_fusion(enable) -> None:
-    """Llama-engine epilogue fusions: True/15 all, False/0 none, or a mask (1 SwiGLU, 2 RoPE in
-    the QKV epilogue, 4 CE first pass in the lm_head epilogue, 8 RoPE's inverse in the attention
-    backward epilogues); 1 and 2 are bit-identical to the separate kernels, 4 and 8 round once
-    where the separate passes round twice."""
-    N.check(N.lib.cft_set_fusion(15 if enable is True else int(enable)))
+    """Llama-engine epilogue fusions: True/7 all, False/0 none, or a mask (1 SwiGLU, 2 RoPE,
+    4 CE first pass in the lm_head epilogue); 1 and 2 are bit-identical to the separate kernels."""
+    N.check(N.lib.cft_set_fusion(7 if enable is True else int(enable)))
 
 
 def set_gemm_policy(policy: int) -> None:

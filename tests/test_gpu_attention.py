@@ -81,33 +81,3 @@ def test_attention_rejects_unsupported_shapes(cuda):
         ops.attention_fwd(qkv, 1, 4, 4, 200, 64)
     with pytest.raises(CftError, match="head_dim"):
         ops.attention_fwd(qkv, 1, 4, 2, 128, 96)
-
-
-@pytest.mark.parametrize("B,H,KVH,S,hd", [(2, 4, 2, 256, 64), (1, 8, 2, 384, 128)])
-def test_attention_backward_with_fused_rope_inverse(cuda, B, H, KVH, S, hd):
-    """cft_attention_bwd_rope: dQ and dK rotated back through RoPE's inverse inside the kernels'
-    epilogues (rotate-half, position = row % seq; llama_kernels.cu rope_vec_kernel is the
-    separate pass it replaces) against the unfused backward followed by the inverse rotation in
-    fp64.  dV is untouched (bitwise); dQ / dK within the bf16 bar (the fused path rounds once)."""
-    from paper_2605_21177_b200 import ops
-    theta = 500000.0
-    g = torch.Generator(device=cuda).manual_seed(11 + hd)
-    qkv = torch.randn(B * S, (H + 2 * KVH) * hd, device=cuda, generator=g).to(torch.bfloat16)
-    dout = torch.randn(B * S, H * hd, device=cuda, generator=g).to(torch.bfloat16)
-    o, lse = ops.attention_fwd(qkv, B, H, KVH, S, hd)
-    plain = ops.attention_bwd(qkv, o, dout, lse, B, H, KVH, S, hd)
-    fused = ops.attention_bwd(qkv, o, dout, lse, B, H, KVH, S, hd, rope_theta=theta)
-    torch.cuda.synchronize()
-    half = hd // 2
-    pos = (torch.arange(B * S, device=cuda) % S).double()
-    inv = theta ** (-2.0 * torch.arange(half, device=cuda).double() / hd)
-    ang = pos[:, None] * inv[None, :]
-    c, s = ang.cos()[:, None, :], ang.sin()[:, None, :]
-    x = plain.double().view(B * S, H + 2 * KVH, hd)
-    x1, x2 = x[:, :H + KVH, :half], x[:, :H + KVH, half:]
-    want = torch.cat([x1 * c + x2 * s, x2 * c - x1 * s], -1)
-    got = fused.double().view(B * S, H + 2 * KVH, hd)
-    assert rel(got[:, :H], want[:, :H]) < 1e-2, ("dQ", rel(got[:, :H], want[:, :H]))
-    assert rel(got[:, H:H + KVH], want[:, H:]) < 1e-2, ("dK", rel(got[:, H:H + KVH], want[:, H:]))
-    assert torch.equal(fused.view(B * S, H + 2 * KVH, hd)[:, H + KVH:],
-                       plain.view(B * S, H + 2 * KVH, hd)[:, H + KVH:])
