@@ -139,6 +139,17 @@ int cft_scheduler_get_events(const cft_scheduler* s, cft_transfer_event* out, in
 /* write_transfer_log_csv (schedule.cpp:137-154) of this scheduler's events. */
 int cft_scheduler_write_transfer_log_csv(const cft_scheduler* s, const char* path);
 
+/* simulate_memory_trace (src/accounting.cpp:154-166) with sample_memory's categories
+ * (accounting.cpp:141-152): the per-step total bytes of a schedule dry run over `plan`, written
+ * to totals[0, cfg->total_steps); no training, no device.  The reference's acceptance check of
+ * the 2M + 16M/K memory model (tests/acceptance.cpp:254-296) runs on it. */
+int cft_simulate_memory_trace(const cft_plan* plan, const cft_tensor_info* infos, int n,
+                              const cft_schedule_config* cfg, int64_t activation_bytes,
+                              int64_t* totals, int64_t cap);
+/* model_peak_bytes (accounting.cpp:70-76): M * param_bytes + M * 16 / K for the default policy;
+ * -1 for M < 1 or K < 1 (the reference throws). */
+double cft_model_peak_bytes(int64_t m_elements, int K, const cft_cost_policy* policy);
+
 /* ===================================================================== */
 /* 2. Parity kernels: chunkft::kernels (include/chunkft/kernels.hpp:20-65) */
 /*    Host double* in/out; computed on the current CUDA device in fp64.    */

@@ -57,6 +57,24 @@ if REF is not None:
     _s("ref_config_json", CT.c_int, CT.c_char_p, CT.c_char_p, CT.c_char_p, i64)
     _s("ref_run_preset", CT.c_int, CT.c_char_p, CT.c_char_p, CT.c_char_p, i64)
     _s("ref_run_preset_checks", CT.c_int, CT.c_char_p, i64)
+    _s("ref_simulate_memory_trace", i64, CT.c_int, vp, vp, vp, vp, CT.c_int, CT.c_int, i64,
+       CT.c_int, i64, i64, vp)
+
+
+def simulate_memory_trace(tensors, K, T, steps, prefetch=False, bw=0, activation_bytes=0):
+    """simulate_memory_trace (src/accounting.cpp:154-166) over partition(K); tensors: list of
+    (id, rows, cols, storage_precision).  Returns the per-step totals."""
+    _need()
+    ids = np.array([t[0] for t in tensors], np.int32)
+    rows = np.array([t[1] for t in tensors], np.int64)
+    cols = np.array([t[2] for t in tensors], np.int64)
+    sp = np.array([t[3] for t in tensors], np.int32)
+    out = np.zeros(max(1, steps), np.int64)
+    n = REF.ref_simulate_memory_trace(len(tensors), _p(ids), _p(rows), _p(cols), _p(sp), K, T,
+                                      steps, int(prefetch), bw, activation_bytes, _p(out))
+    if n < 0:
+        raise RuntimeError(_err())
+    return [int(v) for v in out[:n]]
 
 
 def config_json(text=None, preset=None):

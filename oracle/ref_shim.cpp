@@ -27,6 +27,7 @@
 #include "chunkft/schedule.hpp"
 #include "chunkft/trainer.hpp"
 #include "chunkft/runner.hpp"
+#include "chunkft/accounting.hpp"
 #include <sstream>
 
 using namespace chunkft;
@@ -426,6 +427,37 @@ int ref_config_json(const char* text, const char* preset, char* out, int64_t cap
     const std::string s = config_to_json(cfg).dump(2);
     if (out && cap > 0) std::snprintf(out, static_cast<size_t>(cap), "%s", s.c_str());
     return 0;
+  } catch (const std::exception& e) {
+    set_err(e.what());
+    return -1;
+  }
+}
+
+// simulate_memory_trace (accounting.cpp:154-166) over partition(infos, K): per-step totals.
+int64_t ref_simulate_memory_trace(int n, const int32_t* ids, const int64_t* rows,
+                                  const int64_t* cols, const int32_t* storage, int K, int T,
+                                  int64_t total_steps, int prefetch, int64_t bw,
+                                  int64_t activation_bytes, int64_t* totals) {
+  try {
+    std::vector<TensorInfo> infos(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      infos[i].id = ids[i];
+      infos[i].reg_order = ids[i];
+      infos[i].rows = rows[i];
+      infos[i].cols = cols[i];
+      infos[i].storage_precision = storage[i];
+      infos[i].name = "t" + std::to_string(i);
+    }
+    const ChunkPlan plan = partition(infos, K);
+    ScheduleConfig sc;
+    sc.K = plan.K();
+    sc.T = T;
+    sc.total_steps = total_steps;
+    sc.prefetch = prefetch != 0;
+    sc.bandwidth_bytes_per_step = bw;
+    const MemoryTrace tr = simulate_memory_trace(infos, plan, sc, activation_bytes);
+    for (size_t i = 0; i < tr.samples.size(); ++i) totals[i] = tr.samples[i].total();
+    return static_cast<int64_t>(tr.samples.size());
   } catch (const std::exception& e) {
     set_err(e.what());
     return -1;

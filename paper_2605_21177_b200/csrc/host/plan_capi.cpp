@@ -210,6 +210,47 @@ int cft_scheduler_get_events(const cft_scheduler* s, cft_transfer_event* out, in
   });
 }
 
+// simulate_memory_trace + sample_memory (src/accounting.cpp:141-166): the schedule dry-run of
+// a plan's per-step memory, no training.  Per step: resident parameters (every tensor at its
+// storage precision), the scheduler's device state (+ the active chunk's gradient bytes when
+// it is resident), the activation bytes and the in-flight transfer bytes.
+int cft_simulate_memory_trace(const cft_plan* plan, const cft_tensor_info* infos, int n,
+                              const cft_schedule_config* cfg, int64_t activation_bytes,
+                              int64_t* totals, int64_t cap) {
+  return guard([&] {
+    const ChunkPlan& P = plan->plan;
+    ScheduleConfig sc;
+    sc.K = cfg->K;
+    sc.T = cfg->T;
+    sc.total_steps = cfg->total_steps;
+    sc.prefetch = cfg->prefetch != 0;
+    sc.bandwidth_bytes_per_step = cfg->bandwidth_bytes_per_step;
+    if (sc.total_steps > cap) throw PlanError("simulate_memory_trace: output buffer too small");
+    std::vector<int64_t> elems;
+    for (const auto& ch : P.chunks) elems.push_back(ch.elements);
+    RotationScheduler sched(sc, elems, P.policy);
+    int64_t resident = 0;
+    for (const TensorInfo& t : to_infos(infos, n)) resident += t.elements() * t.storage_precision;
+    for (int64_t t = 0; t < sc.total_steps; ++t) {
+      const int active = sched.step_begin().active;
+      int64_t state = sched.device_state_bytes();
+      if (active >= 0 && sched.is_resident(active))
+        state += P.chunk_elements(active) * P.policy.grad_bytes;
+      totals[t] = resident + state + activation_bytes + sched.transfer_inflight_bytes(t);
+      sched.step_end();
+    }
+    sched.finish();
+  });
+}
+
+// model_peak_bytes (src/accounting.cpp:70-76): M * param_bytes + M * mutable_bytes / K.
+double cft_model_peak_bytes(int64_t m_elements, int K, const cft_cost_policy* policy) {
+  const CostPolicy c = to_policy(policy);
+  if (m_elements < 1 || K < 1) return -1.0;
+  const double m = static_cast<double>(m_elements);
+  return m * c.param_bytes + m * c.mutable_bytes_per_element() / K;
+}
+
 int cft_scheduler_write_transfer_log_csv(const cft_scheduler* s, const char* path) {
   return guard([&] {
     if (!path) throw PlanError("write_transfer_log_csv: null path");

@@ -45,6 +45,9 @@ for _name, _res, _args in [
     ("cft_scheduler_num_events", C.c_int64, [C.c_void_p]),
     ("cft_scheduler_get_events", C.c_int, [C.c_void_p, _P(N.TransferEventC), C.c_int64]),
     ("cft_scheduler_write_transfer_log_csv", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("cft_simulate_memory_trace", C.c_int, [C.c_void_p, _P(N.TensorInfo), C.c_int,
+                                            _P(N.ScheduleConfig), C.c_int64, C.c_void_p, C.c_int64]),
+    ("cft_model_peak_bytes", C.c_double, [C.c_int64, C.c_int, _P(N.CostPolicy)]),
 ]:
     _fn = getattr(_L, _name)
     _fn.restype = _res
@@ -298,3 +301,27 @@ class RotationScheduler:
         N.check(_L.cft_scheduler_get_events(self._h, buf, n))
         return [TransferEvent(e.step, e.chunk, "load" if e.dir == 0 else "offload", e.bytes,
                               e.latency_steps) for e in buf[:n]]
+
+
+def simulate_memory_trace(infos, plan: ChunkPlan, config: ScheduleConfig,
+                          activation_bytes: int = 0) -> List[int]:
+    """simulate_memory_trace (src/accounting.cpp:154-166): per-step total bytes of a schedule dry
+    run over ``plan`` -- resident parameters at their storage precision, the scheduler's device
+    state (+ the resident active chunk's gradient), activations and in-flight transfers."""
+    import numpy as np
+    cfg = N.ScheduleConfig(config.K, config.T, config.total_steps, int(config.prefetch), 0,
+                           config.bandwidth_bytes_per_step)
+    out = np.zeros(max(1, config.total_steps), dtype=np.int64)
+    arr = _infos_c(infos)
+    N.check(_L.cft_simulate_memory_trace(plan._h, arr, len(infos), C.byref(cfg), activation_bytes,
+                                         out.ctypes.data, out.size), "simulate_memory_trace")
+    return [int(v) for v in out[:config.total_steps]]
+
+
+def model_peak_bytes(m_elements: int, K: int, policy: CostPolicy | None = None) -> float:
+    """model_peak_bytes (src/accounting.cpp:70-76): M * param_bytes + M * mutable_bytes / K."""
+    pc = (policy or CostPolicy())._c()
+    v = _L.cft_model_peak_bytes(m_elements, K, C.byref(pc))
+    if v < 0:
+        raise Error("model_peak_bytes: M and K must be at least 1")
+    return v

@@ -1,0 +1,133 @@
+"""The reference's acceptance gate (tests/acceptance.cpp) on the GPU engine, for the criteria
+SURVEY §2 row 18 marks as hot path:
+
+* criterion 1 (acceptance.cpp:88-194): chunk-masked gradients equal the dense slices -- over
+  random layer stacks, the chunk gradients of every chunk of a K-way plan, stitched back
+  together, equal the K = 1 (dense) gradient bit for bit (fp64 path);
+* criterion 2 (:196-252): K = 1, T = 1 reproduces the dense AdamW loop bit for bit -- covered by
+  the `dense_reduction` golden in test_gpu_engine.py (bit-exact trajectory and parameters);
+* criterion 3 (:254-296): the memory model -- host only, tests/test_acceptance_memory.py;
+* criterion 7 (:435-493): optimizer state survives the host round trip -- offload on / off give
+  identical runs, test_gpu_engine.py;
+* criterion 8 (:495-537): prefetch leaves results untouched -- every preset run through the
+  experiment runner with prefetch off and on writes byte-identical checkpoints and the same
+  final loss (here)."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _random_stack(rng):
+    """A random layer stack in the spirit of acceptance.cpp:96-135 (our own generator):
+    optional embedding, 1-3 sections of [layernorm?] linear [tanh?], a squared / half_sq /
+    softmax_ce loss, well under 10^4 parameters."""
+    from paper_2605_21177_b200.engine import Model
+    rows = int(rng.integers(1, 6))
+    batch = {}
+    if rng.integers(0, 4) == 0:
+        vocab, dim, seq = int(rng.integers(3, 25)), int(rng.integers(1, 7)), int(rng.integers(1, 4))
+        layers = [("embedding", vocab, dim, seq)]
+        width = dim * seq
+        batch["tokens"] = rng.integers(0, vocab, (rows, seq)).astype(np.int32)
+    else:
+        width = int(rng.integers(1, 11))
+        layers = []
+        batch["x"] = rng.uniform(-1, 1, (rows, width))
+    for _ in range(int(rng.integers(1, 4))):
+        if rng.integers(0, 3) == 0:
+            layers.append(("layernorm", width))
+        out = int(rng.integers(1, 11))
+        layers.append(("linear", width, out, bool(rng.integers(0, 2))))
+        width = out
+        if rng.integers(0, 2):
+            layers.append(("tanh",))
+    if width >= 2 and rng.integers(0, 2):
+        loss = "softmax_ce"
+        batch["labels"] = rng.integers(0, width, rows).astype(np.int32)
+    else:
+        loss = "half_sq" if rng.integers(0, 2) else "squared"
+        batch["target"] = rng.uniform(-1, 1, (rows, width))
+    m = Model(loss=loss)
+    for L in layers:
+        if L[0] == "embedding":
+            m.add_embedding(L[1], L[2], L[3])
+        elif L[0] == "layernorm":
+            m.add_layernorm(L[1])
+        elif L[0] == "linear":
+            m.add_linear(L[1], L[2], L[3])
+        else:
+            m.add_tanh()
+    return m, batch, rows
+
+
+def _chunk_grads(model, params, batch, rows, K):
+    """Every chunk's gradient (plan order within the chunk) with the weights held fixed."""
+    from paper_2605_21177_b200.engine import AdamWHyper, ChunkEngine, TrainOptions
+    from paper_2605_21177_b200.plan import ScheduleConfig
+    opts = TrainOptions(schedule=ScheduleConfig(K=K, T=1, total_steps=K), dtype="fp64",
+                        hyper=AdamWHyper(eta=1e-300))  # updates below half an ulp: weights held
+    eng = ChunkEngine(model, params, rows, opts)
+    staged = eng.stage(batch, device=True)
+    out = []
+    for _ in range(K):
+        c = eng.step_begin()
+        eng.forward_backward(staged, 0)
+        out.append((c, eng.grad_tensor().cpu().numpy().copy()))
+        eng.step_end()
+    eng.finish()
+    return out
+
+
+def test_criterion1_chunk_gradients_stitch_to_the_dense_gradient(cuda):
+    from paper_2605_21177_b200.plan import TensorInfo, partition
+    rng = np.random.default_rng(20260822)
+    checked = 0
+    for trial in range(12):
+        model, batch, rows = _random_stack(rng)
+        tensors = model.tensors()
+        n = sum(r * c for _, r, c in tensors)
+        assert n < 10000
+        params = rng.uniform(-0.5, 0.5, n)
+        offs = np.cumsum([0] + [r * c for _, r, c in tensors])
+        total_rows = sum(r for _, r, _ in tensors)
+        K = int(rng.integers(1, min(12, total_rows) + 1))
+        dense = _chunk_grads(model, params, batch, rows, 1)[0][1]
+        infos = [TensorInfo(i, nm, r, c) for i, (nm, r, c) in enumerate(tensors)]
+        plan = partition(infos, K)
+        stitched = np.full(n, np.nan)
+        for c, g in _chunk_grads(model, params, batch, rows, K):
+            pos = 0
+            for s in plan.chunks[c].slices:
+                cols = tensors[s.tensor_id][2]
+                cnt = (s.row_end - s.row_begin) * cols
+                base = offs[s.tensor_id] + s.row_begin * cols
+                stitched[base: base + cnt] = g[pos: pos + cnt]
+                pos += cnt
+            assert pos == g.size
+        assert not np.isnan(stitched).any(), trial
+        assert np.array_equal(stitched, dense), (trial, np.abs(stitched - dense).max())
+        checked += 1
+    assert checked == 12
+
+
+def test_criterion8_prefetch_leaves_every_preset_untouched(tmp_path):
+    from paper_2605_21177_b200 import runner
+    for name in runner.preset_names():
+        digests, losses = {}, {}
+        for prefetch in (False, True):
+            doc = runner.make_preset(name).to_dict()
+            doc["schedule"]["prefetch"] = prefetch
+            out = tmp_path / f"{name}-{int(prefetch)}"
+            doc["out_dir"] = str(out)
+            summary = runner.run_experiment(runner.parse_config(doc), dtype="fp64")
+            losses[prefetch] = dict(ln.split(" ", 1) for ln in summary.splitlines())["final_loss"]
+            ck = out / "checkpoints"
+            digests[prefetch] = {f: hashlib.sha256((ck / f).read_bytes()).hexdigest()
+                                 for f in sorted(os.listdir(ck))}
+        assert digests[False] and digests[False] == digests[True], name
+        assert losses[False] == losses[True], name
