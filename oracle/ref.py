@@ -57,8 +57,21 @@ if REF is not None:
     _s("ref_config_json", CT.c_int, CT.c_char_p, CT.c_char_p, CT.c_char_p, i64)
     _s("ref_run_preset", CT.c_int, CT.c_char_p, CT.c_char_p, CT.c_char_p, i64)
     _s("ref_run_preset_checks", CT.c_int, CT.c_char_p, i64)
+    _s("ref_dense_run", i64, CT.c_char_p, i64, vp, vp, i64)
     _s("ref_simulate_memory_trace", i64, CT.c_int, vp, vp, vp, vp, CT.c_int, CT.c_int, i64,
        CT.c_int, i64, i64, vp)
+
+
+def dense_run(config_json, steps):
+    """reference::dense_adamw_run (src/trainer.cpp:117-181) on the config's model and batches:
+    (losses per step, final parameters)."""
+    _need()
+    losses = np.zeros(max(1, steps))
+    params = np.zeros(1 << 20)
+    n = REF.ref_dense_run(config_json.encode(), steps, _p(losses), _p(params), params.size)
+    if n < 0:
+        raise RuntimeError(_err())
+    return losses[:steps], params[:n].copy()
 
 
 def simulate_memory_trace(tensors, K, T, steps, prefetch=False, bw=0, activation_bytes=0):

@@ -464,6 +464,30 @@ int64_t ref_simulate_memory_trace(int n, const int32_t* ids, const int64_t* rows
   }
 }
 
+// reference::dense_adamw_run (trainer.cpp:117-181) on build_model(parse_config(json)) over its
+// make_stream batches: the textbook dense loop the acceptance gate's criterion 2 compares the
+// K = T = 1 chunked run against (tests/acceptance.cpp:196-252).  Returns the parameter count.
+int64_t ref_dense_run(const char* json, int64_t steps, double* losses, double* params,
+                      int64_t cap) {
+  try {
+    const ExperimentConfig cfg = parse_config(nlohmann::json::parse(json));
+    Model m = build_model(cfg);
+    std::unique_ptr<DataStream> data = make_stream(cfg.dataset, m);
+    const auto r = reference::dense_adamw_run(m, *data, cfg.hyper, steps, cfg.micro_batches);
+    for (size_t i = 0; i < r.losses.size(); ++i) losses[i] = r.losses[i];
+    const auto flat = m.snapshot_params();
+    if (static_cast<int64_t>(flat.size()) > cap) {
+      set_err("params capacity");
+      return -1;
+    }
+    std::memcpy(params, flat.data(), sizeof(double) * flat.size());
+    return static_cast<int64_t>(flat.size());
+  } catch (const std::exception& e) {
+    set_err(e.what());
+    return -1;
+  }
+}
+
 // make_preset(name) + run_experiment with out_dir set (runner.cpp:144-192): writes the
 // artifact bundle and returns summary_text in `summary`.
 int ref_run_preset(const char* name, const char* out_dir, char* summary, int64_t cap) {
