@@ -134,11 +134,14 @@ __global__ void rms_bwd_reg_kernel(const bf16* __restrict__ dy, const bf16* __re
   const uint4* dyr = reinterpret_cast<const uint4*>(dy + r * d);
   const uint4* xr = reinterpret_cast<const uint4*>(x + r * d);
   const uint4* gr = reinterpret_cast<const uint4*>(g);
-  uint4 dv[VPT], xv[VPT];
+  uint4 dv[VPT], xv[VPT], rv[VPT];
+  // the residual row is loaded with dy and x, so its latency hides behind the row reduction
+  const uint4* rr = res ? reinterpret_cast<const uint4*>(res + r * d) : nullptr;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     dv[k] = __ldcs(dyr + threadIdx.x + k * blockDim.x);
     xv[k] = xr[threadIdx.x + k * blockDim.x];
+    if (rr) rv[k] = __ldcs(rr + threadIdx.x + k * blockDim.x);
   }
   float c = 0.f;
 #pragma unroll
@@ -151,7 +154,6 @@ __global__ void rms_bwd_reg_kernel(const bf16* __restrict__ dy, const bf16* __re
     for (int e = 0; e < 8; ++e) c += gg[e] * a[e] * b[e] * rs;
   }
   c = block_sum_small<VPT>(c) / d;
-  const uint4* rr = res ? reinterpret_cast<const uint4*>(res + r * d) : nullptr;
   uint4* orow = reinterpret_cast<uint4*>(out + r * d);
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
@@ -160,7 +162,7 @@ __global__ void rms_bwd_reg_kernel(const bf16* __restrict__ dy, const bf16* __re
     unpack8(dv[k], a);
     unpack8(xv[k], b);
     unpack8(gr[j], gg);
-    if (rr) unpack8(rr[j], o);
+    if (rr) unpack8(rv[k], o);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const float v = rs * (gg[e] * a[e] - b[e] * rs * c);
@@ -191,11 +193,13 @@ __global__ void rms_bwd_dg_kernel(const bf16* __restrict__ dy, const bf16* __res
     const float rs = rstd[r];
     const uint4* dyr = reinterpret_cast<const uint4*>(dy + r * d);
     const uint4* xr = reinterpret_cast<const uint4*>(x + r * d);
-    uint4 dv[VPT], xv[VPT];
+    const uint4* rr = res ? reinterpret_cast<const uint4*>(res + r * d) : nullptr;
+    uint4 dv[VPT], xv[VPT], rv[VPT];
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
+    for (int k = 0; k < VPT; ++k) {  // the residual row too, ahead of the row reduction
       dv[k] = __ldcs(dyr + threadIdx.x + k * blockDim.x);
       xv[k] = xr[threadIdx.x + k * blockDim.x];
+      if (rr) rv[k] = __ldcs(rr + threadIdx.x + k * blockDim.x);
     }
     float c = 0.f;
 #pragma unroll
@@ -211,7 +215,6 @@ __global__ void rms_bwd_dg_kernel(const bf16* __restrict__ dy, const bf16* __res
       }
     }
     c = block_sum_small<VPT>(c) / d;
-    const uint4* rr = res ? reinterpret_cast<const uint4*>(res + r * d) : nullptr;
     uint4* orow = reinterpret_cast<uint4*>(out + r * d);
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
@@ -220,7 +223,7 @@ __global__ void rms_bwd_dg_kernel(const bf16* __restrict__ dy, const bf16* __res
       unpack8(dv[k], a);
       unpack8(xv[k], b);
       unpack8(gr[j], gg);
-      if (rr) unpack8(rr[j], o);
+      if (rr) unpack8(rv[k], o);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float v = rs * (gg[e] * a[e] - b[e] * rs * c);
