@@ -762,12 +762,14 @@ def run_llama(args, rank, world, local_rank):
     gemm_launches = sum(phases[k][1] for k in ("fwd_gemm", "dgrad", "wgrad"))
     alg_bytes_launch = sum(pbytes[k] for k in ("fwd_gemm", "dgrad", "wgrad")) / max(gemm_launches, 1)
     traffic, traffic_src = None, None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_gemm_traffic.json")
-    if args.workload == "llama8b" and os.path.exists(tpath):
-        with open(tpath) as f:
+    pdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    tname = next((n for n in ("r2_gemm_traffic.json", "r1_gemm_traffic.json")
+                  if os.path.exists(os.path.join(pdir, n))), None)
+    if args.workload == "llama8b" and tname:
+        with open(os.path.join(pdir, tname)) as f:
             tj = json.load(f)
         traffic = tj["dram_bytes_per_launch"]
-        traffic_src = ("profiles/r1_gemm_traffic.json: ncu dram__bytes_read+write per GEMM launch "
+        traffic_src = (f"profiles/{tname}: ncu dram__bytes_read+write per GEMM launch "
                        f"over one step ({tj['gemm_launches']} launches, L2 flushed per kernel); "
                        f"{tj['ratio']:.2f}x the algorithmic bytes")
     wg_tflops = phases["wgrad"][2] / max(phases["wgrad"][0], 1e-9) / 1e9
