@@ -212,7 +212,7 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
 }
 
 // ------------------------------------------------------------------------------------------
-// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax of head A, 6-9 of B.
+// forward: warp 0 TMA, warp 1 MMA issuer + TMEM owner, warps 4-7 softmax of head A, 8-11 of B.
 // 128-row key blocks (K ring of 2, V ring of 3).  TMEM: S_A, S_B (128 columns each), O_A, O_B;
 // the softmax thread of a row reads its 128 scores, writes P (bf16) into the first 64
 // columns of its own S row, and P.V runs with A from TMEM.  The tensor pipe executes
@@ -226,7 +226,10 @@ struct FwdSmem {
   static constexpr size_t BYTES = 1024 + BAR + 256;
 };
 
-constexpr int kFwdThreads = 64 + 8 * 32;  // TMA warp, MMA warp, 8 softmax warps
+// warpgroup 0: TMA warp, MMA warp, two idle warps (warpgroup-aligned roles, so the register
+// file can be re-split with setmaxnreg); warpgroups 1 and 2: the softmax of head A and head B
+constexpr int kFwdThreads = 128 + 8 * 32;
+constexpr int kFwdCtlRegs = 56, kFwdSoftmaxRegs = 224;  // 128 x 56 + 256 x 224 <= 64K
 
 // Work item = (query tile, batch, KV head, head pair), longest query tiles first; a persistent
 // CTA walks items blockIdx.x, +gridDim.x, ...  The next item's Q tiles load while the current
@@ -295,7 +298,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tslot;
   // TMEM: S_t at [128 t, +128) (P_t in its first 64 columns), O_t at [256 + HD t, +HD)
-
+  // the softmax warpgroups get the registers the control warpgroup does not need (the row's
+  // 128 scores stay in registers); each warpgroup re-sizes at the top of its own branch
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kFwdCtlRegs));
   if (warp == 0) {
     if (lane == 0) {
       // issue order per item: Q, K0, K1, V0, K2, V1, ... (keys one block ahead of values)
@@ -400,10 +406,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
     }
+  }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kFwdSoftmaxRegs));
     // softmax: 4 warps per head, one per TMEM lane quarter; a thread owns a whole row (the
     // block's 128 scores and O's HD columns), so the row max needs no exchange between warps.
-    const int idx = warp - 2;
+    const int idx = warp - 4;
     const int t = idx / 4;
     const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
