@@ -123,8 +123,8 @@ __device__ __forceinline__ void st_row32(bf16* p, const uint32_t (&r)[32], float
 
 
 // 2^x on the FMA pipe (degree-3 minimax of 2^f on [-1/2, 1/2], rel. error 7.5e-5 -- far below
-// the bf16 rounding of P): the MUFU unit (16 ex2 / clock / SM) would otherwise bound the
-// softmax; a quarter of the exponentials go this way.
+// the bf16 rounding of P), for offloading a share of the exponentials from the MUFU unit
+// (CFT_POLY_SHARE below; measured best at 0 on B200).
 __device__ __forceinline__ float ex2_poly(float x) {
   // clamped at 2^-126 (the exponent add must not underflow): masked (-inf) scores give
   // ~6e-39 here against exactly 0 from MUFU -- far below any bf16 P the row sums with
@@ -136,7 +136,10 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 #ifndef CFT_POLY_SHARE
-#define CFT_POLY_SHARE 1  // exponentials on the FMA pipe per 4 (0..4)
+// exponentials on the FMA pipe per 4 (0..4).  Measured at the 8B layer (scripts/
+// attn_share_sweep.sh, warpgroup-aligned forward): 0 -> fwd 90.1 / bwd 273.1 us, 1 -> 91.0 /
+// 279.7, 2 -> 101.1 / 291.2 -- the issue slots, not the MUFU unit, are the limit, so all on MUFU
+#define CFT_POLY_SHARE 0
 #endif
 template <int E>
 __device__ __forceinline__ float ex2_mix(float x) {
