@@ -473,24 +473,28 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
         float2 accs[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        // P packed in place (word e/2 holds columns e, e+1), in two halves: the first half's
+        // TMEM store (P words 0..31 over S columns 0..31, already read) runs while the second
+        // half's exponentials are computed
 #pragma unroll
-        for (int e = 0; e < 128; e += 4) {  // P packed in place: word e/2 holds columns e, e+1
-          float2 x0 = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
-          float2 x1 = __ffma2_rn(make_float2(f32(v[e + 2]), f32(v[e + 3])), c2, nm2);
-          x0.x = ex2_mix<0>(x0.x);
-          x0.y = ex2_mix<1>(x0.y);
-          x1.x = ex2_mix<2>(x1.x);
-          x1.y = ex2_mix<3>(x1.y);
-          accs[(e >> 2) & 1] = __fadd2_rn(accs[(e >> 2) & 1], __fadd2_rn(x0, x1));
-          v[e / 2] = pack_bf16(x0.x, x0.y);
-          v[e / 2 + 1] = pack_bf16(x1.x, x1.y);
+        for (int half = 0; half < 2; ++half) {
+#pragma unroll
+          for (int e = 64 * half; e < 64 * half + 64; e += 4) {
+            float2 x0 = __ffma2_rn(make_float2(f32(v[e]), f32(v[e + 1])), c2, nm2);
+            float2 x1 = __ffma2_rn(make_float2(f32(v[e + 2]), f32(v[e + 3])), c2, nm2);
+            x0.x = ex2_mix<0>(x0.x);
+            x0.y = ex2_mix<1>(x0.y);
+            x1.x = ex2_mix<2>(x1.x);
+            x1.y = ex2_mix<3>(x1.y);
+            accs[(e >> 2) & 1] = __fadd2_rn(accs[(e >> 2) & 1], __fadd2_rn(x0, x1));
+            v[e / 2] = pack_bf16(x0.x, x0.y);
+            v[e / 2 + 1] = pack_bf16(x1.x, x1.y);
+          }
+          tmem_st32(tS + 32 * half, *reinterpret_cast<const uint32_t(*)[32]>(v + 32 * half));
         }
         const float2 acc = __fadd2_rn(accs[0], accs[1]);
         l += acc.x + acc.y;
         trace_ev(tr, 1 + t, tcnt, kEvExpDone, t, g);
-        // P words [0, 64) of the row: columns 0 .. 127 in K order, over the row's S columns
-        tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(v));
-        tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(v + 32));
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
