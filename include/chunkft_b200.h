@@ -218,6 +218,16 @@ int cft_linear_dbias_slice(cft_dtype dtype, const void* dy, int64_t n_tok, int64
                            int64_t row_begin, int64_t row_end, void* db_slice, int accumulate,
                            cft_stream_t stream);
 
+/* Norm weight-gradient slice: dgamma_slice[j-rb] (+)= sum_b dy[b,j] (x[b,j] - mean[b]) rstd[b],
+ * j in [rb,re) -- layernorm_dgamma (kernels.hpp:56-60, kernels_serial.cpp:132-143); mean NULL is
+ * RMSNorm (x_hat = x rstd).  mean / rstd hold one fp32 per row (fp64 for CFT_F64, whose path is
+ * the reference's layernorm and needs mean); dgamma_slice is fp32 (fp64 for CFT_F64).
+ * dbeta is cft_linear_dbias_slice over the same dy (kernels_serial.cpp:145-152). */
+int cft_norm_dgamma_slice(cft_dtype dtype, const void* dy, const void* x, const void* mean,
+                          const void* rstd, int64_t n_tok, int64_t dim, int64_t row_begin,
+                          int64_t row_end, void* dgamma_slice, int accumulate,
+                          cft_stream_t stream);
+
 /* y[p,:] = table[tokens[p],:] for a table of table_rows rows.    kernels.hpp:35-37
  * An id outside [0, table_rows) reads nothing: its output row is zeroed and counted in
  * *bad_dev (device uint64, may be NULL) -- the device-side form of the range check the
@@ -490,6 +500,34 @@ typedef struct {
   int (*barrier)(void* ctx, cft_stream_t stream);
 } cft_comm;
 int cft_engine_step_dp(cft_engine* e, const cft_batch* batches, const cft_comm* comm);
+
+/* The rotation's physical state moves (load_to_device / offload_to_host, optimizer.hpp:65-66,
+ * src/optimizer.cpp:101-122) for a host driving its own rotation with cft_scheduler_*.  Host
+ * tier: one pinned block per chunk, [master | m | v] of n elements each (the reference's blob
+ * without its [n][E] header, optimizer.cpp:45-73); device slot: three arrays.  The copies are
+ * queued on `stream` after waiting on `wait_event` (a cudaEvent_t, or NULL) -- the slot's last
+ * offload, or the step that last wrote the state -- and `done_event` (or NULL) is recorded after
+ * them.  A host block that is not pinned is an error (the copy would not be asynchronous). */
+int cft_states_prefetch(const void* host_block, int64_t n, cft_dtype state_dtype,
+                        void* dev_master, void* dev_m, void* dev_v, cft_stream_t stream,
+                        void* wait_event, void* done_event);
+int cft_states_offload(const void* dev_master, const void* dev_m, const void* dev_v, int64_t n,
+                       cft_dtype state_dtype, void* host_block, cft_stream_t stream,
+                       void* wait_event, void* done_event);
+
+/* NCCL behind the communicator (SURVEY §8(b) "cft_allreduce_f32(buf, n, ncclComm_t, stream)").
+ * `nccl_comm` is an ncclComm_t the host created (ncclCommInitRank, one rank per GPU); NCCL is
+ * resolved at run time from libnccl.so.2 (the host's copy when already loaded), so the library
+ * carries no link-time NCCL dependency.  Collectives are queued on `stream` and sum in NCCL's
+ * order: with world > 2 the fp64 path is no longer bit-identical to the reference's rank-order
+ * accumulation (use the peer-memory protocol for that).
+ *   cft_allreduce_f32      in-place SUM of n floats over the communicator's ranks;
+ *   cft_comm_nccl_create   fills a cft_comm (world / rank from the communicator; barrier = a
+ *                          one-element all-reduce) for cft_engine_step_dp;
+ *   cft_comm_nccl_destroy  frees what create allocated (not the NCCL communicator). */
+int cft_allreduce_f32(float* buf, int64_t n, void* nccl_comm, cft_stream_t stream);
+int cft_comm_nccl_create(void* nccl_comm, cft_comm* out);
+void cft_comm_nccl_destroy(cft_comm* comm);
 
 /* TrainTrajectoryEntry (trainer.hpp:26-33): step, chunk, loss (pre-update mean), grad_norm_sq. */
 int64_t cft_engine_trajectory(cft_engine* e, int64_t* step, int32_t* chunk, double* loss,

@@ -81,6 +81,8 @@ _sig("cft_linear_fwd_swiglu", C.c_int, vp, i64, i64, vp, i64, vp, vp, vp)
 _sig("cft_linear_dgrad_swiglu", C.c_int, vp, i64, i64, vp, i64, vp, vp, vp)
 _sig("cft_linear_wgrad_slice", C.c_int, C.c_int, vp, i64, i64, vp, i64, i64, i64, vp, C.c_int, vp)
 _sig("cft_linear_dbias_slice", C.c_int, C.c_int, vp, i64, i64, i64, i64, vp, C.c_int, vp)
+_sig("cft_norm_dgamma_slice", C.c_int, C.c_int, vp, vp, vp, vp, i64, i64, i64, i64, vp, C.c_int,
+     vp)
 _sig("cft_embedding_gather", C.c_int, C.c_int, vp, i64, i64, vp, i64, vp, vp, vp)
 _sig("cft_embedding_scatter_slice", C.c_int, C.c_int, vp, i64, vp, i64, i64, i64, vp, vp, vp)
 _sig("cft_grad_stats", C.c_int, C.c_int, vp, i64, f64, vp, vp)
@@ -96,6 +98,9 @@ _sig("cft_set_gemm_policy", C.c_int, C.c_int)
 _sig("cft_set_fusion", C.c_int, C.c_int)
 _sig("cft_sgd_slice", C.c_int, C.c_int, vp, vp, i64, f64, f64, C.c_int, vp, vp, i32, vp, vp)
 _sig("cft_convert", C.c_int, C.c_int, vp, C.c_int, vp, i64, vp)
+_sig("cft_states_prefetch", C.c_int, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp)
+_sig("cft_states_offload", C.c_int, vp, vp, vp, i64, C.c_int, vp, vp, vp, vp)
+_sig("cft_allreduce_f32", C.c_int, vp, i64, vp, vp)
 
 # ---- parity kernels (chunkft::kernels signatures, host double*) ----
 dp = vp  # numpy arrays are passed by address

@@ -86,7 +86,8 @@ __global__ void ln_dinput_kernel(const T* dy, const T* x, const float* mean, con
   }
 }
 
-// dgamma[j-rb] (+)= sum_b dy[b,j] * xhat[b,j], j in [rb,re)  (kernels_serial.cpp:132-143)
+// dgamma[j-rb] (+)= sum_b dy[b,j] * xhat[b,j], j in [rb,re)  (kernels_serial.cpp:132-143);
+// mean == nullptr: RMSNorm's xhat = x * rstd
 template <typename T>
 __global__ void ln_dgamma_kernel(const T* dy, const T* x, const float* mean, const float* rstd,
                                  long long rows, long long dim, long long rb, long long re,
@@ -97,7 +98,7 @@ __global__ void ln_dgamma_kernel(const T* dy, const T* x, const float* mean, con
   float acc = 0.f;
   if (j < re)
     for (long long b = part; b < rows; b += 8)
-      acc += ldf(dy + b * dim + j) * (ldf(x + b * dim + j) - mean[b]) * rstd[b];
+      acc += ldf(dy + b * dim + j) * (ldf(x + b * dim + j) - (mean ? mean[b] : 0.f)) * rstd[b];
   red[part][threadIdx.x % 32] = acc;
   __syncthreads();
   if (part == 0 && j < re) {

@@ -294,6 +294,33 @@ int cft_linear_dbias_slice(cft_dtype dtype, const void* dy, int64_t n_tok, int64
   });
 }
 
+int cft_norm_dgamma_slice(cft_dtype dtype, const void* dy, const void* x, const void* mean,
+                          const void* rstd, int64_t n_tok, int64_t dim, int64_t rb, int64_t re,
+                          void* dgamma, int accumulate, cft_stream_t stream) {
+  return guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    CFT_CHECK(rb >= 0 && re <= dim && rb <= re, "norm dgamma: row range out of bounds");
+    CFT_CHECK(rstd, "norm dgamma: rstd is required");
+    if (re == rb) return;
+    if (dtype == CFT_F64) {
+      CFT_CHECK(mean, "norm dgamma: the fp64 path is the reference's layernorm (mean required)");
+      if (!accumulate) CFT_CUDA(cudaMemsetAsync(dgamma, 0, sizeof(double) * (re - rb), s));
+      f64::layernorm_dgamma(static_cast<const double*>(dy), static_cast<const double*>(x),
+                            static_cast<const double*>(mean), static_cast<const double*>(rstd),
+                            (int)n_tok, (int)dim, rb, re, static_cast<double*>(dgamma), s);
+    } else if (dtype == CFT_BF16) {
+      layers::layernorm_dgamma(static_cast<const __nv_bfloat16*>(dy),
+                               static_cast<const __nv_bfloat16*>(x),
+                               static_cast<const float*>(mean), static_cast<const float*>(rstd),
+                               n_tok, dim, rb, re, static_cast<float*>(dgamma), accumulate, s);
+    } else {
+      layers::layernorm_dgamma(static_cast<const float*>(dy), static_cast<const float*>(x),
+                               static_cast<const float*>(mean), static_cast<const float*>(rstd),
+                               n_tok, dim, rb, re, static_cast<float*>(dgamma), accumulate, s);
+    }
+  });
+}
+
 int cft_softmax_ce(cft_dtype dtype, const void* y, const int32_t* labels, int64_t rows,
                    int64_t cols, void* dy, double* loss_dev, uint64_t* bad_label_dev,
                    cft_stream_t stream) {

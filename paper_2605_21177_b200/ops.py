@@ -102,6 +102,25 @@ def linear_dbias_slice(dy: torch.Tensor, row_begin: int, row_end: int,
     return out
 
 
+def norm_dgamma_slice(dy: torch.Tensor, x: torch.Tensor, rstd: torch.Tensor, row_begin: int,
+                      row_end: int, mean: torch.Tensor | None = None,
+                      out: torch.Tensor | None = None, accumulate: bool = False,
+                      stream=None) -> torch.Tensor:
+    """dgamma[j - rb] (+)= sum_b dy[b,j] (x[b,j] - mean[b]) rstd[b] over [rb, re): LayerNorm
+    (kernels_serial.cpp:132-143); mean None = RMSNorm.  dbeta = linear_dbias_slice(dy, ...)."""
+    _contig(dy, x, rstd, mean)
+    n_tok, dim = dy.shape
+    odt = torch.float64 if dy.dtype == torch.float64 else torch.float32
+    if out is None:
+        out = torch.empty(row_end - row_begin, dtype=odt, device=dy.device)
+        accumulate = False
+    N.check(N.lib.cft_norm_dgamma_slice(_dtype(dy), dy.data_ptr(), x.data_ptr(), _ptr(mean),
+                                        rstd.data_ptr(), n_tok, dim, row_begin, row_end,
+                                        out.data_ptr(), int(accumulate), _stream(stream)),
+            "norm_dgamma_slice")
+    return out
+
+
 def embedding_gather(table: torch.Tensor, tokens: torch.Tensor, out=None, bad=None, stream=None):
     """y[p] = table[tokens[p]]; ids outside [0, rows) give a zero row and are counted in `bad`
     (a 1-element int64 device tensor) when given."""
