@@ -40,6 +40,13 @@ typedef enum { CFT_F32 = 0, CFT_BF16 = 1, CFT_F64 = 2 } cft_dtype;
 const char* cft_last_error(void);
 int cft_last_status(void);
 int cft_version(void);
+/* Context (SURVEY §8(b) "cft_init / cft_destroy"): cft_init binds the calling thread to
+ * `device` (which must be an sm_100 B200; anything else is refused: there is no other code
+ * path), creates its primary context and resolves the driver entry points now instead of inside
+ * the first step.  The library allocates nothing per context -- callers own every buffer, engines
+ * their own (cft_engine_destroy) -- so cft_destroy only clears the thread's error state. */
+int cft_init(int device);
+int cft_destroy(void);
 
 /* ===================================================================== */
 /* 1. Host planning                                                        */

@@ -73,6 +73,8 @@ def _sig(name, res, *args):
 _sig("cft_last_error", cp)
 _sig("cft_last_status", C.c_int)
 _sig("cft_version", C.c_int)
+_sig("cft_init", C.c_int, C.c_int)
+_sig("cft_destroy", C.c_int)
 
 # ---- performance level ----
 _sig("cft_linear_fwd", C.c_int, C.c_int, vp, i64, i64, vp, i64, vp, vp, vp)

@@ -26,7 +26,7 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static EncodeTiledFn encode_fn() {
+EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -110,6 +110,30 @@ int cft_set_kernel_variant(int op, int variant) {
 
 int cft_set_deterministic(int on) {
   cft::deterministic() = on != 0;
+  return CFT_OK;
+}
+
+int cft_init(int device) {
+  return cft::guarded([&] {
+    int n = 0;
+    CFT_CUDA(cudaGetDeviceCount(&n));
+    CFT_CHECK(device >= 0 && device < n, "cft_init: no such CUDA device");
+    cudaDeviceProp p{};
+    CFT_CUDA(cudaGetDeviceProperties(&p, device));
+    CFT_CHECK(p.major == 10 && p.minor == 0,
+              "cft_init: the library is built for sm_100a (B200) only, device is sm_" +
+                  std::to_string(p.major) + std::to_string(p.minor));
+    CFT_CUDA(cudaSetDevice(device));
+    CFT_CUDA(cudaFree(nullptr));  // the primary context, now rather than inside the first step
+    cft::encode_fn();             // the TMA descriptor encoder's driver entry point
+    cft::num_sms();
+  });
+}
+int cft_destroy(void) {
+  // Callers own every buffer and the engines own theirs (cft_engine_destroy): the library holds
+  // no per-context allocation to release; this only clears the calling thread's error state.
+  cft::t_err.clear();
+  cft::t_status = CFT_OK;
   return CFT_OK;
 }
 
