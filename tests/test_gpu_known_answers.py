@@ -102,3 +102,24 @@ def test_embedding_layernorm_known_answers(cuda, dtype):
     assert np.all(g["embedding0.table"][3] == 0.0)  # token 3 never occurs
     if dtype == "fp64":
         check_bf16(m, batch, loss, g)
+
+
+def test_adamw_known_answers_fp64(cuda):
+    """tests/test_optimizer.cpp:17-20, 60-92 on the fused fp64 AdamW kernel: a fresh step
+    (theta 1, g 0.5, eta 0.1) lands exactly on kFreshStepTheta, a decay-only step (g 0,
+    lambda 0.1) on kDecayOnlyTheta, and five zero-gradient steps without decay leave theta
+    bit-identical."""
+    from paper_2605_21177_b200 import ops
+    from paper_2605_21177_b200.engine import AdamWHyper
+
+    def run(theta, g, steps=1, **kw):
+        dev = dict(dtype=torch.float64, device="cuda")
+        master, m, v = torch.tensor([theta], **dev), torch.zeros(1, **dev), torch.zeros(1, **dev)
+        for n in range(1, steps + 1):
+            grad = torch.tensor([g], **dev)
+            ops.adamw_slice(master, m, v, grad, AdamWHyper(**kw), n, stats=ops.grad_stats(grad))
+        return master.item()
+
+    assert run(1.0, 0.5, eta=0.1) == 0.90000000199999997
+    assert run(1.0, 0.0, eta=0.1, weight_decay=0.1) == 0.98999999999999999
+    assert run(0.37, 0.0, steps=5) == 0.37
