@@ -952,15 +952,17 @@ void fill_units(Args& a, int bm, int bn, int slots, double us_per_kb, bool allow
   a.splits = (a.total_kb + a.kb_per_split - 1) / a.kb_per_split;
   a.num_units = tiles * a.splits;
   // concurrent tiles ~ slots: the square-ish block (in bytes of operand slab per tile side)
-  // minimises the wave's distinct k-slabs: group_m ~ sqrt(slots * bn / bm).  CTA-pair tiles:
-  // measured under the power cap (tools/probe_group.py, 8B shapes), tall groups (16) win for
-  // wide N or long K -- fewer DRAM re-reads of the weight -- and short ones (2) for the small
-  // 4096-wide GEMMs.
+  // minimises the wave's distinct k-slabs: group_m ~ sqrt(slots * bn / bm).  CTA-pair tiles,
+  // measured under the power cap on the 8B shapes: wide N (the w1|w3 and lm_head forwards)
+  // wants tall groups (16) -- the activation operand stays in L2, so only the weight's DRAM
+  // re-reads count; long K (the w2 forward, the w1|w3 / lm_head dgrads: both operands larger
+  // than L2) wants the balanced 8 (A/B on one box, `scripts/ab_env.sh`: +0.5 % tokens/s over
+  // 16, with a higher capped clock -- fewer DRAM bytes); the small 4096-wide GEMMs short (2).
   const int concurrent = std::max(1, slots / a.splits);
   int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(concurrent) * bn / bm)));
   static const int g_longk = [] {
     const char* e = std::getenv("CFT_GEMM_GROUP_LONGK");
-    return e ? std::atoi(e) : 16;
+    return e ? std::atoi(e) : 8;
   }();
   static const int g_wide = [] {
     const char* e = std::getenv("CFT_GEMM_GROUP_WIDE");
