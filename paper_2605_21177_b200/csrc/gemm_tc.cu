@@ -957,7 +957,8 @@ void fill_units(Args& a, int bm, int bn, int slots, double us_per_kb, bool allow
   // wants tall groups (16) -- the activation operand stays in L2, so only the weight's DRAM
   // re-reads count; long K (the w2 forward, the w1|w3 / lm_head dgrads: both operands larger
   // than L2) wants the balanced 8 (A/B on one box, `scripts/ab_env.sh`: +0.5 % tokens/s over
-  // 16, with a higher capped clock -- fewer DRAM bytes); the small 4096-wide GEMMs short (2).
+  // 16 in six of six pairs; the DRAM bytes with the step's warm L2 are the same within 1 %,
+  // profiles/r2_gemm_traffic.json); the small 4096-wide GEMMs short (2).
   const int concurrent = std::max(1, slots / a.splits);
   int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(concurrent) * bn / bm)));
   static const int g_longk = [] {
