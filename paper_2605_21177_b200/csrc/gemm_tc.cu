@@ -969,7 +969,11 @@ void fill_units(Args& a, int bm, int bn, int slots, double us_per_kb, bool allow
     const char* e = std::getenv("CFT_GEMM_GROUP_WIDE");
     return e ? std::atoi(e) : 16;
   }();
-  if (bm == 256) g = a.K > 8192 ? g_longk : a.tiles_n > 20 ? g_wide : 2;
+  static const int g_small = [] {
+    const char* e = std::getenv("CFT_GEMM_GROUP_SMALL");
+    return e ? std::atoi(e) : 2;
+  }();
+  if (bm == 256) g = a.K > 8192 ? g_longk : a.tiles_n > 20 ? g_wide : g_small;
   static const int forced = [] {
     const char* e = std::getenv("CFT_GEMM_GROUP_M");  // experiments: fixed group size
     return e ? std::atoi(e) : 0;
