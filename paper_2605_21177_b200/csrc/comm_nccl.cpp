@@ -11,6 +11,7 @@
 #include <nccl.h>  // types and prototypes only; the symbols come from dlsym below
 
 #include <string>
+#include <type_traits>
 
 #include "cft_common.h"
 
