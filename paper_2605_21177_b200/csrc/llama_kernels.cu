@@ -463,35 +463,60 @@ __global__ void rope_table_kernel(float2* cs, int seq, int half, double theta) {
   cs[t] = make_float2(static_cast<float>(cos(a)), static_cast<float>(sin(a)));
 }
 
-// Table-driven, 8 pairs per thread with 16-byte loads/stores.
+// Table-driven, 8 pairs per thread with 16-byte loads/stores.  One thread rotates the same
+// 8 pairs of kRopeHeads consecutive heads of one token: its cos / sin values are loaded once
+// (two 16-byte loads per 8 pairs were one 8-byte load per pair and head) and the heads' 2 x
+// kRopeHeads row loads are all in flight before the first store.
+constexpr int kRopeHeads = 8;
 __global__ void rope_vec_kernel(bf16* qkv, long long tokens, int seq, int heads, int hd, int ld,
                                 const float2* __restrict__ cs, float sign) {
   const int half = hd / 2, vpr = half / 8;
-  const long long total = tokens * heads * vpr;
+  const int groups = (heads + kRopeHeads - 1) / kRopeHeads;
+  const long long total = tokens * groups * vpr;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const int v = static_cast<int>(t % vpr);
-    const long long th = t / vpr;
-    const int h = static_cast<int>(th % heads);
-    const long long tok = th / heads;
+    const long long tg = t / vpr;
+    const int h0 = static_cast<int>(tg % groups) * kRopeHeads;
+    const long long tok = tg / groups;
     const int pos = static_cast<int>(tok % seq);
-    bf16* p = qkv + tok * ld + static_cast<long long>(h) * hd + v * 8;
-    float x1[8], x2[8];
-    unpack8(*reinterpret_cast<const uint4*>(p), x1);
-    unpack8(*reinterpret_cast<const uint4*>(p + half), x2);
-    const float2* c = cs + static_cast<long long>(pos) * half + v * 8;
-    float y1[8], y2[8];
+    const float4* c4 = reinterpret_cast<const float4*>(cs + static_cast<long long>(pos) * half + v * 8);
+    float cx[8], sn[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      // explicit roundings (no FMA contraction): the QKV GEMM epilogue applies the same
-      // rotation bit for bit (gemm_tc.cu rope_epilogue)
-      const float2 q = c[e];
-      const float sn = sign * q.y;
-      y1[e] = __fsub_rn(__fmul_rn(x1[e], q.x), __fmul_rn(x2[e], sn));
-      y2[e] = __fadd_rn(__fmul_rn(x2[e], q.x), __fmul_rn(x1[e], sn));
+    for (int e = 0; e < 4; ++e) {
+      const float4 q = __ldg(c4 + e);
+      cx[2 * e] = q.x;
+      sn[2 * e] = sign * q.y;
+      cx[2 * e + 1] = q.z;
+      sn[2 * e + 1] = sign * q.w;
     }
-    *reinterpret_cast<uint4*>(p) = pack8(y1);
-    *reinterpret_cast<uint4*>(p + half) = pack8(y2);
+    bf16* base = qkv + tok * ld + v * 8;
+    uint4 a[kRopeHeads], b[kRopeHeads];
+#pragma unroll
+    for (int i = 0; i < kRopeHeads; ++i) {
+      if (h0 + i < heads) {
+        const bf16* p = base + static_cast<long long>(h0 + i) * hd;
+        a[i] = *reinterpret_cast<const uint4*>(p);
+        b[i] = *reinterpret_cast<const uint4*>(p + half);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kRopeHeads; ++i) {
+      if (h0 + i >= heads) break;
+      float x1[8], x2[8], y1[8], y2[8];
+      unpack8(a[i], x1);
+      unpack8(b[i], x2);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        // explicit roundings (no FMA contraction): the QKV GEMM epilogue applies the same
+        // rotation bit for bit (gemm_tc.cu rope_epilogue)
+        y1[e] = __fsub_rn(__fmul_rn(x1[e], cx[e]), __fmul_rn(x2[e], sn[e]));
+        y2[e] = __fadd_rn(__fmul_rn(x2[e], cx[e]), __fmul_rn(x1[e], sn[e]));
+      }
+      bf16* p = base + static_cast<long long>(h0 + i) * hd;
+      *reinterpret_cast<uint4*>(p) = pack8(y1);
+      *reinterpret_cast<uint4*>(p + half) = pack8(y2);
+    }
   }
 }
 
@@ -524,7 +549,7 @@ void rope(bf16* qkv, long long tokens, int seq, int heads, int hd, int ld, float
   const int half = hd / 2;
   if (half % 8 == 0 && ld % 8 == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0) {
     const float2* cs = rope_table(seq, hd, theta);
-    rope_vec_kernel<<<grid_for(tokens * heads * half / 8), 256, 0, s>>>(
+    rope_vec_kernel<<<grid_for(tokens * ((heads + kRopeHeads - 1) / kRopeHeads) * (half / 8)), 256, 0, s>>>(
         qkv, tokens, seq, heads, hd, ld, cs, backward ? -1.f : 1.f);
     check_launch("rope_vec");
     return;
